@@ -1,0 +1,408 @@
+"""Benchmark: Fisher-BT iterations/s on BASELINE config 2 (n = 3,600, 5 replicate fits).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Own arm ("ours"): one process per GPU (torchrun for N > 1).  Each rank runs its own five
+replicate Fisher-BT fits of config 2 (weak scaling: rank r fits seeds 5r..5r+4; rank 0 uses
+the golden seeds 0-4) concurrently from five host threads, one CUDA stream and one
+device-resident dataset per replica.  A step = all five fits from theta0 to convergence.
+  value  = sum of grad_calls (Fisher iterations) over all ranks / max-over-ranks step time,
+           inputs resident in HBM (contexts created and warmed before timing);
+  e2e    = same metric through the public API from host numpy buffers: every step creates
+           the datasets (H2D of locations and z), runs the fits and reads the results back.
+Reference arm (--impl reference): the reference's own CPU algorithm (oracle port of
+maternmle, numpy/scipy/OpenBLAS on all host cores) on the same config, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+GOLDEN = REPO / "tests" / "golden"
+CONFIG = "config2"
+THETA0 = (0.8, 0.1, 1.0)
+N_REPLICAS = 5
+FP64_PEAK_TFLOPS = 36.08   # cuBLAS DGEMM 16384^3 on this pool's B200 (profiles/r01_fp64_peaks.txt)
+METRIC = "Fisher-BT iterations/s at n"
+
+
+def workload_desc():
+    return {"workload": "config2: n=3600 jittered 60x60 grid on [0,1]^2, true theta=(1.0,0.2,1.5), "
+                        "5 replicate FP64 fields per GPU, Fisher-BT from theta0=(0.8,0.1,1.0) "
+                        "to ||grad||<=1e-3 (reference stopping rule)",
+            "n": 3600, "replicas_per_gpu": N_REPLICAS, "nb": 128,
+            "l2": "inputs larger than L2: 3 x 110 MB matrices per replica, 5 replicas"}
+
+
+def replica_seeds(rank: int):
+    """Weak scaling: rank r owns seeds 5r..5r+4 (no data-path collective)."""
+    return [N_REPLICAS * rank + s for s in range(N_REPLICAS)]
+
+
+def load_replica(seed, device):
+    """Locations and z for one replica (golden z for seeds 0-4, GPU-simulated otherwise)."""
+    import paper_2601_11437_b200 as m
+
+    path = GOLDEN / f"{CONFIG}_seed{seed}_data.npz"
+    if path.exists():
+        d = np.load(path)
+        return d["loc"], d["z"]
+    wl = m.WORKLOADS[CONFIG]
+    loc = wl.locations(seed)
+    return loc, m.simulate_field(loc, wl.theta_true, seed, device=device)
+
+
+class TimedObjective:
+    """GPU objective that also accumulates device phase times / launches per evaluation."""
+
+    def __init__(self, data):
+        import paper_2601_11437_b200 as m
+
+        self.inner = m.LikelihoodObjective(data)
+        self.eng = data.engine()
+        self.acc = {"flops": 0.0, "factor_ms": 0.0, "gen_ms": 0.0, "gen_bytes": 0.0,
+                    "launches": 0, "evals": 0}
+
+    @property
+    def loglik_calls(self):
+        return self.inner.loglik_calls
+
+    @property
+    def grad_calls(self):
+        return self.inner.grad_calls
+
+    def _note(self):
+        p = self.eng.phase_times()
+        self.acc["flops"] += p["flops"]
+        self.acc["factor_ms"] += p["potrf_ms"] + p["solve_ms"]
+        self.acc["gen_ms"] += p["gen_ms"]
+        self.acc["gen_bytes"] += p["gen_bytes"]
+        self.acc["launches"] += p["launches"]
+        self.acc["evals"] += 1
+
+    def loglik(self, theta):
+        v = self.inner.loglik(theta)
+        self._note()
+        return v
+
+    def eval_all(self, theta):
+        v = self.inner.eval_all(theta)
+        self._note()
+        return v
+
+
+def run_fits(datasets, objectives_out=None):
+    """Fit every dataset from THETA0 concurrently (one host thread per replica)."""
+    import paper_2601_11437_b200 as m
+
+    th0 = m.MaternParams(*THETA0)
+    cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    results = [None] * len(datasets)
+    objs = [TimedObjective(d) for d in datasets]
+
+    def work(i):
+        results[i] = m.fisher_bt(datasets[i], cfg, objective=objs[i])
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(datasets))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if any(r is None for r in results):
+        raise RuntimeError("a replicate fit failed")
+    if objectives_out is not None:
+        objectives_out.extend(objs)
+    return results
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def isolated_phase_rates(data, theta, reps=5):
+    """Kernel-level rates from single-stream evaluations (CUDA events on the ctx stream)."""
+    eng = data.engine()
+    eng.eval_all(theta)
+    fl = fac = gen = gb = 0.0
+    for _ in range(reps):
+        eng.eval_all(theta)
+        p = eng.phase_times()
+        fl += p["flops"]
+        fac += p["potrf_ms"] + p["solve_ms"]
+        gen += p["gen_ms"]
+        gb += p["gen_bytes"]
+        last = p
+    ll_ms = []
+    for _ in range(reps):
+        eng.loglik(theta)
+        ll_ms.append(eng.phase_times())
+    return {"eval_factor_solve_tflops": fl / (fac * 1e-3) / 1e12,
+            "gen_gbs": gb / (gen * 1e-3) / 1e9, "eval_phases_ms": last,
+            "loglik_potrf_ms": statistics.median(p["potrf_ms"] for p in ll_ms),
+            "loglik_potrf_tflops": ll_ms[-1]["flops"] / (statistics.median(
+                p["potrf_ms"] for p in ll_ms) * 1e-3) / 1e12}
+
+
+# ----------------------------------------------------------------------------- CPU side
+def cpu_iteration_sample(reps=1):
+    """Oracle (reference algorithm, numpy/scipy/OpenBLAS) timing of one mean Fisher
+    iteration of config 2: one eval_all plus rho loglik calls, rho = the reference fits'
+    (loglik_calls - grad_calls) / grad_calls over seeds 0-4 (golden)."""
+    from oracle import maternmle_cpu as O
+
+    fits = [json.loads((GOLDEN / f"{CONFIG}_seed{s}_fit.json").read_text()) for s in range(5)]
+    g = sum(f["grad_calls"] for f in fits)
+    rho = (sum(f["loglik_calls"] for f in fits) - g) / g
+    d = np.load(GOLDEN / f"{CONFIG}_seed0_data.npz")
+    loc, z = d["loc"], d["z"]
+    th = (1.0, 0.2, 1.5)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.eval_all(loc, z, th)
+        t1 = time.perf_counter()
+        O.loglik(loc, z, th)
+        t2 = time.perf_counter()
+        times.append((t1 - t0) + rho * (t2 - t1))
+    t_iter = statistics.median(times)
+    return {"value": 1.0 / t_iter, "t_eval_all_s": t1 - t0, "t_loglik_s": t2 - t1, "rho": rho}
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            return int(info[0]["num_threads"])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        from oracle import maternmle_cpu as O  # noqa: F401  (import / BLAS warm-up only)
+    samples = [cpu_iteration_sample(1) for _ in range(args.steps)]
+    val = statistics.median(s["value"] for s in samples)
+    cores = cpu_cores()
+    sample = ("one config-2 eval_all + rho=%.3f loglik at n=3600 per step (the reference "
+              "fits' mean evaluation mix per Fisher iteration); generation is single-threaded "
+              "numpy/scipy as in the reference, LAPACK on %d threads" % (samples[0]["rho"], cores))
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "it/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_desc(),
+            "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "detail": {"t_eval_all_s": samples[-1]["t_eval_all_s"],
+                       "t_loglik_s": samples[-1]["t_loglik_s"]}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU side
+def ours_arm(args, rank, world, local_rank):
+    import torch
+    import paper_2601_11437_b200 as m
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    seeds = replica_seeds(rank)
+    host = [load_replica(s, local_rank) for s in seeds]
+    datasets = [m.SpatialDataset(loc, z, device=local_rank) for loc, z in host]
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn):
+        barrier_sync()
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        out = fn()
+        torch.cuda.synchronize()
+        stop.record()
+        stop.synchronize()
+        return out, start.elapsed_time(stop)
+
+    for _ in range(args.warmup):
+        run_fits(datasets)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    objs, step_ms, grad_calls, loglik_calls = [], [], 0, 0
+    for _ in range(args.steps):
+        step_objs = []
+        res, ms = timed(lambda: run_fits(datasets, step_objs))
+        objs.extend(step_objs)
+        step_ms.append(ms)
+        grad_calls += sum(r.grad_calls for r in res)
+        loglik_calls += sum(r.loglik_calls for r in res)
+    clk = clocks.stop()
+    last_fits = res
+
+    # end-to-end: host arrays -> public API -> results on host, every step
+    h2d = sum(loc.nbytes + z.nbytes for loc, z in host)
+    e2e_ms, e2e_grad, e2e_evals = [], 0, 0
+    for _ in range(max(1, args.steps)):
+        def e2e_step():
+            ds = [m.SpatialDataset(loc, z, device=local_rank) for loc, z in host]
+            r = run_fits(ds)
+            for d in ds:
+                d.release()
+            return r
+        res_e2e, ms = timed(e2e_step)
+        e2e_ms.append(ms)
+        e2e_grad += sum(r.grad_calls for r in res_e2e)
+        e2e_evals += sum(r.loglik_calls for r in res_e2e)
+
+    tot_ms = sum(step_ms)
+    tot_e2e = sum(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([tot_ms, tot_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c = torch.tensor([grad_calls, e2e_grad, loglik_calls], dtype=torch.float64, device="cuda")
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        tot_ms, tot_e2e = float(t[0]), float(t[1])
+        grad_all, e2e_grad_all, ll_all = (float(v) for v in c)
+    else:
+        grad_all, e2e_grad_all, ll_all = float(grad_calls), float(e2e_grad), float(loglik_calls)
+
+    if rank != 0:
+        return
+    value = grad_all / (tot_ms * 1e-3)
+    e2e_value = e2e_grad_all / (tot_e2e * 1e-3)
+    acc = {k: sum(o.acc[k] for o in objs) for k in objs[0].acc}
+    iso = isolated_phase_rates(datasets[0], m.WORKLOADS[CONFIG].theta_true)
+    achieved = iso["eval_factor_solve_tflops"]
+    # 9 result doubles + failure flag + pivot per evaluation come back to the host
+    d2h = int(e2e_evals / max(1, len(e2e_ms)) * (9 * 8 + 4 + 8))
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_desc(),
+        "roofline": {
+            "bound": "tensor", "unit": "TFLOP/s", "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "kernel": "Cholesky + solve phase of one eval_all at n=3600 (DMMA dgemm_kernel "
+                      "launches + potrf_diag_kernel), standard-count flops n^3/3 + 2(n^3 + n^3/3)"
+                      ", CUDA events on the context stream, single stream",
+            "peak_source": "measured cuBLAS DGEMM 16384^3 FP64 on this pool's B200 "
+                           "(MEASURED_PEAKS.json has no FP64 entry)"},
+        "fp64_tflops_chol_solve": achieved,
+        "fp64_tflops_chol_solve_in_fits": acc["flops"] / (acc["factor_ms"] * 1e-3) / 1e12,
+        "gen_hbm_gbs": iso["gen_gbs"],
+        "gpu_launches": int(acc["launches"]),
+        "clocks": clk,
+        "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "fits": {"grad_calls_per_step": grad_all / args.steps,
+                 "loglik_calls_per_step": ll_all / args.steps,
+                 "theta_hat_rank0": [r.theta_hat.as_array().tolist() for r in last_fits]},
+        "isolated": iso,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_iteration_sample(1)
+        line["cpu_baseline"] = {
+            "value": cpu["value"], "unit": "it/s", "cores": cpu_cores(), "kind": "port",
+            "sample": "one config-2 eval_all + rho=%.3f loglik (reference algorithm, numpy/scipy/"
+                      "OpenBLAS) = one mean Fisher iteration; eval_all %.2fs, loglik %.2fs"
+                      % (cpu["rho"], cpu["t_eval_all_s"], cpu["t_loglik_s"])}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        ours_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,118 @@
+/*
+ * maternfisher.h — C ABI of the B200 (sm_100a) exact-likelihood engine behind Fisher-BT.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2601.11437, package
+ * `maternmle`).  Every entry point takes plain pointers and sizes; no torch or CUDA types
+ * cross it.  The reference binds the path through Python objects; each function below
+ * names the reference interface it replaces (path:line into the reference tree):
+ *
+ *   mle_ctx_create   <- SpatialDataset(locations, values)           pkg/src/maternmle/matern.py:59-84
+ *   mle_loglik       <- log_likelihood(data, theta)                 pkg/src/maternmle/likelihood.py:81-89
+ *                       LikelihoodObjective.loglik                  pkg/src/maternmle/optimizer.py:127-134
+ *   mle_eval_all     <- grad_and_fisher(data, theta)                pkg/src/maternmle/likelihood.py:107-149
+ *                       LikelihoodObjective.eval_all                pkg/src/maternmle/optimizer.py:136-142
+ *   mle_build        <- build_cov_matrix / build_dcov_matrix        pkg/src/maternmle/matern.py:186-203
+ *   mle_cholesky     <- cholesky_lower(sigma)                       pkg/src/maternmle/likelihood.py:63-78
+ *   mle_bessel_k     <- bessel_k(nu, x)                             pkg/src/maternmle/bessel.py:80-100
+ *   mle_dnu_xnu_knu  <- dnu_xnu_knu(nu, x)                          pkg/src/maternmle/bessel.py:327-370
+ *   mle_matern_elem  <- matern_cov / dcov_dalpha / dcov_dnu / dcov_dsigma2 on distance arrays
+ *                                                                    pkg/src/maternmle/matern.py:100-168
+ *
+ * Return codes (all functions returning int):
+ *   MLE_OK (0)            success
+ *   MLE_NOT_PD (1)        Cholesky failed; *bad_pivot holds the 0-based failing pivot
+ *                         (reference: NotPositiveDefinite(pivot=info-1), likelihood.py:76-77)
+ *   MLE_INVALID (2)       invalid argument (reference raises ValueError: matern.py:44-48,
+ *                         bessel.py:93-96, 341-345, matern.py:198-201)
+ *   MLE_CUDA_ERROR (3)    CUDA runtime failure (message via mle_last_error)
+ *
+ * Threading: calls on one context are serialised on that context's own CUDA stream;
+ * distinct contexts are independent and may be driven from different host threads
+ * concurrently (the reference's functions are pure and concurrency-safe).
+ */
+#ifndef MATERNFISHER_H
+#define MATERNFISHER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLE_OK 0
+#define MLE_NOT_PD 1
+#define MLE_INVALID 2
+#define MLE_CUDA_ERROR 3
+
+/* Which matrix mle_build writes (reference build_dcov_matrix `which`, matern.py:191-203). */
+#define MLE_WHICH_SIGMA 0   /* Sigma(theta)                       build_cov_matrix        */
+#define MLE_WHICH_SIGMA2 1  /* dSigma/dsigma2 = C/sigma2, diag 1  build_dcov_matrix sigma2 */
+#define MLE_WHICH_ALPHA 2   /* dSigma/dalpha, zero diagonal       build_dcov_matrix alpha  */
+#define MLE_WHICH_NU 3      /* dSigma/dnu, zero diagonal          build_dcov_matrix nu     */
+
+/* Phase timers returned by mle_phase_times (milliseconds of device time, last call). */
+#define MLE_PHASE_GEN 0
+#define MLE_PHASE_POTRF 1
+#define MLE_PHASE_SOLVE 2
+#define MLE_PHASE_REDUCE 3
+#define MLE_PHASE_TOTAL 4
+#define MLE_NUM_PHASES 5
+
+typedef struct mle_ctx mle_ctx;
+
+/* Library version string and the last error message of the calling thread. */
+const char* mle_version(void);
+const char* mle_last_error(void);
+
+/* Number of visible CUDA devices (0 if none); lets a host fail loudly without a GPU. */
+int mle_device_count(void);
+
+/*
+ * Create a context owning device-resident copies of the n locations (n x 2, row-major
+ * x,y pairs) and the n observed values z.  `device` selects the GPU.  `nugget` >= 0 adds
+ * tau^2 to the diagonal of Sigma (0 reproduces the reference, which has no nugget).
+ * All O(n^2) matrices are allocated lazily on first use.
+ */
+int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device,
+                   double nugget, mle_ctx** out);
+void mle_ctx_destroy(mle_ctx* ctx);
+int64_t mle_ctx_n(const mle_ctx* ctx);
+
+/* Replace the observed values z (same n); used to refit a new field on the same locations. */
+int mle_ctx_set_values(mle_ctx* ctx, const double* z);
+
+/* Exact log-likelihood at theta = [sigma2, alpha, nu]. */
+int mle_loglik(mle_ctx* ctx, const double theta[3], double* loglik, int64_t* bad_pivot);
+
+/* Log-likelihood, score (3) and Fisher information (3x3 row-major, exactly symmetric). */
+int mle_eval_all(mle_ctx* ctx, const double theta[3], double* loglik, double grad[3],
+                 double fisher[9], int64_t* bad_pivot);
+
+/* Write one full n x n matrix (row-major == column-major, symmetric) to host memory. */
+int mle_build(mle_ctx* ctx, const double theta[3], int which, double* out_host);
+
+/* Device-time breakdown of the last mle_loglik / mle_eval_all call (MLE_NUM_PHASES doubles)
+ * followed by: standard-count FP64 flops of the factor/solve phase, algorithmic bytes
+ * written by generation, and the number of kernels the call launched
+ * (MLE_NUM_PHASES + 3 doubles in total). */
+int mle_phase_times(const mle_ctx* ctx, double* out);
+
+/* Dense lower Cholesky of a host n x n symmetric matrix (row-major; only the lower triangle
+ * is read).  l_out receives L with a zeroed strict upper triangle (LAPACK clean=1). */
+int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t* bad_pivot);
+
+/* Elementwise special functions on the GPU, m points, host in/out. */
+int mle_bessel_k(double nu, const double* x, int64_t m, int device, double* out);
+int mle_dnu_xnu_knu(double nu, const double* x, int64_t m, int device, double* out);
+
+/* Elementwise Matern covariance / derivatives at distances h (h >= 0) for theta:
+ * which = MLE_WHICH_* selects C, dC/dsigma2, dC/dalpha or dC/dnu; h = 0 gives the
+ * zero-lag limit (sigma2, 1, 0, 0). */
+int mle_matern_elem(const double theta[3], int which, const double* h, int64_t m, int device,
+                    double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MATERNFISHER_H */

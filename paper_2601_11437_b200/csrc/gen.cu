@@ -1,0 +1,233 @@
+// gen.cu — covariance / derivative tile generation (sm_100a).
+//
+// Replaces build_cov_matrix / build_dcov_matrix (reference matern.py:171-203) and the
+// per-distance evaluators _cov_positive / _dalpha_positive / _dnu_positive
+// (matern.py:100-125).  Distances are recomputed per element (no pdist + np.unique dedup,
+// matern.py:86-97) with the same rounding as scipy's pdist: sqrt((dx*dx) + (dy*dy)).
+//
+// One CTA owns one 32x32 lower tile (I >= J) of the padded, column-major N x N matrices.
+// It writes tile (I, J) of every requested output with coalesced column stores and, for the
+// derivative matrices that must be stored in full, the mirrored tile (J, I) through a
+// shared-memory transpose.
+//
+// Engine layout: index n is the augmented row carrying z (Sigma[n, j] = z_j,
+// Sigma[n, n] = 0), indices > n are padding (identity in Sigma, zero in the derivatives).
+#include <cuda_runtime.h>
+
+#include "special.cuh"
+#include "kernels.h"
+
+namespace mle {
+
+
+namespace {
+
+constexpr int kGT = 32;         // generation tile edge
+constexpr int kGThreads = 256;  // 8 columns per pass, 4 passes
+
+__device__ __forceinline__ void lower_tile_index(long long b, int* ti, int* tj) {
+  // b = I (I + 1) / 2 + J, 0 <= J <= I
+  long long I = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while (I * (I + 1) / 2 > b) --I;
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  *ti = (int)I;
+  *tj = (int)(b - I * (I + 1) / 2);
+}
+
+// pdist-identical Euclidean distance (no FMA contraction).
+__device__ __forceinline__ double pair_distance(const double* lx, const double* ly, int i, int j) {
+  const double dx = __dsub_rn(lx[i], lx[j]);
+  const double dy = __dsub_rn(ly[i], ly[j]);
+  return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+}
+
+}  // namespace
+
+// kMode: 0 = Sigma only (loglik), 1 = Sigma + dSigma/dalpha + dSigma/dnu (eval_all).
+template <int kMode>
+__global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
+  if (a.fail_flag != nullptr && *a.fail_flag) return;
+  int ti, tj;
+  lower_tile_index((long long)blockIdx.x, &ti, &tj);
+  const ThetaParams& P = a.P;
+  const int lane_row = threadIdx.x & (kGT - 1);
+  const int col0 = threadIdx.x >> 5;
+  const int i = ti * kGT + lane_row;
+  const long long ld = a.ld;
+  const int n = a.n;
+  __shared__ double s_da[kGT][kGT + 1];
+  __shared__ double s_dn[kGT][kGT + 1];
+#pragma unroll 1
+  for (int r = 0; r < kGT / 8; ++r) {
+    const int jl = col0 + 8 * r;
+    const int j = tj * kGT + jl;
+    double c, da = 0.0, dn = 0.0;
+    if (i >= n || j >= n) {
+      // augmented row / padding
+      if (i == j) {
+        c = (i == n) ? 0.0 : 1.0;
+      } else if (i == n && j < n) {
+        c = a.z[j];
+      } else if (j == n && i < n) {
+        c = a.z[i];
+      } else {
+        c = 0.0;
+      }
+    } else if (i == j) {
+      c = P.sigma2 + P.nugget;  // matern.py:182 fill_diagonal(sigma2)
+    } else {
+      const double h = pair_distance(a.lx, a.ly, i, j);
+      if (h > 0.0) {
+        const MaternVals v = matern_positive<kMode == 1>(P, h);
+        c = v.c;
+        da = v.dalpha;
+        dn = v.dnu;
+      } else {
+        c = P.sigma2;  // coincident locations: zero-lag limit (matern.py:173-178)
+      }
+    }
+    const long long off = (long long)i + (long long)j * ld;
+    a.sigma[off] = c;
+    if (kMode == 1) {
+      a.dalpha[off] = da;
+      a.dnu[off] = dn;
+      s_da[lane_row][jl] = da;
+      s_dn[lane_row][jl] = dn;
+    }
+  }
+  if (kMode == 1 && ti != tj) {
+    __syncthreads();
+    // mirrored tile (J, I): rows from tile J, columns from tile I
+    const int i2 = tj * kGT + lane_row;
+#pragma unroll 1
+    for (int r = 0; r < kGT / 8; ++r) {
+      const int jl = col0 + 8 * r;
+      const int j2 = ti * kGT + jl;
+      const long long off = (long long)i2 + (long long)j2 * ld;
+      a.dalpha[off] = s_da[jl][lane_row];
+      a.dnu[off] = s_dn[jl][lane_row];
+    }
+  }
+}
+
+// Full symmetric n x n matrix of one kind (mle_build), no augmentation / padding.
+__global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int which) {
+  int ti, tj;
+  lower_tile_index((long long)blockIdx.x, &ti, &tj);
+  const ThetaParams& P = a.P;
+  const int lane_row = threadIdx.x & (kGT - 1);
+  const int col0 = threadIdx.x >> 5;
+  const int i = ti * kGT + lane_row;
+  const long long ld = a.ld;
+  const int n = a.n;
+  __shared__ double s_v[kGT][kGT + 1];
+#pragma unroll 1
+  for (int r = 0; r < kGT / 8; ++r) {
+    const int jl = col0 + 8 * r;
+    const int j = tj * kGT + jl;
+    double v = 0.0;
+    if (i < n && j < n) {
+      if (i == j) {
+        v = (which == MLE_WHICH_SIGMA) ? P.sigma2 + P.nugget
+                                       : (which == MLE_WHICH_SIGMA2 ? 1.0 : 0.0);
+      } else {
+        const double h = pair_distance(a.lx, a.ly, i, j);
+        if (h > 0.0) {
+          if (which == MLE_WHICH_SIGMA || which == MLE_WHICH_SIGMA2) {
+            const MaternVals m = matern_positive<false>(P, h);
+            v = (which == MLE_WHICH_SIGMA) ? m.c : m.c / P.sigma2;  // matern.py:160
+          } else {
+            const MaternVals m = matern_positive<true>(P, h);
+            v = (which == MLE_WHICH_ALPHA) ? m.dalpha : m.dnu;
+          }
+        } else {
+          v = (which == MLE_WHICH_SIGMA) ? P.sigma2 : (which == MLE_WHICH_SIGMA2 ? 1.0 : 0.0);
+        }
+      }
+      a.sigma[(long long)i + (long long)j * ld] = v;
+    }
+    s_v[lane_row][jl] = v;
+  }
+  if (ti != tj) {
+    __syncthreads();
+    const int i2 = tj * kGT + lane_row;
+#pragma unroll 1
+    for (int r = 0; r < kGT / 8; ++r) {
+      const int jl = col0 + 8 * r;
+      const int j2 = ti * kGT + jl;
+      if (i2 < n && j2 < n) a.sigma[(long long)i2 + (long long)j2 * ld] = s_v[jl][lane_row];
+    }
+  }
+}
+
+// Elementwise evaluators (parity surface for bessel.py / matern.py scalar functions).
+__global__ void elem_kernel(ThetaParams P, int op, int which, const double* __restrict__ x,
+                            long long m, double* __restrict__ out) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double v = x[t];
+    double r;
+    if (op == 0) {  // bessel_k(nu, x) = K_|nu|(x), x > 0 validated on the host
+      double k_nu, k_m1;
+      bessel_k_ladder(P.kmain, v, &k_nu, &k_m1);
+      r = k_nu;
+    } else if (op == 1) {  // dnu_xnu_knu(nu, x), x >= 0
+      if (v == 0.0) {
+        r = 0.0;  // bessel.py:358 (ZERO_ARG)
+      } else {
+        double k_nu, k_m1;
+        bessel_k_ladder(P.kmain, v, &k_nu, &k_m1);
+        r = dnu_xnu_knu(P, v, pow(v, P.nu) * k_nu);
+      }
+    } else {  // Matern value / derivative at distance h >= 0
+      if (v > 0.0) {
+        if (which == MLE_WHICH_SIGMA || which == MLE_WHICH_SIGMA2) {
+          const MaternVals mv = matern_positive<false>(P, v);
+          r = (which == MLE_WHICH_SIGMA) ? mv.c : mv.c / P.sigma2;
+        } else {
+          const MaternVals mv = matern_positive<true>(P, v);
+          r = (which == MLE_WHICH_ALPHA) ? mv.dalpha : mv.dnu;
+        }
+      } else {
+        r = (which == MLE_WHICH_SIGMA) ? P.sigma2 : (which == MLE_WHICH_SIGMA2 ? 1.0 : 0.0);
+      }
+    }
+    out[t] = r;
+  }
+}
+
+cudaError_t upload_u_tables(const double* u, const double* du) {
+  cudaError_t e = cudaMemcpyToSymbol(c_u_coef, u, sizeof(double) * (MLE_CASE3_NEAR + 1) *
+                                                      MLE_U_COEFF_STRIDE);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_du_coef, du,
+                            sizeof(double) * (MLE_CASE3_NEAR + 1) * MLE_U_COEFF_STRIDE);
+}
+
+static long long lower_tiles(long long rows) {
+  const long long t = (rows + kGT - 1) / kGT;
+  return t * (t + 1) / 2;
+}
+
+void launch_gen_engine(const GenArgs& a, bool derivs, cudaStream_t s) {
+  const long long blocks = lower_tiles(a.rows);
+  if (derivs)
+    gen_engine_kernel<1><<<(unsigned)blocks, kGThreads, 0, s>>>(a);
+  else
+    gen_engine_kernel<0><<<(unsigned)blocks, kGThreads, 0, s>>>(a);
+}
+
+void launch_gen_build(const GenArgs& a, int which, cudaStream_t s) {
+  const long long blocks = lower_tiles(a.n);
+  gen_build_kernel<<<(unsigned)blocks, kGThreads, 0, s>>>(a, which);
+}
+
+void launch_elem(const ThetaParams& P, int op, int which, const double* x, long long m,
+                 double* out, cudaStream_t s) {
+  long long blocks = (m + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks < 1) blocks = 1;
+  elem_kernel<<<(unsigned)blocks, 256, 0, s>>>(P, op, which, x, m, out);
+}
+
+}  // namespace mle

@@ -1,0 +1,517 @@
+// linalg.cu — FP64 dense linear algebra for the likelihood engine on sm_100a.
+//
+// Replaces the LAPACK/BLAS calls of the reference (likelihood.py:75 dpotrf,
+// likelihood.py:84,121,125,134-135 solve_triangular) and the Frobenius reductions of
+// trace_product (likelihood.py:92-104).
+//
+//  * dgemm_kernel: 128x128x16 CTA tiles, 8 warps of 64x32, FP64 tensor-core MMA
+//    (mma.sync.m16n8k8.f64 -> DMMA), 3-stage cp.async shared-memory pipeline.  Used for every
+//    panel product and trailing update: Cholesky (panel x Linv^T, lower SYRK), forward
+//    solve X = L^-1 S (row panel, full update), lower-only right solve B = X L^-T.
+//  * potrf_diag_kernel: one CTA factors a 128x128 diagonal tile in shared memory (16-wide
+//    blocked right-looking) and inverts it (blocked by 16), reporting the first failing
+//    pivot with LAPACK dpotrf semantics (info - 1, likelihood.py:76-77).
+//  * reduce kernels: deterministic two-pass FP64 sums of log L_jj, y^T y, tr B_i,
+//    <B_i, B_j>_F and y^T B_i y (the augmented entry B_i[n, n]).
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace mle {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+constexpr int GEMM_THREADS = 256;
+constexpr int SA = BM + 4;   // A smem: [BK][SA], m contiguous (SA = 4 mod 16 -> conflict free)
+constexpr int SBN = BN + 4;  // B (kBNK) smem: [BK][SBN]
+constexpr int SBK = BK + 4;  // B (kBKN) smem: [BN][SBK]
+constexpr int A_STAGE = BK * SA;
+constexpr int B_STAGE_NK = BK * SBN;
+constexpr int B_STAGE_KN = BN * SBK;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4],
+                                            const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+__device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn) {
+  const int b = blockIdx.x;
+  if (g.lower) {
+    int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > b) --I;
+    while ((I + 1) * (I + 2) / 2 <= b) ++I;
+    *tm = I;
+    *tn = b - I * (I + 1) / 2;
+  } else {
+    *tm = b % g.tiles_m;
+    *tn = b / g.tiles_m;
+  }
+}
+
+}  // namespace
+
+// C[tm, tn] = alpha * sum_k A(m, k) B(n, k) + beta * C, A(m,k) = A[m + k*lda].
+template <int kBL>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
+  if (g.fail_flag != nullptr && *g.fail_flag) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_STAGE;
+  constexpr int B_STAGE = (kBL == kBNK) ? B_STAGE_NK : B_STAGE_KN;
+
+  int tm, tn;
+  tile_coords(g, &tm, &tn);
+  const bool z1 = blockIdx.z != 0;
+  // no __restrict__: panel products run in place (C aliases A or B; see engine.cu)
+  const double* A = (z1 ? g.A[1] : g.A[0]) + (long long)tm * BM;
+  const double* Bz = z1 ? g.B[1] : g.B[0];
+  const double* B = (kBL == kBNK) ? Bz + (long long)tn * BN : Bz + (long long)tn * BN * g.ldb;
+  double* C = (z1 ? g.C[1] : g.C[0]) + (long long)tm * BM + (long long)tn * BN * g.ldc;
+  const long long lda = g.lda, ldb = g.ldb, ldc = g.ldc;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps, warp tile 64 x 32
+  const int gq = lane >> 2, tq = lane & 3;
+
+  auto load_stage = [&](int stage, int kt) {
+    double* as = As + stage * A_STAGE;
+    double* bs = Bs + stage * B_STAGE;
+    const int k0 = kt * BK;
+#pragma unroll
+    for (int r = 0; r < (BM * BK / 2) / GEMM_THREADS; ++r) {
+      const int c = tid + r * GEMM_THREADS;
+      const int k = c >> 6, m2 = (c & 63) << 1;
+      cp_async16(as + k * SA + m2, A + m2 + (long long)(k0 + k) * lda);
+    }
+    if (kBL == kBNK) {
+#pragma unroll
+      for (int r = 0; r < (BN * BK / 2) / GEMM_THREADS; ++r) {
+        const int c = tid + r * GEMM_THREADS;
+        const int k = c >> 6, n2 = (c & 63) << 1;
+        cp_async16(bs + k * SBN + n2, B + n2 + (long long)(k0 + k) * ldb);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < (BN * BK / 2) / GEMM_THREADS; ++r) {
+        const int c = tid + r * GEMM_THREADS;
+        const int nn = c >> 3, k2 = (c & 7) << 1;
+        cp_async16(bs + nn * SBK + k2, B + (k0 + k2) + (long long)nn * ldb);
+      }
+    }
+  };
+
+  double acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  const int KT = g.K / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 8) {
+      double af[4][4], bf[4][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int r0 = wm * 64 + mi * 16 + gq;
+        af[mi][0] = as[(kk + tq) * SA + r0];
+        af[mi][1] = as[(kk + tq) * SA + r0 + 8];
+        af[mi][2] = as[(kk + tq + 4) * SA + r0];
+        af[mi][3] = as[(kk + tq + 4) * SA + r0 + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int c0 = wn * 32 + ni * 8 + gq;
+        if (kBL == kBNK) {
+          bf[ni][0] = bs[(kk + tq) * SBN + c0];
+          bf[ni][1] = bs[(kk + tq + 4) * SBN + c0];
+        } else {
+          bf[ni][0] = bs[c0 * SBK + kk + tq];
+          bf[ni][1] = bs[c0 * SBK + kk + tq + 4];
+        }
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_16x8x8(acc[mi][ni], af[mi], bf[ni]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
+  const double alpha = g.alpha, beta = g.beta;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int r = wm * 64 + mi * 16 + gq;
+      const int c = wn * 32 + ni * 8 + 2 * tq;
+      double* p00 = C + r + (long long)c * ldc;
+      double* p01 = C + r + (long long)(c + 1) * ldc;
+      double* p10 = p00 + 8;
+      double* p11 = p01 + 8;
+      if (beta != 0.0) {
+        *p00 = alpha * acc[mi][ni][0] + beta * *p00;
+        *p01 = alpha * acc[mi][ni][1] + beta * *p01;
+        *p10 = alpha * acc[mi][ni][2] + beta * *p10;
+        *p11 = alpha * acc[mi][ni][3] + beta * *p11;
+      } else {
+        *p00 = alpha * acc[mi][ni][0];
+        *p01 = alpha * acc[mi][ni][1];
+        *p10 = alpha * acc[mi][ni][2];
+        *p11 = alpha * acc[mi][ni][3];
+      }
+    }
+  }
+}
+
+// Opt-in shared-memory limits; must run once per device before the first launch.
+cudaError_t init_kernel_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<kBNK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * STAGES * (A_STAGE + B_STAGE_NK)));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(dgemm_kernel<kBKN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double) * STAGES * (A_STAGE + B_STAGE_KN)));
+  if (e != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
+cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s) {
+  const long long tiles =
+      g.lower ? (long long)g.tiles_m * (g.tiles_m + 1) / 2 : (long long)g.tiles_m * g.tiles_n;
+  if (tiles <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)tiles, 1, (unsigned)batch);
+  if (bl == kBNK) {
+    const size_t smem = sizeof(double) * STAGES * (A_STAGE + B_STAGE_NK);
+    dgemm_kernel<kBNK><<<grid, GEMM_THREADS, smem, s>>>(g);
+  } else {
+    const size_t smem = sizeof(double) * STAGES * (A_STAGE + B_STAGE_KN);
+    dgemm_kernel<kBKN><<<grid, GEMM_THREADS, smem, s>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Diagonal tile: Cholesky + inverse in shared memory.
+// Ls is column-major with stride 129: L(i, j) (i >= j) at Ls[j*129 + i]; the inverse
+// X = L^-1 (i > j) is kept in the other triangle at Ls[i*129 + j], its diagonal in dinv.
+namespace {
+constexpr int DT = kNB;           // 128
+constexpr int DS = DT + 1;        // smem stride
+constexpr int DB = 16;            // inner block
+constexpr int DTHREADS = 512;
+}  // namespace
+
+__global__ void __launch_bounds__(DTHREADS, 1)
+    potrf_diag_kernel(double* a, long long ld, int k0, long long n_aug, double* linv,
+                      int* fail_flag, long long* fail_idx) {
+  if (*fail_flag) return;
+  extern __shared__ __align__(16) double dsm[];
+  double* Ls = dsm;                     // DT * DS
+  double* dinv = Ls + DT * DS;          // DT
+  double* T = dinv + DT;                // 7 * 256 scratch
+  __shared__ int s_fail;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  double* A = a + (long long)k0 + (long long)k0 * ld;
+  for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
+    const int i = idx & (DT - 1), j = idx >> 7;
+    Ls[j * DS + i] = A[i + (long long)j * ld];
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+
+#define LS(i, j) Ls[(j) * DS + (i)]
+  for (int J = 0; J < DT / DB; ++J) {
+    const int j0 = J * DB;
+    // (a) factor the 16x16 diagonal block with one warp
+    if (warp == 0) {
+      for (int c = 0; c < DB; ++c) {
+        const int jc = j0 + c;
+        const long long gidx = (long long)k0 + jc;
+        const double d = LS(jc, jc);
+        double piv;
+        if (gidx == n_aug) {
+          piv = 1.0;
+        } else {
+          if (!(d > 0.0)) {
+            if (lane == 0) {
+              s_fail = 1;
+              *fail_idx = gidx;
+              *fail_flag = 1;
+            }
+            break;
+          }
+          piv = sqrt(d);
+        }
+        __syncwarp();
+        if (lane == 0) LS(jc, jc) = piv;
+        if (lane > c && lane < DB) LS(j0 + lane, jc) /= piv;
+        __syncwarp();
+        for (int e = lane; e < DB * DB; e += 32) {
+          const int r = e & (DB - 1), s = e >> 4;
+          if (s > c && r >= s) LS(j0 + r, j0 + s) -= LS(j0 + r, jc) * LS(j0 + s, jc);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (s_fail) return;
+    const int rem = DT - j0 - DB;  // rows below the block
+    // (b) panel rows solve x L_JJ^T = a_row
+    if (tid < rem) {
+      const int i = j0 + DB + tid;
+      double x[DB];
+#pragma unroll
+      for (int c = 0; c < DB; ++c) {
+        double v = LS(i, j0 + c);
+#pragma unroll
+        for (int m = 0; m < c; ++m) v -= x[m] * LS(j0 + c, j0 + m);
+        x[c] = v / LS(j0 + c, j0 + c);
+      }
+#pragma unroll
+      for (int c = 0; c < DB; ++c) LS(i, j0 + c) = x[c];
+    }
+    __syncthreads();
+    // (c) trailing lower update
+    if (rem > 0) {
+      const int base = j0 + DB;
+      for (int e = tid; e < rem * rem; e += DTHREADS) {
+        const int il = e % rem, jl = e / rem;
+        if (il < jl) continue;
+        const int i = base + il, j = base + jl;
+        double v = LS(i, j);
+#pragma unroll
+        for (int m = 0; m < DB; ++m) v -= LS(i, j0 + m) * LS(j, j0 + m);
+        LS(i, j) = v;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- inverse X = L^-1, blocked by 16 ----
+  // diagonal 16x16 blocks: thread per (block, column)
+  if (tid < DT) {
+    const int blk = tid >> 4, c = tid & (DB - 1);
+    const int o = blk * DB;
+    double x[DB];
+#pragma unroll
+    for (int r = 0; r < DB; ++r) {
+      if (r < c) {
+        x[r] = 0.0;
+      } else if (r == c) {
+        x[r] = 1.0 / LS(o + r, o + r);
+      } else {
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < r; ++m)
+          if (m >= c) v += LS(o + r, o + m) * x[m];
+        x[r] = -v / LS(o + r, o + r);
+      }
+    }
+    dinv[o + c] = x[c];
+#pragma unroll
+    for (int r = 0; r < DB; ++r)
+      if (r > c) Ls[(o + r) * DS + (o + c)] = x[r];
+  }
+  __syncthreads();
+#define XS(i, j) ((i) == (j) ? dinv[i] : ((i) > (j) ? Ls[(i) * DS + (j)] : 0.0))
+  for (int I = 1; I < DT / DB; ++I) {
+    // T_IJ = sum_{M=J}^{I-1} L[I, M] X[M, J]
+    for (int e = tid; e < I * DB * DB; e += DTHREADS) {
+      const int J = e >> 8, rs = e & 255;
+      const int r = rs & (DB - 1), s = rs >> 4;
+      const int i = I * DB + r, j = J * DB + s;
+      double v = 0.0;
+      for (int m = J * DB; m < I * DB; ++m) v += LS(i, m) * XS(m, j);
+      T[e] = v;
+    }
+    __syncthreads();
+    // X[I, J] = - X_II T_IJ
+    for (int e = tid; e < I * DB * DB; e += DTHREADS) {
+      const int J = e >> 8, rs = e & 255;
+      const int r = rs & (DB - 1), s = rs >> 4;
+      const int i = I * DB + r;
+      double v = 0.0;
+      for (int q = 0; q <= r; ++q) v += XS(i, I * DB + q) * T[(J << 8) + (s << 4) + q];
+      Ls[i * DS + J * DB + s] = -v;
+    }
+    __syncthreads();
+  }
+  // write back L (lower incl. diagonal) and Linv (dense 128x128, zero upper)
+  for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
+    const int i = idx & (DT - 1), j = idx >> 7;
+    if (i >= j) A[i + (long long)j * ld] = LS(i, j);
+    linv[idx] = XS(i, j);
+  }
+#undef XS
+#undef LS
+}
+
+cudaError_t init_diag_attributes() {
+  return cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(sizeof(double) * (DT * DS + DT + 7 * 256)));
+}
+
+cudaError_t launch_potrf_diag(double* a, long long ld, int k0, long long n_aug, double* linv,
+                              int* fail_flag, long long* fail_idx, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (DT * DS + DT + 7 * 256);
+  potrf_diag_kernel<<<1, DTHREADS, smem, s>>>(a, ld, k0, n_aug, linv, fail_flag, fail_idx);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Reductions.  Partials: per block 7 sums [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>].
+namespace {
+constexpr int RTHREADS = 256;
+constexpr int RBLOCKS = 148 * 4;
+constexpr int RN = 7;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += sh[w];
+  return r;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __restrict__ L,
+                                                               const double* __restrict__ Ba,
+                                                               const double* __restrict__ Bn,
+                                                               long long ld, int n,
+                                                               double* partials,
+                                                               const int* fail_flag) {
+  if (*fail_flag) return;
+  __shared__ double sh[RTHREADS / 32];
+  double s[RN] = {0, 0, 0, 0, 0, 0, 0};
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    const long long cj = (long long)j * ld;
+    if (threadIdx.x == 0) {
+      s[0] += log(L[j + cj]);
+      const double y = L[n + cj];
+      s[1] += y * y;
+      const double a = Ba[j + cj], b = Bn[j + cj];
+      s[2] += a;
+      s[3] += b;
+      s[4] += a * a;
+      s[5] += a * b;
+      s[6] += b * b;
+    }
+    for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
+      const double a = Ba[i + cj], b = Bn[i + cj];
+      s[4] += 2.0 * a * a;
+      s[5] += 2.0 * a * b;
+      s[6] += 2.0 * b * b;
+    }
+  }
+  for (int q = 0; q < RN; ++q) {
+    const double t = block_sum(s[q], sh);
+    if (threadIdx.x == 0) partials[blockIdx.x * RN + q] = t;
+  }
+}
+
+__global__ void __launch_bounds__(RTHREADS) reduce_loglik_kernel(const double* __restrict__ L,
+                                                                 long long ld, int n,
+                                                                 double* partials,
+                                                                 const int* fail_flag) {
+  if (*fail_flag) return;
+  __shared__ double sh[RTHREADS / 32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int j = blockIdx.x * RTHREADS + threadIdx.x; j < n; j += gridDim.x * RTHREADS) {
+    const long long cj = (long long)j * ld;
+    s0 += log(L[j + cj]);
+    const double y = L[n + cj];
+    s1 += y * y;
+  }
+  const double t0 = block_sum(s0, sh);
+  const double t1 = block_sum(s1, sh);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x * RN + 0] = t0;
+    partials[blockIdx.x * RN + 1] = t1;
+    for (int q = 2; q < RN; ++q) partials[blockIdx.x * RN + q] = 0.0;
+  }
+}
+
+// out[0..6] = fixed-order sums of the partials; out[7], out[8] = B_alpha[n,n], B_nu[n,n].
+__global__ void reduce_final_kernel(const double* partials, int nblocks, const double* Ba,
+                                    const double* Bn, long long ld, int n, double* out,
+                                    const int* fail_flag) {
+  if (*fail_flag) return;
+  const int q = threadIdx.x;
+  if (q < RN) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += partials[b * RN + q];
+    out[q] = s;
+  }
+  if (q == RN) out[RN] = Ba ? Ba[n + (long long)n * ld] : 0.0;
+  if (q == RN + 1) out[RN + 1] = Bn ? Bn[n + (long long)n * ld] : 0.0;
+}
+
+cudaError_t launch_reduce_eval(const double* L, const double* Ba, const double* Bn,
+                               long long ld, int n, double* partials, double* out,
+                               const int* fail_flag, cudaStream_t s) {
+  reduce_eval_kernel<<<RBLOCKS, RTHREADS, 0, s>>>(L, Ba, Bn, ld, n, partials, fail_flag);
+  reduce_final_kernel<<<1, 32, 0, s>>>(partials, RBLOCKS, Ba, Bn, ld, n, out, fail_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_loglik(const double* L, long long ld, int n, double* partials,
+                                 double* out, const int* fail_flag, cudaStream_t s) {
+  const int blocks = 32;
+  reduce_loglik_kernel<<<blocks, RTHREADS, 0, s>>>(L, ld, n, partials, fail_flag);
+  reduce_final_kernel<<<1, 32, 0, s>>>(partials, blocks, nullptr, nullptr, ld, n, out,
+                                        fail_flag);
+  return cudaGetLastError();
+}
+
+__global__ void clear_upper_kernel(double* a, long long ld, int n) {
+  const int j = blockIdx.x;
+  for (int i = threadIdx.x; i < j && i < n; i += blockDim.x) a[i + (long long)j * ld] = 0.0;
+}
+
+cudaError_t launch_clear_upper(double* a, long long ld, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  clear_upper_kernel<<<n, 256, 0, s>>>(a, ld, n);
+  return cudaGetLastError();
+}
+
+}  // namespace mle

@@ -1,0 +1,231 @@
+// special.cuh — per-thread FP64 special functions for the Matern generation kernel.
+//
+//  * K_mu / K_{mu+1} for |mu| <= 1/2: Temme's series for x < 2, Steed's continued fraction
+//    (CF2, Thompson-Barnett) for x >= 2; then upward recurrence to K_nu and K_{nu-1}.
+//    This replaces scipy.special.kv (reference call sites bessel.py:97, matern.py:104, 111,
+//    123, bessel.py:322-323).
+//  * d/dnu [x^nu K_nu(x)] by the reference's four-regime dispatch (bessel.py:327-370):
+//    case 2 ascending series (bessel.py:184-223), case 3 uniform asymptotics
+//    (bessel.py:226-283), case 4 large-x (bessel.py:286-318), forward difference
+//    (bessel.py:321-324).  nu-only factors come precomputed in ThetaParams.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "theta.h"
+
+namespace mle {
+
+// Debye U_k and U_k' coefficient tables (theta independent), uploaded once per device.
+// Defined here: gen.cu is the only translation unit that includes this header.
+__constant__ double c_u_coef[(MLE_CASE3_NEAR + 1) * MLE_U_COEFF_STRIDE];
+__constant__ double c_du_coef[(MLE_CASE3_NEAR + 1) * MLE_U_COEFF_STRIDE];
+
+#define MLE_EPS 1.1102230246251565e-16
+#define MLE_PI 3.141592653589793
+#define MLE_SQRT_HALF_PI 1.2533141373155003  // sqrt(pi/2), bessel.py:58
+
+// K_mu(x), K_{mu+1}(x) for |mu| <= 1/2, x > 0.
+__device__ __forceinline__ void bessel_k_pair(const KLadder& L, double x, double* k_mu,
+                                              double* k_mu1) {
+  const double mu = L.mu;
+  if (x < 2.0) {
+    // Temme: K_mu = sum_k c_k f_k,  K_{mu+1} = (2/x) sum_k c_k (p_k - k f_k),
+    // c_k = (x^2/4)^k / k!.
+    const double x2 = 0.5 * x;
+    const double lnx2 = -log(x2);  // log(2/x)
+    const double e = mu * lnx2;
+    double sinh_e_over_e;
+    if (fabs(e) < 1e-3) {
+      const double e2 = e * e;
+      sinh_e_over_e = 1.0 + e2 * (1.0 / 6.0 + e2 * (1.0 / 120.0 + e2 * (1.0 / 5040.0)));
+    } else {
+      sinh_e_over_e = sinh(e) / e;
+    }
+    double ff = L.fact * (L.gam1 * cosh(e) + L.gam2 * sinh_e_over_e * lnx2);
+    double sum = ff;
+    const double ee = exp(e);
+    double p = 0.5 * ee / L.gampl;
+    double q = 0.5 / (ee * L.gammi);
+    double c = 1.0;
+    const double d = x2 * x2;
+    double sum1 = p;
+    const double mu2 = mu * mu;
+#pragma unroll 1
+    for (int i = 1; i < 64; ++i) {
+      const double di = (double)i;
+      ff = (di * ff + p + q) / (di * di - mu2);
+      c *= d / di;
+      p /= (di - mu);
+      q /= (di + mu);
+      const double del = c * ff;
+      sum += del;
+      const double del1 = c * (p - di * ff);
+      sum1 += del1;
+      if (fabs(del) < fabs(sum) * MLE_EPS) break;
+    }
+    *k_mu = sum;
+    *k_mu1 = sum1 * (2.0 / x);
+  } else {
+    // Steed's method for CF2 with the Thompson-Barnett normalisation.
+    double b = 2.0 * (1.0 + x);
+    double d = 1.0 / b;
+    double h = d, delh = d;
+    double q1 = 0.0, q2 = 1.0;
+    const double a1 = 0.25 - mu * mu;
+    double q = a1, c = a1;
+    double a = -a1;
+    double s = 1.0 + q * delh;
+#pragma unroll 1
+    for (int i = 2; i < 200; ++i) {
+      const double di = (double)i;
+      a -= 2.0 * (di - 1.0);
+      c = -a * c / di;
+      const double qnew = (q1 - b * q2) / a;
+      q1 = q2;
+      q2 = qnew;
+      q += c * qnew;
+      b += 2.0;
+      d = 1.0 / (b + a * d);
+      delh = (b * d - 1.0) * delh;
+      h += delh;
+      const double dels = q * delh;
+      s += dels;
+      if (fabs(dels) < fabs(s) * MLE_EPS) break;
+    }
+    h = a1 * h;
+    const double kmu = sqrt(MLE_PI / (2.0 * x)) * exp(-x) / s;
+    *k_mu = kmu;
+    *k_mu1 = kmu * (mu + x + 0.5 - h) / x;
+  }
+}
+
+// Runs the ladder: returns K_order (and K_{order-1} if wanted) for the ladder's order.
+__device__ __forceinline__ void bessel_k_ladder(const KLadder& L, double x, double* k_nu,
+                                                double* k_num1) {
+  double k0, k1;
+  bessel_k_pair(L, x, &k0, &k1);
+  const double two_over_x = 2.0 / x;
+#pragma unroll 1
+  for (int j = 1; j <= L.nsteps; ++j) {
+    const double kn = k0 + (L.mu + (double)j) * two_over_x * k1;
+    k0 = k1;
+    k1 = kn;
+  }
+  if (L.order_is_low) {
+    *k_nu = k0;
+    *k_num1 = k1;
+  } else {
+    *k_nu = k1;
+    *k_num1 = k0;
+  }
+}
+
+// numpy.polynomial.polynomial.polyval order (Horner from the top coefficient).
+__device__ __forceinline__ double polyval_const(const double* c, int ncoef, double p) {
+  double acc = c[ncoef - 1];
+#pragma unroll 1
+  for (int i = ncoef - 2; i >= 0; --i) acc = c[i] + acc * p;
+  return acc;
+}
+
+// Case 2: 0 < x < 8.5, nu away from integers (bessel.py:184-223).
+__device__ __forceinline__ double dnu_case2(const ThetaParams& P, double x) {
+  const double two_log_x = 2.0 * log(x);
+  const double x_two_nu = pow(x, P.two_nu);
+  const double quarter_x2 = 0.25 * x * x;
+  const double lead = P.c2_two_m_nu * x_two_nu;
+  const double log2 = 0.6931471805599453;
+  double prefactor = 0.5;
+  double total = 0.0;
+#pragma unroll 1
+  for (int k = 0; k <= MLE_CASE2_TERMS; ++k) {
+    if (k > 0) prefactor = prefactor * quarter_x2 / (double)k;
+    const double term_neg =
+        lead * (-log2 + two_log_x - P.c2_psi_neg + P.c2_d_pos[k]) * P.c2_gam_neg * P.c2_g_pos[k];
+    total = total + prefactor * (P.c2_term_pos[k] + term_neg);
+  }
+  return total;
+}
+
+// Case 3: 8.5 <= x < 30 (bessel.py:226-283).
+__device__ __forceinline__ double dnu_case3(const ThetaParams& P, double x) {
+  const double nu = P.nu;
+  const int kterms = (x < MLE_MID_TRUNC_SPLIT) ? MLE_CASE3_NEAR : MLE_CASE3_FAR;
+  const double z = x / nu;
+  const double zz1 = 1.0 + z * z;
+  const double root = sqrt(zz1);
+  const double p = 1.0 / root;
+  const double eta = root + log(z / (1.0 + root));
+  const double prefactor = pow(x, nu) * P.c3_sqrt_pi_2nu * exp(-nu * eta) / sqrt(root);
+  double sum_u = 0.0, sum_ku = 0.0, sum_du = 0.0;
+#pragma unroll 1
+  for (int k = 0; k <= kterms; ++k) {
+    const double u_val = polyval_const(c_u_coef + k * MLE_U_COEFF_STRIDE, 3 * k + 1, p);
+    const double du_val =
+        k == 0 ? 0.0 : polyval_const(c_du_coef + k * MLE_U_COEFF_STRIDE, 3 * k, p);
+    sum_u += P.c3_w[k] * u_val;
+    sum_ku += P.c3_wk[k] * u_val;
+    sum_du += P.c3_w[k] * du_val;
+  }
+  const double bracket = P.c3_log_nu + log(1.0 + root) - 1.0 / (2.0 * nu * zz1);
+  return bracket * prefactor * sum_u - prefactor * sum_ku +
+         (x * x / P.c3_nu3) * pow(zz1, -1.5) * prefactor * sum_du;
+}
+
+// Case 4: x >= 30 (bessel.py:286-318).
+__device__ __forceinline__ double dnu_case4(const ThetaParams& P, double x) {
+  const double log_x = log(x);
+  double total = log_x;
+  double x_pow = 1.0;
+#pragma unroll 1
+  for (int k = 1; k <= P.c4_kmax; ++k) {
+    x_pow = x_pow / x;
+    total = total + x_pow * (log_x + P.c4_b[k]) * P.c4_a[k];
+  }
+  return MLE_SQRT_HALF_PI * pow(x, P.nu_m_half) * exp(-x) * total;
+}
+
+// Forward difference (bessel.py:321-324); f_lo = x^nu K_nu(x) is shared with the caller.
+__device__ __forceinline__ double dnu_fd(const ThetaParams& P, double x, double f_lo) {
+  double k_hi, unused;
+  bessel_k_ladder(P.kfd, x, &k_hi, &unused);
+  const double f_hi = pow(x, P.nu_fd) * k_hi;
+  return (f_hi - f_lo) / MLE_FD_LAG;
+}
+
+// d/dnu [x^nu K_nu(x)] for x > 0 with the regime dispatch of bessel.py:327-370.
+__device__ __forceinline__ double dnu_xnu_knu(const ThetaParams& P, double x, double f) {
+  if (x < MLE_SMALL_MID_SPLIT) {
+    return P.fd_small ? dnu_fd(P, x, f) : dnu_case2(P, x);
+  } else if (x < MLE_MID_LARGE_SPLIT) {
+    return dnu_case3(P, x);
+  } else {
+    return P.fd_large ? dnu_fd(P, x, f) : dnu_case4(P, x);
+  }
+}
+
+// Matern covariance and its alpha / nu derivatives at distance h > 0 (matern.py:100-125).
+struct MaternVals {
+  double c, dalpha, dnu;
+};
+
+template <bool kDerivs>
+__device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, double h) {
+  MaternVals out;
+  const double u = h / P.alpha;
+  double k_nu, k_num1;
+  bessel_k_ladder(P.kmain, u, &k_nu, &k_num1);
+  const double u_nu = pow(u, P.nu);
+  out.c = P.scale_c * u_nu * k_nu;                                  // matern.py:104
+  if (kDerivs) {
+    out.dalpha = P.scale_a * pow(u, P.nu + 1.0) * k_num1;           // matern.py:111
+    const double f = u_nu * k_nu;                                   // matern.py:122
+    out.dnu = P.sigma2 * P.q * (P.dlog_q * f + dnu_xnu_knu(P, u, f));  // matern.py:125
+  } else {
+    out.dalpha = 0.0;
+    out.dnu = 0.0;
+  }
+  return out;
+}
+
+}  // namespace mle

@@ -1,0 +1,78 @@
+// theta.h — per-theta scalar prologue shared by the host (prologue.cpp) and the device
+// kernels.  Everything that depends on nu alone is hoisted here once per evaluation so the
+// per-pair work in the generation kernel is only the x-dependent part of each series.
+//
+// Sources of every quantity (reference tree, path:line):
+//   scale_c, scale_a, q, dlog_q       pkg/src/maternmle/matern.py:100-125
+//   case-2 constants (g_k, d_k, ...)   pkg/src/maternmle/bessel.py:184-223
+//   case-3 weights (sign * nu^-k ...)  pkg/src/maternmle/bessel.py:226-283
+//   case-4 a_k, b_k                    pkg/src/maternmle/bessel.py:286-318
+//   FD band and lag                    pkg/src/maternmle/bessel.py:117-141, 321-324
+// The K_nu ladder parameters (Temme / Steed CF2) replace scipy.special.kv.
+#pragma once
+
+#define MLE_CASE2_TERMS 20       // bessel.py:52  (k = 0..20)
+#define MLE_CASE3_NEAR 12        // bessel.py:53
+#define MLE_CASE3_FAR 8          // bessel.py:54
+#define MLE_CASE4_TERMS 5        // bessel.py:55
+#define MLE_U_COEFF_STRIDE 40    // >= 3*12+1 coefficients per Debye polynomial
+#define MLE_SMALL_MID_SPLIT 8.5  // bessel.py:46
+#define MLE_MID_LARGE_SPLIT 30.0 // bessel.py:47
+#define MLE_MID_TRUNC_SPLIT 15.0 // bessel.py:48
+#define MLE_FD_LAG 1e-9          // bessel.py:50
+
+// Parameters of one K-ladder: K_mu, K_{mu+1} by Temme's series (x <= 2) or Steed's
+// continued fraction (x > 2), |mu| <= 1/2, then `nsteps` upward recurrences.
+struct KLadder {
+  double mu;
+  double gam1, gam2;     // (1/G(1-mu) - 1/G(1+mu)) / (2 mu),  (1/G(1-mu) + 1/G(1+mu)) / 2
+  double gampl, gammi;   // 1/G(1+mu), 1/G(1-mu)
+  double fact;           // pi mu / sin(pi mu)
+  int nsteps;            // upward recurrence steps applied to (K_mu, K_{mu+1})
+  int order_is_low;      // 1: K_nu is the lower member of the final pair (nu < 1/2 case)
+};
+
+struct ThetaParams {
+  double sigma2, alpha, nu, nugget;
+  double scale_c;   // sigma2 * 2^(1-nu) / Gamma(nu)               matern.py:102
+  double scale_a;   // 2^(1-nu)/Gamma(nu) * sigma2 / alpha          matern.py:109
+  double q;         // 2^(1-nu) / Gamma(nu)                         matern.py:121
+  double dlog_q;    // -log 2 - psi(nu)                             matern.py:123
+  double nu_fd;     // fl(nu + 1e-9)                                bessel.py:322
+  int fd_small;     // nu within 1e-6 of an integer: x in (0, 8.5) uses the FD fallback
+  int fd_large;     // nu within 1e-6 of a half-integer: x >= 30 uses the FD fallback
+  KLadder kmain;    // ladder for K_nu and K_{nu-1}
+  KLadder kfd;      // ladder for K_{nu_fd} (only used in FD bands)
+  // ---- case 2 (0 < x < 8.5) ----
+  double c2_term_pos[MLE_CASE2_TERMS + 1];  // 2^nu (log2 + psi(nu) - d_k(-nu)) G(nu) g_k(-nu)
+  double c2_d_pos[MLE_CASE2_TERMS + 1];     // d_k(nu)
+  double c2_g_pos[MLE_CASE2_TERMS + 1];     // g_k(nu)
+  double c2_two_m_nu;                       // 2^-nu
+  double c2_psi_neg;                        // psi(-nu)
+  double c2_gam_neg;                        // Gamma(-nu) by reflection
+  double two_nu;                            // 2 nu
+  // ---- case 3 (8.5 <= x < 30) ----
+  double c3_w[MLE_CASE3_NEAR + 1];          // sign * nu^-k
+  double c3_wk[MLE_CASE3_NEAR + 1];         // sign * (k nu^-k / nu)
+  double c3_log_nu;                         // log(nu)
+  double c3_sqrt_pi_2nu;                    // sqrt(pi / (2 nu))
+  double c3_nu3;                            // nu^3
+  // ---- case 4 (x >= 30) ----
+  double c4_a[MLE_CASE4_TERMS + 1];
+  double c4_b[MLE_CASE4_TERMS + 1];
+  int c4_kmax;                              // last k with a_k != 0
+  double nu_m_half;                         // nu - 0.5
+};
+
+#ifdef __cplusplus
+extern "C++" {
+// Host prologue: fills P from theta (+ nugget).  Returns 0, or 2 for invalid theta
+// (non-finite or <= 0 components: MaternParams.__post_init__, matern.py:44-48).
+int mle_fill_theta(const double theta[3], double nugget, ThetaParams* P);
+// Ladder for a single order >= 0 (bessel_k of any non-negative order, including 0).
+void mle_fill_ladder(double order, KLadder* L);
+// Debye U_k coefficient tables (bessel.py:144-176), flattened [k][j] with stride
+// MLE_U_COEFF_STRIDE, for U and U'.  Filled once.
+void mle_fill_u_tables(double* u, double* du);
+}
+#endif

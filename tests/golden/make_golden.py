@@ -1,0 +1,195 @@
+"""Generate the committed golden fixtures under tests/golden/.
+
+Runs HERE only (needs the reference at /root/reference and mpmath); the GPU box
+never executes it.  Every value stored is either
+  * an output of the unmodified reference package (``maternmle``) on the pinned
+    synthetic inputs, or
+  * an independent 40-digit mpmath evaluation (Bessel order-derivative grid),
+so the oracle restatement (oracle/) and the CUDA engine are both pinned to the
+reference's own numbers.
+
+Usage:
+    python tests/golden/make_golden.py bessel
+    python tests/golden/make_golden.py small
+    python tests/golden/make_golden.py config1
+    python tests/golden/make_golden.py evals2        # config 2 seed 0 evaluations
+    python tests/golden/make_golden.py fit config2 SEED
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+REF_SRC = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF_SRC))
+sys.path.insert(0, str(REPO))
+
+import maternmle as ref  # noqa: E402  (the reference, imported read-only)
+
+from paper_2601_11437_b200.datasets import WORKLOADS  # noqa: E402
+
+
+def _eval_record(data, theta):
+    rec = {"theta": list(theta)}
+    params = ref.MaternParams(*theta)
+    try:
+        rec["loglik"] = ref.log_likelihood(data, params)
+    except ref.NotPositiveDefinite as exc:
+        rec["not_pd_pivot"] = exc.pivot
+        return rec
+    ev = ref.grad_and_fisher(data, params)
+    rec["eval_loglik"] = ev.loglik
+    rec["grad"] = ev.grad.tolist()
+    rec["fisher"] = ev.fisher.tolist()
+    return rec
+
+
+def make_bessel():
+    import mpmath as mp
+
+    mp.mp.dps = 40
+
+    def dnu_mp(nu, x):
+        f = lambda v: mp.mpf(x) ** v * mp.besselk(v, mp.mpf(x))  # noqa: E731
+        return float(mp.diff(f, mp.mpf(nu)))
+
+    grid = []
+    for nu in np.linspace(0.06, 2.47, 10):
+        for x in np.geomspace(1e-3, 60.0, 20):
+            nu_f, x_f = float(nu), float(x)
+            grid.append({
+                "nu": nu_f, "x": x_f,
+                "dnu_mp": dnu_mp(nu_f, x_f),
+                "k_mp": float(mp.besselk(nu_f, x_f)),
+                "dnu_ref": float(ref.dnu_xnu_knu(nu_f, x_f)),
+                "k_ref": float(ref.bessel_k(nu_f, x_f)),
+            })
+    spots = []
+    for nu, x in [(0.5, 1.0), (0.3, 2.0), (1.4, 0.01), (0.5, 10.0), (1.3, 20.0), (0.3, 35.0),
+                  (0.8, 14.9999), (0.8, 15.0001), (0.5, 8.4999), (0.5, 8.5001), (1.0, 3.0),
+                  (1.2, 30.0), (0.77, 0.5), (0.77, 5.0), (0.77, 10.0), (0.77, 31.0),
+                  (1.5, 40.0), (2.0, 0.7), (0.5, 45.0)]:
+        spots.append({"nu": nu, "x": x, "dnu_mp": dnu_mp(nu, x),
+                      "dnu_ref": float(ref.dnu_xnu_knu(nu, x)),
+                      "regime": ref.select_regime(nu, x).value})
+    kspots = [{"nu": nu, "x": x, "k_mp": float(mp.besselk(nu, x)), "k_ref": ref.bessel_k(nu, x)}
+              for nu, x in [(1.3, 0.7), (0.5, 1.0), (0.0, 0.3), (2.7, 4.0), (0.2, 1e-5),
+                            (1.9999999, 2.0), (3.5, 120.0)]]
+    out = {"description": "d/dnu[x^nu K_nu(x)] and K_nu: 40-digit mpmath (mp.diff of besselk) "
+                          "next to the reference maternmle outputs on the same points",
+           "grid": grid, "spots": spots, "k_spots": kspots}
+    (HERE / "bessel_golden.json").write_text(json.dumps(out, indent=1))
+
+
+def _grid_corner(side):
+    axis = np.linspace(0.0, 1.0, side)
+    gx, gy = np.meshgrid(axis, axis, indexing="ij")
+    return np.column_stack([gx.ravel(), gy.ravel()])
+
+
+def make_small():
+    """Small datasets (reference conftest/test shapes) with matrices + evaluations."""
+    rng = np.random.default_rng(0)
+    cases = {}
+    # 5x5 corner grid, theta (1, .1, .5), seed 20240901 (reference tests/conftest.py:35-37)
+    loc = _grid_corner(5)
+    cases["grid5"] = (loc, ref.simulate_grf(loc, ref.MaternParams(1.0, 0.1, 0.5), 20240901))
+    for n in (20, 50, 100):
+        loc = rng.uniform(size=(n, 2))
+        cases[f"rand{n}"] = (loc, rng.standard_normal(n))
+    loc = _grid_corner(12)
+    cases["grid12"] = (loc, ref.simulate_grf(loc, ref.MaternParams(1.0, 0.1, 0.5), 4))
+    # ragged: 131 points (crosses one 128-tile boundary)
+    loc = rng.uniform(size=(131, 2))
+    cases["rand131"] = (loc, ref.simulate_grf(loc, ref.MaternParams(1.2, 0.15, 0.9), 7))
+    thetas = [(1.0, 0.1, 0.5), (2.0, 0.3, 1.2), (0.5, 0.2, 0.8), (1.0, 0.15, 1.5),
+              (0.7, 0.08, 1.0), (1.3, 0.25, 2.3), (0.9, 0.4, 0.3)]
+    arrays = {}
+    meta = {}
+    for name, (loc, z) in cases.items():
+        arrays[f"{name}_loc"] = loc
+        arrays[f"{name}_z"] = z
+        data = ref.SpatialDataset(loc, z)
+        meta[name] = [_eval_record(data, th) for th in thetas]
+        if loc.shape[0] <= 100:
+            for th_i, th in enumerate(thetas[:4]):
+                p = ref.MaternParams(*th)
+                arrays[f"{name}_t{th_i}_sigma"] = ref.build_cov_matrix(data, p)
+                for w in ("sigma2", "alpha", "nu"):
+                    arrays[f"{name}_t{th_i}_{w}"] = ref.build_dcov_matrix(data, p, w)
+    np.savez_compressed(HERE / "small.npz", **arrays)
+    (HERE / "small_evals.json").write_text(json.dumps({"thetas": thetas, "cases": meta}, indent=1))
+
+
+def _config_data(name, seed):
+    wl = WORKLOADS[name]
+    loc = wl.locations(seed)
+    z = ref.simulate_grf(loc, ref.MaternParams(*wl.theta_true), seed)
+    return loc, z
+
+
+def make_config1():
+    loc, z = _config_data("config1", 0)
+    np.savez_compressed(HERE / "config1_seed0_data.npz", loc=loc, z=z)
+    data = ref.SpatialDataset(loc, z)
+    wl = WORKLOADS["config1"]
+    thetas = [wl.theta_true, wl.theta0, (0.8, 0.08, 0.65), (1.2, 0.12, 1.5), (0.9, 0.1, 2.0)]
+    evals = [_eval_record(data, th) for th in thetas]
+    (HERE / "config1_evals.json").write_text(json.dumps(evals, indent=1))
+
+
+def make_evals2():
+    loc, z = _config_data("config2", 0)
+    data = ref.SpatialDataset(loc, z)
+    wl = WORKLOADS["config2"]
+    evals = [_eval_record(data, th) for th in (wl.theta_true, wl.theta0)]
+    (HERE / "config2_evals.json").write_text(json.dumps(evals, indent=1))
+
+
+def make_fit(name, seed):
+    wl = WORKLOADS[name]
+    loc, z = _config_data(name, seed)
+    np.savez_compressed(HERE / f"{name}_seed{seed}_data.npz", loc=loc, z=z)
+    data = ref.SpatialDataset(loc, z)
+    th0 = ref.MaternParams(*wl.theta0)
+    cfg = ref.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    t0 = time.perf_counter()
+    res = ref.fisher_bt(data, cfg)
+    wall = time.perf_counter() - t0
+    rec = {
+        "config": name, "seed": seed, "theta0": list(wl.theta0),
+        "theta_hat": res.theta_hat.as_array().tolist(),
+        "loglik_at_hat": res.loglik_at_hat,
+        "fisher_at_hat": np.asarray(res.fisher_at_hat).tolist(),
+        "loglik_calls": res.loglik_calls, "grad_calls": res.grad_calls,
+        "used_fallback": res.used_fallback, "termination": res.termination.value,
+        "fisher_phase_loglik_calls": res.fisher_phase_loglik_calls,
+        "fisher_phase_grad_calls": res.fisher_phase_grad_calls,
+        "iterate_trace": [[t.as_array().tolist(), ll] for t, ll in res.iterate_trace],
+        "cpu_wall_s": wall, "cpu_threads": os.environ.get("OPENBLAS_NUM_THREADS", "default"),
+    }
+    (HERE / f"{name}_seed{seed}_fit.json").write_text(json.dumps(rec, indent=1))
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    if what == "bessel":
+        make_bessel()
+    elif what == "small":
+        make_small()
+    elif what == "config1":
+        make_config1()
+    elif what == "evals2":
+        make_evals2()
+    elif what == "fit":
+        make_fit(sys.argv[2], int(sys.argv[3]))
+    else:
+        raise SystemExit(f"unknown target {what}")

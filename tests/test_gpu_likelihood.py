@@ -1,0 +1,195 @@
+"""CUDA covariance assembly, Cholesky, log-likelihood, score and Fisher information vs the
+golden reference outputs and the CPU oracle.  Tolerances (north_star): log-likelihood 1e-10
+relative; Fisher 1e-8 relative; score 1e-8 relative to its two component magnitudes
+(SURVEY.md §8(c)).  At finite-difference-regime theta (nu within 1e-6 of an integer) the
+reference's own d/dnu entries carry lag-1e-9 forward-difference noise (~1e-6 per element,
+amplified by cond(Sigma)), so the nu-dependent entries are compared at 1e-3 there."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import config_data, fd_regime, load_json
+
+pytestmark = pytest.mark.gpu
+
+LL_TOL, FISHER_TOL, SCORE_TOL, FD_TOL = 1e-10, 1e-8, 1e-8, 1e-3
+
+
+def score_scale(theta, n, grad, fisher):
+    """Component magnitudes 1/2|tr(S^-1 S_i)| + 1/2|w^T S_i w| from the engine's outputs."""
+    s2 = theta[0]
+    half_tr = np.array([n / (2 * s2), s2 * abs(fisher[0, 1]), s2 * abs(fisher[0, 2])])
+    half_quad = np.array([abs(grad[0]) + n / (2 * s2),
+                          abs(grad[1] + s2 * fisher[0, 1]), abs(grad[2] + s2 * fisher[0, 2])])
+    return half_tr + half_quad
+
+
+def check_eval(gpu, data, rec, n):
+    th = rec["theta"]
+    ll = gpu.log_likelihood(data, th)
+    assert ll == pytest.approx(rec["loglik"], rel=LL_TOL)
+    ev = gpu.grad_and_fisher(data, th)
+    assert ev.loglik == pytest.approx(rec["eval_loglik"], rel=LL_TOL)
+    np.testing.assert_array_equal(ev.fisher, ev.fisher.T)
+    ref_g, ref_f = np.array(rec["grad"]), np.array(rec["fisher"])
+    scale = score_scale(th, n, ev.grad, ev.fisher)
+    fd = fd_regime(th)
+    for i in range(3):
+        tol = FD_TOL if (fd and i == 2) else SCORE_TOL
+        assert abs(ev.grad[i] - ref_g[i]) <= tol * scale[i], (th, i, ev.grad, ref_g)
+        for j in range(3):
+            tol = FD_TOL if (fd and 2 in (i, j)) else FISHER_TOL
+            assert abs(ev.fisher[i, j] - ref_f[i, j]) <= tol * abs(ref_f[i, j]) + 1e-300, (
+                th, i, j, ev.fisher, ref_f)
+
+
+def test_matrices_vs_golden(gpu, golden_small):
+    arrays, ev = golden_small
+    thetas = ev["thetas"]
+    for name in ev["cases"]:
+        if f"{name}_t0_sigma" not in arrays:
+            continue
+        data = gpu.SpatialDataset(arrays[f"{name}_loc"], arrays[f"{name}_z"])
+        for ti in range(4):
+            th = thetas[ti]
+            sig = gpu.build_cov_matrix(data, th)
+            ref = arrays[f"{name}_t{ti}_sigma"]
+            np.testing.assert_allclose(sig, ref, rtol=1e-13, atol=0)
+            assert np.array_equal(sig, sig.T)
+            np.testing.assert_array_equal(np.diag(sig), th[0])
+            s2 = gpu.build_dcov_matrix(data, th, "sigma2")
+            np.testing.assert_array_equal(s2, sig / th[0])
+            for w in ("alpha", "nu"):
+                got = gpu.build_dcov_matrix(data, th, w)
+                ref = arrays[f"{name}_t{ti}_{w}"]
+                assert np.array_equal(got, got.T)
+                np.testing.assert_array_equal(np.diag(got), 0.0)
+                assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref)), (name, ti, w)
+    with pytest.raises(ValueError):
+        gpu.build_dcov_matrix(data, thetas[0], "range")
+
+
+def test_small_evaluations_vs_golden(gpu, golden_small):
+    arrays, ev = golden_small
+    for name, recs in ev["cases"].items():
+        loc, z = arrays[f"{name}_loc"], arrays[f"{name}_z"]
+        data = gpu.SpatialDataset(loc, z)
+        for rec in recs:
+            if "not_pd_pivot" in rec:
+                with pytest.raises(gpu.NotPositiveDefinite):
+                    gpu.log_likelihood(data, rec["theta"])
+                continue
+            check_eval(gpu, data, rec, loc.shape[0])
+
+
+def test_config1_evaluations_vs_golden(gpu):
+    loc, z = config_data("config1")
+    data = gpu.SpatialDataset(loc, z)
+    for rec in load_json("config1_evals.json"):
+        check_eval(gpu, data, rec, loc.shape[0])
+
+
+def test_config2_evaluations_vs_golden(gpu):
+    loc, z = config_data("config2")
+    data = gpu.SpatialDataset(loc, z)
+    for rec in load_json("config2_evals.json"):
+        check_eval(gpu, data, rec, loc.shape[0])
+
+
+def test_oracle_parity_random(gpu):
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(11)
+    for n in (1, 2, 7, 127, 128, 129, 257):
+        loc = rng.uniform(size=(n, 2))
+        th = tuple(rng.uniform(0.3, 1.6, 3))
+        th = (th[0], 0.05 + 0.2 * th[1], th[2] + 0.013)
+        z = rng.standard_normal(n)
+        data = gpu.SpatialDataset(loc, z)
+        ll, g, f = O.eval_all(loc, z, th)
+        check_eval(gpu, data, {"theta": th, "loglik": O.loglik(loc, z, th), "eval_loglik": ll,
+                               "grad": g.tolist(), "fisher": f.tolist()}, n)
+
+
+def test_univariate_and_closed_forms(gpu):
+    d0 = gpu.SpatialDataset(np.array([[0.0, 0.0]]), np.array([0.0]))
+    assert gpu.log_likelihood(d0, (1.0, 0.1, 0.5)) == pytest.approx(-0.5 * math.log(2 * math.pi),
+                                                                     rel=1e-14)
+    d1 = gpu.SpatialDataset(np.array([[0.0, 0.0]]), np.array([1.0]))
+    assert gpu.log_likelihood(d1, (1.0, 0.1, 0.5)) == pytest.approx(
+        -0.5 * math.log(2 * math.pi) - 0.5, rel=1e-14)
+    loc = np.array([[i / 9, j / 9] for i in range(10) for j in range(10)])
+    data = gpu.SpatialDataset(loc, np.random.default_rng(3).standard_normal(100))
+    assert gpu.grad_and_fisher(data, (2.0, 0.1, 0.5)).fisher[0, 0] == 100 / (2.0 * 4.0)
+
+
+def test_grad_sigma2_zero_when_quadratic_form_is_n(gpu):
+    axis = np.linspace(0, 1, 4)
+    gx, gy = np.meshgrid(axis, axis, indexing="ij")
+    loc = np.column_stack([gx.ravel(), gy.ravel()])
+    holder = gpu.SpatialDataset(loc, np.zeros(16))
+    low = gpu.cholesky_lower(gpu.build_cov_matrix(holder, (1.0, 0.1, 0.5)))
+    z = low @ (4.0 * np.eye(16)[0])
+    ev = gpu.grad_and_fisher(gpu.SpatialDataset(loc, z), (1.0, 0.1, 0.5))
+    assert ev.grad[0] == pytest.approx(0.0, abs=1e-10)
+
+
+def test_not_positive_definite_paths(gpu):
+    coincident = gpu.SpatialDataset(np.array([[0.0, 0.0], [0.0, 0.0]]), np.zeros(2))
+    with pytest.raises(gpu.NotPositiveDefinite) as info:
+        gpu.log_likelihood(coincident, (1.0, 0.1, 0.5))
+    assert info.value.pivot == 1
+    with pytest.raises(gpu.NotPositiveDefinite):
+        gpu.grad_and_fisher(coincident, (1.0, 0.1, 0.5))
+    obj = gpu.LikelihoodObjective(coincident)
+    assert obj.loglik([1.0, 0.1, 0.5]) == -math.inf
+    assert obj.loglik([1.0, -0.1, 0.5]) == -math.inf  # invalid theta -> -inf, still counted
+    assert obj.loglik_calls == 2
+    with pytest.raises(gpu.InitializationFailed):
+        c = gpu.MaternParams(2.505, 2.505, 1.005)
+        gpu.fisher_bt(coincident, gpu.FisherBTConfig(theta_lower=c, theta_upper=c))
+
+
+def test_cholesky(gpu):
+    np.testing.assert_array_equal(gpu.cholesky_lower(np.eye(3)), np.eye(3))
+    np.testing.assert_allclose(gpu.cholesky_lower(np.array([[4.0, 2.0], [2.0, 5.0]])),
+                               [[2.0, 0.0], [1.0, 2.0]], atol=1e-15)
+    with pytest.raises(gpu.NotPositiveDefinite) as info:
+        gpu.cholesky_lower(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    assert info.value.pivot == 1
+    with pytest.raises(ValueError):
+        gpu.cholesky_lower(np.zeros((2, 3)))
+    rng = np.random.default_rng(5)
+    for n in (1, 5, 127, 128, 129, 300, 1000):
+        a = rng.standard_normal((n, n))
+        spd = a @ a.T + n * np.eye(n)
+        low = gpu.cholesky_lower(spd)
+        assert np.all(np.triu(low, 1) == 0.0)
+        np.testing.assert_allclose(low @ low.T, spd, rtol=0, atol=1e-12 * np.max(np.abs(spd)))
+    # failing pivot deep inside a tile and across tiles
+    for n, p in ((200, 150), (300, 5)):
+        spd = np.eye(n)
+        spd[p, p] = -1.0
+        with pytest.raises(gpu.NotPositiveDefinite) as info:
+            gpu.cholesky_lower(spd)
+        assert info.value.pivot == p
+
+
+def test_sigma2_scaling_identity_large(gpu):
+    """Size-independent property at n = 16,384: Sigma(c s2) = c Sigma(s2) gives
+    l(c s2) = l(s2) - n/2 log c - q (1/c - 1)/2 with q = z^T Sigma^-1 z from the score."""
+    loc = gpu.jittered_grid(128, 0)
+    z = np.random.default_rng(0).standard_normal(loc.shape[0])
+    data = gpu.SpatialDataset(loc, z)
+    th = (1.5, 0.05, 0.8)
+    ev = gpu.grad_and_fisher(data, th)
+    n = loc.shape[0]
+    q = 2 * th[0] * ev.grad[0] + n
+    c = 2.0
+    pred = ev.loglik - 0.5 * n * math.log(c) - 0.5 * q * (1 / c - 1)
+    got = gpu.log_likelihood(data, (c * th[0], th[1], th[2]))
+    assert got == pytest.approx(pred, rel=1e-11)
+    assert gpu.log_likelihood(data, th) == ev.loglik
+    assert np.all(np.linalg.eigvalsh(ev.fisher) > 0)

@@ -1,0 +1,113 @@
+"""CUDA special functions vs the golden vectors (reference outputs + 40-digit mpmath)."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_bessel_k_grid(gpu, bessel_golden):
+    nus = np.array([p["nu"] for p in bessel_golden["grid"]])
+    xs = np.array([p["x"] for p in bessel_golden["grid"]])
+    k_mp = np.array([p["k_mp"] for p in bessel_golden["grid"]])
+    k_ref = np.array([p["k_ref"] for p in bessel_golden["grid"]])
+    got = gpu.bessel_k(nus, xs)
+    # Temme/CF2 in FP64 is within a few ulp of the 40-digit value; scipy's AMOS kv (the
+    # reference) itself deviates by up to ~7e-14 near x = 2.
+    assert np.max(np.abs(got - k_mp) / k_mp) <= 5e-15
+    assert np.max(np.abs(got - k_ref) / k_ref) <= 2e-13
+
+
+def test_bessel_k_spots_and_closed_forms(gpu, bessel_golden):
+    for s in bessel_golden["k_spots"]:
+        assert gpu.bessel_k(s["nu"], s["x"]) == pytest.approx(s["k_mp"], rel=2e-14)
+    xs = np.linspace(0.05, 30.0, 200)
+    closed = np.sqrt(np.pi / (2 * xs)) * np.exp(-xs)
+    np.testing.assert_allclose(gpu.bessel_k(0.5, xs), closed, rtol=1e-14)
+    for nu in np.linspace(0.0, 3.0, 31):
+        for x in (0.01, 0.5, 3.0, 25.0):
+            assert gpu.bessel_k(nu, x) == gpu.bessel_k(-nu, x)
+
+
+def test_dnu_grid(gpu, bessel_golden):
+    worst_mp = worst_ref = 0.0
+    for nu in sorted({p["nu"] for p in bessel_golden["grid"]}):
+        pts = [p for p in bessel_golden["grid"] if p["nu"] == nu]
+        xs = np.array([p["x"] for p in pts])
+        got = gpu.dnu_xnu_knu(nu, xs)
+        mp_ = np.array([p["dnu_mp"] for p in pts])
+        ref = np.array([p["dnu_ref"] for p in pts])
+        worst_mp = max(worst_mp, np.max(np.abs(got - mp_) / (1 + np.abs(mp_))))
+        worst_ref = max(worst_ref, np.max(np.abs(got - ref) / (1 + np.abs(ref))))
+    assert worst_mp <= 1e-6      # reference acceptance criterion 1
+    assert worst_ref <= 1e-9     # parity with the reference's own outputs
+
+
+def test_dnu_spots(gpu, bessel_golden):
+    for s in bessel_golden["spots"]:
+        got = gpu.dnu_xnu_knu(s["nu"], s["x"])
+        if s["regime"] == "finite_diff":
+            # the reference's lag-1e-9 forward difference carries ~1e-6 relative noise
+            assert abs(got - s["dnu_ref"]) <= 1e-5 * (1 + abs(s["dnu_ref"]))
+            assert abs(got - s["dnu_mp"]) <= 1e-5 * (1 + abs(s["dnu_mp"]))
+        else:
+            assert abs(got - s["dnu_ref"]) <= 1e-9 * (1 + abs(s["dnu_ref"])), s
+            assert abs(got - s["dnu_mp"]) <= 1e-6 * (1 + abs(s["dnu_mp"])), s
+
+
+def test_dnu_zero_and_domain(gpu):
+    assert gpu.dnu_xnu_knu(0.7, 0.0) == 0.0
+    out = gpu.dnu_xnu_knu(0.77, np.array([0.0, 0.5, 5.0, 10.0, 31.0]))
+    for x, v in zip([0.0, 0.5, 5.0, 10.0, 31.0], out):
+        assert v == gpu.dnu_xnu_knu(0.77, x)
+    with pytest.raises(ValueError):
+        gpu.dnu_xnu_knu(0.0, 1.0)
+    with pytest.raises(ValueError):
+        gpu.dnu_xnu_knu(0.5, -1.0)
+    with pytest.raises(ValueError):
+        gpu.bessel_k(0.5, -1.0)
+    with pytest.raises(ValueError):
+        gpu.bessel_k(math.nan, 1.0)
+
+
+def test_case4_half_integer(gpu):
+    # nu = 1/2 near-half-integer band at x >= 30 uses the forward difference; nu = 0.3 the
+    # large-x series; both must track the 40-digit value.
+    x = 35.0
+    closed = math.sqrt(math.pi / 2.0) * math.exp(-x) * math.log(x)
+    assert gpu.dnu_xnu_knu(0.5, x) == pytest.approx(closed, rel=1e-5)
+
+
+def test_matern_elementwise_closed_forms(gpu):
+    h = np.linspace(0.01, 5.0, 200)
+    np.testing.assert_allclose(gpu.matern_cov(h, (1.0, 0.1, 0.5)), np.exp(-h / 0.1), rtol=1e-12)
+    np.testing.assert_allclose(gpu.matern_cov(h, (2.0, 1.0, 1.5)), 2 * (1 + h) * np.exp(-h),
+                               rtol=1e-12)
+    assert gpu.matern_cov(0.0, (3.2, 1.7, 1.9)) == 3.2
+    assert gpu.dcov_dsigma2(0.0, (1.7, 0.2, 0.8)) == 1.0
+    assert gpu.dcov_dalpha(0.0, (1.0, 0.3, 1.2)) == 0.0
+    assert gpu.dcov_dnu(0.0, (1.0, 0.3, 1.2)) == 0.0
+    assert gpu.dcov_dalpha(0.1, (1.0, 0.1, 0.5)) == pytest.approx(10 * math.exp(-1), rel=1e-12)
+    grid = np.arange(0.0, 5.0 + 1e-9, 0.01)
+    for th in ((1.0, 0.1, 0.5), (0.3, 0.7, 1.3), (2.0, 0.25, 2.4)):
+        v = gpu.matern_cov(grid, th)
+        assert np.all(np.diff(v) <= 0.0) and np.all(v[1:] > 0.0) and np.all(v <= th[0])
+    with pytest.raises(ValueError):
+        gpu.matern_cov(-0.1, (1.0, 0.1, 0.5))
+
+
+def test_matern_derivatives_vs_oracle(gpu):
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(3)
+    h = rng.uniform(0.0, 2.0, 4000)
+    for th in ((1.0, 0.3, 1.2), (0.7, 0.05, 0.4), (1.5, 0.05, 0.8), (1.0, 0.2, 1.5),
+               (0.9, 0.08, 2.6)):
+        for kind, fn in (("sigma", gpu.matern_cov), ("sigma2", gpu.dcov_dsigma2),
+                         ("alpha", gpu.dcov_dalpha), ("nu", gpu.dcov_dnu)):
+            got, ref = fn(h, th), O.elem(h, th, kind)
+            scale = np.max(np.abs(ref))
+            tol = 1e-12 if kind != "nu" else 1e-10  # case-2 series cancels near x = 8.5
+            assert np.max(np.abs(got - ref)) <= tol * scale, (th, kind)
