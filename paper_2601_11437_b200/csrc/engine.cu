@@ -15,6 +15,7 @@
 // tr(Sigma^-1 S_i) = tr B_i, w^T S_i w = y^T B_i y and tr(W_i W_j) = <B_i, B_j>_F.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -117,34 +118,62 @@ GemmArgs gemm_base(const mle_ctx* c) {
   return g;
 }
 
+// Two-level blocking: inner steps of kNB = 128 (diagonal tile factor/inverse, panel
+// products, updates confined to the current outer block), then one trailing update per
+// outer block of kOuter tiles with K = kOuter * 128, which amortises the GEMM pipeline
+// fill / C traffic over 4x more k-steps than a single-level right-looking sweep.
+constexpr int kOuter = 4;
+
+int gemm(mle_ctx* c, const GemmArgs& g, BLayout bl, int batch) {
+  ++c->launches;
+  CUDA_TRY(launch_gemm(g, bl, batch, c->stream));
+  return MLE_OK;
+}
+
 // Right-looking blocked Cholesky of the padded, augmented matrix `a` (ld = N).
 int run_potrf(mle_ctx* c, double* a, long long N, int Nt, long long n_aug) {
   const long long ld = N;
-  for (int k = 0; k < Nt; ++k) {
-    const long long k0 = (long long)k * kNB;
-    double* linv_k = c->linv + (size_t)k * kNB * kNB;
-    ++c->launches;
-    CUDA_TRY(launch_potrf_diag(a, ld, (int)k0, n_aug, linv_k, c->fail_flag, c->fail_idx,
-                               c->stream));
-    const int rem = Nt - k - 1;
-    if (rem == 0) break;
-    double* panel = a + (k0 + kNB) + k0 * ld;
-    // panel <- panel * Linv_k^T   (in place: BN = 128 covers the whole panel width)
-    GemmArgs g = gemm_base(c);
-    g.A[0] = panel; g.lda = ld;
-    g.B[0] = linv_k; g.ldb = kNB;
-    g.C[0] = panel; g.ldc = ld;
-    g.tiles_m = rem; g.tiles_n = 1; g.lower = 0; g.alpha = 1.0; g.beta = 0.0;
-    ++c->launches;
-    CUDA_TRY(launch_gemm(g, kBNK, 1, c->stream));
-    // trailing lower tiles: A_TT -= P P^T
+  int rc;
+  for (int b0 = 0; b0 < Nt; b0 += kOuter) {
+    const int b1 = std::min(Nt, b0 + kOuter);
+    for (int k = b0; k < b1; ++k) {
+      const long long k0 = (long long)k * kNB;
+      double* linv_k = c->linv + (size_t)k * kNB * kNB;
+      ++c->launches;
+      CUDA_TRY(launch_potrf_diag(a, ld, (int)k0, n_aug, linv_k, c->fail_flag, c->fail_idx,
+                                 c->stream));
+      const int rem = Nt - k - 1;
+      if (rem == 0) break;
+      double* panel = a + (k0 + kNB) + k0 * ld;
+      // panel <- panel * Linv_k^T   (in place: BN = 128 covers the whole panel width)
+      GemmArgs g = gemm_base(c);
+      g.A[0] = panel; g.lda = ld;
+      g.B[0] = linv_k; g.ldb = kNB;
+      g.C[0] = panel; g.ldc = ld;
+      g.tiles_m = rem; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
+      if ((rc = gemm(c, g, kBNK, 1))) return rc;
+      // inner update of the remaining columns of this outer block (lower trapezoid)
+      const int wcols = b1 - k - 1;
+      if (wcols > 0) {
+        GemmArgs t = gemm_base(c);
+        t.A[0] = panel; t.lda = ld;
+        t.B[0] = panel; t.ldb = ld;
+        t.C[0] = a + (k0 + kNB) + (k0 + kNB) * ld; t.ldc = ld;
+        t.tiles_m = rem; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
+        if ((rc = gemm(c, t, kBNK, 1))) return rc;
+      }
+    }
+    const int rem = Nt - b1;
+    if (rem <= 0) continue;
+    // outer trailing update: A_TT -= P P^T with P = L[T, b0:b1], K = (b1 - b0) * 128
+    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
     GemmArgs t = gemm_base(c);
-    t.A[0] = panel; t.lda = ld;
-    t.B[0] = panel; t.ldb = ld;
-    t.C[0] = a + (k0 + kNB) + (k0 + kNB) * ld; t.ldc = ld;
+    t.A[0] = a + t0 + c0 * ld; t.lda = ld;
+    t.B[0] = a + t0 + c0 * ld; t.ldb = ld;
+    t.C[0] = a + t0 + t0 * ld; t.ldc = ld;
+    t.K = (b1 - b0) * kNB;
     t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
-    ++c->launches;
-    CUDA_TRY(launch_gemm(t, kBNK, 1, c->stream));
+    if ((rc = gemm(c, t, kBNK, 1))) return rc;
   }
   return MLE_OK;
 }
@@ -154,59 +183,91 @@ int run_solves(mle_ctx* c) {
   const long long N = c->N, ld = N;
   const int Nt = c->Nt;
   double* S[2] = {c->sa, c->sn};
-  // forward sweep X = L^-1 S (all columns)
-  for (int k = 0; k < Nt; ++k) {
-    const long long k0 = (long long)k * kNB;
-    const double* linv_k = c->linv + (size_t)k * kNB * kNB;
-    GemmArgs g = gemm_base(c);
-    for (int b = 0; b < 2; ++b) {
-      g.A[b] = linv_k;
-      g.B[b] = S[b] + k0;   // B(n, kk) = S[k0 + kk, n]  (kBKN)
-      g.C[b] = S[b] + k0;   // in place: BM = 128 covers the whole row panel
+  const double* L = c->sigma;
+  int rc;
+  // forward sweep X = L^-1 S (all columns), row blocks top-down
+  for (int b0 = 0; b0 < Nt; b0 += kOuter) {
+    const int b1 = std::min(Nt, b0 + kOuter);
+    for (int k = b0; k < b1; ++k) {
+      const long long k0 = (long long)k * kNB;
+      const double* linv_k = c->linv + (size_t)k * kNB * kNB;
+      GemmArgs g = gemm_base(c);
+      for (int b = 0; b < 2; ++b) {
+        g.A[b] = linv_k;
+        g.B[b] = S[b] + k0;   // B(n, kk) = S[k0 + kk, n]  (kBKN)
+        g.C[b] = S[b] + k0;   // in place: BM = 128 covers the whole row panel
+      }
+      g.lda = kNB; g.ldb = ld; g.ldc = ld;
+      g.tiles_m = 1; g.tiles_n = Nt; g.alpha = 1.0; g.beta = 0.0;
+      if ((rc = gemm(c, g, kBKN, 2))) return rc;
+      const int wrows = b1 - k - 1;  // remaining row tiles of this outer block
+      if (wrows > 0) {
+        GemmArgs t = gemm_base(c);
+        for (int b = 0; b < 2; ++b) {
+          t.A[b] = L + (k0 + kNB) + k0 * ld;   // L[k+1 : b1, k]
+          t.B[b] = S[b] + k0;                  // X_k (kBKN)
+          t.C[b] = S[b] + (k0 + kNB);
+        }
+        t.lda = ld; t.ldb = ld; t.ldc = ld;
+        t.tiles_m = wrows; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
+        if ((rc = gemm(c, t, kBKN, 2))) return rc;
+      }
     }
-    g.lda = kNB; g.ldb = ld; g.ldc = ld;
-    g.tiles_m = 1; g.tiles_n = Nt; g.alpha = 1.0; g.beta = 0.0;
-    ++c->launches;
-    CUDA_TRY(launch_gemm(g, kBKN, 2, c->stream));
-    const int rem = Nt - k - 1;
-    if (rem == 0) break;
+    const int rem = Nt - b1;
+    if (rem <= 0) continue;
+    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
     GemmArgs t = gemm_base(c);
     for (int b = 0; b < 2; ++b) {
-      t.A[b] = c->sigma + (k0 + kNB) + k0 * ld;   // L[T, k]
-      t.B[b] = S[b] + k0;                         // X_k (kBKN)
-      t.C[b] = S[b] + (k0 + kNB);
+      t.A[b] = L + t0 + c0 * ld;   // L[T, b0:b1]
+      t.B[b] = S[b] + c0;          // X[b0:b1, :] (kBKN)
+      t.C[b] = S[b] + t0;
     }
     t.lda = ld; t.ldb = ld; t.ldc = ld;
+    t.K = (b1 - b0) * kNB;
     t.tiles_m = rem; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
-    ++c->launches;
-    CUDA_TRY(launch_gemm(t, kBKN, 2, c->stream));
+    if ((rc = gemm(c, t, kBKN, 2))) return rc;
   }
   // right sweep on lower tiles: B[j:, j] = X[j:, j] Linv_j^T ; X[T,T] -= B[T,j] L[T,j]^T
-  for (int j = 0; j < Nt; ++j) {
-    const long long j0 = (long long)j * kNB;
-    const double* linv_j = c->linv + (size_t)j * kNB * kNB;
-    GemmArgs g = gemm_base(c);
-    for (int b = 0; b < 2; ++b) {
-      g.A[b] = S[b] + j0 + j0 * ld;
-      g.B[b] = linv_j;
-      g.C[b] = S[b] + j0 + j0 * ld;
+  for (int b0 = 0; b0 < Nt; b0 += kOuter) {
+    const int b1 = std::min(Nt, b0 + kOuter);
+    for (int j = b0; j < b1; ++j) {
+      const long long j0 = (long long)j * kNB;
+      const double* linv_j = c->linv + (size_t)j * kNB * kNB;
+      GemmArgs g = gemm_base(c);
+      for (int b = 0; b < 2; ++b) {
+        g.A[b] = S[b] + j0 + j0 * ld;
+        g.B[b] = linv_j;
+        g.C[b] = S[b] + j0 + j0 * ld;
+      }
+      g.lda = ld; g.ldb = kNB; g.ldc = ld;
+      g.tiles_m = Nt - j; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
+      if ((rc = gemm(c, g, kBNK, 2))) return rc;
+      const int wcols = b1 - j - 1;
+      if (wcols > 0) {
+        GemmArgs t = gemm_base(c);
+        for (int b = 0; b < 2; ++b) {
+          t.A[b] = S[b] + (j0 + kNB) + j0 * ld;   // B[T, j]
+          t.B[b] = L + (j0 + kNB) + j0 * ld;      // L[T, j]  (kBNK)
+          t.C[b] = S[b] + (j0 + kNB) + (j0 + kNB) * ld;
+        }
+        t.lda = ld; t.ldb = ld; t.ldc = ld;
+        t.tiles_m = Nt - j - 1; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
+        if ((rc = gemm(c, t, kBNK, 2))) return rc;
+      }
     }
-    g.lda = ld; g.ldb = kNB; g.ldc = ld;
-    g.tiles_m = Nt - j; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
-    ++c->launches;
-    CUDA_TRY(launch_gemm(g, kBNK, 2, c->stream));
-    const int rem = Nt - j - 1;
-    if (rem == 0) break;
+    const int rem = Nt - b1;
+    if (rem <= 0) continue;
+    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
     GemmArgs t = gemm_base(c);
     for (int b = 0; b < 2; ++b) {
-      t.A[b] = S[b] + (j0 + kNB) + j0 * ld;            // B[T, j]
-      t.B[b] = c->sigma + (j0 + kNB) + j0 * ld;         // L[T, j]  (kBNK)
-      t.C[b] = S[b] + (j0 + kNB) + (j0 + kNB) * ld;
+      t.A[b] = S[b] + t0 + c0 * ld;   // B[T, b0:b1]
+      t.B[b] = L + t0 + c0 * ld;      // L[T, b0:b1]
+      t.C[b] = S[b] + t0 + t0 * ld;
     }
     t.lda = ld; t.ldb = ld; t.ldc = ld;
+    t.K = (b1 - b0) * kNB;
     t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
-    ++c->launches;
-    CUDA_TRY(launch_gemm(t, kBNK, 2, c->stream));
+    if ((rc = gemm(c, t, kBNK, 2))) return rc;
   }
   return MLE_OK;
 }

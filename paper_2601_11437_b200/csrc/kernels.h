@@ -37,7 +37,9 @@ struct GemmArgs {
   int tiles_m;       // number of 128-row tiles of C
   int tiles_n;       // number of 128-column tiles of C (full mode)
   int lower;         // 1: only tiles (tm >= tn) of a tiles_m x tiles_m grid
-  double alpha, beta;
+  int trap;          // full mode: 1 skips tiles with tm < tn (lower trapezoid)
+  double alpha;      // +1 or -1
+  double beta;       // 0 (overwrite) or 1 (accumulate into C)
   const int* fail_flag;
 };
 

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
 
   int tm, tn;
   tile_coords(g, &tm, &tn);
+  if (g.trap && tm < tn) return;
   const bool z1 = blockIdx.z != 0;
   // no __restrict__: panel products run in place (C aliases A or B; see engine.cu)
   const double* A = (z1 ? g.A[1] : g.A[0]) + (long long)tm * BM;
@@ -116,20 +117,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
     }
   };
 
-  double acc[4][4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
-
   const int KT = g.K / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) load_stage(s, s);
     cp_async_commit();
   }
+
+  // Accumulators start from C (beta = 1) so the C read overlaps the pipeline prologue and
+  // the epilogue is store-only; alpha = -1 is applied by negating the A fragments.
+  // mma f64 fragment map: c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1).
+  double acc[4][4][4];
+  if (g.beta != 0.0) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int r = wm * 64 + mi * 16 + gq;
+        const int c = wn * 32 + ni * 8 + 2 * tq;
+        const double* p0 = C + r + (long long)c * ldc;
+        const double* p1 = p0 + ldc;
+        acc[mi][ni][0] = p0[0];
+        acc[mi][ni][1] = p1[0];
+        acc[mi][ni][2] = p0[8];
+        acc[mi][ni][3] = p1[8];
+      }
+  } else {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[mi][ni][e] = 0.0;
+  }
+  const unsigned neg = g.alpha < 0.0 ? 0x80000000u : 0u;
 
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
@@ -151,6 +172,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
         af[mi][1] = as[(kk + tq) * SA + r0 + 8];
         af[mi][2] = as[(kk + tq + 4) * SA + r0];
         af[mi][3] = as[(kk + tq + 4) * SA + r0 + 8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)  // sign flip on the integer pipe (alpha = -1)
+          af[mi][e] = __hiloint2double(__double2hiint(af[mi][e]) ^ (int)neg,
+                                       __double2loint(af[mi][e]));
       }
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
@@ -171,29 +196,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // epilogue: c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
-  const double alpha = g.alpha, beta = g.beta;
+  // epilogue: store-only
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
       const int r = wm * 64 + mi * 16 + gq;
       const int c = wn * 32 + ni * 8 + 2 * tq;
-      double* p00 = C + r + (long long)c * ldc;
-      double* p01 = C + r + (long long)(c + 1) * ldc;
-      double* p10 = p00 + 8;
-      double* p11 = p01 + 8;
-      if (beta != 0.0) {
-        *p00 = alpha * acc[mi][ni][0] + beta * *p00;
-        *p01 = alpha * acc[mi][ni][1] + beta * *p01;
-        *p10 = alpha * acc[mi][ni][2] + beta * *p10;
-        *p11 = alpha * acc[mi][ni][3] + beta * *p11;
-      } else {
-        *p00 = alpha * acc[mi][ni][0];
-        *p01 = alpha * acc[mi][ni][1];
-        *p10 = alpha * acc[mi][ni][2];
-        *p11 = alpha * acc[mi][ni][3];
-      }
+      double* p0 = C + r + (long long)c * ldc;
+      double* p1 = p0 + ldc;
+      p0[0] = acc[mi][ni][0];
+      p1[0] = acc[mi][ni][1];
+      p0[8] = acc[mi][ni][2];
+      p1[8] = acc[mi][ni][3];
     }
   }
 }
@@ -226,27 +241,105 @@ cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s
 }
 
 // ---------------------------------------------------------------------------------------
-// Diagonal tile: Cholesky + inverse in shared memory.
-// Ls is column-major with stride 129: L(i, j) (i >= j) at Ls[j*129 + i]; the inverse
-// X = L^-1 (i > j) is kept in the other triangle at Ls[i*129 + j], its diagonal in dinv.
+// Diagonal tile: Cholesky + inverse of one 128x128 tile in shared memory (one CTA).
+// Ls is column-major with stride DS: L(i, j) (i >= j) at Ls[j*DS + i].  The inverse
+// X = L^-1 lives in the other triangle, row-major: X(i, j) (i > j) at Ls[i*DS + j], with
+// its diagonal in dinv.  Only the pivot chain is scalar (16x16 blocks in one warp's
+// registers) plus the 16-row panel solves; trailing updates and the inverse assembly
+// (recursive doubling 16 -> 32 -> 64 -> 128) are 16x16-blocked DMMA products over smem.
 namespace {
-constexpr int DT = kNB;           // 128
-constexpr int DS = DT + 1;        // smem stride
-constexpr int DB = 16;            // inner block
+constexpr int DT = kNB;     // 128
+constexpr int DS = DT + 4;  // smem stride (= 4 mod 16: conflict-free mma fragment loads)
+constexpr int DB = 16;      // register block
 constexpr int DTHREADS = 512;
+constexpr int DWARPS = DTHREADS / 32;
+constexpr int DSCR = 64 * 64;  // scratch for the inverse doubling products
+constexpr size_t kDiagSmem = sizeof(double) * (DT * DS + DT + DSCR);
+
+__device__ __forceinline__ double flip_sign(double x, unsigned neg) {
+  return __hiloint2double(__double2hiint(x) ^ (int)neg, __double2loint(x));
+}
+
+// acc (one 16x16 output block = two n8 tiles) += sign * A(16 x K) * B(16 x K)^T, with the
+// operands read through accessor functors fa(row, k), fb(col, k).
+template <class FA, class FB>
+__device__ __forceinline__ void mma16x16(double (&acc)[2][4], FA fa, FB fb, int K,
+                                         unsigned neg) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    double a[4] = {fa(g, k0 + t), fa(g + 8, k0 + t), fa(g, k0 + t + 4), fa(g + 8, k0 + t + 4)};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) a[e] = flip_sign(a[e], neg);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const double b[2] = {fb(nt * 8 + g, k0 + t), fb(nt * 8 + g, k0 + t + 4)};
+      dmma_16x8x8(acc[nt], a, b);
+    }
+  }
+}
+
+// Lower-triangle task index -> (bi, bj), bi >= bj.
+__device__ __forceinline__ void tri_index(int t, int* bi, int* bj) {
+  int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while (i * (i + 1) / 2 > t) --i;
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  *bi = i;
+  *bj = t - i * (i + 1) / 2;
+}
+
+// One pivot step of the register-resident 16x16 Cholesky (lane r holds row r); recursion
+// keeps every index of v[] a compile-time constant so the block never leaves registers.
+template <int C>
+__device__ __forceinline__ void chol16_step(double (&v)[16], int r, int lane, long long g0,
+                                            long long n_aug, bool& failed, int* s_fail,
+                                            long long* fail_idx, int* fail_flag) {
+  if constexpr (C < 16) {
+    const double d = __shfl_sync(0xffffffffu, v[C], C);
+    const bool aug = (g0 + C == n_aug);  // augmented index n carries y: no pivot there
+    if (!aug && !(d > 0.0) && !failed) {  // LAPACK dpotf2: AJJ <= 0 or NaN; first wins
+      if (lane == 0) {
+        *s_fail = 1;
+        *fail_idx = g0 + C;
+        *fail_flag = 1;
+      }
+      failed = true;
+    }
+    // LAPACK dpotf2 arithmetic: AJJ = sqrt(AJJ), column scaled by ONE / AJJ (keeps exactly
+    // singular inputs, e.g. coincident locations, failing at the same pivot)
+    const double piv = aug ? 1.0 : sqrt(d);
+    const double rinv = aug ? 1.0 : 1.0 / piv;
+    const double vc = (r == C) ? piv : ((r > C) ? v[C] * rinv : v[C]);
+    v[C] = vc;
+#pragma unroll
+    for (int s = C + 1; s < 16; ++s) {
+      const double lsc = __shfl_sync(0xffffffffu, vc, s);
+      v[s] = (r >= s) ? fma(-vc, lsc, v[s]) : v[s];
+    }
+    chol16_step<C + 1>(v, r, lane, g0, n_aug, failed, s_fail, fail_idx, fail_flag);
+  }
+}
 }  // namespace
+
+#ifdef MLE_DIAG_TIMING
+__device__ long long g_diag_clock[32];
+#define DIAG_T(slot) \
+  if (threadIdx.x == 0) g_diag_clock[slot] = clock64();
+#else
+#define DIAG_T(slot)
+#endif
 
 __global__ void __launch_bounds__(DTHREADS, 1)
     potrf_diag_kernel(double* a, long long ld, int k0, long long n_aug, double* linv,
                       int* fail_flag, long long* fail_idx) {
   if (*fail_flag) return;
   extern __shared__ __align__(16) double dsm[];
-  double* Ls = dsm;                     // DT * DS
-  double* dinv = Ls + DT * DS;          // DT
-  double* T = dinv + DT;                // 7 * 256 scratch
+  double* Ls = dsm;             // DT * DS
+  double* dinv = Ls + DT * DS;  // DT
+  double* scr = dinv + DT;      // DSCR
   __shared__ int s_fail;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
   double* A = a + (long long)k0 + (long long)k0 * ld;
   for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
     const int i = idx & (DT - 1), j = idx >> 7;
@@ -254,124 +347,145 @@ __global__ void __launch_bounds__(DTHREADS, 1)
   }
   if (tid == 0) s_fail = 0;
   __syncthreads();
-
+  DIAG_T(0)
 #define LS(i, j) Ls[(j) * DS + (i)]
+#pragma unroll 1
   for (int J = 0; J < DT / DB; ++J) {
     const int j0 = J * DB;
-    // (a) factor the 16x16 diagonal block with one warp
+    // (a) pivot chain of the 16x16 diagonal block in warp 0's registers
     if (warp == 0) {
-      for (int c = 0; c < DB; ++c) {
-        const int jc = j0 + c;
-        const long long gidx = (long long)k0 + jc;
-        const double d = LS(jc, jc);
-        double piv;
-        if (gidx == n_aug) {
-          piv = 1.0;
-        } else {
-          if (!(d > 0.0)) {
-            if (lane == 0) {
-              s_fail = 1;
-              *fail_idx = gidx;
-              *fail_flag = 1;
-            }
-            break;
-          }
-          piv = sqrt(d);
-        }
-        __syncwarp();
-        if (lane == 0) LS(jc, jc) = piv;
-        if (lane > c && lane < DB) LS(j0 + lane, jc) /= piv;
-        __syncwarp();
-        for (int e = lane; e < DB * DB; e += 32) {
-          const int r = e & (DB - 1), s = e >> 4;
-          if (s > c && r >= s) LS(j0 + r, j0 + s) -= LS(j0 + r, jc) * LS(j0 + s, jc);
-        }
-        __syncwarp();
+      const int r = lane & (DB - 1);
+      double v[DB];
+#pragma unroll
+      for (int s = 0; s < DB; ++s) v[s] = (s <= r) ? LS(j0 + r, j0 + s) : 0.0;
+      bool failed = false;
+      chol16_step<0>(v, r, lane, (long long)k0 + j0, n_aug, failed, &s_fail, fail_idx,
+                     fail_flag);
+      if (lane < DB) {
+#pragma unroll
+        for (int s = 0; s < DB; ++s)
+          if (s <= r) LS(j0 + r, j0 + s) = v[s];
       }
     }
     __syncthreads();
+    DIAG_T(1 + 3 * J)
     if (s_fail) return;
     const int rem = DT - j0 - DB;  // rows below the block
-    // (b) panel rows solve x L_JJ^T = a_row
+    const int base = j0 + DB;
+    // (b) panel rows: x L_JJ^T = a_row, right-looking with reciprocal pivots (dtrsm order)
     if (tid < rem) {
-      const int i = j0 + DB + tid;
+      const int i = base + tid;
       double x[DB];
 #pragma unroll
-      for (int c = 0; c < DB; ++c) {
-        double v = LS(i, j0 + c);
+      for (int c = 0; c < DB; ++c) x[c] = LS(i, j0 + c);
 #pragma unroll
-        for (int m = 0; m < c; ++m) v -= x[m] * LS(j0 + c, j0 + m);
-        x[c] = v / LS(j0 + c, j0 + c);
+      for (int c = 0; c < DB; ++c) {
+        x[c] *= 1.0 / LS(j0 + c, j0 + c);
+#pragma unroll
+        for (int m = c + 1; m < DB; ++m) x[m] -= x[c] * LS(j0 + m, j0 + c);
       }
 #pragma unroll
       for (int c = 0; c < DB; ++c) LS(i, j0 + c) = x[c];
     }
     __syncthreads();
-    // (c) trailing lower update
-    if (rem > 0) {
-      const int base = j0 + DB;
-      for (int e = tid; e < rem * rem; e += DTHREADS) {
-        const int il = e % rem, jl = e / rem;
-        if (il < jl) continue;
-        const int i = base + il, j = base + jl;
-        double v = LS(i, j);
+    DIAG_T(2 + 3 * J)
+    // (c) trailing lower update A22 -= L21 L21^T on 16x16 blocks with DMMA (K = 16)
+    const int nblk = rem / DB;
+    for (int task = warp; task < nblk * (nblk + 1) / 2; task += DWARPS) {
+      int bi, bj;
+      tri_index(task, &bi, &bj);
+      const int r0 = base + bi * DB, c0 = base + bj * DB;
+      double acc[2][4];
 #pragma unroll
-        for (int m = 0; m < DB; ++m) v -= LS(i, j0 + m) * LS(j, j0 + m);
-        LS(i, j) = v;
+      for (int nt = 0; nt < 2; ++nt) {
+        acc[nt][0] = LS(r0 + g, c0 + nt * 8 + 2 * t);
+        acc[nt][1] = LS(r0 + g, c0 + nt * 8 + 2 * t + 1);
+        acc[nt][2] = LS(r0 + g + 8, c0 + nt * 8 + 2 * t);
+        acc[nt][3] = LS(r0 + g + 8, c0 + nt * 8 + 2 * t + 1);
+      }
+      mma16x16(
+          acc, [&](int rr, int k) { return LS(r0 + rr, j0 + k); },
+          [&](int cc, int k) { return LS(c0 + cc, j0 + k); }, DB, 0x80000000u);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        LS(r0 + g, c0 + nt * 8 + 2 * t) = acc[nt][0];
+        LS(r0 + g, c0 + nt * 8 + 2 * t + 1) = acc[nt][1];
+        LS(r0 + g + 8, c0 + nt * 8 + 2 * t) = acc[nt][2];
+        LS(r0 + g + 8, c0 + nt * 8 + 2 * t + 1) = acc[nt][3];
       }
     }
     __syncthreads();
+    DIAG_T(3 + 3 * J)
   }
 
-  // ---- inverse X = L^-1, blocked by 16 ----
-  // diagonal 16x16 blocks: thread per (block, column)
+  // ---- inverse X = L^-1 ----
+  if (tid < DT) dinv[tid] = 1.0 / LS(tid, tid);
+  __syncthreads();
+  // (i) diagonal 16x16 blocks: thread per (block, column), forward substitution in registers
   if (tid < DT) {
     const int blk = tid >> 4, c = tid & (DB - 1);
     const int o = blk * DB;
     double x[DB];
 #pragma unroll
     for (int r = 0; r < DB; ++r) {
-      if (r < c) {
-        x[r] = 0.0;
-      } else if (r == c) {
-        x[r] = 1.0 / LS(o + r, o + r);
-      } else {
-        double v = 0.0;
+      double v = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-        for (int m = 0; m < r; ++m)
-          if (m >= c) v += LS(o + r, o + m) * x[m];
-        x[r] = -v / LS(o + r, o + r);
-      }
+      for (int m = 0; m < r; ++m) v -= LS(o + r, o + m) * x[m];
+      x[r] = (r >= c) ? v * dinv[o + r] : 0.0;
     }
-    dinv[o + c] = x[c];
 #pragma unroll
     for (int r = 0; r < DB; ++r)
       if (r > c) Ls[(o + r) * DS + (o + c)] = x[r];
   }
   __syncthreads();
-#define XS(i, j) ((i) == (j) ? dinv[i] : ((i) > (j) ? Ls[(i) * DS + (j)] : 0.0))
-  for (int I = 1; I < DT / DB; ++I) {
-    // T_IJ = sum_{M=J}^{I-1} L[I, M] X[M, J]
-    for (int e = tid; e < I * DB * DB; e += DTHREADS) {
-      const int J = e >> 8, rs = e & 255;
-      const int r = rs & (DB - 1), s = rs >> 4;
-      const int i = I * DB + r, j = J * DB + s;
-      double v = 0.0;
-      for (int m = J * DB; m < I * DB; ++m) v += LS(i, m) * XS(m, j);
-      T[e] = v;
+  DIAG_T(25)
+  // (ii) recursive doubling: [[X11, 0], [X21, X22]] with X21 = -X22 (L21 X11)
+#define XS(i, j) ((i) > (j) ? Ls[(i) * DS + (j)] : ((i) == (j) ? dinv[i] : 0.0))
+#pragma unroll 1
+  for (int s = DB; s < DT; s *= 2) {
+    const int pairs = DT / (2 * s), bps = s / DB, per_pair = bps * bps;
+    // T_p = L21 X11   (s x s, column-major in scr at p * s * s)
+    for (int task = warp; task < pairs * per_pair; task += DWARPS) {
+      const int p = task / per_pair, q = task % per_pair;
+      const int bi = q % bps, bj = q / bps;
+      const int o = 2 * s * p;
+      double acc[2][4] = {};
+      mma16x16(
+          acc, [&](int rr, int k) { return LS(o + s + bi * DB + rr, o + k); },
+          [&](int cc, int k) { return XS(o + k, o + bj * DB + cc); }, s, 0u);
+      double* T = scr + p * s * s;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int cc = bj * DB + nt * 8 + 2 * t, rr = bi * DB + g;
+        T[cc * s + rr] = acc[nt][0];
+        T[(cc + 1) * s + rr] = acc[nt][1];
+        T[cc * s + rr + 8] = acc[nt][2];
+        T[(cc + 1) * s + rr + 8] = acc[nt][3];
+      }
     }
     __syncthreads();
-    // X[I, J] = - X_II T_IJ
-    for (int e = tid; e < I * DB * DB; e += DTHREADS) {
-      const int J = e >> 8, rs = e & 255;
-      const int r = rs & (DB - 1), s = rs >> 4;
-      const int i = I * DB + r;
-      double v = 0.0;
-      for (int q = 0; q <= r; ++q) v += XS(i, I * DB + q) * T[(J << 8) + (s << 4) + q];
-      Ls[i * DS + J * DB + s] = -v;
+    // X21 = -X22 T_p
+    for (int task = warp; task < pairs * per_pair; task += DWARPS) {
+      const int p = task / per_pair, q = task % per_pair;
+      const int bi = q % bps, bj = q / bps;
+      const int o = 2 * s * p;
+      const double* T = scr + p * s * s;
+      double acc[2][4] = {};
+      mma16x16(
+          acc, [&](int rr, int k) { return XS(o + s + bi * DB + rr, o + s + k); },
+          [&](int cc, int k) { return T[(bj * DB + cc) * s + k]; }, s, 0x80000000u);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int i0 = o + s + bi * DB + g, j1 = o + bj * DB + nt * 8 + 2 * t;
+        Ls[i0 * DS + j1] = acc[nt][0];
+        Ls[i0 * DS + j1 + 1] = acc[nt][1];
+        Ls[(i0 + 8) * DS + j1] = acc[nt][2];
+        Ls[(i0 + 8) * DS + j1 + 1] = acc[nt][3];
+      }
     }
     __syncthreads();
   }
+  DIAG_T(26)
   // write back L (lower incl. diagonal) and Linv (dense 128x128, zero upper)
   for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
     const int i = idx & (DT - 1), j = idx >> 7;
@@ -384,13 +498,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 
 cudaError_t init_diag_attributes() {
   return cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(sizeof(double) * (DT * DS + DT + 7 * 256)));
+                              (int)kDiagSmem);
 }
 
 cudaError_t launch_potrf_diag(double* a, long long ld, int k0, long long n_aug, double* linv,
                               int* fail_flag, long long* fail_idx, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (DT * DS + DT + 7 * 256);
-  potrf_diag_kernel<<<1, DTHREADS, smem, s>>>(a, ld, k0, n_aug, linv, fail_flag, fail_idx);
+  potrf_diag_kernel<<<1, DTHREADS, kDiagSmem, s>>>(a, ld, k0, n_aug, linv, fail_flag,
+                                                   fail_idx);
   return cudaGetLastError();
 }
 
@@ -429,6 +543,7 @@ __global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __r
       s[0] += log(L[j + cj]);
       const double y = L[n + cj];
       s[1] += y * y;
+      if (Ba == nullptr) continue;  // loglik: same summation order as eval_all
       const double a = Ba[j + cj], b = Bn[j + cj];
       s[2] += a;
       s[3] += b;
@@ -436,6 +551,7 @@ __global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __r
       s[5] += a * b;
       s[6] += b * b;
     }
+    if (Ba == nullptr) continue;
     for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
       const double a = Ba[i + cj], b = Bn[i + cj];
       s[4] += 2.0 * a * a;
@@ -446,28 +562,6 @@ __global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __r
   for (int q = 0; q < RN; ++q) {
     const double t = block_sum(s[q], sh);
     if (threadIdx.x == 0) partials[blockIdx.x * RN + q] = t;
-  }
-}
-
-__global__ void __launch_bounds__(RTHREADS) reduce_loglik_kernel(const double* __restrict__ L,
-                                                                 long long ld, int n,
-                                                                 double* partials,
-                                                                 const int* fail_flag) {
-  if (*fail_flag) return;
-  __shared__ double sh[RTHREADS / 32];
-  double s0 = 0.0, s1 = 0.0;
-  for (int j = blockIdx.x * RTHREADS + threadIdx.x; j < n; j += gridDim.x * RTHREADS) {
-    const long long cj = (long long)j * ld;
-    s0 += log(L[j + cj]);
-    const double y = L[n + cj];
-    s1 += y * y;
-  }
-  const double t0 = block_sum(s0, sh);
-  const double t1 = block_sum(s1, sh);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x * RN + 0] = t0;
-    partials[blockIdx.x * RN + 1] = t1;
-    for (int q = 2; q < RN; ++q) partials[blockIdx.x * RN + q] = 0.0;
   }
 }
 
@@ -496,9 +590,9 @@ cudaError_t launch_reduce_eval(const double* L, const double* Ba, const double* 
 
 cudaError_t launch_reduce_loglik(const double* L, long long ld, int n, double* partials,
                                  double* out, const int* fail_flag, cudaStream_t s) {
-  const int blocks = 32;
-  reduce_loglik_kernel<<<blocks, RTHREADS, 0, s>>>(L, ld, n, partials, fail_flag);
-  reduce_final_kernel<<<1, 32, 0, s>>>(partials, blocks, nullptr, nullptr, ld, n, out,
+  reduce_eval_kernel<<<RBLOCKS, RTHREADS, 0, s>>>(L, nullptr, nullptr, ld, n, partials,
+                                                  fail_flag);
+  reduce_final_kernel<<<1, 32, 0, s>>>(partials, RBLOCKS, nullptr, nullptr, ld, n, out,
                                         fail_flag);
   return cudaGetLastError();
 }
