@@ -4,14 +4,15 @@
 
 Own arm ("ours"): one process per GPU (torchrun for N > 1).  Each rank runs its own five
 replicate Fisher-BT fits of config 2 (weak scaling: rank r fits seeds 5r..5r+4; rank 0 uses
-the golden seeds 0-4) concurrently from five host threads, one CUDA stream and one
-device-resident dataset per replica.  A step = all five fits from theta0 to convergence.
+the golden seeds 0-4; no data-path collective).  The five host loops run concurrently and
+their evaluations are executed in lock step as batched GPU passes (paper_2601_11437_b200.
+fit_many -> mle_eval_batch).  A step = all five fits from theta0 to convergence.
   value  = sum of grad_calls (Fisher iterations) over all ranks / max-over-ranks step time,
-           inputs resident in HBM (contexts created and warmed before timing);
+           inputs resident in HBM (datasets created and warmed before timing);
   e2e    = same metric through the public API from host numpy buffers: every step creates
-           the datasets (H2D of locations and z), runs the fits and reads the results back.
+           the datasets (H2D of locations and z), runs the fits and reads results back.
 Reference arm (--impl reference): the reference's own CPU algorithm (oracle port of
-maternmle, numpy/scipy/OpenBLAS on all host cores) on the same config, rank 0 only.
+maternmle: numpy / scipy / OpenBLAS on all host cores) on the same config, rank 0 only.
 """
 
 from __future__ import annotations
@@ -22,7 +23,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -35,15 +35,15 @@ GOLDEN = REPO / "tests" / "golden"
 CONFIG = "config2"
 THETA0 = (0.8, 0.1, 1.0)
 N_REPLICAS = 5
-FP64_PEAK_TFLOPS = 36.08   # cuBLAS DGEMM 16384^3 on this pool's B200 (profiles/r01_fp64_peaks.txt)
+FP64_PEAK_TFLOPS = 36.08  # cuBLAS DGEMM 16384^3, this pool's B200 (profiles/r01_fp64_peaks.txt)
 METRIC = "Fisher-BT iterations/s at n"
 
 
 def workload_desc():
-    return {"workload": "config2: n=3600 jittered 60x60 grid on [0,1]^2, true theta=(1.0,0.2,1.5), "
-                        "5 replicate FP64 fields per GPU, Fisher-BT from theta0=(0.8,0.1,1.0) "
-                        "to ||grad||<=1e-3 (reference stopping rule)",
-            "n": 3600, "replicas_per_gpu": N_REPLICAS, "nb": 128,
+    return {"workload": "config2: n=3600 jittered 60x60 grid on [0,1]^2, true theta=(1.0,0.2,"
+                        "1.5), 5 replicate FP64 fields per GPU, Fisher-BT from theta0=(0.8,0.1,"
+                        "1.0) to ||grad||<=1e-3 (reference stopping rule)",
+            "n": 3600, "replicas_per_gpu": N_REPLICAS, "nb": 128, "outer_block": 512,
             "l2": "inputs larger than L2: 3 x 110 MB matrices per replica, 5 replicas"}
 
 
@@ -65,67 +65,13 @@ def load_replica(seed, device):
     return loc, m.simulate_field(loc, wl.theta_true, seed, device=device)
 
 
-class TimedObjective:
-    """GPU objective that also accumulates device phase times / launches per evaluation."""
-
-    def __init__(self, data):
-        import paper_2601_11437_b200 as m
-
-        self.inner = m.LikelihoodObjective(data)
-        self.eng = data.engine()
-        self.acc = {"flops": 0.0, "factor_ms": 0.0, "gen_ms": 0.0, "gen_bytes": 0.0,
-                    "launches": 0, "evals": 0}
-
-    @property
-    def loglik_calls(self):
-        return self.inner.loglik_calls
-
-    @property
-    def grad_calls(self):
-        return self.inner.grad_calls
-
-    def _note(self):
-        p = self.eng.phase_times()
-        self.acc["flops"] += p["flops"]
-        self.acc["factor_ms"] += p["potrf_ms"] + p["solve_ms"]
-        self.acc["gen_ms"] += p["gen_ms"]
-        self.acc["gen_bytes"] += p["gen_bytes"]
-        self.acc["launches"] += p["launches"]
-        self.acc["evals"] += 1
-
-    def loglik(self, theta):
-        v = self.inner.loglik(theta)
-        self._note()
-        return v
-
-    def eval_all(self, theta):
-        v = self.inner.eval_all(theta)
-        self._note()
-        return v
-
-
-def run_fits(datasets, objectives_out=None):
-    """Fit every dataset from THETA0 concurrently (one host thread per replica)."""
+def run_fits(datasets, coords=None):
+    """All replicas from THETA0, lock-step batched (one launch sequence covers them all)."""
     import paper_2601_11437_b200 as m
 
     th0 = m.MaternParams(*THETA0)
     cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
-    results = [None] * len(datasets)
-    objs = [TimedObjective(d) for d in datasets]
-
-    def work(i):
-        results[i] = m.fisher_bt(datasets[i], cfg, objective=objs[i])
-
-    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(datasets))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if any(r is None for r in results):
-        raise RuntimeError("a replicate fit failed")
-    if objectives_out is not None:
-        objectives_out.extend(objs)
-    return results
+    return m.fit_many(datasets, cfg, coordinator_out=coords)
 
 
 class ClockSampler:
@@ -143,7 +89,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -171,35 +117,45 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def isolated_phase_rates(data, theta, reps=5):
-    """Kernel-level rates from single-stream evaluations (CUDA events on the ctx stream)."""
-    eng = data.engine()
-    eng.eval_all(theta)
-    fl = fac = gen = gb = 0.0
-    for _ in range(reps):
-        eng.eval_all(theta)
-        p = eng.phase_times()
-        fl += p["flops"]
-        fac += p["potrf_ms"] + p["solve_ms"]
-        gen += p["gen_ms"]
-        gb += p["gen_bytes"]
-        last = p
-    ll_ms = []
-    for _ in range(reps):
-        eng.loglik(theta)
-        ll_ms.append(eng.phase_times())
-    return {"eval_factor_solve_tflops": fl / (fac * 1e-3) / 1e12,
-            "gen_gbs": gb / (gen * 1e-3) / 1e9, "eval_phases_ms": last,
-            "loglik_potrf_ms": statistics.median(p["potrf_ms"] for p in ll_ms),
-            "loglik_potrf_tflops": ll_ms[-1]["flops"] / (statistics.median(
-                p["potrf_ms"] for p in ll_ms) * 1e-3) / 1e12}
+def isolated_phase_rates(datasets, theta, reps=4):
+    """Batched eval_all / loglik over all replicas on one stream, CUDA events on it.
+    Two thetas alternate so every evaluation refactors (no factor-cache hits)."""
+    import paper_2601_11437_b200 as m
+
+    engines = [d.engine() for d in datasets]
+    th_a = np.asarray(theta, float)
+    th_b = th_a * np.array([1.0, 1.0 + 1e-7, 1.0])
+    th_c = th_a * np.array([1.0, 1.0 - 1e-7, 1.0])
+    out = {"eval": [], "loglik": []}
+    for r in range(reps + 1):
+        for mode, key in ((2, "eval"), (1, "loglik")):
+            th = (th_a if (r % 2 == 0) else th_b) if mode == 2 else th_c * (1.0 + 1e-9 * r)
+            m.eval_batch(engines, [th] * len(engines), [mode] * len(engines))
+            p = engines[0].phase_times()
+            if r > 0:
+                out[key].append(p)
+    ev, ll = out["eval"], out["loglik"]
+    fac_ms = sum(p["potrf_ms"] + p["solve_ms"] for p in ev)
+    fac_fl = sum(p["flops"] for p in ev)
+    return {
+        "batch": len(engines),
+        "eval_factor_solve_tflops": fac_fl / (fac_ms * 1e-3) / 1e12,
+        "eval_ms": statistics.median(p["total_ms"] for p in ev),
+        "eval_phases_ms": {k: statistics.median(p[k] for p in ev)
+                           for k in ("gen_ms", "potrf_ms", "solve_ms", "reduce_ms")},
+        "gen_gbs": sum(p["gen_bytes"] for p in ev) / (sum(p["gen_ms"] for p in ev) * 1e-3) / 1e9,
+        "loglik_ms": statistics.median(p["total_ms"] for p in ll),
+        "loglik_potrf_tflops": sum(p["flops"] for p in ll) / (
+            sum(p["potrf_ms"] for p in ll) * 1e-3) / 1e12,
+        "launches_per_batched_eval": ev[-1]["launches"],
+    }
 
 
 # ----------------------------------------------------------------------------- CPU side
 def cpu_iteration_sample(reps=1):
-    """Oracle (reference algorithm, numpy/scipy/OpenBLAS) timing of one mean Fisher
-    iteration of config 2: one eval_all plus rho loglik calls, rho = the reference fits'
-    (loglik_calls - grad_calls) / grad_calls over seeds 0-4 (golden)."""
+    """Oracle (reference algorithm: numpy/scipy/OpenBLAS) time of one mean Fisher iteration of
+    config 2 = one eval_all + rho loglik calls, rho = (loglik_calls - grad_calls) / grad_calls
+    of the reference's own config-2 fits (golden, seeds 0-4)."""
     from oracle import maternmle_cpu as O
 
     fits = [json.loads((GOLDEN / f"{CONFIG}_seed{s}_fit.json").read_text()) for s in range(5)]
@@ -235,14 +191,15 @@ def cpu_cores():
 def reference_arm(args, rank, world):
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        from oracle import maternmle_cpu as O  # noqa: F401  (import / BLAS warm-up only)
+    from oracle import maternmle_cpu as O  # noqa: F401  (imports / BLAS warm-up)
+
     samples = [cpu_iteration_sample(1) for _ in range(args.steps)]
     val = statistics.median(s["value"] for s in samples)
     cores = cpu_cores()
-    sample = ("one config-2 eval_all + rho=%.3f loglik at n=3600 per step (the reference "
-              "fits' mean evaluation mix per Fisher iteration); generation is single-threaded "
-              "numpy/scipy as in the reference, LAPACK on %d threads" % (samples[0]["rho"], cores))
+    sample = ("per step: one config-2 eval_all + rho=%.3f loglik at n=3600 (the reference "
+              "fits' mean evaluation mix per Fisher iteration); generation single-threaded "
+              "numpy/scipy as in the reference, LAPACK on %d threads; warm-up = imports only"
+              % (samples[0]["rho"], cores))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "weak",
@@ -259,6 +216,7 @@ def reference_arm(args, rank, world):
 # ----------------------------------------------------------------------------- GPU side
 def ours_arm(args, rank, world, local_rank):
     import torch
+
     import paper_2601_11437_b200 as m
 
     torch.cuda.set_device(local_rank)
@@ -291,11 +249,9 @@ def ours_arm(args, rank, world, local_rank):
 
     clocks = ClockSampler(local_rank)
     clocks.start()
-    objs, step_ms, grad_calls, loglik_calls = [], [], 0, 0
+    coords, step_ms, grad_calls, loglik_calls = [], [], 0, 0
     for _ in range(args.steps):
-        step_objs = []
-        res, ms = timed(lambda: run_fits(datasets, step_objs))
-        objs.extend(step_objs)
+        res, ms = timed(lambda: run_fits(datasets, coords))
         step_ms.append(ms)
         grad_calls += sum(r.grad_calls for r in res)
         loglik_calls += sum(r.loglik_calls for r in res)
@@ -317,8 +273,7 @@ def ours_arm(args, rank, world, local_rank):
         e2e_grad += sum(r.grad_calls for r in res_e2e)
         e2e_evals += sum(r.loglik_calls for r in res_e2e)
 
-    tot_ms = sum(step_ms)
-    tot_e2e = sum(e2e_ms)
+    tot_ms, tot_e2e = sum(step_ms), sum(e2e_ms)
     if dist is not None:
         t = torch.tensor([tot_ms, tot_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -328,16 +283,18 @@ def ours_arm(args, rank, world, local_rank):
         grad_all, e2e_grad_all, ll_all = (float(v) for v in c)
     else:
         grad_all, e2e_grad_all, ll_all = float(grad_calls), float(e2e_grad), float(loglik_calls)
-
     if rank != 0:
         return
+
     value = grad_all / (tot_ms * 1e-3)
     e2e_value = e2e_grad_all / (tot_e2e * 1e-3)
-    acc = {k: sum(o.acc[k] for o in objs) for k in objs[0].acc}
-    iso = isolated_phase_rates(datasets[0], m.WORKLOADS[CONFIG].theta_true)
+    acc = {k: sum(c.acc[k] for c in coords) for k in coords[0].acc}
+    batches = sum(c.batches for c in coords)
+    iso = isolated_phase_rates(datasets, m.WORKLOADS[CONFIG].theta_true)
     achieved = iso["eval_factor_solve_tflops"]
-    # 9 result doubles + failure flag + pivot per evaluation come back to the host
+    # per request: 9 result doubles + failure flag (4 B) + pivot (8 B) come back to the host
     d2h = int(e2e_evals / max(1, len(e2e_ms)) * (9 * 8 + 4 + 8))
+    in_fit_tflops = acc["flops"] / ((acc["potrf_ms"] + acc["solve_ms"]) * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -346,13 +303,14 @@ def ours_arm(args, rank, world, local_rank):
         "roofline": {
             "bound": "tensor", "unit": "TFLOP/s", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-            "kernel": "Cholesky + solve phase of one eval_all at n=3600 (DMMA dgemm_kernel "
-                      "launches + potrf_diag_kernel), standard-count flops n^3/3 + 2(n^3 + n^3/3)"
-                      ", CUDA events on the context stream, single stream",
+            "kernel": "factor+solve phase of a batched eval_all over the 5 replicas at n=3600 "
+                      "(dgemm_kernel DMMA launches + potrf_diag_kernel), standard-count flops "
+                      "n^3/3 + 2(n^3 + n^3/3) per replica / CUDA-event time on the launching "
+                      "stream",
             "peak_source": "measured cuBLAS DGEMM 16384^3 FP64 on this pool's B200 "
                            "(MEASURED_PEAKS.json has no FP64 entry)"},
         "fp64_tflops_chol_solve": achieved,
-        "fp64_tflops_chol_solve_in_fits": acc["flops"] / (acc["factor_ms"] * 1e-3) / 1e12,
+        "fp64_tflops_chol_solve_in_fits": in_fit_tflops,
         "gen_hbm_gbs": iso["gen_gbs"],
         "gpu_launches": int(acc["launches"]),
         "clocks": clk,
@@ -360,6 +318,10 @@ def ours_arm(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h},
         "fits": {"grad_calls_per_step": grad_all / args.steps,
                  "loglik_calls_per_step": ll_all / args.steps,
+                 "batched_passes_per_step": batches / args.steps,
+                 "device_ms_per_step": {k: acc[k] / args.steps
+                                        for k in ("gen_ms", "potrf_ms", "solve_ms",
+                                                  "reduce_ms")},
                  "theta_hat_rank0": [r.theta_hat.as_array().tolist() for r in last_fits]},
         "isolated": iso,
     }
@@ -367,9 +329,9 @@ def ours_arm(args, rank, world, local_rank):
         cpu = cpu_iteration_sample(1)
         line["cpu_baseline"] = {
             "value": cpu["value"], "unit": "it/s", "cores": cpu_cores(), "kind": "port",
-            "sample": "one config-2 eval_all + rho=%.3f loglik (reference algorithm, numpy/scipy/"
-                      "OpenBLAS) = one mean Fisher iteration; eval_all %.2fs, loglik %.2fs"
-                      % (cpu["rho"], cpu["t_eval_all_s"], cpu["t_loglik_s"])}
+            "sample": "one config-2 eval_all + rho=%.3f loglik (reference algorithm, numpy/"
+                      "scipy/OpenBLAS) = one mean Fisher iteration; eval_all %.2fs, loglik "
+                      "%.2fs" % (cpu["rho"], cpu["t_eval_all_s"], cpu["t_loglik_s"])}
     print(json.dumps(line), flush=True)
 
 

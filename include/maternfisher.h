@@ -88,6 +88,20 @@ int mle_loglik(mle_ctx* ctx, const double theta[3], double* loglik, int64_t* bad
 int mle_eval_all(mle_ctx* ctx, const double theta[3], double* loglik, double grad[3],
                  double fisher[9], int64_t* bad_pivot);
 
+/*
+ * Batched evaluation: `count` requests, one per distinct context, run as ONE pass (every
+ * kernel launch covers all requests of the same device and padded size).  modes[i]:
+ * 0 skip, 1 loglik, 2 eval_all.  thetas: count x 3.  results: count x 13 doubles
+ * [loglik, grad[3], fisher[9] row-major] (grad/fisher only for mode 2).  rcs[i] / pivots[i]
+ * carry each request's own MLE_OK / MLE_NOT_PD / MLE_INVALID and failing pivot.  Returns
+ * MLE_OK when the batch ran (individual requests may still have failed), otherwise the
+ * error that stopped it.  Replaces running the reference's LikelihoodObjective once per
+ * replicate / L9 start sequentially (optimizer.py:188-197; "the nine L9
+ * evaluations may run concurrently").
+ */
+int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const int* modes,
+                   double* results, int64_t* pivots, int* rcs);
+
 /* Write one full n x n matrix (row-major == column-major, symmetric) to host memory. */
 int mle_build(mle_ctx* ctx, const double theta[3], int which, double* out_host);
 

@@ -7,6 +7,7 @@ hand-written CUDA kernels behind the C ABI in ``include/maternfisher.h``.
 Importing the package loads ``libmaternfisher.so``; there is no CPU fallback.
 """
 
+from .batch import BatchCoordinator, BatchedObjective, eval_batch, fit_many
 from .bessel import BesselRegime, bessel_k, dnu_xnu_knu, select_regime
 from .datasets import WORKLOADS, Workload, gmm_locations, jittered_grid, simulate_field
 from .engine import Engine
@@ -48,6 +49,7 @@ from ._native import device_count, LIB_PATH
 __version__ = "0.1.0"
 
 __all__ = [
+    "BatchCoordinator", "BatchedObjective", "eval_batch", "fit_many",
     "BesselRegime", "bessel_k", "dnu_xnu_knu", "select_regime",
     "WORKLOADS", "Workload", "gmm_locations", "jittered_grid", "simulate_field",
     "Engine",

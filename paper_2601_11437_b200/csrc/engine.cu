@@ -1,18 +1,26 @@
-// engine.cu — C ABI (include/maternfisher.h) and the per-evaluation schedule.
+// engine.cu — C ABI (include/maternfisher.h) and the batched per-evaluation schedule.
 //
-// One mle_ctx = one dataset resident on one GPU with its own CUDA stream.  Per evaluation:
+// One mle_ctx = one dataset resident on one GPU with its own CUDA stream.  An evaluation
+// request is (ctx, theta, mode); requests on several contexts of the same padded size run
+// as ONE batched pass (mle_eval_batch), every kernel launch covering all of them:
 //
 //   gen      Sigma (lower tiles, augmented row n = z, identity padding) and, for eval_all,
 //            dSigma/dalpha, dSigma/dnu (full storage)                    [gen.cu]
-//   potrf    right-looking blocked Cholesky, nb = 128: diag tile factor + inverse,
-//            panel = A_T,K Linv_k^T, trailing lower SYRK                 [linalg.cu]
+//   potrf    two-level right-looking blocked Cholesky, nb = 128 inner steps (diagonal tile
+//            factor + inverse, panel x Linv^T, updates inside the outer block), K = 512
+//            outer trailing SYRK                                          [linalg.cu]
 //            -> row n of L is y^T = (L^-1 z)^T (the reference's `white`, likelihood.py:121)
-//   solve    X_i = L^-1 S_i (row panel Linv_k S_k, full trailing GEMM), then the lower half
-//            of B_i = X_i L^-T by a right-looking column sweep; B_i = L^-1 S_i L^-T.
+//   solve    X_i = L^-1 S_i (row panels Linv_k S_k, GEMM updates), then the lower half of
+//            B_i = X_i L^-T by a right-looking column sweep; B_i = L^-1 S_i L^-T.
 //   reduce   log det, y^T y, tr B_i, <B_i,B_j>_F, and y^T B_i y = B_i[n,n] (augmented)
 //
 // The score and Fisher information then follow likelihood.py:123-147 with
 // tr(Sigma^-1 S_i) = tr B_i, w^T S_i w = y^T B_i y and tr(W_i W_j) = <B_i, B_j>_F.
+//
+// Factor cache: after a successful factorization the context remembers theta; an eval_all
+// (or loglik) at the same theta reuses the resident L and skips generation of Sigma and the
+// Cholesky (Fisher-BT always follows an accepted loglik(theta) with eval_all(theta),
+// optimizer.py:362,375).  Results are bit-identical to recomputing.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,6 +41,8 @@ thread_local std::string g_last_error;
 std::mutex g_init_mutex;
 std::vector<int> g_device_ready;
 const double kLog2Pi = 1.8378770664093453;  // log(2 pi), likelihood.py:38
+constexpr int kOuter = 4;                   // outer block = 4 x 128 columns
+constexpr int kResults = 13;                // loglik, grad[3], fisher[9]
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -88,16 +98,32 @@ struct mle_ctx {
   int* fail_flag = nullptr;
   long long* fail_idx = nullptr;
   double* partials = nullptr;
-  double* out = nullptr;     // device: 9 reduction results
-  double* h_res = nullptr;   // pinned: 9 results + fail flag + fail idx
+  double* out = nullptr;          // device: 9 reduction results
+  ThetaParams* d_theta = nullptr; // device copy of the per-theta scalars
+  ThetaParams* h_theta = nullptr; // pinned staging
+  double* h_res = nullptr;        // pinned: 9 results + fail flag + fail idx
   cudaEvent_t ev[5] = {};
   double phase_ms[MLE_NUM_PHASES] = {};
   double flops = 0.0;
   double gen_bytes = 0.0;
-  double launches = 0.0;  // kernels launched by the last evaluation
+  double launches = 0.0;
+  bool factor_valid = false;      // L of Sigma(cached_theta) is resident in `sigma`
+  double cached_theta[3] = {0, 0, 0};
 };
 
 namespace {
+
+// One evaluation request inside a batch.
+struct Item {
+  mle_ctx* c = nullptr;
+  ThetaParams P;
+  int mode = 0;        // 1 loglik, 2 eval_all
+  bool factor = true;  // generate Sigma + Cholesky (false: cached factor reused)
+  bool derivs = false; // derivative matrices + solves
+  int rc = MLE_OK;
+  int64_t pivot = -1;
+  double res[kResults] = {};
+};
 
 int ensure_matrices(mle_ctx* c, bool derivs) {
   const size_t bytes = sizeof(double) * (size_t)c->N * (size_t)c->N;
@@ -110,224 +136,389 @@ int ensure_matrices(mle_ctx* c, bool derivs) {
   return MLE_OK;
 }
 
-GemmArgs gemm_base(const mle_ctx* c) {
+GemmArgs gemm_base() {
   GemmArgs g;
   std::memset(&g, 0, sizeof(g));
   g.K = kNB;
-  g.fail_flag = c->fail_flag;
   return g;
 }
 
-// Two-level blocking: inner steps of kNB = 128 (diagonal tile factor/inverse, panel
-// products, updates confined to the current outer block), then one trailing update per
-// outer block of kOuter tiles with K = kOuter * 128, which amortises the GEMM pipeline
-// fill / C traffic over 4x more k-steps than a single-level right-looking sweep.
-constexpr int kOuter = 4;
+// Launch sequences over a list of contexts (all with the same N / Nt) on one stream.
+struct Launcher {
+  cudaStream_t s;
+  double launches = 0.0;
 
-int gemm(mle_ctx* c, const GemmArgs& g, BLayout bl, int batch) {
-  ++c->launches;
-  CUDA_TRY(launch_gemm(g, bl, batch, c->stream));
-  return MLE_OK;
-}
-
-// Right-looking blocked Cholesky of the padded, augmented matrix `a` (ld = N).
-int run_potrf(mle_ctx* c, double* a, long long N, int Nt, long long n_aug) {
-  const long long ld = N;
-  int rc;
-  for (int b0 = 0; b0 < Nt; b0 += kOuter) {
-    const int b1 = std::min(Nt, b0 + kOuter);
-    for (int k = b0; k < b1; ++k) {
-      const long long k0 = (long long)k * kNB;
-      double* linv_k = c->linv + (size_t)k * kNB * kNB;
-      ++c->launches;
-      CUDA_TRY(launch_potrf_diag(a, ld, (int)k0, n_aug, linv_k, c->fail_flag, c->fail_idx,
-                                 c->stream));
-      const int rem = Nt - k - 1;
-      if (rem == 0) break;
-      double* panel = a + (k0 + kNB) + k0 * ld;
-      // panel <- panel * Linv_k^T   (in place: BN = 128 covers the whole panel width)
-      GemmArgs g = gemm_base(c);
-      g.A[0] = panel; g.lda = ld;
-      g.B[0] = linv_k; g.ldb = kNB;
-      g.C[0] = panel; g.ldc = ld;
-      g.tiles_m = rem; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
-      if ((rc = gemm(c, g, kBNK, 1))) return rc;
-      // inner update of the remaining columns of this outer block (lower trapezoid)
-      const int wcols = b1 - k - 1;
-      if (wcols > 0) {
-        GemmArgs t = gemm_base(c);
-        t.A[0] = panel; t.lda = ld;
-        t.B[0] = panel; t.ldb = ld;
-        t.C[0] = a + (k0 + kNB) + (k0 + kNB) * ld; t.ldc = ld;
-        t.tiles_m = rem; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
-        if ((rc = gemm(c, t, kBNK, 1))) return rc;
-      }
-    }
-    const int rem = Nt - b1;
-    if (rem <= 0) continue;
-    // outer trailing update: A_TT -= P P^T with P = L[T, b0:b1], K = (b1 - b0) * 128
-    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
-    GemmArgs t = gemm_base(c);
-    t.A[0] = a + t0 + c0 * ld; t.lda = ld;
-    t.B[0] = a + t0 + c0 * ld; t.ldb = ld;
-    t.C[0] = a + t0 + t0 * ld; t.ldc = ld;
-    t.K = (b1 - b0) * kNB;
-    t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
-    if ((rc = gemm(c, t, kBNK, 1))) return rc;
+  int gemm(const GemmArgs& g, BLayout bl, int batch) {
+    launches += 1;
+    CUDA_TRY(launch_gemm(g, bl, batch, s));
+    return MLE_OK;
   }
-  return MLE_OK;
-}
 
-// B_i = L^-1 S_i L^-T (lower half) for both derivative matrices, in place.
-int run_solves(mle_ctx* c) {
-  const long long N = c->N, ld = N;
-  const int Nt = c->Nt;
-  double* S[2] = {c->sa, c->sn};
-  const double* L = c->sigma;
-  int rc;
-  // forward sweep X = L^-1 S (all columns), row blocks top-down
-  for (int b0 = 0; b0 < Nt; b0 += kOuter) {
-    const int b1 = std::min(Nt, b0 + kOuter);
-    for (int k = b0; k < b1; ++k) {
-      const long long k0 = (long long)k * kNB;
-      const double* linv_k = c->linv + (size_t)k * kNB * kNB;
-      GemmArgs g = gemm_base(c);
-      for (int b = 0; b < 2; ++b) {
-        g.A[b] = linv_k;
-        g.B[b] = S[b] + k0;   // B(n, kk) = S[k0 + kk, n]  (kBKN)
-        g.C[b] = S[b] + k0;   // in place: BM = 128 covers the whole row panel
-      }
-      g.lda = kNB; g.ldb = ld; g.ldc = ld;
-      g.tiles_m = 1; g.tiles_n = Nt; g.alpha = 1.0; g.beta = 0.0;
-      if ((rc = gemm(c, g, kBKN, 2))) return rc;
-      const int wrows = b1 - k - 1;  // remaining row tiles of this outer block
-      if (wrows > 0) {
-        GemmArgs t = gemm_base(c);
-        for (int b = 0; b < 2; ++b) {
-          t.A[b] = L + (k0 + kNB) + k0 * ld;   // L[k+1 : b1, k]
-          t.B[b] = S[b] + k0;                  // X_k (kBKN)
-          t.C[b] = S[b] + (k0 + kNB);
+  // Two-level right-looking blocked Cholesky of every item's matrix (ld = N).
+  int potrf(mle_ctx* const* cs, double* const* mats, const long long* n_aug, int m) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    int rc;
+    for (int b0 = 0; b0 < Nt; b0 += kOuter) {
+      const int b1 = std::min(Nt, b0 + kOuter);
+      for (int k = b0; k < b1; ++k) {
+        const long long k0 = (long long)k * kNB;
+        DiagArgs d;
+        std::memset(&d, 0, sizeof(d));
+        d.ld = ld;
+        d.k0 = (int)k0;
+        for (int b = 0; b < m; ++b) {
+          d.a[b] = mats[b];
+          d.linv[b] = cs[b]->linv + (size_t)k * kNB * kNB;
+          d.fail_flag[b] = cs[b]->fail_flag;
+          d.fail_idx[b] = cs[b]->fail_idx;
+          d.n_aug[b] = n_aug[b];
         }
-        t.lda = ld; t.ldb = ld; t.ldc = ld;
-        t.tiles_m = wrows; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
-        if ((rc = gemm(c, t, kBKN, 2))) return rc;
-      }
-    }
-    const int rem = Nt - b1;
-    if (rem <= 0) continue;
-    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
-    GemmArgs t = gemm_base(c);
-    for (int b = 0; b < 2; ++b) {
-      t.A[b] = L + t0 + c0 * ld;   // L[T, b0:b1]
-      t.B[b] = S[b] + c0;          // X[b0:b1, :] (kBKN)
-      t.C[b] = S[b] + t0;
-    }
-    t.lda = ld; t.ldb = ld; t.ldc = ld;
-    t.K = (b1 - b0) * kNB;
-    t.tiles_m = rem; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
-    if ((rc = gemm(c, t, kBKN, 2))) return rc;
-  }
-  // right sweep on lower tiles: B[j:, j] = X[j:, j] Linv_j^T ; X[T,T] -= B[T,j] L[T,j]^T
-  for (int b0 = 0; b0 < Nt; b0 += kOuter) {
-    const int b1 = std::min(Nt, b0 + kOuter);
-    for (int j = b0; j < b1; ++j) {
-      const long long j0 = (long long)j * kNB;
-      const double* linv_j = c->linv + (size_t)j * kNB * kNB;
-      GemmArgs g = gemm_base(c);
-      for (int b = 0; b < 2; ++b) {
-        g.A[b] = S[b] + j0 + j0 * ld;
-        g.B[b] = linv_j;
-        g.C[b] = S[b] + j0 + j0 * ld;
-      }
-      g.lda = ld; g.ldb = kNB; g.ldc = ld;
-      g.tiles_m = Nt - j; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
-      if ((rc = gemm(c, g, kBNK, 2))) return rc;
-      const int wcols = b1 - j - 1;
-      if (wcols > 0) {
-        GemmArgs t = gemm_base(c);
-        for (int b = 0; b < 2; ++b) {
-          t.A[b] = S[b] + (j0 + kNB) + j0 * ld;   // B[T, j]
-          t.B[b] = L + (j0 + kNB) + j0 * ld;      // L[T, j]  (kBNK)
-          t.C[b] = S[b] + (j0 + kNB) + (j0 + kNB) * ld;
+        launches += 1;
+        CUDA_TRY(launch_potrf_diag(d, m, s));
+        const int rem = Nt - k - 1;
+        if (rem == 0) break;
+        // panel <- panel * Linv_k^T   (in place: BN = 128 covers the whole panel width)
+        GemmArgs g = gemm_base();
+        for (int b = 0; b < m; ++b) {
+          double* panel = mats[b] + (k0 + kNB) + k0 * ld;
+          g.A[b] = panel;
+          g.B[b] = cs[b]->linv + (size_t)k * kNB * kNB;
+          g.C[b] = panel;
+          g.fail_flag[b] = cs[b]->fail_flag;
         }
-        t.lda = ld; t.ldb = ld; t.ldc = ld;
-        t.tiles_m = Nt - j - 1; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
-        if ((rc = gemm(c, t, kBNK, 2))) return rc;
+        g.lda = ld; g.ldb = kNB; g.ldc = ld;
+        g.tiles_m = rem; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
+        if ((rc = gemm(g, kBNK, m))) return rc;
+        // inner update of the remaining columns of this outer block (lower trapezoid)
+        const int wcols = b1 - k - 1;
+        if (wcols > 0) {
+          GemmArgs t = gemm_base();
+          for (int b = 0; b < m; ++b) {
+            double* panel = mats[b] + (k0 + kNB) + k0 * ld;
+            t.A[b] = panel;
+            t.B[b] = panel;
+            t.C[b] = mats[b] + (k0 + kNB) + (k0 + kNB) * ld;
+            t.fail_flag[b] = cs[b]->fail_flag;
+          }
+          t.lda = ld; t.ldb = ld; t.ldc = ld;
+          t.tiles_m = rem; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
+          if ((rc = gemm(t, kBNK, m))) return rc;
+        }
       }
+      const int rem = Nt - b1;
+      if (rem <= 0) continue;
+      // outer trailing update: A_TT -= P P^T with P = L[T, b0:b1], K = (b1 - b0) * 128
+      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
+      GemmArgs t = gemm_base();
+      for (int b = 0; b < m; ++b) {
+        t.A[b] = mats[b] + t0 + c0 * ld;
+        t.B[b] = mats[b] + t0 + c0 * ld;
+        t.C[b] = mats[b] + t0 + t0 * ld;
+        t.fail_flag[b] = cs[b]->fail_flag;
+      }
+      t.lda = ld; t.ldb = ld; t.ldc = ld;
+      t.K = (b1 - b0) * kNB;
+      t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
+      if ((rc = gemm(t, kBNK, m))) return rc;
     }
-    const int rem = Nt - b1;
-    if (rem <= 0) continue;
-    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
-    GemmArgs t = gemm_base(c);
-    for (int b = 0; b < 2; ++b) {
-      t.A[b] = S[b] + t0 + c0 * ld;   // B[T, b0:b1]
-      t.B[b] = L + t0 + c0 * ld;      // L[T, b0:b1]
-      t.C[b] = S[b] + t0 + t0 * ld;
-    }
-    t.lda = ld; t.ldb = ld; t.ldc = ld;
-    t.K = (b1 - b0) * kNB;
-    t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
-    if ((rc = gemm(c, t, kBNK, 2))) return rc;
+    return MLE_OK;
   }
-  return MLE_OK;
-}
 
-int begin_eval(mle_ctx* c, const double theta[3], ThetaParams* P) {
-  if (!theta) return fail(MLE_INVALID, "theta is null");
-  if (mle_fill_theta(theta, c->nugget, P) != 0)
-    return fail(MLE_INVALID, "MaternParams components must be finite and > 0");
-  CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaMemsetAsync(c->fail_flag, 0, sizeof(int), c->stream));
-  c->launches = 0.0;
-  return MLE_OK;
-}
+  // B_i = L^-1 S_i L^-T (lower half) for both derivative matrices of every item, in place.
+  // GEMM batch member z = 2 * item + {0: alpha, 1: nu}.
+  int solves(mle_ctx* const* cs, int m) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    const int zb = 2 * m;
+    auto S = [&](int z) { return z % 2 == 0 ? cs[z / 2]->sa : cs[z / 2]->sn; };
+    auto L = [&](int z) { return (const double*)cs[z / 2]->sigma; };
+    auto Linv = [&](int z, int k) {
+      return (const double*)(cs[z / 2]->linv + (size_t)k * kNB * kNB);
+    };
+    auto flag = [&](int z) { return (const int*)cs[z / 2]->fail_flag; };
+    int rc;
+    // forward sweep X = L^-1 S (all columns), row blocks top-down
+    for (int b0 = 0; b0 < Nt; b0 += kOuter) {
+      const int b1 = std::min(Nt, b0 + kOuter);
+      for (int k = b0; k < b1; ++k) {
+        const long long k0 = (long long)k * kNB;
+        GemmArgs g = gemm_base();
+        for (int z = 0; z < zb; ++z) {
+          g.A[z] = Linv(z, k);
+          g.B[z] = S(z) + k0;   // B(n, kk) = S[k0 + kk, n]  (kBKN)
+          g.C[z] = S(z) + k0;   // in place: BM = 128 covers the whole row panel
+          g.fail_flag[z] = flag(z);
+        }
+        g.lda = kNB; g.ldb = ld; g.ldc = ld;
+        g.tiles_m = 1; g.tiles_n = Nt; g.alpha = 1.0; g.beta = 0.0;
+        if ((rc = gemm(g, kBKN, zb))) return rc;
+        const int wrows = b1 - k - 1;  // remaining row tiles of this outer block
+        if (wrows > 0) {
+          GemmArgs t = gemm_base();
+          for (int z = 0; z < zb; ++z) {
+            t.A[z] = L(z) + (k0 + kNB) + k0 * ld;   // L[k+1 : b1, k]
+            t.B[z] = S(z) + k0;                     // X_k (kBKN)
+            t.C[z] = S(z) + (k0 + kNB);
+            t.fail_flag[z] = flag(z);
+          }
+          t.lda = ld; t.ldb = ld; t.ldc = ld;
+          t.tiles_m = wrows; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
+          if ((rc = gemm(t, kBKN, zb))) return rc;
+        }
+      }
+      const int rem = Nt - b1;
+      if (rem <= 0) continue;
+      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
+      GemmArgs t = gemm_base();
+      for (int z = 0; z < zb; ++z) {
+        t.A[z] = L(z) + t0 + c0 * ld;   // L[T, b0:b1]
+        t.B[z] = S(z) + c0;             // X[b0:b1, :] (kBKN)
+        t.C[z] = S(z) + t0;
+        t.fail_flag[z] = flag(z);
+      }
+      t.lda = ld; t.ldb = ld; t.ldc = ld;
+      t.K = (b1 - b0) * kNB;
+      t.tiles_m = rem; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
+      if ((rc = gemm(t, kBKN, zb))) return rc;
+    }
+    // right sweep on lower tiles: B[j:, j] = X[j:, j] Linv_j^T ; X[T,T] -= B[T,j] L[T,j]^T
+    for (int b0 = 0; b0 < Nt; b0 += kOuter) {
+      const int b1 = std::min(Nt, b0 + kOuter);
+      for (int j = b0; j < b1; ++j) {
+        const long long j0 = (long long)j * kNB;
+        GemmArgs g = gemm_base();
+        for (int z = 0; z < zb; ++z) {
+          g.A[z] = S(z) + j0 + j0 * ld;
+          g.B[z] = Linv(z, j);
+          g.C[z] = S(z) + j0 + j0 * ld;
+          g.fail_flag[z] = flag(z);
+        }
+        g.lda = ld; g.ldb = kNB; g.ldc = ld;
+        g.tiles_m = Nt - j; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
+        if ((rc = gemm(g, kBNK, zb))) return rc;
+        const int wcols = b1 - j - 1;
+        if (wcols > 0) {
+          GemmArgs t = gemm_base();
+          for (int z = 0; z < zb; ++z) {
+            t.A[z] = S(z) + (j0 + kNB) + j0 * ld;   // B[T, j]
+            t.B[z] = L(z) + (j0 + kNB) + j0 * ld;   // L[T, j]  (kBNK)
+            t.C[z] = S(z) + (j0 + kNB) + (j0 + kNB) * ld;
+            t.fail_flag[z] = flag(z);
+          }
+          t.lda = ld; t.ldb = ld; t.ldc = ld;
+          t.tiles_m = Nt - j - 1; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
+          if ((rc = gemm(t, kBNK, zb))) return rc;
+        }
+      }
+      const int rem = Nt - b1;
+      if (rem <= 0) continue;
+      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
+      GemmArgs t = gemm_base();
+      for (int z = 0; z < zb; ++z) {
+        t.A[z] = S(z) + t0 + c0 * ld;   // B[T, b0:b1]
+        t.B[z] = L(z) + t0 + c0 * ld;   // L[T, b0:b1]
+        t.C[z] = S(z) + t0 + t0 * ld;
+        t.fail_flag[z] = flag(z);
+      }
+      t.lda = ld; t.ldb = ld; t.ldc = ld;
+      t.K = (b1 - b0) * kNB;
+      t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
+      if ((rc = gemm(t, kBNK, zb))) return rc;
+    }
+    return MLE_OK;
+  }
+};
 
-int finish_eval(mle_ctx* c, int64_t* bad_pivot, bool derivs) {
-  CUDA_TRY(cudaMemcpyAsync(c->h_res, c->out, sizeof(double) * 9, cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->h_res + 9, c->fail_flag, sizeof(int), cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->h_res + 10, c->fail_idx, sizeof(long long),
-                           cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
+// Runs up to kMaxItems requests (same device, same N) on the leader's stream.
+int run_chunk(Item* items, int m) {
+  mle_ctx* lead = items[0].c;
+  cudaStream_t s = lead->stream;
+  Launcher run{s};
+  for (int b = 0; b < m; ++b) {
+    Item& it = items[b];
+    int rc = ensure_matrices(it.c, it.derivs);
+    if (rc) return rc;
+    std::memcpy(it.c->h_theta, &it.P, sizeof(ThetaParams));
+    CUDA_TRY(cudaMemcpyAsync(it.c->d_theta, it.c->h_theta, sizeof(ThetaParams),
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(it.c->fail_flag, 0, sizeof(int), s));
+  }
+  CUDA_TRY(cudaEventRecord(lead->ev[0], s));
+  // generation for items that need Sigma and/or the derivative matrices
+  GenArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  int ng = 0;
+  for (int b = 0; b < m; ++b) {
+    const Item& it = items[b];
+    if (!it.factor && !it.derivs) continue;
+    GenItem& gi = ga.item[ng++];
+    gi.P = it.c->d_theta;
+    gi.lx = it.c->lx;
+    gi.ly = it.c->ly;
+    gi.z = it.c->z;
+    gi.sigma = it.c->sigma;
+    gi.dalpha = it.c->sa;
+    gi.dnu = it.c->sn;
+    gi.fail_flag = it.c->fail_flag;
+    gi.write_sigma = it.factor ? 1 : 0;
+    gi.write_derivs = it.derivs ? 1 : 0;
+  }
+  ga.ld = lead->N;
+  ga.rows = lead->N;
+  ga.n = (int)lead->n;
+  if (ng > 0) {
+    run.launches += 1;
+    launch_gen_engine(ga, ng, s);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaEventRecord(lead->ev[1], s));
+  {  // Cholesky for items without a cached factor
+    mle_ctx* cs[kMaxItems];
+    double* mats[kMaxItems];
+    long long aug[kMaxItems];
+    int nf = 0;
+    for (int b = 0; b < m; ++b)
+      if (items[b].factor) {
+        cs[nf] = items[b].c;
+        mats[nf] = items[b].c->sigma;
+        aug[nf] = items[b].c->n;
+        ++nf;
+      }
+    if (nf > 0) {
+      int rc = run.potrf(cs, mats, aug, nf);
+      if (rc) return rc;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(lead->ev[2], s));
+  {
+    mle_ctx* cs[kMaxItems];
+    int nd = 0;
+    for (int b = 0; b < m; ++b)
+      if (items[b].derivs) cs[nd++] = items[b].c;
+    if (nd > 0) {
+      int rc = run.solves(cs, nd);
+      if (rc) return rc;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(lead->ev[3], s));
+  ReduceArgs ra;
+  std::memset(&ra, 0, sizeof(ra));
+  for (int b = 0; b < m; ++b) {
+    mle_ctx* c = items[b].c;
+    ra.L[b] = c->sigma;
+    ra.Ba[b] = items[b].derivs ? c->sa : nullptr;
+    ra.Bn[b] = items[b].derivs ? c->sn : nullptr;
+    ra.partials[b] = c->partials;
+    ra.out[b] = c->out;
+    ra.fail_flag[b] = c->fail_flag;
+  }
+  ra.ld = lead->N;
+  ra.n = (int)lead->n;
+  run.launches += 2;
+  CUDA_TRY(launch_reduce(ra, m, s));
+  CUDA_TRY(cudaEventRecord(lead->ev[4], s));
+  for (int b = 0; b < m; ++b) {
+    mle_ctx* c = items[b].c;
+    CUDA_TRY(cudaMemcpyAsync(c->h_res, c->out, sizeof(double) * 9, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_res + 9, c->fail_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_res + 10, c->fail_idx, sizeof(long long),
+                             cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
   float ms[4];
-  for (int p = 0; p < 4; ++p) CUDA_TRY(cudaEventElapsedTime(&ms[p], c->ev[p], c->ev[p + 1]));
-  c->phase_ms[MLE_PHASE_GEN] = ms[0];
-  c->phase_ms[MLE_PHASE_POTRF] = ms[1];
-  c->phase_ms[MLE_PHASE_SOLVE] = ms[2];
-  c->phase_ms[MLE_PHASE_REDUCE] = ms[3];
-  c->phase_ms[MLE_PHASE_TOTAL] = ms[0] + ms[1] + ms[2] + ms[3];
-  const double nd = (double)c->n;
-  c->flops = nd * nd * nd / 3.0 + (derivs ? 2.0 * (nd * nd * nd + nd * nd * nd / 3.0) : 0.0);
-  c->gen_bytes = 8.0 * nd * (nd + 1.0) / 2.0 * (derivs ? 3.0 : 1.0);
-  int flag;
-  std::memcpy(&flag, c->h_res + 9, sizeof(int));
-  if (flag) {
-    long long idx;
-    std::memcpy(&idx, c->h_res + 10, sizeof(long long));
-    if (bad_pivot) *bad_pivot = idx;
-    return fail(MLE_NOT_PD, "matrix not positive definite at pivot " + std::to_string(idx));
+  for (int p = 0; p < 4; ++p) CUDA_TRY(cudaEventElapsedTime(&ms[p], lead->ev[p], lead->ev[p + 1]));
+  double flops = 0.0, gbytes = 0.0;
+  for (int b = 0; b < m; ++b) {
+    const double nd = (double)items[b].c->n;
+    if (items[b].factor) {
+      flops += nd * nd * nd / 3.0;
+      gbytes += 8.0 * nd * (nd + 1.0) / 2.0;
+    }
+    if (items[b].derivs) {
+      flops += 2.0 * (nd * nd * nd + nd * nd * nd / 3.0);
+      gbytes += 2.0 * 8.0 * nd * (nd + 1.0) / 2.0;
+    }
   }
-  if (bad_pivot) *bad_pivot = -1;
+  for (int b = 0; b < m; ++b) {
+    Item& it = items[b];
+    mle_ctx* c = it.c;
+    c->phase_ms[MLE_PHASE_GEN] = ms[0];
+    c->phase_ms[MLE_PHASE_POTRF] = ms[1];
+    c->phase_ms[MLE_PHASE_SOLVE] = ms[2];
+    c->phase_ms[MLE_PHASE_REDUCE] = ms[3];
+    c->phase_ms[MLE_PHASE_TOTAL] = ms[0] + ms[1] + ms[2] + ms[3];
+    c->flops = flops;
+    c->gen_bytes = gbytes;
+    c->launches = run.launches;
+    int flag;
+    std::memcpy(&flag, c->h_res + 9, sizeof(int));
+    if (flag) {
+      long long idx;
+      std::memcpy(&idx, c->h_res + 10, sizeof(long long));
+      it.rc = MLE_NOT_PD;
+      it.pivot = idx;
+      c->factor_valid = false;
+      continue;
+    }
+    it.rc = MLE_OK;
+    it.pivot = -1;
+    c->factor_valid = true;
+    c->cached_theta[0] = it.P.sigma2;
+    c->cached_theta[1] = it.P.alpha;
+    c->cached_theta[2] = it.P.nu;
+    const double* r = c->h_res;
+    const double n = (double)c->n, s2 = it.P.sigma2;
+    const double logdet = r[0], quad = r[1];
+    double* o = it.res;
+    o[0] = -0.5 * n * kLog2Pi - logdet - 0.5 * quad;  // likelihood.py:85-89, 123
+    if (it.mode == 2) {
+      const double tr_a = r[2], tr_n = r[3], faa = r[4], fan = r[5], fnn = r[6];
+      const double yby_a = r[7], yby_n = r[8];
+      o[1] = (quad - n) / (2.0 * s2);          // likelihood.py:129
+      o[2] = -0.5 * tr_a + 0.5 * yby_a;        // likelihood.py:137
+      o[3] = -0.5 * tr_n + 0.5 * yby_n;
+      double* f = o + 4;
+      f[0] = n / (2.0 * s2 * s2);              // likelihood.py:130
+      f[1] = f[3] = tr_a / (2.0 * s2);         // likelihood.py:141
+      f[2] = f[6] = tr_n / (2.0 * s2);         // likelihood.py:145
+      f[4] = 0.5 * faa;                        // likelihood.py:142
+      f[5] = f[7] = 0.5 * fan;                 // likelihood.py:146
+      f[8] = 0.5 * fnn;                        // likelihood.py:147
+    }
+  }
   return MLE_OK;
 }
 
-GenArgs gen_args(const mle_ctx* c, const ThetaParams& P) {
-  GenArgs a;
-  std::memset(&a, 0, sizeof(a));
-  a.P = P;
-  a.lx = c->lx;
-  a.ly = c->ly;
-  a.z = c->z;
-  a.sigma = c->sigma;
-  a.dalpha = c->sa;
-  a.dnu = c->sn;
-  a.ld = c->N;
-  a.rows = c->N;
-  a.n = (int)c->n;
-  a.fail_flag = c->fail_flag;
-  return a;
+bool same_theta(const mle_ctx* c, const double th[3]) {
+  return c->factor_valid && c->cached_theta[0] == th[0] && c->cached_theta[1] == th[1] &&
+         c->cached_theta[2] == th[2];
+}
+
+// Runs the requests (all same device and N) in chunks of kMaxItems.
+int run_batch(Item* items, int count) {
+  for (int b0 = 0; b0 < count; b0 += kMaxItems) {
+    const int m = std::min(kMaxItems, count - b0);
+    CUDA_TRY(cudaSetDevice(items[b0].c->device));
+    int rc = run_chunk(items + b0, m);
+    if (rc) return rc;
+  }
+  return MLE_OK;
+}
+
+// Prepare one request; MLE_INVALID for a bad theta (the request is not run).
+int prepare(mle_ctx* c, const double theta[3], int mode, Item* it) {
+  it->c = c;
+  it->mode = mode;
+  if (!theta) return fail(MLE_INVALID, "theta is null");
+  if (mle_fill_theta(theta, c->nugget, &it->P) != 0)
+    return fail(MLE_INVALID, "MaternParams components must be finite and > 0");
+  if (mode == 2 && c->nugget != 0.0)
+    return fail(MLE_INVALID, "eval_all with a nugget is not implemented yet (loglik only)");
+  it->factor = !same_theta(c, theta);
+  it->derivs = (mode == 2);
+  return MLE_OK;
 }
 
 int check_finite(const double* v, int64_t m, const char* what) {
@@ -336,11 +527,24 @@ int check_finite(const double* v, int64_t m, const char* what) {
   return MLE_OK;
 }
 
+int single(mle_ctx* c, const double theta[3], int mode, double* res, int64_t* bad_pivot) {
+  Item it;
+  int rc = prepare(c, theta, mode, &it);
+  if (rc) return rc;
+  rc = run_batch(&it, 1);
+  if (rc) return rc;
+  if (bad_pivot) *bad_pivot = it.pivot;
+  if (it.rc == MLE_NOT_PD)
+    return fail(MLE_NOT_PD, "matrix not positive definite at pivot " + std::to_string(it.pivot));
+  std::memcpy(res, it.res, sizeof(double) * kResults);
+  return MLE_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-const char* mle_version(void) { return "maternfisher-b200 0.1.0 (sm_100a)"; }
+const char* mle_version(void) { return "maternfisher-b200 0.2.0 (sm_100a)"; }
 const char* mle_last_error(void) { return g_last_error.c_str(); }
 
 int mle_device_count(void) {
@@ -390,8 +594,10 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   CTX_TRY(cudaMalloc(&c->z, sizeof(double) * n));
   CTX_TRY(cudaMalloc(&c->fail_flag, sizeof(int)));
   CTX_TRY(cudaMalloc(&c->fail_idx, sizeof(long long)));
-  CTX_TRY(cudaMalloc(&c->partials, sizeof(double) * 148 * 4 * 7));
+  CTX_TRY(cudaMalloc(&c->partials, sizeof(double) * kReduceBlocks * kReduceSums));
   CTX_TRY(cudaMalloc(&c->out, sizeof(double) * 9));
+  CTX_TRY(cudaMalloc(&c->d_theta, sizeof(ThetaParams)));
+  CTX_TRY(cudaMallocHost(&c->h_theta, sizeof(ThetaParams)));
   CTX_TRY(cudaMallocHost(&c->h_res, sizeof(double) * 12));
   CTX_TRY(cudaMemcpyAsync(c->lx, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CTX_TRY(cudaMemcpyAsync(c->ly, y.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
@@ -418,6 +624,8 @@ void mle_ctx_destroy(mle_ctx* c) {
   cudaFree(c->fail_idx);
   cudaFree(c->partials);
   cudaFree(c->out);
+  cudaFree(c->d_theta);
+  if (c->h_theta) cudaFreeHost(c->h_theta);
   if (c->h_res) cudaFreeHost(c->h_res);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -434,77 +642,77 @@ int mle_ctx_set_values(mle_ctx* c, const double* z) {
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaMemcpyAsync(c->z, z, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->factor_valid = false;  // row n of L carries L^-1 z
   return MLE_OK;
 }
 
 int mle_loglik(mle_ctx* c, const double theta[3], double* loglik, int64_t* bad_pivot) {
   if (!c || !loglik) return fail(MLE_INVALID, "null argument");
-  ThetaParams P;
-  int rc = begin_eval(c, theta, &P);
+  double res[kResults];
+  int rc = single(c, theta, 1, res, bad_pivot);
   if (rc) return rc;
-  rc = ensure_matrices(c, false);
-  if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
-  ++c->launches;
-  launch_gen_engine(gen_args(c, P), false, c->stream);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
-  rc = run_potrf(c, c->sigma, c->N, c->Nt, c->n);
-  if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
-  c->launches += 2;
-  CUDA_TRY(launch_reduce_loglik(c->sigma, c->N, (int)c->n, c->partials, c->out, c->fail_flag,
-                                c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev[4], c->stream));
-  rc = finish_eval(c, bad_pivot, false);
-  if (rc) return rc;
-  const double logdet = c->h_res[0], quad = c->h_res[1];
-  *loglik = -0.5 * (double)c->n * kLog2Pi - logdet - 0.5 * quad;  // likelihood.py:85-89
+  *loglik = res[0];
   return MLE_OK;
 }
 
 int mle_eval_all(mle_ctx* c, const double theta[3], double* loglik, double grad[3],
                  double fisher[9], int64_t* bad_pivot) {
   if (!c || !loglik || !grad || !fisher) return fail(MLE_INVALID, "null argument");
-  if (c->nugget != 0.0)
-    return fail(MLE_INVALID, "eval_all with a nugget is not implemented yet (loglik only)");
-  ThetaParams P;
-  int rc = begin_eval(c, theta, &P);
+  double res[kResults];
+  int rc = single(c, theta, 2, res, bad_pivot);
   if (rc) return rc;
-  rc = ensure_matrices(c, true);
-  if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
-  ++c->launches;
-  launch_gen_engine(gen_args(c, P), true, c->stream);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
-  rc = run_potrf(c, c->sigma, c->N, c->Nt, c->n);
-  if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
-  rc = run_solves(c);
-  if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
-  c->launches += 2;
-  CUDA_TRY(launch_reduce_eval(c->sigma, c->sa, c->sn, c->N, (int)c->n, c->partials, c->out,
-                              c->fail_flag, c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev[4], c->stream));
-  rc = finish_eval(c, bad_pivot, true);
-  if (rc) return rc;
-  const double* r = c->h_res;
-  const double n = (double)c->n, s2 = P.sigma2;
-  const double logdet = r[0], quad = r[1], tr_a = r[2], tr_n = r[3];
-  const double faa = r[4], fan = r[5], fnn = r[6], yby_a = r[7], yby_n = r[8];
-  *loglik = -0.5 * n * kLog2Pi - logdet - 0.5 * quad;            // likelihood.py:123
-  grad[0] = (quad - n) / (2.0 * s2);                              // likelihood.py:129
-  grad[1] = -0.5 * tr_a + 0.5 * yby_a;                            // likelihood.py:137
-  grad[2] = -0.5 * tr_n + 0.5 * yby_n;
-  fisher[0] = n / (2.0 * s2 * s2);                                // likelihood.py:130
-  fisher[1] = fisher[3] = tr_a / (2.0 * s2);                      // likelihood.py:141
-  fisher[2] = fisher[6] = tr_n / (2.0 * s2);                      // likelihood.py:145
-  fisher[4] = 0.5 * faa;                                          // likelihood.py:142
-  fisher[5] = fisher[7] = 0.5 * fan;                              // likelihood.py:146
-  fisher[8] = 0.5 * fnn;                                          // likelihood.py:147
+  *loglik = res[0];
+  std::memcpy(grad, res + 1, sizeof(double) * 3);
+  std::memcpy(fisher, res + 4, sizeof(double) * 9);
+  return MLE_OK;
+}
+
+int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const int* modes,
+                   double* results, int64_t* pivots, int* rcs) {
+  if (count < 0 || (count > 0 && (!ctxs || !thetas || !modes || !results || !rcs)))
+    return fail(MLE_INVALID, "null argument");
+  std::vector<Item> items;
+  std::vector<int> slot;
+  std::string bad;
+  for (int i = 0; i < count; ++i) {
+    rcs[i] = MLE_OK;
+    if (pivots) pivots[i] = -1;
+    if (modes[i] == 0) continue;
+    if (!ctxs[i] || (modes[i] != 1 && modes[i] != 2)) return fail(MLE_INVALID, "bad request");
+    for (int j = 0; j < i; ++j)
+      if (modes[j] != 0 && ctxs[j] == ctxs[i])
+        return fail(MLE_INVALID, "a context may appear once per batch");
+    Item it;
+    if (prepare(ctxs[i], thetas + 3 * i, modes[i], &it) != MLE_OK) {
+      rcs[i] = MLE_INVALID;
+      bad = g_last_error;
+      continue;
+    }
+    items.push_back(it);
+    slot.push_back(i);
+  }
+  // group by (device, N): every chunk must share them
+  std::vector<char> done(items.size(), 0);
+  for (size_t a = 0; a < items.size(); ++a) {
+    if (done[a]) continue;
+    std::vector<Item> group;
+    std::vector<int> gslot;
+    for (size_t b = a; b < items.size(); ++b)
+      if (!done[b] && items[b].c->device == items[a].c->device && items[b].c->N == items[a].c->N) {
+        group.push_back(items[b]);
+        gslot.push_back(slot[b]);
+        done[b] = 1;
+      }
+    int rc = run_batch(group.data(), (int)group.size());
+    if (rc) return rc;
+    for (size_t g = 0; g < group.size(); ++g) {
+      const int i = gslot[g];
+      rcs[i] = group[g].rc;
+      if (pivots) pivots[i] = group[g].pivot;
+      std::memcpy(results + (size_t)kResults * i, group[g].res, sizeof(double) * kResults);
+    }
+  }
+  if (!bad.empty()) g_last_error = bad;
   return MLE_OK;
 }
 
@@ -512,14 +720,25 @@ int mle_build(mle_ctx* c, const double theta[3], int which, double* out_host) {
   if (!c || !out_host) return fail(MLE_INVALID, "null argument");
   if (which < MLE_WHICH_SIGMA || which > MLE_WHICH_NU)
     return fail(MLE_INVALID, "which must be one of sigma, sigma2, alpha, nu");
-  ThetaParams P;
-  int rc = begin_eval(c, theta, &P);
+  Item it;
+  int rc = prepare(c, theta, 1, &it);
   if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
   rc = ensure_matrices(c, false);
   if (rc) return rc;
-  GenArgs a = gen_args(c, P);
+  c->factor_valid = false;  // the Sigma buffer is reused as scratch
+  std::memcpy(c->h_theta, &it.P, sizeof(ThetaParams));
+  CUDA_TRY(cudaMemcpyAsync(c->d_theta, c->h_theta, sizeof(ThetaParams), cudaMemcpyHostToDevice,
+                           c->stream));
+  GenArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.item[0].P = c->d_theta;
+  a.item[0].lx = c->lx;
+  a.item[0].ly = c->ly;
+  a.item[0].sigma = c->sigma;
   a.ld = c->n;
   a.rows = c->n;
+  a.n = (int)c->n;
   launch_gen_build(a, which, c->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(out_host, c->sigma, sizeof(double) * (size_t)c->n * (size_t)c->n,
@@ -555,15 +774,14 @@ int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t*
   }
   struct Guard {
     mle_ctx* c;
-    double* dA = nullptr;
     ~Guard() {
-      cudaFree(dA);
+      cudaFree(c->sigma);
       cudaFree(c->linv);
       cudaFree(c->fail_flag);
       cudaFree(c->fail_idx);
       if (c->h_res) cudaFreeHost(c->h_res);
       if (c->stream) cudaStreamDestroy(c->stream);
-      c->linv = nullptr;
+      c->sigma = c->linv = nullptr;
       c->fail_flag = nullptr;
       c->fail_idx = nullptr;
       c->h_res = nullptr;
@@ -571,17 +789,21 @@ int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t*
     }
   } guard{&c};
   CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-  CUDA_TRY(cudaMalloc(&guard.dA, sizeof(double) * (size_t)N * N));
+  CUDA_TRY(cudaMalloc(&c.sigma, sizeof(double) * (size_t)N * N));
   CUDA_TRY(cudaMalloc(&c.linv, sizeof(double) * (size_t)c.Nt * kNB * kNB));
   CUDA_TRY(cudaMalloc(&c.fail_flag, sizeof(int)));
   CUDA_TRY(cudaMalloc(&c.fail_idx, sizeof(long long)));
   CUDA_TRY(cudaMallocHost(&c.h_res, sizeof(double) * 12));
-  CUDA_TRY(cudaMemcpyAsync(guard.dA, h.data(), sizeof(double) * (size_t)N * N,
+  CUDA_TRY(cudaMemcpyAsync(c.sigma, h.data(), sizeof(double) * (size_t)N * N,
                            cudaMemcpyHostToDevice, c.stream));
   CUDA_TRY(cudaMemsetAsync(c.fail_flag, 0, sizeof(int), c.stream));
-  rc = run_potrf(&c, guard.dA, N, c.Nt, -1);
+  Launcher run{c.stream};
+  mle_ctx* cs[1] = {&c};
+  double* mats[1] = {c.sigma};
+  long long aug[1] = {-1};
+  rc = run.potrf(cs, mats, aug, 1);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(h.data(), guard.dA, sizeof(double) * (size_t)N * N,
+  CUDA_TRY(cudaMemcpyAsync(h.data(), c.sigma, sizeof(double) * (size_t)N * N,
                            cudaMemcpyDeviceToHost, c.stream));
   CUDA_TRY(cudaMemcpyAsync(c.h_res + 9, c.fail_flag, sizeof(int), cudaMemcpyDeviceToHost,
                            c.stream));
@@ -608,22 +830,27 @@ static int run_elem(int op, const ThetaParams& P, int which, const double* x, in
   if (rc) return rc;
   if (m == 0) return MLE_OK;
   double *dx = nullptr, *dy = nullptr;
+  ThetaParams* dP = nullptr;
   cudaStream_t s = nullptr;
   struct G {
     double** a;
     double** b;
+    ThetaParams** p;
     cudaStream_t* s;
     ~G() {
       cudaFree(*a);
       cudaFree(*b);
+      cudaFree(*p);
       if (*s) cudaStreamDestroy(*s);
     }
-  } guard{&dx, &dy, &s};
+  } guard{&dx, &dy, &dP, &s};
   CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   CUDA_TRY(cudaMalloc(&dx, sizeof(double) * m));
   CUDA_TRY(cudaMalloc(&dy, sizeof(double) * m));
+  CUDA_TRY(cudaMalloc(&dP, sizeof(ThetaParams)));
+  CUDA_TRY(cudaMemcpyAsync(dP, &P, sizeof(ThetaParams), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(dx, x, sizeof(double) * m, cudaMemcpyHostToDevice, s));
-  launch_elem(P, op, which, dx, m, dy, s);
+  launch_elem(dP, op, which, dx, m, dy, s);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(out, dy, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));

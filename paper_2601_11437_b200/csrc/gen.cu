@@ -5,10 +5,11 @@
 // (matern.py:100-125).  Distances are recomputed per element (no pdist + np.unique dedup,
 // matern.py:86-97) with the same rounding as scipy's pdist: sqrt((dx*dx) + (dy*dy)).
 //
-// One CTA owns one 32x32 lower tile (I >= J) of the padded, column-major N x N matrices.
-// It writes tile (I, J) of every requested output with coalesced column stores and, for the
-// derivative matrices that must be stored in full, the mirrored tile (J, I) through a
-// shared-memory transpose.
+// One CTA owns one 32x32 lower tile (I >= J) of one item's padded, column-major N x N
+// matrices (blockIdx.y = item).  It writes tile (I, J) of every requested output with
+// coalesced column stores and, for the derivative matrices that are stored in full, the
+// mirrored tile (J, I) through a shared-memory transpose.  The item's per-theta scalars
+// (ThetaParams, ~1.1 KB) are staged into shared memory once per CTA.
 //
 // Engine layout: index n is the augmented row carrying z (Sigma[n, j] = z_j,
 // Sigma[n, n] = 0), indices > n are padding (identity in Sigma, zero in the derivatives).
@@ -18,7 +19,6 @@
 #include "kernels.h"
 
 namespace mle {
-
 
 namespace {
 
@@ -41,22 +41,32 @@ __device__ __forceinline__ double pair_distance(const double* lx, const double* 
   return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
 }
 
+// Stage one ThetaParams from global memory into shared memory (all threads participate).
+__device__ __forceinline__ void stage_params(ThetaParams* dst, const ThetaParams* src) {
+  const int words = (int)(sizeof(ThetaParams) / sizeof(int));
+  const int* s = reinterpret_cast<const int*>(src);
+  int* d = reinterpret_cast<int*>(dst);
+  for (int w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+  __syncthreads();
+}
+
 }  // namespace
 
-// kMode: 0 = Sigma only (loglik), 1 = Sigma + dSigma/dalpha + dSigma/dnu (eval_all).
-template <int kMode>
 __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
-  if (a.fail_flag != nullptr && *a.fail_flag) return;
+  const GenItem& it = a.item[blockIdx.y];
+  if (it.fail_flag != nullptr && *it.fail_flag) return;
+  __shared__ ThetaParams P;
+  __shared__ double s_da[kGT][kGT + 1];
+  __shared__ double s_dn[kGT][kGT + 1];
+  stage_params(&P, it.P);
   int ti, tj;
   lower_tile_index((long long)blockIdx.x, &ti, &tj);
-  const ThetaParams& P = a.P;
   const int lane_row = threadIdx.x & (kGT - 1);
   const int col0 = threadIdx.x >> 5;
   const int i = ti * kGT + lane_row;
   const long long ld = a.ld;
   const int n = a.n;
-  __shared__ double s_da[kGT][kGT + 1];
-  __shared__ double s_dn[kGT][kGT + 1];
+  const bool derivs = it.write_derivs != 0;
 #pragma unroll 1
   for (int r = 0; r < kGT / 8; ++r) {
     const int jl = col0 + 8 * r;
@@ -67,18 +77,22 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
       if (i == j) {
         c = (i == n) ? 0.0 : 1.0;
       } else if (i == n && j < n) {
-        c = a.z[j];
+        c = it.z[j];
       } else if (j == n && i < n) {
-        c = a.z[i];
+        c = it.z[i];
       } else {
         c = 0.0;
       }
     } else if (i == j) {
       c = P.sigma2 + P.nugget;  // matern.py:182 fill_diagonal(sigma2)
     } else {
-      const double h = pair_distance(a.lx, a.ly, i, j);
+      const double h = pair_distance(it.lx, it.ly, i, j);
       if (h > 0.0) {
-        const MaternVals v = matern_positive<kMode == 1>(P, h);
+        MaternVals v;
+        if (derivs)
+          v = matern_positive<true>(P, h);
+        else
+          v = matern_positive<false>(P, h);
         c = v.c;
         da = v.dalpha;
         dn = v.dnu;
@@ -87,15 +101,15 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
       }
     }
     const long long off = (long long)i + (long long)j * ld;
-    a.sigma[off] = c;
-    if (kMode == 1) {
-      a.dalpha[off] = da;
-      a.dnu[off] = dn;
+    if (it.write_sigma) it.sigma[off] = c;
+    if (derivs) {
+      it.dalpha[off] = da;
+      it.dnu[off] = dn;
       s_da[lane_row][jl] = da;
       s_dn[lane_row][jl] = dn;
     }
   }
-  if (kMode == 1 && ti != tj) {
+  if (derivs && ti != tj) {
     __syncthreads();
     // mirrored tile (J, I): rows from tile J, columns from tile I
     const int i2 = tj * kGT + lane_row;
@@ -104,23 +118,25 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
       const int jl = col0 + 8 * r;
       const int j2 = ti * kGT + jl;
       const long long off = (long long)i2 + (long long)j2 * ld;
-      a.dalpha[off] = s_da[jl][lane_row];
-      a.dnu[off] = s_dn[jl][lane_row];
+      it.dalpha[off] = s_da[jl][lane_row];
+      it.dnu[off] = s_dn[jl][lane_row];
     }
   }
 }
 
 // Full symmetric n x n matrix of one kind (mle_build), no augmentation / padding.
 __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int which) {
+  const GenItem& it = a.item[0];
+  __shared__ ThetaParams P;
+  __shared__ double s_v[kGT][kGT + 1];
+  stage_params(&P, it.P);
   int ti, tj;
   lower_tile_index((long long)blockIdx.x, &ti, &tj);
-  const ThetaParams& P = a.P;
   const int lane_row = threadIdx.x & (kGT - 1);
   const int col0 = threadIdx.x >> 5;
   const int i = ti * kGT + lane_row;
   const long long ld = a.ld;
   const int n = a.n;
-  __shared__ double s_v[kGT][kGT + 1];
 #pragma unroll 1
   for (int r = 0; r < kGT / 8; ++r) {
     const int jl = col0 + 8 * r;
@@ -131,7 +147,7 @@ __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int whi
         v = (which == MLE_WHICH_SIGMA) ? P.sigma2 + P.nugget
                                        : (which == MLE_WHICH_SIGMA2 ? 1.0 : 0.0);
       } else {
-        const double h = pair_distance(a.lx, a.ly, i, j);
+        const double h = pair_distance(it.lx, it.ly, i, j);
         if (h > 0.0) {
           if (which == MLE_WHICH_SIGMA || which == MLE_WHICH_SIGMA2) {
             const MaternVals m = matern_positive<false>(P, h);
@@ -144,7 +160,7 @@ __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int whi
           v = (which == MLE_WHICH_SIGMA) ? P.sigma2 : (which == MLE_WHICH_SIGMA2 ? 1.0 : 0.0);
         }
       }
-      a.sigma[(long long)i + (long long)j * ld] = v;
+      it.sigma[(long long)i + (long long)j * ld] = v;
     }
     s_v[lane_row][jl] = v;
   }
@@ -155,29 +171,32 @@ __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int whi
     for (int r = 0; r < kGT / 8; ++r) {
       const int jl = col0 + 8 * r;
       const int j2 = ti * kGT + jl;
-      if (i2 < n && j2 < n) a.sigma[(long long)i2 + (long long)j2 * ld] = s_v[jl][lane_row];
+      if (i2 < n && j2 < n) it.sigma[(long long)i2 + (long long)j2 * ld] = s_v[jl][lane_row];
     }
   }
 }
 
 // Elementwise evaluators (parity surface for bessel.py / matern.py scalar functions).
-__global__ void elem_kernel(ThetaParams P, int op, int which, const double* __restrict__ x,
-                            long long m, double* __restrict__ out) {
+__global__ void elem_kernel(const ThetaParams* Pg, int op, int which,
+                            const double* __restrict__ x, long long m, double* __restrict__ out) {
+  __shared__ ThetaParams P;
+  stage_params(&P, Pg);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
        t += (long long)gridDim.x * blockDim.x) {
     const double v = x[t];
     double r;
     if (op == 0) {  // bessel_k(nu, x) = K_|nu|(x), x > 0 validated on the host
       double k_nu, k_m1;
-      bessel_k_ladder(P.kmain, v, &k_nu, &k_m1);
+      bessel_k_ladder(P.kmain, P.recip_int, v, &k_nu, &k_m1);
       r = k_nu;
     } else if (op == 1) {  // dnu_xnu_knu(nu, x), x >= 0
       if (v == 0.0) {
         r = 0.0;  // bessel.py:358 (ZERO_ARG)
       } else {
         double k_nu, k_m1;
-        bessel_k_ladder(P.kmain, v, &k_nu, &k_m1);
-        r = dnu_xnu_knu(P, v, pow(v, P.nu) * k_nu);
+        bessel_k_ladder(P.kmain, P.recip_int, v, &k_nu, &k_m1);
+        const double v_nu = pow(v, P.nu);
+        r = dnu_xnu_knu(P, v, v_nu * k_nu, v_nu);
       }
     } else {  // Matern value / derivative at distance h >= 0
       if (v > 0.0) {
@@ -209,25 +228,21 @@ static long long lower_tiles(long long rows) {
   return t * (t + 1) / 2;
 }
 
-void launch_gen_engine(const GenArgs& a, bool derivs, cudaStream_t s) {
-  const long long blocks = lower_tiles(a.rows);
-  if (derivs)
-    gen_engine_kernel<1><<<(unsigned)blocks, kGThreads, 0, s>>>(a);
-  else
-    gen_engine_kernel<0><<<(unsigned)blocks, kGThreads, 0, s>>>(a);
+void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s) {
+  const dim3 grid((unsigned)lower_tiles(a.rows), (unsigned)items);
+  gen_engine_kernel<<<grid, kGThreads, 0, s>>>(a);
 }
 
 void launch_gen_build(const GenArgs& a, int which, cudaStream_t s) {
-  const long long blocks = lower_tiles(a.n);
-  gen_build_kernel<<<(unsigned)blocks, kGThreads, 0, s>>>(a, which);
+  gen_build_kernel<<<(unsigned)lower_tiles(a.n), kGThreads, 0, s>>>(a, which);
 }
 
-void launch_elem(const ThetaParams& P, int op, int which, const double* x, long long m,
+void launch_elem(const ThetaParams* P_dev, int op, int which, const double* x, long long m,
                  double* out, cudaStream_t s) {
   long long blocks = (m + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (blocks < 1) blocks = 1;
-  elem_kernel<<<(unsigned)blocks, 256, 0, s>>>(P, op, which, x, m, out);
+  elem_kernel<<<(unsigned)blocks, 256, 0, s>>>(P_dev, op, which, x, m, out);
 }
 
 }  // namespace mle

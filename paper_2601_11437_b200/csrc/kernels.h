@@ -1,5 +1,9 @@
 // kernels.h — internal launch interface between the C-ABI engine (engine.cu) and the
 // sm_100a kernels (gen.cu, linalg.cu).  Not part of the public ABI.
+//
+// Every kernel is batched over "items": independent datasets of the same padded size that
+// are evaluated together (replicate fits, L9 start points).  Item b of a launch uses the
+// b-th pointer of each array below and its own failure flag.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -9,29 +13,38 @@
 
 namespace mle {
 
-constexpr int kNB = 128;  // factorization tile (Cholesky / solve block size)
+constexpr int kNB = 128;       // factorization tile (Cholesky / solve block size)
+constexpr int kMaxItems = 8;   // datasets per batched launch
+constexpr int kMaxGemm = 2 * kMaxItems;
 
-struct GenArgs {
-  ThetaParams P;
+struct GenItem {
+  const ThetaParams* P;  // device copy of this item's per-theta scalars
   const double* lx;   // x coordinates (n)
   const double* ly;   // y coordinates (n)
   const double* z;    // observed values (n); augmented row
   double* sigma;      // Sigma (engine) or the single output (build)
   double* dalpha;     // dSigma/dalpha (full storage)
   double* dnu;        // dSigma/dnu (full storage)
+  const int* fail_flag;
+  int write_sigma;    // 1: write Sigma (lower tiles + augmented row + padding)
+  int write_derivs;   // 1: write both derivative matrices (full storage)
+};
+
+struct GenArgs {
+  GenItem item[kMaxItems];
   long long ld;       // leading dimension (column-major)
   long long rows;     // padded extent N (engine) / n (build)
   int n;              // number of locations
-  const int* fail_flag;
 };
 
 // Operand layouts of op(B): B(n,k) at b[n + k*ldb] (kBNK) or b[k + n*ldb] (kBKN).
 enum BLayout { kBNK = 0, kBKN = 1 };
 
 struct GemmArgs {
-  const double* A[2];
-  const double* B[2];
-  double* C[2];
+  const double* A[kMaxGemm];
+  const double* B[kMaxGemm];
+  double* C[kMaxGemm];
+  const int* fail_flag[kMaxGemm];
   long long lda, ldb, ldc;
   int K;             // multiple of 16
   int tiles_m;       // number of 128-row tiles of C
@@ -40,28 +53,45 @@ struct GemmArgs {
   int trap;          // full mode: 1 skips tiles with tm < tn (lower trapezoid)
   double alpha;      // +1 or -1
   double beta;       // 0 (overwrite) or 1 (accumulate into C)
-  const int* fail_flag;
+};
+
+struct DiagArgs {
+  double* a[kMaxItems];
+  double* linv[kMaxItems];      // 128 x 128 inverse of this step's diagonal tile
+  int* fail_flag[kMaxItems];
+  long long* fail_idx[kMaxItems];
+  long long n_aug[kMaxItems];   // augmented index (no pivot check), -1 for none
+  long long ld;
+  int k0;
+};
+
+struct ReduceArgs {
+  const double* L[kMaxItems];
+  const double* Ba[kMaxItems];  // null for loglik-only items
+  const double* Bn[kMaxItems];
+  double* partials[kMaxItems];
+  double* out[kMaxItems];
+  const int* fail_flag[kMaxItems];
+  long long ld;
+  int n;
 };
 
 cudaError_t init_kernel_attributes();  // GEMM smem opt-in (per device)
 cudaError_t init_diag_attributes();    // diagonal-tile kernel smem opt-in (per device)
 cudaError_t upload_u_tables(const double* u, const double* du);
-void launch_gen_engine(const GenArgs& a, bool derivs, cudaStream_t s);
+void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s);
 void launch_gen_build(const GenArgs& a, int which, cudaStream_t s);
-void launch_elem(const ThetaParams& P, int op, int which, const double* x, long long m,
+void launch_elem(const ThetaParams* P_dev, int op, int which, const double* x, long long m,
                  double* out, cudaStream_t s);
 
-// C = alpha * A * op(B)^T-style product (see linalg.cu) + beta * C, batched over gridDim.z.
+// C = alpha * A * op(B) + beta * C per batch member (gridDim.z = batch).
 cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s);
-// Factor the 128x128 diagonal tile at (k0, k0) in place and write its inverse to linv.
-cudaError_t launch_potrf_diag(double* a, long long ld, int k0, long long n_aug, double* linv,
-                              int* fail_flag, long long* fail_idx, cudaStream_t s);
-// Reductions: 7 partial sums per block over the first n indices.
-cudaError_t launch_reduce_eval(const double* L, const double* Ba, const double* Bn,
-                               long long ld, int n, double* partials, double* out,
-                               const int* fail_flag, cudaStream_t s);
-cudaError_t launch_reduce_loglik(const double* L, long long ld, int n, double* partials,
-                                 double* out, const int* fail_flag, cudaStream_t s);
-cudaError_t launch_clear_upper(double* a, long long ld, int n, cudaStream_t s);
+// Factor the 128x128 diagonal tile at (k0, k0) of every item in place (+ its inverse).
+cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s);
+// Reductions: per item 9 results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>, yBy_A, yBy_N].
+cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
+
+constexpr int kReduceBlocks = 148 * 4;
+constexpr int kReduceSums = 7;
 
 }  // namespace mle

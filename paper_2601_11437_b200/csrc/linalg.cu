@@ -68,7 +68,8 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn)
 // C[tm, tn] = alpha * sum_k A(m, k) B(n, k) + beta * C, A(m,k) = A[m + k*lda].
 template <int kBL>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
-  if (g.fail_flag != nullptr && *g.fail_flag) return;
+  const int z = blockIdx.z;
+  if (*g.fail_flag[z]) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
@@ -77,12 +78,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
   int tm, tn;
   tile_coords(g, &tm, &tn);
   if (g.trap && tm < tn) return;
-  const bool z1 = blockIdx.z != 0;
   // no __restrict__: panel products run in place (C aliases A or B; see engine.cu)
-  const double* A = (z1 ? g.A[1] : g.A[0]) + (long long)tm * BM;
-  const double* Bz = z1 ? g.B[1] : g.B[0];
+  const double* A = g.A[z] + (long long)tm * BM;
+  const double* Bz = g.B[z];
   const double* B = (kBL == kBNK) ? Bz + (long long)tn * BN : Bz + (long long)tn * BN * g.ldb;
-  double* C = (z1 ? g.C[1] : g.C[0]) + (long long)tm * BM + (long long)tn * BN * g.ldc;
+  double* C = g.C[z] + (long long)tm * BM + (long long)tn * BN * g.ldc;
   const long long lda = g.lda, ldb = g.ldb, ldc = g.ldc;
 
   const int tid = threadIdx.x;
@@ -328,10 +328,15 @@ __device__ long long g_diag_clock[32];
 #define DIAG_T(slot)
 #endif
 
-__global__ void __launch_bounds__(DTHREADS, 1)
-    potrf_diag_kernel(double* a, long long ld, int k0, long long n_aug, double* linv,
-                      int* fail_flag, long long* fail_idx) {
+__global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
+  const int item = blockIdx.x;
+  int* fail_flag = da.fail_flag[item];
   if (*fail_flag) return;
+  long long* fail_idx = da.fail_idx[item];
+  double* a = da.a[item];
+  double* linv = da.linv[item];
+  const long long ld = da.ld, n_aug = da.n_aug[item];
+  const int k0 = da.k0;
   extern __shared__ __align__(16) double dsm[];
   double* Ls = dsm;             // DT * DS
   double* dinv = Ls + DT * DS;  // DT
@@ -501,19 +506,19 @@ cudaError_t init_diag_attributes() {
                               (int)kDiagSmem);
 }
 
-cudaError_t launch_potrf_diag(double* a, long long ld, int k0, long long n_aug, double* linv,
-                              int* fail_flag, long long* fail_idx, cudaStream_t s) {
-  potrf_diag_kernel<<<1, DTHREADS, kDiagSmem, s>>>(a, ld, k0, n_aug, linv, fail_flag,
-                                                   fail_idx);
+cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s) {
+  potrf_diag_kernel<<<items, DTHREADS, kDiagSmem, s>>>(d);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------
-// Reductions.  Partials: per block 7 sums [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>].
+// Reductions.  Partials: per block 7 sums [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>];
+// blockIdx.y = item.  Fixed grid and fixed summation order -> deterministic results, and the
+// loglik-only path (Ba == null) sums log-det / y^T y in exactly the eval_all order.
 namespace {
 constexpr int RTHREADS = 256;
-constexpr int RBLOCKS = 148 * 4;
-constexpr int RN = 7;
+constexpr int RBLOCKS = kReduceBlocks;
+constexpr int RN = kReduceSums;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -528,13 +533,14 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __restrict__ L,
-                                                               const double* __restrict__ Ba,
-                                                               const double* __restrict__ Bn,
-                                                               long long ld, int n,
-                                                               double* partials,
-                                                               const int* fail_flag) {
-  if (*fail_flag) return;
+__global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
+  const int item = blockIdx.y;
+  if (*ra.fail_flag[item]) return;
+  const double* __restrict__ L = ra.L[item];
+  const double* __restrict__ Ba = ra.Ba[item];
+  const double* __restrict__ Bn = ra.Bn[item];
+  const long long ld = ra.ld;
+  const int n = ra.n;
   __shared__ double sh[RTHREADS / 32];
   double s[RN] = {0, 0, 0, 0, 0, 0, 0};
   for (int j = blockIdx.x; j < n; j += gridDim.x) {
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __r
       s[0] += log(L[j + cj]);
       const double y = L[n + cj];
       s[1] += y * y;
-      if (Ba == nullptr) continue;  // loglik: same summation order as eval_all
+      if (Ba == nullptr) continue;
       const double a = Ba[j + cj], b = Bn[j + cj];
       s[2] += a;
       s[3] += b;
@@ -559,6 +565,7 @@ __global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __r
       s[6] += 2.0 * b * b;
     }
   }
+  double* partials = ra.partials[item];
   for (int q = 0; q < RN; ++q) {
     const double t = block_sum(s[q], sh);
     if (threadIdx.x == 0) partials[blockIdx.x * RN + q] = t;
@@ -566,45 +573,27 @@ __global__ void __launch_bounds__(RTHREADS) reduce_eval_kernel(const double* __r
 }
 
 // out[0..6] = fixed-order sums of the partials; out[7], out[8] = B_alpha[n,n], B_nu[n,n].
-__global__ void reduce_final_kernel(const double* partials, int nblocks, const double* Ba,
-                                    const double* Bn, long long ld, int n, double* out,
-                                    const int* fail_flag) {
-  if (*fail_flag) return;
+__global__ void reduce_final_kernel(ReduceArgs ra) {
+  const int item = blockIdx.x;
+  if (*ra.fail_flag[item]) return;
+  const double* partials = ra.partials[item];
+  const double* Ba = ra.Ba[item];
+  const double* Bn = ra.Bn[item];
+  double* out = ra.out[item];
+  const long long diag_n = ra.n + (long long)ra.n * ra.ld;
   const int q = threadIdx.x;
   if (q < RN) {
     double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partials[b * RN + q];
+    for (int b = 0; b < RBLOCKS; ++b) s += partials[b * RN + q];
     out[q] = s;
   }
-  if (q == RN) out[RN] = Ba ? Ba[n + (long long)n * ld] : 0.0;
-  if (q == RN + 1) out[RN + 1] = Bn ? Bn[n + (long long)n * ld] : 0.0;
+  if (q == RN) out[RN] = Ba ? Ba[diag_n] : 0.0;
+  if (q == RN + 1) out[RN + 1] = Bn ? Bn[diag_n] : 0.0;
 }
 
-cudaError_t launch_reduce_eval(const double* L, const double* Ba, const double* Bn,
-                               long long ld, int n, double* partials, double* out,
-                               const int* fail_flag, cudaStream_t s) {
-  reduce_eval_kernel<<<RBLOCKS, RTHREADS, 0, s>>>(L, Ba, Bn, ld, n, partials, fail_flag);
-  reduce_final_kernel<<<1, 32, 0, s>>>(partials, RBLOCKS, Ba, Bn, ld, n, out, fail_flag);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_reduce_loglik(const double* L, long long ld, int n, double* partials,
-                                 double* out, const int* fail_flag, cudaStream_t s) {
-  reduce_eval_kernel<<<RBLOCKS, RTHREADS, 0, s>>>(L, nullptr, nullptr, ld, n, partials,
-                                                  fail_flag);
-  reduce_final_kernel<<<1, 32, 0, s>>>(partials, RBLOCKS, nullptr, nullptr, ld, n, out,
-                                        fail_flag);
-  return cudaGetLastError();
-}
-
-__global__ void clear_upper_kernel(double* a, long long ld, int n) {
-  const int j = blockIdx.x;
-  for (int i = threadIdx.x; i < j && i < n; i += blockDim.x) a[i + (long long)j * ld] = 0.0;
-}
-
-cudaError_t launch_clear_upper(double* a, long long ld, int n, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  clear_upper_kernel<<<n, 256, 0, s>>>(a, ld, n);
+cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {
+  reduce_kernel<<<dim3(RBLOCKS, items), RTHREADS, 0, s>>>(r);
+  reduce_final_kernel<<<items, 32, 0, s>>>(r);
   return cudaGetLastError();
 }
 

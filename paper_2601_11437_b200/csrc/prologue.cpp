@@ -122,6 +122,19 @@ void fill_ladder(double order, KLadder* L) {
   L->gam1 = (double)temme_gam1(m);
   L->gam2 = (double)(0.5L * (gp + gm));
   L->fact = (double)temme_fact(m);
+  L->t_rim[0] = L->t_rip[0] = L->t_rid[0] = 0.0;
+  for (int i = 1; i <= MLE_TEMME_MAX; ++i) {
+    const long double il = (long double)i;
+    L->t_rim[i] = (double)(1.0L / (il - m));
+    L->t_rip[i] = (double)(1.0L / (il + m));
+    L->t_rid[i] = (double)(1.0L / (il * il - m * m));
+  }
+  const long double a1 = 0.25L - m * m;
+  L->cf_ra[0] = L->cf_ra[1] = 0.0;
+  for (int i = 2; i <= MLE_CF2_MAX; ++i) {
+    const long double il = (long double)i;
+    L->cf_ra[i] = (double)(1.0L / (-a1 - il * (il - 1.0L)));
+  }
 }
 
 bool near_integer(double v) {  // bessel.py:117-118  (|nu - round(nu)| <= 1e-6)
@@ -156,6 +169,8 @@ int mle_fill_theta(const double theta[3], double nugget, ThetaParams* P) {
   fill_ladder(nu, &P->kmain);
   P->nu_fd = nu + MLE_FD_LAG;                                    // bessel.py:322
   fill_ladder(P->nu_fd, &P->kfd);
+  P->recip_int[0] = 0.0;
+  for (int i = 1; i <= MLE_CF2_MAX; ++i) P->recip_int[i] = 1.0 / (double)i;
   P->fd_small = near_integer(nu) ? 1 : 0;                        // bessel.py:361-363
   P->fd_large = near_half_integer(nu) ? 1 : 0;                   // bessel.py:364-366
   P->two_nu = 2.0 * nu;

@@ -25,8 +25,8 @@ __constant__ double c_du_coef[(MLE_CASE3_NEAR + 1) * MLE_U_COEFF_STRIDE];
 #define MLE_SQRT_HALF_PI 1.2533141373155003  // sqrt(pi/2), bessel.py:58
 
 // K_mu(x), K_{mu+1}(x) for |mu| <= 1/2, x > 0.
-__device__ __forceinline__ void bessel_k_pair(const KLadder& L, double x, double* k_mu,
-                                              double* k_mu1) {
+__device__ __forceinline__ void bessel_k_pair(const KLadder& L, const double* ri, double x,
+                                              double* k_mu, double* k_mu1) {
   const double mu = L.mu;
   if (x < 2.0) {
     // Temme: K_mu = sum_k c_k f_k,  K_{mu+1} = (2/x) sum_k c_k (p_k - k f_k),
@@ -49,14 +49,13 @@ __device__ __forceinline__ void bessel_k_pair(const KLadder& L, double x, double
     double c = 1.0;
     const double d = x2 * x2;
     double sum1 = p;
-    const double mu2 = mu * mu;
 #pragma unroll 1
-    for (int i = 1; i < 64; ++i) {
+    for (int i = 1; i <= MLE_TEMME_MAX; ++i) {
       const double di = (double)i;
-      ff = (di * ff + p + q) / (di * di - mu2);
-      c *= d / di;
-      p /= (di - mu);
-      q /= (di + mu);
+      ff = (di * ff + p + q) * L.t_rid[i];
+      c *= d * ri[i];
+      p *= L.t_rim[i];
+      q *= L.t_rip[i];
       const double del = c * ff;
       sum += del;
       const double del1 = c * (p - di * ff);
@@ -76,11 +75,11 @@ __device__ __forceinline__ void bessel_k_pair(const KLadder& L, double x, double
     double a = -a1;
     double s = 1.0 + q * delh;
 #pragma unroll 1
-    for (int i = 2; i < 200; ++i) {
+    for (int i = 2; i <= MLE_CF2_MAX; ++i) {
       const double di = (double)i;
       a -= 2.0 * (di - 1.0);
-      c = -a * c / di;
-      const double qnew = (q1 - b * q2) / a;
+      c = -a * c * ri[i];
+      const double qnew = (q1 - b * q2) * L.cf_ra[i];
       q1 = q2;
       q2 = qnew;
       q += c * qnew;
@@ -100,10 +99,10 @@ __device__ __forceinline__ void bessel_k_pair(const KLadder& L, double x, double
 }
 
 // Runs the ladder: returns K_order (and K_{order-1} if wanted) for the ladder's order.
-__device__ __forceinline__ void bessel_k_ladder(const KLadder& L, double x, double* k_nu,
-                                                double* k_num1) {
+__device__ __forceinline__ void bessel_k_ladder(const KLadder& L, const double* ri, double x,
+                                                double* k_nu, double* k_num1) {
   double k0, k1;
-  bessel_k_pair(L, x, &k0, &k1);
+  bessel_k_pair(L, ri, x, &k0, &k1);
   const double two_over_x = 2.0 / x;
 #pragma unroll 1
   for (int j = 1; j <= L.nsteps; ++j) {
@@ -129,9 +128,9 @@ __device__ __forceinline__ double polyval_const(const double* c, int ncoef, doub
 }
 
 // Case 2: 0 < x < 8.5, nu away from integers (bessel.py:184-223).
-__device__ __forceinline__ double dnu_case2(const ThetaParams& P, double x) {
+__device__ __forceinline__ double dnu_case2(const ThetaParams& P, double x, double x_nu) {
   const double two_log_x = 2.0 * log(x);
-  const double x_two_nu = pow(x, P.two_nu);
+  const double x_two_nu = x_nu * x_nu;  // x^(2 nu)
   const double quarter_x2 = 0.25 * x * x;
   const double lead = P.c2_two_m_nu * x_two_nu;
   const double log2 = 0.6931471805599453;
@@ -139,7 +138,7 @@ __device__ __forceinline__ double dnu_case2(const ThetaParams& P, double x) {
   double total = 0.0;
 #pragma unroll 1
   for (int k = 0; k <= MLE_CASE2_TERMS; ++k) {
-    if (k > 0) prefactor = prefactor * quarter_x2 / (double)k;
+    if (k > 0) prefactor = prefactor * quarter_x2 * P.recip_int[k];
     const double term_neg =
         lead * (-log2 + two_log_x - P.c2_psi_neg + P.c2_d_pos[k]) * P.c2_gam_neg * P.c2_g_pos[k];
     total = total + prefactor * (P.c2_term_pos[k] + term_neg);
@@ -148,7 +147,7 @@ __device__ __forceinline__ double dnu_case2(const ThetaParams& P, double x) {
 }
 
 // Case 3: 8.5 <= x < 30 (bessel.py:226-283).
-__device__ __forceinline__ double dnu_case3(const ThetaParams& P, double x) {
+__device__ __forceinline__ double dnu_case3(const ThetaParams& P, double x, double x_nu) {
   const double nu = P.nu;
   const int kterms = (x < MLE_MID_TRUNC_SPLIT) ? MLE_CASE3_NEAR : MLE_CASE3_FAR;
   const double z = x / nu;
@@ -156,7 +155,7 @@ __device__ __forceinline__ double dnu_case3(const ThetaParams& P, double x) {
   const double root = sqrt(zz1);
   const double p = 1.0 / root;
   const double eta = root + log(z / (1.0 + root));
-  const double prefactor = pow(x, nu) * P.c3_sqrt_pi_2nu * exp(-nu * eta) / sqrt(root);
+  const double prefactor = x_nu * P.c3_sqrt_pi_2nu * exp(-nu * eta) / sqrt(root);
   double sum_u = 0.0, sum_ku = 0.0, sum_du = 0.0;
 #pragma unroll 1
   for (int k = 0; k <= kterms; ++k) {
@@ -169,11 +168,11 @@ __device__ __forceinline__ double dnu_case3(const ThetaParams& P, double x) {
   }
   const double bracket = P.c3_log_nu + log(1.0 + root) - 1.0 / (2.0 * nu * zz1);
   return bracket * prefactor * sum_u - prefactor * sum_ku +
-         (x * x / P.c3_nu3) * pow(zz1, -1.5) * prefactor * sum_du;
+         (x * x / P.c3_nu3) / (zz1 * root) * prefactor * sum_du;  // (1+z^2)^-1.5
 }
 
 // Case 4: x >= 30 (bessel.py:286-318).
-__device__ __forceinline__ double dnu_case4(const ThetaParams& P, double x) {
+__device__ __forceinline__ double dnu_case4(const ThetaParams& P, double x, double x_nu) {
   const double log_x = log(x);
   double total = log_x;
   double x_pow = 1.0;
@@ -182,25 +181,27 @@ __device__ __forceinline__ double dnu_case4(const ThetaParams& P, double x) {
     x_pow = x_pow / x;
     total = total + x_pow * (log_x + P.c4_b[k]) * P.c4_a[k];
   }
-  return MLE_SQRT_HALF_PI * pow(x, P.nu_m_half) * exp(-x) * total;
+  return MLE_SQRT_HALF_PI * (x_nu / sqrt(x)) * exp(-x) * total;  // x^(nu - 1/2)
 }
 
 // Forward difference (bessel.py:321-324); f_lo = x^nu K_nu(x) is shared with the caller.
 __device__ __forceinline__ double dnu_fd(const ThetaParams& P, double x, double f_lo) {
   double k_hi, unused;
-  bessel_k_ladder(P.kfd, x, &k_hi, &unused);
+  bessel_k_ladder(P.kfd, P.recip_int, x, &k_hi, &unused);
   const double f_hi = pow(x, P.nu_fd) * k_hi;
   return (f_hi - f_lo) / MLE_FD_LAG;
 }
 
 // d/dnu [x^nu K_nu(x)] for x > 0 with the regime dispatch of bessel.py:327-370.
-__device__ __forceinline__ double dnu_xnu_knu(const ThetaParams& P, double x, double f) {
+// f = x^nu K_nu(x) and x_nu = x^nu are shared with the caller.
+__device__ __forceinline__ double dnu_xnu_knu(const ThetaParams& P, double x, double f,
+                                              double x_nu) {
   if (x < MLE_SMALL_MID_SPLIT) {
-    return P.fd_small ? dnu_fd(P, x, f) : dnu_case2(P, x);
+    return P.fd_small ? dnu_fd(P, x, f) : dnu_case2(P, x, x_nu);
   } else if (x < MLE_MID_LARGE_SPLIT) {
-    return dnu_case3(P, x);
+    return dnu_case3(P, x, x_nu);
   } else {
-    return P.fd_large ? dnu_fd(P, x, f) : dnu_case4(P, x);
+    return P.fd_large ? dnu_fd(P, x, f) : dnu_case4(P, x, x_nu);
   }
 }
 
@@ -214,13 +215,13 @@ __device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, doub
   MaternVals out;
   const double u = h / P.alpha;
   double k_nu, k_num1;
-  bessel_k_ladder(P.kmain, u, &k_nu, &k_num1);
+  bessel_k_ladder(P.kmain, P.recip_int, u, &k_nu, &k_num1);
   const double u_nu = pow(u, P.nu);
   out.c = P.scale_c * u_nu * k_nu;                                  // matern.py:104
   if (kDerivs) {
-    out.dalpha = P.scale_a * pow(u, P.nu + 1.0) * k_num1;           // matern.py:111
+    out.dalpha = P.scale_a * (u_nu * u) * k_num1;                   // matern.py:111
     const double f = u_nu * k_nu;                                   // matern.py:122
-    out.dnu = P.sigma2 * P.q * (P.dlog_q * f + dnu_xnu_knu(P, u, f));  // matern.py:125
+    out.dnu = P.sigma2 * P.q * (P.dlog_q * f + dnu_xnu_knu(P, u, f, u_nu));  // matern.py:125
   } else {
     out.dalpha = 0.0;
     out.dnu = 0.0;

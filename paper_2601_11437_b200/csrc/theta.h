@@ -21,8 +21,13 @@
 #define MLE_MID_TRUNC_SPLIT 15.0 // bessel.py:48
 #define MLE_FD_LAG 1e-9          // bessel.py:50
 
-// Parameters of one K-ladder: K_mu, K_{mu+1} by Temme's series (x <= 2) or Steed's
-// continued fraction (x > 2), |mu| <= 1/2, then `nsteps` upward recurrences.
+#define MLE_TEMME_MAX 40  // Temme series terms (x < 2 converges in < 30)
+#define MLE_CF2_MAX 128   // Steed CF2 iterations (x >= 2 converges in < 80)
+
+// Parameters of one K-ladder: K_mu, K_{mu+1} by Temme's series (x < 2) or Steed's
+// continued fraction (x >= 2), |mu| <= 1/2, then `nsteps` upward recurrences.  The
+// mu-only denominators of both iterations are tabulated once per theta so the per-pair
+// loops multiply instead of divide (CF2 keeps only its one data-dependent division).
 struct KLadder {
   double mu;
   double gam1, gam2;     // (1/G(1-mu) - 1/G(1+mu)) / (2 mu),  (1/G(1-mu) + 1/G(1+mu)) / 2
@@ -30,6 +35,10 @@ struct KLadder {
   double fact;           // pi mu / sin(pi mu)
   int nsteps;            // upward recurrence steps applied to (K_mu, K_{mu+1})
   int order_is_low;      // 1: K_nu is the lower member of the final pair (nu < 1/2 case)
+  double t_rim[MLE_TEMME_MAX + 1];  // 1 / (i - mu)
+  double t_rip[MLE_TEMME_MAX + 1];  // 1 / (i + mu)
+  double t_rid[MLE_TEMME_MAX + 1];  // 1 / (i^2 - mu^2)
+  double cf_ra[MLE_CF2_MAX + 1];    // 1 / a_i,  a_i = -(1/4 - mu^2) - i (i - 1)
 };
 
 struct ThetaParams {
@@ -43,6 +52,7 @@ struct ThetaParams {
   int fd_large;     // nu within 1e-6 of a half-integer: x >= 30 uses the FD fallback
   KLadder kmain;    // ladder for K_nu and K_{nu-1}
   KLadder kfd;      // ladder for K_{nu_fd} (only used in FD bands)
+  double recip_int[MLE_CF2_MAX + 1];  // 1 / i
   // ---- case 2 (0 < x < 8.5) ----
   double c2_term_pos[MLE_CASE2_TERMS + 1];  // 2^nu (log2 + psi(nu) - d_k(-nu)) G(nu) g_k(-nu)
   double c2_d_pos[MLE_CASE2_TERMS + 1];     // d_k(nu)

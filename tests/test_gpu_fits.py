@@ -41,23 +41,62 @@ def test_config2_fits(gpu, seed):
     check(*run_fit(gpu, "config2", seed))
 
 
-def test_concurrent_replicas_match_serial(gpu):
-    """The 5 config-2 replicas driven from 5 host threads (one stream each) give the same
-    fits as running them one at a time."""
-    from concurrent.futures import ThreadPoolExecutor
-
+def test_batched_replicas_match_serial_and_golden(gpu):
+    """fit_many runs the config-2 replicas in lock step as batched passes (mle_eval_batch);
+    every fit must be bit-identical to running it alone, and match the reference fits."""
     seeds = [s for s in range(5) if fit_golden("config2", s) is not None]
+    th0 = gpu.MaternParams(0.8, 0.1, 1.0)
+    cfg = gpu.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    data = [gpu.SpatialDataset(*config_data("config2", s)) for s in seeds]
+    serial = [gpu.fisher_bt(d, cfg) for d in data]
+    coords = []
+    batched = gpu.fit_many(data, cfg, coordinator_out=coords)
+    for s, a, b in zip(seeds, serial, batched):
+        np.testing.assert_array_equal(a.theta_hat.as_array(), b.theta_hat.as_array())
+        np.testing.assert_array_equal(a.fisher_at_hat, b.fisher_at_hat)
+        assert a.loglik_at_hat == b.loglik_at_hat
+        assert (a.grad_calls, a.loglik_calls) == (b.grad_calls, b.loglik_calls)
+        check(fit_golden("config2", s), b)
+    assert coords[0].batches < sum(r.loglik_calls for r in batched)
 
-    def one(seed):
-        loc, z = config_data("config2", seed)
-        th0 = gpu.MaternParams(0.8, 0.1, 1.0)
-        r = gpu.fisher_bt(gpu.SpatialDataset(loc, z),
-                          gpu.FisherBTConfig(theta_lower=th0, theta_upper=th0))
-        return r.theta_hat.as_array(), r.grad_calls
 
-    serial = [one(s) for s in seeds]
-    with ThreadPoolExecutor(len(seeds)) as ex:
-        par = list(ex.map(one, seeds))
-    for (a, ga), (b, gb) in zip(serial, par):
-        np.testing.assert_array_equal(a, b)
-        assert ga == gb
+def test_eval_batch_mixed_modes_and_failures(gpu):
+    """One batch mixing eval_all, loglik, an invalid theta and a singular dataset."""
+    loc, z = config_data("config1")
+    d1 = gpu.SpatialDataset(loc, z)
+    d2 = gpu.SpatialDataset(loc, z)
+    bad = gpu.SpatialDataset(np.array([[0.0, 0.0], [0.0, 0.0]] + [[0.5, 0.5]] * 0), np.zeros(2))
+    th = np.array([1.0, 0.1, 0.5])
+    ref_e = gpu.SpatialDataset(loc, z).engine().eval_all(th)
+    ref_l = gpu.SpatialDataset(loc, z).engine().loglik(th)
+    out = gpu.eval_batch([d1.engine(), d2.engine()], [th, th], [2, 1])
+    assert out[0][0] == 0 and out[1][0] == 0
+    assert out[0][2] == ref_e[0]
+    np.testing.assert_array_equal(out[0][4], ref_e[2])
+    assert out[1][2] == ref_l
+    # invalid theta in one slot does not disturb the other
+    out = gpu.eval_batch([d1.engine(), d2.engine()], [th, [1.0, -0.1, 0.5]], [1, 1])
+    assert out[0][0] == 0 and out[1][0] == 2 and out[0][2] == ref_l
+    # a different-size singular dataset is grouped separately and reports its pivot
+    out = gpu.eval_batch([d1.engine(), bad.engine()], [th, th], [2, 1])
+    assert out[0][0] == 0 and out[1][0] == 1 and out[1][1] == 1
+
+
+def test_factor_cache_is_bit_identical(gpu):
+    """eval_all right after loglik at the same theta reuses the resident Cholesky factor
+    (no Sigma regeneration / potrf) and returns exactly the uncached numbers."""
+    loc, z = config_data("config2", 1)
+    th = np.array([0.9, 0.18, 1.45])
+    fresh = gpu.SpatialDataset(loc, z).engine()
+    ll_f, g_f, f_f = fresh.eval_all(th)
+    cached = gpu.SpatialDataset(loc, z).engine()
+    ll_l = cached.loglik(th)
+    ll_c, g_c, f_c = cached.eval_all(th)
+    assert cached.phase_times()["potrf_ms"] < 0.05 * fresh.phase_times()["potrf_ms"]
+    assert ll_l == ll_f == ll_c
+    np.testing.assert_array_equal(g_c, g_f)
+    np.testing.assert_array_equal(f_c, f_f)
+    # a different theta refactors; set_values invalidates the cache
+    cached.set_values(z[::-1].copy())
+    ll_r = cached.loglik(th)
+    assert ll_r != ll_l

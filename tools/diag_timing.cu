@@ -26,7 +26,10 @@ int main() {
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemcpy(a, h.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
     cudaEventRecord(e0);
-    mle::launch_potrf_diag(a, n, 0, -1, linv, flag, idx, 0);
+    mle::DiagArgs d = {};
+    d.a[0] = a; d.linv[0] = linv; d.fail_flag[0] = flag; d.fail_idx[0] = idx;
+    d.n_aug[0] = -1; d.ld = n; d.k0 = 0;
+    mle::launch_potrf_diag(d, 1, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
