@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
 #pragma unroll
       for (int r = 0; r < (BN * BK / 2) / GEMM_THREADS; ++r) {
         const int c = tid + r * GEMM_THREADS;
-        const int nn = c >> 3, k2 = (c & 7) << 1;
+        const int nn = c / (BK / 2), k2 = (c % (BK / 2)) * 2;
         cp_async16(bs + nn * SBK + k2, B + (k0 + k2) + (long long)nn * ldb);
       }
     }
@@ -126,29 +126,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
 
   // Accumulators start from C (beta = 1) so the C read overlaps the pipeline prologue and
   // the epilogue is store-only; alpha = -1 is applied by negating the A fragments.
-  // mma f64 fragment map: c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1).
-  double acc[4][4][4];
+  // Warp tile 64 x 32 = 8 x 4 blocks of m8n8k4 DMMA; fragment map (f64):
+  // a0 = A(g, t), b0 = B(k = t, n = g), c0 = C(g, 2t), c1 = C(g, 2t+1).
+  double acc[8][4][2];
   if (g.beta != 0.0) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
-        const int r = wm * 64 + mi * 16 + gq;
+        const int r = wm * 64 + mi * 8 + gq;
         const int c = wn * 32 + ni * 8 + 2 * tq;
         const double* p0 = C + r + (long long)c * ldc;
-        const double* p1 = p0 + ldc;
         acc[mi][ni][0] = p0[0];
-        acc[mi][ni][1] = p1[0];
-        acc[mi][ni][2] = p0[8];
-        acc[mi][ni][3] = p1[8];
+        acc[mi][ni][1] = p0[ldc];
       }
   } else {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[mi][ni][e] = 0.0;
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
   }
   const unsigned neg = g.alpha < 0.0 ? 0x80000000u : 0u;
 
@@ -163,52 +159,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
     const double* as = As + (kt % STAGES) * A_STAGE;
     const double* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 8) {
-      double af[4][4], bf[4][2];
+    for (int kk = 0; kk < BK; kk += 4) {
+      // k-outer ordering: 32 independent DMMAs per k4 step keep the tensor pipe fed
+      double af[8], bf[4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int r0 = wm * 64 + mi * 16 + gq;
-        af[mi][0] = as[(kk + tq) * SA + r0];
-        af[mi][1] = as[(kk + tq) * SA + r0 + 8];
-        af[mi][2] = as[(kk + tq + 4) * SA + r0];
-        af[mi][3] = as[(kk + tq + 4) * SA + r0 + 8];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)  // sign flip on the integer pipe (alpha = -1)
-          af[mi][e] = __hiloint2double(__double2hiint(af[mi][e]) ^ (int)neg,
-                                       __double2loint(af[mi][e]));
+      for (int mi = 0; mi < 8; ++mi) {
+        const double v = as[(kk + tq) * SA + wm * 64 + mi * 8 + gq];
+        af[mi] = __hiloint2double(__double2hiint(v) ^ (int)neg, __double2loint(v));
       }
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
         const int c0 = wn * 32 + ni * 8 + gq;
-        if (kBL == kBNK) {
-          bf[ni][0] = bs[(kk + tq) * SBN + c0];
-          bf[ni][1] = bs[(kk + tq + 4) * SBN + c0];
-        } else {
-          bf[ni][0] = bs[c0 * SBK + kk + tq];
-          bf[ni][1] = bs[c0 * SBK + kk + tq + 4];
-        }
+        bf[ni] = (kBL == kBNK) ? bs[(kk + tq) * SBN + c0] : bs[c0 * SBK + kk + tq];
       }
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma_16x8x8(acc[mi][ni], af[mi], bf[ni]);
+        for (int ni = 0; ni < 4; ++ni)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+              : "d"(af[mi]), "d"(bf[ni]));
     }
   }
   cp_async_wait<0>();
 
   // epilogue: store-only
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
+  for (int mi = 0; mi < 8; ++mi) {
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
-      const int r = wm * 64 + mi * 16 + gq;
+      const int r = wm * 64 + mi * 8 + gq;
       const int c = wn * 32 + ni * 8 + 2 * tq;
       double* p0 = C + r + (long long)c * ldc;
-      double* p1 = p0 + ldc;
       p0[0] = acc[mi][ni][0];
-      p1[0] = acc[mi][ni][1];
-      p0[8] = acc[mi][ni][2];
-      p1[8] = acc[mi][ni][3];
+      p0[ldc] = acc[mi][ni][1];
     }
   }
 }
