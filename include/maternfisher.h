@@ -102,6 +102,15 @@ int mle_eval_all(mle_ctx* ctx, const double theta[3], double* loglik, double gra
 int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const int* modes,
                    double* results, int64_t* pivots, int* rcs);
 
+/*
+ * One exact draw z = L w from N(0, Sigma(theta)) on the context's locations, with w the
+ * caller's n standard normals: the device factorization followed by a device L w
+ * (replaces simulate_grf, pkg/src/maternmle/simulate.py:100-106, whose `lower @ normals`
+ * cannot run on a host at n >= 65,536).  The factor stays cached for theta.
+ */
+int mle_simulate(mle_ctx* ctx, const double theta[3], const double* w, double* z_out,
+                 int64_t* bad_pivot);
+
 /* Write one full n x n matrix (row-major == column-major, symmetric) to host memory. */
 int mle_build(mle_ctx* ctx, const double theta[3], int which, double* out_host);
 

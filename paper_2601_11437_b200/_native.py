@@ -29,7 +29,7 @@ EXPORTED = (
     "mle_version", "mle_last_error", "mle_device_count", "mle_ctx_create", "mle_ctx_destroy",
     "mle_ctx_n", "mle_ctx_set_values", "mle_loglik", "mle_eval_all", "mle_build",
     "mle_phase_times", "mle_cholesky", "mle_bessel_k", "mle_dnu_xnu_knu", "mle_matern_elem",
-    "mle_eval_batch",
+    "mle_eval_batch", "mle_simulate",
 )
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -59,6 +59,7 @@ def _load():
         "mle_eval_batch": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, _dp,
                                           ctypes.POINTER(ctypes.c_int), _dp, _i64p,
                                           ctypes.POINTER(ctypes.c_int)]),
+        "mle_simulate": (ctypes.c_int, [_vp, _dp, _dp, _dp, _i64p]),
         "mle_phase_times": (ctypes.c_int, [_vp, _dp]),
         "mle_cholesky": (ctypes.c_int, [_dp, ctypes.c_int64, ctypes.c_int, _dp, _i64p]),
         "mle_bessel_k": (ctypes.c_int, [ctypes.c_double, _dp, ctypes.c_int64, ctypes.c_int, _dp]),

@@ -716,6 +716,32 @@ int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const 
   return MLE_OK;
 }
 
+int mle_simulate(mle_ctx* c, const double theta[3], const double* w, double* z_out,
+                 int64_t* bad_pivot) {
+  if (!c || !w || !z_out) return fail(MLE_INVALID, "null argument");
+  int rc = check_finite(w, c->n, "normals");
+  if (rc) return rc;
+  double res[kResults];
+  rc = single(c, theta, 1, res, bad_pivot);  // factor Sigma(theta) (cached afterwards)
+  if (rc) return rc;
+  double *dw = nullptr, *dz = nullptr;
+  struct G {
+    double** a;
+    double** b;
+    ~G() {
+      cudaFree(*a);
+      cudaFree(*b);
+    }
+  } guard{&dw, &dz};
+  CUDA_TRY(cudaMalloc(&dw, sizeof(double) * c->n));
+  CUDA_TRY(cudaMalloc(&dz, sizeof(double) * c->n));
+  CUDA_TRY(cudaMemcpyAsync(dw, w, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_trmv_lower(c->sigma, c->N, (int)c->n, dw, dz, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(z_out, dz, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return MLE_OK;
+}
+
 int mle_build(mle_ctx* c, const double theta[3], int which, double* out_host) {
   if (!c || !out_host) return fail(MLE_INVALID, "null argument");
   if (which < MLE_WHICH_SIGMA || which > MLE_WHICH_NU)

@@ -91,6 +91,10 @@ cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s);
 // Reductions: per item 9 results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>, yBy_A, yBy_N].
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
 
+// z = L w over the leading n x n block of a resident Cholesky factor.
+cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double* w, double* z,
+                              cudaStream_t s);
+
 constexpr int kReduceBlocks = 148 * 4;
 constexpr int kReduceSums = 7;
 

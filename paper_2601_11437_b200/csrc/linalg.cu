@@ -583,3 +583,25 @@ cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {
 }
 
 }  // namespace mle
+
+namespace mle {
+
+// z = L[0:n, 0:n] w for a resident Cholesky factor (column-major, lower): the GPU half of
+// the reference's simulate_grf (simulate.py:104-106, `lower @ normals`).  Thread per row;
+// for every column the warp reads consecutive rows (coalesced).
+__global__ void trmv_lower_kernel(const double* __restrict__ L, long long ld, int n,
+                                  const double* __restrict__ w, double* __restrict__ z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int j = 0; j <= i; ++j) acc = fma(L[i + (long long)j * ld], w[j], acc);
+  z[i] = acc;
+}
+
+cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double* w, double* z,
+                              cudaStream_t s) {
+  trmv_lower_kernel<<<(n + 255) / 256, 256, 0, s>>>(L, ld, n, w, z);
+  return cudaGetLastError();
+}
+
+}  // namespace mle

@@ -67,15 +67,15 @@ def gmm_locations(n: int, seed: int, components: int = 8,
 def simulate_field(locations, theta, seed: int, device: int = 0) -> np.ndarray:
     """One exact draw z = L w from N(0, Sigma(theta)) computed on the GPU
     (reference ``simulate_grf``, simulate.py:100-106)."""
-    from .matern import MaternParams, SpatialDataset, build_cov_matrix
-    from .likelihood import cholesky_lower
+    from .matern import MaternParams, SpatialDataset
 
     locations = np.asarray(locations, dtype=float)
     theta = theta if isinstance(theta, MaternParams) else MaternParams.from_array(theta)
     holder = SpatialDataset(locations, np.zeros(locations.shape[0]), device=device)
-    lower = cholesky_lower(build_cov_matrix(holder, theta), device=device)
     normals = np.random.default_rng(seed).standard_normal(locations.shape[0])
-    return lower @ normals
+    z = holder.engine().simulate(theta.as_array(), normals)
+    holder.release()
+    return z
 
 
 @dataclass(frozen=True)

@@ -81,6 +81,20 @@ class Engine:
         nat.check(rc, piv.value)
         return float(ll[0]), grad, fisher.reshape(3, 3)
 
+    def simulate(self, theta, normals) -> np.ndarray:
+        """z = L w with L the device Cholesky factor of Sigma(theta) (simulate.py:100-106)."""
+        th = self._theta(theta)
+        w = np.ascontiguousarray(np.asarray(normals, dtype=np.float64))
+        if w.shape != (self.n,):
+            raise ValueError("normals must have length n")
+        z = np.empty(self.n)
+        piv = ctypes.c_int64(-1)
+        with self._lock:
+            rc = nat.lib.mle_simulate(self._ctx, nat.as_ptr(th), nat.as_ptr(w), nat.as_ptr(z),
+                                      ctypes.byref(piv))
+        nat.check(rc, piv.value)
+        return z
+
     def build(self, theta, which: str) -> np.ndarray:
         if which not in nat.WHICH:
             raise ValueError(f"which must be one of {sorted(nat.WHICH)}, got {which!r}")

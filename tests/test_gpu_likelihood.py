@@ -193,3 +193,10 @@ def test_sigma2_scaling_identity_large(gpu):
     assert got == pytest.approx(pred, rel=1e-11)
     assert gpu.log_likelihood(data, th) == ev.loglik
     assert np.all(np.linalg.eigvalsh(ev.fisher) > 0)
+
+
+def test_simulate_field_matches_reference_simulation(gpu):
+    """z = L w on the GPU (simulate.py:100-106) reproduces the reference's config-1 field."""
+    loc, z = config_data("config1")
+    z_gpu = gpu.simulate_field(loc, (1.0, 0.1, 0.5), 0)
+    np.testing.assert_allclose(z_gpu, z, rtol=0, atol=1e-12 * np.max(np.abs(z)))
