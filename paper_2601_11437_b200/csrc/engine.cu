@@ -43,6 +43,7 @@ std::vector<int> g_device_ready;
 const double kLog2Pi = 1.8378770664093453;  // log(2 pi), likelihood.py:38
 constexpr int kOuter = 4;                   // outer block = 4 x 128 columns
 constexpr int kResults = 13;                // loglik, grad[3], fisher[9]
+constexpr int kPoolEvents = 16;             // cross-stream join events per context
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -87,7 +88,10 @@ struct mle_ctx {
   long long N = 0;   // padded extent (multiple of kNB), >= n + 1
   int Nt = 0;        // N / kNB
   double nugget = 0.0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // main stream (every call is serialised on it)
+  cudaStream_t side = nullptr;    // look-ahead bulk trailing updates
+  cudaStream_t aux = nullptr;     // derivative generation concurrent with the Cholesky
+  cudaEvent_t pool[kPoolEvents] = {};
   double* lx = nullptr;
   double* ly = nullptr;
   double* z = nullptr;
@@ -143,16 +147,39 @@ GemmArgs gemm_base() {
   return g;
 }
 
-// Launch sequences over a list of contexts (all with the same N / Nt) on one stream.
+// Launch sequences over a list of contexts (all with the same N / Nt).
+//
+// Look-ahead: every sweep (Cholesky, forward solve, right solve) is a chain of latency-bound
+// inner steps per outer block of kOuter tiles, followed by a large trailing GEMM.  The
+// trailing GEMM of block b is split into
+//   (i)  the part the next block's inner chain reads (its kOuter tiles)  -> main stream s
+//   (ii) everything beyond                                               -> side stream s2
+// so the inner chain of block b+1 runs on `s` while (ii) of block b runs on `s2`.  (i) of
+// block b+1 touches tiles (ii) of block b also updates, so `s` waits for (ii)(b) first.
 struct Launcher {
-  cudaStream_t s;
+  cudaStream_t s;              // main: inner chains
+  cudaStream_t s2 = nullptr;   // side: bulk trailing updates (null: everything on s)
+  cudaEvent_t* pool = nullptr; // event pool for cross-stream joins
+  int npool = 0;
+  int next = 0;
   double launches = 0.0;
 
-  int gemm(const GemmArgs& g, BLayout bl, int batch) {
+  int gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t st) {
     launches += 1;
-    CUDA_TRY(launch_gemm(g, bl, batch, s));
+    CUDA_TRY(launch_gemm(g, bl, batch, st));
     return MLE_OK;
   }
+  int gemm(const GemmArgs& g, BLayout bl, int batch) { return gemm(g, bl, batch, s); }
+
+  // `to` waits for all work enqueued so far on `from`.
+  int join(cudaStream_t from, cudaStream_t to) {
+    if (from == to || from == nullptr || to == nullptr) return MLE_OK;
+    cudaEvent_t e = pool[next++ % npool];
+    CUDA_TRY(cudaEventRecord(e, from));
+    CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
+    return MLE_OK;
+  }
+  cudaStream_t bulk() const { return s2 ? s2 : s; }
 
   // Two-level right-looking blocked Cholesky of every item's matrix (ld = N).
   int potrf(mle_ctx* const* cs, double* const* mats, const long long* n_aug, int m) {
@@ -206,11 +233,12 @@ struct Launcher {
           if ((rc = gemm(t, kBNK, m))) return rc;
         }
       }
-      const int rem = Nt - b1;
-      if (rem <= 0) continue;
-      // outer trailing update: A_TT -= P P^T with P = L[T, b0:b1], K = (b1 - b0) * 128
-      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
-      GemmArgs t = gemm_base();
+      if (b1 >= Nt) continue;
+      // trailing update with P = L[T, b0:b1], K = (b1 - b0) * 128
+      const int b2 = std::min(Nt, b1 + kOuter);
+      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
+      if ((rc = join(s2, s))) return rc;  // (ii) of the previous block touched these tiles
+      GemmArgs t = gemm_base();           // (i): columns [b1, b2), rows >= b1
       for (int b = 0; b < m; ++b) {
         t.A[b] = mats[b] + t0 + c0 * ld;
         t.B[b] = mats[b] + t0 + c0 * ld;
@@ -219,10 +247,23 @@ struct Launcher {
       }
       t.lda = ld; t.ldb = ld; t.ldc = ld;
       t.K = (b1 - b0) * kNB;
-      t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
+      t.tiles_m = Nt - b1; t.tiles_n = b2 - b1; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
       if ((rc = gemm(t, kBNK, m))) return rc;
+      if (b2 >= Nt) continue;
+      if ((rc = join(s, s2))) return rc;
+      GemmArgs u = gemm_base();           // (ii): lower tiles of [b2, Nt)
+      for (int b = 0; b < m; ++b) {
+        u.A[b] = mats[b] + u0 + c0 * ld;
+        u.B[b] = mats[b] + u0 + c0 * ld;
+        u.C[b] = mats[b] + u0 + u0 * ld;
+        u.fail_flag[b] = cs[b]->fail_flag;
+      }
+      u.lda = ld; u.ldb = ld; u.ldc = ld;
+      u.K = (b1 - b0) * kNB;
+      u.tiles_m = Nt - b2; u.lower = 1; u.alpha = -1.0; u.beta = 1.0;
+      if ((rc = gemm(u, kBNK, m, bulk()))) return rc;
     }
-    return MLE_OK;
+    return join(s2, s);
   }
 
   // B_i = L^-1 S_i L^-T (lower half) for both derivative matrices of every item, in place.
@@ -267,21 +308,36 @@ struct Launcher {
           if ((rc = gemm(t, kBKN, zb))) return rc;
         }
       }
-      const int rem = Nt - b1;
-      if (rem <= 0) continue;
-      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
-      GemmArgs t = gemm_base();
+      if (b1 >= Nt) continue;
+      const int b2 = std::min(Nt, b1 + kOuter);
+      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
+      if ((rc = join(s2, s))) return rc;
+      GemmArgs t = gemm_base();   // (i): rows [b1, b2), all columns
       for (int z = 0; z < zb; ++z) {
-        t.A[z] = L(z) + t0 + c0 * ld;   // L[T, b0:b1]
+        t.A[z] = L(z) + t0 + c0 * ld;   // L[b1:b2, b0:b1]
         t.B[z] = S(z) + c0;             // X[b0:b1, :] (kBKN)
         t.C[z] = S(z) + t0;
         t.fail_flag[z] = flag(z);
       }
       t.lda = ld; t.ldb = ld; t.ldc = ld;
       t.K = (b1 - b0) * kNB;
-      t.tiles_m = rem; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
+      t.tiles_m = b2 - b1; t.tiles_n = Nt; t.alpha = -1.0; t.beta = 1.0;
       if ((rc = gemm(t, kBKN, zb))) return rc;
+      if (b2 >= Nt) continue;
+      if ((rc = join(s, s2))) return rc;
+      GemmArgs u = gemm_base();   // (ii): rows >= b2
+      for (int z = 0; z < zb; ++z) {
+        u.A[z] = L(z) + u0 + c0 * ld;
+        u.B[z] = S(z) + c0;
+        u.C[z] = S(z) + u0;
+        u.fail_flag[z] = flag(z);
+      }
+      u.lda = ld; u.ldb = ld; u.ldc = ld;
+      u.K = (b1 - b0) * kNB;
+      u.tiles_m = Nt - b2; u.tiles_n = Nt; u.alpha = -1.0; u.beta = 1.0;
+      if ((rc = gemm(u, kBKN, zb, bulk()))) return rc;
     }
+    if ((rc = join(s2, s))) return rc;
     // right sweep on lower tiles: B[j:, j] = X[j:, j] Linv_j^T ; X[T,T] -= B[T,j] L[T,j]^T
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
       const int b1 = std::min(Nt, b0 + kOuter);
@@ -311,22 +367,36 @@ struct Launcher {
           if ((rc = gemm(t, kBNK, zb))) return rc;
         }
       }
-      const int rem = Nt - b1;
-      if (rem <= 0) continue;
-      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
-      GemmArgs t = gemm_base();
+      if (b1 >= Nt) continue;
+      const int b2 = std::min(Nt, b1 + kOuter);
+      const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
+      if ((rc = join(s2, s))) return rc;
+      GemmArgs t = gemm_base();   // (i): columns [b1, b2), rows >= b1
       for (int z = 0; z < zb; ++z) {
         t.A[z] = S(z) + t0 + c0 * ld;   // B[T, b0:b1]
-        t.B[z] = L(z) + t0 + c0 * ld;   // L[T, b0:b1]
+        t.B[z] = L(z) + t0 + c0 * ld;   // L[b1:b2, b0:b1]
         t.C[z] = S(z) + t0 + t0 * ld;
         t.fail_flag[z] = flag(z);
       }
       t.lda = ld; t.ldb = ld; t.ldc = ld;
       t.K = (b1 - b0) * kNB;
-      t.tiles_m = rem; t.lower = 1; t.alpha = -1.0; t.beta = 1.0;
+      t.tiles_m = Nt - b1; t.tiles_n = b2 - b1; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
       if ((rc = gemm(t, kBNK, zb))) return rc;
+      if (b2 >= Nt) continue;
+      if ((rc = join(s, s2))) return rc;
+      GemmArgs u = gemm_base();   // (ii): lower tiles of [b2, Nt)
+      for (int z = 0; z < zb; ++z) {
+        u.A[z] = S(z) + u0 + c0 * ld;
+        u.B[z] = L(z) + u0 + c0 * ld;
+        u.C[z] = S(z) + u0 + u0 * ld;
+        u.fail_flag[z] = flag(z);
+      }
+      u.lda = ld; u.ldb = ld; u.ldc = ld;
+      u.K = (b1 - b0) * kNB;
+      u.tiles_m = Nt - b2; u.lower = 1; u.alpha = -1.0; u.beta = 1.0;
+      if ((rc = gemm(u, kBNK, zb, bulk()))) return rc;
     }
-    return MLE_OK;
+    return join(s2, s);
   }
 };
 
@@ -334,7 +404,7 @@ struct Launcher {
 int run_chunk(Item* items, int m) {
   mle_ctx* lead = items[0].c;
   cudaStream_t s = lead->stream;
-  Launcher run{s};
+  Launcher run{s, lead->side, lead->pool, kPoolEvents};
   for (int b = 0; b < m; ++b) {
     Item& it = items[b];
     int rc = ensure_matrices(it.c, it.derivs);
@@ -345,31 +415,44 @@ int run_chunk(Item* items, int m) {
     CUDA_TRY(cudaMemsetAsync(it.c->fail_flag, 0, sizeof(int), s));
   }
   CUDA_TRY(cudaEventRecord(lead->ev[0], s));
-  // generation for items that need Sigma and/or the derivative matrices
-  GenArgs ga;
-  std::memset(&ga, 0, sizeof(ga));
-  int ng = 0;
-  for (int b = 0; b < m; ++b) {
-    const Item& it = items[b];
-    if (!it.factor && !it.derivs) continue;
-    GenItem& gi = ga.item[ng++];
-    gi.P = it.c->d_theta;
-    gi.lx = it.c->lx;
-    gi.ly = it.c->ly;
-    gi.z = it.c->z;
-    gi.sigma = it.c->sigma;
-    gi.dalpha = it.c->sa;
-    gi.dnu = it.c->sn;
-    gi.fail_flag = it.c->fail_flag;
-    gi.write_sigma = it.factor ? 1 : 0;
-    gi.write_derivs = it.derivs ? 1 : 0;
-  }
-  ga.ld = lead->N;
-  ga.rows = lead->N;
-  ga.n = (int)lead->n;
-  if (ng > 0) {
+  // Generation.  Sigma (items that factor) on the main stream; the derivative matrices on
+  // the aux stream, concurrently with the Cholesky (they are only needed by the solves).
+  auto gen_set = [&](bool sigma_pass) {
+    GenArgs ga;
+    std::memset(&ga, 0, sizeof(ga));
+    int ng = 0;
+    for (int b = 0; b < m; ++b) {
+      const Item& it = items[b];
+      if (sigma_pass ? !it.factor : !it.derivs) continue;
+      GenItem& gi = ga.item[ng++];
+      gi.P = it.c->d_theta;
+      gi.lx = it.c->lx;
+      gi.ly = it.c->ly;
+      gi.z = it.c->z;
+      gi.sigma = it.c->sigma;
+      gi.dalpha = it.c->sa;
+      gi.dnu = it.c->sn;
+      gi.fail_flag = it.c->fail_flag;
+      gi.write_sigma = sigma_pass ? 1 : 0;
+      gi.write_derivs = sigma_pass ? 0 : 1;
+    }
+    ga.ld = lead->N;
+    ga.rows = lead->N;
+    ga.n = (int)lead->n;
+    return std::make_pair(ga, ng);
+  };
+  auto sig = gen_set(true);
+  if (sig.second > 0) {
     run.launches += 1;
-    launch_gen_engine(ga, ng, s);
+    launch_gen_engine(sig.first, sig.second, s);
+    CUDA_TRY(cudaGetLastError());
+  }
+  auto der = gen_set(false);
+  if (der.second > 0) {
+    int rc = run.join(s, lead->aux);
+    if (rc) return rc;
+    run.launches += 1;
+    launch_gen_engine(der.first, der.second, lead->aux);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaEventRecord(lead->ev[1], s));
@@ -392,6 +475,8 @@ int run_chunk(Item* items, int m) {
   }
   CUDA_TRY(cudaEventRecord(lead->ev[2], s));
   {
+    int rc = run.join(lead->aux, s);  // derivative matrices generated
+    if (rc) return rc;
     mle_ctx* cs[kMaxItems];
     int nd = 0;
     for (int b = 0; b < m; ++b)
@@ -588,7 +673,10 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
       return bail(fail(MLE_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
   } while (0)
   CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CTX_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CTX_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
+  for (auto& e : c->pool) CTX_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CTX_TRY(cudaMalloc(&c->lx, sizeof(double) * n));
   CTX_TRY(cudaMalloc(&c->ly, sizeof(double) * n));
   CTX_TRY(cudaMalloc(&c->z, sizeof(double) * n));
@@ -629,6 +717,10 @@ void mle_ctx_destroy(mle_ctx* c) {
   if (c->h_res) cudaFreeHost(c->h_res);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->pool)
+    if (e) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->aux) cudaStreamDestroy(c->aux);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -823,7 +915,7 @@ int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t*
   CUDA_TRY(cudaMemcpyAsync(c.sigma, h.data(), sizeof(double) * (size_t)N * N,
                            cudaMemcpyHostToDevice, c.stream));
   CUDA_TRY(cudaMemsetAsync(c.fail_flag, 0, sizeof(int), c.stream));
-  Launcher run{c.stream};
+  Launcher run{c.stream};  // single stream (no look-ahead) for the standalone factorization
   mle_ctx* cs[1] = {&c};
   double* mats[1] = {c.sigma};
   long long aug[1] = {-1};
