@@ -215,7 +215,7 @@ struct Launcher {
           g.fail_flag[b] = cs[b]->fail_flag;
         }
         g.lda = ld; g.ldb = kNB; g.ldc = ld;
-        g.tiles_m = rem; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
+        g.tiles_m = rem; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
         if ((rc = gemm(g, kBNK, m))) return rc;
         // inner update of the remaining columns of this outer block (lower trapezoid)
         const int wcols = b1 - k - 1;
@@ -351,7 +351,7 @@ struct Launcher {
           g.fail_flag[z] = flag(z);
         }
         g.lda = ld; g.ldb = kNB; g.ldc = ld;
-        g.tiles_m = Nt - j; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0;
+        g.tiles_m = Nt - j; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
         if ((rc = gemm(g, kBNK, zb))) return rc;
         const int wcols = b1 - j - 1;
         if (wcols > 0) {

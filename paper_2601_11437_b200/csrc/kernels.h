@@ -51,6 +51,7 @@ struct GemmArgs {
   int tiles_n;       // number of 128-column tiles of C (full mode)
   int lower;         // 1: only tiles (tm >= tn) of a tiles_m x tiles_m grid
   int trap;          // full mode: 1 skips tiles with tm < tn (lower trapezoid)
+  int wide;          // 1: 128-column CTAs (C aliases A across the 128-wide panel)
   double alpha;      // +1 or -1
   double beta;       // 0 (overwrite) or 1 (accumulate into C)
 };

@@ -21,14 +21,33 @@ namespace mle {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+constexpr int BM = 128, BK = 16, STAGES = 3;
 constexpr int GEMM_THREADS = 256;
 constexpr int SA = BM + 4;   // A smem: [BK][SA], m contiguous (SA = 4 mod 16 -> conflict free)
-constexpr int SBN = BN + 4;  // B (kBNK) smem: [BK][SBN]
 constexpr int SBK = BK + 4;  // B (kBKN) smem: [BN][SBK]
 constexpr int A_STAGE = BK * SA;
-constexpr int B_STAGE_NK = BK * SBN;
-constexpr int B_STAGE_KN = BN * SBK;
+
+// Per CTA-width constants.  kBN = 128: 2 x 4 warps of 64 x 32 (1 CTA / SM, used for the
+// in-place panel products that need the whole 128-column panel in one CTA).  kBN = 64:
+// 4 x 2 warps of 32 x 32 with <= 128 registers, so two CTAs share an SM and one CTA's
+// C preload / store phases overlap the other's DMMA main loop.
+template <int kBN>
+struct Tile {
+  static constexpr int WM_CNT = (kBN == 128) ? 2 : 4;
+  static constexpr int WN_CNT = 8 / WM_CNT;
+  static constexpr int WTM = BM / WM_CNT;  // rows per warp
+  static constexpr int WTN = kBN / WN_CNT; // cols per warp (32)
+  static constexpr int MI = WTM / 8;       // m8 blocks per warp
+  static constexpr int NI = WTN / 8;       // n8 blocks per warp
+  static constexpr int SBN = kBN + 4;      // B (kBNK) smem stride
+  static constexpr int B_STAGE_NK = BK * SBN;
+  static constexpr int B_STAGE_KN = kBN * SBK;
+  static constexpr int MIN_BLOCKS = (kBN == 128) ? 1 : 2;
+  template <int kBL>
+  static constexpr size_t smem_bytes() {
+    return sizeof(double) * STAGES * (A_STAGE + (kBL == kBNK ? B_STAGE_NK : B_STAGE_KN));
+  }
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -49,8 +68,12 @@ __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4]
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
-__device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn) {
-  const int b = blockIdx.x;
+// 128-row tile index tm and 128-column tile index tn128 (+ 64-column half for kBN = 64).
+template <int kBN>
+__device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn, int* half) {
+  const int sub = (kBN == 128) ? 1 : 2;
+  const int b = blockIdx.x / sub;
+  *half = blockIdx.x % sub;
   if (g.lower) {
     int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
     while (I * (I + 1) / 2 > b) --I;
@@ -66,28 +89,30 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn)
 }  // namespace
 
 // C[tm, tn] = alpha * sum_k A(m, k) B(n, k) + beta * C, A(m,k) = A[m + k*lda].
-template <int kBL>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
+template <int kBL, int kBN>
+__global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_kernel(GemmArgs g) {
+  using T = Tile<kBN>;
   const int z = blockIdx.z;
   if (*g.fail_flag[z]) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
-  constexpr int B_STAGE = (kBL == kBNK) ? B_STAGE_NK : B_STAGE_KN;
+  constexpr int B_STAGE = (kBL == kBNK) ? T::B_STAGE_NK : T::B_STAGE_KN;
 
-  int tm, tn;
-  tile_coords(g, &tm, &tn);
+  int tm, tn, half;
+  tile_coords<kBN>(g, &tm, &tn, &half);
   if (g.trap && tm < tn) return;
+  const long long col0 = (long long)tn * 128 + (long long)half * kBN;
   // no __restrict__: panel products run in place (C aliases A or B; see engine.cu)
   const double* A = g.A[z] + (long long)tm * BM;
   const double* Bz = g.B[z];
-  const double* B = (kBL == kBNK) ? Bz + (long long)tn * BN : Bz + (long long)tn * BN * g.ldb;
-  double* C = g.C[z] + (long long)tm * BM + (long long)tn * BN * g.ldc;
+  const double* B = (kBL == kBNK) ? Bz + col0 : Bz + col0 * g.ldb;
+  double* C = g.C[z] + (long long)tm * BM + col0 * g.ldc;
   const long long lda = g.lda, ldb = g.ldb, ldc = g.ldc;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps, warp tile 64 x 32
+  const int wm = warp % T::WM_CNT, wn = warp / T::WM_CNT;
   const int gq = lane >> 2, tq = lane & 3;
 
   auto load_stage = [&](int stage, int kt) {
@@ -100,17 +125,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
       const int k = c >> 6, m2 = (c & 63) << 1;
       cp_async16(as + k * SA + m2, A + m2 + (long long)(k0 + k) * lda);
     }
-    if (kBL == kBNK) {
 #pragma unroll
-      for (int r = 0; r < (BN * BK / 2) / GEMM_THREADS; ++r) {
-        const int c = tid + r * GEMM_THREADS;
-        const int k = c >> 6, n2 = (c & 63) << 1;
-        cp_async16(bs + k * SBN + n2, B + n2 + (long long)(k0 + k) * ldb);
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < (BN * BK / 2) / GEMM_THREADS; ++r) {
-        const int c = tid + r * GEMM_THREADS;
+    for (int r = 0; r < (kBN * BK / 2) / GEMM_THREADS; ++r) {
+      const int c = tid + r * GEMM_THREADS;
+      if (kBL == kBNK) {
+        const int k = c / (kBN / 2), n2 = (c % (kBN / 2)) * 2;
+        cp_async16(bs + k * T::SBN + n2, B + n2 + (long long)(k0 + k) * ldb);
+      } else {
         const int nn = c / (BK / 2), k2 = (c % (BK / 2)) * 2;
         cp_async16(bs + nn * SBK + k2, B + (k0 + k2) + (long long)nn * ldb);
       }
@@ -126,25 +147,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
 
   // Accumulators start from C (beta = 1) so the C read overlaps the pipeline prologue and
   // the epilogue is store-only; alpha = -1 is applied by negating the A fragments.
-  // Warp tile 64 x 32 = 8 x 4 blocks of m8n8k4 DMMA; fragment map (f64):
-  // a0 = A(g, t), b0 = B(k = t, n = g), c0 = C(g, 2t), c1 = C(g, 2t+1).
-  double acc[8][4][2];
+  // m8n8k4 DMMA fragment map (f64): a0 = A(g, t), b0 = B(k = t, n = g),
+  // c0 = C(g, 2t), c1 = C(g, 2t+1).
+  double acc[T::MI][T::NI][2];
   if (g.beta != 0.0) {
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < T::MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int r = wm * 64 + mi * 8 + gq;
-        const int c = wn * 32 + ni * 8 + 2 * tq;
+      for (int ni = 0; ni < T::NI; ++ni) {
+        const int r = wm * T::WTM + mi * 8 + gq;
+        const int c = wn * T::WTN + ni * 8 + 2 * tq;
         const double* p0 = C + r + (long long)c * ldc;
         acc[mi][ni][0] = p0[0];
         acc[mi][ni][1] = p0[ldc];
       }
   } else {
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < T::MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < T::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
   }
   const unsigned neg = g.alpha < 0.0 ? 0x80000000u : 0u;
 
@@ -160,22 +181,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
     const double* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      // k-outer ordering: 32 independent DMMAs per k4 step keep the tensor pipe fed
-      double af[8], bf[4];
+      // k-outer ordering: MI x NI independent DMMAs per k4 step keep the tensor pipe fed
+      double af[T::MI], bf[T::NI];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const double v = as[(kk + tq) * SA + wm * 64 + mi * 8 + gq];
+      for (int mi = 0; mi < T::MI; ++mi) {
+        const double v = as[(kk + tq) * SA + wm * T::WTM + mi * 8 + gq];
         af[mi] = __hiloint2double(__double2hiint(v) ^ (int)neg, __double2loint(v));
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int c0 = wn * 32 + ni * 8 + gq;
-        bf[ni] = (kBL == kBNK) ? bs[(kk + tq) * SBN + c0] : bs[c0 * SBK + kk + tq];
+      for (int ni = 0; ni < T::NI; ++ni) {
+        const int c0 = wn * T::WTN + ni * 8 + gq;
+        bf[ni] = (kBL == kBNK) ? bs[(kk + tq) * T::SBN + c0] : bs[c0 * SBK + kk + tq];
       }
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+      for (int mi = 0; mi < T::MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < T::NI; ++ni)
           asm volatile(
               "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
               : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
@@ -186,11 +207,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
 
   // epilogue: store-only
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
+  for (int mi = 0; mi < T::MI; ++mi) {
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int r = wm * 64 + mi * 8 + gq;
-      const int c = wn * 32 + ni * 8 + 2 * tq;
+    for (int ni = 0; ni < T::NI; ++ni) {
+      const int r = wm * T::WTM + mi * 8 + gq;
+      const int c = wn * T::WTN + ni * 8 + 2 * tq;
       double* p0 = C + r + (long long)c * ldc;
       p0[0] = acc[mi][ni][0];
       p0[ldc] = acc[mi][ni][1];
@@ -200,27 +221,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dgemm_kernel(GemmArgs g) {
 
 // Opt-in shared-memory limits; must run once per device before the first launch.
 cudaError_t init_kernel_attributes() {
-  cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<kBNK>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * STAGES * (A_STAGE + B_STAGE_NK)));
+  cudaError_t e;
+#define MLE_SET_SMEM(BL, BNW)                                                           \
+  e = cudaFuncSetAttribute(dgemm_kernel<BL, BNW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)Tile<BNW>::template smem_bytes<BL>());                   \
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(dgemm_kernel<kBKN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(double) * STAGES * (A_STAGE + B_STAGE_KN)));
-  if (e != cudaSuccess) return e;
+  MLE_SET_SMEM(kBNK, 128)
+  MLE_SET_SMEM(kBKN, 128)
+  MLE_SET_SMEM(kBNK, 64)
+  MLE_SET_SMEM(kBKN, 64)
+#undef MLE_SET_SMEM
   return cudaSuccess;
 }
 
+// wide = 1 selects 128-column CTAs (required when C aliases A across the whole panel).
 cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s) {
   const long long tiles =
       g.lower ? (long long)g.tiles_m * (g.tiles_m + 1) / 2 : (long long)g.tiles_m * g.tiles_n;
   if (tiles <= 0) return cudaSuccess;
-  const dim3 grid((unsigned)tiles, 1, (unsigned)batch);
-  if (bl == kBNK) {
-    const size_t smem = sizeof(double) * STAGES * (A_STAGE + B_STAGE_NK);
-    dgemm_kernel<kBNK><<<grid, GEMM_THREADS, smem, s>>>(g);
+  if (g.wide) {
+    const dim3 grid((unsigned)tiles, 1, (unsigned)batch);
+    if (bl == kBNK)
+      dgemm_kernel<kBNK, 128><<<grid, GEMM_THREADS, Tile<128>::smem_bytes<kBNK>(), s>>>(g);
+    else
+      dgemm_kernel<kBKN, 128><<<grid, GEMM_THREADS, Tile<128>::smem_bytes<kBKN>(), s>>>(g);
   } else {
-    const size_t smem = sizeof(double) * STAGES * (A_STAGE + B_STAGE_KN);
-    dgemm_kernel<kBKN><<<grid, GEMM_THREADS, smem, s>>>(g);
+    const dim3 grid((unsigned)(2 * tiles), 1, (unsigned)batch);
+    if (bl == kBNK)
+      dgemm_kernel<kBNK, 64><<<grid, GEMM_THREADS, Tile<64>::smem_bytes<kBNK>(), s>>>(g);
+    else
+      dgemm_kernel<kBKN, 64><<<grid, GEMM_THREADS, Tile<64>::smem_bytes<kBKN>(), s>>>(g);
   }
   return cudaGetLastError();
 }
