@@ -319,6 +319,7 @@ def ours_arm(args, rank, world, local_rank):
         "fits": {"grad_calls_per_step": grad_all / args.steps,
                  "loglik_calls_per_step": ll_all / args.steps,
                  "batched_passes_per_step": batches / args.steps,
+                 "eval_passes_per_step": sum(c.eval_passes for c in coords) / args.steps,
                  "device_ms_per_step": {k: acc[k] / args.steps
                                         for k in ("gen_ms", "potrf_ms", "solve_ms",
                                                   "reduce_ms")},

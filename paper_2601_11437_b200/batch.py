@@ -68,12 +68,22 @@ class BatchCoordinator:
         self._error = None
         self.batches = 0
         self.requests = 0
+        self.eval_passes = 0
         # device-side accounting of every batch (CUDA events on the launching stream)
         self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
                     "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0}
 
     def _run_locked_batch(self):
+        # Alignment policy: while some clients wait on a cheap loglik (gen + Cholesky) and
+        # others on an eval_all (derivatives + solves), run only the logliks; the eval_all
+        # requests then meet in one full pass instead of paying the solve sweeps' latency
+        # chain once per straggler.  Every pass makes progress, so no client starves.
         ids = sorted(self._pending)
+        cheap = [i for i in ids if self._pending[i][2] == LOGLIK]
+        if cheap and len(cheap) < len(ids):
+            ids = cheap
+        else:
+            self.eval_passes += int(any(self._pending[i][2] == EVAL_ALL for i in ids))
         reqs = [self._pending.pop(i) for i in ids]
         self._cv.release()
         try:
