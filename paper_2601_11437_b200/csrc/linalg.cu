@@ -21,11 +21,9 @@ namespace mle {
 
 namespace {
 
-constexpr int BM = 128, BK = 16, STAGES = 3;
+constexpr int BM = 128;
 constexpr int GEMM_THREADS = 256;
 constexpr int SA = BM + 4;   // A smem: [BK][SA], m contiguous (SA = 4 mod 16 -> conflict free)
-constexpr int SBK = BK + 4;  // B (kBKN) smem: [BN][SBK]
-constexpr int A_STAGE = BK * SA;
 
 // Per CTA-width constants.  kBN = 128: 2 x 4 warps of 64 x 32 (1 CTA / SM, used for the
 // in-place panel products that need the whole 128-column panel in one CTA).  kBN = 64:
@@ -40,12 +38,14 @@ struct Tile {
   static constexpr int MI = WTM / 8;       // m8 blocks per warp
   static constexpr int NI = WTN / 8;       // n8 blocks per warp
   static constexpr int SBN = kBN + 4;      // B (kBNK) smem stride
-  static constexpr int B_STAGE_NK = BK * SBN;
-  static constexpr int B_STAGE_KN = kBN * SBK;
   static constexpr int MIN_BLOCKS = (kBN == 128) ? 1 : 2;
+  static constexpr int BK = (kBN == 128) ? 16 : 32;     // k-tile
+  static constexpr int STAGES = (kBN == 128) ? 3 : 2;   // cp.async pipeline depth
+  static constexpr int SBK = BK + 4;                    // B (kBKN) smem: [BN][SBK]
+  static constexpr int A_STAGE = BK * SA;
   template <int kBL>
   static constexpr size_t smem_bytes() {
-    return sizeof(double) * STAGES * (A_STAGE + (kBL == kBNK ? B_STAGE_NK : B_STAGE_KN));
+    return sizeof(double) * STAGES * (A_STAGE + (kBL == kBNK ? BK * SBN : kBN * SBK));
   }
 };
 
@@ -92,12 +92,13 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn,
 template <int kBL, int kBN>
 __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_kernel(GemmArgs g) {
   using T = Tile<kBN>;
+  constexpr int BK = T::BK, STAGES = T::STAGES, SBK = T::SBK, A_STAGE = T::A_STAGE;
   const int z = blockIdx.z;
   if (*g.fail_flag[z]) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
-  constexpr int B_STAGE = (kBL == kBNK) ? T::B_STAGE_NK : T::B_STAGE_KN;
+  constexpr int B_STAGE = (kBL == kBNK) ? BK * T::SBN : kBN * SBK;
 
   int tm, tn, half;
   tile_coords<kBN>(g, &tm, &tn, &half);
