@@ -68,6 +68,28 @@ const char* mle_last_error(void);
 int mle_device_count(void);
 
 /*
+ * Buffers of destroyed contexts are kept in a per-(device, size) cache and reused by the
+ * next context of the same size (no cudaMalloc / cudaFree in the steady state of fitting
+ * many datasets).  This returns every idle cached buffer to the driver.  Runtime utility:
+ * the reference has no device memory to manage.
+ */
+int mle_release_cached_memory(void);
+
+/*
+ * Kernel profiling of the FP64 trailing-update GEMMs (roofline evidence for bench.py).
+ * With profiling enabled, a pass (loglik / eval_all / eval_batch led by this context) runs
+ * on one stream and brackets every Ozaki GEMM and slicing launch with CUDA events.
+ * mle_kernel_stats then returns, for the last pass, MLE_KSTATS doubles:
+ *   [0] GEMM launches  [1] GEMM ms (sum of launch durations)  [2] FP64-equivalent tile
+ *   flops  [3] int8 tensor-core ops (36 slice products)  [4] slicing launches  [5] slicing
+ *   ms  [6] slicing algorithmic bytes  [7] reserved.
+ * Diagnostic only: no reference counterpart.
+ */
+#define MLE_KSTATS 8
+int mle_kernel_profile(mle_ctx* ctx, int enable);
+int mle_kernel_stats(const mle_ctx* ctx, double* out);
+
+/*
  * Create a context owning device-resident copies of the n locations (n x 2, row-major
  * x,y pairs) and the n observed values z.  `device` selects the GPU.  `nugget` >= 0 adds
  * tau^2 to the diagonal of Sigma (0 reproduces the reference, which has no nugget).

@@ -29,7 +29,8 @@ EXPORTED = (
     "mle_version", "mle_last_error", "mle_device_count", "mle_ctx_create", "mle_ctx_destroy",
     "mle_ctx_n", "mle_ctx_set_values", "mle_loglik", "mle_eval_all", "mle_build",
     "mle_phase_times", "mle_cholesky", "mle_bessel_k", "mle_dnu_xnu_knu", "mle_matern_elem",
-    "mle_eval_batch", "mle_simulate",
+    "mle_eval_batch", "mle_simulate", "mle_release_cached_memory",
+    "mle_kernel_profile", "mle_kernel_stats",
 )
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -48,6 +49,9 @@ def _load():
         "mle_version": (ctypes.c_char_p, []),
         "mle_last_error": (ctypes.c_char_p, []),
         "mle_device_count": (ctypes.c_int, []),
+        "mle_release_cached_memory": (ctypes.c_int, []),
+        "mle_kernel_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+        "mle_kernel_stats": (ctypes.c_int, [ctypes.c_void_p, _dp]),
         "mle_ctx_create": (ctypes.c_int, [_dp, _dp, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
                                           ctypes.POINTER(_vp)]),
         "mle_ctx_destroy": (None, [_vp]),

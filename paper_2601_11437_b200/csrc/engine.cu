@@ -26,8 +26,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -49,6 +52,114 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+
+// Caching allocator for device and pinned host buffers.  Contexts of the same size are
+// created and destroyed repeatedly (one per dataset, fit after fit); returning their
+// buffers to per-(device, size) free lists keeps cudaMalloc / cudaFree -- which map pages
+// and synchronise the device -- out of the steady state.  Idle bytes are capped; an
+// allocation that fails releases the idle buffers and retries once.
+struct BufferCache {
+  std::mutex mu;
+  std::unordered_map<void*, std::pair<int, size_t>> live;  // ptr -> (device or -1, bytes)
+  std::multimap<std::pair<int, size_t>, void*> idle;
+  size_t idle_bytes = 0;
+};
+BufferCache& buffer_cache() {
+  static BufferCache* c = new BufferCache();  // never destroyed: frees may run at exit
+  return *c;
+}
+constexpr size_t kCacheIdleCap = size_t(48) << 30;
+
+void raw_free(int dev, void* p) {
+  if (dev < 0) {
+    cudaFreeHost(p);
+    return;
+  }
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaFree(p);
+  if (cur != dev && cur >= 0) cudaSetDevice(cur);
+}
+
+void cache_trim(int dev_filter) {  // dev_filter < -1: every device and the host
+  std::vector<std::pair<int, void*>> drop;
+  {
+    BufferCache& c = buffer_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    for (auto it = c.idle.begin(); it != c.idle.end();) {
+      if (dev_filter < -1 || it->first.first == dev_filter) {
+        drop.push_back({it->first.first, it->second});
+        c.idle_bytes -= it->first.second;
+        it = c.idle.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  for (auto& d : drop) raw_free(d.first, d.second);
+}
+
+cudaError_t cache_alloc(void** p, size_t bytes, bool host) {
+  int dev = -1;
+  if (!host) {
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+  }
+  bytes = std::max<size_t>(bytes, 1);
+  BufferCache& c = buffer_cache();
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.idle.find({dev, bytes});
+    if (it != c.idle.end()) {
+      *p = it->second;
+      c.idle.erase(it);
+      c.idle_bytes -= bytes;
+      c.live[*p] = {dev, bytes};
+      return cudaSuccess;
+    }
+  }
+  auto raw = [&]() { return host ? cudaMallocHost(p, bytes) : cudaMalloc(p, bytes); };
+  cudaError_t e = raw();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cache_trim(dev);
+    e = raw();
+    if (e != cudaSuccess) return e;
+  }
+  std::lock_guard<std::mutex> lock(c.mu);
+  c.live[*p] = {dev, bytes};
+  return cudaSuccess;
+}
+
+void cache_free(void* p) {
+  if (!p) return;
+  BufferCache& c = buffer_cache();
+  std::pair<int, size_t> info;
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.live.find(p);
+    if (it == c.live.end()) return;
+    info = it->second;
+    c.live.erase(it);
+    if (c.idle_bytes + info.second <= kCacheIdleCap) {
+      c.idle.insert({info, p});
+      c.idle_bytes += info.second;
+      return;
+    }
+  }
+  raw_free(info.first, p);
+}
+
+template <class T>
+cudaError_t dmalloc(T** p, size_t bytes) {
+  return cache_alloc(reinterpret_cast<void**>(p), bytes, false);
+}
+template <class T>
+cudaError_t hmalloc(T** p, size_t bytes) {
+  return cache_alloc(reinterpret_cast<void**>(p), bytes, true);
+}
+inline void dfree(const void* p) { cache_free(const_cast<void*>(p)); }
 
 #define CUDA_TRY(expr)                                                                  \
   do {                                                                                  \
@@ -73,12 +184,19 @@ int ensure_device(int device) {
     CUDA_TRY(upload_u_tables(u.data(), du.data()));
     CUDA_TRY(init_kernel_attributes());
     CUDA_TRY(init_diag_attributes());
+    CUDA_TRY(init_ozaki_attributes());
     g_device_ready[device] = 1;
   }
   return MLE_OK;
 }
 
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+
+// FP64 trailing-update GEMM: Ozaki int8 tensor-core emulation (default) or DMMA.
+bool use_ozaki() {
+  const char* v = std::getenv("MLE_FP64_GEMM");
+  return !(v && std::strcmp(v, "dmma") == 0);
+}
 
 }  // namespace
 
@@ -113,6 +231,19 @@ struct mle_ctx {
   double launches = 0.0;
   bool factor_valid = false;      // L of Sigma(cached_theta) is resident in `sigma`
   double cached_theta[3] = {0, 0, 0};
+  // Ozaki-scheme FP64 GEMM (ozaki.cu) for the K = 512 trailing updates.  The factor's outer
+  // panels L[b1:, b0:b1] are sliced once during the Cholesky and kept with the factor (both
+  // solve sweeps and the factor cache reuse them); the solve operands use a scratch.
+  bool ozaki = true;              // MLE_FP64_GEMM=dmma at context creation disables it
+  int8_t* lsl = nullptr;          // slices of every outer panel of L
+  int* lex = nullptr;             // their row exponents
+  int8_t* xsl = nullptr;          // solve-operand slices, one region per derivative matrix
+  int* xex = nullptr;
+  // Kernel profiling (mle_kernel_profile): single stream, CUDA events around every Ozaki
+  // GEMM and slicing launch of the pass; mle_kernel_stats reports the sums.
+  bool kprof = false;
+  std::vector<cudaEvent_t> kev;
+  double kstats[MLE_KSTATS] = {};
 };
 
 namespace {
@@ -129,13 +260,42 @@ struct Item {
   double res[kResults] = {};
 };
 
+int ensure_ozaki(mle_ctx* c, bool derivs);
+
 int ensure_matrices(mle_ctx* c, bool derivs) {
   const size_t bytes = sizeof(double) * (size_t)c->N * (size_t)c->N;
-  if (!c->sigma) CUDA_TRY(cudaMalloc(&c->sigma, bytes));
-  if (!c->linv) CUDA_TRY(cudaMalloc(&c->linv, sizeof(double) * (size_t)c->Nt * kNB * kNB));
+  if (!c->sigma) CUDA_TRY(dmalloc(&c->sigma, bytes));
+  if (!c->linv) CUDA_TRY(dmalloc(&c->linv, sizeof(double) * (size_t)c->Nt * kNB * kNB));
   if (derivs) {
-    if (!c->sa) CUDA_TRY(cudaMalloc(&c->sa, bytes));
-    if (!c->sn) CUDA_TRY(cudaMalloc(&c->sn, bytes));
+    if (!c->sa) CUDA_TRY(dmalloc(&c->sa, bytes));
+    if (!c->sn) CUDA_TRY(dmalloc(&c->sn, bytes));
+  }
+  return ensure_ozaki(c, derivs);
+}
+
+// Outer panel ob of the factor: rows [b1, N) x columns [b0, b1), b1 = (ob + 1) kOuter.
+long long oz_panel_rows(int Nt, int ob) {
+  return (long long)std::max(0, Nt - std::min(Nt, (ob + 1) * kOuter)) * kNB;
+}
+long long oz_panel_row_offset(int Nt, int ob) {  // rows of the panels before ob
+  long long r = 0;
+  for (int o = 0; o < ob; ++o) r += oz_panel_rows(Nt, o);
+  return r;
+}
+constexpr int kOzK = kOuter * kNB;               // K of every trailing update
+constexpr size_t kOzRowBytes = (size_t)kOzK * kOzSlices;
+constexpr size_t kOzTileBytes = kOzRowBytes * kNB;
+
+int ensure_ozaki(mle_ctx* c, bool derivs) {
+  if (!c->ozaki) return MLE_OK;
+  if (!c->lsl) {
+    const long long rows = oz_panel_row_offset(c->Nt, (c->Nt + kOuter - 1) / kOuter);
+    CUDA_TRY(dmalloc(&c->lsl, std::max<size_t>(1, (size_t)rows * kOzRowBytes)));
+    CUDA_TRY(dmalloc(&c->lex, sizeof(int) * std::max<long long>(1, rows)));
+  }
+  if (derivs && !c->xsl) {
+    CUDA_TRY(dmalloc(&c->xsl, 2 * (size_t)c->N * kOzRowBytes));
+    CUDA_TRY(dmalloc(&c->xex, 2 * sizeof(int) * (size_t)c->N));
   }
   return MLE_OK;
 }
@@ -170,6 +330,76 @@ struct Launcher {
     return MLE_OK;
   }
   int gemm(const GemmArgs& g, BLayout bl, int batch) { return gemm(g, bl, batch, s); }
+  // kernel profiling: event pair per launch (kind 0 ozgemm, 1 slicing) + algorithmic work
+  mle_ctx* prof = nullptr;
+  std::vector<int> pkind;
+  std::vector<double> pwork;
+  int prof_begin(cudaStream_t st) {
+    if (!prof) return MLE_OK;
+    const size_t i = 2 * pkind.size();
+    while (prof->kev.size() < i + 2) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      prof->kev.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(prof->kev[i], st));
+    return MLE_OK;
+  }
+  int prof_end(cudaStream_t st, int kind, double work) {
+    if (!prof) return MLE_OK;
+    CUDA_TRY(cudaEventRecord(prof->kev[2 * pkind.size() + 1], st));
+    pkind.push_back(kind);
+    pwork.push_back(work);
+    return MLE_OK;
+  }
+  int slice(const OzSliceArgs& a, long long rows, bool row_contig, int batch) {
+    launches += 1;
+    int rc = prof_begin(s);
+    if (rc) return rc;
+    CUDA_TRY(launch_oz_slice(a, (int)rows, row_contig, batch, s));
+    // algorithmic bytes: the FP64 operand read once, 8 int8 slices + exponents written
+    return prof_end(s, 1, (double)batch * rows * (16.0 * a.K + 4.0));
+  }
+  int ozgemm(const OzGemmArgs& g, int batch, cudaStream_t st) {
+    launches += 1;
+    int rc = prof_begin(st);
+    if (rc) return rc;
+    CUDA_TRY(launch_ozgemm(g, batch, st));
+    double tiles;
+    if (g.lower) tiles = 0.5 * g.tiles_m * (g.tiles_m + 1.0);
+    else if (g.trap) {
+      tiles = 0;
+      for (int tn = 0; tn < g.tiles_n; ++tn) tiles += std::max(0, g.tiles_m - tn);
+    } else tiles = (double)g.tiles_m * g.tiles_n;
+    // FP64-equivalent tile flops (2 x 128 x 128 x K per tile)
+    return prof_end(st, 0, (double)batch * tiles * 2.0 * kNB * kNB * (32.0 * g.kblocks));
+  }
+  int prof_collect() {
+    if (!prof) return MLE_OK;
+    double st[MLE_KSTATS] = {};
+    for (size_t i = 0; i < pkind.size(); ++i) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, prof->kev[2 * i], prof->kev[2 * i + 1]));
+      const int base = pkind[i] == 0 ? 0 : 4;
+      st[base] += 1.0;
+      st[base + 1] += ms;
+      st[base + 2] += pwork[i];
+    }
+    st[3] = st[2] * kOzProducts;  // int8 tensor ops: every FP64 MAC is 36 int8 MACs
+    std::memcpy(prof->kstats, st, sizeof(st));
+    return MLE_OK;
+  }
+  static OzGemmArgs oz_base(long long ldc, int tiles_m, int tiles_n) {
+    OzGemmArgs g;
+    std::memset(&g, 0, sizeof(g));
+    g.ldc = ldc;
+    g.kblocks = kOzK / 32;
+    g.tiles_m = tiles_m;
+    g.tiles_n = tiles_n;
+    g.alpha = -1.0;
+    g.beta = 1.0;
+    return g;
+  }
 
   // `to` waits for all work enqueued so far on `from`.
   int join(cudaStream_t from, cudaStream_t to) {
@@ -238,6 +468,43 @@ struct Launcher {
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
       if ((rc = join(s2, s))) return rc;  // (ii) of the previous block touched these tiles
+      if (cs[0]->lsl) {
+        // Ozaki path: slice P = L[b1:, b0:b1] once (kept for the solves), then C -= P P^T
+        const int ob = b0 / kOuter;
+        const long long eo = oz_panel_row_offset(Nt, ob);
+        OzSliceArgs sa;
+        std::memset(&sa, 0, sizeof(sa));
+        for (int b = 0; b < m; ++b) {
+          sa.X[b] = mats[b] + t0 + c0 * ld;
+          sa.slices[b] = cs[b]->lsl + (size_t)eo * kOzRowBytes;
+          sa.e[b] = cs[b]->lex + eo;
+          sa.fail_flag[b] = cs[b]->fail_flag;
+        }
+        sa.ld = ld;
+        sa.K = kOzK;
+        if ((rc = slice(sa, (long long)(Nt - b1) * kNB, true, m))) return rc;
+        OzGemmArgs t = oz_base(ld, Nt - b1, b2 - b1);  // (i)
+        t.trap = 1;
+        for (int b = 0; b < m; ++b) {
+          t.As[b] = t.Bs[b] = sa.slices[b];
+          t.ea[b] = t.eb[b] = sa.e[b];
+          t.C[b] = mats[b] + t0 + t0 * ld;
+          t.fail_flag[b] = cs[b]->fail_flag;
+        }
+        if ((rc = ozgemm(t, m, s))) return rc;
+        if (b2 >= Nt) continue;
+        if ((rc = join(s, s2))) return rc;
+        OzGemmArgs u = oz_base(ld, Nt - b2, 0);        // (ii)
+        u.lower = 1;
+        for (int b = 0; b < m; ++b) {
+          u.As[b] = u.Bs[b] = sa.slices[b] + (size_t)(b2 - b1) * kOzTileBytes;
+          u.ea[b] = u.eb[b] = sa.e[b] + (size_t)(b2 - b1) * kNB;
+          u.C[b] = mats[b] + u0 + u0 * ld;
+          u.fail_flag[b] = cs[b]->fail_flag;
+        }
+        if ((rc = ozgemm(u, m, bulk()))) return rc;
+        continue;
+      }
       GemmArgs t = gemm_base();           // (i): columns [b1, b2), rows >= b1
       for (int b = 0; b < m; ++b) {
         t.A[b] = mats[b] + t0 + c0 * ld;
@@ -278,6 +545,11 @@ struct Launcher {
       return (const double*)(cs[z / 2]->linv + (size_t)k * kNB * kNB);
     };
     auto flag = [&](int z) { return (const int*)cs[z / 2]->fail_flag; };
+    const bool oz = cs[0]->lsl != nullptr && cs[0]->xsl != nullptr;
+    auto LS = [&](int z) { return (const int8_t*)cs[z / 2]->lsl; };
+    auto LE = [&](int z) { return (const int*)cs[z / 2]->lex; };
+    auto XS = [&](int z) { return cs[z / 2]->xsl + (size_t)(z % 2) * ld * kOzRowBytes; };
+    auto XE = [&](int z) { return cs[z / 2]->xex + (size_t)(z % 2) * ld; };
     int rc;
     // forward sweep X = L^-1 S (all columns), row blocks top-down
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
@@ -312,6 +584,43 @@ struct Launcher {
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
       if ((rc = join(s2, s))) return rc;
+      if (oz) {
+        // A = factor panel ob (sliced by the Cholesky), B(n, k) = X[c0 + k, n]
+        const int ob = b0 / kOuter;
+        const long long eo = oz_panel_row_offset(Nt, ob);
+        OzSliceArgs sa;
+        std::memset(&sa, 0, sizeof(sa));
+        for (int z = 0; z < zb; ++z) {
+          sa.X[z] = S(z) + c0;
+          sa.slices[z] = XS(z);
+          sa.e[z] = XE(z);
+          sa.fail_flag[z] = flag(z);
+        }
+        sa.ld = ld;
+        sa.K = kOzK;
+        if ((rc = slice(sa, ld, false, zb))) return rc;
+        OzGemmArgs t = oz_base(ld, b2 - b1, Nt);  // (i): rows [b1, b2)
+        for (int z = 0; z < zb; ++z) {
+          t.As[z] = LS(z) + (size_t)eo * kOzRowBytes;
+          t.ea[z] = LE(z) + eo;
+          t.Bs[z] = XS(z);
+          t.eb[z] = XE(z);
+          t.C[z] = S(z) + t0;
+          t.fail_flag[z] = flag(z);
+        }
+        if ((rc = ozgemm(t, zb, s))) return rc;
+        if (b2 >= Nt) continue;
+        if ((rc = join(s, s2))) return rc;
+        OzGemmArgs u = t;                          // (ii): rows >= b2
+        u.tiles_m = Nt - b2;
+        for (int z = 0; z < zb; ++z) {
+          u.As[z] = t.As[z] + (size_t)(b2 - b1) * kOzTileBytes;
+          u.ea[z] = t.ea[z] + (size_t)(b2 - b1) * kNB;
+          u.C[z] = S(z) + u0;
+        }
+        if ((rc = ozgemm(u, zb, bulk()))) return rc;
+        continue;
+      }
       GemmArgs t = gemm_base();   // (i): rows [b1, b2), all columns
       for (int z = 0; z < zb; ++z) {
         t.A[z] = L(z) + t0 + c0 * ld;   // L[b1:b2, b0:b1]
@@ -371,6 +680,48 @@ struct Launcher {
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
       if ((rc = join(s2, s))) return rc;
+      if (oz) {
+        // A = B[T, b0:b1] (sliced here), B = factor panel ob
+        const int ob = b0 / kOuter;
+        const long long eo = oz_panel_row_offset(Nt, ob);
+        OzSliceArgs sa;
+        std::memset(&sa, 0, sizeof(sa));
+        for (int z = 0; z < zb; ++z) {
+          sa.X[z] = S(z) + t0 + c0 * ld;
+          sa.slices[z] = XS(z);
+          sa.e[z] = XE(z);
+          sa.fail_flag[z] = flag(z);
+        }
+        sa.ld = ld;
+        sa.K = kOzK;
+        if ((rc = slice(sa, (long long)(Nt - b1) * kNB, true, zb))) return rc;
+        OzGemmArgs t = oz_base(ld, Nt - b1, b2 - b1);  // (i)
+        t.trap = 1;
+        for (int z = 0; z < zb; ++z) {
+          t.As[z] = XS(z);
+          t.ea[z] = XE(z);
+          t.Bs[z] = LS(z) + (size_t)eo * kOzRowBytes;
+          t.eb[z] = LE(z) + eo;
+          t.C[z] = S(z) + t0 + t0 * ld;
+          t.fail_flag[z] = flag(z);
+        }
+        if ((rc = ozgemm(t, zb, s))) return rc;
+        if (b2 >= Nt) continue;
+        if ((rc = join(s, s2))) return rc;
+        OzGemmArgs u = oz_base(ld, Nt - b2, 0);         // (ii): lower tiles of [b2, Nt)
+        u.lower = 1;
+        for (int z = 0; z < zb; ++z) {
+          const size_t to = (size_t)(b2 - b1);
+          u.As[z] = t.As[z] + to * kOzTileBytes;
+          u.ea[z] = t.ea[z] + to * kNB;
+          u.Bs[z] = t.Bs[z] + to * kOzTileBytes;
+          u.eb[z] = t.eb[z] + to * kNB;
+          u.C[z] = S(z) + u0 + u0 * ld;
+          u.fail_flag[z] = flag(z);
+        }
+        if ((rc = ozgemm(u, zb, bulk()))) return rc;
+        continue;
+      }
       GemmArgs t = gemm_base();   // (i): columns [b1, b2), rows >= b1
       for (int z = 0; z < zb; ++z) {
         t.A[z] = S(z) + t0 + c0 * ld;   // B[T, b0:b1]
@@ -404,7 +755,9 @@ struct Launcher {
 int run_chunk(Item* items, int m) {
   mle_ctx* lead = items[0].c;
   cudaStream_t s = lead->stream;
-  Launcher run{s, lead->side, lead->pool, kPoolEvents};
+  Launcher run{s, lead->kprof ? nullptr : lead->side, lead->pool, kPoolEvents};
+  if (lead->kprof) run.prof = lead;
+  cudaStream_t aux = lead->kprof ? s : lead->aux;  // profiling: everything serialised
   for (int b = 0; b < m; ++b) {
     Item& it = items[b];
     int rc = ensure_matrices(it.c, it.derivs);
@@ -449,10 +802,10 @@ int run_chunk(Item* items, int m) {
   }
   auto der = gen_set(false);
   if (der.second > 0) {
-    int rc = run.join(s, lead->aux);
+    int rc = run.join(s, aux);
     if (rc) return rc;
     run.launches += 1;
-    launch_gen_engine(der.first, der.second, lead->aux);
+    launch_gen_engine(der.first, der.second, aux);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaEventRecord(lead->ev[1], s));
@@ -475,7 +828,7 @@ int run_chunk(Item* items, int m) {
   }
   CUDA_TRY(cudaEventRecord(lead->ev[2], s));
   {
-    int rc = run.join(lead->aux, s);  // derivative matrices generated
+    int rc = run.join(aux, s);  // derivative matrices generated
     if (rc) return rc;
     mle_ctx* cs[kMaxItems];
     int nd = 0;
@@ -512,6 +865,10 @@ int run_chunk(Item* items, int m) {
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
+  {
+    int rc = run.prof_collect();
+    if (rc) return rc;
+  }
   float ms[4];
   for (int p = 0; p < 4; ++p) CUDA_TRY(cudaEventElapsedTime(&ms[p], lead->ev[p], lead->ev[p + 1]));
   double flops = 0.0, gbytes = 0.0;
@@ -537,6 +894,7 @@ int run_chunk(Item* items, int m) {
     c->flops = flops;
     c->gen_bytes = gbytes;
     c->launches = run.launches;
+    if (c != lead) std::memcpy(c->kstats, lead->kstats, sizeof(c->kstats));
     int flag;
     std::memcpy(&flag, c->h_res + 9, sizeof(int));
     if (flag) {
@@ -638,6 +996,24 @@ int mle_device_count(void) {
   return count;
 }
 
+int mle_kernel_profile(mle_ctx* ctx, int enable) {
+  if (!ctx) return fail(MLE_INVALID, "null context");
+  ctx->kprof = enable != 0;
+  std::memset(ctx->kstats, 0, sizeof(ctx->kstats));
+  return MLE_OK;
+}
+
+int mle_kernel_stats(const mle_ctx* ctx, double* out) {
+  if (!ctx || !out) return fail(MLE_INVALID, "null argument");
+  std::memcpy(out, ctx->kstats, sizeof(ctx->kstats));
+  return MLE_OK;
+}
+
+int mle_release_cached_memory(void) {
+  cache_trim(-2);
+  return MLE_OK;
+}
+
 int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device, double nugget,
                    mle_ctx** out) {
   if (!out) return fail(MLE_INVALID, "out is null");
@@ -657,6 +1033,7 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   c->N = round_up(n + 1, kNB);
   c->Nt = (int)(c->N / kNB);
   c->nugget = nugget;
+  c->ozaki = use_ozaki();
   std::vector<double> x(n), y(n);
   for (int64_t i = 0; i < n; ++i) {
     x[i] = locs_xy[2 * i];
@@ -677,16 +1054,16 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   CTX_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
   for (auto& e : c->pool) CTX_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CTX_TRY(cudaMalloc(&c->lx, sizeof(double) * n));
-  CTX_TRY(cudaMalloc(&c->ly, sizeof(double) * n));
-  CTX_TRY(cudaMalloc(&c->z, sizeof(double) * n));
-  CTX_TRY(cudaMalloc(&c->fail_flag, sizeof(int)));
-  CTX_TRY(cudaMalloc(&c->fail_idx, sizeof(long long)));
-  CTX_TRY(cudaMalloc(&c->partials, sizeof(double) * kReduceBlocks * kReduceSums));
-  CTX_TRY(cudaMalloc(&c->out, sizeof(double) * 9));
-  CTX_TRY(cudaMalloc(&c->d_theta, sizeof(ThetaParams)));
-  CTX_TRY(cudaMallocHost(&c->h_theta, sizeof(ThetaParams)));
-  CTX_TRY(cudaMallocHost(&c->h_res, sizeof(double) * 12));
+  CTX_TRY(dmalloc(&c->lx, sizeof(double) * n));
+  CTX_TRY(dmalloc(&c->ly, sizeof(double) * n));
+  CTX_TRY(dmalloc(&c->z, sizeof(double) * n));
+  CTX_TRY(dmalloc(&c->fail_flag, sizeof(int)));
+  CTX_TRY(dmalloc(&c->fail_idx, sizeof(long long)));
+  CTX_TRY(dmalloc(&c->partials, sizeof(double) * kReduceBlocks * kReduceSums));
+  CTX_TRY(dmalloc(&c->out, sizeof(double) * 9));
+  CTX_TRY(dmalloc(&c->d_theta, sizeof(ThetaParams)));
+  CTX_TRY(hmalloc(&c->h_theta, sizeof(ThetaParams)));
+  CTX_TRY(hmalloc(&c->h_res, sizeof(double) * 12));
   CTX_TRY(cudaMemcpyAsync(c->lx, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CTX_TRY(cudaMemcpyAsync(c->ly, y.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CTX_TRY(cudaMemcpyAsync(c->z, z, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
@@ -701,24 +1078,29 @@ void mle_ctx_destroy(mle_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  cudaFree(c->lx);
-  cudaFree(c->ly);
-  cudaFree(c->z);
-  cudaFree(c->sigma);
-  cudaFree(c->sa);
-  cudaFree(c->sn);
-  cudaFree(c->linv);
-  cudaFree(c->fail_flag);
-  cudaFree(c->fail_idx);
-  cudaFree(c->partials);
-  cudaFree(c->out);
-  cudaFree(c->d_theta);
-  if (c->h_theta) cudaFreeHost(c->h_theta);
-  if (c->h_res) cudaFreeHost(c->h_res);
+  dfree(c->lx);
+  dfree(c->ly);
+  dfree(c->z);
+  dfree(c->sigma);
+  dfree(c->sa);
+  dfree(c->sn);
+  dfree(c->linv);
+  dfree(c->fail_flag);
+  dfree(c->fail_idx);
+  dfree(c->partials);
+  dfree(c->out);
+  dfree(c->d_theta);
+  dfree(c->lsl);
+  dfree(c->lex);
+  dfree(c->xsl);
+  dfree(c->xex);
+  if (c->h_theta) dfree(c->h_theta);
+  if (c->h_res) dfree(c->h_res);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->pool)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->kev) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -821,12 +1203,12 @@ int mle_simulate(mle_ctx* c, const double theta[3], const double* w, double* z_o
     double** a;
     double** b;
     ~G() {
-      cudaFree(*a);
-      cudaFree(*b);
+      dfree(*a);
+      dfree(*b);
     }
   } guard{&dw, &dz};
-  CUDA_TRY(cudaMalloc(&dw, sizeof(double) * c->n));
-  CUDA_TRY(cudaMalloc(&dz, sizeof(double) * c->n));
+  CUDA_TRY(dmalloc(&dw, sizeof(double) * c->n));
+  CUDA_TRY(dmalloc(&dz, sizeof(double) * c->n));
   CUDA_TRY(cudaMemcpyAsync(dw, w, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(launch_trmv_lower(c->sigma, c->N, (int)c->n, dw, dz, c->stream));
   CUDA_TRY(cudaMemcpyAsync(z_out, dz, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
@@ -893,11 +1275,13 @@ int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t*
   struct Guard {
     mle_ctx* c;
     ~Guard() {
-      cudaFree(c->sigma);
-      cudaFree(c->linv);
-      cudaFree(c->fail_flag);
-      cudaFree(c->fail_idx);
-      if (c->h_res) cudaFreeHost(c->h_res);
+      dfree(c->sigma);
+      dfree(c->linv);
+      dfree(c->fail_flag);
+      dfree(c->fail_idx);
+      dfree(c->lsl);
+      dfree(c->lex);
+      if (c->h_res) dfree(c->h_res);
       if (c->stream) cudaStreamDestroy(c->stream);
       c->sigma = c->linv = nullptr;
       c->fail_flag = nullptr;
@@ -907,11 +1291,13 @@ int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t*
     }
   } guard{&c};
   CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-  CUDA_TRY(cudaMalloc(&c.sigma, sizeof(double) * (size_t)N * N));
-  CUDA_TRY(cudaMalloc(&c.linv, sizeof(double) * (size_t)c.Nt * kNB * kNB));
-  CUDA_TRY(cudaMalloc(&c.fail_flag, sizeof(int)));
-  CUDA_TRY(cudaMalloc(&c.fail_idx, sizeof(long long)));
-  CUDA_TRY(cudaMallocHost(&c.h_res, sizeof(double) * 12));
+  CUDA_TRY(dmalloc(&c.sigma, sizeof(double) * (size_t)N * N));
+  CUDA_TRY(dmalloc(&c.linv, sizeof(double) * (size_t)c.Nt * kNB * kNB));
+  CUDA_TRY(dmalloc(&c.fail_flag, sizeof(int)));
+  CUDA_TRY(dmalloc(&c.fail_idx, sizeof(long long)));
+  CUDA_TRY(hmalloc(&c.h_res, sizeof(double) * 12));
+  c.ozaki = use_ozaki();
+  if ((rc = ensure_ozaki(&c, false))) return rc;
   CUDA_TRY(cudaMemcpyAsync(c.sigma, h.data(), sizeof(double) * (size_t)N * N,
                            cudaMemcpyHostToDevice, c.stream));
   CUDA_TRY(cudaMemsetAsync(c.fail_flag, 0, sizeof(int), c.stream));
@@ -956,16 +1342,16 @@ static int run_elem(int op, const ThetaParams& P, int which, const double* x, in
     ThetaParams** p;
     cudaStream_t* s;
     ~G() {
-      cudaFree(*a);
-      cudaFree(*b);
-      cudaFree(*p);
+      dfree(*a);
+      dfree(*b);
+      dfree(*p);
       if (*s) cudaStreamDestroy(*s);
     }
   } guard{&dx, &dy, &dP, &s};
   CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  CUDA_TRY(cudaMalloc(&dx, sizeof(double) * m));
-  CUDA_TRY(cudaMalloc(&dy, sizeof(double) * m));
-  CUDA_TRY(cudaMalloc(&dP, sizeof(ThetaParams)));
+  CUDA_TRY(dmalloc(&dx, sizeof(double) * m));
+  CUDA_TRY(dmalloc(&dy, sizeof(double) * m));
+  CUDA_TRY(dmalloc(&dP, sizeof(ThetaParams)));
   CUDA_TRY(cudaMemcpyAsync(dP, &P, sizeof(ThetaParams), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(dx, x, sizeof(double) * m, cudaMemcpyHostToDevice, s));
   launch_elem(dP, op, which, dx, m, dy, s);

@@ -96,6 +96,42 @@ cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
 cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double* w, double* z,
                               cudaStream_t s);
 
+// Ozaki-scheme FP64 GEMM on tcgen05 int8 tensor cores (ozaki.cu).
+// Slicing: X is rows x K (rows multiple of 128, K multiple of 32) with X(r,k) at
+// X[r + k*ld] (row_contig) or X[k + r*ld]; writes 8 int8 slices in UMMA canonical layout
+// [rows/128][K/32][8][128x32] and one power-of-two exponent per row.
+struct OzSliceArgs {
+  const double* X[kMaxGemm];
+  int8_t* slices[kMaxGemm];
+  int* e[kMaxGemm];
+  const int* fail_flag[kMaxGemm];
+  long long ld;
+  int K;
+};
+// C = alpha * A B^T + beta * C from slices (A: M rows, B: N rows, both over the same K).
+struct OzGemmArgs {
+  const int8_t* As[kMaxGemm];
+  const int8_t* Bs[kMaxGemm];
+  const int* ea[kMaxGemm];
+  const int* eb[kMaxGemm];
+  double* C[kMaxGemm];
+  const int* fail_flag[kMaxGemm];
+  long long ldc;
+  int kblocks;   // K / 32
+  int tiles_m;   // 128-row tiles
+  int tiles_n;   // 128-column tiles (full mode)
+  int lower, trap;
+  double alpha, beta;
+};
+constexpr int kOzSlices = 8;
+constexpr int kOzProducts = 36;  // slice products with p + q <= kOzSlices + 1
+// bytes of slice storage for a rows x K operand
+inline size_t oz_slice_bytes(long long rows, int K) { return (size_t)rows * K * kOzSlices; }
+cudaError_t init_ozaki_attributes();
+cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int batch,
+                            cudaStream_t s);
+cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile = 32);
+
 constexpr int kReduceBlocks = 148 * 4;
 constexpr int kReduceSums = 7;
 

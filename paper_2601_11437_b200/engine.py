@@ -105,6 +105,19 @@ class Engine:
         nat.check(rc)
         return out
 
+    def kernel_profile(self, enable: bool = True):
+        """Serialise passes led by this engine and event-time every Ozaki GEMM / slicing."""
+        nat.check(nat.lib.mle_kernel_profile(self._ctx, int(bool(enable))))
+
+    def kernel_stats(self) -> dict:
+        """Per-kernel sums of the last profiled pass (see mle_kernel_stats)."""
+        out = np.zeros(8)
+        nat.check(nat.lib.mle_kernel_stats(self._ctx, nat.as_ptr(out)))
+        return {"gemm_launches": int(out[0]), "gemm_ms": float(out[1]),
+                "gemm_fp64_flops": float(out[2]), "gemm_int8_ops": float(out[3]),
+                "slice_launches": int(out[4]), "slice_ms": float(out[5]),
+                "slice_bytes": float(out[6])}
+
     def phase_times(self) -> dict:
         out = np.zeros(len(nat.PHASES) + 3)
         nat.check(nat.lib.mle_phase_times(self._ctx, nat.as_ptr(out)))

@@ -1,0 +1,84 @@
+"""The Ozaki-scheme FP64 trailing-update GEMM (int8 tcgen05, ozaki.cu) inside the engine.
+
+* against the DMMA path (MLE_FP64_GEMM=dmma) on the config-2 data: both approximate the same
+  exact products; their difference must sit far inside the north-star tolerances
+  (the default engine is the Ozaki path, so test_gpu_likelihood / test_gpu_fits hold it to
+  the reference's golden evaluations and fits)
+* kernel profiling counters are self-consistent (36 int8 products per FP64 MAC)
+* the buffer cache: a context rebuilt from cached buffers gives bit-identical results
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import config_data
+from test_gpu_likelihood import score_scale
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(gpu, loc, z, gemm):
+    old = os.environ.get("MLE_FP64_GEMM")
+    os.environ["MLE_FP64_GEMM"] = gemm
+    try:
+        return gpu.Engine(loc, z)
+    finally:
+        if old is None:
+            del os.environ["MLE_FP64_GEMM"]
+        else:
+            os.environ["MLE_FP64_GEMM"] = old
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))
+
+
+def test_ozaki_vs_dmma_engine(gpu):
+    loc, z = config_data("config2", 0)
+    th = np.array([1.0, 0.2, 1.5])
+    oz = _engine(gpu, loc, z, "ozaki").eval_all(th)
+    dm = _engine(gpu, loc, z, "dmma").eval_all(th)
+    assert abs(oz[0] - dm[0]) <= 1e-12 * abs(dm[0])
+    # the score is a difference of two O(n) terms: compare on their magnitude, as the
+    # golden parity tests do, two orders inside the 1e-8 north-star tolerance
+    scale = score_scale(th, len(z), dm[1], dm[2])
+    assert np.all(np.abs(oz[1] - dm[1]) <= 1e-10 * scale), (oz[1], dm[1], scale)
+    assert _rel(oz[2], dm[2]) < 1e-10
+
+
+def test_kernel_stats(gpu):
+    loc, z = config_data("config2", 1)
+    eng = gpu.Engine(loc, z)
+    eng.kernel_profile(True)
+    ref = eng.eval_all(np.array([1.0, 0.2, 1.5]))
+    st = eng.kernel_stats()
+    eng.kernel_profile(False)
+    again = eng.eval_all(np.array([1.0, 0.2, 1.5]))
+    # profiling serialises the streams but computes exactly the same thing
+    assert ref[0] == again[0]
+    np.testing.assert_array_equal(ref[2], again[2])
+    assert st["gemm_launches"] > 0 and st["gemm_ms"] > 0.0
+    assert st["slice_launches"] > 0 and st["slice_ms"] > 0.0
+    assert st["gemm_int8_ops"] == pytest.approx(36.0 * st["gemm_fp64_flops"])
+    n = eng.n
+    # the K=512 trailing updates carry most of the 3 n^3 + n^3 / 3 flops of an eval_all
+    assert 0.5 * (3.0 + 1.0 / 3.0) * n ** 3 < st["gemm_fp64_flops"] < 4.0 * n ** 3
+
+
+def test_buffer_cache_reuse_bit_identical(gpu):
+    loc, z = config_data("config2", 2)
+    th = np.array([0.9, 0.18, 1.4])
+    first = gpu.Engine(loc, z)
+    a = first.eval_all(th)
+    first.close()                      # buffers go to the cache ...
+    second = gpu.Engine(loc, z)        # ... and are reused here
+    b = second.eval_all(th)
+    assert a[0] == b[0]
+    np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(a[2], b[2])
+    second.close()
+    from paper_2601_11437_b200 import _native as nat
+    nat.check(nat.lib.mle_release_cached_memory())
