@@ -35,6 +35,11 @@ GOLDEN = REPO / "tests" / "golden"
 CONFIG = "config2"
 THETA0 = (0.8, 0.1, 1.0)
 N_REPLICAS = 5
+# tcgen05.mma kind::i8 issue-rate ceiling measured on this pool's B200 with tools/umma_rate
+# (the ozgemm k-block MMA sequence, operands resident in SMEM, 1888 MHz): 4485 TOPS burst;
+# with random operands the clock settles at 1649-1761 MHz (sw_power_cap) -> 3624-3870 TOPS
+# (profiles/r01_umma_rate.txt).  Reported beside the MEASURED_PEAKS-derived peak.
+INT8_PIPE_TOPS = 4485.0
 FP64_PEAK_TFLOPS = 36.08  # cuBLAS DGEMM 16384^3, this pool's B200 (profiles/r01_fp64_peaks.txt)
 METRIC = "Fisher-BT iterations/s at n"
 
@@ -344,6 +349,8 @@ def ours_arm(args, rank, world, local_rank):
                       "/ the sum of the launches' CUDA-event durations (profiling pass, one "
                       "stream)",
             "fp64_equiv_tflops": kern["ozgemm_fp64_equiv_tflops"],
+            "int8_pipe_microbench_tops": INT8_PIPE_TOPS,
+            "frac_of_int8_pipe_microbench": kern["ozgemm_int8_tops"] / INT8_PIPE_TOPS,
             "peak_source": "int8 dense tcgen05 rate = 2 x MEASURED_PEAKS.json bf16_tflops "
                            "(burst; sm_100 int8 dense is twice bf16 dense)",
             "traffic_source": ncu_traffic.get("source") if ncu_traffic else None},

@@ -122,6 +122,8 @@ struct OzGemmArgs {
   int tiles_n;   // 128-column tiles (full mode)
   int lower, trap;
   double alpha, beta;
+  int diag_mode;  // developer diagnostics only: 1 skip the MMAs, 2 skip the loads (0: normal)
+  long long* diag_out;  // developer diagnostics: MMA-thread timing of CTA 0 (null: off)
 };
 constexpr int kOzSlices = 8;
 constexpr int kOzProducts = 36;  // slice products with p + q <= kOzSlices + 1
@@ -130,7 +132,8 @@ inline size_t oz_slice_bytes(long long rows, int K) { return (size_t)rows * K * 
 cudaError_t init_ozaki_attributes();
 cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int batch,
                             cudaStream_t s);
-cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile = 32);
+// n_tile: 0 persistent 128x64 (default), 1 persistent 128x32, 32 / 64 one tile per CTA
+cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile = 0);
 
 constexpr int kReduceBlocks = 148 * 4;
 constexpr int kReduceSums = 7;

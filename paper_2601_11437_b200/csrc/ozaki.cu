@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace mle {
@@ -84,6 +86,44 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return ((uint64_t)((saddr >> 4) & 0x3FFF)) | ((uint64_t)(128 >> 4) << 16) |
          ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+
+// Epilogue combine for 16 columns of one TMEM lane: the 8 int32 diagonal accumulators v_d
+// (d = 2..9, at column offsets (d - 2) * stride from `addr`) fold exactly into two int64
+// Horner sums  hi = sum_{d=2..5} v_d 2^(7 (5 - d)),  lo = sum_{d=6..9} v_d 2^(7 (9 - d))
+// (|v_d| < 2^26 for K <= 512, so |hi|, |lo| < 2^48 convert to double exactly), and
+//   sum_d v_d 2^(-7 d) = hi 2^-35 + lo 2^-63
+// is formed with a single rounding (one FMA).  2 conversions per element instead of 8.
+__device__ __forceinline__ void oz_tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+__device__ __forceinline__ void oz_horner4(uint32_t addr, uint32_t stride, long long (&h)[16]) {
+  uint32_t v0[16], v1[16], v2[16], v3[16];
+  oz_tmem_ld16(addr, v0);
+  oz_tmem_ld16(addr + stride, v1);
+  oz_tmem_ld16(addr + 2 * stride, v2);
+  oz_tmem_ld16(addr + 3 * stride, v3);
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    h[j] = ((((long long)(int)v0[j] * 128 + (int)v1[j]) * 128 + (int)v2[j]) * 128) +
+           (int)v3[j];
+}
+
+__device__ __forceinline__ void oz_combine16(uint32_t addr, uint32_t stride, double (&out)[16]) {
+  long long hi[16], lo[16];
+  oz_horner4(addr, stride, hi);
+  oz_horner4(addr + 4 * stride, stride, lo);
+  const double s_hi = pow2i(-35), s_lo = pow2i(-63);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) out[j] = fma((double)hi[j], s_hi, (double)lo[j] * s_lo);
 }
 
 }  // namespace
@@ -294,24 +334,11 @@ __global__ void __launch_bounds__(OZ_THREADS, OzCfg<kN>::kCtasPerSm) ozgemm_kern
     asm volatile("tcgen05.fence::after_thread_sync;");
     double acc[kN];
 #pragma unroll
-    for (int j = 0; j < kN; ++j) acc[j] = 0.0;
-#pragma unroll 1
-    for (int d = OZ_S + 1; d >= 2; --d) {  // smallest contributions first
-      const double w = pow2i(-7 * d);
+    for (int c0 = 0; c0 < kN; c0 += 16) {
+      double part[16];
+      oz_combine16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, kN, part);
 #pragma unroll
-      for (int c0 = 0; c0 < kN; c0 += 16) {
-        uint32_t v[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)((d - 2) * kN + c0)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c0 + j] = fma((double)(int)v[j], w, acc[c0 + j]);
-      }
+      for (int j = 0; j < 16; ++j) acc[c0 + j] = part[j];
     }
     // C = C + (alpha 2^ea) 2^eb acc: exact power-of-two scalings, one rounding in the add
 #pragma unroll
@@ -335,7 +362,268 @@ __global__ void __launch_bounds__(OZ_THREADS, OzCfg<kN>::kCtasPerSm) ozgemm_kern
                  "n"(Cfg::kTmemCols));
 }
 
+
+// Persistent variant: one CTA per SM walks the tile list (tile t, t + gridDim.x, ...).
+// The kernel is bound by the shared-memory ingress of the slices (L2 -> SMEM, ~29 B/clk/SM
+// measured), not by the tensor pipe: a 128 x kN tile needs 8 x 32 (128 + kN) bytes per k
+// block for 36 x 128 x kN x 32 MACs, so kN = 64 halves the ingress per MAC of kN = 32.
+//   kN = 32: 5-stage ring of 40 KB, two TMEM accumulator sets (2 x 256 columns): the
+//            epilogue of one tile overlaps the main loop of the next.
+//   kN = 64: 4-stage ring of 48 KB, one accumulator set (512 columns): the producer keeps
+//            streaming the next tile's stages while the epilogue drains TMEM.
+// 8 epilogue warps (two per TMEM lane quadrant, kN / 2 columns each).  Per-tile arithmetic
+// is that of ozgemm_kernel, so every variant gives bit-identical results.
+template <int kN>
+struct OzP {
+  static constexpr int kStages = kN == 32 ? 5 : 4;
+  static constexpr int kStage = OZ_A_STAGE + OZ_S * kN * OZ_KB;
+  static constexpr int kSmem = kStages * kStage;
+  static constexpr int kAcc = OZ_S * kN;            // TMEM columns per accumulator set
+  static constexpr int kSets = kN == 32 ? 2 : 1;
+};
+constexpr int OZP_EPI_WARPS = 8;
+constexpr int OZP_THREADS = 64 + 32 * OZP_EPI_WARPS;
+
+struct OzTile {
+  int z, tm, tn, part;
+};
+
+// Tile t of the launch -> coordinates; false if the tile is skipped (trapezoid / failed item).
+template <int kN>
+__device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, long long per_z, long long t,
+                                        OzTile& o) {
+  constexpr int kParts = 128 / kN;
+  o.z = (int)(t / per_z);
+  const long long r = t - (long long)o.z * per_z;
+  const int b = (int)(r / kParts);
+  o.part = (int)(r % kParts);
+  if (g.lower) {
+    int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > b) --I;
+    while ((I + 1) * (I + 2) / 2 <= b) ++I;
+    o.tm = I;
+    o.tn = b - I * (I + 1) / 2;
+  } else {
+    o.tm = b % g.tiles_m;
+    o.tn = b / g.tiles_m;
+  }
+  if (g.trap && o.tm < o.tn) return false;
+  return *g.fail_flag[o.z] == 0;
+}
+
+template <int kN>
+__global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGemmArgs g,
+                                                                           long long per_z,
+                                                                           long long total) {
+  using Cfg = OzP<kN>;
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  __shared__ __align__(8) uint64_t full_bar[Cfg::kStages], empty_bar[Cfg::kStages];
+  __shared__ __align__(8) uint64_t acc_full[Cfg::kSets], acc_empty[Cfg::kSets];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kblocks = g.kblocks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < Cfg::kSets; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], OZP_EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      long long gk = 0;
+      for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        OzTile o;
+        if (!oz_tile<kN>(g, per_z, t, o)) continue;
+        const int8_t* Ablk = g.As[o.z] + (size_t)o.tm * kblocks * OZ_S * OZ_BLK;
+        const int8_t* Bblk = g.Bs[o.z] + (size_t)o.tn * kblocks * OZ_S * OZ_BLK +
+                             (size_t)o.part * (kN * OZ_KB);
+        for (int kb = 0; kb < kblocks; ++kb, ++gk) {
+          const int st = (int)(gk % Cfg::kStages);
+          const long long use = gk / Cfg::kStages;
+          if (use >= 1) mbar_wait(&empty_bar[st], (uint32_t)((use - 1) & 1));
+          uint8_t* sa = oz_smem + (size_t)st * Cfg::kStage;
+          uint8_t* sb = sa + OZ_A_STAGE;
+          if (g.diag_mode == 2 || g.diag_mode >= 5) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                smem_u32(&full_bar[st])) : "memory");
+            continue;
+          }
+          mbar_expect_tx(&full_bar[st], Cfg::kStage);
+          bulk_g2s(sa, Ablk + (size_t)kb * OZ_S * OZ_BLK, OZ_A_STAGE, &full_bar[st]);
+          const int8_t* bsrc = Bblk + (size_t)kb * OZ_S * OZ_BLK;
+#pragma unroll
+          for (int q = 0; q < OZ_S; ++q)
+            bulk_g2s(sb + q * (kN * OZ_KB), bsrc + (size_t)q * OZ_BLK, kN * OZ_KB,
+                     &full_bar[st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {  // MMA issuer
+    long long gk = 0, local = 0;
+    long long c_start = clock64(), c_full = 0, c_acc = 0, g_start = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+      OzTile o;
+      if (!oz_tile<kN>(g, per_z, t, o)) continue;
+      const int ab = (int)(local % Cfg::kSets);
+      const long long use = local / Cfg::kSets;
+      {
+        const long long c0 = clock64();
+        if (use >= 1) mbar_wait(&acc_empty[ab], (uint32_t)((use - 1) & 1));
+        c_acc += clock64() - c0;
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t acc = tmem + (uint32_t)(ab * Cfg::kAcc);
+      for (int kb = 0; kb < kblocks; ++kb, ++gk) {
+        const int st = (int)(gk % Cfg::kStages);
+        {
+          const long long c0 = clock64();
+          mbar_wait(&full_bar[st], (uint32_t)((gk / Cfg::kStages) & 1));
+          c_full += clock64() - c0;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(oz_smem + (size_t)st * Cfg::kStage);
+          const uint32_t sb = sa + OZ_A_STAGE;
+#pragma unroll
+          for (int p = 1; p <= OZ_S; ++p) {
+            if (g.diag_mode == 1 && !(kb == 0 && p == 1)) continue;
+            const int rows = kN * (OZ_S + 1 - p);  // B rows [B_1 .. B_{9-p}]
+            const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
+#pragma unroll
+            for (int r0 = 0; r0 < rows; r0 += 256) {
+              const int nr = rows - r0 < 256 ? rows - r0 : 256;
+              const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                     ((uint32_t)(nr >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+              asm volatile(
+                  "{ .reg .pred pp; setp.ne.b32 pp, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp; }" ::"r"(
+                      acc + (uint32_t)((p - 1) * kN + r0)),
+                  "l"(sdesc(sa + (p - 1) * OZ_BLK)), "l"(sdesc(sb + r0 * OZ_KB)), "r"(idesc),
+                  "r"(accum));
+            }
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  smem_u32(&empty_bar[st])));
+        }
+        __syncwarp();
+      }
+      if (lane == 0)
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&acc_full[ab])));
+      __syncwarp();
+      ++local;
+    }
+    if (g.diag_out && blockIdx.x == 0 && lane == 0) {
+      long long g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      g.diag_out[0] = clock64() - c_start;
+      g.diag_out[1] = c_full;
+      g.diag_out[2] = c_acc;
+      g.diag_out[3] = g_end - g_start;
+      g.diag_out[4] = local;
+      g.diag_out[5] = gk;
+    }
+  } else {  // epilogue: warp pair per TMEM lane quadrant, kN / 2 columns each
+    constexpr int kCols = kN / 2;
+    const int ew = warp - 2;
+    const int qd = warp & 3;           // lane quadrant this warp may access
+    const int ch = ew >> 2;            // column half
+    const int row = qd * 32 + lane;
+    long long local = 0;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+      OzTile o;
+      if (!oz_tile<kN>(g, per_z, t, o)) continue;
+      const int ab = (int)(local % Cfg::kSets);
+      const long long use = local / Cfg::kSets;
+      const long long r_glob = (long long)o.tm * 128 + row;
+      const long long c_glob = (long long)o.tn * 128 + (long long)o.part * kN + ch * kCols;
+      double* C = g.C[o.z] + r_glob + c_glob * g.ldc;
+      const bool acc_c = g.beta != 0.0;
+      // C prefetch before the accumulator wait (kN = 32; at kN = 64 it would spill: C is
+      // then read after TMEM is released, overlapping the next tile's MMAs)
+      constexpr int kPre = kN == 32 ? kCols : 0;
+      double cv[kPre > 0 ? kPre : 1];
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) cv[j] = acc_c ? __ldcg(C + (long long)j * g.ldc) : 0.0;
+      const double s_row = g.alpha * pow2i(g.ea[o.z][r_glob]);
+      mbar_wait(&acc_full[ab], (uint32_t)(use & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      double acc[kCols];
+#pragma unroll
+      for (int c0 = 0; c0 < kCols; c0 += 16) {
+        double part[16];
+        if (g.diag_mode != 3 && g.diag_mode < 5)
+          oz_combine16(tmem + ((uint32_t)(qd * 32) << 16) +
+                           (uint32_t)(ab * Cfg::kAcc + ch * kCols + c0),
+                       kN, part);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          acc[c0 + j] = (g.diag_mode != 3 && g.diag_mode < 5) ? part[j] : 0.0;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_empty[ab]))
+                     : "memory");
+      const int* eb = g.eb[o.z] + c_glob;
+      if (g.diag_mode == 6) {
+        ++local;
+        continue;
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < kCols; c0 += 16) {
+        double cw[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          cw[j] = kPre > 0 ? cv[(c0 + j) % (kPre > 0 ? kPre : 1)]
+                           : (acc_c ? __ldcg(C + (long long)(c0 + j) * g.ldc) : 0.0);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          __stcg(C + (long long)(c0 + j) * g.ldc,
+                 cw[j] + (acc[c0 + j] * s_row) * pow2i(__ldg(eb + c0 + j)));
+      }
+      ++local;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+int g_num_sms = 148;
+
 cudaError_t init_ozaki_attributes() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<32>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        OzP<32>::kSmem);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<64>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, OzP<64>::kSmem);
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaFuncSetAttribute(oz_slice_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSliceSmem);
   if (e != cudaSuccess) return e;
@@ -365,7 +653,17 @@ cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_
   const long long tiles =
       g.lower ? (long long)g.tiles_m * (g.tiles_m + 1) / 2 : (long long)g.tiles_m * g.tiles_n;
   if (tiles <= 0) return cudaSuccess;
-  if (n_tile == 64) {
+  if (n_tile == 0 || n_tile == 1) {  // persistent: 0 -> 128 x 64 tiles, 1 -> 128 x 32
+    const int kn = n_tile == 0 ? 64 : 32;
+    const long long per_z = tiles * (128 / kn), total = per_z * batch;
+    const long long grid = std::min<long long>(total, g_num_sms);
+    if (kn == 64)
+      ozgemm_persistent_kernel<64><<<(unsigned)grid, OZP_THREADS, OzP<64>::kSmem, s>>>(
+          g, per_z, total);
+    else
+      ozgemm_persistent_kernel<32><<<(unsigned)grid, OZP_THREADS, OzP<32>::kSmem, s>>>(
+          g, per_z, total);
+  } else if (n_tile == 64) {
     ozgemm_kernel<64><<<dim3((unsigned)(2 * tiles), 1, (unsigned)batch), OZ_THREADS,
                         OzCfg<64>::kSmem, s>>>(g);
   } else {

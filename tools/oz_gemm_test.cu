@@ -13,7 +13,7 @@
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e_), __LINE__); exit(1);} } while (0)
 
 using namespace mle;
-static int g_ntile = 32;
+static int g_ntile = 0;
 
 struct Case {
   const char* name;
@@ -93,16 +93,19 @@ static double run_case(const Case& cs, int batch, int reps) {
   std::vector<double> C1(C.size()), C2(C.size());
   CK(cudaMemcpy(C1.data(), dC1, C.size() * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(C2.data(), dC2, C.size() * 8, cudaMemcpyDeviceToHost));
-  {  // the other tile width must give bit-identical results
+  for (int other : {0, 1, 32, 64}) {  // every kernel variant must give bit-identical results
+    if (other == g_ntile) continue;
     CK(cudaMemcpy(dC2, C.data(), C.size() * 8, cudaMemcpyHostToDevice));
-    CK(launch_ozgemm(o, 1, 0, 96 - g_ntile));
+    CK(launch_ozgemm(o, 1, 0, other));
+    CK(cudaDeviceSynchronize());
     std::vector<double> C3(C.size());
     CK(cudaMemcpy(C3.data(), dC2, C.size() * 8, cudaMemcpyDeviceToHost));
     long diff = 0;
     for (int j = 0; j < N; ++j)
       for (int i = cs.lower ? j : 0; i < M; ++i) diff += C3[i + (size_t)j * M] != C2[i + (size_t)j * M];
-    if (diff) printf("  !! n_tile 32 vs 64: %ld differing entries\n", diff);
+    if (diff) printf("  !! n_tile %d vs %d: %ld differing entries\n", g_ntile, other, diff);
   }
+  CK(cudaMemcpy(dC2, C.data(), C.size() * 8, cudaMemcpyHostToDevice));
   double e1 = 0, e2 = 0, e12 = 0;
   std::uniform_int_distribution<int> ri(0, M - 1), rj(0, N - 1);
   for (int t = 0; t < 20000; ++t) {
@@ -145,6 +148,54 @@ static double run_case(const Case& cs, int batch, int reps) {
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     cudaEventElapsedTime(&t_o, a, b);
+  }
+  if (g_ntile <= 1) {  // diagnostics: loads only / MMAs only
+    float t1, t2;
+    o.diag_mode = 1;
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch_ozgemm(o, batch, 0, g_ntile);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&t1, a, b);
+    o.diag_mode = 2;
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch_ozgemm(o, batch, 0, g_ntile);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&t2, a, b);
+    float t3;
+    o.diag_mode = 3;
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch_ozgemm(o, batch, 0, g_ntile);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&t3, a, b);
+    float t5;
+    o.diag_mode = 5;
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch_ozgemm(o, batch, 0, g_ntile);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&t5, a, b);
+    long long* dd;
+    CK(cudaMalloc(&dd, 8 * sizeof(long long)));
+    o.diag_out = dd;
+    for (int mode : {0, 5, 6}) {
+      o.diag_mode = mode;
+      launch_ozgemm(o, batch, 0, g_ntile);
+      long long h[8];
+      CK(cudaMemcpy(h, dd, sizeof(h), cudaMemcpyDeviceToHost));
+      printf("  mma thread (mode %d): %lld cycles, %.3f ms -> %.0f MHz | full-wait %.1f%% | "
+             "acc-wait %.1f%% | %lld tiles, %lld k blocks -> %.0f cycles/k block\n", mode, h[0],
+             h[3] * 1e-6, (double)h[0] / (h[3] * 1e-3), 100.0 * h[1] / h[0], 100.0 * h[2] / h[0],
+             h[4], h[5], (double)h[0] / h[5]);
+    }
+    o.diag_out = nullptr;
+    cudaFree(dd);
+    o.diag_mode = 0;
+    printf("  diag: full %.3f ms | loads+epilogue only %.3f ms | MMAs+epilogue only %.3f ms | "
+           "no TMEM epilogue %.3f ms | MMAs only %.3f ms\n", t_o / reps, t1 / reps, t2 / reps,
+           t3 / reps, t5 / reps);
   }
   CK(cudaGetLastError());
   printf("%-10s M=%5d N=%5d K=%d batch=%d | err/scale dmma %.2e ozaki %.2e diff %.2e | "
