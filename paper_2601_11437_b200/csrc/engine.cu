@@ -237,8 +237,16 @@ struct mle_ctx {
   bool ozaki = true;              // MLE_FP64_GEMM=dmma at context creation disables it
   int8_t* lsl = nullptr;          // slices of every outer panel of L
   int* lex = nullptr;             // their row exponents
-  int8_t* xsl = nullptr;          // solve-operand slices, one region per derivative matrix
+  int8_t* xsl = nullptr;          // solve-operand slices: 2 regions per derivative matrix
   int* xex = nullptr;
+  // block-inverse solves: D_b^-1 per outer block (ld 512, zero upper), scratch, W_b slices
+  double* dinv = nullptr;
+  double* tscr = nullptr;
+  double* wbuf = nullptr;
+  int8_t* dtsl = nullptr;
+  int* dtex = nullptr;
+  int8_t* wsl = nullptr;
+  int* wex = nullptr;
   // Kernel profiling (mle_kernel_profile): single stream, CUDA events around every Ozaki
   // GEMM and slicing launch of the pass; mle_kernel_stats reports the sums.
   bool kprof = false;
@@ -282,6 +290,20 @@ long long oz_panel_row_offset(int Nt, int ob) {  // rows of the panels before ob
   for (int o = 0; o < ob; ++o) r += oz_panel_rows(Nt, o);
   return r;
 }
+// W_b of outer block b: rows [c0, N) x kb; byte and row offsets of its slices.
+long long w_row_offset(int Nt, int b) {
+  long long r = 0;
+  for (int o = 0; o < b; ++o) r += (long long)(Nt - o * kOuter) * kNB;
+  return r;
+}
+size_t w_byte_offset(int Nt, int b) {
+  size_t r = 0;
+  for (int o = 0; o < b; ++o) {
+    const long long kb = (long long)(std::min(Nt, (o + 1) * kOuter) - o * kOuter) * kNB;
+    r += (size_t)(Nt - o * kOuter) * kNB * kb * kOzSlices;
+  }
+  return r;
+}
 constexpr int kOzK = kOuter * kNB;               // K of every trailing update
 constexpr size_t kOzRowBytes = (size_t)kOzK * kOzSlices;
 constexpr size_t kOzTileBytes = kOzRowBytes * kNB;
@@ -294,8 +316,19 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
     CUDA_TRY(dmalloc(&c->lex, sizeof(int) * std::max<long long>(1, rows)));
   }
   if (derivs && !c->xsl) {
-    CUDA_TRY(dmalloc(&c->xsl, 2 * (size_t)c->N * kOzRowBytes));
-    CUDA_TRY(dmalloc(&c->xex, 2 * sizeof(int) * (size_t)c->N));
+    const int nb = (c->Nt + kOuter - 1) / kOuter;
+    CUDA_TRY(dmalloc(&c->xsl, 4 * (size_t)c->N * kOzRowBytes));
+    CUDA_TRY(dmalloc(&c->xex, 4 * sizeof(int) * (size_t)c->N));
+    CUDA_TRY(dmalloc(&c->dinv, sizeof(double) * (size_t)nb * 512 * 512));
+    CUDA_TRY(dmalloc(&c->tscr, sizeof(double) * (size_t)nb * kNB * 512));
+    CUDA_TRY(dmalloc(&c->wbuf, sizeof(double) * (size_t)c->N * 512));
+    CUDA_TRY(dmalloc(&c->dtsl, (size_t)512 * kOzRowBytes));
+    CUDA_TRY(dmalloc(&c->dtex, sizeof(int) * 512));
+    CUDA_TRY(dmalloc(&c->wsl, std::max<size_t>(1, w_byte_offset(c->Nt, nb))));
+    CUDA_TRY(dmalloc(&c->wex, sizeof(int) * std::max<long long>(1, w_row_offset(c->Nt, nb))));
+    // the upper tiles of every D_b^-1 are never written and must read as exact zeros
+    CUDA_TRY(cudaMemsetAsync(c->dinv, 0, sizeof(double) * (size_t)nb * 512 * 512, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
   return MLE_OK;
 }
@@ -536,6 +569,269 @@ struct Launcher {
   // B_i = L^-1 S_i L^-T (lower half) for both derivative matrices of every item, in place.
   // GEMM batch member z = 2 * item + {0: alpha, 1: nu}.
   int solves(mle_ctx* const* cs, int m) {
+    if (cs[0]->wsl) {
+      int rc = compute_w(cs, m);
+      if (rc) return rc;
+      return solves_w(cs, m);
+    }
+    return solves_dmma(cs, m);
+  }
+
+  // ---- block-inverse formulation on the Ozaki GEMM ----------------------------------
+  // For outer block b (tiles [t0, t1), columns [c0, c1), kb = c1 - c0) with diagonal block
+  // D_b = L[c0:c1, c0:c1] and panel P_b = L[c1:, c0:c1], let
+  //     W_b = [ D_b^-1 ; -P_b D_b^-1 ]            (rows c0 .. N, kb columns).
+  // Forward sweep X = L^-1 S, block b:  X[c0:, :] = W_b X[c0:c1, :] with the top kb rows
+  //   overwritten (D_b^-1 S_b) and the rows below accumulated (-P_b D_b^-1 S_b).
+  // Right sweep B = X L^-T (lower half), block b:  X[i, c0:] += X[i, c0:c1] W_b^T, the
+  //   first kb columns overwritten (X D_b^-T = B[:, b]) and later columns accumulated
+  //   (-B[:, b] P_b^T).
+  // Each block of each sweep is one slicing + one Ozaki GEMM (split (i)/(ii) for look-ahead);
+  // the 128-wide DMMA inner steps disappear.
+  struct Blk {
+    int t0, t1;
+    long long c0, kb;
+  };
+  static Blk blk(int Nt, int b) {
+    Blk o;
+    o.t0 = b * kOuter;
+    o.t1 = std::min(Nt, o.t0 + kOuter);
+    o.c0 = (long long)o.t0 * kNB;
+    o.kb = (long long)(o.t1 - o.t0) * kNB;
+    return o;
+  }
+
+  // D_b^-1 for every outer block (DMMA, from the Linv tiles) and the slices of W_b.
+  int compute_w(mle_ctx* const* cs, int m) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    const int nb = (Nt + kOuter - 1) / kOuter;
+    int rc;
+    {
+      double* dv[kMaxItems];
+      const double* lv[kMaxItems];
+      for (int it = 0; it < m; ++it) {
+        dv[it] = cs[it]->dinv;
+        lv[it] = cs[it]->linv;
+      }
+      launches += 1;
+      CUDA_TRY(launch_linv_to_dinv(dv, lv, Nt, m, s));
+    }
+    // tile row i of every block:  T = L[i, 0:i] Dinv[0:i, 0:i];  Dinv[i, 0:i] = -Linv_i T
+    for (int i = 1; i < kOuter; ++i) {
+      struct Ent {
+        const double* lrow;
+        double* dinv_b;
+        double* T;
+        const double* linv_i;
+        const int* flag;
+      };
+      std::vector<Ent> ents;
+      for (int b = 0; b < nb; ++b) {
+        const Blk k = blk(Nt, b);
+        if (k.t1 - k.t0 <= i) continue;
+        for (int it = 0; it < m; ++it)
+          ents.push_back({cs[it]->sigma + (k.c0 + i * kNB) + k.c0 * ld,
+                          cs[it]->dinv + (size_t)b * 512 * 512,
+                          cs[it]->tscr + (size_t)b * kNB * 512,
+                          cs[it]->linv + (size_t)(k.t0 + i) * kNB * kNB, cs[it]->fail_flag});
+      }
+      for (size_t e0 = 0; e0 < ents.size(); e0 += kMaxGemm) {
+        const int cnt = (int)std::min<size_t>(kMaxGemm, ents.size() - e0);
+        GemmArgs t = gemm_base(), u = gemm_base();
+        for (int z = 0; z < cnt; ++z) {
+          const Ent& e = ents[e0 + z];
+          t.A[z] = e.lrow;    // 128 x 128 i, lda = N
+          t.B[z] = e.dinv_b;  // B(n, k) = Dinv(k, n)  (kBKN, ldb 512)
+          t.C[z] = e.T;
+          t.fail_flag[z] = e.flag;
+          u.A[z] = e.linv_i;  // Linv_i (128 x 128)
+          u.B[z] = e.T;       // B(n, k) = T(k, n)  (kBKN, ldb 128)
+          u.C[z] = e.dinv_b + i * kNB;
+          u.fail_flag[z] = e.flag;
+        }
+        t.lda = ld; t.ldb = 512; t.ldc = kNB; t.K = i * kNB;
+        t.tiles_m = 1; t.tiles_n = i; t.alpha = 1.0; t.beta = 0.0;
+        if ((rc = gemm(t, kBKN, cnt))) return rc;
+        u.lda = kNB; u.ldb = kNB; u.ldc = 512; u.K = kNB;
+        u.tiles_m = 1; u.tiles_n = i; u.alpha = -1.0; u.beta = 0.0;
+        if ((rc = gemm(u, kBKN, cnt))) return rc;
+      }
+    }
+    // slices of W_b, block by block (the FP64 bottom part reuses one scratch)
+    for (int b = 0; b < nb; ++b) {
+      const Blk k = blk(Nt, b);
+      const long long c1 = k.c0 + k.kb;
+      const size_t woff = w_byte_offset(Nt, b);
+      const long long eoff = w_row_offset(Nt, b);
+      const size_t tile_bytes = (size_t)kNB * k.kb * kOzSlices;
+      OzSliceArgs top;  // rows of D_b^-1 (row-contig, ld 512)
+      std::memset(&top, 0, sizeof(top));
+      for (int it = 0; it < m; ++it) {
+        top.X[it] = cs[it]->dinv + (size_t)b * 512 * 512;
+        top.slices[it] = cs[it]->wsl + woff;
+        top.e[it] = cs[it]->wex + eoff;
+        top.fail_flag[it] = cs[it]->fail_flag;
+      }
+      top.ld = 512;
+      top.K = (int)k.kb;
+      if ((rc = slice(top, k.kb, true, m))) return rc;
+      if (c1 >= ld) continue;
+      OzSliceArgs dt;  // B(j, kk) = Dinv(kk, j): D_b^-T rows (k-contig, ld 512)
+      std::memset(&dt, 0, sizeof(dt));
+      for (int it = 0; it < m; ++it) {
+        dt.X[it] = cs[it]->dinv + (size_t)b * 512 * 512;
+        dt.slices[it] = cs[it]->dtsl;
+        dt.e[it] = cs[it]->dtex;
+        dt.fail_flag[it] = cs[it]->fail_flag;
+      }
+      dt.ld = 512;
+      dt.K = (int)k.kb;
+      if ((rc = slice(dt, k.kb, false, m))) return rc;
+      const long long eo = oz_panel_row_offset(Nt, b);
+      OzGemmArgs g = oz_base(ld, (int)((ld - c1) / kNB), (int)(k.kb / kNB));
+      g.kblocks = (int)(k.kb / 32);
+      g.beta = 0.0;  // C = -P_b D_b^-1
+      for (int it = 0; it < m; ++it) {
+        g.As[it] = cs[it]->lsl + (size_t)eo * kOzRowBytes;
+        g.ea[it] = cs[it]->lex + eo;
+        g.Bs[it] = cs[it]->dtsl;
+        g.eb[it] = cs[it]->dtex;
+        g.C[it] = cs[it]->wbuf;
+        g.fail_flag[it] = cs[it]->fail_flag;
+      }
+      if ((rc = ozgemm(g, m, s))) return rc;
+      OzSliceArgs bot;
+      std::memset(&bot, 0, sizeof(bot));
+      for (int it = 0; it < m; ++it) {
+        bot.X[it] = cs[it]->wbuf;
+        bot.slices[it] = cs[it]->wsl + woff + (size_t)(k.t1 - k.t0) * tile_bytes;
+        bot.e[it] = cs[it]->wex + eoff + k.kb;
+        bot.fail_flag[it] = cs[it]->fail_flag;
+      }
+      bot.ld = ld;
+      bot.K = (int)k.kb;
+      if ((rc = slice(bot, ld - c1, true, m))) return rc;
+    }
+    return MLE_OK;
+  }
+
+  int solves_w(mle_ctx* const* cs, int m) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    const int nb = (Nt + kOuter - 1) / kOuter;
+    const int zb = 2 * m;
+    auto S = [&](int z) { return z % 2 == 0 ? cs[z / 2]->sa : cs[z / 2]->sn; };
+    auto flag = [&](int z) { return (const int*)cs[z / 2]->fail_flag; };
+    // solve-operand slices: two regions per matrix, alternating by block (look-ahead)
+    auto XS = [&](int z, int b) {
+      return cs[z / 2]->xsl + ((size_t)(z % 2) * 2 + (b & 1)) * ld * kOzRowBytes;
+    };
+    auto XE = [&](int z, int b) {
+      return cs[z / 2]->xex + ((size_t)(z % 2) * 2 + (b & 1)) * ld;
+    };
+    int rc;
+    // forward sweep, row blocks top-down
+    for (int b = 0; b < nb; ++b) {
+      const Blk k = blk(Nt, b);
+      const int t2 = std::min(Nt, k.t1 + kOuter);
+      const size_t woff = w_byte_offset(Nt, b);
+      const long long eoff = w_row_offset(Nt, b);
+      const size_t tile_bytes = (size_t)kNB * k.kb * kOzSlices;
+      OzSliceArgs sa;  // B(n, kk) = X[c0 + kk, n]
+      std::memset(&sa, 0, sizeof(sa));
+      for (int z = 0; z < zb; ++z) {
+        sa.X[z] = S(z) + k.c0;
+        sa.slices[z] = XS(z, b);
+        sa.e[z] = XE(z, b);
+        sa.fail_flag[z] = flag(z);
+      }
+      sa.ld = ld;
+      sa.K = (int)k.kb;
+      if ((rc = slice(sa, ld, false, zb))) return rc;
+      if ((rc = join(s2, s))) return rc;  // (ii) of the previous block wrote rows of (i)
+      OzGemmArgs t = oz_base(ld, t2 - k.t0, Nt);  // (i): rows [c0, c2)
+      t.kblocks = (int)(k.kb / 32);
+      t.alpha = 1.0;
+      t.beta0_tm = k.t1 - k.t0;
+      for (int z = 0; z < zb; ++z) {
+        t.As[z] = cs[z / 2]->wsl + woff;
+        t.ea[z] = cs[z / 2]->wex + eoff;
+        t.Bs[z] = XS(z, b);
+        t.eb[z] = XE(z, b);
+        t.C[z] = S(z) + k.c0;
+        t.fail_flag[z] = flag(z);
+      }
+      if ((rc = ozgemm(t, zb, s))) return rc;
+      if (t2 >= Nt) continue;
+      if ((rc = join(s, s2))) return rc;
+      OzGemmArgs u = t;  // (ii): rows [c2, N)
+      u.tiles_m = Nt - t2;
+      u.beta0_tm = 0;
+      for (int z = 0; z < zb; ++z) {
+        u.As[z] = t.As[z] + (size_t)(t2 - k.t0) * tile_bytes;
+        u.ea[z] = t.ea[z] + (size_t)(t2 - k.t0) * kNB;
+        u.C[z] = S(z) + (long long)t2 * kNB;
+      }
+      if ((rc = ozgemm(u, zb, bulk()))) return rc;
+    }
+    if ((rc = join(s2, s))) return rc;
+    // right sweep, column blocks left to right, lower tiles only
+    for (int b = 0; b < nb; ++b) {
+      const Blk k = blk(Nt, b);
+      const int t2 = std::min(Nt, k.t1 + kOuter);
+      const size_t woff = w_byte_offset(Nt, b);
+      const long long eoff = w_row_offset(Nt, b);
+      const size_t tile_bytes = (size_t)kNB * k.kb * kOzSlices;
+      OzSliceArgs sa;  // A(i, kk) = X[c0 + i, c0 + kk], kk <= i only
+      std::memset(&sa, 0, sizeof(sa));
+      for (int z = 0; z < zb; ++z) {
+        sa.X[z] = S(z) + k.c0 + k.c0 * ld;
+        sa.slices[z] = XS(z, b);
+        sa.e[z] = XE(z, b);
+        sa.fail_flag[z] = flag(z);
+      }
+      sa.ld = ld;
+      sa.K = (int)k.kb;
+      sa.upper_zero = 1;
+      if ((rc = slice(sa, ld - k.c0, true, zb))) return rc;
+      if ((rc = join(s2, s))) return rc;
+      OzGemmArgs t = oz_base(ld, Nt - k.t0, t2 - k.t0);  // (i): columns [c0, c2)
+      t.kblocks = (int)(k.kb / 32);
+      t.trap = 1;
+      t.alpha = 1.0;
+      t.beta0_tn = k.t1 - k.t0;
+      for (int z = 0; z < zb; ++z) {
+        t.As[z] = XS(z, b);
+        t.ea[z] = XE(z, b);
+        t.Bs[z] = cs[z / 2]->wsl + woff;
+        t.eb[z] = cs[z / 2]->wex + eoff;
+        t.C[z] = S(z) + k.c0 + k.c0 * ld;
+        t.fail_flag[z] = flag(z);
+      }
+      if ((rc = ozgemm(t, zb, s))) return rc;
+      if (t2 >= Nt) continue;
+      if ((rc = join(s, s2))) return rc;
+      OzGemmArgs u = oz_base(ld, Nt - t2, 0);  // (ii): lower tiles of [c2, N)
+      u.kblocks = t.kblocks;
+      u.lower = 1;
+      u.alpha = 1.0;
+      const long long c2 = (long long)t2 * kNB;
+      for (int z = 0; z < zb; ++z) {
+        u.As[z] = t.As[z] + (size_t)(t2 - k.t0) * tile_bytes;
+        u.ea[z] = t.ea[z] + (size_t)(t2 - k.t0) * kNB;
+        u.Bs[z] = t.Bs[z] + (size_t)(t2 - k.t0) * tile_bytes;
+        u.eb[z] = t.eb[z] + (size_t)(t2 - k.t0) * kNB;
+        u.C[z] = S(z) + c2 + c2 * ld;
+        u.fail_flag[z] = flag(z);
+      }
+      if ((rc = ozgemm(u, zb, bulk()))) return rc;
+    }
+    return join(s2, s);
+  }
+
+  // DMMA path (MLE_FP64_GEMM=dmma): 128-wide inner steps + K = 512 outer updates.
+  int solves_dmma(mle_ctx* const* cs, int m) {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
     const int zb = 2 * m;
@@ -545,11 +841,6 @@ struct Launcher {
       return (const double*)(cs[z / 2]->linv + (size_t)k * kNB * kNB);
     };
     auto flag = [&](int z) { return (const int*)cs[z / 2]->fail_flag; };
-    const bool oz = cs[0]->lsl != nullptr && cs[0]->xsl != nullptr;
-    auto LS = [&](int z) { return (const int8_t*)cs[z / 2]->lsl; };
-    auto LE = [&](int z) { return (const int*)cs[z / 2]->lex; };
-    auto XS = [&](int z) { return cs[z / 2]->xsl + (size_t)(z % 2) * ld * kOzRowBytes; };
-    auto XE = [&](int z) { return cs[z / 2]->xex + (size_t)(z % 2) * ld; };
     int rc;
     // forward sweep X = L^-1 S (all columns), row blocks top-down
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
@@ -584,43 +875,6 @@ struct Launcher {
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
       if ((rc = join(s2, s))) return rc;
-      if (oz) {
-        // A = factor panel ob (sliced by the Cholesky), B(n, k) = X[c0 + k, n]
-        const int ob = b0 / kOuter;
-        const long long eo = oz_panel_row_offset(Nt, ob);
-        OzSliceArgs sa;
-        std::memset(&sa, 0, sizeof(sa));
-        for (int z = 0; z < zb; ++z) {
-          sa.X[z] = S(z) + c0;
-          sa.slices[z] = XS(z);
-          sa.e[z] = XE(z);
-          sa.fail_flag[z] = flag(z);
-        }
-        sa.ld = ld;
-        sa.K = kOzK;
-        if ((rc = slice(sa, ld, false, zb))) return rc;
-        OzGemmArgs t = oz_base(ld, b2 - b1, Nt);  // (i): rows [b1, b2)
-        for (int z = 0; z < zb; ++z) {
-          t.As[z] = LS(z) + (size_t)eo * kOzRowBytes;
-          t.ea[z] = LE(z) + eo;
-          t.Bs[z] = XS(z);
-          t.eb[z] = XE(z);
-          t.C[z] = S(z) + t0;
-          t.fail_flag[z] = flag(z);
-        }
-        if ((rc = ozgemm(t, zb, s))) return rc;
-        if (b2 >= Nt) continue;
-        if ((rc = join(s, s2))) return rc;
-        OzGemmArgs u = t;                          // (ii): rows >= b2
-        u.tiles_m = Nt - b2;
-        for (int z = 0; z < zb; ++z) {
-          u.As[z] = t.As[z] + (size_t)(b2 - b1) * kOzTileBytes;
-          u.ea[z] = t.ea[z] + (size_t)(b2 - b1) * kNB;
-          u.C[z] = S(z) + u0;
-        }
-        if ((rc = ozgemm(u, zb, bulk()))) return rc;
-        continue;
-      }
       GemmArgs t = gemm_base();   // (i): rows [b1, b2), all columns
       for (int z = 0; z < zb; ++z) {
         t.A[z] = L(z) + t0 + c0 * ld;   // L[b1:b2, b0:b1]
@@ -680,48 +934,6 @@ struct Launcher {
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
       if ((rc = join(s2, s))) return rc;
-      if (oz) {
-        // A = B[T, b0:b1] (sliced here), B = factor panel ob
-        const int ob = b0 / kOuter;
-        const long long eo = oz_panel_row_offset(Nt, ob);
-        OzSliceArgs sa;
-        std::memset(&sa, 0, sizeof(sa));
-        for (int z = 0; z < zb; ++z) {
-          sa.X[z] = S(z) + t0 + c0 * ld;
-          sa.slices[z] = XS(z);
-          sa.e[z] = XE(z);
-          sa.fail_flag[z] = flag(z);
-        }
-        sa.ld = ld;
-        sa.K = kOzK;
-        if ((rc = slice(sa, (long long)(Nt - b1) * kNB, true, zb))) return rc;
-        OzGemmArgs t = oz_base(ld, Nt - b1, b2 - b1);  // (i)
-        t.trap = 1;
-        for (int z = 0; z < zb; ++z) {
-          t.As[z] = XS(z);
-          t.ea[z] = XE(z);
-          t.Bs[z] = LS(z) + (size_t)eo * kOzRowBytes;
-          t.eb[z] = LE(z) + eo;
-          t.C[z] = S(z) + t0 + t0 * ld;
-          t.fail_flag[z] = flag(z);
-        }
-        if ((rc = ozgemm(t, zb, s))) return rc;
-        if (b2 >= Nt) continue;
-        if ((rc = join(s, s2))) return rc;
-        OzGemmArgs u = oz_base(ld, Nt - b2, 0);         // (ii): lower tiles of [b2, Nt)
-        u.lower = 1;
-        for (int z = 0; z < zb; ++z) {
-          const size_t to = (size_t)(b2 - b1);
-          u.As[z] = t.As[z] + to * kOzTileBytes;
-          u.ea[z] = t.ea[z] + to * kNB;
-          u.Bs[z] = t.Bs[z] + to * kOzTileBytes;
-          u.eb[z] = t.eb[z] + to * kNB;
-          u.C[z] = S(z) + u0 + u0 * ld;
-          u.fail_flag[z] = flag(z);
-        }
-        if ((rc = ozgemm(u, zb, bulk()))) return rc;
-        continue;
-      }
       GemmArgs t = gemm_base();   // (i): columns [b1, b2), rows >= b1
       for (int z = 0; z < zb; ++z) {
         t.A[z] = S(z) + t0 + c0 * ld;   // B[T, b0:b1]
@@ -1094,6 +1306,13 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->lex);
   dfree(c->xsl);
   dfree(c->xex);
+  dfree(c->dinv);
+  dfree(c->tscr);
+  dfree(c->wbuf);
+  dfree(c->dtsl);
+  dfree(c->dtex);
+  dfree(c->wsl);
+  dfree(c->wex);
   if (c->h_theta) dfree(c->h_theta);
   if (c->h_res) dfree(c->h_res);
   for (auto& e : c->ev)

@@ -15,7 +15,7 @@ namespace mle {
 
 constexpr int kNB = 128;       // factorization tile (Cholesky / solve block size)
 constexpr int kMaxItems = 8;   // datasets per batched launch
-constexpr int kMaxGemm = 2 * kMaxItems;
+constexpr int kMaxGemm = 8 * kMaxItems;  // batch members per GEMM launch (item x block)
 
 struct GenItem {
   const ThetaParams* P;  // device copy of this item's per-theta scalars
@@ -92,6 +92,11 @@ cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s);
 // Reductions: per item 9 results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>, yBy_A, yBy_N].
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
 
+// Scatter the diagonal-tile inverses Linv_k into the per-outer-block inverse storage:
+// dinv[z] + (k / 4) 512^2 + (k % 4) 128 (1 + 512)  <-  linv[z] + k 128^2   (k < Nt).
+cudaError_t launch_linv_to_dinv(double* const* dinv, const double* const* linv, int Nt,
+                                int items, cudaStream_t s);
+
 // z = L w over the leading n x n block of a resident Cholesky factor.
 cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double* w, double* z,
                               cudaStream_t s);
@@ -107,6 +112,8 @@ struct OzSliceArgs {
   const int* fail_flag[kMaxGemm];
   long long ld;
   int K;
+  int upper_zero;  // 1: element (r, k) with k > r (same origin) is taken as 0
+  int rows_z[kMaxGemm];  // per-member row count (0: the launch's rows)
 };
 // C = alpha * A B^T + beta * C from slices (A: M rows, B: N rows, both over the same K).
 struct OzGemmArgs {
@@ -122,6 +129,8 @@ struct OzGemmArgs {
   int tiles_n;   // 128-column tiles (full mode)
   int lower, trap;
   double alpha, beta;
+  int beta0_tm, beta0_tn;  // tiles with tm < beta0_tm or tn < beta0_tn overwrite (beta = 0)
+  int tiles_m_z[kMaxGemm];  // full/trap mode: per-member row tiles (0: tiles_m)
   int diag_mode;  // developer diagnostics only: 1 skip the MMAs, 2 skip the loads (0: normal)
   long long* diag_out;  // developer diagnostics: MMA-thread timing of CTA 0 (null: off)
 };

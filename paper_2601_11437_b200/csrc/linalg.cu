@@ -635,4 +635,30 @@ cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double
   return cudaGetLastError();
 }
 
+struct LinvDinvArgs {
+  double* dinv[kMaxItems];
+  const double* linv[kMaxItems];
+};
+
+__global__ void __launch_bounds__(256) linv_to_dinv_kernel(LinvDinvArgs a) {
+  const int k = blockIdx.x, z = blockIdx.y;
+  const double* src = a.linv[z] + (size_t)k * kNB * kNB;
+  double* dst = a.dinv[z] + (size_t)(k / 4) * 512 * 512 + (size_t)(k % 4) * kNB * (1 + 512);
+  for (int e = threadIdx.x; e < kNB * kNB; e += 256) {
+    const int r = e & (kNB - 1), c = e / kNB;
+    dst[r + (size_t)c * 512] = src[e];
+  }
+}
+
+cudaError_t launch_linv_to_dinv(double* const* dinv, const double* const* linv, int Nt,
+                                int items, cudaStream_t s) {
+  LinvDinvArgs a;
+  for (int z = 0; z < items; ++z) {
+    a.dinv[z] = dinv[z];
+    a.linv[z] = linv[z];
+  }
+  linv_to_dinv_kernel<<<dim3((unsigned)Nt, (unsigned)items), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace mle

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzSliceArgs sa) {
   const long long ld = sa.ld;
   const int K = sa.K, t = threadIdx.x, w = t >> 5, l = t & 31;
   const long long r0 = (long long)blockIdx.x * kOzSliceRows;
+  if (sa.rows_z[z] > 0 && r0 >= sa.rows_z[z]) return;
   if (kRowContig) {  // X(r,k) = X[r + k ld]: lanes along r
     for (int k = w; k < K; k += 8) tile[l * kOzSliceStride + k] = X[r0 + l + (long long)k * ld];
   } else {           // X(r,k) = X[k + r ld]: lanes along k
@@ -155,6 +156,12 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzSliceArgs sa) {
       const double* row = X + (r0 + r) * ld;
       for (int k = l; k < K; k += 32) tile[r * kOzSliceStride + k] = row[k];
     }
+  }
+  if (sa.upper_zero) {  // only the lower trapezoid k <= r is valid: zero the rest
+    __syncthreads();
+    for (int r = w; r < kOzSliceRows; r += 8)
+      for (int k = l; k < K; k += 32)
+        if (k > r0 + r) tile[r * kOzSliceStride + k] = 0.0;
   }
   __syncthreads();
   for (int r = w; r < kOzSliceRows; r += 8) {
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(OZ_THREADS, OzCfg<kN>::kCtasPerSm) ozgemm_kern
     double* C = g.C[z] + r_glob + c_glob * g.ldc;
     const int* eb = g.eb[z] + c_glob;
     const double alpha = g.alpha;
-    const bool acc_c = g.beta != 0.0;
+    const bool acc_c = g.beta != 0.0 && tm >= g.beta0_tm && tn >= g.beta0_tn;
     const double s_row = alpha * pow2i(g.ea[z][r_glob]);
     constexpr int kPre = kN == 32 ? 32 : 16;  // C values prefetched before the main loop ends
     double cpre[kPre];
@@ -406,6 +413,7 @@ __device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, long long per_z, lo
   } else {
     o.tm = b % g.tiles_m;
     o.tn = b / g.tiles_m;
+    if (g.tiles_m_z[o.z] > 0 && o.tm >= g.tiles_m_z[o.z]) return false;
   }
   if (g.trap && o.tm < o.tn) return false;
   return *g.fail_flag[o.z] == 0;
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       const long long r_glob = (long long)o.tm * 128 + row;
       const long long c_glob = (long long)o.tn * 128 + (long long)o.part * kN + ch * kCols;
       double* C = g.C[o.z] + r_glob + c_glob * g.ldc;
-      const bool acc_c = g.beta != 0.0;
+      const bool acc_c = g.beta != 0.0 && o.tm >= g.beta0_tm && o.tn >= g.beta0_tn;
       // C prefetch before the accumulator wait (kN = 32; at kN = 64 it would spill: C is
       // then read after TMEM is released, overlapping the next tile's MMAs)
       constexpr int kPre = kN == 32 ? kCols : 0;
