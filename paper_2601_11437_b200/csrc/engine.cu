@@ -192,6 +192,11 @@ int ensure_device(int device) {
 
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
+bool use_speculation() {
+  const char* v = std::getenv("MLE_SPECULATE");
+  return !(v && std::strcmp(v, "0") == 0);
+}
+
 // FP64 trailing-update GEMM: Ozaki int8 tensor-core emulation (default) or DMMA.
 bool use_ozaki() {
   const char* v = std::getenv("MLE_FP64_GEMM");
@@ -225,6 +230,7 @@ struct mle_ctx {
   ThetaParams* h_theta = nullptr; // pinned staging
   double* h_res = nullptr;        // pinned: 9 results + fail flag + fail idx
   cudaEvent_t ev[5] = {};
+  cudaEvent_t ev_der = nullptr;   // derivative generation for this pass's eval_all items
   double phase_ms[MLE_NUM_PHASES] = {};
   double flops = 0.0;
   double gen_bytes = 0.0;
@@ -251,6 +257,14 @@ struct mle_ctx {
   // GEMM and slicing launch of the pass; mle_kernel_stats reports the sums.
   bool kprof = false;
   std::vector<cudaEvent_t> kev;
+  // Speculation: a loglik pass that factors Sigma(theta) also generates dSigma/dalpha,
+  // dSigma/dnu and the W_b slices on the aux stream (overlapping the latency-bound
+  // Cholesky), because Fisher-BT follows an accepted loglik(theta) with eval_all(theta).
+  // spec_ready: sa / sn / wsl hold that work for spec_theta (valid while the factor is).
+  bool spec_ready = false;
+  bool spec_pending = false;      // spec_done not yet waited for by a later pass
+  double spec_theta[3] = {0, 0, 0};
+  cudaEvent_t spec_done = nullptr;
   double kstats[MLE_KSTATS] = {};
 };
 
@@ -263,10 +277,23 @@ struct Item {
   int mode = 0;        // 1 loglik, 2 eval_all
   bool factor = true;  // generate Sigma + Cholesky (false: cached factor reused)
   bool derivs = false; // derivative matrices + solves
+  bool gen_derivs = false;  // generate the derivative matrices in this pass
+  bool need_w = false;      // compute the W_b slices in this pass
+  bool spec = false;        // loglik item: speculative derivatives + W on the aux stream
   int rc = MLE_OK;
   int64_t pivot = -1;
   double res[kResults] = {};
 };
+
+// Pending speculative work (issued on some batch leader's aux stream) must finish before
+// anything else touches this context's buffers.
+int wait_spec(mle_ctx* c, cudaStream_t s) {
+  if (c->spec_pending) {
+    CUDA_TRY(cudaStreamWaitEvent(s, c->spec_done, 0));
+    c->spec_pending = false;
+  }
+  return MLE_OK;
+}
 
 int ensure_ozaki(mle_ctx* c, bool derivs);
 
@@ -568,10 +595,12 @@ struct Launcher {
 
   // B_i = L^-1 S_i L^-T (lower half) for both derivative matrices of every item, in place.
   // GEMM batch member z = 2 * item + {0: alpha, 1: nu}.
-  int solves(mle_ctx* const* cs, int m) {
+  int solves(mle_ctx* const* cs, int m, mle_ctx* const* cw, int mw) {
     if (cs[0]->wsl) {
-      int rc = compute_w(cs, m);
-      if (rc) return rc;
+      if (mw > 0) {
+        int rc = compute_w(cw, mw);
+        if (rc) return rc;
+      }
       return solves_w(cs, m);
     }
     return solves_dmma(cs, m);
@@ -972,8 +1001,12 @@ int run_chunk(Item* items, int m) {
   cudaStream_t aux = lead->kprof ? s : lead->aux;  // profiling: everything serialised
   for (int b = 0; b < m; ++b) {
     Item& it = items[b];
-    int rc = ensure_matrices(it.c, it.derivs);
+    int rc = wait_spec(it.c, s);
     if (rc) return rc;
+    rc = ensure_matrices(it.c, it.derivs);
+    if (rc) return rc;
+    // this pass overwrites what a previous speculation left in sa / sn / wsl
+    if (it.factor || it.derivs) it.c->spec_ready = false;  // the solves consume S in place
     std::memcpy(it.c->h_theta, &it.P, sizeof(ThetaParams));
     CUDA_TRY(cudaMemcpyAsync(it.c->d_theta, it.c->h_theta, sizeof(ThetaParams),
                              cudaMemcpyHostToDevice, s));
@@ -988,7 +1021,7 @@ int run_chunk(Item* items, int m) {
     int ng = 0;
     for (int b = 0; b < m; ++b) {
       const Item& it = items[b];
-      if (sigma_pass ? !it.factor : !it.derivs) continue;
+      if (sigma_pass ? !it.factor : !(it.gen_derivs || it.spec)) continue;
       GenItem& gi = ga.item[ng++];
       gi.P = it.c->d_theta;
       gi.lx = it.c->lx;
@@ -1012,13 +1045,35 @@ int run_chunk(Item* items, int m) {
     launch_gen_engine(sig.first, sig.second, s);
     CUDA_TRY(cudaGetLastError());
   }
+  // derivative matrices: eval_all items first (the solves wait for these only), then the
+  // speculative loglik items
   auto der = gen_set(false);
+  bool any_spec = false;
+  for (int b = 0; b < m; ++b) any_spec = any_spec || items[b].spec;
   if (der.second > 0) {
     int rc = run.join(s, aux);
     if (rc) return rc;
-    run.launches += 1;
-    launch_gen_engine(der.first, der.second, aux);
-    CUDA_TRY(cudaGetLastError());
+    GenArgs now = der.first, later = der.first;
+    int nn = 0, nl = 0;
+    for (int b = 0, g = 0; b < m; ++b) {
+      if (!(items[b].gen_derivs || items[b].spec)) continue;
+      if (items[b].spec) later.item[nl++] = der.first.item[g];
+      else now.item[nn++] = der.first.item[g];
+      ++g;
+    }
+    if (nn > 0) {
+      run.launches += 1;
+      launch_gen_engine(now, nn, aux);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
+    if (nl > 0) {
+      run.launches += 1;
+      launch_gen_engine(later, nl, aux);
+      CUDA_TRY(cudaGetLastError());
+    }
+  } else {
+    CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
   }
   CUDA_TRY(cudaEventRecord(lead->ev[1], s));
   {  // Cholesky for items without a cached factor
@@ -1039,15 +1094,34 @@ int run_chunk(Item* items, int m) {
     }
   }
   CUDA_TRY(cudaEventRecord(lead->ev[2], s));
-  {
-    int rc = run.join(aux, s);  // derivative matrices generated
-    if (rc) return rc;
+  if (any_spec) {
+    // speculative W_b for the loglik items, on the aux stream after their Cholesky
     mle_ctx* cs[kMaxItems];
-    int nd = 0;
+    int ns = 0;
     for (int b = 0; b < m; ++b)
+      if (items[b].spec) cs[ns++] = items[b].c;
+    int rc = run.join(s, aux);
+    if (rc) return rc;
+    Launcher sp{aux};
+    rc = sp.compute_w(cs, ns);
+    if (rc) return rc;
+    run.launches += sp.launches;
+    for (int b = 0; b < ns; ++b) {
+      CUDA_TRY(cudaEventRecord(cs[b]->spec_done, aux));
+      cs[b]->spec_pending = true;
+    }
+  }
+  {
+    if (der.second > 0) CUDA_TRY(cudaStreamWaitEvent(s, lead->ev_der, 0));
+    mle_ctx* cs[kMaxItems];
+    mle_ctx* cw[kMaxItems];
+    int nd = 0, nw = 0;
+    for (int b = 0; b < m; ++b) {
       if (items[b].derivs) cs[nd++] = items[b].c;
+      if (items[b].need_w) cw[nw++] = items[b].c;
+    }
     if (nd > 0) {
-      int rc = run.solves(cs, nd);
+      int rc = run.solves(cs, nd, cw, nw);
       if (rc) return rc;
     }
   }
@@ -1115,7 +1189,14 @@ int run_chunk(Item* items, int m) {
       it.rc = MLE_NOT_PD;
       it.pivot = idx;
       c->factor_valid = false;
+      c->spec_ready = false;
       continue;
+    }
+    if (it.spec) {
+      c->spec_ready = true;
+      c->spec_theta[0] = it.P.sigma2;
+      c->spec_theta[1] = it.P.alpha;
+      c->spec_theta[2] = it.P.nu;
     }
     it.rc = MLE_OK;
     it.pivot = -1;
@@ -1173,6 +1254,12 @@ int prepare(mle_ctx* c, const double theta[3], int mode, Item* it) {
     return fail(MLE_INVALID, "eval_all with a nugget is not implemented yet (loglik only)");
   it->factor = !same_theta(c, theta);
   it->derivs = (mode == 2);
+  const bool spec_hit = !it->factor && c->spec_ready && c->spec_theta[0] == theta[0] &&
+                        c->spec_theta[1] == theta[1] && c->spec_theta[2] == theta[2];
+  it->gen_derivs = it->derivs && !spec_hit;
+  it->need_w = it->derivs && !spec_hit;
+  it->spec = mode == 1 && it->factor && c->ozaki && c->sa && c->sn && c->wsl &&
+             use_speculation();
   return MLE_OK;
 }
 
@@ -1261,10 +1348,16 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
     if (_e != cudaSuccess)                                                             \
       return bail(fail(MLE_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
   } while (0)
-  CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  CTX_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-  CTX_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  // Priorities: the latency-bound factorization chain (main, look-ahead) wins SMs over the
+  // throughput work on aux (derivative generation, speculation) as CTAs retire.
+  int prio_low = 0, prio_high = 0;
+  CTX_TRY(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+  CTX_TRY(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_high));
+  CTX_TRY(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_high));
+  CTX_TRY(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_low));
   for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
+  CTX_TRY(cudaEventCreateWithFlags(&c->ev_der, cudaEventDisableTiming));
+  CTX_TRY(cudaEventCreateWithFlags(&c->spec_done, cudaEventDisableTiming));
   for (auto& e : c->pool) CTX_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CTX_TRY(dmalloc(&c->lx, sizeof(double) * n));
   CTX_TRY(dmalloc(&c->ly, sizeof(double) * n));
@@ -1289,6 +1382,7 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
 void mle_ctx_destroy(mle_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->spec_pending && c->spec_done) cudaEventSynchronize(c->spec_done);
   if (c->stream) cudaStreamSynchronize(c->stream);
   dfree(c->lx);
   dfree(c->ly);
@@ -1320,6 +1414,8 @@ void mle_ctx_destroy(mle_ctx* c) {
   for (auto& e : c->pool)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->kev) cudaEventDestroy(e);
+  if (c->ev_der) cudaEventDestroy(c->ev_der);
+  if (c->spec_done) cudaEventDestroy(c->spec_done);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1333,9 +1429,11 @@ int mle_ctx_set_values(mle_ctx* c, const double* z) {
   int rc = check_finite(z, c->n, "values");
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
+  if ((rc = wait_spec(c, c->stream))) return rc;
   CUDA_TRY(cudaMemcpyAsync(c->z, z, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->factor_valid = false;  // row n of L carries L^-1 z
+  c->spec_ready = false;
   return MLE_OK;
 }
 
@@ -1445,7 +1543,9 @@ int mle_build(mle_ctx* c, const double theta[3], int which, double* out_host) {
   CUDA_TRY(cudaSetDevice(c->device));
   rc = ensure_matrices(c, false);
   if (rc) return rc;
+  if ((rc = wait_spec(c, c->stream))) return rc;
   c->factor_valid = false;  // the Sigma buffer is reused as scratch
+  c->spec_ready = false;
   std::memcpy(c->h_theta, &it.P, sizeof(ThetaParams));
   CUDA_TRY(cudaMemcpyAsync(c->d_theta, c->h_theta, sizeof(ThetaParams), cudaMemcpyHostToDevice,
                            c->stream));

@@ -82,3 +82,54 @@ def test_buffer_cache_reuse_bit_identical(gpu):
     second.close()
     from paper_2601_11437_b200 import _native as nat
     nat.check(nat.lib.mle_release_cached_memory())
+
+
+def _with_env(key, value, fn):
+    old = os.environ.get(key)
+    os.environ[key] = value
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[key]
+        else:
+            os.environ[key] = old
+
+
+def test_speculation_bit_identical(gpu):
+    """Speculative derivative/W generation in loglik passes must not change any result."""
+    loc, z = config_data("config2", 3)
+    th0 = gpu.MaternParams(0.8, 0.1, 1.0)
+    cfg = gpu.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+
+    def fit():
+        return gpu.fisher_bt(gpu.SpatialDataset(loc, z), cfg)
+
+    off = _with_env("MLE_SPECULATE", "0", fit)
+    on = _with_env("MLE_SPECULATE", "1", fit)
+    np.testing.assert_array_equal(off.theta_hat.as_array(), on.theta_hat.as_array())
+    np.testing.assert_array_equal(off.fisher_at_hat, on.fisher_at_hat)
+    assert off.loglik_at_hat == on.loglik_at_hat
+    assert (off.grad_calls, off.loglik_calls) == (on.grad_calls, on.loglik_calls)
+
+    def seq():
+        eng = gpu.Engine(loc, z)
+        eng.eval_all(np.array([1.0, 0.2, 1.5]))   # allocates the derivative buffers
+        out = []
+        for th in ([0.9, 0.15, 1.3], [0.9, 0.15, 1.3], [1.1, 0.25, 1.7]):
+            th = np.array(th)
+            out.append(eng.loglik(th))
+            out.append(eng.eval_all(th))           # speculation hit (same theta)
+        out.append(eng.eval_all(np.array([0.95, 0.2, 1.5])))  # miss
+        eng.close()
+        return out
+
+    a = _with_env("MLE_SPECULATE", "0", seq)
+    b = _with_env("MLE_SPECULATE", "1", seq)
+    for x, y in zip(a, b):
+        if isinstance(x, tuple):
+            assert x[0] == y[0]
+            np.testing.assert_array_equal(x[1], y[1])
+            np.testing.assert_array_equal(x[2], y[2])
+        else:
+            assert x == y
