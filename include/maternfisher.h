@@ -82,7 +82,8 @@ int mle_release_cached_memory(void);
  * mle_kernel_stats then returns, for the last pass, MLE_KSTATS doubles:
  *   [0] GEMM launches  [1] GEMM ms (sum of launch durations)  [2] FP64-equivalent tile
  *   flops  [3] int8 tensor-core ops (36 slice products)  [4] slicing launches  [5] slicing
- *   ms  [6] slicing algorithmic bytes  [7] reserved.
+ *   ms  [6] slicing algorithmic bytes  [7] host time to enqueue the last pass (ms; also
+ *   maintained when profiling is off).
  * Diagnostic only: no reference counterpart.
  */
 #define MLE_KSTATS 8
@@ -92,7 +93,9 @@ int mle_kernel_stats(const mle_ctx* ctx, double* out);
 /*
  * Create a context owning device-resident copies of the n locations (n x 2, row-major
  * x,y pairs) and the n observed values z.  `device` selects the GPU.  `nugget` >= 0 adds
- * tau^2 to the diagonal of Sigma (0 reproduces the reference, which has no nugget).
+ * tau^2 to the diagonal of Sigma (0 reproduces the reference, which has no nugget).  With a
+ * nugget, eval_all treats dSigma/dsigma^2 = (Sigma - tau^2 I)/sigma^2 as a third derivative
+ * block (config 5; oracle/maternmle_cpu.py eval_all_nugget -- not in the reference).
  * All O(n^2) matrices are allocated lazily on first use.
  */
 int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device,

@@ -298,12 +298,48 @@ def eval_all(locations, z, th):
     return ll, grad, fis
 
 
+def eval_all_nugget(locations, z, th, nugget):
+    """NOT IN THE REFERENCE -- config-5 restatement ("Nugget" row).
+
+    The reference has no nugget: its diagonal is hard-wired to sigma^2 (matern.py:186-188)
+    and its sigma^2 closed forms (likelihood.py:129-130, 141, 145) assume
+    dSigma/dsigma^2 = Sigma / sigma^2.  With Sigma_tau = Sigma + tau^2 I that no longer holds;
+    dSigma_tau/dsigma^2 = (Sigma_tau - tau^2 I) / sigma^2 = R (the Matern correlation) is
+    treated as a third derivative block with exactly the algorithm of likelihood.py:107-149:
+    A_i = Sigma_tau^-1 S_i by two triangular solves (:134-135), g_i = -tr(A_i)/2 +
+    w^T S_i w / 2 (:136-137), I_ij = trace_product(A_i, A_j) / 2 (:140-147).  nugget = 0 gives
+    the reference's eval_all up to rounding (tests/test_oracle.py).  Parity is unpinned by
+    construction: no reference output exists for this case.
+    """
+    n = len(z)
+    s2 = th[0]
+    low = cholesky(matrix(locations, th, "sigma", nugget))
+    y = solve_triangular(low, z, lower=True, check_finite=False)
+    quad = float(y @ y)
+    ll = -0.5 * n * LOG_2PI - float(np.sum(np.log(np.diag(low)))) - 0.5 * quad
+    w = solve_triangular(low, y, lower=True, trans="T", check_finite=False)
+    blocks = []
+    for kind in ("sigma2", "alpha", "nu"):
+        si = matrix(locations, th, "sigma") / s2 if kind == "sigma2" else matrix(locations, th,
+                                                                                   kind)
+        a = solve_triangular(low, solve_triangular(low, si, lower=True, check_finite=False),
+                             lower=True, trans="T", check_finite=False)
+        blocks.append((a, -0.5 * float(np.trace(a)) + 0.5 * float(w @ (si @ w))))
+    grad = np.array([g for _, g in blocks])
+    fis = np.empty((3, 3))
+    for i in range(3):
+        for j in range(i, 3):
+            fis[i, j] = fis[j, i] = 0.5 * trace_product(blocks[i][0], blocks[j][0])
+    return ll, grad, fis
+
+
 class CountingObjective:
     """optimizer.py:114-142 semantics over the oracle (CPU fits for parity tests)."""
 
-    def __init__(self, locations, z):
+    def __init__(self, locations, z, nugget=0.0):
         self.locations = np.asarray(locations, float)
         self.z = np.asarray(z, float)
+        self.nugget = float(nugget)  # nugget > 0: config-5 restatement (eval_all_nugget)
         self.loglik_calls = 0
         self.grad_calls = 0
 
@@ -314,7 +350,7 @@ class CountingObjective:
             return -math.inf
         try:
             with np.errstate(over="ignore", under="ignore", invalid="ignore"):
-                v = loglik(self.locations, self.z, th)
+                v = loglik(self.locations, self.z, th, self.nugget)
         except (NotPD, ValueError):
             return -math.inf
         return -math.inf if math.isnan(v) else v
@@ -326,4 +362,6 @@ class CountingObjective:
         if not all(math.isfinite(v) and v > 0.0 for v in th):
             raise ValueError("theta components must be finite and > 0")
         with np.errstate(over="ignore", under="ignore", invalid="ignore"):
+            if self.nugget > 0.0:
+                return eval_all_nugget(self.locations, self.z, th, self.nugget)
             return eval_all(self.locations, self.z, th)

@@ -71,7 +71,7 @@ class BatchCoordinator:
         self.eval_passes = 0
         # device-side accounting of every batch (CUDA events on the launching stream)
         self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
-                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0}
+                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0}
 
     def _run_locked_batch(self):
         # Alignment policy: while some clients wait on a cheap loglik (gen + Cholesky) and
@@ -92,6 +92,7 @@ class BatchCoordinator:
                                  [r[2] for r in reqs])
                 err = None
                 p = reqs[0][0].phase_times()  # batch-level (same on every member)
+                p["host_enqueue_ms"] = reqs[0][0].kernel_stats()["host_enqueue_ms"]
                 for key in self.acc:
                     self.acc[key] += p[key]
             except Exception as exc:  # CUDA failures reach every client

@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -221,6 +222,7 @@ struct mle_ctx {
   double* sigma = nullptr;
   double* sa = nullptr;
   double* sn = nullptr;
+  double* smat = nullptr;         // nugget contexts: I_n -> M = L^-1 L^-T (third block)
   double* linv = nullptr;
   int* fail_flag = nullptr;
   long long* fail_idx = nullptr;
@@ -228,7 +230,7 @@ struct mle_ctx {
   double* out = nullptr;          // device: 9 reduction results
   ThetaParams* d_theta = nullptr; // device copy of the per-theta scalars
   ThetaParams* h_theta = nullptr; // pinned staging
-  double* h_res = nullptr;        // pinned: 9 results + fail flag + fail idx
+  double* h_res = nullptr;        // pinned: kReduceOut results + fail flag + fail idx
   cudaEvent_t ev[5] = {};
   cudaEvent_t ev_der = nullptr;   // derivative generation for this pass's eval_all items
   double phase_ms[MLE_NUM_PHASES] = {};
@@ -266,6 +268,7 @@ struct mle_ctx {
   double spec_theta[3] = {0, 0, 0};
   cudaEvent_t spec_done = nullptr;
   double kstats[MLE_KSTATS] = {};
+  double host_wait_ms = 0.0;
 };
 
 namespace {
@@ -304,6 +307,7 @@ int ensure_matrices(mle_ctx* c, bool derivs) {
   if (derivs) {
     if (!c->sa) CUDA_TRY(dmalloc(&c->sa, bytes));
     if (!c->sn) CUDA_TRY(dmalloc(&c->sn, bytes));
+    if (c->nugget > 0.0 && !c->smat) CUDA_TRY(dmalloc(&c->smat, bytes));
   }
   return ensure_ozaki(c, derivs);
 }
@@ -344,8 +348,9 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
   }
   if (derivs && !c->xsl) {
     const int nb = (c->Nt + kOuter - 1) / kOuter;
-    CUDA_TRY(dmalloc(&c->xsl, 4 * (size_t)c->N * kOzRowBytes));
-    CUDA_TRY(dmalloc(&c->xex, 4 * sizeof(int) * (size_t)c->N));
+    const int regions = c->nugget > 0.0 ? 6 : 4;  // 2 per derivative block (look-ahead)
+    CUDA_TRY(dmalloc(&c->xsl, regions * (size_t)c->N * kOzRowBytes));
+    CUDA_TRY(dmalloc(&c->xex, regions * sizeof(int) * (size_t)c->N));
     CUDA_TRY(dmalloc(&c->dinv, sizeof(double) * (size_t)nb * 512 * 512));
     CUDA_TRY(dmalloc(&c->tscr, sizeof(double) * (size_t)nb * kNB * 512));
     CUDA_TRY(dmalloc(&c->wbuf, sizeof(double) * (size_t)c->N * 512));
@@ -376,6 +381,24 @@ GemmArgs gemm_base() {
 //   (ii) everything beyond                                               -> side stream s2
 // so the inner chain of block b+1 runs on `s` while (ii) of block b runs on `s2`.  (i) of
 // block b+1 touches tiles (ii) of block b also updates, so `s` waits for (ii)(b) first.
+// The derivative blocks of a pass: (alpha, nu) per item, plus M for nugget items.
+struct MatList {
+  mle_ctx* c[kMaxGemm];
+  int which[kMaxGemm];  // 0 S_alpha, 1 S_nu, 2 I_n -> M
+  int count = 0;
+  MatList(mle_ctx* const* cs, int m) {
+    for (int i = 0; i < m; ++i) {
+      for (int w = 0; w < (cs[i]->smat ? 3 : 2); ++w) {
+        c[count] = cs[i];
+        which[count++] = w;
+      }
+    }
+  }
+  double* S(int z) const {
+    return which[z] == 0 ? c[z]->sa : which[z] == 1 ? c[z]->sn : c[z]->smat;
+  }
+};
+
 struct Launcher {
   cudaStream_t s;              // main: inner chains
   cudaStream_t s2 = nullptr;   // side: bulk trailing updates (null: everything on s)
@@ -749,15 +772,16 @@ struct Launcher {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
     const int nb = (Nt + kOuter - 1) / kOuter;
-    const int zb = 2 * m;
-    auto S = [&](int z) { return z % 2 == 0 ? cs[z / 2]->sa : cs[z / 2]->sn; };
-    auto flag = [&](int z) { return (const int*)cs[z / 2]->fail_flag; };
+    MatList ml(cs, m);
+    const int zb = ml.count;
+    auto S = [&](int z) { return ml.S(z); };
+    auto flag = [&](int z) { return (const int*)ml.c[z]->fail_flag; };
     // solve-operand slices: two regions per matrix, alternating by block (look-ahead)
     auto XS = [&](int z, int b) {
-      return cs[z / 2]->xsl + ((size_t)(z % 2) * 2 + (b & 1)) * ld * kOzRowBytes;
+      return ml.c[z]->xsl + ((size_t)ml.which[z] * 2 + (b & 1)) * ld * kOzRowBytes;
     };
     auto XE = [&](int z, int b) {
-      return cs[z / 2]->xex + ((size_t)(z % 2) * 2 + (b & 1)) * ld;
+      return ml.c[z]->xex + ((size_t)ml.which[z] * 2 + (b & 1)) * ld;
     };
     int rc;
     // forward sweep, row blocks top-down
@@ -784,8 +808,8 @@ struct Launcher {
       t.alpha = 1.0;
       t.beta0_tm = k.t1 - k.t0;
       for (int z = 0; z < zb; ++z) {
-        t.As[z] = cs[z / 2]->wsl + woff;
-        t.ea[z] = cs[z / 2]->wex + eoff;
+        t.As[z] = ml.c[z]->wsl + woff;
+        t.ea[z] = ml.c[z]->wex + eoff;
         t.Bs[z] = XS(z, b);
         t.eb[z] = XE(z, b);
         t.C[z] = S(z) + k.c0;
@@ -833,8 +857,8 @@ struct Launcher {
       for (int z = 0; z < zb; ++z) {
         t.As[z] = XS(z, b);
         t.ea[z] = XE(z, b);
-        t.Bs[z] = cs[z / 2]->wsl + woff;
-        t.eb[z] = cs[z / 2]->wex + eoff;
+        t.Bs[z] = ml.c[z]->wsl + woff;
+        t.eb[z] = ml.c[z]->wex + eoff;
         t.C[z] = S(z) + k.c0 + k.c0 * ld;
         t.fail_flag[z] = flag(z);
       }
@@ -863,13 +887,14 @@ struct Launcher {
   int solves_dmma(mle_ctx* const* cs, int m) {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
-    const int zb = 2 * m;
-    auto S = [&](int z) { return z % 2 == 0 ? cs[z / 2]->sa : cs[z / 2]->sn; };
-    auto L = [&](int z) { return (const double*)cs[z / 2]->sigma; };
+    MatList ml(cs, m);
+    const int zb = ml.count;
+    auto S = [&](int z) { return ml.S(z); };
+    auto L = [&](int z) { return (const double*)ml.c[z]->sigma; };
     auto Linv = [&](int z, int k) {
-      return (const double*)(cs[z / 2]->linv + (size_t)k * kNB * kNB);
+      return (const double*)(ml.c[z]->linv + (size_t)k * kNB * kNB);
     };
-    auto flag = [&](int z) { return (const int*)cs[z / 2]->fail_flag; };
+    auto flag = [&](int z) { return (const int*)ml.c[z]->fail_flag; };
     int rc;
     // forward sweep X = L^-1 S (all columns), row blocks top-down
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
@@ -994,6 +1019,7 @@ struct Launcher {
 
 // Runs up to kMaxItems requests (same device, same N) on the leader's stream.
 int run_chunk(Item* items, int m) {
+  const auto host_t0 = std::chrono::steady_clock::now();
   mle_ctx* lead = items[0].c;
   cudaStream_t s = lead->stream;
   Launcher run{s, lead->kprof ? nullptr : lead->side, lead->pool, kPoolEvents};
@@ -1061,17 +1087,31 @@ int run_chunk(Item* items, int m) {
       else now.item[nn++] = der.first.item[g];
       ++g;
     }
+    auto identities = [&](bool spec_items) -> int {  // nugget: third block S = I_n
+      double* mats[kMaxItems];
+      int k = 0;
+      for (int b = 0; b < m; ++b)
+        if (items[b].c->smat && (spec_items ? items[b].spec : items[b].gen_derivs))
+          mats[k++] = items[b].c->smat;
+      if (k > 0) {
+        run.launches += 1;
+        CUDA_TRY(launch_set_identity(mats, lead->N, (int)lead->n, k, aux));
+      }
+      return MLE_OK;
+    };
     if (nn > 0) {
       run.launches += 1;
       launch_gen_engine(now, nn, aux);
       CUDA_TRY(cudaGetLastError());
     }
+    if ((rc = identities(false))) return rc;
     CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
     if (nl > 0) {
       run.launches += 1;
       launch_gen_engine(later, nl, aux);
       CUDA_TRY(cudaGetLastError());
     }
+    if ((rc = identities(true))) return rc;
   } else {
     CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
   }
@@ -1133,6 +1173,7 @@ int run_chunk(Item* items, int m) {
     ra.L[b] = c->sigma;
     ra.Ba[b] = items[b].derivs ? c->sa : nullptr;
     ra.Bn[b] = items[b].derivs ? c->sn : nullptr;
+    ra.Bm[b] = items[b].derivs ? c->smat : nullptr;
     ra.partials[b] = c->partials;
     ra.out[b] = c->out;
     ra.fail_flag[b] = c->fail_flag;
@@ -1144,13 +1185,17 @@ int run_chunk(Item* items, int m) {
   CUDA_TRY(cudaEventRecord(lead->ev[4], s));
   for (int b = 0; b < m; ++b) {
     mle_ctx* c = items[b].c;
-    CUDA_TRY(cudaMemcpyAsync(c->h_res, c->out, sizeof(double) * 9, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(c->h_res + 9, c->fail_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(c->h_res + 10, c->fail_idx, sizeof(long long),
+    CUDA_TRY(cudaMemcpyAsync(c->h_res, c->out, sizeof(double) * kReduceOut,
+                             cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_res + kReduceOut, c->fail_flag, sizeof(int),
+                             cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_res + kReduceOut + 1, c->fail_idx, sizeof(long long),
                              cudaMemcpyDeviceToHost, s));
   }
+  const auto host_t1 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
+  const auto host_t2 = std::chrono::steady_clock::now();
   {
     int rc = run.prof_collect();
     if (rc) return rc;
@@ -1180,12 +1225,16 @@ int run_chunk(Item* items, int m) {
     c->flops = flops;
     c->gen_bytes = gbytes;
     c->launches = run.launches;
+    if (c == lead) {
+      c->kstats[7] = std::chrono::duration<double, std::milli>(host_t1 - host_t0).count();
+      c->host_wait_ms = std::chrono::duration<double, std::milli>(host_t2 - host_t1).count();
+    }
     if (c != lead) std::memcpy(c->kstats, lead->kstats, sizeof(c->kstats));
     int flag;
-    std::memcpy(&flag, c->h_res + 9, sizeof(int));
+    std::memcpy(&flag, c->h_res + kReduceOut, sizeof(int));
     if (flag) {
       long long idx;
-      std::memcpy(&idx, c->h_res + 10, sizeof(long long));
+      std::memcpy(&idx, c->h_res + kReduceOut + 1, sizeof(long long));
       it.rc = MLE_NOT_PD;
       it.pivot = idx;
       c->factor_valid = false;
@@ -1211,17 +1260,28 @@ int run_chunk(Item* items, int m) {
     o[0] = -0.5 * n * kLog2Pi - logdet - 0.5 * quad;  // likelihood.py:85-89, 123
     if (it.mode == 2) {
       const double tr_a = r[2], tr_n = r[3], faa = r[4], fan = r[5], fnn = r[6];
-      const double yby_a = r[7], yby_n = r[8];
-      o[1] = (quad - n) / (2.0 * s2);          // likelihood.py:129
+      const double yby_a = r[kReduceSums], yby_n = r[kReduceSums + 1];
       o[2] = -0.5 * tr_a + 0.5 * yby_a;        // likelihood.py:137
       o[3] = -0.5 * tr_n + 0.5 * yby_n;
       double* f = o + 4;
-      f[0] = n / (2.0 * s2 * s2);              // likelihood.py:130
-      f[1] = f[3] = tr_a / (2.0 * s2);         // likelihood.py:141
-      f[2] = f[6] = tr_n / (2.0 * s2);         // likelihood.py:145
       f[4] = 0.5 * faa;                        // likelihood.py:142
       f[5] = f[7] = 0.5 * fan;                 // likelihood.py:146
       f[8] = 0.5 * fnn;                        // likelihood.py:147
+      if (c->nugget == 0.0) {
+        o[1] = (quad - n) / (2.0 * s2);        // likelihood.py:129
+        f[0] = n / (2.0 * s2 * s2);            // likelihood.py:130
+        f[1] = f[3] = tr_a / (2.0 * s2);       // likelihood.py:141
+        f[2] = f[6] = tr_n / (2.0 * s2);       // likelihood.py:145
+      } else {
+        // Nugget (config 5; not in the reference, oracle eval_all_nugget): dSigma/dsigma^2 =
+        // (Sigma - tau^2 I) / sigma^2, so B_s2 = (I - tau^2 M) / sigma^2, M = L^-1 L^-T.
+        const double t = c->nugget, tr_m = r[7], fam = r[8], fnm = r[9], fmm = r[10];
+        const double yby_m = r[kReduceSums + 2];  // y^T M y = |Sigma^-1 z|^2
+        o[1] = -0.5 * (n - t * tr_m) / s2 + 0.5 * (quad - t * yby_m) / s2;
+        f[0] = 0.5 * (n - 2.0 * t * tr_m + t * t * fmm) / (s2 * s2);
+        f[1] = f[3] = 0.5 * (tr_a - t * fam) / s2;
+        f[2] = f[6] = 0.5 * (tr_n - t * fnm) / s2;
+      }
     }
   }
   return MLE_OK;
@@ -1250,8 +1310,6 @@ int prepare(mle_ctx* c, const double theta[3], int mode, Item* it) {
   if (!theta) return fail(MLE_INVALID, "theta is null");
   if (mle_fill_theta(theta, c->nugget, &it->P) != 0)
     return fail(MLE_INVALID, "MaternParams components must be finite and > 0");
-  if (mode == 2 && c->nugget != 0.0)
-    return fail(MLE_INVALID, "eval_all with a nugget is not implemented yet (loglik only)");
   it->factor = !same_theta(c, theta);
   it->derivs = (mode == 2);
   const bool spec_hit = !it->factor && c->spec_ready && c->spec_theta[0] == theta[0] &&
@@ -1365,10 +1423,10 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   CTX_TRY(dmalloc(&c->fail_flag, sizeof(int)));
   CTX_TRY(dmalloc(&c->fail_idx, sizeof(long long)));
   CTX_TRY(dmalloc(&c->partials, sizeof(double) * kReduceBlocks * kReduceSums));
-  CTX_TRY(dmalloc(&c->out, sizeof(double) * 9));
+  CTX_TRY(dmalloc(&c->out, sizeof(double) * kReduceOut));
   CTX_TRY(dmalloc(&c->d_theta, sizeof(ThetaParams)));
   CTX_TRY(hmalloc(&c->h_theta, sizeof(ThetaParams)));
-  CTX_TRY(hmalloc(&c->h_res, sizeof(double) * 12));
+  CTX_TRY(hmalloc(&c->h_res, sizeof(double) * (kReduceOut + 2)));
   CTX_TRY(cudaMemcpyAsync(c->lx, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CTX_TRY(cudaMemcpyAsync(c->ly, y.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CTX_TRY(cudaMemcpyAsync(c->z, z, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
@@ -1390,6 +1448,7 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->sigma);
   dfree(c->sa);
   dfree(c->sn);
+  dfree(c->smat);
   dfree(c->linv);
   dfree(c->fail_flag);
   dfree(c->fail_idx);

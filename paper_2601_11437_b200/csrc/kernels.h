@@ -70,6 +70,7 @@ struct ReduceArgs {
   const double* L[kMaxItems];
   const double* Ba[kMaxItems];  // null for loglik-only items
   const double* Bn[kMaxItems];
+  const double* Bm[kMaxItems];  // nugget items: M = L^-1 L^-T (null otherwise)
   double* partials[kMaxItems];
   double* out[kMaxItems];
   const int* fail_flag[kMaxItems];
@@ -89,13 +90,18 @@ void launch_elem(const ThetaParams* P_dev, int op, int which, const double* x, l
 cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s);
 // Factor the 128x128 diagonal tile at (k0, k0) of every item in place (+ its inverse).
 cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s);
-// Reductions: per item 9 results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>, yBy_A, yBy_N].
+// Reductions: per item kReduceOut results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>,
+// trM, <A,M>, <N,M>, <M,M>, yBy_A, yBy_N, yBy_M] (the M terms only for nugget items).
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
 
 // Scatter the diagonal-tile inverses Linv_k into the per-outer-block inverse storage:
 // dinv[z] + (k / 4) 512^2 + (k % 4) 128 (1 + 512)  <-  linv[z] + k 128^2   (k < Nt).
 cudaError_t launch_linv_to_dinv(double* const* dinv, const double* const* linv, int Nt,
                                 int items, cudaStream_t s);
+
+// S = I_n inside the padded N x N matrix (zero elsewhere), for every item.
+cudaError_t launch_set_identity(double* const* S, long long ld, int n, int items,
+                                cudaStream_t s);
 
 // z = L w over the leading n x n block of a resident Cholesky factor.
 cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double* w, double* z,
@@ -145,6 +151,7 @@ cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int
 cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile = 0);
 
 constexpr int kReduceBlocks = 148 * 4;
-constexpr int kReduceSums = 7;
+constexpr int kReduceSums = 11;
+constexpr int kReduceOut = kReduceSums + 3;
 
 }  // namespace mle

@@ -555,10 +555,13 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   const double* __restrict__ L = ra.L[item];
   const double* __restrict__ Ba = ra.Ba[item];
   const double* __restrict__ Bn = ra.Bn[item];
+  const double* __restrict__ Bm = ra.Bm[item];
   const long long ld = ra.ld;
   const int n = ra.n;
   __shared__ double sh[RTHREADS / 32];
-  double s[RN] = {0, 0, 0, 0, 0, 0, 0};
+  double s[RN];
+#pragma unroll
+  for (int q = 0; q < RN; ++q) s[q] = 0.0;
   for (int j = blockIdx.x; j < n; j += gridDim.x) {
     const long long cj = (long long)j * ld;
     if (threadIdx.x == 0) {
@@ -572,13 +575,32 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
       s[4] += a * a;
       s[5] += a * b;
       s[6] += b * b;
+      if (Bm != nullptr) {
+        const double c = Bm[j + cj];
+        s[7] += c;
+        s[8] += a * c;
+        s[9] += b * c;
+        s[10] += c * c;
+      }
     }
     if (Ba == nullptr) continue;
-    for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
-      const double a = Ba[i + cj], b = Bn[i + cj];
-      s[4] += 2.0 * a * a;
-      s[5] += 2.0 * a * b;
-      s[6] += 2.0 * b * b;
+    if (Bm == nullptr) {
+      for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
+        const double a = Ba[i + cj], b = Bn[i + cj];
+        s[4] += 2.0 * a * a;
+        s[5] += 2.0 * a * b;
+        s[6] += 2.0 * b * b;
+      }
+    } else {
+      for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
+        const double a = Ba[i + cj], b = Bn[i + cj], c = Bm[i + cj];
+        s[4] += 2.0 * a * a;
+        s[5] += 2.0 * a * b;
+        s[6] += 2.0 * b * b;
+        s[8] += 2.0 * a * c;
+        s[9] += 2.0 * b * c;
+        s[10] += 2.0 * c * c;
+      }
     }
   }
   double* partials = ra.partials[item];
@@ -588,13 +610,14 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   }
 }
 
-// out[0..6] = fixed-order sums of the partials; out[7], out[8] = B_alpha[n,n], B_nu[n,n].
+// out[0..RN) = fixed-order sums of the partials; out[RN..RN+3) = B_alpha, B_nu, M at [n,n].
 __global__ void reduce_final_kernel(ReduceArgs ra) {
   const int item = blockIdx.x;
   if (*ra.fail_flag[item]) return;
   const double* partials = ra.partials[item];
   const double* Ba = ra.Ba[item];
   const double* Bn = ra.Bn[item];
+  const double* Bm = ra.Bm[item];
   double* out = ra.out[item];
   const long long diag_n = ra.n + (long long)ra.n * ra.ld;
   const int q = threadIdx.x;
@@ -605,6 +628,7 @@ __global__ void reduce_final_kernel(ReduceArgs ra) {
   }
   if (q == RN) out[RN] = Ba ? Ba[diag_n] : 0.0;
   if (q == RN + 1) out[RN + 1] = Bn ? Bn[diag_n] : 0.0;
+  if (q == RN + 2) out[RN + 2] = Bm ? Bm[diag_n] : 0.0;
 }
 
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {
@@ -658,6 +682,28 @@ cudaError_t launch_linv_to_dinv(double* const* dinv, const double* const* linv, 
     a.linv[z] = linv[z];
   }
   linv_to_dinv_kernel<<<dim3((unsigned)Nt, (unsigned)items), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+struct IdentityArgs {
+  double* S[kMaxItems];
+};
+
+__global__ void __launch_bounds__(256) set_identity_kernel(IdentityArgs a, long long ld, int n) {
+  double* S = a.S[blockIdx.y];
+  const long long total = ld * ld;
+  for (long long e = (long long)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (long long)gridDim.x * 256) {
+    const long long i = e % ld, j = e / ld;
+    S[e] = (i == j && i < n) ? 1.0 : 0.0;
+  }
+}
+
+cudaError_t launch_set_identity(double* const* S, long long ld, int n, int items,
+                                cudaStream_t s) {
+  IdentityArgs a;
+  for (int z = 0; z < items; ++z) a.S[z] = S[z];
+  set_identity_kernel<<<dim3(148 * 8, (unsigned)items), 256, 0, s>>>(a, ld, n);
   return cudaGetLastError();
 }
 

@@ -116,7 +116,7 @@ class Engine:
         return {"gemm_launches": int(out[0]), "gemm_ms": float(out[1]),
                 "gemm_fp64_flops": float(out[2]), "gemm_int8_ops": float(out[3]),
                 "slice_launches": int(out[4]), "slice_ms": float(out[5]),
-                "slice_bytes": float(out[6])}
+                "slice_bytes": float(out[6]), "host_enqueue_ms": float(out[7])}
 
     def phase_times(self) -> dict:
         out = np.zeros(len(nat.PHASES) + 3)

@@ -142,3 +142,31 @@ def test_domain_errors():
         O.dnu_xnu_knu(0.5, -1.0)
     assert O.dnu_xnu_knu(0.7, 0.0) == 0.0
     assert math.isinf(O.CountingObjective(np.zeros((2, 2)), np.zeros(2)).loglik([1.0, 0.1, 0.5]))
+
+
+def test_nugget_restatement_pins():
+    """eval_all_nugget (config 5, not in the reference): tau^2 = 0 reproduces the reference
+    algorithm's eval_all, and the sigma^2 score matches a central difference of the
+    nugget log-likelihood."""
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(7)
+    loc = rng.uniform(size=(120, 2))
+    th = (1.1, 0.15, 1.3)
+    z = O.cholesky(O.matrix(loc, th)) @ rng.standard_normal(120)
+    a, b = O.eval_all(loc, z, th), O.eval_all_nugget(loc, z, th, 0.0)
+    assert b[0] == pytest.approx(a[0], rel=1e-13)
+    np.testing.assert_allclose(b[1], a[1], rtol=1e-10)
+    np.testing.assert_allclose(b[2], a[2], rtol=1e-10)
+    tau2 = 1e-2
+    ll, g, f = O.eval_all_nugget(loc, z, th, tau2)
+    assert ll == pytest.approx(O.loglik(loc, z, th, tau2), rel=1e-14)
+    for i in range(3):
+        h = 1e-6 * th[i]
+        tp, tm = list(th), list(th)
+        tp[i] += h
+        tm[i] -= h
+        fd = (O.loglik(loc, z, tp, tau2) - O.loglik(loc, z, tm, tau2)) / (2 * h)
+        assert g[i] == pytest.approx(fd, rel=1e-5, abs=1e-6)
+    np.testing.assert_array_equal(f, f.T)
+    assert np.all(np.linalg.eigvalsh(f) > 0)
