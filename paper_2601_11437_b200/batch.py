@@ -3,14 +3,16 @@
 Replicate fits (BASELINE config 2: five fields of n = 3,600) are independent, and each
 Fisher-BT step issues one loglik or eval_all at a time (optimizer.py:345-375).  Instead of
 running the fits one after another, or on five streams that each leave most of the GPU
-idle at this size, every fit runs its unchanged host loop in its own thread while its
-objective hands each evaluation request to a shared :class:`BatchCoordinator`.  When all
-live fits have a request pending, the last one to arrive runs them as ONE batched pass
-through ``mle_eval_batch`` (each kernel launch covers all datasets), then every fit resumes
-with its own result.  Counters, -inf mapping and exception behaviour per fit are exactly
-those of :class:`~paper_2601_11437_b200.fisher_bt.LikelihoodObjective`, and the batched
-kernels compute each item with the same arithmetic as a single evaluation, so every fit is
-bit-identical to running it alone.
+idle at this size, :func:`fit_many` runs every fit as the request generator
+``fisher_bt_gen`` (the unchanged host algorithm) and answers the pending requests of all
+live fits with ONE batched pass through ``mle_eval_batch`` (each kernel launch covers all
+datasets), from a single host thread.  Counters, -inf mapping and exception behaviour per
+fit are exactly those of :class:`~paper_2601_11437_b200.fisher_bt.LikelihoodObjective`, and
+the batched kernels compute each item with the same arithmetic as a single evaluation, so
+every fit is bit-identical to running it alone.
+
+:class:`BatchCoordinator` / :class:`BatchedObjective` offer the same batching to callers that
+run their own objective-calling loops in threads.
 """
 
 from __future__ import annotations
@@ -26,9 +28,10 @@ from .fisher_bt import FisherBTConfig, OptResult, fisher_bt
 from .likelihood import NotPositiveDefinite
 from .matern import MaternParams, SpatialDataset
 
-__all__ = ["BatchCoordinator", "BatchedObjective", "eval_batch", "fit_many"]
+__all__ = ["BatchCoordinator", "BatchedObjective", "LockstepStats", "eval_batch", "fit_many"]
 
 LOGLIK, EVAL_ALL = 1, 2
+LOGLIK_MODE, EVAL_MODE = LOGLIK, EVAL_ALL  # mle_eval_batch modes
 
 
 def eval_batch(engines, thetas, modes):
@@ -158,34 +161,107 @@ class BatchedObjective:
         return ll, grad, fisher
 
 
+class _Counters:
+    """Per-fit call counters with the reference objective's semantics (optimizer.py:127-138)."""
+
+    def __init__(self, data: SpatialDataset):
+        self.data = data
+        self.loglik_calls = 0
+        self.grad_calls = 0
+
+
+class LockstepStats:
+    """Accounting of a lock-step run (same fields as BatchCoordinator)."""
+
+    def __init__(self):
+        self.batches = 0
+        self.requests = 0
+        self.eval_passes = 0
+        self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
+                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0}
+
+
 def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None):
     """Run one Fisher-BT fit per dataset concurrently with lock-step batched evaluation.
 
-    Returns the list of :class:`OptResult` (same order as ``datasets``).
+    Every fit is the request generator ``fisher_bt_gen`` (the unchanged Algorithm 1); one host
+    thread collects the pending request of every live fit and answers them with ONE batched
+    engine pass (``mle_eval_batch``), so no thread hand-offs sit between GPU passes.  Alignment
+    policy as in :class:`BatchCoordinator`: while some fits wait on a loglik and others on an
+    eval_all, only the logliks run.  Counters, -inf mapping and exceptions per fit are those of
+    :class:`~paper_2601_11437_b200.fisher_bt.LikelihoodObjective`; each fit is bit-identical to
+    running it alone.  Returns the list of :class:`OptResult` (same order as ``datasets``).
     """
-    coord = BatchCoordinator(len(datasets))
+    from .fisher_bt import EVAL_ALL, LOGLIK, fisher_bt_gen
+
+    stats = LockstepStats()
     if coordinator_out is not None:
-        coordinator_out.append(coord)
-    objs = [BatchedObjective(d, coord, i) for i, d in enumerate(datasets)]
+        coordinator_out.append(stats)
+    cnt = [_Counters(d) for d in datasets]
+    gens = [fisher_bt_gen(cfg, c) for c in cnt]
     results: list = [None] * len(datasets)
-    errors: list = [None] * len(datasets)
+    pending = {}
 
-    def work(i):
+    def advance(i, how, value):
         try:
-            results[i] = fisher_bt(datasets[i], cfg, objective=objs[i])
-        except BaseException as exc:  # surfaced after join
-            errors[i] = exc
-        finally:
-            coord.retire()
+            pending[i] = how(value) if how is not None else next(gens[i])
+        except StopIteration as stop:
+            pending.pop(i, None)
+            results[i] = stop.value
 
-    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(datasets))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    for e in errors:
-        if e is not None:
-            raise e
+    for i in range(len(gens)):
+        advance(i, None, None)
+    while pending:
+        ids = sorted(pending)
+        cheap = [i for i in ids if pending[i][0] == LOGLIK]
+        if cheap and len(cheap) < len(ids):
+            ids = cheap
+        else:
+            stats.eval_passes += int(any(pending[i][0] == EVAL_ALL for i in ids))
+        answers = {}
+        run, thetas, modes = [], [], []
+        for i in ids:
+            kind, theta_vec = pending[i]
+            c = cnt[i]
+            c.loglik_calls += 1
+            if kind == EVAL_ALL:
+                c.grad_calls += 1
+            try:
+                th = MaternParams.from_array(theta_vec).as_array()
+            except ValueError as exc:  # loglik -> -inf; eval_all raises (optimizer.py:131-138)
+                answers[i] = (-math.inf, None) if kind == LOGLIK else (None, exc)
+                continue
+            run.append(i)
+            thetas.append(th)
+            modes.append(LOGLIK_MODE if kind == LOGLIK else EVAL_MODE)
+        if run:
+            try:
+                out = eval_batch([datasets[i].engine() for i in run], thetas, modes)
+                p = datasets[run[0]].engine().phase_times()
+                p["host_enqueue_ms"] = datasets[run[0]].engine().kernel_stats()["host_enqueue_ms"]
+                for key in stats.acc:
+                    stats.acc[key] += p[key]
+                for i, (rc, piv, ll, grad, fisher) in zip(run, out):
+                    if pending[i][0] == LOGLIK:
+                        ok = rc == nat.MLE_OK and not math.isnan(ll)
+                        answers[i] = (ll if ok else -math.inf, None)
+                    elif rc == nat.MLE_NOT_PD:
+                        answers[i] = (None, NotPositiveDefinite(piv))
+                    elif rc != nat.MLE_OK:
+                        answers[i] = (None, ValueError(nat.last_error()))
+                    else:
+                        answers[i] = ((ll, grad, fisher), None)
+            except Exception as exc:  # CUDA failures reach every fit of the pass
+                for i in run:
+                    answers[i] = (None, exc)
+            stats.batches += 1
+            stats.requests += len(run)
+        for i in ids:
+            value, exc = answers[i]
+            if exc is not None:
+                advance(i, gens[i].throw, exc)
+            else:
+                advance(i, gens[i].send, value)
     if objectives_out is not None:
-        objectives_out.extend(objs)
+        objectives_out.extend(cnt)
     return results

@@ -549,13 +549,14 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 }
 }  // namespace
 
+template <int kSums>  // 7 (no nugget item) or RN = 11
 __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   const int item = blockIdx.y;
   if (*ra.fail_flag[item]) return;
   const double* __restrict__ L = ra.L[item];
   const double* __restrict__ Ba = ra.Ba[item];
   const double* __restrict__ Bn = ra.Bn[item];
-  const double* __restrict__ Bm = ra.Bm[item];
+  const double* __restrict__ Bm = kSums > 7 ? ra.Bm[item] : nullptr;
   const long long ld = ra.ld;
   const int n = ra.n;
   __shared__ double sh[RTHREADS / 32];
@@ -605,7 +606,7 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   }
   double* partials = ra.partials[item];
   for (int q = 0; q < RN; ++q) {
-    const double t = block_sum(s[q], sh);
+    const double t = q < kSums ? block_sum(s[q], sh) : 0.0;
     if (threadIdx.x == 0) partials[blockIdx.x * RN + q] = t;
   }
 }
@@ -632,7 +633,12 @@ __global__ void reduce_final_kernel(ReduceArgs ra) {
 }
 
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {
-  reduce_kernel<<<dim3(RBLOCKS, items), RTHREADS, 0, s>>>(r);
+  bool any_m = false;
+  for (int i = 0; i < items; ++i) any_m = any_m || r.Bm[i] != nullptr;
+  if (any_m)
+    reduce_kernel<RN><<<dim3(RBLOCKS, items), RTHREADS, 0, s>>>(r);
+  else
+    reduce_kernel<7><<<dim3(RBLOCKS, items), RTHREADS, 0, s>>>(r);
   reduce_final_kernel<<<items, 32, 0, s>>>(r);
   return cudaGetLastError();
 }
