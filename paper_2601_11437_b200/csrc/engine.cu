@@ -193,6 +193,11 @@ int ensure_device(int device) {
 
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
+bool use_gen_table() {
+  const char* v = std::getenv("MLE_GEN_TABLE");
+  return !(v && std::strcmp(v, "0") == 0);
+}
+
 bool use_speculation() {
   const char* v = std::getenv("MLE_SPECULATE");
   return !(v && std::strcmp(v, "0") == 0);
@@ -223,6 +228,9 @@ struct mle_ctx {
   double* sa = nullptr;
   double* sn = nullptr;
   double* smat = nullptr;         // nugget contexts: I_n -> M = L^-1 L^-T (third block)
+  double h_max = 0.0;             // bounding-box diagonal of the locations (>= every distance)
+  double* gtab_s = nullptr;       // generation tables: Sigma pass / derivative pass
+  double* gtab_d = nullptr;
   double* linv = nullptr;
   int* fail_flag = nullptr;
   long long* fail_idx = nullptr;
@@ -1033,6 +1041,10 @@ int run_chunk(Item* items, int m) {
     if (rc) return rc;
     // this pass overwrites what a previous speculation left in sa / sn / wsl
     if (it.factor || it.derivs) it.c->spec_ready = false;  // the solves consume S in place
+    if (use_gen_table())
+      mle_fill_gen_table(it.c->h_max / it.P.alpha, &it.P);
+    else
+      it.P.tab_n = 0;
     std::memcpy(it.c->h_theta, &it.P, sizeof(ThetaParams));
     CUDA_TRY(cudaMemcpyAsync(it.c->d_theta, it.c->h_theta, sizeof(ThetaParams),
                              cudaMemcpyHostToDevice, s));
@@ -1057,6 +1069,7 @@ int run_chunk(Item* items, int m) {
       gi.dalpha = it.c->sa;
       gi.dnu = it.c->sn;
       gi.fail_flag = it.c->fail_flag;
+      gi.tab = it.P.tab_n > 0 ? (sigma_pass ? it.c->gtab_s : it.c->gtab_d) : nullptr;
       gi.write_sigma = sigma_pass ? 1 : 0;
       gi.write_derivs = sigma_pass ? 0 : 1;
     }
@@ -1067,7 +1080,8 @@ int run_chunk(Item* items, int m) {
   };
   auto sig = gen_set(true);
   if (sig.second > 0) {
-    run.launches += 1;
+    run.launches += 2;
+    launch_gen_table(sig.first, sig.second, false, s);
     launch_gen_engine(sig.first, sig.second, s);
     CUDA_TRY(cudaGetLastError());
   }
@@ -1100,14 +1114,16 @@ int run_chunk(Item* items, int m) {
       return MLE_OK;
     };
     if (nn > 0) {
-      run.launches += 1;
+      run.launches += 2;
+      launch_gen_table(now, nn, true, aux);
       launch_gen_engine(now, nn, aux);
       CUDA_TRY(cudaGetLastError());
     }
     if ((rc = identities(false))) return rc;
     CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
     if (nl > 0) {
-      run.launches += 1;
+      run.launches += 2;
+      launch_gen_table(later, nl, true, aux);
       launch_gen_engine(later, nl, aux);
       CUDA_TRY(cudaGetLastError());
     }
@@ -1425,6 +1441,18 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   CTX_TRY(dmalloc(&c->partials, sizeof(double) * kReduceBlocks * kReduceSums));
   CTX_TRY(dmalloc(&c->out, sizeof(double) * kReduceOut));
   CTX_TRY(dmalloc(&c->d_theta, sizeof(ThetaParams)));
+  CTX_TRY(dmalloc(&c->gtab_s, sizeof(double) * MLE_TAB_MAX * 3 * MLE_TAB_P));
+  CTX_TRY(dmalloc(&c->gtab_d, sizeof(double) * MLE_TAB_MAX * 3 * MLE_TAB_P));
+  {
+    double x0 = x[0], x1 = x[0], y0 = y[0], y1 = y[0];
+    for (int64_t i = 1; i < n; ++i) {
+      x0 = std::fmin(x0, x[i]);
+      x1 = std::fmax(x1, x[i]);
+      y0 = std::fmin(y0, y[i]);
+      y1 = std::fmax(y1, y[i]);
+    }
+    c->h_max = std::hypot(x1 - x0, y1 - y0);
+  }
   CTX_TRY(hmalloc(&c->h_theta, sizeof(ThetaParams)));
   CTX_TRY(hmalloc(&c->h_res, sizeof(double) * (kReduceOut + 2)));
   CTX_TRY(cudaMemcpyAsync(c->lx, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
@@ -1455,6 +1483,8 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->partials);
   dfree(c->out);
   dfree(c->d_theta);
+  dfree(c->gtab_s);
+  dfree(c->gtab_d);
   dfree(c->lsl);
   dfree(c->lex);
   dfree(c->xsl);

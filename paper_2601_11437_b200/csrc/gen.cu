@@ -89,10 +89,17 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
       const double h = pair_distance(it.lx, it.ly, i, j);
       if (h > 0.0) {
         MaternVals v;
-        if (derivs)
-          v = matern_positive<true>(P, h);
-        else
-          v = matern_positive<false>(P, h);
+        const double u = h / P.alpha;
+        if (it.tab != nullptr && u >= P.tab_lo && u < P.tab_hi) {
+          if (derivs)
+            v = matern_table<true>(P, it.tab, u);
+          else
+            v = matern_table<false>(P, it.tab, u);
+        } else if (derivs) {
+          v = matern_u<true>(P, u);
+        } else {
+          v = matern_u<false>(P, u);
+        }
         c = v.c;
         da = v.dalpha;
         dn = v.dnu;
@@ -121,6 +128,38 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
       it.dalpha[off] = s_da[jl][lane_row];
       it.dnu[off] = s_dn[jl][lane_row];
     }
+  }
+}
+
+// Chebyshev coefficients of e^u * {c, dalpha, dnu}(u) on every table interval of every item
+// (grid: MLE_TAB_MAX x items; one CTA per interval).  Node values come from the exact
+// evaluator (matern_u), so the table inherits its accuracy; with a convergence factor ~22 per
+// interval the degree-13 truncation error is far below one ulp.
+__global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
+  const GenItem& it = a.item[blockIdx.y];
+  if (it.tab == nullptr || (it.fail_flag != nullptr && *it.fail_flag)) return;
+  const ThetaParams& P = *it.P;
+  const int k = blockIdx.x;
+  if (k >= P.tab_n) return;
+  __shared__ double f[3][MLE_TAB_P];
+  const int t = threadIdx.x;
+  if (t < MLE_TAB_P) {
+    const double x = cospi((t + 0.5) / MLE_TAB_P);
+    const double u = P.tab_ctr[k] + P.tab_hw[k] * x;
+    const MaternVals v = derivs ? matern_u<true>(P, u) : matern_u<false>(P, u);
+    const double e = u < MLE_SMALL_MID_SPLIT ? 1.0 : exp(u);  // as matern_table
+    f[0][t] = e * v.c;
+    f[1][t] = e * v.dalpha;
+    f[2][t] = e * v.dnu;
+  }
+  __syncthreads();
+  if (t < 3 * MLE_TAB_P) {
+    const int fn = t / MLE_TAB_P, j = t % MLE_TAB_P;
+    double s = 0.0;
+    for (int q = 0; q < MLE_TAB_P; ++q) s += f[fn][q] * cospi(j * (q + 0.5) / MLE_TAB_P);
+    s *= 2.0 / MLE_TAB_P;
+    if (j == 0) s *= 0.5;
+    it.tab[((size_t)k * 3 + fn) * MLE_TAB_P + j] = s;
   }
 }
 
@@ -231,6 +270,10 @@ static long long lower_tiles(long long rows) {
 void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s) {
   const dim3 grid((unsigned)lower_tiles(a.rows), (unsigned)items);
   gen_engine_kernel<<<grid, kGThreads, 0, s>>>(a);
+}
+
+void launch_gen_table(const GenArgs& a, int items, bool derivs, cudaStream_t s) {
+  gen_table_kernel<<<dim3(MLE_TAB_MAX, (unsigned)items), 64, 0, s>>>(a, derivs ? 1 : 0);
 }
 
 void launch_gen_build(const GenArgs& a, int which, cudaStream_t s) {

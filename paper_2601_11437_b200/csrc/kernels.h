@@ -26,6 +26,7 @@ struct GenItem {
   double* dalpha;     // dSigma/dalpha (full storage)
   double* dnu;        // dSigma/dnu (full storage)
   const int* fail_flag;
+  double* tab;        // generation table ([MLE_TAB_MAX][3][MLE_TAB_P]); null: exact path
   int write_sigma;    // 1: write Sigma (lower tiles + augmented row + padding)
   int write_derivs;   // 1: write both derivative matrices (full storage)
 };
@@ -82,6 +83,8 @@ cudaError_t init_kernel_attributes();  // GEMM smem opt-in (per device)
 cudaError_t init_diag_attributes();    // diagonal-tile kernel smem opt-in (per device)
 cudaError_t upload_u_tables(const double* u, const double* du);
 void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s);
+// Coefficients of the items' generation tables (items with tab == null are skipped).
+void launch_gen_table(const GenArgs& a, int items, bool derivs, cudaStream_t s);
 void launch_gen_build(const GenArgs& a, int which, cudaStream_t s);
 void launch_elem(const ThetaParams* P_dev, int op, int which, const double* x, long long m,
                  double* out, cudaStream_t s);

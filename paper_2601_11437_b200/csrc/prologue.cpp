@@ -7,6 +7,7 @@
 // special functions the reference takes from scipy (Gamma, digamma) are evaluated in
 // 80-bit long double and rounded once.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "theta.h"
@@ -260,4 +261,42 @@ void mle_fill_u_tables(double* u, double* du) {
     const int size = 3 * k + 1;
     for (int j = 1; j < size; ++j) d[j - 1] = c[j] * (double)j;
   }
+}
+
+void mle_fill_gen_table(double u_max, ThetaParams* P) {
+  P->tab_n = 0;
+  for (int sgi = 0; sgi < 3; ++sgi) {
+    P->seg_base[sgi] = 0;
+    P->seg_cnt[sgi] = 0;
+    P->seg_log0[sgi] = 0.0;
+    P->seg_inv[sgi] = 0.0;
+  }
+  const double hi = std::fmin(u_max * (1.0 + 1e-9), MLE_TAB_HI);
+  double lo = MLE_TAB_LO;
+  if (const char* v = std::getenv("MLE_TAB_LO")) lo = std::atof(v);  // developer override
+  P->tab_lo = lo;
+  P->tab_hi = hi;
+  if (!(hi > lo) || !(lo < MLE_SMALL_MID_SPLIT)) return;
+  const double bounds[4] = {lo, MLE_SMALL_MID_SPLIT, MLE_MID_LARGE_SPLIT, MLE_TAB_HI};
+  const double max_ratio = 1.2;  // interval [a, 1.2 a]: Chebyshev convergence factor ~22
+  int k = 0;
+  for (int sgi = 0; sgi < 3; ++sgi) {
+    const double a = bounds[sgi], b = std::fmin(bounds[sgi + 1], hi);
+    P->seg_base[sgi] = k;
+    if (!(b > a)) continue;
+    int cnt = (int)std::ceil(std::log(b / a) / std::log(max_ratio));
+    if (cnt < 1) cnt = 1;
+    const double ratio = std::pow(b / a, 1.0 / cnt);
+    P->seg_cnt[sgi] = cnt;
+    P->seg_log0[sgi] = std::log2(a);
+    P->seg_inv[sgi] = 1.0 / std::log2(ratio);
+    for (int j = 0; j < cnt; ++j, ++k) {
+      const double lo = a * std::pow(ratio, (double)j);
+      const double up = (j == cnt - 1) ? b : a * std::pow(ratio, (double)(j + 1));
+      P->tab_ctr[k] = 0.5 * (lo + up);
+      P->tab_hw[k] = 0.5 * (up - lo);
+      P->tab_ihw[k] = 1.0 / P->tab_hw[k];
+    }
+  }
+  P->tab_n = k;
 }

@@ -210,10 +210,10 @@ struct MaternVals {
   double c, dalpha, dnu;
 };
 
+// Element values as functions of the scaled distance u = h / alpha > 0.
 template <bool kDerivs>
-__device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, double h) {
+__device__ __forceinline__ MaternVals matern_u(const ThetaParams& P, double u) {
   MaternVals out;
-  const double u = h / P.alpha;
   double k_nu, k_num1;
   bessel_k_ladder(P.kmain, P.recip_int, u, &k_nu, &k_num1);
   const double u_nu = pow(u, P.nu);
@@ -222,6 +222,56 @@ __device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, doub
     out.dalpha = P.scale_a * (u_nu * u) * k_num1;                   // matern.py:111
     const double f = u_nu * k_nu;                                   // matern.py:122
     out.dnu = P.sigma2 * P.q * (P.dlog_q * f + dnu_xnu_knu(P, u, f, u_nu));  // matern.py:125
+  } else {
+    out.dalpha = 0.0;
+    out.dnu = 0.0;
+  }
+  return out;
+}
+
+template <bool kDerivs>
+__device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, double h) {
+  return matern_u<kDerivs>(P, h / P.alpha);  // u = h / alpha (matern.py:103)
+}
+
+// ---- table path ------------------------------------------------------------------------
+// Interval of u (segment chosen by exact comparison with the regime boundaries, position
+// inside the segment by a float log2; an off-by-one near an interval edge only evaluates
+// the neighbouring Chebyshev series marginally outside [-1, 1]).
+__device__ __forceinline__ int gen_tab_index(const ThetaParams& P, double u) {
+  const int s = u < MLE_SMALL_MID_SPLIT ? 0 : (u < MLE_MID_LARGE_SPLIT ? 1 : 2);
+  int k = (int)((__log2f((float)u) - (float)P.seg_log0[s]) * (float)P.seg_inv[s]);
+  k = k < 0 ? 0 : (k >= P.seg_cnt[s] ? P.seg_cnt[s] - 1 : k);
+  return P.seg_base[s] + k;
+}
+
+// Clenshaw sum of c[0] + sum_{j>=1} c[j] T_j(t)  (c[0] stored halved).
+__device__ __forceinline__ double cheb_eval(const double* __restrict__ c, double t) {
+  const double t2 = 2.0 * t;
+  double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+  for (int j = MLE_TAB_P - 1; j >= 1; --j) {
+    const double b0 = fma(t2, b1, __ldg(c + j) - b2);
+    b2 = b1;
+    b1 = b0;
+  }
+  return fma(t, b1, __ldg(c) - b2);
+}
+
+// tab: [MLE_TAB_MAX][3][MLE_TAB_P] coefficients of e^u * {c, dalpha, dnu}.
+template <bool kDerivs>
+__device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
+                                                   const double* __restrict__ tab, double u) {
+  const int k = gen_tab_index(P, u);
+  const double t = (u - P.tab_ctr[k]) * P.tab_ihw[k];
+  // below 8.5 the series are of E itself (no e^u scaling error); above, of e^u E
+  const double eu = u < MLE_SMALL_MID_SPLIT ? 1.0 : exp(-u);
+  const double* c = tab + (size_t)k * 3 * MLE_TAB_P;
+  MaternVals out;
+  out.c = eu * cheb_eval(c, t);
+  if (kDerivs) {
+    out.dalpha = eu * cheb_eval(c + MLE_TAB_P, t);
+    out.dnu = eu * cheb_eval(c + 2 * MLE_TAB_P, t);
   } else {
     out.dalpha = 0.0;
     out.dnu = 0.0;

@@ -16,6 +16,10 @@
 #define MLE_CASE3_FAR 8          // bessel.py:54
 #define MLE_CASE4_TERMS 5        // bessel.py:55
 #define MLE_U_COEFF_STRIDE 40    // >= 3*12+1 coefficients per Debye polynomial
+#define MLE_TAB_P 14              // Chebyshev points per interval (degree 13)
+#define MLE_TAB_MAX 48            // intervals per table
+#define MLE_TAB_LO 0.25           // below: exact evaluation (few pairs)
+#define MLE_TAB_HI 800.0          // above: exact evaluation (elements underflow anyway)
 #define MLE_SMALL_MID_SPLIT 8.5  // bessel.py:46
 #define MLE_MID_LARGE_SPLIT 30.0 // bessel.py:47
 #define MLE_MID_TRUNC_SPLIT 15.0 // bessel.py:48
@@ -72,6 +76,15 @@ struct ThetaParams {
   double c4_b[MLE_CASE4_TERMS + 1];
   int c4_kmax;                              // last k with a_k != 0
   double nu_m_half;                         // nu - 0.5
+  // ---- engine generation tables (filled per pass by the engine, mle_fill_gen_table) ----
+  // For u = h / alpha in [tab_lo, tab_hi): e^u * {Sigma, dalpha, dnu element} as Chebyshev
+  // series of degree MLE_TAB_P - 1 on log-spaced intervals, in three segments split exactly
+  // at the reference's dnu regime boundaries 8.5 and 30 (bessel.py:46-47).
+  int tab_n;                                // intervals (0: exact evaluation everywhere)
+  int seg_base[3], seg_cnt[3];
+  double seg_log0[3], seg_inv[3];           // log2(segment start), 1 / log2(ratio)
+  double tab_lo, tab_hi;
+  double tab_ctr[MLE_TAB_MAX], tab_hw[MLE_TAB_MAX], tab_ihw[MLE_TAB_MAX];
 };
 
 #ifdef __cplusplus
@@ -84,5 +97,8 @@ void mle_fill_ladder(double order, KLadder* L);
 // Debye U_k coefficient tables (bessel.py:144-176), flattened [k][j] with stride
 // MLE_U_COEFF_STRIDE, for U and U'.  Filled once.
 void mle_fill_u_tables(double* u, double* du);
+// Interval layout of the generation tables for scaled distances up to u_max (tab_n = 0
+// when u_max < MLE_TAB_LO).
+void mle_fill_gen_table(double u_max, ThetaParams* P);
 }
 #endif

@@ -133,3 +133,25 @@ def test_speculation_bit_identical(gpu):
             np.testing.assert_array_equal(x[2], y[2])
         else:
             assert x == y
+
+
+def test_generation_tables_vs_exact(gpu):
+    """Chebyshev generation tables (gen.cu) vs the exact per-element evaluator: same
+    likelihood / Fisher / score to well inside the north-star tolerances (the FD band at
+    nu = 1 keeps the reference's own ~1e-6 element noise, compared at the FD carve-out)."""
+    from conftest import fd_regime
+
+    loc, z = config_data("config2", 4)
+    for th in ([1.0, 0.2, 1.5], [0.8, 0.1, 1.0], [1.3, 0.05, 0.7], [1.2, 0.15, 1.2]):
+        th = np.array(th)
+        ex = _with_env("MLE_GEN_TABLE", "0", lambda: gpu.Engine(loc, z).eval_all(th))
+        tb = _with_env("MLE_GEN_TABLE", "1", lambda: gpu.Engine(loc, z).eval_all(th))
+        assert tb[0] == pytest.approx(ex[0], rel=1e-11)
+        fd = fd_regime(th)
+        tol_f = np.full((3, 3), 1e-9)
+        if fd:
+            tol_f[2, :] = tol_f[:, 2] = 1e-5
+        assert np.all(np.abs(tb[2] - ex[2]) <= tol_f * np.abs(ex[2])), (th, tb[2], ex[2])
+        scale = score_scale(th, len(z), ex[1], ex[2])
+        tol_g = np.array([1e-10, 1e-10, 1e-5 if fd else 1e-9])
+        assert np.all(np.abs(tb[1] - ex[1]) <= tol_g * scale), (th, tb[1], ex[1])
