@@ -198,6 +198,11 @@ bool use_gen_table() {
   return !(v && std::strcmp(v, "0") == 0);
 }
 
+bool use_lookahead() {  // MLE_LOOKAHEAD=0: everything on the main stream (A/B timing)
+  const char* v = std::getenv("MLE_LOOKAHEAD");
+  return !(v && std::strcmp(v, "0") == 0);
+}
+
 bool use_speculation() {
   const char* v = std::getenv("MLE_SPECULATE");
   return !(v && std::strcmp(v, "0") == 0);
@@ -219,6 +224,7 @@ struct mle_ctx {
   double nugget = 0.0;
   cudaStream_t stream = nullptr;  // main stream (every call is serialised on it)
   cudaStream_t side = nullptr;    // look-ahead bulk trailing updates
+  cudaStream_t inner = nullptr;   // inner (128-wide) look-ahead of the Cholesky
   cudaStream_t aux = nullptr;     // derivative generation concurrent with the Cholesky
   cudaEvent_t pool[kPoolEvents] = {};
   double* lx = nullptr;
@@ -344,6 +350,7 @@ size_t w_byte_offset(int Nt, int b) {
   return r;
 }
 constexpr int kOzK = kOuter * kNB;               // K of every trailing update
+constexpr int kLookaheadCtas = 148 - 24;         // persistent grid of look-ahead updates
 constexpr size_t kOzRowBytes = (size_t)kOzK * kOzSlices;
 constexpr size_t kOzTileBytes = kOzRowBytes * kNB;
 
@@ -501,6 +508,8 @@ struct Launcher {
     return MLE_OK;
   }
   cudaStream_t bulk() const { return s2 ? s2 : s; }
+  cudaStream_t s3 = nullptr;   // inner look-ahead of the Cholesky (null: on s)
+  cudaStream_t inner() const { return s3 ? s3 : s; }
 
   // Two-level right-looking blocked Cholesky of every item's matrix (ld = N).
   int potrf(mle_ctx* const* cs, double* const* mats, const long long* n_aug, int m) {
@@ -526,34 +535,59 @@ struct Launcher {
         CUDA_TRY(launch_potrf_diag(d, m, s));
         const int rem = Nt - k - 1;
         if (rem == 0) break;
-        // panel <- panel * Linv_k^T   (in place: BN = 128 covers the whole panel width)
-        GemmArgs g = gemm_base();
-        for (int b = 0; b < m; ++b) {
-          double* panel = mats[b] + (k0 + kNB) + k0 * ld;
-          g.A[b] = panel;
-          g.B[b] = cs[b]->linv + (size_t)k * kNB * kNB;
-          g.C[b] = panel;
-          g.fail_flag[b] = cs[b]->fail_flag;
-        }
-        g.lda = ld; g.ldb = kNB; g.ldc = ld;
-        g.tiles_m = rem; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
-        if ((rc = gemm(g, kBNK, m))) return rc;
-        // inner update of the remaining columns of this outer block (lower trapezoid)
-        const int wcols = b1 - k - 1;
-        if (wcols > 0) {
+        const int wcols = b1 - k - 1;  // remaining tile columns of this outer block
+        auto panel_gemm = [&](int row_tiles, int row_off, cudaStream_t st) {
+          // panel rows [k+1+row_off, k+1+row_off+row_tiles) <- panel * Linv_k^T, in place
+          // (BN = 128 covers the whole panel width)
+          GemmArgs g = gemm_base();
+          for (int b = 0; b < m; ++b) {
+            double* panel = mats[b] + (k0 + kNB + (long long)row_off * kNB) + k0 * ld;
+            g.A[b] = panel;
+            g.B[b] = cs[b]->linv + (size_t)k * kNB * kNB;
+            g.C[b] = panel;
+            g.fail_flag[b] = cs[b]->fail_flag;
+          }
+          g.lda = ld; g.ldb = kNB; g.ldc = ld;
+          g.tiles_m = row_tiles; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
+          return gemm(g, kBNK, m, st);
+        };
+        // A[r0+.., c0+..] -= P[r0..] P[c0..]^T over tile rows/cols of this outer block
+        auto update = [&](int row_off, int row_tiles, int col_off, int col_tiles, bool trap,
+                          cudaStream_t st) {
           GemmArgs t = gemm_base();
           for (int b = 0; b < m; ++b) {
             double* panel = mats[b] + (k0 + kNB) + k0 * ld;
-            t.A[b] = panel;
-            t.B[b] = panel;
-            t.C[b] = mats[b] + (k0 + kNB) + (k0 + kNB) * ld;
+            t.A[b] = panel + (long long)row_off * kNB;
+            t.B[b] = panel + (long long)col_off * kNB;
+            t.C[b] = mats[b] + (k0 + kNB + (long long)row_off * kNB) +
+                     (k0 + kNB + (long long)col_off * kNB) * ld;
             t.fail_flag[b] = cs[b]->fail_flag;
           }
           t.lda = ld; t.ldb = ld; t.ldc = ld;
-          t.tiles_m = rem; t.tiles_n = wcols; t.trap = 1; t.alpha = -1.0; t.beta = 1.0;
-          if ((rc = gemm(t, kBNK, m))) return rc;
+          t.tiles_m = row_tiles; t.tiles_n = col_tiles; t.trap = trap ? 1 : 0;
+          t.alpha = -1.0; t.beta = 1.0;
+          return gemm(t, kBNK, m, st);
+        };
+        if ((rc = join(s3, s))) return rc;  // the previous step's bulk work on the inner stream
+        if (wcols == 0) {
+          // last tile of the outer block: the whole panel (read by the trailing update)
+          if ((rc = panel_gemm(rem, 0, s))) return rc;
+          continue;
+        }
+        // Inner look-ahead: the critical chain to the next diagonal tile is only
+        //   panel rows of tile k+1  ->  update of tile (k+1, k+1)  ->  diag(k+1);
+        // the other panel rows and updates run on the inner stream meanwhile.
+        if ((rc = panel_gemm(1, 0, s))) return rc;
+        if ((rc = join(s, s3))) return rc;
+        if ((rc = update(0, 1, 0, 1, true, s))) return rc;
+        if (rem > 1) {
+          cudaStream_t in = inner();
+          if ((rc = panel_gemm(rem - 1, 1, in))) return rc;
+          if ((rc = update(1, rem - 1, 0, 1, false, in))) return rc;  // column k+1, rows >= k+2
+          if (wcols > 1 && (rc = update(1, rem - 1, 1, wcols - 1, true, in))) return rc;
         }
       }
+      if ((rc = join(s3, s))) return rc;
       if (b1 >= Nt) continue;
       // trailing update with P = L[T, b0:b1], K = (b1 - b0) * 128
       const int b2 = std::min(Nt, b1 + kOuter);
@@ -587,6 +621,7 @@ struct Launcher {
         if ((rc = join(s, s2))) return rc;
         OzGemmArgs u = oz_base(ld, Nt - b2, 0);        // (ii)
         u.lower = 1;
+        u.max_ctas = kLookaheadCtas;  // the next block's diagonal chain runs meanwhile
         for (int b = 0; b < m; ++b) {
           u.As[b] = u.Bs[b] = sa.slices[b] + (size_t)(b2 - b1) * kOzTileBytes;
           u.ea[b] = u.eb[b] = sa.e[b] + (size_t)(b2 - b1) * kNB;
@@ -1030,7 +1065,9 @@ int run_chunk(Item* items, int m) {
   const auto host_t0 = std::chrono::steady_clock::now();
   mle_ctx* lead = items[0].c;
   cudaStream_t s = lead->stream;
-  Launcher run{s, lead->kprof ? nullptr : lead->side, lead->pool, kPoolEvents};
+  const bool lookahead = !lead->kprof && use_lookahead();
+  Launcher run{s, lookahead ? lead->side : nullptr, lead->pool, kPoolEvents};
+  if (lookahead) run.s3 = lead->inner;
   if (lead->kprof) run.prof = lead;
   cudaStream_t aux = lead->kprof ? s : lead->aux;  // profiling: everything serialised
   for (int b = 0; b < m; ++b) {
@@ -1428,6 +1465,7 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   CTX_TRY(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
   CTX_TRY(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_high));
   CTX_TRY(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_high));
+  CTX_TRY(cudaStreamCreateWithPriority(&c->inner, cudaStreamNonBlocking, prio_high));
   CTX_TRY(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_low));
   for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
   CTX_TRY(cudaEventCreateWithFlags(&c->ev_der, cudaEventDisableTiming));
@@ -1506,6 +1544,7 @@ void mle_ctx_destroy(mle_ctx* c) {
   if (c->ev_der) cudaEventDestroy(c->ev_der);
   if (c->spec_done) cudaEventDestroy(c->spec_done);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->inner) cudaStreamDestroy(c->inner);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;

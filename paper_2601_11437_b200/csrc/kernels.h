@@ -140,6 +140,8 @@ struct OzGemmArgs {
   double alpha, beta;
   int beta0_tm, beta0_tn;  // tiles with tm < beta0_tm or tn < beta0_tn overwrite (beta = 0)
   int tiles_m_z[kMaxGemm];  // full/trap mode: per-member row tiles (0: tiles_m)
+  int max_ctas;             // persistent grid cap (0: one CTA per SM); look-ahead launches
+                            // leave SMs to the latency-bound factorization chain
   int diag_mode;  // developer diagnostics only: 1 skip the MMAs, 2 skip the loads (0: normal)
   long long* diag_out;  // developer diagnostics: MMA-thread timing of CTA 0 (null: off)
 };

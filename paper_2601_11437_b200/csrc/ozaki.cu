@@ -138,8 +138,11 @@ constexpr int kOzSliceMaxK = 512;
 constexpr int kOzSliceStride = kOzSliceMaxK + 1;  // odd stride: conflict-free row access
 constexpr int kOzSliceSmem = kOzSliceRows * kOzSliceStride * 8;
 
+constexpr int kOzSliceThreads = 512;
+constexpr int kOzSliceWarps = kOzSliceThreads / 32;
+
 template <int kRowContig>
-__global__ void __launch_bounds__(256) oz_slice_kernel(OzSliceArgs sa) {
+__global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs sa) {
   const int z = blockIdx.z;
   if (sa.fail_flag[z] && *sa.fail_flag[z]) return;
   extern __shared__ double tile[];  // [32][kOzSliceStride]
@@ -149,22 +152,46 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzSliceArgs sa) {
   const int K = sa.K, t = threadIdx.x, w = t >> 5, l = t & 31;
   const long long r0 = (long long)blockIdx.x * kOzSliceRows;
   if (sa.rows_z[z] > 0 && r0 >= sa.rows_z[z]) return;
-  if (kRowContig) {  // X(r,k) = X[r + k ld]: lanes along r
-    for (int k = w; k < K; k += 8) tile[l * kOzSliceStride + k] = X[r0 + l + (long long)k * ld];
-  } else {           // X(r,k) = X[k + r ld]: lanes along k
-    for (int r = w; r < kOzSliceRows; r += 8) {
+  // loads: 16 independent 8-byte loads in flight per lane, then the shared-memory stores
+  if (kRowContig) {  // X(r,k) = X[r + k ld]: lanes along r, warps over k
+    constexpr int kStep = kOzSliceWarps * 16;
+    for (int k0 = w; k0 < K; k0 += kStep) {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = k0 + q * kOzSliceWarps;
+        v[q] = k < K ? X[r0 + l + (long long)k * ld] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = k0 + q * kOzSliceWarps;
+        if (k < K) tile[l * kOzSliceStride + k] = v[q];
+      }
+    }
+  } else {           // X(r,k) = X[k + r ld]: lanes along k, warps over rows
+    for (int r = w; r < kOzSliceRows; r += kOzSliceWarps) {
       const double* row = X + (r0 + r) * ld;
-      for (int k = l; k < K; k += 32) tile[r * kOzSliceStride + k] = row[k];
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = l + 32 * q;
+        v[q] = k < K ? row[k] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = l + 32 * q;
+        if (k < K) tile[r * kOzSliceStride + k] = v[q];
+      }
     }
   }
   if (sa.upper_zero) {  // only the lower trapezoid k <= r is valid: zero the rest
     __syncthreads();
-    for (int r = w; r < kOzSliceRows; r += 8)
+    for (int r = w; r < kOzSliceRows; r += kOzSliceWarps)
       for (int k = l; k < K; k += 32)
         if (k > r0 + r) tile[r * kOzSliceStride + k] = 0.0;
   }
   __syncthreads();
-  for (int r = w; r < kOzSliceRows; r += 8) {
+  for (int r = w; r < kOzSliceRows; r += kOzSliceWarps) {
     double mx = 0.0;
     for (int k = l; k < K; k += 32) mx = fmax(mx, fabs(tile[r * kOzSliceStride + k]));
 #pragma unroll
@@ -182,7 +209,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzSliceArgs sa) {
   const long long tile128 = r0 >> 7;
   const int rsub = (int)(r0 & 127);
   // work item = (row, 16-wide k chunk); lanes on consecutive rows
-  for (int item = t; item < kOzSliceRows * (K / 16); item += 256) {
+  for (int item = t; item < kOzSliceRows * (K / 16); item += kOzSliceThreads) {
     const int r = item & (kOzSliceRows - 1), ch = item / kOzSliceRows;
     // |x| 2^(56 - e) < 2^56 is exact (power-of-two scaling); its truncation holds the 8
     // base-128 digits the float recurrence (x 2^7, trunc, subtract) would produce.
@@ -651,9 +678,9 @@ cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int
   if (a.K > kOzSliceMaxK || a.K % OZ_KB || rows % 128) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)(rows / kOzSliceRows), 1, (unsigned)batch);
   if (row_contig)
-    oz_slice_kernel<1><<<grid, 256, kOzSliceSmem, s>>>(a);
+    oz_slice_kernel<1><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   else
-    oz_slice_kernel<0><<<grid, 256, kOzSliceSmem, s>>>(a);
+    oz_slice_kernel<0><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -664,7 +691,8 @@ cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_
   if (n_tile == 0 || n_tile == 1) {  // persistent: 0 -> 128 x 64 tiles, 1 -> 128 x 32
     const int kn = n_tile == 0 ? 64 : 32;
     const long long per_z = tiles * (128 / kn), total = per_z * batch;
-    const long long grid = std::min<long long>(total, g_num_sms);
+    const long long cap = g.max_ctas > 0 ? std::min(g.max_ctas, g_num_sms) : g_num_sms;
+    const long long grid = std::min<long long>(total, cap);
     if (kn == 64)
       ozgemm_persistent_kernel<64><<<(unsigned)grid, OZP_THREADS, OzP<64>::kSmem, s>>>(
           g, per_z, total);
