@@ -244,6 +244,12 @@ struct mle_ctx {
   double* out = nullptr;          // device: 9 reduction results
   ThetaParams* d_theta = nullptr; // device copy of the per-theta scalars
   ThetaParams* h_theta = nullptr; // pinned staging
+  // batch-leader staging: every item's ThetaParams (H2D once per pass) and every item's
+  // results (D2H once per pass)
+  ThetaParams* h_stage = nullptr;
+  ThetaParams* d_stage = nullptr;
+  double* h_resb = nullptr;
+  double* d_resb = nullptr;
   double* h_res = nullptr;        // pinned: kReduceOut results + fail flag + fail idx
   cudaEvent_t ev[5] = {};
   cudaEvent_t ev_der = nullptr;   // derivative generation for this pass's eval_all items
@@ -1082,10 +1088,19 @@ int run_chunk(Item* items, int m) {
       mle_fill_gen_table(it.c->h_max / it.P.alpha, &it.P);
     else
       it.P.tab_n = 0;
-    std::memcpy(it.c->h_theta, &it.P, sizeof(ThetaParams));
-    CUDA_TRY(cudaMemcpyAsync(it.c->d_theta, it.c->h_theta, sizeof(ThetaParams),
+    std::memcpy(lead->h_stage + b, &it.P, sizeof(ThetaParams));
+  }
+  {  // one H2D copy of all items' parameters, scattered (+ failure flags cleared) on device
+    PassIo io;
+    std::memset(&io, 0, sizeof(io));
+    for (int b = 0; b < m; ++b) {
+      io.theta[b] = items[b].c->d_theta;
+      io.flag[b] = items[b].c->fail_flag;
+    }
+    CUDA_TRY(cudaMemcpyAsync(lead->d_stage, lead->h_stage, sizeof(ThetaParams) * m,
                              cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemsetAsync(it.c->fail_flag, 0, sizeof(int), s));
+    run.launches += 1;
+    CUDA_TRY(launch_scatter_theta(io, lead->d_stage, m, s));
   }
   CUDA_TRY(cudaEventRecord(lead->ev[0], s));
   // Generation.  Sigma (items that factor) on the main stream; the derivative matrices on
@@ -1236,13 +1251,17 @@ int run_chunk(Item* items, int m) {
   run.launches += 2;
   CUDA_TRY(launch_reduce(ra, m, s));
   CUDA_TRY(cudaEventRecord(lead->ev[4], s));
-  for (int b = 0; b < m; ++b) {
-    mle_ctx* c = items[b].c;
-    CUDA_TRY(cudaMemcpyAsync(c->h_res, c->out, sizeof(double) * kReduceOut,
-                             cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(c->h_res + kReduceOut, c->fail_flag, sizeof(int),
-                             cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(c->h_res + kReduceOut + 1, c->fail_idx, sizeof(long long),
+  {  // gather every item's results + flag + pivot, one D2H copy
+    PassIo io;
+    std::memset(&io, 0, sizeof(io));
+    for (int b = 0; b < m; ++b) {
+      io.out[b] = items[b].c->out;
+      io.flag[b] = items[b].c->fail_flag;
+      io.idx[b] = items[b].c->fail_idx;
+    }
+    run.launches += 1;
+    CUDA_TRY(launch_gather_results(io, lead->d_resb, m, s));
+    CUDA_TRY(cudaMemcpyAsync(lead->h_resb, lead->d_resb, sizeof(double) * m * (kReduceOut + 2),
                              cudaMemcpyDeviceToHost, s));
   }
   const auto host_t1 = std::chrono::steady_clock::now();
@@ -1267,6 +1286,9 @@ int run_chunk(Item* items, int m) {
       gbytes += 2.0 * 8.0 * nd * (nd + 1.0) / 2.0;
     }
   }
+  for (int b = 0; b < m; ++b)
+    std::memcpy(items[b].c->h_res, lead->h_resb + (size_t)b * (kReduceOut + 2),
+                sizeof(double) * (kReduceOut + 2));
   for (int b = 0; b < m; ++b) {
     Item& it = items[b];
     mle_ctx* c = it.c;
@@ -1492,6 +1514,10 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
     c->h_max = std::hypot(x1 - x0, y1 - y0);
   }
   CTX_TRY(hmalloc(&c->h_theta, sizeof(ThetaParams)));
+  CTX_TRY(hmalloc(&c->h_stage, sizeof(ThetaParams) * kMaxItems));
+  CTX_TRY(dmalloc(&c->d_stage, sizeof(ThetaParams) * kMaxItems));
+  CTX_TRY(hmalloc(&c->h_resb, sizeof(double) * kMaxItems * (kReduceOut + 2)));
+  CTX_TRY(dmalloc(&c->d_resb, sizeof(double) * kMaxItems * (kReduceOut + 2)));
   CTX_TRY(hmalloc(&c->h_res, sizeof(double) * (kReduceOut + 2)));
   CTX_TRY(cudaMemcpyAsync(c->lx, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CTX_TRY(cudaMemcpyAsync(c->ly, y.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
@@ -1521,6 +1547,10 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->partials);
   dfree(c->out);
   dfree(c->d_theta);
+  dfree(c->d_stage);
+  dfree(c->d_resb);
+  if (c->h_stage) dfree(c->h_stage);
+  if (c->h_resb) dfree(c->h_resb);
   dfree(c->gtab_s);
   dfree(c->gtab_d);
   dfree(c->lsl);

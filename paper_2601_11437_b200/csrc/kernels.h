@@ -102,6 +102,20 @@ cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
 cudaError_t launch_linv_to_dinv(double* const* dinv, const double* const* linv, int Nt,
                                 int items, cudaStream_t s);
 
+// Per-pass bookkeeping in two launches instead of per-item copies: scatter the staged
+// ThetaParams of every item into its context (and clear its failure flag), and gather every
+// item's kReduceOut results + failure flag + pivot into one buffer (slots of 8 bytes:
+// [0, kReduceOut) results, kReduceOut flag (int), kReduceOut + 1 pivot (long long)).
+struct PassIo {
+  ThetaParams* theta[kMaxItems];
+  int* flag[kMaxItems];
+  const double* out[kMaxItems];
+  const long long* idx[kMaxItems];
+};
+cudaError_t launch_scatter_theta(const PassIo& io, const ThetaParams* staged, int items,
+                                 cudaStream_t s);
+cudaError_t launch_gather_results(const PassIo& io, double* dst, int items, cudaStream_t s);
+
 // S = I_n inside the padded N x N matrix (zero elsewhere), for every item.
 cudaError_t launch_set_identity(double* const* S, long long ld, int n, int items,
                                 cudaStream_t s);

@@ -713,4 +713,39 @@ cudaError_t launch_set_identity(double* const* S, long long ld, int n, int items
   return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) scatter_theta_kernel(PassIo io,
+                                                            const ThetaParams* staged) {
+  const int b = blockIdx.x;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(staged + b);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(io.theta[b]);
+  constexpr int words = (int)(sizeof(ThetaParams) / 8);
+  static_assert(sizeof(ThetaParams) % 8 == 0, "ThetaParams is copied in 8-byte words");
+  for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+  if (threadIdx.x == 0) *io.flag[b] = 0;
+}
+
+__global__ void gather_results_kernel(PassIo io, double* dst) {
+  const int b = blockIdx.x, q = threadIdx.x;
+  double* d = dst + (size_t)b * (kReduceOut + 2);
+  if (q < kReduceOut) d[q] = io.out[b][q];
+  if (q == kReduceOut) {
+    int f = *io.flag[b];
+    long long bits = 0;
+    memcpy(&bits, &f, sizeof(int));
+    reinterpret_cast<long long*>(d)[kReduceOut] = bits;
+  }
+  if (q == kReduceOut + 1) reinterpret_cast<long long*>(d)[kReduceOut + 1] = *io.idx[b];
+}
+
+cudaError_t launch_scatter_theta(const PassIo& io, const ThetaParams* staged, int items,
+                                 cudaStream_t s) {
+  scatter_theta_kernel<<<items, 256, 0, s>>>(io, staged);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_results(const PassIo& io, double* dst, int items, cudaStream_t s) {
+  gather_results_kernel<<<items, 32, 0, s>>>(io, dst);
+  return cudaGetLastError();
+}
+
 }  // namespace mle
