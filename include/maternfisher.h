@@ -159,6 +159,40 @@ int mle_dnu_xnu_knu(double nu, const double* x, int64_t m, int device, double* o
 int mle_matern_elem(const double theta[3], int which, const double* h, int64_t m, int device,
                     double* out);
 
+
+/* ---- Distributed engine (configs 4-5 over several GPUs) ----------------------
+ * One context per rank.  Outer blocks of 512 columns are owned cyclically (block b by rank
+ * b % world); a rank holds the full-height column panels of Sigma -> L and of the derivative
+ * blocks for its blocks.  The host driver (paper_2601_11437_b200/distributed.py) runs, per
+ * evaluation:
+ *   begin(theta) on every rank;
+ *   for b: factor(b) on its owner -> broadcast P_b -> update(b) on every rank;
+ *   (eval_all) for b: wblock(b) on the owner -> broadcast W_b -> forward(b) everywhere;
+ *   (eval_all) for b: owner re-sends W_b, right_operand(b) -> broadcast X_b -> right(b);
+ *   partials() on every rank -> all-reduce(sum).
+ * Exchange buffers are device memory owned by the caller (NCCL sends them); sizes from
+ * mle_dctx_layout.  Every call returns after this rank's stream drained.  Replaces the
+ * reference's single-process likelihood.py:107-149 for n beyond one GPU's memory.
+ */
+typedef struct mle_dctx mle_dctx;
+int mle_dctx_create(const double* locs_xy, const double* z, int64_t n, int device,
+                    double nugget, int rank, int world, mle_dctx** out);
+void mle_dctx_destroy(mle_dctx* d);
+/* out[0] N, [1] blocks, [2] P-exchange bytes, [3] W-exchange bytes, [4] X-exchange bytes,
+ * [5] derivative blocks (2, or 3 with a nugget), [6] blocks owned by this rank */
+int mle_dctx_layout(const mle_dctx* d, int64_t* out);
+int mle_dctx_begin(mle_dctx* d, const double theta[3], int derivs);
+int mle_dctx_factor(mle_dctx* d, int b, void* exch_p);
+int mle_dctx_update(mle_dctx* d, int b, const void* exch_p);
+int mle_dctx_wblock(mle_dctx* d, int b, void* exch_w);
+int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w);
+int mle_dctx_right_operand(mle_dctx* d, int b, void* exch_x);
+int mle_dctx_right(mle_dctx* d, int b, const void* exch_w, const void* exch_x);
+/* out: MLE_DCTX_SUMS partial sums [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>, trM, <A,M>,
+ * <N,M>, <M,M>, yBy_A, yBy_N, yBy_M], then the failure flag and the 0-based pivot */
+#define MLE_DCTX_SUMS 14
+int mle_dctx_partials(mle_dctx* d, double* out);
+
 #ifdef __cplusplus
 }
 #endif

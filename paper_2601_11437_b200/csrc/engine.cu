@@ -518,82 +518,93 @@ struct Launcher {
   cudaStream_t inner() const { return s3 ? s3 : s; }
 
   // Two-level right-looking blocked Cholesky of every item's matrix (ld = N).
+  // Inner (128-wide) steps of outer block [b0, b1): diagonal tiles, panels and the updates
+  // inside the block; leaves L[:, b0:b1] final (all rows).  mats[] may be "virtual" base
+  // pointers of column panels (element (i, j) at mats[b][i + j ld] for j in the block).
+  int inner_block(mle_ctx* const* cs, double* const* mats, const long long* n_aug, int m,
+                  int b0, int b1) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    int rc;
+    for (int k = b0; k < b1; ++k) {
+      const long long k0 = (long long)k * kNB;
+      DiagArgs d;
+      std::memset(&d, 0, sizeof(d));
+      d.ld = ld;
+      d.k0 = (int)k0;
+      for (int b = 0; b < m; ++b) {
+        d.a[b] = mats[b];
+        d.linv[b] = cs[b]->linv + (size_t)k * kNB * kNB;
+        d.fail_flag[b] = cs[b]->fail_flag;
+        d.fail_idx[b] = cs[b]->fail_idx;
+        d.n_aug[b] = n_aug[b];
+      }
+      launches += 1;
+      CUDA_TRY(launch_potrf_diag(d, m, s));
+      const int rem = Nt - k - 1;
+      if (rem == 0) break;
+      const int wcols = b1 - k - 1;  // remaining tile columns of this outer block
+      auto panel_gemm = [&](int row_tiles, int row_off, cudaStream_t st) {
+        // panel rows [k+1+row_off, k+1+row_off+row_tiles) <- panel * Linv_k^T, in place
+        // (BN = 128 covers the whole panel width)
+        GemmArgs g = gemm_base();
+        for (int b = 0; b < m; ++b) {
+          double* panel = mats[b] + (k0 + kNB + (long long)row_off * kNB) + k0 * ld;
+          g.A[b] = panel;
+          g.B[b] = cs[b]->linv + (size_t)k * kNB * kNB;
+          g.C[b] = panel;
+          g.fail_flag[b] = cs[b]->fail_flag;
+        }
+        g.lda = ld; g.ldb = kNB; g.ldc = ld;
+        g.tiles_m = row_tiles; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
+        return gemm(g, kBNK, m, st);
+      };
+      // A[r0+.., c0+..] -= P[r0..] P[c0..]^T over tile rows/cols of this outer block
+      auto update = [&](int row_off, int row_tiles, int col_off, int col_tiles, bool trap,
+                        cudaStream_t st) {
+        GemmArgs t = gemm_base();
+        for (int b = 0; b < m; ++b) {
+          double* panel = mats[b] + (k0 + kNB) + k0 * ld;
+          t.A[b] = panel + (long long)row_off * kNB;
+          t.B[b] = panel + (long long)col_off * kNB;
+          t.C[b] = mats[b] + (k0 + kNB + (long long)row_off * kNB) +
+                   (k0 + kNB + (long long)col_off * kNB) * ld;
+          t.fail_flag[b] = cs[b]->fail_flag;
+        }
+        t.lda = ld; t.ldb = ld; t.ldc = ld;
+        t.tiles_m = row_tiles; t.tiles_n = col_tiles; t.trap = trap ? 1 : 0;
+        t.alpha = -1.0; t.beta = 1.0;
+        return gemm(t, kBNK, m, st);
+      };
+      if ((rc = join(s3, s))) return rc;  // the previous step's bulk work on the inner stream
+      if (wcols == 0) {
+        // last tile of the outer block: the whole panel (read by the trailing update)
+        if ((rc = panel_gemm(rem, 0, s))) return rc;
+        continue;
+      }
+      // Inner look-ahead: the critical chain to the next diagonal tile is only
+      //   panel rows of tile k+1  ->  update of tile (k+1, k+1)  ->  diag(k+1);
+      // the other panel rows and updates run on the inner stream meanwhile.
+      if ((rc = panel_gemm(1, 0, s))) return rc;
+      if ((rc = join(s, s3))) return rc;
+      if ((rc = update(0, 1, 0, 1, true, s))) return rc;
+      if (rem > 1) {
+        cudaStream_t in = inner();
+        if ((rc = panel_gemm(rem - 1, 1, in))) return rc;
+        if ((rc = update(1, rem - 1, 0, 1, false, in))) return rc;  // column k+1, rows >= k+2
+        if (wcols > 1 && (rc = update(1, rem - 1, 1, wcols - 1, true, in))) return rc;
+      }
+    }
+    return join(s3, s);
+  }
+
   int potrf(mle_ctx* const* cs, double* const* mats, const long long* n_aug, int m) {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
     int rc;
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
       const int b1 = std::min(Nt, b0 + kOuter);
-      for (int k = b0; k < b1; ++k) {
-        const long long k0 = (long long)k * kNB;
-        DiagArgs d;
-        std::memset(&d, 0, sizeof(d));
-        d.ld = ld;
-        d.k0 = (int)k0;
-        for (int b = 0; b < m; ++b) {
-          d.a[b] = mats[b];
-          d.linv[b] = cs[b]->linv + (size_t)k * kNB * kNB;
-          d.fail_flag[b] = cs[b]->fail_flag;
-          d.fail_idx[b] = cs[b]->fail_idx;
-          d.n_aug[b] = n_aug[b];
-        }
-        launches += 1;
-        CUDA_TRY(launch_potrf_diag(d, m, s));
-        const int rem = Nt - k - 1;
-        if (rem == 0) break;
-        const int wcols = b1 - k - 1;  // remaining tile columns of this outer block
-        auto panel_gemm = [&](int row_tiles, int row_off, cudaStream_t st) {
-          // panel rows [k+1+row_off, k+1+row_off+row_tiles) <- panel * Linv_k^T, in place
-          // (BN = 128 covers the whole panel width)
-          GemmArgs g = gemm_base();
-          for (int b = 0; b < m; ++b) {
-            double* panel = mats[b] + (k0 + kNB + (long long)row_off * kNB) + k0 * ld;
-            g.A[b] = panel;
-            g.B[b] = cs[b]->linv + (size_t)k * kNB * kNB;
-            g.C[b] = panel;
-            g.fail_flag[b] = cs[b]->fail_flag;
-          }
-          g.lda = ld; g.ldb = kNB; g.ldc = ld;
-          g.tiles_m = row_tiles; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
-          return gemm(g, kBNK, m, st);
-        };
-        // A[r0+.., c0+..] -= P[r0..] P[c0..]^T over tile rows/cols of this outer block
-        auto update = [&](int row_off, int row_tiles, int col_off, int col_tiles, bool trap,
-                          cudaStream_t st) {
-          GemmArgs t = gemm_base();
-          for (int b = 0; b < m; ++b) {
-            double* panel = mats[b] + (k0 + kNB) + k0 * ld;
-            t.A[b] = panel + (long long)row_off * kNB;
-            t.B[b] = panel + (long long)col_off * kNB;
-            t.C[b] = mats[b] + (k0 + kNB + (long long)row_off * kNB) +
-                     (k0 + kNB + (long long)col_off * kNB) * ld;
-            t.fail_flag[b] = cs[b]->fail_flag;
-          }
-          t.lda = ld; t.ldb = ld; t.ldc = ld;
-          t.tiles_m = row_tiles; t.tiles_n = col_tiles; t.trap = trap ? 1 : 0;
-          t.alpha = -1.0; t.beta = 1.0;
-          return gemm(t, kBNK, m, st);
-        };
-        if ((rc = join(s3, s))) return rc;  // the previous step's bulk work on the inner stream
-        if (wcols == 0) {
-          // last tile of the outer block: the whole panel (read by the trailing update)
-          if ((rc = panel_gemm(rem, 0, s))) return rc;
-          continue;
-        }
-        // Inner look-ahead: the critical chain to the next diagonal tile is only
-        //   panel rows of tile k+1  ->  update of tile (k+1, k+1)  ->  diag(k+1);
-        // the other panel rows and updates run on the inner stream meanwhile.
-        if ((rc = panel_gemm(1, 0, s))) return rc;
-        if ((rc = join(s, s3))) return rc;
-        if ((rc = update(0, 1, 0, 1, true, s))) return rc;
-        if (rem > 1) {
-          cudaStream_t in = inner();
-          if ((rc = panel_gemm(rem - 1, 1, in))) return rc;
-          if ((rc = update(1, rem - 1, 0, 1, false, in))) return rc;  // column k+1, rows >= k+2
-          if (wcols > 1 && (rc = update(1, rem - 1, 1, wcols - 1, true, in))) return rc;
-        }
-      }
-      if ((rc = join(s3, s))) return rc;
+      if ((rc = inner_block(cs, mats, n_aug, m, b0, b1))) return rc;
       if (b1 >= Nt) continue;
       // trailing update with P = L[T, b0:b1], K = (b1 - b0) * 128
       const int b2 = std::min(Nt, b1 + kOuter);
@@ -1446,8 +1457,16 @@ int mle_release_cached_memory(void) {
   return MLE_OK;
 }
 
+static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n, int device,
+                              double nugget, long long align, mle_ctx** out);
+
 int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device, double nugget,
                    mle_ctx** out) {
+  return create_ctx_aligned(locs_xy, z, n, device, nugget, kNB, out);
+}
+
+static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n, int device,
+                              double nugget, long long align, mle_ctx** out) {
   if (!out) return fail(MLE_INVALID, "out is null");
   *out = nullptr;
   if (!locs_xy || !z || n < 1) return fail(MLE_INVALID, "at least one location is required");
@@ -1462,7 +1481,7 @@ int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device
   mle_ctx* c = new mle_ctx();
   c->device = device;
   c->n = n;
-  c->N = round_up(n + 1, kNB);
+  c->N = round_up(n + 1, align);
   c->Nt = (int)(c->N / kNB);
   c->nugget = nugget;
   c->ozaki = use_ozaki();
@@ -1874,6 +1893,546 @@ int mle_matern_elem(const double theta[3], int which, const double* h, int64_t m
   for (int64_t i = 0; i < m; ++i)
     if (!(h[i] >= 0.0)) return fail(MLE_INVALID, "distances must be non-negative");
   return run_elem(2, P, which, h, m, device, out);
+}
+
+}  // extern "C"
+
+// ---- distributed engine: one rank's column panels -----------------------------------------
+// Outer blocks of 512 columns are owned cyclically (block b by rank b % world).  A rank holds,
+// for each owned block, the full-height column panel of Sigma -> L and of every derivative
+// block (N x 512, ld = N; N a multiple of 512).  The Python driver (distributed.py) sequences
+// the block steps and the collectives; each entry point below runs one rank's share of one
+// step on its stream and returns after the stream has drained (the exchange buffers are then
+// ready for NCCL on any stream).  Kernels are the single-GPU engine's, addressed through
+// "virtual" base pointers vb = panel - c0 N, so that element (i, j) is vb[i + j N].
+struct mle_dctx {
+  mle_ctx* c = nullptr;
+  int rank = 0, world = 1, nb = 0, nmat = 2;
+  bool derivs = false;
+  std::vector<int> owned;                      // blocks owned by this rank, ascending
+  std::vector<double*> sig, mat[3];            // per owned block: panels
+  std::vector<int8_t*> lsl;                    // per owned block: P_b slices (rows c1..N)
+  std::vector<int*> lex;
+  std::vector<int8_t*> wsl;                    // per owned block: W_b slices (rows c0..N)
+  std::vector<int*> wex;
+  std::vector<double*> dinv;                   // per owned block: D_b^-1 (512 x 512, ld 512)
+  double* tscr = nullptr;                      // 128 x 512
+  double* wbuf = nullptr;                      // N x 512
+  int8_t* dtsl = nullptr;                      // D_b^-T slices
+  int* dtex = nullptr;
+  int8_t* xsl = nullptr;                       // forward-sweep operand slices
+  int* xex = nullptr;
+  double* part = nullptr;                      // panel reduce partials
+  std::vector<double> h_part;
+};
+
+namespace {
+
+constexpr long long kDB = 512;  // distributed block width
+
+long long d_c0(int b) { return (long long)b * kDB; }
+size_t d_pbytes(long long N) { return (size_t)(N - kDB) * kOzRowBytes; }  // P slices (max)
+size_t d_wbytes(long long N) { return (size_t)N * kOzRowBytes; }          // W / X slices (max)
+size_t d_xstride(long long N) { return d_wbytes(N) + sizeof(int) * (size_t)N; }
+
+int d_index(const mle_dctx* d, int b) {
+  for (size_t i = 0; i < d->owned.size(); ++i)
+    if (d->owned[i] == b) return (int)i;
+  return -1;
+}
+
+double* d_mat(const mle_dctx* d, int m, int q) {  // derivative block m of owned panel q
+  return d->mat[m][q];
+}
+
+int d_sync(mle_dctx* d) {
+  CUDA_TRY(cudaStreamSynchronize(d->c->stream));
+  CUDA_TRY(cudaStreamSynchronize(d->c->inner));
+  CUDA_TRY(cudaGetLastError());
+  return MLE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mle_dctx_create(const double* locs_xy, const double* z, int64_t n, int device,
+                    double nugget, int rank, int world, mle_dctx** out) {
+  if (!out) return fail(MLE_INVALID, "out is null");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(MLE_INVALID, "bad rank / world");
+  mle_ctx* c = nullptr;
+  int rc = create_ctx_aligned(locs_xy, z, n, device, nugget, kDB, &c);
+  if (rc) return rc;
+  mle_dctx* d = new mle_dctx();
+  d->c = c;
+  d->rank = rank;
+  d->world = world;
+  d->nb = (int)(c->N / kDB);
+  d->nmat = nugget > 0.0 ? 3 : 2;
+  for (int b = rank; b < d->nb; b += world) d->owned.push_back(b);
+  *out = d;
+  return MLE_OK;
+}
+
+void mle_dctx_destroy(mle_dctx* d) {
+  if (!d) return;
+  if (d->c) {
+    cudaSetDevice(d->c->device);
+    cudaStreamSynchronize(d->c->stream);
+    cudaStreamSynchronize(d->c->inner);
+  }
+  for (auto* p : d->sig) dfree(p);
+  for (auto& v : d->mat)
+    for (auto* p : v) dfree(p);
+  for (auto* p : d->lsl) dfree(p);
+  for (auto* p : d->lex) dfree(p);
+  for (auto* p : d->wsl) dfree(p);
+  for (auto* p : d->wex) dfree(p);
+  for (auto* p : d->dinv) dfree(p);
+  dfree(d->tscr);
+  dfree(d->wbuf);
+  dfree(d->dtsl);
+  dfree(d->dtex);
+  dfree(d->xsl);
+  dfree(d->xex);
+  dfree(d->part);
+  mle_ctx_destroy(d->c);
+  delete d;
+}
+
+int mle_dctx_layout(const mle_dctx* d, int64_t* out) {
+  if (!d || !out) return fail(MLE_INVALID, "null argument");
+  const long long N = d->c->N;
+  out[0] = N;
+  out[1] = d->nb;
+  out[2] = (int64_t)(d_pbytes(N) + sizeof(int) * (size_t)(N - kDB));  // P exchange
+  out[3] = (int64_t)d_xstride(N);                                      // W exchange
+  out[4] = (int64_t)(d_xstride(N) * (size_t)d->nmat);                  // X exchange
+  out[5] = d->nmat;
+  out[6] = (int64_t)d->owned.size();
+  return MLE_OK;
+}
+
+// Set theta and generate the owned panels (Sigma; the derivative blocks when derivs).
+int mle_dctx_begin(mle_dctx* d, const double theta[3], int derivs) {
+  if (!d || !theta) return fail(MLE_INVALID, "null argument");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  ThetaParams P;
+  if (mle_fill_theta(theta, c->nugget, &P) != 0)
+    return fail(MLE_INVALID, "MaternParams components must be finite and > 0");
+  if (use_gen_table())
+    mle_fill_gen_table(c->h_max / P.alpha, &P);
+  else
+    P.tab_n = 0;
+  const long long N = c->N;
+  const size_t pbytes = sizeof(double) * (size_t)N * kDB;
+  const int no = (int)d->owned.size();
+  d->derivs = derivs != 0;
+  if (!c->linv) CUDA_TRY(dmalloc(&c->linv, sizeof(double) * (size_t)c->Nt * kNB * kNB));
+  if ((int)d->sig.size() < no) {
+    d->sig.assign(no, nullptr);
+    d->lsl.assign(no, nullptr);
+    d->lex.assign(no, nullptr);
+    for (int q = 0; q < no; ++q) {
+      CUDA_TRY(dmalloc(&d->sig[q], pbytes));
+      const long long rows = N - d_c0(d->owned[q]) - kDB;
+      if (rows > 0) {
+        CUDA_TRY(dmalloc(&d->lsl[q], (size_t)rows * kOzRowBytes));
+        CUDA_TRY(dmalloc(&d->lex[q], sizeof(int) * (size_t)rows));
+      }
+    }
+    CUDA_TRY(dmalloc(&d->part, sizeof(double) * (size_t)no * kDB * kPanelSums));
+    d->h_part.assign((size_t)no * kDB * kPanelSums, 0.0);
+  }
+  if (d->derivs && d->mat[0].size() < (size_t)no) {
+    for (int m = 0; m < d->nmat; ++m) {
+      d->mat[m].assign(no, nullptr);
+      for (int q = 0; q < no; ++q) CUDA_TRY(dmalloc(&d->mat[m][q], pbytes));
+    }
+    d->wsl.assign(no, nullptr);
+    d->wex.assign(no, nullptr);
+    d->dinv.assign(no, nullptr);
+    for (int q = 0; q < no; ++q) {
+      const long long rows = N - d_c0(d->owned[q]);
+      CUDA_TRY(dmalloc(&d->wsl[q], (size_t)rows * kOzRowBytes));
+      CUDA_TRY(dmalloc(&d->wex[q], sizeof(int) * (size_t)rows));
+      CUDA_TRY(dmalloc(&d->dinv[q], sizeof(double) * kDB * kDB));
+      CUDA_TRY(cudaMemsetAsync(d->dinv[q], 0, sizeof(double) * kDB * kDB, c->stream));
+    }
+    CUDA_TRY(dmalloc(&d->tscr, sizeof(double) * kNB * kDB));
+    CUDA_TRY(dmalloc(&d->wbuf, sizeof(double) * (size_t)N * kDB));
+    CUDA_TRY(dmalloc(&d->dtsl, (size_t)kDB * kOzRowBytes));
+    CUDA_TRY(dmalloc(&d->dtex, sizeof(int) * kDB));
+    CUDA_TRY(dmalloc(&d->xsl, (size_t)no * d->nmat * kDB * kOzRowBytes));
+    CUDA_TRY(dmalloc(&d->xex, sizeof(int) * (size_t)no * d->nmat * kDB));
+  }
+  std::memcpy(c->h_theta, &P, sizeof(P));
+  CUDA_TRY(cudaMemcpyAsync(c->d_theta, c->h_theta, sizeof(P), cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->fail_flag, 0, sizeof(int), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->fail_idx, 0, sizeof(long long), c->stream));
+  // generation tables, then the panels in chunks of kMaxItems
+  GenArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  ga.ld = N;
+  ga.rows = N;
+  ga.n = (int)c->n;
+  GenItem base;
+  std::memset(&base, 0, sizeof(base));
+  base.P = c->d_theta;
+  base.lx = c->lx;
+  base.ly = c->ly;
+  base.z = c->z;
+  base.fail_flag = c->fail_flag;
+  base.tab = P.tab_n > 0 ? (d->derivs ? c->gtab_d : c->gtab_s) : nullptr;
+  base.write_sigma = 1;
+  base.write_derivs = d->derivs ? 1 : 0;
+  ga.item[0] = base;
+  launch_gen_table(ga, 1, d->derivs, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  std::vector<int> c0s(no);
+  for (int q = 0; q < no; ++q) c0s[q] = (int)d_c0(d->owned[q]);
+  int* d_c0s = nullptr;
+  CUDA_TRY(dmalloc(&d_c0s, sizeof(int) * std::max(1, no)));
+  CUDA_TRY(cudaMemcpyAsync(d_c0s, c0s.data(), sizeof(int) * no, cudaMemcpyHostToDevice,
+                           c->stream));
+  for (int q0 = 0; q0 < no; q0 += kMaxItems) {
+    const int cnt = std::min(kMaxItems, no - q0);
+    for (int i = 0; i < cnt; ++i) {
+      GenItem gi = base;
+      gi.sigma = d->sig[q0 + i];
+      gi.dalpha = d->derivs ? d->mat[0][q0 + i] : nullptr;
+      gi.dnu = d->derivs ? d->mat[1][q0 + i] : nullptr;
+      ga.item[i] = gi;
+    }
+    launch_gen_panels(ga, d_c0s + q0, (int)kDB, cnt, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    if (d->derivs && d->nmat == 3) {
+      PanelArgs pa;
+      std::memset(&pa, 0, sizeof(pa));
+      for (int i = 0; i < cnt; ++i) {
+        pa.p[i] = d->mat[2][q0 + i];
+        pa.c0[i] = c0s[q0 + i];
+      }
+      pa.ld = N;
+      pa.width = (int)kDB;
+      pa.n = (int)c->n;
+      CUDA_TRY(launch_panel_identity(pa, cnt, c->stream));
+    }
+  }
+  int rc = d_sync(d);
+  dfree(d_c0s);
+  return rc;
+}
+
+// Owner of block b: inner steps on its panel; P_b = L[c1:, b] sliced into exch_p
+// ([rows][4 KB] int8 slices, then int exponents at offset d_pbytes(N)).
+int mle_dctx_factor(mle_dctx* d, int b, void* exch_p) {
+  const int q = d ? d_index(d, b) : -1;
+  if (q < 0) return fail(MLE_INVALID, "block not owned by this rank");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c0 = d_c0(b), c1 = c0 + kDB;
+  double* vb = d->sig[q] - c0 * N;
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  run.s3 = c->inner;
+  mle_ctx* cs[1] = {c};
+  double* mats[1] = {vb};
+  long long aug[1] = {c->n};
+  int rc = run.inner_block(cs, mats, aug, 1, (int)(c0 / kNB), (int)(c1 / kNB));
+  if (rc) return rc;
+  if (c1 < N) {
+    OzSliceArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    sa.X[0] = vb + c1 + c0 * N;
+    sa.slices[0] = d->lsl[q];
+    sa.e[0] = d->lex[q];
+    sa.fail_flag[0] = c->fail_flag;
+    sa.ld = N;
+    sa.K = (int)kDB;
+    if ((rc = run.slice(sa, N - c1, true, 1))) return rc;
+    if (exch_p) {
+      int8_t* ex = static_cast<int8_t*>(exch_p);
+      CUDA_TRY(cudaMemcpyAsync(ex, d->lsl[q], (size_t)(N - c1) * kOzRowBytes,
+                               cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(ex + d_pbytes(N), d->lex[q], sizeof(int) * (size_t)(N - c1),
+                               cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  return d_sync(d);
+}
+
+// Every rank: trailing update of its panels j > b with P_b (exch_p as produced by factor).
+int mle_dctx_update(mle_dctx* d, int b, const void* exch_p) {
+  if (!d || !exch_p) return fail(MLE_INVALID, "null argument");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c1 = d_c0(b) + kDB;
+  const int8_t* ps = static_cast<const int8_t*>(exch_p);
+  const int* pe = reinterpret_cast<const int*>(ps + d_pbytes(N));
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  std::vector<int> qs;
+  for (size_t q = 0; q < d->owned.size(); ++q)
+    if (d->owned[q] > b) qs.push_back((int)q);
+  for (size_t i0 = 0; i0 < qs.size(); i0 += kMaxGemm) {
+    const int cnt = (int)std::min<size_t>(kMaxGemm, qs.size() - i0);
+    OzGemmArgs g = Launcher::oz_base(N, (int)((N - c1) / kNB), (int)(kDB / kNB));
+    g.trap = 1;
+    for (int z = 0; z < cnt; ++z) {
+      const int q = qs[i0 + z];
+      const long long cj = d_c0(d->owned[q]);
+      const size_t toff = (size_t)((cj - c1) / kNB) * kOzTileBytes;
+      g.As[z] = g.Bs[z] = ps + toff;
+      g.ea[z] = g.eb[z] = pe + (cj - c1);
+      g.C[z] = d->sig[q] + cj;  // rows cj.., first column of panel j
+      g.tiles_m_z[z] = (int)((N - cj) / kNB);
+      g.fail_flag[z] = c->fail_flag;
+    }
+    int rc = run.ozgemm(g, cnt, c->stream);
+    if (rc) return rc;
+  }
+  return d_sync(d);
+}
+
+// Owner of block b: W_b = [D_b^-1; -P_b D_b^-1] sliced into exch_w (slices, exponents at
+// d_wbytes(N)) and kept for the right sweep.
+int mle_dctx_wblock(mle_dctx* d, int b, void* exch_w) {
+  const int q = d ? d_index(d, b) : -1;
+  if (q < 0 || !d->derivs) return fail(MLE_INVALID, "block not owned / no derivatives");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c0 = d_c0(b), c1 = c0 + kDB;
+  const int t0 = (int)(c0 / kNB);
+  double* vb = d->sig[q] - c0 * N;
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  int rc;
+  {
+    double* dv[1] = {d->dinv[q]};
+    const double* lv[1] = {c->linv};
+    run.launches += 1;
+    CUDA_TRY(launch_linv_to_dinv_block(dv, lv, t0, (int)(kDB / kNB), 1, c->stream));
+  }
+  for (int i = 1; i < (int)(kDB / kNB); ++i) {
+    GemmArgs t = gemm_base(), u = gemm_base();
+    t.A[0] = vb + (c0 + i * kNB) + c0 * N;
+    t.B[0] = d->dinv[q];
+    t.C[0] = d->tscr;
+    t.fail_flag[0] = c->fail_flag;
+    u.A[0] = c->linv + (size_t)(t0 + i) * kNB * kNB;
+    u.B[0] = d->tscr;
+    u.C[0] = d->dinv[q] + i * kNB;
+    u.fail_flag[0] = c->fail_flag;
+    t.lda = N; t.ldb = kDB; t.ldc = kNB; t.K = i * kNB;
+    t.tiles_m = 1; t.tiles_n = i; t.alpha = 1.0; t.beta = 0.0;
+    if ((rc = run.gemm(t, kBKN, 1))) return rc;
+    u.lda = kNB; u.ldb = kNB; u.ldc = kDB; u.K = kNB;
+    u.tiles_m = 1; u.tiles_n = i; u.alpha = -1.0; u.beta = 0.0;
+    if ((rc = run.gemm(u, kBKN, 1))) return rc;
+  }
+  OzSliceArgs top;
+  std::memset(&top, 0, sizeof(top));
+  top.X[0] = d->dinv[q];
+  top.slices[0] = d->wsl[q];
+  top.e[0] = d->wex[q];
+  top.fail_flag[0] = c->fail_flag;
+  top.ld = kDB;
+  top.K = (int)kDB;
+  if ((rc = run.slice(top, kDB, true, 1))) return rc;
+  if (c1 < N) {
+    OzSliceArgs dt;
+    std::memset(&dt, 0, sizeof(dt));
+    dt.X[0] = d->dinv[q];
+    dt.slices[0] = d->dtsl;
+    dt.e[0] = d->dtex;
+    dt.fail_flag[0] = c->fail_flag;
+    dt.ld = kDB;
+    dt.K = (int)kDB;
+    if ((rc = run.slice(dt, kDB, false, 1))) return rc;
+    OzGemmArgs g = Launcher::oz_base(N, (int)((N - c1) / kNB), (int)(kDB / kNB));
+    g.beta = 0.0;
+    g.As[0] = d->lsl[q];
+    g.ea[0] = d->lex[q];
+    g.Bs[0] = d->dtsl;
+    g.eb[0] = d->dtex;
+    g.C[0] = d->wbuf;
+    g.fail_flag[0] = c->fail_flag;
+    if ((rc = run.ozgemm(g, 1, c->stream))) return rc;
+    OzSliceArgs bot;
+    std::memset(&bot, 0, sizeof(bot));
+    bot.X[0] = d->wbuf;
+    bot.slices[0] = d->wsl[q] + (size_t)(kDB / kNB) * kOzTileBytes;
+    bot.e[0] = d->wex[q] + kDB;
+    bot.fail_flag[0] = c->fail_flag;
+    bot.ld = N;
+    bot.K = (int)kDB;
+    if ((rc = run.slice(bot, N - c1, true, 1))) return rc;
+  }
+  if (exch_w) {
+    int8_t* ex = static_cast<int8_t*>(exch_w);
+    CUDA_TRY(cudaMemcpyAsync(ex, d->wsl[q], (size_t)(N - c0) * kOzRowBytes,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(ex + d_wbytes(N), d->wex[q], sizeof(int) * (size_t)(N - c0),
+                             cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return d_sync(d);
+}
+
+// Every rank, forward sweep X = L^-1 S, block b: X[c0:, owned columns] = W_b X[c0:c1, owned].
+int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w) {
+  if (!d || !exch_w || !d->derivs) return fail(MLE_INVALID, "null argument / no derivatives");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c0 = d_c0(b);
+  const int8_t* ws = static_cast<const int8_t*>(exch_w);
+  const int* we = reinterpret_cast<const int*>(ws + d_wbytes(N));
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  const int no = (int)d->owned.size(), total = no * d->nmat;
+  int rc;
+  for (int i0 = 0; i0 < total; i0 += kMaxGemm) {
+    const int cnt = std::min(kMaxGemm, total - i0);
+    OzSliceArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    OzGemmArgs g = Launcher::oz_base(N, (int)((N - c0) / kNB), (int)(kDB / kNB));
+    g.alpha = 1.0;
+    g.beta0_tm = (int)(kDB / kNB);
+    for (int z = 0; z < cnt; ++z) {
+      const int idx = i0 + z, q = idx / d->nmat, m = idx % d->nmat;
+      double* panel = d_mat(d, m, q);
+      sa.X[z] = panel + c0;  // B(n, k) = X[c0 + k, n]: k-contig rows = the panel's columns
+      sa.slices[z] = d->xsl + (size_t)idx * kDB * kOzRowBytes;
+      sa.e[z] = d->xex + (size_t)idx * kDB;
+      sa.fail_flag[z] = c->fail_flag;
+      g.As[z] = ws;
+      g.ea[z] = we;
+      g.Bs[z] = sa.slices[z];
+      g.eb[z] = sa.e[z];
+      g.C[z] = panel + c0;
+      g.fail_flag[z] = c->fail_flag;
+    }
+    sa.ld = N;
+    sa.K = (int)kDB;
+    if ((rc = run.slice(sa, kDB, false, cnt))) return rc;
+    if ((rc = run.ozgemm(g, cnt, c->stream))) return rc;
+  }
+  return d_sync(d);
+}
+
+// Owner of block b: the right-sweep operand X[c0:, b] (entries above the diagonal zeroed) of
+// every derivative block into exch_x (block m at m * d_xstride(N); exponents after the slices).
+int mle_dctx_right_operand(mle_dctx* d, int b, void* exch_x) {
+  const int q = d ? d_index(d, b) : -1;
+  if (q < 0 || !exch_x || !d->derivs) return fail(MLE_INVALID, "block not owned / no derivs");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c0 = d_c0(b);
+  int8_t* ex = static_cast<int8_t*>(exch_x);
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  OzSliceArgs sa;
+  std::memset(&sa, 0, sizeof(sa));
+  for (int m = 0; m < d->nmat; ++m) {
+    sa.X[m] = d_mat(d, m, q) + c0;
+    sa.slices[m] = ex + (size_t)m * d_xstride(N);
+    sa.e[m] = reinterpret_cast<int*>(ex + (size_t)m * d_xstride(N) + d_wbytes(N));
+    sa.fail_flag[m] = c->fail_flag;
+  }
+  sa.ld = N;
+  sa.K = (int)kDB;
+  sa.upper_zero = 1;
+  int rc = run.slice(sa, N - c0, true, d->nmat);
+  if (rc) return rc;
+  return d_sync(d);
+}
+
+// Every rank, right sweep block b: X[i, j] += X[i, c0:c1] W_b[j - c0, :] for its panels j >= b
+// (rows i >= j's block start; block b's own columns are overwritten: they become B[:, b]).
+int mle_dctx_right(mle_dctx* d, int b, const void* exch_w, const void* exch_x) {
+  if (!d || !exch_w || !exch_x || !d->derivs) return fail(MLE_INVALID, "null argument");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c0 = d_c0(b);
+  const int8_t* ws = static_cast<const int8_t*>(exch_w);
+  const int* we = reinterpret_cast<const int*>(ws + d_wbytes(N));
+  const int8_t* xs = static_cast<const int8_t*>(exch_x);
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  for (int own = 1; own >= 0; --own) {  // own == 1: the owner's block b (overwrite)
+    std::vector<std::pair<int, int>> zs;  // (q, m)
+    for (size_t q = 0; q < d->owned.size(); ++q) {
+      const int bj = d->owned[q];
+      if (bj < b || (bj == b) != (own == 1)) continue;
+      for (int m = 0; m < d->nmat; ++m) zs.push_back({(int)q, m});
+    }
+    for (size_t i0 = 0; i0 < zs.size(); i0 += kMaxGemm) {
+      const int cnt = (int)std::min<size_t>(kMaxGemm, zs.size() - i0);
+      OzGemmArgs g = Launcher::oz_base(N, (int)((N - c0) / kNB), (int)(kDB / kNB));
+      g.trap = 1;
+      g.alpha = 1.0;
+      g.beta0_tn = own ? (int)(kDB / kNB) : 0;
+      for (int z = 0; z < cnt; ++z) {
+        const int q = zs[i0 + z].first, m = zs[i0 + z].second;
+        const long long cj = d_c0(d->owned[q]);
+        const size_t toff = (size_t)((cj - c0) / kNB) * kOzTileBytes;
+        const int8_t* xm = xs + (size_t)m * d_xstride(N);
+        g.As[z] = xm + toff;
+        g.ea[z] = reinterpret_cast<const int*>(xm + d_wbytes(N)) + (cj - c0);
+        g.Bs[z] = ws + toff;
+        g.eb[z] = we + (cj - c0);
+        g.C[z] = d_mat(d, m, q) + cj;
+        g.tiles_m_z[z] = (int)((N - cj) / kNB);
+        g.fail_flag[z] = c->fail_flag;
+      }
+      int rc = run.ozgemm(g, cnt, c->stream);
+      if (rc) return rc;
+    }
+  }
+  return d_sync(d);
+}
+
+// This rank's partial sums over its panels: out[0..kPanelSums) (the kReduceOut layout of the
+// single-GPU reduction), out[kPanelSums] = failure flag, out[kPanelSums + 1] = pivot.
+int mle_dctx_partials(mle_dctx* d, double* out) {
+  if (!d || !out) return fail(MLE_INVALID, "null argument");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int no = (int)d->owned.size();
+  for (int q0 = 0; q0 < no; q0 += kMaxItems) {
+    const int cnt = std::min(kMaxItems, no - q0);
+    PanelReduceArgs ra;
+    std::memset(&ra, 0, sizeof(ra));
+    for (int i = 0; i < cnt; ++i) {
+      const int q = q0 + i;
+      ra.L[i] = d->sig[q];
+      ra.Ba[i] = d->derivs ? d->mat[0][q] : nullptr;
+      ra.Bn[i] = d->derivs ? d->mat[1][q] : nullptr;
+      ra.Bm[i] = (d->derivs && d->nmat == 3) ? d->mat[2][q] : nullptr;
+      ra.partials[i] = d->part + (size_t)q * kDB * kPanelSums;
+      ra.c0[i] = d_c0(d->owned[q]);
+    }
+    ra.ld = c->N;
+    ra.n = (int)c->n;
+    CUDA_TRY(launch_panel_reduce(ra, (int)kDB, cnt, c->stream));
+  }
+  CUDA_TRY(cudaMemcpyAsync(d->h_part.data(), d->part, sizeof(double) * d->h_part.size(),
+                           cudaMemcpyDeviceToHost, c->stream));
+  int flag = 0;
+  long long idx = 0;
+  CUDA_TRY(cudaMemcpyAsync(c->h_res, c->fail_flag, sizeof(int), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_res + 1, c->fail_idx, sizeof(long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  int rc = d_sync(d);
+  if (rc) return rc;
+  std::memcpy(&flag, c->h_res, sizeof(int));
+  std::memcpy(&idx, c->h_res + 1, sizeof(long long));
+  for (int k = 0; k < kPanelSums; ++k) out[k] = 0.0;
+  for (int q = 0; q < no; ++q)
+    for (long long jl = 0; jl < kDB; ++jl)
+      for (int k = 0; k < kPanelSums; ++k)
+        out[k] += d->h_part[((size_t)q * kDB + jl) * kPanelSums + k];
+  out[kPanelSums] = (double)flag;
+  out[kPanelSums + 1] = (double)idx;
+  return MLE_OK;
 }
 
 }  // extern "C"

@@ -52,6 +52,50 @@ __device__ __forceinline__ void stage_params(ThetaParams* dst, const ThetaParams
 
 }  // namespace
 
+// Element (i, j) of the engine's padded matrices (Sigma with the augmented row / column n
+// and identity padding; the derivative blocks zero outside [0, n)^2).
+__device__ __forceinline__ void engine_element(const GenItem& it, const ThetaParams& P, int i,
+                                               int j, int n, bool derivs, double& c, double& da,
+                                               double& dn) {
+  da = 0.0;
+  dn = 0.0;
+  if (i >= n || j >= n) {
+    // augmented row / padding
+    if (i == j) {
+      c = (i == n) ? 0.0 : 1.0;
+    } else if (i == n && j < n) {
+      c = it.z[j];
+    } else if (j == n && i < n) {
+      c = it.z[i];
+    } else {
+      c = 0.0;
+    }
+  } else if (i == j) {
+    c = P.sigma2 + P.nugget;  // matern.py:182 fill_diagonal(sigma2)
+  } else {
+    const double h = pair_distance(it.lx, it.ly, i, j);
+    if (h > 0.0) {
+      MaternVals v;
+      const double u = h / P.alpha;
+      if (it.tab != nullptr && u >= P.tab_lo && u < P.tab_hi) {
+        if (derivs)
+          v = matern_table<true>(P, it.tab, u);
+        else
+          v = matern_table<false>(P, it.tab, u);
+      } else if (derivs) {
+        v = matern_u<true>(P, u);
+      } else {
+        v = matern_u<false>(P, u);
+      }
+      c = v.c;
+      da = v.dalpha;
+      dn = v.dnu;
+    } else {
+      c = P.sigma2;  // coincident locations: zero-lag limit (matern.py:173-178)
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
   const GenItem& it = a.item[blockIdx.y];
   if (it.fail_flag != nullptr && *it.fail_flag) return;
@@ -71,42 +115,8 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
   for (int r = 0; r < kGT / 8; ++r) {
     const int jl = col0 + 8 * r;
     const int j = tj * kGT + jl;
-    double c, da = 0.0, dn = 0.0;
-    if (i >= n || j >= n) {
-      // augmented row / padding
-      if (i == j) {
-        c = (i == n) ? 0.0 : 1.0;
-      } else if (i == n && j < n) {
-        c = it.z[j];
-      } else if (j == n && i < n) {
-        c = it.z[i];
-      } else {
-        c = 0.0;
-      }
-    } else if (i == j) {
-      c = P.sigma2 + P.nugget;  // matern.py:182 fill_diagonal(sigma2)
-    } else {
-      const double h = pair_distance(it.lx, it.ly, i, j);
-      if (h > 0.0) {
-        MaternVals v;
-        const double u = h / P.alpha;
-        if (it.tab != nullptr && u >= P.tab_lo && u < P.tab_hi) {
-          if (derivs)
-            v = matern_table<true>(P, it.tab, u);
-          else
-            v = matern_table<false>(P, it.tab, u);
-        } else if (derivs) {
-          v = matern_u<true>(P, u);
-        } else {
-          v = matern_u<false>(P, u);
-        }
-        c = v.c;
-        da = v.dalpha;
-        dn = v.dnu;
-      } else {
-        c = P.sigma2;  // coincident locations: zero-lag limit (matern.py:173-178)
-      }
-    }
+    double c, da, dn;
+    engine_element(it, P, i, j, n, derivs, c, da, dn);
     const long long off = (long long)i + (long long)j * ld;
     if (it.write_sigma) it.sigma[off] = c;
     if (derivs) {
@@ -127,6 +137,38 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
       const long long off = (long long)i2 + (long long)j2 * ld;
       it.dalpha[off] = s_da[jl][lane_row];
       it.dnu[off] = s_dn[jl][lane_row];
+    }
+  }
+}
+
+// Column panels (distributed engine): every element (i, j) of the panel's columns
+// [c0, c0 + width), all rows [0, rows), written to panel[i + (j - c0) ld] (no symmetry
+// shortcut: derivative panels hold full columns).  GenItem.sigma / dalpha / dnu are the
+// panel bases; item b of the launch has its own c0 in a.item[b] via the `z` slot reuse below.
+__global__ void __launch_bounds__(kGThreads) gen_panel_kernel(GenArgs a, const int* c0s,
+                                                              int width) {
+  const GenItem& it = a.item[blockIdx.z];
+  if (it.fail_flag != nullptr && *it.fail_flag) return;
+  __shared__ ThetaParams P;
+  stage_params(&P, it.P);
+  const int c0 = c0s[blockIdx.z];
+  const int i = blockIdx.x * kGT + (threadIdx.x & (kGT - 1));
+  const int jl0 = blockIdx.y * kGT;
+  const bool derivs = it.write_derivs != 0;
+  const long long ld = a.ld;
+  if (i >= a.rows) return;
+#pragma unroll 1
+  for (int r = 0; r < kGT / 8; ++r) {
+    const int jl = jl0 + (threadIdx.x >> 5) + 8 * r;
+    if (jl >= width) continue;
+    const int j = c0 + jl;
+    double c, da, dn;
+    engine_element(it, P, i, j, a.n, derivs, c, da, dn);
+    const long long off = (long long)i + (long long)jl * ld;
+    if (it.write_sigma) it.sigma[off] = c;
+    if (derivs) {
+      it.dalpha[off] = da;
+      it.dnu[off] = dn;
     }
   }
 }
@@ -270,6 +312,13 @@ static long long lower_tiles(long long rows) {
 void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s) {
   const dim3 grid((unsigned)lower_tiles(a.rows), (unsigned)items);
   gen_engine_kernel<<<grid, kGThreads, 0, s>>>(a);
+}
+
+void launch_gen_panels(const GenArgs& a, const int* c0s_dev, int width, int items,
+                       cudaStream_t s) {
+  const dim3 grid((unsigned)((a.rows + kGT - 1) / kGT), (unsigned)((width + kGT - 1) / kGT),
+                  (unsigned)items);
+  gen_panel_kernel<<<grid, kGThreads, 0, s>>>(a, c0s_dev, width);
 }
 
 void launch_gen_table(const GenArgs& a, int items, bool derivs, cudaStream_t s) {

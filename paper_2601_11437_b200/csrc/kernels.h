@@ -83,6 +83,10 @@ cudaError_t init_kernel_attributes();  // GEMM smem opt-in (per device)
 cudaError_t init_diag_attributes();    // diagonal-tile kernel smem opt-in (per device)
 cudaError_t upload_u_tables(const double* u, const double* du);
 void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s);
+// Column panels of the distributed engine: columns [c0s[b], c0s[b] + width) of item b, all
+// rows; c0s_dev is a device array (one int per item).
+void launch_gen_panels(const GenArgs& a, const int* c0s_dev, int width, int items,
+                       cudaStream_t s);
 // Coefficients of the items' generation tables (items with tab == null are skipped).
 void launch_gen_table(const GenArgs& a, int items, bool derivs, cudaStream_t s);
 void launch_gen_build(const GenArgs& a, int which, cudaStream_t s);
@@ -168,6 +172,30 @@ cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int
                             cudaStream_t s);
 // n_tile: 0 persistent 128x64 (default), 1 persistent 128x32, 32 / 64 one tile per CTA
 cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile = 0);
+
+// ---- distributed engine: column panels (element (i, j) of panel z at p[z][i + (j - c0) ld])
+struct PanelArgs {
+  double* p[kMaxItems];
+  long long c0[kMaxItems];
+  long long ld;
+  int width;
+  int n;
+};
+constexpr int kPanelSums = 14;  // reduce sums (kReduceSums) + B_alpha / B_nu / M at [n, n]
+struct PanelReduceArgs {
+  const double* L[kMaxItems];
+  const double* Ba[kMaxItems];
+  const double* Bn[kMaxItems];
+  const double* Bm[kMaxItems];
+  double* partials[kMaxItems];  // [width][kPanelSums]
+  long long c0[kMaxItems];
+  long long ld;
+  int n;
+};
+cudaError_t launch_linv_to_dinv_block(double* const* dinv, const double* const* linv,
+                                      int k_begin, int tiles, int items, cudaStream_t s);
+cudaError_t launch_panel_identity(const PanelArgs& a, int items, cudaStream_t s);
+cudaError_t launch_panel_reduce(const PanelReduceArgs& r, int width, int items, cudaStream_t s);
 
 constexpr int kReduceBlocks = 148 * 4;
 constexpr int kReduceSums = 11;

@@ -748,4 +748,112 @@ cudaError_t launch_gather_results(const PassIo& io, double* dst, int items, cuda
   return cudaGetLastError();
 }
 
+// ---- distributed engine (column panels) -----------------------------------------------
+__global__ void __launch_bounds__(256) linv_to_dinv_range_kernel(LinvDinvArgs a, int k_begin) {
+  const int k = k_begin + blockIdx.x, z = blockIdx.y;
+  const double* src = a.linv[z] + (size_t)k * kNB * kNB;
+  double* dst = a.dinv[z] + (size_t)(k % 4) * kNB * (1 + 512);
+  for (int e = threadIdx.x; e < kNB * kNB; e += 256) {
+    const int r = e & (kNB - 1), c = e / kNB;
+    dst[r + (size_t)c * 512] = src[e];
+  }
+}
+
+cudaError_t launch_linv_to_dinv_block(double* const* dinv, const double* const* linv,
+                                      int k_begin, int tiles, int items, cudaStream_t s) {
+  LinvDinvArgs a;
+  for (int z = 0; z < items; ++z) {
+    a.dinv[z] = dinv[z];
+    a.linv[z] = linv[z];
+  }
+  linv_to_dinv_range_kernel<<<dim3((unsigned)tiles, (unsigned)items), 256, 0, s>>>(a, k_begin);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) panel_identity_kernel(PanelArgs a) {
+  double* S = a.p[blockIdx.y];
+  const long long c0 = a.c0[blockIdx.y];
+  const long long total = a.ld * a.width;
+  for (long long e = (long long)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (long long)gridDim.x * 256) {
+    const long long i = e % a.ld, jl = e / a.ld;
+    S[e] = (i == c0 + jl && i < a.n) ? 1.0 : 0.0;
+  }
+}
+
+cudaError_t launch_panel_identity(const PanelArgs& a, int items, cudaStream_t s) {
+  panel_identity_kernel<<<dim3(148 * 2, (unsigned)items), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// One CTA per (panel column, panel): the same sums as reduce_kernel restricted to column j,
+// written to partials[z][jl][0..RN) plus the three B[n, n] slots; the host adds them in a
+// fixed order.
+__global__ void __launch_bounds__(RTHREADS) panel_reduce_kernel(PanelReduceArgs ra) {
+  const int z = blockIdx.y, jl = blockIdx.x;
+  const long long j = ra.c0[z] + jl, ld = ra.ld;
+  const int n = ra.n;
+  const double* L = ra.L[z];
+  const double* Ba = ra.Ba[z];
+  const double* Bn = ra.Bn[z];
+  const double* Bm = ra.Bm[z];
+  double* out = ra.partials[z] + (size_t)jl * kPanelSums;
+  __shared__ double sh[RTHREADS / 32];
+  double s[RN];
+#pragma unroll
+  for (int q = 0; q < RN; ++q) s[q] = 0.0;
+  const long long cj = (long long)jl * ld;
+  if (j < n) {
+    if (threadIdx.x == 0) {
+      s[0] = log(L[j + cj]);
+      const double y = L[n + cj];
+      s[1] = y * y;
+      if (Ba != nullptr) {
+        const double a = Ba[j + cj], b = Bn[j + cj];
+        s[2] = a;
+        s[3] = b;
+        s[4] = a * a;
+        s[5] = a * b;
+        s[6] = b * b;
+        if (Bm != nullptr) {
+          const double c = Bm[j + cj];
+          s[7] = c;
+          s[8] = a * c;
+          s[9] = b * c;
+          s[10] = c * c;
+        }
+      }
+    }
+    if (Ba != nullptr) {
+      for (long long i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
+        const double a = Ba[i + cj], b = Bn[i + cj];
+        s[4] += 2.0 * a * a;
+        s[5] += 2.0 * a * b;
+        s[6] += 2.0 * b * b;
+        if (Bm != nullptr) {
+          const double c = Bm[i + cj];
+          s[8] += 2.0 * a * c;
+          s[9] += 2.0 * b * c;
+          s[10] += 2.0 * c * c;
+        }
+      }
+    }
+  }
+  for (int q = 0; q < RN; ++q) {
+    const double t = block_sum(s[q], sh);
+    if (threadIdx.x == 0) out[q] = t;
+  }
+  if (threadIdx.x == 0) {
+    const bool has_n = (j == n);
+    out[RN] = (has_n && Ba) ? Ba[n + cj] : 0.0;
+    out[RN + 1] = (has_n && Bn) ? Bn[n + cj] : 0.0;
+    out[RN + 2] = (has_n && Bm) ? Bm[n + cj] : 0.0;
+  }
+}
+
+cudaError_t launch_panel_reduce(const PanelReduceArgs& r, int width, int items, cudaStream_t s) {
+  panel_reduce_kernel<<<dim3((unsigned)width, (unsigned)items), RTHREADS, 0, s>>>(r);
+  return cudaGetLastError();
+}
+
 }  // namespace mle
