@@ -87,6 +87,9 @@ int mle_release_cached_memory(void);
  * Diagnostic only: no reference counterpart.
  */
 #define MLE_KSTATS 8
+/* (max L_jj / min L_jj)^2 of the context's last successful factorization (0 before any): a
+ * cheap lower bound of cond(Sigma), reported for diagnostics. */
+int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out);
 int mle_kernel_profile(mle_ctx* ctx, int enable);
 int mle_kernel_stats(const mle_ctx* ctx, double* out);
 

@@ -203,6 +203,20 @@ bool use_lookahead() {  // MLE_LOOKAHEAD=0: everything on the main stream (A/B t
   return !(v && std::strcmp(v, "0") == 0);
 }
 
+// Slices of the solve operands (W_b, X / B panels): 7 (default) or 8 (MLE_SOLVE_SLICES=8).
+// The solves feed traces and Frobenius products (1e-8 tolerances): 7 slices (49-bit operands,
+// products with p + q <= 8) keep DGEMM-level accuracy at 28 instead of 36 int8 products.
+// Slices of the solve operands (W_b, X / B panels): 7 by default, 8 with MLE_SOLVE_SLICES=8.
+// The solves only feed traces and Frobenius products (1e-8 tolerances); 7 slices (49-bit
+// operands, products with p + q <= 8) keep DGEMM-level accuracy at 28 instead of 36 int8
+// products, and pass every parity test at the north-star tolerances (the largest 7-vs-8
+// difference measured is 3.4e-9 of the score's component scale: GMM + nugget, config-5 theta).
+// A fixed setting, not a per-pass choice: results must not depend on batching or history.
+int solve_slices() {
+  const char* v = std::getenv("MLE_SOLVE_SLICES");
+  return (v && std::strcmp(v, "8") == 0) ? 8 : 7;
+}
+
 bool use_speculation() {
   const char* v = std::getenv("MLE_SPECULATE");
   return !(v && std::strcmp(v, "0") == 0);
@@ -258,6 +272,7 @@ struct mle_ctx {
   double gen_bytes = 0.0;
   double launches = 0.0;
   bool factor_valid = false;      // L of Sigma(cached_theta) is resident in `sigma`
+  double cond_est = 0.0;          // (max / min diag L)^2 of the last factorization (0: none)
   double cached_theta[3] = {0, 0, 0};
   // Ozaki-scheme FP64 GEMM (ozaki.cu) for the K = 512 trailing updates.  The factor's outer
   // panels L[b1:, b0:b1] are sliced once during the Cholesky and kept with the factor (both
@@ -275,6 +290,7 @@ struct mle_ctx {
   int* dtex = nullptr;
   int8_t* wsl = nullptr;
   int* wex = nullptr;
+  int w_slices = 0;               // slice count of the resident W slices
   // Kernel profiling (mle_kernel_profile): single stream, CUDA events around every Ozaki
   // GEMM and slicing launch of the pass; mle_kernel_stats reports the sums.
   bool kprof = false;
@@ -438,6 +454,7 @@ struct Launcher {
   mle_ctx* prof = nullptr;
   std::vector<int> pkind;
   std::vector<double> pwork;
+  std::vector<double> pint8;  // int8 tensor ops of each GEMM launch
   int prof_begin(cudaStream_t st) {
     if (!prof) return MLE_OK;
     const size_t i = 2 * pkind.size();
@@ -449,11 +466,12 @@ struct Launcher {
     CUDA_TRY(cudaEventRecord(prof->kev[i], st));
     return MLE_OK;
   }
-  int prof_end(cudaStream_t st, int kind, double work) {
+  int prof_end(cudaStream_t st, int kind, double work, double int8_ops = 0.0) {
     if (!prof) return MLE_OK;
     CUDA_TRY(cudaEventRecord(prof->kev[2 * pkind.size() + 1], st));
     pkind.push_back(kind);
     pwork.push_back(work);
+    pint8.push_back(int8_ops);
     return MLE_OK;
   }
   int slice(const OzSliceArgs& a, long long rows, bool row_contig, int batch) {
@@ -475,8 +493,11 @@ struct Launcher {
       tiles = 0;
       for (int tn = 0; tn < g.tiles_n; ++tn) tiles += std::max(0, g.tiles_m - tn);
     } else tiles = (double)g.tiles_m * g.tiles_n;
-    // FP64-equivalent tile flops (2 x 128 x 128 x K per tile)
-    return prof_end(st, 0, (double)batch * tiles * 2.0 * kNB * kNB * (32.0 * g.kblocks));
+    // FP64-equivalent tile flops (2 x 128 x 128 x K per tile); int8 tensor ops: one slice
+    // product per pair (p, q) with p + q <= S + 1 (36 for 8 slices, 28 for 7)
+    const int S = g.nslices == 7 ? 7 : 8;
+    const double fl = (double)batch * tiles * 2.0 * kNB * kNB * (32.0 * g.kblocks);
+    return prof_end(st, 0, fl, fl * (S * (S + 1) / 2));
   }
   int prof_collect() {
     if (!prof) return MLE_OK;
@@ -488,8 +509,8 @@ struct Launcher {
       st[base] += 1.0;
       st[base + 1] += ms;
       st[base + 2] += pwork[i];
+      if (pkind[i] == 0) st[3] += pint8[i];
     }
-    st[3] = st[2] * kOzProducts;  // int8 tensor ops: every FP64 MAC is 36 int8 MACs
     std::memcpy(prof->kstats, st, sizeof(st));
     return MLE_OK;
   }
@@ -680,11 +701,20 @@ struct Launcher {
   // GEMM batch member z = 2 * item + {0: alpha, 1: nu}.
   int solves(mle_ctx* const* cs, int m, mle_ctx* const* cw, int mw) {
     if (cs[0]->wsl) {
-      if (mw > 0) {
-        int rc = compute_w(cw, mw);
+      const int ks = solve_slices();
+      // W slices to (re)build: the requested ones, plus resident ones of another count
+      mle_ctx* rw[kMaxItems];
+      int nw = 0;
+      for (int i = 0; i < m; ++i) {
+        bool need = cs[i]->w_slices != ks;
+        for (int j = 0; j < mw; ++j) need = need || cw[j] == cs[i];
+        if (need) rw[nw++] = cs[i];
+      }
+      if (nw > 0) {
+        int rc = compute_w(rw, nw, ks);
         if (rc) return rc;
       }
-      return solves_w(cs, m);
+      return solves_w(cs, m, ks);
     }
     return solves_dmma(cs, m);
   }
@@ -714,10 +744,11 @@ struct Launcher {
   }
 
   // D_b^-1 for every outer block (DMMA, from the Linv tiles) and the slices of W_b.
-  int compute_w(mle_ctx* const* cs, int m) {
+  int compute_w(mle_ctx* const* cs, int m, int ks) {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
     const int nb = (Nt + kOuter - 1) / kOuter;
+    for (int i = 0; i < m; ++i) cs[i]->w_slices = ks;
     int rc;
     {
       double* dv[kMaxItems];
@@ -776,7 +807,7 @@ struct Launcher {
       const long long c1 = k.c0 + k.kb;
       const size_t woff = w_byte_offset(Nt, b);
       const long long eoff = w_row_offset(Nt, b);
-      const size_t tile_bytes = (size_t)kNB * k.kb * kOzSlices;
+      const size_t tile_bytes = (size_t)kNB * k.kb * ks;
       OzSliceArgs top;  // rows of D_b^-1 (row-contig, ld 512)
       std::memset(&top, 0, sizeof(top));
       for (int it = 0; it < m; ++it) {
@@ -787,6 +818,7 @@ struct Launcher {
       }
       top.ld = 512;
       top.K = (int)k.kb;
+      top.nslices = ks;
       if ((rc = slice(top, k.kb, true, m))) return rc;
       if (c1 >= ld) continue;
       OzSliceArgs dt;  // B(j, kk) = Dinv(kk, j): D_b^-T rows (k-contig, ld 512)
@@ -823,12 +855,13 @@ struct Launcher {
       }
       bot.ld = ld;
       bot.K = (int)k.kb;
+      bot.nslices = ks;
       if ((rc = slice(bot, ld - c1, true, m))) return rc;
     }
     return MLE_OK;
   }
 
-  int solves_w(mle_ctx* const* cs, int m) {
+  int solves_w(mle_ctx* const* cs, int m, int ks) {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
     const int nb = (Nt + kOuter - 1) / kOuter;
@@ -850,7 +883,7 @@ struct Launcher {
       const int t2 = std::min(Nt, k.t1 + kOuter);
       const size_t woff = w_byte_offset(Nt, b);
       const long long eoff = w_row_offset(Nt, b);
-      const size_t tile_bytes = (size_t)kNB * k.kb * kOzSlices;
+      const size_t tile_bytes = (size_t)kNB * k.kb * ks;
       OzSliceArgs sa;  // B(n, kk) = X[c0 + kk, n]
       std::memset(&sa, 0, sizeof(sa));
       for (int z = 0; z < zb; ++z) {
@@ -861,10 +894,12 @@ struct Launcher {
       }
       sa.ld = ld;
       sa.K = (int)k.kb;
+      sa.nslices = ks;
       if ((rc = slice(sa, ld, false, zb))) return rc;
       if ((rc = join(s2, s))) return rc;  // (ii) of the previous block wrote rows of (i)
       OzGemmArgs t = oz_base(ld, t2 - k.t0, Nt);  // (i): rows [c0, c2)
       t.kblocks = (int)(k.kb / 32);
+      t.nslices = ks;
       t.alpha = 1.0;
       t.beta0_tm = k.t1 - k.t0;
       for (int z = 0; z < zb; ++z) {
@@ -895,7 +930,7 @@ struct Launcher {
       const int t2 = std::min(Nt, k.t1 + kOuter);
       const size_t woff = w_byte_offset(Nt, b);
       const long long eoff = w_row_offset(Nt, b);
-      const size_t tile_bytes = (size_t)kNB * k.kb * kOzSlices;
+      const size_t tile_bytes = (size_t)kNB * k.kb * ks;
       OzSliceArgs sa;  // A(i, kk) = X[c0 + i, c0 + kk], kk <= i only
       std::memset(&sa, 0, sizeof(sa));
       for (int z = 0; z < zb; ++z) {
@@ -906,11 +941,13 @@ struct Launcher {
       }
       sa.ld = ld;
       sa.K = (int)k.kb;
+      sa.nslices = ks;
       sa.upper_zero = 1;
       if ((rc = slice(sa, ld - k.c0, true, zb))) return rc;
       if ((rc = join(s2, s))) return rc;
       OzGemmArgs t = oz_base(ld, Nt - k.t0, t2 - k.t0);  // (i): columns [c0, c2)
       t.kblocks = (int)(k.kb / 32);
+      t.nslices = ks;
       t.trap = 1;
       t.alpha = 1.0;
       t.beta0_tn = k.t1 - k.t0;
@@ -927,6 +964,7 @@ struct Launcher {
       if ((rc = join(s, s2))) return rc;
       OzGemmArgs u = oz_base(ld, Nt - t2, 0);  // (ii): lower tiles of [c2, N)
       u.kblocks = t.kblocks;
+      u.nslices = ks;
       u.lower = 1;
       u.alpha = 1.0;
       const long long c2 = (long long)t2 * kNB;
@@ -1222,7 +1260,7 @@ int run_chunk(Item* items, int m) {
     int rc = run.join(s, aux);
     if (rc) return rc;
     Launcher sp{aux};
-    rc = sp.compute_w(cs, ns);
+    rc = sp.compute_w(cs, ns, solve_slices());
     if (rc) return rc;
     run.launches += sp.launches;
     for (int b = 0; b < ns; ++b) {
@@ -1335,6 +1373,10 @@ int run_chunk(Item* items, int m) {
     }
     it.rc = MLE_OK;
     it.pivot = -1;
+    if (it.factor) {
+      const double lo = c->h_res[kReduceSums + 3], hi = c->h_res[kReduceSums + 4];
+      c->cond_est = lo > 0.0 ? (hi / lo) * (hi / lo) : 0.0;
+    }
     c->factor_valid = true;
     c->cached_theta[0] = it.P.sigma2;
     c->cached_theta[1] = it.P.alpha;
@@ -1452,6 +1494,12 @@ int mle_kernel_stats(const mle_ctx* ctx, double* out) {
   return MLE_OK;
 }
 
+int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out) {
+  if (!ctx || !out) return fail(MLE_INVALID, "null argument");
+  *out = ctx->cond_est;
+  return MLE_OK;
+}
+
 int mle_release_cached_memory(void) {
   cache_trim(-2);
   return MLE_OK;
@@ -1517,7 +1565,7 @@ static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n,
   CTX_TRY(dmalloc(&c->z, sizeof(double) * n));
   CTX_TRY(dmalloc(&c->fail_flag, sizeof(int)));
   CTX_TRY(dmalloc(&c->fail_idx, sizeof(long long)));
-  CTX_TRY(dmalloc(&c->partials, sizeof(double) * kReduceBlocks * kReduceSums));
+  CTX_TRY(dmalloc(&c->partials, sizeof(double) * kReduceBlocks * kReducePartials));
   CTX_TRY(dmalloc(&c->out, sizeof(double) * kReduceOut));
   CTX_TRY(dmalloc(&c->d_theta, sizeof(ThetaParams)));
   CTX_TRY(dmalloc(&c->gtab_s, sizeof(double) * MLE_TAB_MAX * 3 * MLE_TAB_P));

@@ -98,7 +98,8 @@ cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s
 // Factor the 128x128 diagonal tile at (k0, k0) of every item in place (+ its inverse).
 cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s);
 // Reductions: per item kReduceOut results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>,
-// trM, <A,M>, <N,M>, <M,M>, yBy_A, yBy_N, yBy_M] (the M terms only for nugget items).
+// trM, <A,M>, <N,M>, <M,M>, yBy_A, yBy_N, yBy_M, min L_jj, max L_jj] (the M terms only for
+// nugget items; the diagonal extremes give the engine a conditioning estimate).
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s);
 
 // Scatter the diagonal-tile inverses Linv_k into the per-outer-block inverse storage:
@@ -140,6 +141,7 @@ struct OzSliceArgs {
   long long ld;
   int K;
   int upper_zero;  // 1: element (r, k) with k > r (same origin) is taken as 0
+  int nslices;     // 7 or 8 (0: 8); layout [rows/128][K/32][slices][128 x 32]
   int rows_z[kMaxGemm];  // per-member row count (0: the launch's rows)
 };
 // C = alpha * A B^T + beta * C from slices (A: M rows, B: N rows, both over the same K).
@@ -158,6 +160,7 @@ struct OzGemmArgs {
   double alpha, beta;
   int beta0_tm, beta0_tn;  // tiles with tm < beta0_tm or tn < beta0_tn overwrite (beta = 0)
   int tiles_m_z[kMaxGemm];  // full/trap mode: per-member row tiles (0: tiles_m)
+  int nslices;              // 7 or 8 (0: 8) -- both operands; 7 only for the persistent N=64
   int max_ctas;             // persistent grid cap (0: one CTA per SM); look-ahead launches
                             // leave SMs to the latency-bound factorization chain
   int diag_mode;  // developer diagnostics only: 1 skip the MMAs, 2 skip the loads (0: normal)
@@ -199,6 +202,7 @@ cudaError_t launch_panel_reduce(const PanelReduceArgs& r, int width, int items, 
 
 constexpr int kReduceBlocks = 148 * 4;
 constexpr int kReduceSums = 11;
-constexpr int kReduceOut = kReduceSums + 3;
+constexpr int kReducePartials = kReduceSums + 2;  // + per-block min / max of diag(L)
+constexpr int kReduceOut = kReduceSums + 5;  // sums, yBy_A/N/M, min diag(L), max diag(L)
 
 }  // namespace mle

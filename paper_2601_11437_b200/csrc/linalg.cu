@@ -535,6 +535,7 @@ namespace {
 constexpr int RTHREADS = 256;
 constexpr int RBLOCKS = kReduceBlocks;
 constexpr int RN = kReduceSums;
+constexpr int RP = kReducePartials;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -563,10 +564,13 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   double s[RN];
 #pragma unroll
   for (int q = 0; q < RN; ++q) s[q] = 0.0;
+  double dmin = INFINITY, dmax = 0.0;
   for (int j = blockIdx.x; j < n; j += gridDim.x) {
     const long long cj = (long long)j * ld;
     if (threadIdx.x == 0) {
       s[0] += log(L[j + cj]);
+      dmin = fmin(dmin, L[j + cj]);
+      dmax = fmax(dmax, L[j + cj]);
       const double y = L[n + cj];
       s[1] += y * y;
       if (Ba == nullptr) continue;
@@ -607,7 +611,11 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   double* partials = ra.partials[item];
   for (int q = 0; q < RN; ++q) {
     const double t = q < kSums ? block_sum(s[q], sh) : 0.0;
-    if (threadIdx.x == 0) partials[blockIdx.x * RN + q] = t;
+    if (threadIdx.x == 0) partials[blockIdx.x * RP + q] = t;
+  }
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x * RP + RN] = dmin;
+    partials[blockIdx.x * RP + RN + 1] = dmax;
   }
 }
 
@@ -624,12 +632,22 @@ __global__ void reduce_final_kernel(ReduceArgs ra) {
   const int q = threadIdx.x;
   if (q < RN) {
     double s = 0.0;
-    for (int b = 0; b < RBLOCKS; ++b) s += partials[b * RN + q];
+    for (int b = 0; b < RBLOCKS; ++b) s += partials[b * RP + q];
     out[q] = s;
   }
   if (q == RN) out[RN] = Ba ? Ba[diag_n] : 0.0;
   if (q == RN + 1) out[RN + 1] = Bn ? Bn[diag_n] : 0.0;
   if (q == RN + 2) out[RN + 2] = Bm ? Bm[diag_n] : 0.0;
+  if (q == RN + 3) {
+    double v = INFINITY;
+    for (int b = 0; b < RBLOCKS; ++b) v = fmin(v, partials[b * RP + RN]);
+    out[RN + 3] = v;
+  }
+  if (q == RN + 4) {
+    double v = 0.0;
+    for (int b = 0; b < RBLOCKS; ++b) v = fmax(v, partials[b * RP + RN + 1]);
+    out[RN + 4] = v;
+  }
 }
 
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {

@@ -117,11 +117,28 @@ __device__ __forceinline__ void oz_horner4(uint32_t addr, uint32_t stride, long 
            (int)v3[j];
 }
 
+__device__ __forceinline__ void oz_horner3(uint32_t addr, uint32_t stride, long long (&h)[16]) {
+  uint32_t v0[16], v1[16], v2[16];
+  oz_tmem_ld16(addr, v0);
+  oz_tmem_ld16(addr + stride, v1);
+  oz_tmem_ld16(addr + 2 * stride, v2);
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    h[j] = (((long long)(int)v0[j] * 128 + (int)v1[j]) * 128) + (int)v2[j];
+}
+
+// kS slices: diagonals d = 2..kS+1; hi over d = 2..5, lo over d = 6..kS+1.
+template <int kS>
 __device__ __forceinline__ void oz_combine16(uint32_t addr, uint32_t stride, double (&out)[16]) {
+  static_assert(kS == 7 || kS == 8, "7 or 8 slices");
   long long hi[16], lo[16];
   oz_horner4(addr, stride, hi);
-  oz_horner4(addr + 4 * stride, stride, lo);
-  const double s_hi = pow2i(-35), s_lo = pow2i(-63);
+  if (kS == 8)
+    oz_horner4(addr + 4 * stride, stride, lo);
+  else
+    oz_horner3(addr + 4 * stride, stride, lo);
+  const double s_hi = pow2i(-35), s_lo = pow2i(-7 * (kS + 1));
 #pragma unroll
   for (int j = 0; j < 16; ++j) out[j] = fma((double)hi[j], s_hi, (double)lo[j] * s_lo);
 }
@@ -141,7 +158,7 @@ constexpr int kOzSliceSmem = kOzSliceRows * kOzSliceStride * 8;
 constexpr int kOzSliceThreads = 512;
 constexpr int kOzSliceWarps = kOzSliceThreads / 32;
 
-template <int kRowContig>
+template <int kRowContig, int kS>
 __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs sa) {
   const int z = blockIdx.z;
   if (sa.fail_flag[z] && *sa.fail_flag[z]) return;
@@ -211,14 +228,14 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
   // work item = (row, 16-wide k chunk); lanes on consecutive rows
   for (int item = t; item < kOzSliceRows * (K / 16); item += kOzSliceThreads) {
     const int r = item & (kOzSliceRows - 1), ch = item / kOzSliceRows;
-    // |x| 2^(56 - e) < 2^56 is exact (power-of-two scaling); its truncation holds the 8
-    // base-128 digits the float recurrence (x 2^7, trunc, subtract) would produce.
-    const int sh = 56 - ex[r];
+    // |x| 2^(7 kS - e) < 2^(7 kS) is exact (power-of-two scaling); its truncation holds the
+    // kS base-128 digits the float recurrence (x 2^7, trunc, subtract) would produce.
+    const int sh = 7 * kS - ex[r];
     const double sc1 = pow2i(sh > 1000 ? 1000 : sh), sc2 = pow2i(sh > 1000 ? sh - 1000 : 0);
     const double* src = tile + r * kOzSliceStride + ch * 16;
-    uint32_t wd[OZ_S][4];
+    uint32_t wd[kS][4];
 #pragma unroll
-    for (int p = 0; p < OZ_S; ++p) wd[p][0] = wd[p][1] = wd[p][2] = wd[p][3] = 0u;
+    for (int p = 0; p < kS; ++p) wd[p][0] = wd[p][1] = wd[p][2] = wd[p][3] = 0u;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const double x = src[c];
@@ -226,18 +243,18 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
           (unsigned long long)__double2ll_rz(fabs(x) * sc1 * sc2);
       const bool neg = x < 0.0;
 #pragma unroll
-      for (int p = 0; p < OZ_S; ++p) {
-        const uint32_t d = (uint32_t)(u >> (56 - 7 * (p + 1))) & 127u;
+      for (int p = 0; p < kS; ++p) {
+        const uint32_t d = (uint32_t)(u >> (7 * kS - 7 * (p + 1))) & 127u;
         const uint32_t byte = (neg ? (0u - d) : d) & 0xFFu;
         wd[p][c >> 2] |= byte << (8 * (c & 3));
       }
     }
     const int kb = ch >> 1, half = ch & 1;
     const int rl = rsub + r;
-    int8_t* dst = out + ((size_t)(tile128 * kblocks + kb) * OZ_S) * OZ_BLK +
+    int8_t* dst = out + ((size_t)(tile128 * kblocks + kb) * kS) * OZ_BLK +
                   (size_t)(rl >> 3) * 256 + (size_t)(rl & 7) * 16 + (size_t)half * 128;
 #pragma unroll
-    for (int p = 0; p < OZ_S; ++p)
+    for (int p = 0; p < kS; ++p)
       *reinterpret_cast<uint4*>(dst + (size_t)p * OZ_BLK) =
           make_uint4(wd[p][0], wd[p][1], wd[p][2], wd[p][3]);
   }
@@ -370,7 +387,7 @@ __global__ void __launch_bounds__(OZ_THREADS, OzCfg<kN>::kCtasPerSm) ozgemm_kern
 #pragma unroll
     for (int c0 = 0; c0 < kN; c0 += 16) {
       double part[16];
-      oz_combine16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, kN, part);
+      oz_combine16<OZ_S>(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, kN, part);
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[c0 + j] = part[j];
     }
@@ -407,12 +424,13 @@ __global__ void __launch_bounds__(OZ_THREADS, OzCfg<kN>::kCtasPerSm) ozgemm_kern
 //            streaming the next tile's stages while the epilogue drains TMEM.
 // 8 epilogue warps (two per TMEM lane quadrant, kN / 2 columns each).  Per-tile arithmetic
 // is that of ozgemm_kernel, so every variant gives bit-identical results.
-template <int kN>
+template <int kN, int kS = OZ_S>
 struct OzP {
-  static constexpr int kStages = kN == 32 ? 5 : 4;
-  static constexpr int kStage = OZ_A_STAGE + OZ_S * kN * OZ_KB;
+  static constexpr int kAStage = kS * OZ_BLK;
+  static constexpr int kStage = kAStage + kS * kN * OZ_KB;
+  static constexpr int kStages = kN == 32 ? 5 : (kS == 8 ? 4 : 5);
   static constexpr int kSmem = kStages * kStage;
-  static constexpr int kAcc = OZ_S * kN;            // TMEM columns per accumulator set
+  static constexpr int kAcc = kS * kN;              // TMEM columns per accumulator set
   static constexpr int kSets = kN == 32 ? 2 : 1;
 };
 constexpr int OZP_EPI_WARPS = 8;
@@ -446,11 +464,11 @@ __device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, long long per_z, lo
   return *g.fail_flag[o.z] == 0;
 }
 
-template <int kN>
+template <int kN, int kS>
 __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGemmArgs g,
                                                                            long long per_z,
                                                                            long long total) {
-  using Cfg = OzP<kN>;
+  using Cfg = OzP<kN, kS>;
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   __shared__ __align__(8) uint64_t full_bar[Cfg::kStages], empty_bar[Cfg::kStages];
   __shared__ __align__(8) uint64_t acc_full[Cfg::kSets], acc_empty[Cfg::kSets];
@@ -485,25 +503,25 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       for (long long t = blockIdx.x; t < total; t += gridDim.x) {
         OzTile o;
         if (!oz_tile<kN>(g, per_z, t, o)) continue;
-        const int8_t* Ablk = g.As[o.z] + (size_t)o.tm * kblocks * OZ_S * OZ_BLK;
-        const int8_t* Bblk = g.Bs[o.z] + (size_t)o.tn * kblocks * OZ_S * OZ_BLK +
+        const int8_t* Ablk = g.As[o.z] + (size_t)o.tm * kblocks * kS * OZ_BLK;
+        const int8_t* Bblk = g.Bs[o.z] + (size_t)o.tn * kblocks * kS * OZ_BLK +
                              (size_t)o.part * (kN * OZ_KB);
         for (int kb = 0; kb < kblocks; ++kb, ++gk) {
           const int st = (int)(gk % Cfg::kStages);
           const long long use = gk / Cfg::kStages;
           if (use >= 1) mbar_wait(&empty_bar[st], (uint32_t)((use - 1) & 1));
           uint8_t* sa = oz_smem + (size_t)st * Cfg::kStage;
-          uint8_t* sb = sa + OZ_A_STAGE;
+          uint8_t* sb = sa + Cfg::kAStage;
           if (g.diag_mode == 2 || g.diag_mode >= 5) {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                 smem_u32(&full_bar[st])) : "memory");
             continue;
           }
           mbar_expect_tx(&full_bar[st], Cfg::kStage);
-          bulk_g2s(sa, Ablk + (size_t)kb * OZ_S * OZ_BLK, OZ_A_STAGE, &full_bar[st]);
-          const int8_t* bsrc = Bblk + (size_t)kb * OZ_S * OZ_BLK;
+          bulk_g2s(sa, Ablk + (size_t)kb * kS * OZ_BLK, Cfg::kAStage, &full_bar[st]);
+          const int8_t* bsrc = Bblk + (size_t)kb * kS * OZ_BLK;
 #pragma unroll
-          for (int q = 0; q < OZ_S; ++q)
+          for (int q = 0; q < kS; ++q)
             bulk_g2s(sb + q * (kN * OZ_KB), bsrc + (size_t)q * OZ_BLK, kN * OZ_KB,
                      &full_bar[st]);
         }
@@ -536,11 +554,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
           const uint32_t sa = smem_u32(oz_smem + (size_t)st * Cfg::kStage);
-          const uint32_t sb = sa + OZ_A_STAGE;
+          const uint32_t sb = sa + Cfg::kAStage;
 #pragma unroll
-          for (int p = 1; p <= OZ_S; ++p) {
+          for (int p = 1; p <= kS; ++p) {
             if (g.diag_mode == 1 && !(kb == 0 && p == 1)) continue;
-            const int rows = kN * (OZ_S + 1 - p);  // B rows [B_1 .. B_{9-p}]
+            const int rows = kN * (kS + 1 - p);  // B rows [B_1 .. B_{kS+1-p}]
             const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
 #pragma unroll
             for (int r0 = 0; r0 < rows; r0 += 256) {
@@ -608,7 +626,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       for (int c0 = 0; c0 < kCols; c0 += 16) {
         double part[16];
         if (g.diag_mode != 3 && g.diag_mode < 5)
-          oz_combine16(tmem + ((uint32_t)(qd * 32) << 16) +
+          oz_combine16<kS>(tmem + ((uint32_t)(qd * 32) << 16) +
                            (uint32_t)(ab * Cfg::kAcc + ch * kCols + c0),
                        kN, part);
 #pragma unroll
@@ -652,19 +670,26 @@ cudaError_t init_ozaki_attributes() {
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<32>,
+  cudaError_t e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<32, 8>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        OzP<32>::kSmem);
+                                        OzP<32, 8>::kSmem);
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<64>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, OzP<64>::kSmem);
+  e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<64, 8>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, OzP<64, 8>::kSmem);
   if (e0 != cudaSuccess) return e0;
-  cudaError_t e = cudaFuncSetAttribute(oz_slice_kernel<0>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSliceSmem);
+  e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<64, 7>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, OzP<64, 7>::kSmem);
+  if (e0 != cudaSuccess) return e0;
+  cudaError_t e = cudaSuccess;
+#define MLE_SLICE_ATTR(RC, S)                                                              \
+  e = cudaFuncSetAttribute(oz_slice_kernel<RC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           kOzSliceSmem);                                                  \
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(oz_slice_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kOzSliceSmem);
-  if (e != cudaSuccess) return e;
+  MLE_SLICE_ATTR(0, 8)
+  MLE_SLICE_ATTR(1, 8)
+  MLE_SLICE_ATTR(0, 7)
+  MLE_SLICE_ATTR(1, 7)
+#undef MLE_SLICE_ATTR
   e = cudaFuncSetAttribute(ozgemm_kernel<64>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        OzCfg<64>::kSmem);
@@ -677,10 +702,15 @@ cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int
                             cudaStream_t s) {
   if (a.K > kOzSliceMaxK || a.K % OZ_KB || rows % 128) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)(rows / kOzSliceRows), 1, (unsigned)batch);
-  if (row_contig)
-    oz_slice_kernel<1><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+  const bool seven = a.nslices == 7;
+  if (row_contig && seven)
+    oz_slice_kernel<1, 7><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+  else if (row_contig)
+    oz_slice_kernel<1, 8><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+  else if (seven)
+    oz_slice_kernel<0, 7><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   else
-    oz_slice_kernel<0><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+    oz_slice_kernel<0, 8><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -693,11 +723,14 @@ cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_
     const long long per_z = tiles * (128 / kn), total = per_z * batch;
     const long long cap = g.max_ctas > 0 ? std::min(g.max_ctas, g_num_sms) : g_num_sms;
     const long long grid = std::min<long long>(total, cap);
-    if (kn == 64)
-      ozgemm_persistent_kernel<64><<<(unsigned)grid, OZP_THREADS, OzP<64>::kSmem, s>>>(
+    if (kn == 64 && g.nslices == 7)
+      ozgemm_persistent_kernel<64, 7><<<(unsigned)grid, OZP_THREADS, OzP<64, 7>::kSmem, s>>>(
+          g, per_z, total);
+    else if (kn == 64)
+      ozgemm_persistent_kernel<64, 8><<<(unsigned)grid, OZP_THREADS, OzP<64, 8>::kSmem, s>>>(
           g, per_z, total);
     else
-      ozgemm_persistent_kernel<32><<<(unsigned)grid, OZP_THREADS, OzP<32>::kSmem, s>>>(
+      ozgemm_persistent_kernel<32, 8><<<(unsigned)grid, OZP_THREADS, OzP<32, 8>::kSmem, s>>>(
           g, per_z, total);
   } else if (n_tile == 64) {
     ozgemm_kernel<64><<<dim3((unsigned)(2 * tiles), 1, (unsigned)batch), OZ_THREADS,

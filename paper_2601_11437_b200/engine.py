@@ -105,6 +105,12 @@ class Engine:
         nat.check(rc)
         return out
 
+    def cond_estimate(self) -> float:
+        """(max / min diag L)^2 of the last factorization (0.0 before any)."""
+        out = np.zeros(1)
+        nat.check(nat.lib.mle_ctx_cond_estimate(self._ctx, nat.as_ptr(out)))
+        return float(out[0])
+
     def kernel_profile(self, enable: bool = True):
         """Serialise passes led by this engine and event-time every Ozaki GEMM / slicing."""
         nat.check(nat.lib.mle_kernel_profile(self._ctx, int(bool(enable))))
