@@ -83,10 +83,11 @@ int mle_release_cached_memory(void);
  *   [0] GEMM launches  [1] GEMM ms (sum of launch durations)  [2] FP64-equivalent tile
  *   flops  [3] int8 tensor-core ops (36 slice products)  [4] slicing launches  [5] slicing
  *   ms  [6] slicing algorithmic bytes  [7] host time to enqueue the last pass (ms; also
- *   maintained when profiling is off).
+ *   maintained when profiling is off)  [8] GPU idle time between the previous pass on this
+ *   device and this one (ms).
  * Diagnostic only: no reference counterpart.
  */
-#define MLE_KSTATS 8
+#define MLE_KSTATS 9
 /* (max L_jj / min L_jj)^2 of the context's last successful factorization (0 before any): a
  * cheap lower bound of cond(Sigma), reported for diagnostics. */
 int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out);

@@ -74,7 +74,8 @@ class BatchCoordinator:
         self.eval_passes = 0
         # device-side accounting of every batch (CUDA events on the launching stream)
         self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
-                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0}
+                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0,
+                    "gpu_gap_ms": 0.0}
 
     def _run_locked_batch(self):
         # Alignment policy: while some clients wait on a cheap loglik (gen + Cholesky) and
@@ -178,7 +179,8 @@ class LockstepStats:
         self.requests = 0
         self.eval_passes = 0
         self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
-                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0}
+                    "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0,
+                    "gpu_gap_ms": 0.0}
 
 
 def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None):
@@ -238,7 +240,9 @@ def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out
             try:
                 out = eval_batch([datasets[i].engine() for i in run], thetas, modes)
                 p = datasets[run[0]].engine().phase_times()
-                p["host_enqueue_ms"] = datasets[run[0]].engine().kernel_stats()["host_enqueue_ms"]
+                ks = datasets[run[0]].engine().kernel_stats()
+                p["host_enqueue_ms"] = ks["host_enqueue_ms"]
+                p["gpu_gap_ms"] = ks["gpu_gap_ms"]
                 for key in stats.acc:
                     stats.acc[key] += p[key]
                 for i, (rc, piv, ll, grad, fisher) in zip(run, out):

@@ -44,6 +44,14 @@ namespace {
 thread_local std::string g_last_error;
 std::mutex g_init_mutex;
 std::vector<int> g_device_ready;
+// GPU idle gap between consecutive passes on a device (diagnostic, kernel-stats slot 8):
+// end-of-pass events alternate between two slots per device.
+struct PassClock {
+  cudaEvent_t end[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr;
+  long long passes = 0;
+};
+std::vector<PassClock> g_pass_clock;
 const double kLog2Pi = 1.8378770664093453;  // log(2 pi), likelihood.py:38
 constexpr int kOuter = 4;                   // outer block = 4 x 128 columns
 constexpr int kResults = 13;                // loglik, grad[3], fisher[9]
@@ -1152,6 +1160,18 @@ int run_chunk(Item* items, int m) {
     CUDA_TRY(launch_scatter_theta(io, lead->d_stage, m, s));
   }
   CUDA_TRY(cudaEventRecord(lead->ev[0], s));
+  PassClock* pc = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_init_mutex);
+    if ((int)g_pass_clock.size() <= lead->device) g_pass_clock.resize(lead->device + 1);
+    pc = &g_pass_clock[lead->device];
+    if (!pc->start) {
+      CUDA_TRY(cudaEventCreate(&pc->start));
+      CUDA_TRY(cudaEventCreate(&pc->end[0]));
+      CUDA_TRY(cudaEventCreate(&pc->end[1]));
+    }
+  }
+  CUDA_TRY(cudaEventRecord(pc->start, s));
   // Generation.  Sigma (items that factor) on the main stream; the derivative matrices on
   // the aux stream, concurrently with the Cholesky (they are only needed by the solves).
   auto gen_set = [&](bool sigma_pass) {
@@ -1313,8 +1333,17 @@ int run_chunk(Item* items, int m) {
     CUDA_TRY(cudaMemcpyAsync(lead->h_resb, lead->d_resb, sizeof(double) * m * (kReduceOut + 2),
                              cudaMemcpyDeviceToHost, s));
   }
+  CUDA_TRY(cudaEventRecord(pc->end[pc->passes & 1], s));
   const auto host_t1 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(s));
+  float gap_ms = 0.f;
+  if (pc->passes > 0) {
+    if (cudaEventElapsedTime(&gap_ms, pc->end[(pc->passes - 1) & 1], pc->start) != cudaSuccess) {
+      cudaGetLastError();
+      gap_ms = 0.f;
+    }
+  }
+  ++pc->passes;
   CUDA_TRY(cudaGetLastError());
   const auto host_t2 = std::chrono::steady_clock::now();
   {
@@ -1351,6 +1380,7 @@ int run_chunk(Item* items, int m) {
     c->launches = run.launches;
     if (c == lead) {
       c->kstats[7] = std::chrono::duration<double, std::milli>(host_t1 - host_t0).count();
+      c->kstats[8] = gap_ms;
       c->host_wait_ms = std::chrono::duration<double, std::milli>(host_t2 - host_t1).count();
     }
     if (c != lead) std::memcpy(c->kstats, lead->kstats, sizeof(c->kstats));

@@ -39,5 +39,6 @@ for r in range(3):
     dev = a["gen_ms"] + a["potrf_ms"] + a["solve_ms"] + a["reduce_ms"]
     print(f"step wall {1e3*wall:.1f} ms | in eval_batch {1e3*acc['eval_batch_s']:.1f} ms "
           f"({acc['calls']} calls) | device phases {dev:.1f} ms | host enqueue "
-          f"{a['host_enqueue_ms']:.1f} ms | python outside eval_batch "
+          f"{a['host_enqueue_ms']:.1f} ms | GPU idle between passes {a['gpu_gap_ms']:.1f} ms "
+          f"| python outside eval_batch "
           f"{1e3*(wall-acc['eval_batch_s']):.1f} ms")
