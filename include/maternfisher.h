@@ -83,11 +83,12 @@ int mle_release_cached_memory(void);
  *   [0] GEMM launches  [1] GEMM ms (sum of launch durations)  [2] FP64-equivalent tile
  *   flops  [3] int8 tensor-core ops (36 slice products)  [4] slicing launches  [5] slicing
  *   ms  [6] slicing algorithmic bytes  [7] host time to enqueue the last pass (ms; also
- *   maintained when profiling is off)  [8] GPU idle time between the previous pass on this
- *   device and this one (ms).
+ *   maintained when profiling is off)  [8] main-stream idle time between the previous pass on
+ *   this device and the host's first enqueue of this one (ms)  [9] time this pass then waited
+ *   for pending speculation and its parameter upload (ms).
  * Diagnostic only: no reference counterpart.
  */
-#define MLE_KSTATS 9
+#define MLE_KSTATS 10
 /* (max L_jj / min L_jj)^2 of the context's last successful factorization (0 before any): a
  * cheap lower bound of cond(Sigma), reported for diagnostics. */
 int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out);

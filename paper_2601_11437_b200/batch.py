@@ -75,7 +75,7 @@ class BatchCoordinator:
         # device-side accounting of every batch (CUDA events on the launching stream)
         self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
                     "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0,
-                    "gpu_gap_ms": 0.0}
+                    "gpu_gap_ms": 0.0, "spec_wait_ms": 0.0}
 
     def _run_locked_batch(self):
         # Alignment policy: while some clients wait on a cheap loglik (gen + Cholesky) and
@@ -96,7 +96,9 @@ class BatchCoordinator:
                                  [r[2] for r in reqs])
                 err = None
                 p = reqs[0][0].phase_times()  # batch-level (same on every member)
-                p["host_enqueue_ms"] = reqs[0][0].kernel_stats()["host_enqueue_ms"]
+                ks = reqs[0][0].kernel_stats()
+                for key in ("host_enqueue_ms", "gpu_gap_ms", "spec_wait_ms"):
+                    p[key] = ks[key]
                 for key in self.acc:
                     self.acc[key] += p[key]
             except Exception as exc:  # CUDA failures reach every client
@@ -180,7 +182,7 @@ class LockstepStats:
         self.eval_passes = 0
         self.acc = {"flops": 0.0, "gen_ms": 0.0, "potrf_ms": 0.0, "solve_ms": 0.0,
                     "reduce_ms": 0.0, "gen_bytes": 0.0, "launches": 0, "host_enqueue_ms": 0.0,
-                    "gpu_gap_ms": 0.0}
+                    "gpu_gap_ms": 0.0, "spec_wait_ms": 0.0}
 
 
 def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None):
@@ -241,8 +243,8 @@ def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out
                 out = eval_batch([datasets[i].engine() for i in run], thetas, modes)
                 p = datasets[run[0]].engine().phase_times()
                 ks = datasets[run[0]].engine().kernel_stats()
-                p["host_enqueue_ms"] = ks["host_enqueue_ms"]
-                p["gpu_gap_ms"] = ks["gpu_gap_ms"]
+                for key in ("host_enqueue_ms", "gpu_gap_ms", "spec_wait_ms"):
+                    p[key] = ks[key]
                 for key in stats.acc:
                     stats.acc[key] += p[key]
                 for i, (rc, piv, ll, grad, fisher) in zip(run, out):

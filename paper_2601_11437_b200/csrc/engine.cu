@@ -49,6 +49,7 @@ std::vector<int> g_device_ready;
 struct PassClock {
   cudaEvent_t end[2] = {nullptr, nullptr};
   cudaEvent_t start = nullptr;
+  cudaEvent_t pre = nullptr;  // before the pass waits on pending speculation
   long long passes = 0;
 };
 std::vector<PassClock> g_pass_clock;
@@ -545,6 +546,22 @@ struct Launcher {
   cudaStream_t bulk() const { return s2 ? s2 : s; }
   cudaStream_t s3 = nullptr;   // inner look-ahead of the Cholesky (null: on s)
   cudaStream_t inner() const { return s3 ? s3 : s; }
+  // W request of the Cholesky: build W_b of these contexts on stream ws as each outer block
+  // of the factor becomes final (Ozaki path only).
+  mle_ctx* const* wreq = nullptr;
+  int nwreq = 0;
+  int wks = 0;
+  cudaStream_t ws = nullptr;
+  int issue_w(int b) {
+    if (nwreq == 0) return MLE_OK;
+    int rc = join(s, ws);
+    if (rc) return rc;
+    const cudaStream_t keep = s;
+    s = ws;
+    rc = compute_w_block(wreq, nwreq, wks, b);
+    s = keep;
+    return rc;
+  }
 
   // Two-level right-looking blocked Cholesky of every item's matrix (ld = N).
   // Inner (128-wide) steps of outer block [b0, b1): diagonal tiles, panels and the updates
@@ -634,7 +651,10 @@ struct Launcher {
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
       const int b1 = std::min(Nt, b0 + kOuter);
       if ((rc = inner_block(cs, mats, n_aug, m, b0, b1))) return rc;
-      if (b1 >= Nt) continue;
+      if (b1 >= Nt) {
+        if ((rc = issue_w(b0 / kOuter))) return rc;
+        continue;
+      }
       // trailing update with P = L[T, b0:b1], K = (b1 - b0) * 128
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
@@ -654,6 +674,7 @@ struct Launcher {
         sa.ld = ld;
         sa.K = kOzK;
         if ((rc = slice(sa, (long long)(Nt - b1) * kNB, true, m))) return rc;
+        if ((rc = issue_w(ob))) return rc;
         OzGemmArgs t = oz_base(ld, Nt - b1, b2 - b1);  // (i)
         t.trap = 1;
         for (int b = 0; b < m; ++b) {
@@ -753,65 +774,56 @@ struct Launcher {
 
   // D_b^-1 for every outer block (DMMA, from the Linv tiles) and the slices of W_b.
   int compute_w(mle_ctx* const* cs, int m, int ks) {
+    const int nb = (cs[0]->Nt + kOuter - 1) / kOuter;
+    for (int b = 0; b < nb; ++b) {
+      int rc = compute_w_block(cs, m, ks, b);
+      if (rc) return rc;
+    }
+    return MLE_OK;
+  }
+
+  // W_b of one outer block: needs only L[c0:, c0:c1] (final once block b is factored) and
+  // its Linv tiles, so the Cholesky issues it block by block (potrf's W request) and the
+  // W_b chain runs under the rest of the factorization instead of after it.
+  int compute_w_block(mle_ctx* const* cs, int m, int ks, int b) {
     const long long ld = cs[0]->N;
     const int Nt = cs[0]->Nt;
-    const int nb = (Nt + kOuter - 1) / kOuter;
     for (int i = 0; i < m; ++i) cs[i]->w_slices = ks;
     int rc;
+    const Blk k = blk(Nt, b);
     {
       double* dv[kMaxItems];
       const double* lv[kMaxItems];
       for (int it = 0; it < m; ++it) {
-        dv[it] = cs[it]->dinv;
+        dv[it] = cs[it]->dinv + (size_t)b * 512 * 512;
         lv[it] = cs[it]->linv;
       }
       launches += 1;
-      CUDA_TRY(launch_linv_to_dinv(dv, lv, Nt, m, s));
+      CUDA_TRY(launch_linv_to_dinv_block(dv, lv, k.t0, k.t1 - k.t0, m, s));
     }
-    // tile row i of every block:  T = L[i, 0:i] Dinv[0:i, 0:i];  Dinv[i, 0:i] = -Linv_i T
-    for (int i = 1; i < kOuter; ++i) {
-      struct Ent {
-        const double* lrow;
-        double* dinv_b;
-        double* T;
-        const double* linv_i;
-        const int* flag;
-      };
-      std::vector<Ent> ents;
-      for (int b = 0; b < nb; ++b) {
-        const Blk k = blk(Nt, b);
-        if (k.t1 - k.t0 <= i) continue;
-        for (int it = 0; it < m; ++it)
-          ents.push_back({cs[it]->sigma + (k.c0 + i * kNB) + k.c0 * ld,
-                          cs[it]->dinv + (size_t)b * 512 * 512,
-                          cs[it]->tscr + (size_t)b * kNB * 512,
-                          cs[it]->linv + (size_t)(k.t0 + i) * kNB * kNB, cs[it]->fail_flag});
+    // tile row i of the block:  T = L[i, 0:i] Dinv[0:i, 0:i];  Dinv[i, 0:i] = -Linv_i T
+    for (int i = 1; i < k.t1 - k.t0; ++i) {
+      GemmArgs t = gemm_base(), u = gemm_base();
+      for (int it = 0; it < m; ++it) {
+        double* dinv_b = cs[it]->dinv + (size_t)b * 512 * 512;
+        double* T = cs[it]->tscr + (size_t)b * kNB * 512;
+        t.A[it] = cs[it]->sigma + (k.c0 + i * kNB) + k.c0 * ld;  // 128 x 128 i, lda = N
+        t.B[it] = dinv_b;  // B(n, k) = Dinv(k, n)  (kBKN, ldb 512)
+        t.C[it] = T;
+        t.fail_flag[it] = cs[it]->fail_flag;
+        u.A[it] = cs[it]->linv + (size_t)(k.t0 + i) * kNB * kNB;  // Linv_i (128 x 128)
+        u.B[it] = T;  // B(n, k) = T(k, n)  (kBKN, ldb 128)
+        u.C[it] = dinv_b + i * kNB;
+        u.fail_flag[it] = cs[it]->fail_flag;
       }
-      for (size_t e0 = 0; e0 < ents.size(); e0 += kMaxGemm) {
-        const int cnt = (int)std::min<size_t>(kMaxGemm, ents.size() - e0);
-        GemmArgs t = gemm_base(), u = gemm_base();
-        for (int z = 0; z < cnt; ++z) {
-          const Ent& e = ents[e0 + z];
-          t.A[z] = e.lrow;    // 128 x 128 i, lda = N
-          t.B[z] = e.dinv_b;  // B(n, k) = Dinv(k, n)  (kBKN, ldb 512)
-          t.C[z] = e.T;
-          t.fail_flag[z] = e.flag;
-          u.A[z] = e.linv_i;  // Linv_i (128 x 128)
-          u.B[z] = e.T;       // B(n, k) = T(k, n)  (kBKN, ldb 128)
-          u.C[z] = e.dinv_b + i * kNB;
-          u.fail_flag[z] = e.flag;
-        }
-        t.lda = ld; t.ldb = 512; t.ldc = kNB; t.K = i * kNB;
-        t.tiles_m = 1; t.tiles_n = i; t.alpha = 1.0; t.beta = 0.0;
-        if ((rc = gemm(t, kBKN, cnt))) return rc;
-        u.lda = kNB; u.ldb = kNB; u.ldc = 512; u.K = kNB;
-        u.tiles_m = 1; u.tiles_n = i; u.alpha = -1.0; u.beta = 0.0;
-        if ((rc = gemm(u, kBKN, cnt))) return rc;
-      }
+      t.lda = ld; t.ldb = 512; t.ldc = kNB; t.K = i * kNB;
+      t.tiles_m = 1; t.tiles_n = i; t.alpha = 1.0; t.beta = 0.0;
+      if ((rc = gemm(t, kBKN, m))) return rc;
+      u.lda = kNB; u.ldb = kNB; u.ldc = 512; u.K = kNB;
+      u.tiles_m = 1; u.tiles_n = i; u.alpha = -1.0; u.beta = 0.0;
+      if ((rc = gemm(u, kBKN, m))) return rc;
     }
-    // slices of W_b, block by block (the FP64 bottom part reuses one scratch)
-    for (int b = 0; b < nb; ++b) {
-      const Blk k = blk(Nt, b);
+    {  // slices of W_b (the FP64 bottom part reuses one scratch per context)
       const long long c1 = k.c0 + k.kb;
       const size_t woff = w_byte_offset(Nt, b);
       const long long eoff = w_row_offset(Nt, b);
@@ -828,7 +840,7 @@ struct Launcher {
       top.K = (int)k.kb;
       top.nslices = ks;
       if ((rc = slice(top, k.kb, true, m))) return rc;
-      if (c1 >= ld) continue;
+      if (c1 >= ld) return MLE_OK;
       OzSliceArgs dt;  // B(j, kk) = Dinv(kk, j): D_b^-T rows (k-contig, ld 512)
       std::memset(&dt, 0, sizeof(dt));
       for (int it = 0; it < m; ++it) {
@@ -1133,6 +1145,19 @@ int run_chunk(Item* items, int m) {
   if (lookahead) run.s3 = lead->inner;
   if (lead->kprof) run.prof = lead;
   cudaStream_t aux = lead->kprof ? s : lead->aux;  // profiling: everything serialised
+  PassClock* pc = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_init_mutex);
+    if ((int)g_pass_clock.size() <= lead->device) g_pass_clock.resize(lead->device + 1);
+    pc = &g_pass_clock[lead->device];
+    if (!pc->start) {
+      CUDA_TRY(cudaEventCreate(&pc->start));
+      CUDA_TRY(cudaEventCreate(&pc->pre));
+      CUDA_TRY(cudaEventCreate(&pc->end[0]));
+      CUDA_TRY(cudaEventCreate(&pc->end[1]));
+    }
+  }
+  CUDA_TRY(cudaEventRecord(pc->pre, s));
   for (int b = 0; b < m; ++b) {
     Item& it = items[b];
     int rc = wait_spec(it.c, s);
@@ -1160,17 +1185,6 @@ int run_chunk(Item* items, int m) {
     CUDA_TRY(launch_scatter_theta(io, lead->d_stage, m, s));
   }
   CUDA_TRY(cudaEventRecord(lead->ev[0], s));
-  PassClock* pc = nullptr;
-  {
-    std::lock_guard<std::mutex> lock(g_init_mutex);
-    if ((int)g_pass_clock.size() <= lead->device) g_pass_clock.resize(lead->device + 1);
-    pc = &g_pass_clock[lead->device];
-    if (!pc->start) {
-      CUDA_TRY(cudaEventCreate(&pc->start));
-      CUDA_TRY(cudaEventCreate(&pc->end[0]));
-      CUDA_TRY(cudaEventCreate(&pc->end[1]));
-    }
-  }
   CUDA_TRY(cudaEventRecord(pc->start, s));
   // Generation.  Sigma (items that factor) on the main stream; the derivative matrices on
   // the aux stream, concurrently with the Cholesky (they are only needed by the solves).
@@ -1253,49 +1267,59 @@ int run_chunk(Item* items, int m) {
     CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
   }
   CUDA_TRY(cudaEventRecord(lead->ev[1], s));
+  // W_b of the items that factor in this pass and need it (eval_all, or speculation for a
+  // loglik item) is built on the aux stream block by block during their Cholesky.
+  bool w_in_potrf[kMaxItems] = {};
+  bool any_w_eval = false;
   {  // Cholesky for items without a cached factor
     mle_ctx* cs[kMaxItems];
+    mle_ctx* wr[kMaxItems];
     double* mats[kMaxItems];
     long long aug[kMaxItems];
-    int nf = 0;
+    int nf = 0, nwr = 0;
     for (int b = 0; b < m; ++b)
       if (items[b].factor) {
-        cs[nf] = items[b].c;
-        mats[nf] = items[b].c->sigma;
-        aug[nf] = items[b].c->n;
+        mle_ctx* c = items[b].c;
+        cs[nf] = c;
+        mats[nf] = c->sigma;
+        aug[nf] = c->n;
         ++nf;
+        if (c->lsl && c->wsl && (items[b].spec || items[b].need_w)) {
+          wr[nwr++] = c;
+          w_in_potrf[b] = true;
+          any_w_eval = any_w_eval || items[b].need_w;
+        }
       }
     if (nf > 0) {
+      run.wreq = wr;
+      run.nwreq = nwr;
+      run.wks = solve_slices();
+      run.ws = aux;
       int rc = run.potrf(cs, mats, aug, nf);
+      run.nwreq = 0;
       if (rc) return rc;
     }
   }
   CUDA_TRY(cudaEventRecord(lead->ev[2], s));
   if (any_spec) {
-    // speculative W_b for the loglik items, on the aux stream after their Cholesky
-    mle_ctx* cs[kMaxItems];
-    int ns = 0;
     for (int b = 0; b < m; ++b)
-      if (items[b].spec) cs[ns++] = items[b].c;
-    int rc = run.join(s, aux);
-    if (rc) return rc;
-    Launcher sp{aux};
-    rc = sp.compute_w(cs, ns, solve_slices());
-    if (rc) return rc;
-    run.launches += sp.launches;
-    for (int b = 0; b < ns; ++b) {
-      CUDA_TRY(cudaEventRecord(cs[b]->spec_done, aux));
-      cs[b]->spec_pending = true;
-    }
+      if (items[b].spec) {
+        CUDA_TRY(cudaEventRecord(items[b].c->spec_done, aux));
+        items[b].c->spec_pending = true;
+      }
   }
   {
     if (der.second > 0) CUDA_TRY(cudaStreamWaitEvent(s, lead->ev_der, 0));
+    if (any_w_eval) {
+      int rc = run.join(aux, s);
+      if (rc) return rc;
+    }
     mle_ctx* cs[kMaxItems];
     mle_ctx* cw[kMaxItems];
     int nd = 0, nw = 0;
     for (int b = 0; b < m; ++b) {
       if (items[b].derivs) cs[nd++] = items[b].c;
-      if (items[b].need_w) cw[nw++] = items[b].c;
+      if (items[b].need_w && !w_in_potrf[b]) cw[nw++] = items[b].c;
     }
     if (nd > 0) {
       int rc = run.solves(cs, nd, cw, nw);
@@ -1336,11 +1360,12 @@ int run_chunk(Item* items, int m) {
   CUDA_TRY(cudaEventRecord(pc->end[pc->passes & 1], s));
   const auto host_t1 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(s));
-  float gap_ms = 0.f;
+  float gap_ms = 0.f, wait_ms = 0.f;
   if (pc->passes > 0) {
-    if (cudaEventElapsedTime(&gap_ms, pc->end[(pc->passes - 1) & 1], pc->start) != cudaSuccess) {
+    if (cudaEventElapsedTime(&gap_ms, pc->end[(pc->passes - 1) & 1], pc->pre) != cudaSuccess ||
+        cudaEventElapsedTime(&wait_ms, pc->pre, pc->start) != cudaSuccess) {
       cudaGetLastError();
-      gap_ms = 0.f;
+      gap_ms = wait_ms = 0.f;
     }
   }
   ++pc->passes;
@@ -1381,6 +1406,7 @@ int run_chunk(Item* items, int m) {
     if (c == lead) {
       c->kstats[7] = std::chrono::duration<double, std::milli>(host_t1 - host_t0).count();
       c->kstats[8] = gap_ms;
+      c->kstats[9] = wait_ms;
       c->host_wait_ms = std::chrono::duration<double, std::milli>(host_t2 - host_t1).count();
     }
     if (c != lead) std::memcpy(c->kstats, lead->kstats, sizeof(c->kstats));

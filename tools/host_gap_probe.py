@@ -29,8 +29,20 @@ def timed_eval_batch(*a, **k):
 
 
 B.eval_batch = timed_eval_batch
+_c_call = B.nat.lib.mle_eval_batch
+acc["c_s"] = 0.0
+
+
+def timed_c_call(*a):
+    t0 = time.perf_counter()
+    rc = _c_call(*a)
+    acc["c_s"] += time.perf_counter() - t0
+    return rc
+
+
+B.nat.lib.mle_eval_batch = timed_c_call
 for r in range(3):
-    acc.update(calls=0, eval_batch_s=0.0)
+    acc.update(calls=0, eval_batch_s=0.0, c_s=0.0)
     coords = []
     t0 = time.perf_counter()
     B.fit_many(data, cfg, coordinator_out=coords)
@@ -40,5 +52,6 @@ for r in range(3):
     print(f"step wall {1e3*wall:.1f} ms | in eval_batch {1e3*acc['eval_batch_s']:.1f} ms "
           f"({acc['calls']} calls) | device phases {dev:.1f} ms | host enqueue "
           f"{a['host_enqueue_ms']:.1f} ms | GPU idle between passes {a['gpu_gap_ms']:.1f} ms "
-          f"| python outside eval_batch "
+          f"+ spec/upload wait {a['spec_wait_ms']:.1f} ms "
+          f"| in C call {1e3*acc['c_s']:.1f} ms | python outside eval_batch "
           f"{1e3*(wall-acc['eval_batch_s']):.1f} ms")
