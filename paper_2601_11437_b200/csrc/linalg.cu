@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "pivot_math.cuh"
 
 namespace mle {
 
@@ -303,35 +304,52 @@ __device__ __forceinline__ void tri_index(int t, int* bi, int* bj) {
   *bj = t - i * (i + 1) / 2;
 }
 
+__device__ __forceinline__ double select_f64(int p, double a, double b) {
+  double o;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\tselp.f64 %0, %2, %3, q;\n\t}"
+      : "=d"(o) : "r"(p), "d"(a), "d"(b));
+  return o;
+}
+
 // One pivot step of the register-resident 16x16 Cholesky (lane r holds row r); recursion
 // keeps every index of v[] a compile-time constant so the block never leaves registers.
+// d is this pivot's value (already broadcast).  The next pivot only needs lane C+1's own
+// update v[C+1] -= vc^2, so it is computed and broadcast first; the rest of the rank-1
+// update (column values through a shared-memory broadcast, col[]) overlaps the next
+// pivot's reciprocal square root.  Entries above the diagonal (s > r) are scratch: they are
+// updated unconditionally (no selects) and never stored.  LAPACK dpotf2 semantics for
+// failures: AJJ <= 0 or NaN stops the factorization; the first failing column is fc.
 template <int C>
-__device__ __forceinline__ void chol16_step(double (&v)[16], int r, int lane, long long g0,
-                                            long long n_aug, bool& failed, int* s_fail,
-                                            long long* fail_idx, int* fail_flag) {
+__device__ __forceinline__ void chol16_step(double (&v)[16], double (&rv)[16], double d, int r,
+                                            long long g0, long long n_aug, int& fc,
+                                            double* col) {
   if constexpr (C < 16) {
-    const double d = __shfl_sync(0xffffffffu, v[C], C);
-    const bool aug = (g0 + C == n_aug);  // augmented index n carries y: no pivot there
-    if (!aug && !(d > 0.0) && !failed) {  // LAPACK dpotf2: AJJ <= 0 or NaN; first wins
-      if (lane == 0) {
-        *s_fail = 1;
-        *fail_idx = g0 + C;
-        *fail_flag = 1;
-      }
-      failed = true;
-    }
-    // LAPACK dpotf2 arithmetic: AJJ = sqrt(AJJ), column scaled by ONE / AJJ (keeps exactly
-    // singular inputs, e.g. coincident locations, failing at the same pivot)
-    const double piv = aug ? 1.0 : sqrt(d);
-    const double rinv = aug ? 1.0 : 1.0 / piv;
-    const double vc = (r == C) ? piv : ((r > C) ? v[C] * rinv : v[C]);
+    const int aug = (g0 + C == n_aug);  // augmented index n carries y: no pivot there
+    fc = (fc < 0 && !aug && !(d > 0.0)) ? C : fc;
+    // LAPACK dpotf2 arithmetic, branch-free (a branch would split the unrolled chain into
+    // separate basic blocks): AJJ = sqrt(AJJ), column scaled by ONE / AJJ
+    const double y = pivot_rsqrt_seed(d);
+    const double piv = select_f64(aug, 1.0, pivot_sqrt_from(d, y));
+    const double rinv = select_f64(aug, 1.0, pivot_rcp_of_sqrt(piv, y));
+    rv[C] = rinv;
+    const double vc = select_f64(r == C, piv, v[C] * rinv);
     v[C] = vc;
+    if constexpr (C + 1 < 16) {
+      double* cb = col + (C & 1) * 32;  // double-buffered: no WAR hazard with the last step
+      const int lane = threadIdx.x & 31;
+      if (lane == C + 1) cb[16] = fma(-vc, vc, v[C + 1]);  // the next pivot, first
+      if (lane < 16) cb[lane] = vc;
+      __syncwarp();
+      const double dn = cb[16];
+      constexpr int s0 = (C + 1) & ~1;  // 16-byte aligned broadcast loads
 #pragma unroll
-    for (int s = C + 1; s < 16; ++s) {
-      const double lsc = __shfl_sync(0xffffffffu, vc, s);
-      v[s] = (r >= s) ? fma(-vc, lsc, v[s]) : v[s];
+      for (int s = s0; s < 16; s += 2) {
+        const double2 l2 = *reinterpret_cast<const double2*>(cb + s);
+        if (s >= C + 1) v[s] = fma(-vc, l2.x, v[s]);
+        v[s + 1] = fma(-vc, l2.y, v[s + 1]);
+      }
+      chol16_step<C + 1>(v, rv, dn, r, g0, n_aug, fc, col);
     }
-    chol16_step<C + 1>(v, r, lane, g0, n_aug, failed, s_fail, fail_idx, fail_flag);
   }
 }
 }  // namespace
@@ -376,16 +394,25 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
     // (a) pivot chain of the 16x16 diagonal block in warp 0's registers
     if (warp == 0) {
       const int r = lane & (DB - 1);
-      double v[DB];
+      double v[DB], rv[DB];
 #pragma unroll
       for (int s = 0; s < DB; ++s) v[s] = (s <= r) ? LS(j0 + r, j0 + s) : 0.0;
-      bool failed = false;
-      chol16_step<0>(v, r, lane, (long long)k0 + j0, n_aug, failed, &s_fail, fail_idx,
-                     fail_flag);
+      int fc = -1;
+      chol16_step<0>(v, rv, LS(j0, j0), r, (long long)k0 + j0, n_aug, fc, scr);
       if (lane < DB) {
 #pragma unroll
         for (int s = 0; s < DB; ++s)
           if (s <= r) LS(j0 + r, j0 + s) = v[s];
+        // reciprocal pivots (1 / L_jj as used by the factorization) for the panel rows and
+        // the inverse
+#pragma unroll
+        for (int s = 0; s < DB; ++s)
+          if (s == r) dinv[j0 + r] = rv[s];
+      }
+      if (fc >= 0 && lane == 0) {
+        s_fail = 1;
+        *fail_idx = (long long)k0 + j0 + fc;
+        *fail_flag = 1;
       }
     }
     __syncthreads();
@@ -401,7 +428,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
       for (int c = 0; c < DB; ++c) x[c] = LS(i, j0 + c);
 #pragma unroll
       for (int c = 0; c < DB; ++c) {
-        x[c] *= 1.0 / LS(j0 + c, j0 + c);
+        x[c] *= dinv[j0 + c];
 #pragma unroll
         for (int m = c + 1; m < DB; ++m) x[m] -= x[c] * LS(j0 + m, j0 + c);
       }
@@ -439,9 +466,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
     DIAG_T(3 + 3 * J)
   }
 
-  // ---- inverse X = L^-1 ----
-  if (tid < DT) dinv[tid] = 1.0 / LS(tid, tid);
-  __syncthreads();
+  // ---- inverse X = L^-1 (dinv holds the reciprocal pivots) ----
   // (i) diagonal 16x16 blocks: thread per (block, column), forward substitution in registers
   if (tid < DT) {
     const int blk = tid >> 4, c = tid & (DB - 1);
