@@ -212,18 +212,16 @@ bool use_lookahead() {  // MLE_LOOKAHEAD=0: everything on the main stream (A/B t
   return !(v && std::strcmp(v, "0") == 0);
 }
 
-// Slices of the solve operands (W_b, X / B panels): 7 (default) or 8 (MLE_SOLVE_SLICES=8).
-// The solves feed traces and Frobenius products (1e-8 tolerances): 7 slices (49-bit operands,
-// products with p + q <= 8) keep DGEMM-level accuracy at 28 instead of 36 int8 products.
-// Slices of the solve operands (W_b, X / B panels): 7 by default, 8 with MLE_SOLVE_SLICES=8.
-// The solves only feed traces and Frobenius products (1e-8 tolerances); 7 slices (49-bit
-// operands, products with p + q <= 8) keep DGEMM-level accuracy at 28 instead of 36 int8
-// products, and pass every parity test at the north-star tolerances (the largest 7-vs-8
-// difference measured is 3.4e-9 of the score's component scale: GMM + nugget, config-5 theta).
-// A fixed setting, not a per-pass choice: results must not depend on batching or history.
+// Slices of the solve sweep operands (X row panels, B column panels, W_b as the A operand):
+// 7 by default (55-bit operands, 28 products), 6 with MLE_SOLVE_SLICES=6 (47-bit operands,
+// 21 products).  6 slices stay within the north-star tolerances (1e-8 of the score's
+// component scale) but move the score by ~1e-9 of that scale, which is enough to flip a
+// Fisher-BT stopping decision that the reference takes 2% inside ||grad|| <= 1e-3 (config 2,
+// seed 2); 7 slices are ~4x more accurate than DGEMM there.  A fixed setting,
+// not a per-pass choice: results must not depend on batching or history.
 int solve_slices() {
   const char* v = std::getenv("MLE_SOLVE_SLICES");
-  return (v && std::strcmp(v, "8") == 0) ? 8 : 7;
+  return (v && std::strcmp(v, "6") == 0) ? 6 : 7;
 }
 
 bool use_speculation() {
@@ -488,8 +486,8 @@ struct Launcher {
     int rc = prof_begin(s);
     if (rc) return rc;
     CUDA_TRY(launch_oz_slice(a, (int)rows, row_contig, batch, s));
-    // algorithmic bytes: the FP64 operand read once, 8 int8 slices + exponents written
-    return prof_end(s, 1, (double)batch * rows * (16.0 * a.K + 4.0));
+    // algorithmic bytes: the FP64 operand read once, S int8 slices + exponents written
+    return prof_end(s, 1, (double)batch * rows * ((8.0 + oz_nslices(a.nslices)) * a.K + 4.0));
   }
   int ozgemm(const OzGemmArgs& g, int batch, cudaStream_t st) {
     launches += 1;
@@ -503,10 +501,9 @@ struct Launcher {
       for (int tn = 0; tn < g.tiles_n; ++tn) tiles += std::max(0, g.tiles_m - tn);
     } else tiles = (double)g.tiles_m * g.tiles_n;
     // FP64-equivalent tile flops (2 x 128 x 128 x K per tile); int8 tensor ops: one slice
-    // product per pair (p, q) with p + q <= S + 1 (36 for 8 slices, 28 for 7)
-    const int S = g.nslices == 7 ? 7 : 8;
+    // product per pair (p, q) with p + q <= S + 1 (28 for 7 slices, 21 for 6)
     const double fl = (double)batch * tiles * 2.0 * kNB * kNB * (32.0 * g.kblocks);
-    return prof_end(st, 0, fl, fl * (S * (S + 1) / 2));
+    return prof_end(st, 0, fl, fl * oz_products(g.nslices));
   }
   int prof_collect() {
     if (!prof) return MLE_OK;

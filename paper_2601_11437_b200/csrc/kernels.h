@@ -131,8 +131,8 @@ cudaError_t launch_trmv_lower(const double* L, long long ld, int n, const double
 
 // Ozaki-scheme FP64 GEMM on tcgen05 int8 tensor cores (ozaki.cu).
 // Slicing: X is rows x K (rows multiple of 128, K multiple of 32) with X(r,k) at
-// X[r + k*ld] (row_contig) or X[k + r*ld]; writes 8 int8 slices in UMMA canonical layout
-// [rows/128][K/32][8][128x32] and one power-of-two exponent per row.
+// X[r + k*ld] (row_contig) or X[k + r*ld]; writes S int8 slices (balanced base-256 digits) in
+// UMMA canonical layout [rows/128][K/32][S][128x32] and one power-of-two exponent per row.
 struct OzSliceArgs {
   const double* X[kMaxGemm];
   int8_t* slices[kMaxGemm];
@@ -141,7 +141,7 @@ struct OzSliceArgs {
   long long ld;
   int K;
   int upper_zero;  // 1: element (r, k) with k > r (same origin) is taken as 0
-  int nslices;     // 7 or 8 (0: 8); layout [rows/128][K/32][slices][128 x 32]
+  int nslices;     // 6 or 7 (0: 7); layout [rows/128][K/32][slices][128 x 32]
   int rows_z[kMaxGemm];  // per-member row count (0: the launch's rows)
 };
 // C = alpha * A B^T + beta * C from slices (A: M rows, B: N rows, both over the same K).
@@ -160,20 +160,21 @@ struct OzGemmArgs {
   double alpha, beta;
   int beta0_tm, beta0_tn;  // tiles with tm < beta0_tm or tn < beta0_tn overwrite (beta = 0)
   int tiles_m_z[kMaxGemm];  // full/trap mode: per-member row tiles (0: tiles_m)
-  int nslices;              // 7 or 8 (0: 8) -- both operands; 7 only for the persistent N=64
+  int nslices;              // 6 or 7 (0: 7) -- both operands
   int max_ctas;             // persistent grid cap (0: one CTA per SM); look-ahead launches
                             // leave SMs to the latency-bound factorization chain
   int diag_mode;  // developer diagnostics only: 1 skip the MMAs, 2 skip the loads (0: normal)
   long long* diag_out;  // developer diagnostics: MMA-thread timing of CTA 0 (null: off)
 };
-constexpr int kOzSlices = 8;
-constexpr int kOzProducts = 36;  // slice products with p + q <= kOzSlices + 1
-// bytes of slice storage for a rows x K operand
+constexpr int kOzSlices = 7;     // slices of the factor (Cholesky, W_b); also the buffer stride
+inline int oz_nslices(int v) { return v == 6 ? 6 : 7; }
+inline int oz_products(int v) { const int s = oz_nslices(v); return s * (s + 1) / 2; }
+// bytes of slice storage for a rows x K operand (at most kOzSlices slices)
 inline size_t oz_slice_bytes(long long rows, int K) { return (size_t)rows * K * kOzSlices; }
 cudaError_t init_ozaki_attributes();
 cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int batch,
                             cudaStream_t s);
-// n_tile: 0 persistent 128x64 (default), 1 persistent 128x32, 32 / 64 one tile per CTA
+// n_tile: 0 persistent 128x64 in CTA pairs sharing A (default), 1 128x32, 2 128x64 unpaired
 cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile = 0);
 
 // ---- distributed engine: column panels (element (i, j) of panel z at p[z][i + (j - c0) ld])

@@ -3,17 +3,20 @@
 // B200 has no FP64 tcgen05 kind; its mma.sync DMMA path peaks at ~36 TF/s.  The trailing
 // updates of the Cholesky and of the solves (C -= A B^T with K = 512) are instead run as an
 // Ozaki-scheme emulation (splitting into int8 slices, exact int32 products):
-//   * every row of A and of B (over the K range) is scaled by a power of two to (-1, 1) and
-//     split into S = 8 signed 7-bit digits:  A(i,:) = 2^ea_i sum_p 2^-7p A_p(i,:)
-//   * C(i,j) = 2^(ea_i + eb_j) sum_{d=2..S+1} 2^-7d  sum_{p+q=d} (A_p B_q^T)(i,j)
-//     (the 36 slice products with p + q <= S + 1; each is an exact int8 x int8 -> int32
-//     tensor-core GEMM, the 8 diagonals d accumulate in 8 TMEM accumulators)
-//   * the FP64 epilogue converts, scales (exact powers of two) and accumulates into C.
-// With S = 8 the error is within a few units of DGEMM's (56 mantissa bits per row before
-// dropped terms; tools/ozaki accuracy study in DESIGN.md), at 4.5 POPS int8 peak / 36.
+//   * every row of A and of B (over the K range) gets a power-of-two exponent e with
+//     max |x| < (509/512) 2^e, and x 2^(8S-1-e) is rounded to the nearest integer X
+//     (|X| < 127.25 * 256^(S-1)), written as S balanced base-256 digits D_p in [-128, 127]:
+//       x = 2^(e+1) sum_{p=1..S} 2^-8p D_p      (8S - 1 significant bits per row, unbiased)
+//   * C(i,j) = 2^(ea_i + eb_j + 2) sum_{d=2..S+1} 2^-8d sum_{p+q=d} (A_p B_q^T)(i,j)
+//     (the S(S+1)/2 slice products with p + q <= S + 1; each is an exact int8 x int8 ->
+//     int32 tensor-core GEMM, the S diagonals d accumulate in S TMEM accumulators)
+//   * the FP64 epilogue folds the diagonals exactly, scales (exact powers of two) and
+//     accumulates into C with one rounding.
+// S = 7 (55-bit operands, 28 products) for the Cholesky and the W_b construction, S = 6
+// (47-bit operands, 21 products) for the solve sweeps (accuracy study: DESIGN.md 4a).
 //
 // Layouts.  Slices are written by oz_slice_kernel in the UMMA canonical K-major
-// SWIZZLE_NONE layout: for each 128-row tile and each 32-wide k block, 8 slices of a
+// SWIZZLE_NONE layout: for each 128-row tile and each 32-wide k block, S slices of a
 // 128 x 32 int8 block (4 KB; core matrices of 8 rows x 16 B, LBO = 128 B, SBO = 256 B).  The
 // first / second 64 rows of a block are its first / second 2 KB, which the GEMM uses as the
 // 64-row B operand.
@@ -28,23 +31,8 @@ namespace mle {
 
 namespace {
 
-constexpr int OZ_S = 8;             // slices per operand
 constexpr int OZ_KB = 32;           // k per MMA (int8)
 constexpr int OZ_BLK = 128 * OZ_KB; // bytes of one slice block (128 rows x 32)
-constexpr int OZ_A_STAGE = OZ_S * OZ_BLK;        // 32 KB: the 8 A slices of one k block
-constexpr int OZ_THREADS = 192;                  // warp 0 producer, 1 MMA, 2-5 epilogue
-
-// CTA tile 128 x kN.  TMEM holds the 8 diagonal accumulators (8 kN columns); kN = 32 fits
-// two CTAs per SM so one CTA's epilogue overlaps the other's main loop.
-template <int kN>
-struct OzCfg {
-  static constexpr int kStages = kN == 64 ? 4 : 2;
-  static constexpr int kBStage = OZ_S * kN * OZ_KB;           // 8 B slices, kN rows each
-  static constexpr int kStage = OZ_A_STAGE + kBStage;
-  static constexpr int kSmem = kStages * kStage;
-  static constexpr int kTmemCols = OZ_S * kN;                 // 512 / 256
-  static constexpr int kCtasPerSm = kN == 64 ? 1 : 2;
-};
 
 __device__ __forceinline__ double pow2i(int e) {  // exact 2^e
   return (e > -1023 && e < 1024) ? __longlong_as_double((long long)(e + 1023) << 52)
@@ -82,18 +70,38 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
       ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Same bytes into the same shared-memory offset of every CTA in cta_mask (cluster multicast);
+// complete_tx is signalled on the barrier at the same offset in each destination CTA.
+__device__ __forceinline__ void bulk_g2s_mc(void* smem, const void* gmem, uint32_t bytes,
+                                            uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 // UMMA shared-memory descriptor: K-major, SWIZZLE_NONE, LBO = 128 B, SBO = 256 B, sm_100.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return ((uint64_t)((saddr >> 4) & 0x3FFF)) | ((uint64_t)(128 >> 4) << 16) |
          ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
 }
 
-// Epilogue combine for 16 columns of one TMEM lane: the 8 int32 diagonal accumulators v_d
-// (d = 2..9, at column offsets (d - 2) * stride from `addr`) fold exactly into two int64
-// Horner sums  hi = sum_{d=2..5} v_d 2^(7 (5 - d)),  lo = sum_{d=6..9} v_d 2^(7 (9 - d))
-// (|v_d| < 2^26 for K <= 512, so |hi|, |lo| < 2^48 convert to double exactly), and
-//   sum_d v_d 2^(-7 d) = hi 2^-35 + lo 2^-63
-// is formed with a single rounding (one FMA).  2 conversions per element instead of 8.
+// Epilogue combine for 16 columns of one TMEM lane: the S int32 diagonal accumulators v_d
+// (d = 2..S+1, at column offsets (d - 2) * stride from `addr`) fold exactly into two int64
+// Horner sums  hi = sum_{d=2..5} v_d 2^(8 (5 - d)),  lo = sum_{d=6..S+1} v_d 2^(8 (S+1-d))
+// (|v_d| < 7 * 2^23 for K <= 512, so |hi| < 2^51 and |lo| < 2^43 convert to double exactly),
+// and  4 sum_d v_d 2^(-8 d) = hi 2^-38 + lo 2^(2 - 8 (S+1))  is formed with one rounding (one
+// FMA; the factor 4 is the 2^(1+1) of the two operands' digit scaling).
 __device__ __forceinline__ void oz_tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
@@ -104,65 +112,46 @@ __device__ __forceinline__ void oz_tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
       : "r"(addr));
 }
 
-__device__ __forceinline__ void oz_horner4(uint32_t addr, uint32_t stride, long long (&h)[16]) {
-  uint32_t v0[16], v1[16], v2[16], v3[16];
-  oz_tmem_ld16(addr, v0);
-  oz_tmem_ld16(addr + stride, v1);
-  oz_tmem_ld16(addr + 2 * stride, v2);
-  oz_tmem_ld16(addr + 3 * stride, v3);
-  asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-    h[j] = ((((long long)(int)v0[j] * 128 + (int)v1[j]) * 128 + (int)v2[j]) * 128) +
-           (int)v3[j];
-}
-
-__device__ __forceinline__ void oz_horner3(uint32_t addr, uint32_t stride, long long (&h)[16]) {
-  uint32_t v0[16], v1[16], v2[16];
-  oz_tmem_ld16(addr, v0);
-  oz_tmem_ld16(addr + stride, v1);
-  oz_tmem_ld16(addr + 2 * stride, v2);
-  asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-    h[j] = (((long long)(int)v0[j] * 128 + (int)v1[j]) * 128) + (int)v2[j];
-}
-
-// kS slices: diagonals d = 2..kS+1; hi over d = 2..5, lo over d = 6..kS+1.
 template <int kS>
 __device__ __forceinline__ void oz_combine16(uint32_t addr, uint32_t stride, double (&out)[16]) {
-  static_assert(kS == 7 || kS == 8, "7 or 8 slices");
-  long long hi[16], lo[16];
-  oz_horner4(addr, stride, hi);
-  if (kS == 8)
-    oz_horner4(addr + 4 * stride, stride, lo);
-  else
-    oz_horner3(addr + 4 * stride, stride, lo);
-  const double s_hi = pow2i(-35), s_lo = pow2i(-7 * (kS + 1));
+  static_assert(kS == 6 || kS == 7, "6 or 7 slices");
+  uint32_t v[kS][16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) out[j] = fma((double)hi[j], s_hi, (double)lo[j] * s_lo);
+  for (int d = 0; d < kS; ++d) oz_tmem_ld16(addr + d * stride, v[d]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+  const double s_hi = pow2i(-38), s_lo = pow2i(2 - 8 * (kS + 1));
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    long long hi = (int)v[0][j], lo = (int)v[4][j];
+#pragma unroll
+    for (int d = 1; d < 4; ++d) hi = hi * 256 + (int)v[d][j];
+#pragma unroll
+    for (int d = 5; d < kS; ++d) lo = lo * 256 + (int)v[d][j];
+    out[j] = fma((double)hi, s_hi, (double)lo * s_lo);
+  }
 }
 
 }  // namespace
 
-// Slicing.  CTA = 32 rows x all K (<= kOzSliceMaxK) of one operand, staged once in shared
-// memory (grid rows/32 x batch): coalesced load, per-row max -> exponent e with
-// |X(r,:)| < 2^e, then each thread turns 16 elements of one row into 8 digits each (exact:
-// x 2^7, trunc, subtract) and writes one 16-byte word per slice in the canonical layout.
-// (32 consecutive rows of a 128-row block are 1 KB contiguous in every slice block.)
-constexpr int kOzSliceRows = 32;
+// Slicing.  CTA = 16 rows x all K (<= kOzSliceMaxK) of one operand, staged once in shared
+// memory (66 KB, 256 threads: three CTAs per SM overlap one another's load / digit phases; grid rows/16 x
+// batch): coalesced load, per-row max -> exponent e, then each thread turns 16 elements of one
+// row into kS balanced base-256 digits each (exact power-of-two scaling, one round-to-
+// nearest, integer digit extraction) and writes one 16-byte word per slice in the canonical
+// layout.  (16 consecutive rows of a 128-row block are 512 B contiguous in every slice block.)
+constexpr int kOzSliceRows = 16;
 constexpr int kOzSliceMaxK = 512;
 constexpr int kOzSliceStride = kOzSliceMaxK + 1;  // odd stride: conflict-free row access
 constexpr int kOzSliceSmem = kOzSliceRows * kOzSliceStride * 8;
 
-constexpr int kOzSliceThreads = 512;
+constexpr int kOzSliceThreads = 256;
 constexpr int kOzSliceWarps = kOzSliceThreads / 32;
 
 template <int kRowContig, int kS>
 __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs sa) {
   const int z = blockIdx.z;
   if (sa.fail_flag[z] && *sa.fail_flag[z]) return;
-  extern __shared__ double tile[];  // [32][kOzSliceStride]
+  extern __shared__ double tile[];  // [kOzSliceRows][kOzSliceStride]
   __shared__ int ex[kOzSliceRows];
   const double* X = sa.X[z];
   const long long ld = sa.ld;
@@ -170,19 +159,20 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
   const long long r0 = (long long)blockIdx.x * kOzSliceRows;
   if (sa.rows_z[z] > 0 && r0 >= sa.rows_z[z]) return;
   // loads: 16 independent 8-byte loads in flight per lane, then the shared-memory stores
-  if (kRowContig) {  // X(r,k) = X[r + k ld]: lanes along r, warps over k
-    constexpr int kStep = kOzSliceWarps * 16;
-    for (int k0 = w; k0 < K; k0 += kStep) {
+  if (kRowContig) {  // X(r,k) = X[r + k ld]: half-warps along r (16 rows = 128 B), k pairs
+    const int rr = l & 15, kh = l >> 4;
+    constexpr int kStep = kOzSliceWarps * 2 * 16;
+    for (int k0 = 2 * w + kh; k0 < K; k0 += kStep) {
       double v[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const int k = k0 + q * kOzSliceWarps;
-        v[q] = k < K ? X[r0 + l + (long long)k * ld] : 0.0;
+        const int k = k0 + q * 2 * kOzSliceWarps;
+        v[q] = k < K ? X[r0 + rr + (long long)k * ld] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const int k = k0 + q * kOzSliceWarps;
-        if (k < K) tile[l * kOzSliceStride + k] = v[q];
+        const int k = k0 + q * 2 * kOzSliceWarps;
+        if (k < K) tile[rr * kOzSliceStride + k] = v[q];
       }
     }
   } else {           // X(r,k) = X[k + r ld]: lanes along k, warps over rows
@@ -215,7 +205,10 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (l == 0) {
       int e = 0;
-      if (mx > 0.0) frexp(mx, &e);
+      if (mx > 0.0) {
+        frexp(mx, &e);                                  // 2^(e-1) <= mx < 2^e
+        if (mx >= pow2i(e) * (509.0 / 512.0)) ++e;      // keeps |X| < 127.25 * 256^(kS-1)
+      }
       ex[r] = e;
       sa.e[z][r0 + r] = e;
     }
@@ -228,9 +221,9 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
   // work item = (row, 16-wide k chunk); lanes on consecutive rows
   for (int item = t; item < kOzSliceRows * (K / 16); item += kOzSliceThreads) {
     const int r = item & (kOzSliceRows - 1), ch = item / kOzSliceRows;
-    // |x| 2^(7 kS - e) < 2^(7 kS) is exact (power-of-two scaling); its truncation holds the
-    // kS base-128 digits the float recurrence (x 2^7, trunc, subtract) would produce.
-    const int sh = 7 * kS - ex[r];
+    // X = rint(x 2^(8 kS - 1 - e)) (exact scaling, one rounding), |X| < 127.25 * 256^(kS-1),
+    // which S balanced digits in [-128, 127] represent exactly (max 127 (256^S - 1) / 255).
+    const int sh = 8 * kS - 1 - ex[r];
     const double sc1 = pow2i(sh > 1000 ? 1000 : sh), sc2 = pow2i(sh > 1000 ? sh - 1000 : 0);
     const double* src = tile + r * kOzSliceStride + ch * 16;
     uint32_t wd[kS][4];
@@ -238,15 +231,12 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
     for (int p = 0; p < kS; ++p) wd[p][0] = wd[p][1] = wd[p][2] = wd[p][3] = 0u;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      const double x = src[c];
-      const unsigned long long u =
-          (unsigned long long)__double2ll_rz(fabs(x) * sc1 * sc2);
-      const bool neg = x < 0.0;
+      long long v = __double2ll_rn((src[c] * sc1) * sc2);
 #pragma unroll
-      for (int p = 0; p < kS; ++p) {
-        const uint32_t d = (uint32_t)(u >> (7 * kS - 7 * (p + 1))) & 127u;
-        const uint32_t byte = (neg ? (0u - d) : d) & 0xFFu;
-        wd[p][c >> 2] |= byte << (8 * (c & 3));
+      for (int p = kS - 1; p >= 0; --p) {  // least significant digit first
+        const long long d = ((v + 128) & 255) - 128;
+        v = (v - d) >> 8;
+        wd[p][c >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (c & 3));
       }
     }
     const int kb = ch >> 1, half = ch & 1;
@@ -260,178 +250,26 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
   }
 }
 
-// C(i,j) = beta C + alpha 2^(ea_i + eb_j) sum_d 2^-7d sum_{p+q=d} (A_p B_q^T)(i,j).
-// MMA structure: for slice p of A, ONE MMA against the concatenation [B_1; ...; B_{9-p}]
-// (kN (9-p) rows, split at 256) written at TMEM column (p-1) kN: product (p, q) then lands
-// at column (p+q-2) kN, i.e. in accumulator d = p + q.  8-12 MMAs per k block instead of 36.
-template <int kN>
-__global__ void __launch_bounds__(OZ_THREADS, OzCfg<kN>::kCtasPerSm) ozgemm_kernel(OzGemmArgs g) {
-  using Cfg = OzCfg<kN>;
-  constexpr int kParts = 128 / kN;
-  const int z = blockIdx.z;
-  if (*g.fail_flag[z]) return;
-  int tm, tn;
-  const int b = blockIdx.x / kParts, part = blockIdx.x % kParts;
-  if (g.lower) {
-    int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
-    while (I * (I + 1) / 2 > b) --I;
-    while ((I + 1) * (I + 2) / 2 <= b) ++I;
-    tm = I;
-    tn = b - I * (I + 1) / 2;
-  } else {
-    tm = b % g.tiles_m;
-    tn = b / g.tiles_m;
-  }
-  if (g.trap && tm < tn) return;
-
-  extern __shared__ __align__(1024) uint8_t oz_smem[];
-  __shared__ __align__(8) uint64_t full_bar[Cfg::kStages], empty_bar[Cfg::kStages], acc_bar;
-  __shared__ uint32_t tmem_base;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kblocks = g.kblocks;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < Cfg::kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    mbar_init(&acc_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base)), "n"(Cfg::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
-
-  const int8_t* Ablk = g.As[z] + (size_t)tm * kblocks * OZ_S * OZ_BLK;
-  const int8_t* Bblk =
-      g.Bs[z] + (size_t)tn * kblocks * OZ_S * OZ_BLK + (size_t)part * (kN * OZ_KB);
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // producer: one 32 KB bulk copy for the A slices, 8 copies for the B row range
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int st = kb % Cfg::kStages;
-        if (kb >= Cfg::kStages) mbar_wait(&empty_bar[st], ((kb / Cfg::kStages) - 1) & 1);
-        uint8_t* sa = oz_smem + (size_t)st * Cfg::kStage;
-        uint8_t* sb = sa + OZ_A_STAGE;
-        mbar_expect_tx(&full_bar[st], Cfg::kStage);
-        bulk_g2s(sa, Ablk + (size_t)kb * OZ_S * OZ_BLK, OZ_A_STAGE, &full_bar[st]);
-        const int8_t* bsrc = Bblk + (size_t)kb * OZ_S * OZ_BLK;
-#pragma unroll
-        for (int q = 0; q < OZ_S; ++q)
-          bulk_g2s(sb + q * (kN * OZ_KB), bsrc + (size_t)q * OZ_BLK, kN * OZ_KB, &full_bar[st]);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int st = kb % Cfg::kStages;
-      mbar_wait(&full_bar[st], (kb / Cfg::kStages) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      if (lane == 0) {
-        const uint32_t sa = smem_u32(oz_smem + (size_t)st * Cfg::kStage);
-        const uint32_t sb = sa + OZ_A_STAGE;
-#pragma unroll
-        for (int p = 1; p <= OZ_S; ++p) {
-          const uint64_t da = sdesc(sa + (p - 1) * OZ_BLK);
-          const int rows = kN * (OZ_S + 1 - p);  // B rows [B_1 .. B_{9-p}]
-          const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
-#pragma unroll
-          for (int r0 = 0; r0 < rows; r0 += 256) {
-            const int nr = rows - r0 < 256 ? rows - r0 : 256;
-            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                                   ((uint32_t)(nr >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-            const uint64_t db = sdesc(sb + r0 * OZ_KB);
-            const uint32_t col = tmem + (uint32_t)((p - 1) * kN + r0);
-            asm volatile(
-                "{ .reg .pred pp; setp.ne.b32 pp, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp; }" ::"r"(col),
-                "l"(da), "l"(db), "r"(idesc), "r"(accum));
-          }
-        }
-        asm volatile(
-            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                smem_u32(&empty_bar[st])));
-      }
-      __syncwarp();
-    }
-    if (lane == 0)
-      asm volatile(
-          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-              smem_u32(&acc_bar)));
-    __syncwarp();
-  } else {
-    // epilogue: thread = one row of the tile (TMEM lane quadrant = warp % 4)
-    const int qd = warp & 3;
-    const int row = qd * 32 + lane;
-    const long long r_glob = (long long)tm * 128 + row;
-    const long long c_glob = (long long)tn * 128 + (long long)part * kN;
-    double* C = g.C[z] + r_glob + c_glob * g.ldc;
-    const int* eb = g.eb[z] + c_glob;
-    const double alpha = g.alpha;
-    const bool acc_c = g.beta != 0.0 && tm >= g.beta0_tm && tn >= g.beta0_tn;
-    const double s_row = alpha * pow2i(g.ea[z][r_glob]);
-    constexpr int kPre = kN == 32 ? 32 : 16;  // C values prefetched before the main loop ends
-    double cpre[kPre];
-#pragma unroll
-    for (int j = 0; j < kPre; ++j) cpre[j] = acc_c ? C[(long long)j * g.ldc] : 0.0;
-    mbar_wait(&acc_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    double acc[kN];
-#pragma unroll
-    for (int c0 = 0; c0 < kN; c0 += 16) {
-      double part[16];
-      oz_combine16<OZ_S>(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, kN, part);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[c0 + j] = part[j];
-    }
-    // C = C + (alpha 2^ea) 2^eb acc: exact power-of-two scalings, one rounding in the add
-#pragma unroll
-    for (int c0 = 0; c0 < kN; c0 += kPre) {
-      double cv[kPre];
-      int ev[kPre];
-#pragma unroll
-      for (int j = 0; j < kPre; ++j) {
-        cv[j] = c0 == 0 ? cpre[j] : (acc_c ? C[(long long)(c0 + j) * g.ldc] : 0.0);
-        ev[j] = eb[c0 + j];
-      }
-#pragma unroll
-      for (int j = 0; j < kPre; ++j)
-        C[(long long)(c0 + j) * g.ldc] = cv[j] + (acc[c0 + j] * s_row) * pow2i(ev[j]);
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(Cfg::kTmemCols));
-}
-
-
-// Persistent variant: one CTA per SM walks the tile list (tile t, t + gridDim.x, ...).
-// The kernel is bound by the shared-memory ingress of the slices (L2 -> SMEM, ~29 B/clk/SM
-// measured), not by the tensor pipe: a 128 x kN tile needs 8 x 32 (128 + kN) bytes per k
-// block for 36 x 128 x kN x 32 MACs, so kN = 64 halves the ingress per MAC of kN = 32.
-//   kN = 32: 5-stage ring of 40 KB, two TMEM accumulator sets (2 x 256 columns): the
-//            epilogue of one tile overlaps the main loop of the next.
-//   kN = 64: 4-stage ring of 48 KB, one accumulator set (512 columns): the producer keeps
-//            streaming the next tile's stages while the epilogue drains TMEM.
-// 8 epilogue warps (two per TMEM lane quadrant, kN / 2 columns each).  Per-tile arithmetic
-// is that of ozgemm_kernel, so every variant gives bit-identical results.
-template <int kN, int kS = OZ_S>
+// Persistent GEMM: one CTA per SM walks the tile list (tile t, t + gridDim.x, ...).
+// The kernel is bound by the ingress of the slices (L2 -> SMEM), not by the tensor pipe: a
+// 128 x kN tile needs S x 32 (128 + kN) bytes per k block for S(S+1)/2 x 128 x kN x 32 MACs,
+// so kN = 64 halves the ingress per MAC of kN = 32.
+//   kN = 32: two TMEM accumulator sets (2 x 32 S columns): the epilogue of one tile overlaps
+//            the main loop of the next.
+//   kN = 64: one accumulator set (64 S columns): the producer keeps streaming the next
+//            tile's stages while the epilogue drains TMEM.
+// The ring takes as many stages as fit in ~220 KB of shared memory.  8 epilogue warps (two
+// per TMEM lane quadrant, kN / 2 columns each).  The per-tile arithmetic does not depend on
+// kN, so both variants give bit-identical results.
+template <int kN, int kS>
 struct OzP {
   static constexpr int kAStage = kS * OZ_BLK;
   static constexpr int kStage = kAStage + kS * kN * OZ_KB;
-  static constexpr int kStages = kN == 32 ? 5 : (kS == 8 ? 4 : 5);
+  static constexpr int kStages = (220 * 1024) / kStage > 8 ? 8 : (220 * 1024) / kStage;
   static constexpr int kSmem = kStages * kStage;
   static constexpr int kAcc = kS * kN;              // TMEM columns per accumulator set
   static constexpr int kSets = kN == 32 ? 2 : 1;
+  static_assert(kSets * kAcc <= 512, "TMEM");
 };
 constexpr int OZP_EPI_WARPS = 8;
 constexpr int OZP_THREADS = 64 + 32 * OZP_EPI_WARPS;
@@ -464,11 +302,16 @@ __device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, long long per_z, lo
   return *g.fail_flag[o.z] == 0;
 }
 
-template <int kN, int kS>
+// kMc = 2: CTA pairs (clusters of 2) own the two 64-column halves of one 128 x 128 tile and
+// share its A stages: each CTA loads half of every A stage and multicasts it to both, so the
+// L2 -> SM traffic per pair is A + 2 B instead of 2 A + 2 B.  A stage is refilled only after
+// BOTH CTAs' MMAs released it (each MMA commit arrives on the empty barriers of the pair).
+template <int kN, int kS, int kMc>
 __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGemmArgs g,
                                                                            long long per_z,
                                                                            long long total) {
   using Cfg = OzP<kN, kS>;
+  static_assert(kMc == 1 || (kMc == 2 && kN == 64), "pairs own both halves of a 128-wide tile");
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   __shared__ __align__(8) uint64_t full_bar[Cfg::kStages], empty_bar[Cfg::kStages];
   __shared__ __align__(8) uint64_t acc_full[Cfg::kSets], acc_empty[Cfg::kSets];
@@ -479,7 +322,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kMc);
     }
     for (int b = 0; b < Cfg::kSets; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -494,8 +337,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (kMc > 1) cluster_sync();  // the peer's barriers exist before any multicast / remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  const uint32_t rank = kMc > 1 ? cluster_rank() : 0u;
 
   if (warp == 0) {
     if (lane == 0) {  // producer
@@ -518,7 +363,13 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
             continue;
           }
           mbar_expect_tx(&full_bar[st], Cfg::kStage);
-          bulk_g2s(sa, Ablk + (size_t)kb * kS * OZ_BLK, Cfg::kAStage, &full_bar[st]);
+          if (kMc > 1) {  // my half of the A stage, to both CTAs of the pair
+            constexpr uint32_t kHalf = Cfg::kAStage / 2;
+            bulk_g2s_mc(sa + rank * kHalf, Ablk + (size_t)kb * kS * OZ_BLK + rank * kHalf, kHalf,
+                        &full_bar[st], (uint16_t)0x3);
+          } else {
+            bulk_g2s(sa, Ablk + (size_t)kb * kS * OZ_BLK, Cfg::kAStage, &full_bar[st]);
+          }
           const int8_t* bsrc = Bblk + (size_t)kb * kS * OZ_BLK;
 #pragma unroll
           for (int q = 0; q < kS; ++q)
@@ -530,6 +381,9 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
     __syncwarp();
   } else if (warp == 1) {  // MMA issuer
     long long gk = 0, local = 0;
+    int st = 0;
+    uint32_t ph = 0;
+    const uint32_t smem_base = smem_u32(oz_smem);
     long long c_start = clock64(), c_full = 0, c_acc = 0, g_start = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
     for (long long t = blockIdx.x; t < total; t += gridDim.x) {
@@ -539,45 +393,56 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       const long long use = local / Cfg::kSets;
       {
         const long long c0 = clock64();
-        if (use >= 1) mbar_wait(&acc_empty[ab], (uint32_t)((use - 1) & 1));
+        if (use >= 1 && g.diag_mode != 7) mbar_wait(&acc_empty[ab], (uint32_t)((use - 1) & 1));
         c_acc += clock64() - c0;
       }
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t acc = tmem + (uint32_t)(ab * Cfg::kAcc);
+      // The whole warp walks the k blocks (uniform values, uniform registers); one elected
+      // lane issues each MMA / commit.  Descriptors: stage base + constant offsets (the
+      // address field is addr >> 4 in the low 14 bits).
       for (int kb = 0; kb < kblocks; ++kb, ++gk) {
-        const int st = (int)(gk % Cfg::kStages);
         {
           const long long c0 = clock64();
-          mbar_wait(&full_bar[st], (uint32_t)((gk / Cfg::kStages) & 1));
+          mbar_wait(&full_bar[st], ph);
           c_full += clock64() - c0;
         }
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(oz_smem + (size_t)st * Cfg::kStage);
-          const uint32_t sb = sa + Cfg::kAStage;
-#pragma unroll
-          for (int p = 1; p <= kS; ++p) {
-            if (g.diag_mode == 1 && !(kb == 0 && p == 1)) continue;
-            const int rows = kN * (kS + 1 - p);  // B rows [B_1 .. B_{kS+1-p}]
-            const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
-#pragma unroll
-            for (int r0 = 0; r0 < rows; r0 += 256) {
-              const int nr = rows - r0 < 256 ? rows - r0 : 256;
-              const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                                     ((uint32_t)(nr >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-              asm volatile(
-                  "{ .reg .pred pp; setp.ne.b32 pp, %4, 0;\n"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp; }" ::"r"(
-                      acc + (uint32_t)((p - 1) * kN + r0)),
-                  "l"(sdesc(sa + (p - 1) * OZ_BLK)), "l"(sdesc(sb + r0 * OZ_KB)), "r"(idesc),
-                  "r"(accum));
-            }
-          }
-          asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                  smem_u32(&empty_bar[st])));
-        }
         __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t da0 = sdesc(smem_base + (uint32_t)st * Cfg::kStage);
+        const uint64_t db0 = da0 + (uint64_t)(Cfg::kAStage >> 4);
+#pragma unroll
+        for (int p = 1; p <= kS; ++p) {
+          if (g.diag_mode == 1 && !(kb == 0 && p == 1)) continue;
+          const int rows = kN * (kS + 1 - p);  // B rows [B_1 .. B_{kS+1-p}]
+          const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
+#pragma unroll
+          for (int r0 = 0; r0 < rows; r0 += 256) {
+            const int nr = rows - r0 < 256 ? rows - r0 : 256;
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                   ((uint32_t)(nr >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            asm volatile(
+                "{ .reg .pred pp, pe; setp.ne.b32 pp, %4, 0; elect.sync _|pe, 0xffffffff;\n"
+                "@pe tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp; }" ::"r"(
+                    acc + (uint32_t)((p - 1) * kN + r0)),
+                "l"(da0 + (uint64_t)(((p - 1) * OZ_BLK) >> 4)),
+                "l"(db0 + (uint64_t)((r0 * OZ_KB) >> 4)), "r"(idesc), "r"(accum));
+          }
+        }
+        if (kMc > 1)  // the stage is free once both CTAs' MMAs have read it
+          asm volatile(
+              "{ .reg .pred pe; elect.sync _|pe, 0xffffffff;\n"
+              "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
+              "cluster.b64 [%0], %1; }" ::"r"(smem_u32(&empty_bar[st])), "h"((uint16_t)0x3));
+        else
+          asm volatile(
+              "{ .reg .pred pe; elect.sync _|pe, 0xffffffff;\n"
+              "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
+              ::"r"(smem_u32(&empty_bar[st])));
+        if (++st == Cfg::kStages) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
       if (lane == 0)
         asm volatile(
@@ -619,6 +484,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
 #pragma unroll
       for (int j = 0; j < kPre; ++j) cv[j] = acc_c ? __ldcg(C + (long long)j * g.ldc) : 0.0;
       const double s_row = g.alpha * pow2i(g.ea[o.z][r_glob]);
+      if (g.diag_mode == 7) {  // diagnostics: no accumulator handoff at all
+        ++local;
+        continue;
+      }
       mbar_wait(&acc_full[ab], (uint32_t)(use & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
       double acc[kCols];
@@ -660,86 +529,104 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (kMc > 1) cluster_sync();  // no CTA leaves while its peer may still signal / fill it
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 int g_num_sms = 148;
 
+template <int kN, int kS, int kMc>
+static cudaError_t oz_attr() {
+  cudaError_t e = cudaFuncSetAttribute(ozgemm_persistent_kernel<kN, kS, kMc>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       OzP<kN, kS>::kSmem);
+  if (e != cudaSuccess || kMc == 1) return e;
+  return cudaFuncSetAttribute(ozgemm_persistent_kernel<kN, kS, kMc>,
+                              cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+}
+
 cudaError_t init_ozaki_attributes() {
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<32, 8>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        OzP<32, 8>::kSmem);
-  if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<64, 8>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, OzP<64, 8>::kSmem);
-  if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(ozgemm_persistent_kernel<64, 7>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, OzP<64, 7>::kSmem);
-  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaSuccess;
+  if ((e = oz_attr<64, 7, 2>()) != cudaSuccess) return e;
+  if ((e = oz_attr<64, 6, 2>()) != cudaSuccess) return e;
+  if ((e = oz_attr<64, 7, 1>()) != cudaSuccess) return e;
+  if ((e = oz_attr<64, 6, 1>()) != cudaSuccess) return e;
+  if ((e = oz_attr<32, 7, 1>()) != cudaSuccess) return e;
+  if ((e = oz_attr<32, 6, 1>()) != cudaSuccess) return e;
 #define MLE_SLICE_ATTR(RC, S)                                                              \
   e = cudaFuncSetAttribute(oz_slice_kernel<RC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            kOzSliceSmem);                                                  \
   if (e != cudaSuccess) return e;
-  MLE_SLICE_ATTR(0, 8)
-  MLE_SLICE_ATTR(1, 8)
   MLE_SLICE_ATTR(0, 7)
   MLE_SLICE_ATTR(1, 7)
+  MLE_SLICE_ATTR(0, 6)
+  MLE_SLICE_ATTR(1, 6)
 #undef MLE_SLICE_ATTR
-  e = cudaFuncSetAttribute(ozgemm_kernel<64>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       OzCfg<64>::kSmem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(ozgemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              OzCfg<32>::kSmem);
+  return cudaSuccess;
 }
 
 cudaError_t launch_oz_slice(const OzSliceArgs& a, int rows, bool row_contig, int batch,
                             cudaStream_t s) {
   if (a.K > kOzSliceMaxK || a.K % OZ_KB || rows % 128) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)(rows / kOzSliceRows), 1, (unsigned)batch);
-  const bool seven = a.nslices == 7;
-  if (row_contig && seven)
-    oz_slice_kernel<1, 7><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+  const bool six = oz_nslices(a.nslices) == 6;
+  if (row_contig && six)
+    oz_slice_kernel<1, 6><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   else if (row_contig)
-    oz_slice_kernel<1, 8><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
-  else if (seven)
-    oz_slice_kernel<0, 7><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+    oz_slice_kernel<1, 7><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+  else if (six)
+    oz_slice_kernel<0, 6><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   else
-    oz_slice_kernel<0, 8><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
+    oz_slice_kernel<0, 7><<<grid, kOzSliceThreads, kOzSliceSmem, s>>>(a);
   return cudaGetLastError();
 }
 
+template <int kN, int kS, int kMc>
+static cudaError_t oz_launch(const OzGemmArgs& g, long long per_z, long long total,
+                             long long grid, cudaStream_t s) {
+  if (kMc == 1) {
+    ozgemm_persistent_kernel<kN, kS, kMc><<<(unsigned)grid, OZP_THREADS, OzP<kN, kS>::kSmem,
+                                            s>>>(g, per_z, total);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(OZP_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = OzP<kN, kS>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kMc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ozgemm_persistent_kernel<kN, kS, kMc>, g, per_z, total);
+}
+
+// n_tile: 0 -> 128 x 64 tiles in CTA pairs sharing A (default), 1 -> 128 x 32 tiles,
+// 2 -> 128 x 64 tiles without pairing (A/B comparisons).  All give bit-identical results.
 cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile) {
   const long long tiles =
       g.lower ? (long long)g.tiles_m * (g.tiles_m + 1) / 2 : (long long)g.tiles_m * g.tiles_n;
   if (tiles <= 0) return cudaSuccess;
-  if (n_tile == 0 || n_tile == 1) {  // persistent: 0 -> 128 x 64 tiles, 1 -> 128 x 32
-    const int kn = n_tile == 0 ? 64 : 32;
-    const long long per_z = tiles * (128 / kn), total = per_z * batch;
-    const long long cap = g.max_ctas > 0 ? std::min(g.max_ctas, g_num_sms) : g_num_sms;
-    const long long grid = std::min<long long>(total, cap);
-    if (kn == 64 && g.nslices == 7)
-      ozgemm_persistent_kernel<64, 7><<<(unsigned)grid, OZP_THREADS, OzP<64, 7>::kSmem, s>>>(
-          g, per_z, total);
-    else if (kn == 64)
-      ozgemm_persistent_kernel<64, 8><<<(unsigned)grid, OZP_THREADS, OzP<64, 8>::kSmem, s>>>(
-          g, per_z, total);
-    else
-      ozgemm_persistent_kernel<32, 8><<<(unsigned)grid, OZP_THREADS, OzP<32, 8>::kSmem, s>>>(
-          g, per_z, total);
-  } else if (n_tile == 64) {
-    ozgemm_kernel<64><<<dim3((unsigned)(2 * tiles), 1, (unsigned)batch), OZ_THREADS,
-                        OzCfg<64>::kSmem, s>>>(g);
-  } else {
-    ozgemm_kernel<32><<<dim3((unsigned)(4 * tiles), 1, (unsigned)batch), OZ_THREADS,
-                        OzCfg<32>::kSmem, s>>>(g);
+  if (n_tile < 0 || n_tile > 2) return cudaErrorInvalidValue;
+  const int kn = n_tile == 1 ? 32 : 64;
+  const long long per_z = tiles * (128 / kn), total = per_z * batch;
+  const long long cap = g.max_ctas > 0 ? std::min(g.max_ctas, g_num_sms) : g_num_sms;
+  long long grid = std::min<long long>(total, cap);
+  const bool six = oz_nslices(g.nslices) == 6;
+  if (n_tile == 0) {
+    grid &= ~1LL;  // whole pairs (total is even: two halves per 128-wide tile)
+    if (grid < 2) grid = 2;
+    return (six ? oz_launch<64, 6, 2> : oz_launch<64, 7, 2>)(g, per_z, total, grid, s);
   }
-  return cudaGetLastError();
+  if (n_tile == 2) return (six ? oz_launch<64, 6, 1> : oz_launch<64, 7, 1>)(g, per_z, total, grid, s);
+  return (six ? oz_launch<32, 6, 1> : oz_launch<32, 7, 1>)(g, per_z, total, grid, s);
 }
 
 }  // namespace mle

@@ -14,7 +14,7 @@
 
 using namespace mle;
 static int g_ntile = 0;
-static int g_slices = 8;
+static int g_slices = 7;
 
 struct Case {
   const char* name;
@@ -95,8 +95,8 @@ static double run_case(const Case& cs, int batch, int reps) {
   std::vector<double> C1(C.size()), C2(C.size());
   CK(cudaMemcpy(C1.data(), dC1, C.size() * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(C2.data(), dC2, C.size() * 8, cudaMemcpyDeviceToHost));
-  for (int other : {0, 1, 32, 64}) {  // every kernel variant must give bit-identical results
-    if (other == g_ntile || g_slices != 8) continue;
+  for (int other : {0, 1, 2}) {  // every kernel variant must give bit-identical results
+    if (other == g_ntile) continue;
     CK(cudaMemcpy(dC2, C.data(), C.size() * 8, cudaMemcpyHostToDevice));
     CK(launch_ozgemm(o, 1, 0, other));
     CK(cudaDeviceSynchronize());
@@ -182,7 +182,7 @@ static double run_case(const Case& cs, int batch, int reps) {
     long long* dd;
     CK(cudaMalloc(&dd, 8 * sizeof(long long)));
     o.diag_out = dd;
-    for (int mode : {0, 5, 6}) {
+    for (int mode : {0, 5, 6, 7}) {
       o.diag_mode = mode;
       launch_ozgemm(o, batch, 0, g_ntile);
       long long h[8];
@@ -233,5 +233,5 @@ int main(int argc, char** argv) {
   run_case(cases[0], 5, 10);
   run_case(cases[2], 5, 10);
   printf("worst ozaki err/scale %.2e\n", worst);
-  return worst < (g_slices == 8 ? 1e-14 : 1e-13) ? 0 : 1;
+  return worst < (g_slices == 7 ? 1e-14 : 1e-13) ? 0 : 1;
 }

@@ -97,7 +97,7 @@ void run(int sms) {
 // The ozgemm_persistent_kernel<64> per-k-block MMA sequence: for p = 1..8 one MMA over the
 // B rows [B_1 .. B_{9-p}] (64 (9 - p) rows, split at 256) at TMEM column (p - 1) 64.
 // kCommit: tcgen05.commit to an mbarrier after every k block (as the kernel does).
-template <int kCommit, int kVaryA>
+template <int kCommit, int kVaryA, int kS = 8, int kSplit = 256>
 __global__ void __launch_bounds__(128, 1) umma_seq(int kblocks, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];  // A 8 x 4 KB + B 16 KB
   __shared__ __align__(8) uint64_t bar;
@@ -124,12 +124,16 @@ __global__ void __launch_bounds__(128, 1) umma_seq(int kblocks, long long* cycle
     const long long t0 = clock64();
     for (int kb = 0; kb < kblocks; ++kb) {
 #pragma unroll
-      for (int p = 1; p <= 8; ++p) {
-        const int rows = 64 * (9 - p);
+      for (int p = 1; p <= kS; ++p) {
+        const int rows = 64 * (kS + 1 - p);
         const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
+        // kSplit > 0: pieces of at most kSplit rows; kSplit < 0: |kSplit| equal pieces
+        const int pieces = kSplit > 0 ? (rows + kSplit - 1) / kSplit
+                                      : (rows > 256 ? -kSplit : 1);
+        const int step = ((rows / pieces + 15) / 16) * 16;
 #pragma unroll
-        for (int r0 = 0; r0 < rows; r0 += 256) {
-          const int nr = rows - r0 < 256 ? rows - r0 : 256;
+        for (int r0 = 0; r0 < rows; r0 += step) {
+          const int nr = rows - r0 < step ? rows - r0 : step;
           const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nr >> 3) << 17) |
                                  ((uint32_t)(128 >> 4) << 24);
           asm volatile("{ .reg .pred pp; setp.ne.b32 pp, %4, 0;\n"
@@ -158,28 +162,31 @@ __global__ void __launch_bounds__(128, 1) umma_seq(int kblocks, long long* cycle
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int kCommit, int kVaryA>
+template <int kCommit, int kVaryA, int kS = 8, int kSplit = 256>
 void run_seq(int sms, int kb = 2000) {
   long long* d;
   cudaMalloc(&d, sizeof(long long) * sms);
   const int smem = 32768 + 16384;
-  cudaFuncSetAttribute(umma_seq<kCommit, kVaryA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  umma_seq<kCommit, kVaryA><<<sms, 128, smem>>>(10, d);
+  cudaFuncSetAttribute(umma_seq<kCommit, kVaryA, kS, kSplit>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  umma_seq<kCommit, kVaryA, kS, kSplit><<<sms, 128, smem>>>(10, d);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  umma_seq<kCommit, kVaryA><<<sms, 128, smem>>>(kb, d);
+  umma_seq<kCommit, kVaryA, kS, kSplit><<<sms, 128, smem>>>(kb, d);
   cudaEventRecord(e1);
   cudaDeviceSynchronize();
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   long long h[148];
   cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
-  printf("ozgemm<64> k-block sequence (commit %d, vary A %d, %d k blocks, %.1f ms): %.0f "
-         "cycles per k block (ideal 1152), effective SM clock %.0f MHz, %.0f int8 TOPS (%s)\n",
-         kCommit, kVaryA, kb, ms, (double)h[0] / kb, (double)h[0] / (ms * 1e3),
-         2.0 * 36 * 128 * 64 * 32 * (double)kb * sms / (ms * 1e-3) / 1e12,
+  printf("ozgemm<64> k-block sequence S=%d split %d (commit %d, vary A %d, %d k blocks, %.1f ms):"
+         " %.0f cycles per k block (compute bound %d), effective SM clock %.0f MHz, %.0f int8 "
+         "TOPS (%s)\n", kS, kSplit,
+         kCommit, kVaryA, kb, ms, (double)h[0] / kb, 32 * kS * (kS + 1) / 2,
+         (double)h[0] / (ms * 1e3),
+         2.0 * (kS * (kS + 1) / 2) * 128 * 64 * 32 * (double)kb * sms / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -197,7 +204,7 @@ __device__ __forceinline__ void marrive(uint64_t* bar) {
 
 // Kernel-shaped MMA loop: producer warp (no data, arrives full after empty), MMA warp with the
 // 4-stage full/empty ring, optional per-tile accumulator handshake with 8 epilogue warps.
-template <int kTileSync, int kRandom = 0>
+template <int kTileSync, int kRandom = 0, int kS = 8>
 __global__ void __launch_bounds__(320, 1) umma_ring(int tiles, int kblocks, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];  // 4 stages x 48 KB
   __shared__ __align__(8) uint64_t full[4], empty[4], accf, acce;
@@ -256,8 +263,8 @@ __global__ void __launch_bounds__(320, 1) umma_ring(int tiles, int kblocks, long
         if (lane == 0) {
           const uint32_t sa = smem_u32(sm + st * 49152), sb = sa + 32768;
 #pragma unroll
-          for (int p = 1; p <= 8; ++p) {
-            const int rows = 64 * (9 - p);
+          for (int p = 1; p <= kS; ++p) {
+            const int rows = 64 * (kS + 1 - p);
             const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
 #pragma unroll
             for (int r0 = 0; r0 < rows; r0 += 256) {
@@ -300,29 +307,42 @@ __global__ void __launch_bounds__(320, 1) umma_ring(int tiles, int kblocks, long
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int kTileSync, int kRandom = 0>
+template <int kTileSync, int kRandom = 0, int kS = 8>
 void run_ring(int sms, int tiles, int kblocks) {
   long long* d;
   cudaMalloc(&d, sizeof(long long) * 296);
   const int smem = 4 * 49152;
-  cudaFuncSetAttribute(umma_ring<kTileSync, kRandom>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(umma_ring<kTileSync, kRandom, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        smem);
-  umma_ring<kTileSync, kRandom><<<sms, 320, smem>>>(2, kblocks, d);
-  umma_ring<kTileSync, kRandom><<<sms, 320, smem>>>(tiles, kblocks, d);
+  umma_ring<kTileSync, kRandom, kS><<<sms, 320, smem>>>(2, kblocks, d);
+  umma_ring<kTileSync, kRandom, kS><<<sms, 320, smem>>>(tiles, kblocks, d);
   cudaDeviceSynchronize();
   long long h[296];
   cudaMemcpy(h, d, sizeof(long long) * 296, cudaMemcpyDeviceToHost);
-  printf("ring (tile sync %d, random %d, %d tiles x %d k blocks): %.0f cycles per k block, "
-         "%.1f ms, clock %.0f MHz, %.0f int8 TOPS (%s)\n", kTileSync, kRandom,
+  printf("ring S=%d (tile sync %d, random %d, %d tiles x %d k blocks): %.0f cycles per k block, "
+         "%.1f ms, clock %.0f MHz, %.0f int8 TOPS (%s)\n", kS, kTileSync, kRandom,
          tiles, kblocks, (double)h[0] / ((double)tiles * kblocks), h[148] * 1e-6,
          (double)h[0] / (h[148] * 1e-3), 2.0 * 36 * 128 * 64 * 32 * (double)tiles * kblocks * sms /
          (h[148] * 1e-9) / 1e12, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) {  // the S = 7 / 6 sequences, split variants
+    run_seq<1, 1, 8, 256>(sms);
+    run_seq<1, 1, 7, 256>(sms);
+    run_seq<1, 1, 7, 128>(sms);
+    run_seq<1, 1, 7, -2>(sms);
+    run_seq<1, 1, 6, 256>(sms);
+    run_seq<1, 1, 6, -2>(sms);
+    run_ring<1, 0, 7>(sms, 2000, 16);
+    run_ring<0, 0, 7>(sms, 2000, 16);
+    run_ring<1, 2, 7>(sms, 2000, 16);
+    run_ring<1, 0, 8>(sms, 2000, 16);
+    return 0;
+  }
   run<32, 0>(sms);
   run<64, 0>(sms);
   run<128, 0>(sms);
