@@ -343,11 +343,12 @@ def ours_arm(args, rank, world, local_rank):
             "bound": "tensor", "unit": "TFLOP/s", "achieved": kern["ozgemm_int8_tops"],
             "peak": int8_peak, "frac": kern["ozgemm_int8_tops"] / int8_peak,
             "traffic": ncu_traffic["dram_bytes"] if ncu_traffic else None,
-            "kernel": "ozgemm_kernel<32> (Ozaki FP64 trailing-update GEMM on tcgen05.mma "
-                      "kind::i8): int8 tensor ops = 36 slice products x 2 x 128 x 128 x K per "
-                      "tile, summed over every launch of a batched eval_all of the 5 replicas, "
-                      "/ the sum of the launches' CUDA-event durations (profiling pass, one "
-                      "stream)",
+            "kernel": "ozgemm_persistent_kernel<64, 7, 2> (Ozaki FP64 trailing-update GEMM on "
+                      "tcgen05.mma kind::i8, 128x64 tiles in CTA pairs sharing A): int8 tensor "
+                      "ops = 28 slice products (7 balanced base-256 slices) x 2 x 128 x 128 x K "
+                      "per 128x128 tile, summed over every launch of a batched eval_all of the 5 "
+                      "replicas, / the sum of the launches' CUDA-event durations (profiling "
+                      "pass, one stream)",
             "fp64_equiv_tflops": kern["ozgemm_fp64_equiv_tflops"],
             "int8_pipe_microbench_tops": INT8_PIPE_TOPS,
             "frac_of_int8_pipe_microbench": kern["ozgemm_int8_tops"] / INT8_PIPE_TOPS,

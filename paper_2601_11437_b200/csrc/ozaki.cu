@@ -223,20 +223,32 @@ __global__ void __launch_bounds__(kOzSliceThreads) oz_slice_kernel(OzSliceArgs s
     const int r = item & (kOzSliceRows - 1), ch = item / kOzSliceRows;
     // X = rint(x 2^(8 kS - 1 - e)) (exact scaling, one rounding), |X| < 127.25 * 256^(kS-1),
     // which S balanced digits in [-128, 127] represent exactly (max 127 (256^S - 1) / 255).
+    // Excess-128 trick: with c = 128 (1 + 256 + ... + 256^(S-1)), Y = X + c lies in
+    // [0, 256^S) and its plain base-256 digits are the balanced digits + 128, so slice byte
+    // = byte(Y) ^ 0x80.  Bytes are gathered four elements at a time with byte permutes.
     const int sh = 8 * kS - 1 - ex[r];
     const double sc1 = pow2i(sh > 1000 ? 1000 : sh), sc2 = pow2i(sh > 1000 ? sh - 1000 : 0);
+    constexpr unsigned long long kExcess = 0x8080808080808080ull >> (8 * (8 - kS));
     const double* src = tile + r * kOzSliceStride + ch * 16;
-    uint32_t wd[kS][4];
-#pragma unroll
-    for (int p = 0; p < kS; ++p) wd[p][0] = wd[p][1] = wd[p][2] = wd[p][3] = 0u;
+    uint32_t lo[16], hi[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      long long v = __double2ll_rn((src[c] * sc1) * sc2);
+      const unsigned long long y =
+          (unsigned long long)__double2ll_rn((src[c] * sc1) * sc2) + kExcess;
+      lo[c] = (uint32_t)y;
+      hi[c] = (uint32_t)(y >> 32);
+    }
+    uint32_t wd[kS][4];
 #pragma unroll
-      for (int p = kS - 1; p >= 0; --p) {  // least significant digit first
-        const long long d = ((v + 128) & 255) - 128;
-        v = (v - d) >> 8;
-        wd[p][c >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (c & 3));
+    for (int p = 0; p < kS; ++p) {  // slice p = digit of weight 256^(kS - 1 - p)
+      const int bp = kS - 1 - p;     // its byte in Y
+      const unsigned sel = (unsigned)((bp & 3) | (((bp & 3) + 4) << 4));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t* w = bp < 4 ? lo : hi;
+        const uint32_t t01 = __byte_perm(w[4 * q], w[4 * q + 1], sel);
+        const uint32_t t23 = __byte_perm(w[4 * q + 2], w[4 * q + 3], sel);
+        wd[p][q] = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
       }
     }
     const int kb = ch >> 1, half = ch & 1;
