@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import threading
 
 import numpy as np
@@ -185,17 +186,66 @@ class LockstepStats:
                     "gpu_gap_ms": 0.0, "spec_wait_ms": 0.0}
 
 
-def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None):
+def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None,
+             groups=None):
     """Run one Fisher-BT fit per dataset concurrently with lock-step batched evaluation.
 
-    Every fit is the request generator ``fisher_bt_gen`` (the unchanged Algorithm 1); one host
-    thread collects the pending request of every live fit and answers them with ONE batched
-    engine pass (``mle_eval_batch``), so no thread hand-offs sit between GPU passes.  Alignment
-    policy as in :class:`BatchCoordinator`: while some fits wait on a loglik and others on an
-    eval_all, only the logliks run.  Counters, -inf mapping and exceptions per fit are those of
-    :class:`~paper_2601_11437_b200.fisher_bt.LikelihoodObjective`; each fit is bit-identical to
-    running it alone.  Returns the list of :class:`OptResult` (same order as ``datasets``).
+    Every fit is the request generator ``fisher_bt_gen`` (the unchanged Algorithm 1); a host
+    thread collects the pending request of every live fit of its group and answers them with
+    ONE batched engine pass (``mle_eval_batch``), so no thread hand-offs sit between GPU passes.
+    Alignment policy as in :class:`BatchCoordinator`: while some fits wait on a loglik and
+    others on an eval_all, only the logliks run.  Counters, -inf mapping and exceptions per fit
+    are those of :class:`~paper_2601_11437_b200.fisher_bt.LikelihoodObjective`; each fit is
+    bit-identical to running it alone.  Returns the list of :class:`OptResult` (same order as
+    ``datasets``).
+
+    ``groups``: the fits are split (interleaved) into this many lock-step groups, each driven
+    by its own host thread on disjoint contexts, so one group's latency-bound Cholesky overlaps
+    the other's tensor-core solves on the GPU.  Default: 2 for four or more fits (env
+    ``MLE_FIT_GROUPS`` overrides), else 1.
     """
+    n = len(datasets)
+    if groups is None:
+        env = os.environ.get("MLE_FIT_GROUPS")
+        groups = int(env) if env else (2 if n >= 4 else 1)
+    groups = max(1, min(int(groups), n)) if n else 1
+    if groups == 1:
+        return _fit_group(datasets, cfg, objectives_out, coordinator_out)
+    parts = [list(range(g, n, groups)) for g in range(groups)]
+    res = [None] * groups
+    objs = [[] for _ in range(groups)]
+    stats = [[] for _ in range(groups)]
+    errors = []
+
+    def work(g):
+        try:
+            res[g] = _fit_group([datasets[i] for i in parts[g]], cfg, objs[g], stats[g])
+        except BaseException as exc:  # re-raised in the caller's thread
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(g,)) for g in range(groups)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    results = [None] * n
+    counters = [None] * n
+    for g, idx in enumerate(parts):
+        for j, i in enumerate(idx):
+            results[i] = res[g][j]
+            counters[i] = objs[g][j]
+    if objectives_out is not None:
+        objectives_out.extend(counters)
+    if coordinator_out is not None:
+        for st in stats:
+            coordinator_out.extend(st)
+    return results
+
+
+def _fit_group(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None):
+    """One lock-step group of :func:`fit_many`, driven by the calling thread."""
     from .fisher_bt import EVAL_ALL, LOGLIK, fisher_bt_gen
 
     stats = LockstepStats()

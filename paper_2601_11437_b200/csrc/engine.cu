@@ -44,15 +44,15 @@ namespace {
 thread_local std::string g_last_error;
 std::mutex g_init_mutex;
 std::vector<int> g_device_ready;
-// GPU idle gap between consecutive passes on a device (diagnostic, kernel-stats slot 8):
-// end-of-pass events alternate between two slots per device.
+// GPU idle gap between consecutive passes led by one context (diagnostic, kernel-stats slot
+// 8): end-of-pass events alternate between two slots.  Per context, so host threads driving
+// disjoint contexts (fit_many groups) never share one.
 struct PassClock {
   cudaEvent_t end[2] = {nullptr, nullptr};
   cudaEvent_t start = nullptr;
   cudaEvent_t pre = nullptr;  // before the pass waits on pending speculation
   long long passes = 0;
 };
-std::vector<PassClock> g_pass_clock;
 const double kLog2Pi = 1.8378770664093453;  // log(2 pi), likelihood.py:38
 constexpr int kOuter = 4;                   // outer block = 4 x 128 columns
 constexpr int kResults = 13;                // loglik, grad[3], fisher[9]
@@ -306,6 +306,7 @@ struct mle_ctx {
   // dSigma/dnu and the W_b slices on the aux stream (overlapping the latency-bound
   // Cholesky), because Fisher-BT follows an accepted loglik(theta) with eval_all(theta).
   // spec_ready: sa / sn / wsl hold that work for spec_theta (valid while the factor is).
+  PassClock pass_clock;           // led passes (diagnostic gap clock)
   bool spec_ready = false;
   bool spec_pending = false;      // spec_done not yet waited for by a later pass
   double spec_theta[3] = {0, 0, 0};
@@ -1142,11 +1143,8 @@ int run_chunk(Item* items, int m) {
   if (lookahead) run.s3 = lead->inner;
   if (lead->kprof) run.prof = lead;
   cudaStream_t aux = lead->kprof ? s : lead->aux;  // profiling: everything serialised
-  PassClock* pc = nullptr;
+  PassClock* pc = &lead->pass_clock;
   {
-    std::lock_guard<std::mutex> lock(g_init_mutex);
-    if ((int)g_pass_clock.size() <= lead->device) g_pass_clock.resize(lead->device + 1);
-    pc = &g_pass_clock[lead->device];
     if (!pc->start) {
       CUDA_TRY(cudaEventCreate(&pc->start));
       CUDA_TRY(cudaEventCreate(&pc->pre));
@@ -1663,6 +1661,9 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->smat);
   dfree(c->linv);
   dfree(c->fail_flag);
+  for (cudaEvent_t e : {c->pass_clock.start, c->pass_clock.pre, c->pass_clock.end[0],
+                        c->pass_clock.end[1]})
+    if (e) cudaEventDestroy(e);
   dfree(c->fail_idx);
   dfree(c->partials);
   dfree(c->out);

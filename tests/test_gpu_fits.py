@@ -50,7 +50,12 @@ def test_batched_replicas_match_serial_and_golden(gpu):
     data = [gpu.SpatialDataset(*config_data("config2", s)) for s in seeds]
     serial = [gpu.fisher_bt(d, cfg) for d in data]
     coords = []
-    batched = gpu.fit_many(data, cfg, coordinator_out=coords)
+    batched = gpu.fit_many(data, cfg, coordinator_out=coords, groups=1)
+    grouped = gpu.fit_many(data, cfg, groups=2)  # two lock-step groups on two host threads
+    for a, b in zip(batched, grouped):
+        np.testing.assert_array_equal(a.theta_hat.as_array(), b.theta_hat.as_array())
+        np.testing.assert_array_equal(a.fisher_at_hat, b.fisher_at_hat)
+        assert (a.grad_calls, a.loglik_calls) == (b.grad_calls, b.loglik_calls)
     for s, a, b in zip(seeds, serial, batched):
         np.testing.assert_array_equal(a.theta_hat.as_array(), b.theta_hat.as_array())
         np.testing.assert_array_equal(a.fisher_at_hat, b.fisher_at_hat)
