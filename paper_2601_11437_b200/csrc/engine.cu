@@ -193,6 +193,7 @@ int ensure_device(int device) {
     mle_fill_u_tables(u.data(), du.data());
     CUDA_TRY(upload_u_tables(u.data(), du.data()));
     CUDA_TRY(init_kernel_attributes());
+    CUDA_TRY(init_small_gemm_attributes());
     CUDA_TRY(init_diag_attributes());
     CUDA_TRY(init_ozaki_attributes());
     g_device_ready[device] = 1;
@@ -458,6 +459,11 @@ struct Launcher {
     return MLE_OK;
   }
   int gemm(const GemmArgs& g, BLayout bl, int batch) { return gemm(g, bl, batch, s); }
+  int gemm_small(const GemmArgs& g, int batch, cudaStream_t st, int rows_only) {
+    launches += 1;
+    CUDA_TRY(launch_gemm_small(g, batch, st, rows_only));
+    return MLE_OK;
+  }
   // kernel profiling: event pair per launch (kind 0 ozgemm, 1 slicing) + algorithmic work
   mle_ctx* prof = nullptr;
   std::vector<int> pkind;
@@ -588,7 +594,7 @@ struct Launcher {
       const int rem = Nt - k - 1;
       if (rem == 0) break;
       const int wcols = b1 - k - 1;  // remaining tile columns of this outer block
-      auto panel_gemm = [&](int row_tiles, int row_off, cudaStream_t st) {
+      auto panel_gemm = [&](int row_tiles, int row_off, cudaStream_t st, bool small = false) {
         // panel rows [k+1+row_off, k+1+row_off+row_tiles) <- panel * Linv_k^T, in place
         // (BN = 128 covers the whole panel width)
         GemmArgs g = gemm_base();
@@ -601,11 +607,11 @@ struct Launcher {
         }
         g.lda = ld; g.ldb = kNB; g.ldc = ld;
         g.tiles_m = row_tiles; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
-        return gemm(g, kBNK, m, st);
+        return small ? gemm_small(g, m, st, 1) : gemm(g, kBNK, m, st);
       };
       // A[r0+.., c0+..] -= P[r0..] P[c0..]^T over tile rows/cols of this outer block
       auto update = [&](int row_off, int row_tiles, int col_off, int col_tiles, bool trap,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool small = false) {
         GemmArgs t = gemm_base();
         for (int b = 0; b < m; ++b) {
           double* panel = mats[b] + (k0 + kNB) + k0 * ld;
@@ -618,7 +624,7 @@ struct Launcher {
         t.lda = ld; t.ldb = ld; t.ldc = ld;
         t.tiles_m = row_tiles; t.tiles_n = col_tiles; t.trap = trap ? 1 : 0;
         t.alpha = -1.0; t.beta = 1.0;
-        return gemm(t, kBNK, m, st);
+        return small ? gemm_small(t, m, st, 0) : gemm(t, kBNK, m, st);
       };
       if ((rc = join(s3, s))) return rc;  // the previous step's bulk work on the inner stream
       if (wcols == 0) {
@@ -629,9 +635,10 @@ struct Launcher {
       // Inner look-ahead: the critical chain to the next diagonal tile is only
       //   panel rows of tile k+1  ->  update of tile (k+1, k+1)  ->  diag(k+1);
       // the other panel rows and updates run on the inner stream meanwhile.
-      if ((rc = panel_gemm(1, 0, s))) return rc;
+      // the chain's two single-tile products on small-tile CTAs (8-16 SMs per dataset)
+      if ((rc = panel_gemm(1, 0, s, true))) return rc;
       if ((rc = join(s, s3))) return rc;
-      if ((rc = update(0, 1, 0, 1, true, s))) return rc;
+      if ((rc = update(0, 1, 0, 1, true, s, true))) return rc;
       if (rem > 1) {
         cudaStream_t in = inner();
         if ((rc = panel_gemm(rem - 1, 1, in))) return rc;

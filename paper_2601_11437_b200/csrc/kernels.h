@@ -95,6 +95,10 @@ void launch_elem(const ThetaParams* P_dev, int op, int which, const double* x, l
 
 // C = alpha * A * op(B) + beta * C per batch member (gridDim.z = batch).
 cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s);
+// Small-tile DMMA GEMM for single 128 x 128 tiles on the Cholesky chain (kBNK B, K <= 128):
+// rows_only = 1 -> 16 x 128 CTAs (C may alias A), 0 -> 32 x 32 CTAs.
+cudaError_t init_small_gemm_attributes();
+cudaError_t launch_gemm_small(const GemmArgs& g, int batch, cudaStream_t s, int rows_only);
 // Factor the 128x128 diagonal tile at (k0, k0) of every item in place (+ its inverse).
 cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s);
 // Reductions: per item kReduceOut results [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>,

@@ -258,6 +258,110 @@ cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s
 }
 
 // ---------------------------------------------------------------------------------------
+// Small-tile DMMA GEMM for the latency-critical products of the Cholesky chain (one 128 x 128
+// output tile per dataset: the next diagonal tile's panel rows and its rank-128 update).  A
+// 128-wide CTA does such a tile at one SM's DMMA rate (~25 us); here TM x TN CTAs (16 x 128
+// for the in-place panel, whose CTAs must own whole rows; 32 x 32 for the update) spread it
+// over 8-16 SMs.  K (<= 128) is staged whole in shared memory before any store, so C may
+// alias A row-wise.  C(m, n) = alpha sum_k A(m, k) B(n, k) + beta C; B layout kBNK.
+namespace {
+constexpr int SM_K = 128;
+template <int TM, int TN>
+__global__ void __launch_bounds__(256) dgemm_small_kernel(GemmArgs g) {
+  constexpr int SAS = TM + 4, SBS = TN + 4;  // smem strides (m / n contiguous per k)
+  constexpr int TILES_M = TM / 8, TILES_N = TN / 8, PER_WARP = TILES_M * TILES_N / 8;
+  static_assert(PER_WARP >= 1 && (TILES_M * TILES_N) % 8 == 0, "tile shape");
+  extern __shared__ __align__(16) double sm_small[];
+  double* As = sm_small;              // [K][SAS]
+  double* Bs = sm_small + SM_K * SAS;  // [K][SBS]
+  const int z = blockIdx.z;
+  if (__ldcv(g.fail_flag[z])) return;
+  constexpr int CM = 128 / TM, CN = 128 / TN;  // CTAs per 128 x 128 tile
+  const int sub = blockIdx.x % (CM * CN), tile = blockIdx.x / (CM * CN);
+  const int sm_ = sub % CM, sn_ = sub / CM;
+  const int tm = tile % g.tiles_m, tn = tile / g.tiles_m;
+  const int r0 = tm * 128 + sm_ * TM, c0 = tn * 128 + sn_ * TN;
+  if (g.trap && r0 + TM <= c0) return;  // sub-tile strictly above the diagonal
+  const int K = g.K;
+  const double* A = g.A[z] + r0;
+  const double* B = g.B[z] + c0;
+  double* C = g.C[z] + r0 + (long long)c0 * g.ldc;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int idx = tid; idx < K * TM; idx += 256) {
+    const int k = idx / TM, m = idx % TM;
+    As[k * SAS + m] = A[m + (long long)k * g.lda];
+  }
+  for (int idx = tid; idx < K * TN; idx += 256) {
+    const int k = idx / TN, n = idx % TN;
+    Bs[k * SBS + n] = B[n + (long long)k * g.ldb];
+  }
+  __syncthreads();
+  const int gq = lane >> 2, tq = lane & 3;
+  const unsigned neg = g.alpha < 0.0 ? 0x80000000u : 0u;
+  double acc[PER_WARP][2];
+  int om[PER_WARP], on[PER_WARP];
+#pragma unroll
+  for (int q = 0; q < PER_WARP; ++q) {
+    const int t = warp * PER_WARP + q;
+    om[q] = (t % TILES_M) * 8;
+    on[q] = (t / TILES_M) * 8;
+    if (g.beta != 0.0) {
+      const double* p0 = C + om[q] + gq + (long long)(on[q] + 2 * tq) * g.ldc;
+      acc[q][0] = p0[0];
+      acc[q][1] = p0[g.ldc];
+    } else {
+      acc[q][0] = acc[q][1] = 0.0;
+    }
+  }
+  for (int kk = 0; kk < K; kk += 4) {
+#pragma unroll
+    for (int q = 0; q < PER_WARP; ++q) {
+      const double v = As[(kk + tq) * SAS + om[q] + gq];
+      const double a = __hiloint2double(__double2hiint(v) ^ (int)neg, __double2loint(v));
+      const double b = Bs[(kk + tq) * SBS + on[q] + gq];
+      asm volatile(
+          "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(acc[q][0]), "+d"(acc[q][1])
+          : "d"(a), "d"(b));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER_WARP; ++q) {
+    double* p0 = C + om[q] + gq + (long long)(on[q] + 2 * tq) * g.ldc;
+    p0[0] = acc[q][0];
+    p0[g.ldc] = acc[q][1];
+  }
+}
+template <int TM, int TN>
+constexpr size_t small_smem() { return sizeof(double) * SM_K * ((TM + 4) + (TN + 4)); }
+}  // namespace
+
+cudaError_t init_small_gemm_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(dgemm_small_kernel<16, 128>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)small_smem<16, 128>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(dgemm_small_kernel<32, 32>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)small_smem<32, 32>());
+}
+
+// rows_only = 1: 16 x 128 CTAs (in-place panels); 0: 32 x 32 CTAs.  K <= 128, kBNK B.
+cudaError_t launch_gemm_small(const GemmArgs& g, int batch, cudaStream_t s, int rows_only) {
+  const long long tiles = (long long)g.tiles_m * g.tiles_n;
+  if (tiles <= 0) return cudaSuccess;
+  if (g.K > SM_K || g.K % 4) return cudaErrorInvalidValue;
+  if (rows_only) {
+    const dim3 grid((unsigned)(tiles * 8), 1, (unsigned)batch);
+    dgemm_small_kernel<16, 128><<<grid, 256, small_smem<16, 128>(), s>>>(g);
+  } else {
+    const dim3 grid((unsigned)(tiles * 16), 1, (unsigned)batch);
+    dgemm_small_kernel<32, 32><<<grid, 256, small_smem<32, 32>(), s>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
 // Diagonal tile: Cholesky + inverse of one 128x128 tile in shared memory (one CTA).
 // Ls is column-major with stride DS: L(i, j) (i >= j) at Ls[j*DS + i].  The inverse
 // X = L^-1 lives in the other triangle, row-major: X(i, j) (i > j) at Ls[i*DS + j], with
