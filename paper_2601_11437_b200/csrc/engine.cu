@@ -308,6 +308,7 @@ struct mle_ctx {
   // Cholesky), because Fisher-BT follows an accepted loglik(theta) with eval_all(theta).
   // spec_ready: sa / sn / wsl hold that work for spec_theta (valid while the factor is).
   PassClock pass_clock;           // led passes (diagnostic gap clock)
+  double cached_ll = 0.0;         // log-likelihood of the resident factor (cached_theta)
   bool spec_ready = false;
   bool spec_pending = false;      // spec_done not yet waited for by a later pass
   double spec_theta[3] = {0, 0, 0};
@@ -1444,6 +1445,7 @@ int run_chunk(Item* items, int m) {
     const double logdet = r[0], quad = r[1];
     double* o = it.res;
     o[0] = -0.5 * n * kLog2Pi - logdet - 0.5 * quad;  // likelihood.py:85-89, 123
+    c->cached_ll = o[0];
     if (it.mode == 2) {
       const double tr_a = r[2], tr_n = r[3], faa = r[4], fan = r[5], fnn = r[6];
       const double yby_a = r[kReduceSums], yby_n = r[kReduceSums + 1];
@@ -1507,6 +1509,17 @@ int prepare(mle_ctx* c, const double theta[3], int mode, Item* it) {
   return MLE_OK;
 }
 
+// loglik at the resident factor's theta: the pass would only rerun the deterministic
+// reduction over the same L, so its value is known on the host (bit-identical).
+bool loglik_cached(Item* it) {
+  if (it->mode != 1 || it->factor) return false;
+  it->rc = MLE_OK;
+  it->pivot = -1;
+  std::memset(it->res, 0, sizeof(it->res));
+  it->res[0] = it->c->cached_ll;
+  return true;
+}
+
 int check_finite(const double* v, int64_t m, const char* what) {
   for (int64_t i = 0; i < m; ++i)
     if (!std::isfinite(v[i])) return fail(MLE_INVALID, std::string(what) + " must be finite");
@@ -1517,8 +1530,10 @@ int single(mle_ctx* c, const double theta[3], int mode, double* res, int64_t* ba
   Item it;
   int rc = prepare(c, theta, mode, &it);
   if (rc) return rc;
-  rc = run_batch(&it, 1);
-  if (rc) return rc;
+  if (!loglik_cached(&it)) {
+    rc = run_batch(&it, 1);
+    if (rc) return rc;
+  }
   if (bad_pivot) *bad_pivot = it.pivot;
   if (it.rc == MLE_NOT_PD)
     return fail(MLE_NOT_PD, "matrix not positive definite at pivot " + std::to_string(it.pivot));
@@ -1626,8 +1641,8 @@ static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n,
   CTX_TRY(dmalloc(&c->partials, sizeof(double) * kReduceBlocks * kReducePartials));
   CTX_TRY(dmalloc(&c->out, sizeof(double) * kReduceOut));
   CTX_TRY(dmalloc(&c->d_theta, sizeof(ThetaParams)));
-  CTX_TRY(dmalloc(&c->gtab_s, sizeof(double) * MLE_TAB_MAX * 3 * MLE_TAB_P));
-  CTX_TRY(dmalloc(&c->gtab_d, sizeof(double) * MLE_TAB_MAX * 3 * MLE_TAB_P));
+  CTX_TRY(dmalloc(&c->gtab_s, sizeof(double) * MLE_TAB_DOUBLES));
+  CTX_TRY(dmalloc(&c->gtab_d, sizeof(double) * MLE_TAB_DOUBLES));
   {
     double x0 = x[0], x1 = x[0], y0 = y[0], y1 = y[0];
     for (int64_t i = 1; i < n; ++i) {
@@ -1750,6 +1765,7 @@ int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const 
     return fail(MLE_INVALID, "null argument");
   std::vector<Item> items;
   std::vector<int> slot;
+  std::vector<mle_ctx*> cached;  // answered from the resident factor, no pass
   std::string bad;
   for (int i = 0; i < count; ++i) {
     rcs[i] = MLE_OK;
@@ -1763,6 +1779,11 @@ int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const 
     if (prepare(ctxs[i], thetas + 3 * i, modes[i], &it) != MLE_OK) {
       rcs[i] = MLE_INVALID;
       bad = g_last_error;
+      continue;
+    }
+    if (loglik_cached(&it)) {
+      std::memcpy(results + (size_t)kResults * i, it.res, sizeof(double) * kResults);
+      cached.push_back(it.c);
       continue;
     }
     items.push_back(it);
@@ -1788,6 +1809,15 @@ int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const 
       if (pivots) pivots[i] = group[g].pivot;
       std::memcpy(results + (size_t)kResults * i, group[g].res, sizeof(double) * kResults);
     }
+  }
+  // per-context pass statistics of the cached answers: those of this call's pass, or none
+  for (mle_ctx* c : cached) {
+    const mle_ctx* src = items.empty() ? nullptr : items[0].c;
+    for (int p = 0; p < MLE_NUM_PHASES; ++p) c->phase_ms[p] = src ? src->phase_ms[p] : 0.0;
+    c->flops = src ? src->flops : 0.0;
+    c->gen_bytes = src ? src->gen_bytes : 0.0;
+    c->launches = src ? src->launches : 0.0;
+    for (int k = 7; k <= 9; ++k) c->kstats[k] = src ? src->kstats[k] : 0.0;
   }
   if (!bad.empty()) g_last_error = bad;
   return MLE_OK;

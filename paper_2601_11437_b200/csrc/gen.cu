@@ -41,12 +41,17 @@ __device__ __forceinline__ double pair_distance(const double* lx, const double* 
   return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
 }
 
-// Stage one ThetaParams from global memory into shared memory (all threads participate).
+// Stage one ThetaParams (~7 KB) from global memory into shared memory (all threads
+// participate; 16-byte words, then the 4-byte tail).
 __device__ __forceinline__ void stage_params(ThetaParams* dst, const ThetaParams* src) {
-  const int words = (int)(sizeof(ThetaParams) / sizeof(int));
+  constexpr int kVec = (int)(sizeof(ThetaParams) / sizeof(int4));
+  constexpr int kWords = (int)(sizeof(ThetaParams) / sizeof(int));
+  const int4* s4 = reinterpret_cast<const int4*>(src);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  for (int w = threadIdx.x; w < kVec; w += blockDim.x) d4[w] = __ldg(s4 + w);
   const int* s = reinterpret_cast<const int*>(src);
   int* d = reinterpret_cast<int*>(dst);
-  for (int w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+  for (int w = 4 * kVec + threadIdx.x; w < kWords; w += blockDim.x) d[w] = s[w];
   __syncthreads();
 }
 
@@ -96,12 +101,16 @@ __device__ __forceinline__ void engine_element(const GenItem& it, const ThetaPar
   }
 }
 
-__global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
+// kDerivs = 0: Sigma (lower tiles); 1: both derivative matrices (full storage, mirrored).
+// Interior off-diagonal tiles (every index < n, i != j: nearly all of them) take a fast path:
+// no padding / augmentation branches, the row point loaded once, column pointers stepped.
+template <int kDerivs>
+__global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
   const GenItem& it = a.item[blockIdx.y];
   if (it.fail_flag != nullptr && *it.fail_flag) return;
-  __shared__ ThetaParams P;
-  __shared__ double s_da[kGT][kGT + 1];
-  __shared__ double s_dn[kGT][kGT + 1];
+  __shared__ __align__(16) ThetaParams P;
+  __shared__ double s_da[kDerivs ? kGT : 1][kGT + 1];
+  __shared__ double s_dn[kDerivs ? kGT : 1][kGT + 1];
   stage_params(&P, it.P);
   int ti, tj;
   lower_tile_index((long long)blockIdx.x, &ti, &tj);
@@ -110,23 +119,58 @@ __global__ void __launch_bounds__(kGThreads) gen_engine_kernel(GenArgs a) {
   const int i = ti * kGT + lane_row;
   const long long ld = a.ld;
   const int n = a.n;
-  const bool derivs = it.write_derivs != 0;
+  if (ti != tj && (ti + 1) * kGT <= n && it.tab != nullptr) {
+    const double xi = it.lx[i], yi = it.ly[i];
+    const double lo = P.tab_lo, hi = P.tab_hi, alpha = P.alpha;
+    const long long j0 = (long long)tj * kGT + col0;
+    double* ps = it.sigma + i + j0 * ld;
+    double* pa = it.dalpha + i + j0 * ld;
+    double* pn = it.dnu + i + j0 * ld;
+#pragma unroll  // four independent elements per thread: overlaps their dependent chains
+    for (int r = 0; r < kGT / 8; ++r) {
+      const int j = (int)j0 + 8 * r;
+      // pdist-identical distance (no FMA contraction), u = h / alpha (matern.py:103)
+      const double dx = __dsub_rn(xi, it.lx[j]);
+      const double dy = __dsub_rn(yi, it.ly[j]);
+      const double h = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+      const double u = h / alpha;
+      MaternVals v;
+      if (u >= lo && u < hi) {
+        v = matern_table<kDerivs != 0>(P, it.tab, u);
+      } else if (h > 0.0) {
+        v = matern_u<kDerivs != 0>(P, u);
+      } else {  // coincident locations: zero-lag limit (matern.py:173-178)
+        v.c = P.sigma2;
+        v.dalpha = v.dnu = 0.0;
+      }
+      if (kDerivs) {
+        pa[8 * r * ld] = v.dalpha;
+        pn[8 * r * ld] = v.dnu;
+        s_da[lane_row][col0 + 8 * r] = v.dalpha;
+        s_dn[lane_row][col0 + 8 * r] = v.dnu;
+      } else {
+        ps[8 * r * ld] = v.c;
+      }
+    }
+  } else {
 #pragma unroll 1
-  for (int r = 0; r < kGT / 8; ++r) {
-    const int jl = col0 + 8 * r;
-    const int j = tj * kGT + jl;
-    double c, da, dn;
-    engine_element(it, P, i, j, n, derivs, c, da, dn);
-    const long long off = (long long)i + (long long)j * ld;
-    if (it.write_sigma) it.sigma[off] = c;
-    if (derivs) {
-      it.dalpha[off] = da;
-      it.dnu[off] = dn;
-      s_da[lane_row][jl] = da;
-      s_dn[lane_row][jl] = dn;
+    for (int r = 0; r < kGT / 8; ++r) {
+      const int jl = col0 + 8 * r;
+      const int j = tj * kGT + jl;
+      double c, da, dn;
+      engine_element(it, P, i, j, n, kDerivs != 0, c, da, dn);
+      const long long off = (long long)i + (long long)j * ld;
+      if (kDerivs) {
+        it.dalpha[off] = da;
+        it.dnu[off] = dn;
+        s_da[lane_row][jl] = da;
+        s_dn[lane_row][jl] = dn;
+      } else {
+        it.sigma[off] = c;
+      }
     }
   }
-  if (derivs && ti != tj) {
+  if (kDerivs && ti != tj) {
     __syncthreads();
     // mirrored tile (J, I): rows from tile J, columns from tile I
     const int i2 = tj * kGT + lane_row;
@@ -149,7 +193,7 @@ __global__ void __launch_bounds__(kGThreads) gen_panel_kernel(GenArgs a, const i
                                                               int width) {
   const GenItem& it = a.item[blockIdx.z];
   if (it.fail_flag != nullptr && *it.fail_flag) return;
-  __shared__ ThetaParams P;
+  __shared__ __align__(16) ThetaParams P;
   stage_params(&P, it.P);
   const int c0 = c0s[blockIdx.z];
   const int i = blockIdx.x * kGT + (threadIdx.x & (kGT - 1));
@@ -173,10 +217,13 @@ __global__ void __launch_bounds__(kGThreads) gen_panel_kernel(GenArgs a, const i
   }
 }
 
-// Chebyshev coefficients of e^u * {c, dalpha, dnu}(u) on every table interval of every item
-// (grid: MLE_TAB_MAX x items; one CTA per interval).  Node values come from the exact
-// evaluator (matern_u), so the table inherits its accuracy; with a convergence factor ~22 per
-// interval the degree-13 truncation error is far below one ulp.
+// Polynomial pieces of e^u * {c, dalpha, dnu}(u) on every table interval of every item (grid:
+// MLE_TAB_MAX x items; one CTA per interval).  Node values come from the exact evaluator
+// (matern_u), so the table inherits its accuracy: Chebyshev interpolation at 14 nodes (a
+// convergence factor ~22 per interval puts the degree-13 truncation far below one ulp), then
+// converted to the monomial basis in t in [-1, 1] for a one-FMA-per-term Horner evaluation.
+// The conversion is benign: |a_i| <~ sum_j |c_j| |T_j coefficients| with |c_j| ~ 22^-j against
+// coefficient growth (1 + sqrt 2)^j.  Layout [interval][power][c, dalpha, dnu, pad].
 __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
   const GenItem& it = a.item[blockIdx.y];
   if (it.tab == nullptr || (it.fail_flag != nullptr && *it.fail_flag)) return;
@@ -184,6 +231,7 @@ __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
   const int k = blockIdx.x;
   if (k >= P.tab_n) return;
   __shared__ double f[3][MLE_TAB_P];
+  __shared__ double cc[3][MLE_TAB_P];
   const int t = threadIdx.x;
   if (t < MLE_TAB_P) {
     const double x = cospi((t + 0.5) / MLE_TAB_P);
@@ -201,14 +249,34 @@ __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
     for (int q = 0; q < MLE_TAB_P; ++q) s += f[fn][q] * cospi(j * (q + 0.5) / MLE_TAB_P);
     s *= 2.0 / MLE_TAB_P;
     if (j == 0) s *= 0.5;
-    it.tab[((size_t)k * 3 + fn) * MLE_TAB_P + j] = s;
+    cc[fn][j] = s;
+  }
+  __syncthreads();
+  if (t < 3) {  // monomial coefficients a_i = sum_j c_j [t^i] T_j(t)
+    double Tm[MLE_TAB_P], Tc[MLE_TAB_P], Tn[MLE_TAB_P], acc[MLE_TAB_P];
+    for (int i = 0; i < MLE_TAB_P; ++i) Tm[i] = Tc[i] = acc[i] = 0.0;
+    Tm[0] = 1.0;             // T_0
+    Tc[1] = 1.0;             // T_1
+    acc[0] = cc[t][0];
+    acc[1] = cc[t][1];
+    for (int j = 2; j < MLE_TAB_P; ++j) {  // T_j = 2 t T_{j-1} - T_{j-2}
+      for (int i = 0; i < MLE_TAB_P; ++i)
+        Tn[i] = (i > 0 ? 2.0 * Tc[i - 1] : 0.0) - Tm[i];
+      for (int i = 0; i < MLE_TAB_P; ++i) {
+        Tm[i] = Tc[i];
+        Tc[i] = Tn[i];
+      }
+      // higher j first would be marginally better; terms shrink ~22x per j either way
+      for (int i = 0; i <= j; ++i) acc[i] = fma(cc[t][j], Tn[i], acc[i]);
+    }
+    for (int i = 0; i < MLE_TAB_P; ++i) it.tab[((size_t)k * MLE_TAB_P + i) * 4 + t] = acc[i];
   }
 }
 
 // Full symmetric n x n matrix of one kind (mle_build), no augmentation / padding.
 __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int which) {
   const GenItem& it = a.item[0];
-  __shared__ ThetaParams P;
+  __shared__ __align__(16) ThetaParams P;
   __shared__ double s_v[kGT][kGT + 1];
   stage_params(&P, it.P);
   int ti, tj;
@@ -260,7 +328,7 @@ __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int whi
 // Elementwise evaluators (parity surface for bessel.py / matern.py scalar functions).
 __global__ void elem_kernel(const ThetaParams* Pg, int op, int which,
                             const double* __restrict__ x, long long m, double* __restrict__ out) {
-  __shared__ ThetaParams P;
+  __shared__ __align__(16) ThetaParams P;
   stage_params(&P, Pg);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m;
        t += (long long)gridDim.x * blockDim.x) {
@@ -309,9 +377,13 @@ static long long lower_tiles(long long rows) {
   return t * (t + 1) / 2;
 }
 
+// Every item of one launch writes the same kind (Sigma, or the derivative pair).
 void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s) {
   const dim3 grid((unsigned)lower_tiles(a.rows), (unsigned)items);
-  gen_engine_kernel<<<grid, kGThreads, 0, s>>>(a);
+  if (a.item[0].write_derivs)
+    gen_engine_kernel<1><<<grid, kGThreads, 0, s>>>(a);
+  else
+    gen_engine_kernel<0><<<grid, kGThreads, 0, s>>>(a);
 }
 
 void launch_gen_panels(const GenArgs& a, const int* c0s_dev, int width, int items,

@@ -245,20 +245,8 @@ __device__ __forceinline__ int gen_tab_index(const ThetaParams& P, double u) {
   return P.seg_base[s] + k;
 }
 
-// Clenshaw sum of c[0] + sum_{j>=1} c[j] T_j(t)  (c[0] stored halved).
-__device__ __forceinline__ double cheb_eval(const double* __restrict__ c, double t) {
-  const double t2 = 2.0 * t;
-  double b1 = 0.0, b2 = 0.0;
-#pragma unroll
-  for (int j = MLE_TAB_P - 1; j >= 1; --j) {
-    const double b0 = fma(t2, b1, __ldg(c + j) - b2);
-    b2 = b1;
-    b1 = b0;
-  }
-  return fma(t, b1, __ldg(c) - b2);
-}
-
-// tab: [MLE_TAB_MAX][3][MLE_TAB_P] coefficients of e^u * {c, dalpha, dnu}.
+// tab: [MLE_TAB_MAX][MLE_TAB_P][4] monomial coefficients (powers of t in [-1, 1]) of
+// e^u * {c, dalpha, dnu}; Horner, one FMA per term.
 template <bool kDerivs>
 __device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
                                                    const double* __restrict__ tab, double u) {
@@ -266,13 +254,26 @@ __device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
   const double t = (u - P.tab_ctr[k]) * P.tab_ihw[k];
   // below 8.5 the series are of E itself (no e^u scaling error); above, of e^u E
   const double eu = u < MLE_SMALL_MID_SPLIT ? 1.0 : exp(-u);
-  const double* c = tab + (size_t)k * 3 * MLE_TAB_P;
+  const double* c = tab + (size_t)k * MLE_TAB_P * 4;
   MaternVals out;
-  out.c = eu * cheb_eval(c, t);
   if (kDerivs) {
-    out.dalpha = eu * cheb_eval(c + MLE_TAB_P, t);
-    out.dnu = eu * cheb_eval(c + 2 * MLE_TAB_P, t);
+    double2 ca = __ldg(reinterpret_cast<const double2*>(c + 4 * (MLE_TAB_P - 1)));
+    double pc = ca.x, pa = ca.y, pn = __ldg(c + 4 * (MLE_TAB_P - 1) + 2);
+#pragma unroll
+    for (int i = MLE_TAB_P - 2; i >= 0; --i) {
+      const double2 q = __ldg(reinterpret_cast<const double2*>(c + 4 * i));
+      pc = fma(pc, t, q.x);
+      pa = fma(pa, t, q.y);
+      pn = fma(pn, t, __ldg(c + 4 * i + 2));
+    }
+    out.c = eu * pc;
+    out.dalpha = eu * pa;
+    out.dnu = eu * pn;
   } else {
+    double pc = __ldg(c + 4 * (MLE_TAB_P - 1));
+#pragma unroll
+    for (int i = MLE_TAB_P - 2; i >= 0; --i) pc = fma(pc, t, __ldg(c + 4 * i));
+    out.c = eu * pc;
     out.dalpha = 0.0;
     out.dnu = 0.0;
   }

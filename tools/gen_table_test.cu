@@ -46,7 +46,7 @@ int main() {
     double *dtab, *du_, *dout;
     cudaMalloc(&dP, sizeof(P));
     cudaMemcpy(dP, &P, sizeof(P), cudaMemcpyHostToDevice);
-    cudaMalloc(&dtab, sizeof(double) * MLE_TAB_MAX * 3 * MLE_TAB_P);
+    cudaMalloc(&dtab, sizeof(double) * MLE_TAB_DOUBLES);
     GenArgs a{};
     a.item[0].P = dP;
     a.item[0].tab = dtab;
