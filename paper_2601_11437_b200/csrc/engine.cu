@@ -528,6 +528,15 @@ struct Launcher {
     std::memcpy(prof->kstats, st, sizeof(st));
     return MLE_OK;
   }
+  // Grid cap of the solve sweeps' GEMMs (MLE_SOLVE_CTAS, 0: every SM): SMs left free let a
+  // concurrent pass's latency-bound Cholesky chain (another fit group) start its kernels.
+  static int solve_ctas() {
+    static const int v = [] {
+      const char* e = std::getenv("MLE_SOLVE_CTAS");
+      return e ? std::atoi(e) : 0;
+    }();
+    return v;
+  }
   static OzGemmArgs oz_base(long long ldc, int tiles_m, int tiles_n) {
     OzGemmArgs g;
     std::memset(&g, 0, sizeof(g));
@@ -936,6 +945,7 @@ struct Launcher {
         t.C[z] = S(z) + k.c0;
         t.fail_flag[z] = flag(z);
       }
+      t.max_ctas = solve_ctas();
       if ((rc = ozgemm(t, zb, s))) return rc;
       if (t2 >= Nt) continue;
       if ((rc = join(s, s2))) return rc;
@@ -947,6 +957,7 @@ struct Launcher {
         u.ea[z] = t.ea[z] + (size_t)(t2 - k.t0) * kNB;
         u.C[z] = S(z) + (long long)t2 * kNB;
       }
+      u.max_ctas = solve_ctas();
       if ((rc = ozgemm(u, zb, bulk()))) return rc;
     }
     if ((rc = join(s2, s))) return rc;
@@ -985,6 +996,7 @@ struct Launcher {
         t.C[z] = S(z) + k.c0 + k.c0 * ld;
         t.fail_flag[z] = flag(z);
       }
+      t.max_ctas = solve_ctas();
       if ((rc = ozgemm(t, zb, s))) return rc;
       if (t2 >= Nt) continue;
       if ((rc = join(s, s2))) return rc;
@@ -1002,6 +1014,7 @@ struct Launcher {
         u.C[z] = S(z) + c2 + c2 * ld;
         u.fail_flag[z] = flag(z);
       }
+      u.max_ctas = solve_ctas();
       if ((rc = ozgemm(u, zb, bulk()))) return rc;
     }
     return join(s2, s);
