@@ -621,7 +621,7 @@ struct Launcher {
       };
       // A[r0+.., c0+..] -= P[r0..] P[c0..]^T over tile rows/cols of this outer block
       auto update = [&](int row_off, int row_tiles, int col_off, int col_tiles, bool trap,
-                        cudaStream_t st, bool small = false) {
+                        cudaStream_t st, bool small = false, int trap_off = 0) {
         GemmArgs t = gemm_base();
         for (int b = 0; b < m; ++b) {
           double* panel = mats[b] + (k0 + kNB) + k0 * ld;
@@ -633,6 +633,7 @@ struct Launcher {
         }
         t.lda = ld; t.ldb = ld; t.ldc = ld;
         t.tiles_m = row_tiles; t.tiles_n = col_tiles; t.trap = trap ? 1 : 0;
+        t.trap_off = trap_off;
         t.alpha = -1.0; t.beta = 1.0;
         return small ? gemm_small(t, m, st, 0) : gemm(t, kBNK, m, st);
       };
@@ -652,8 +653,8 @@ struct Launcher {
       if (rem > 1) {
         cudaStream_t in = inner();
         if ((rc = panel_gemm(rem - 1, 1, in))) return rc;
-        if ((rc = update(1, rem - 1, 0, 1, false, in))) return rc;  // column k+1, rows >= k+2
-        if (wcols > 1 && (rc = update(1, rem - 1, 1, wcols - 1, true, in))) return rc;
+        // rows >= k+2 of the block's remaining columns k+1.. (one launch, lower trapezoid)
+        if ((rc = update(1, rem - 1, 0, wcols, true, in, false, 1))) return rc;
       }
     }
     return join(s3, s);

@@ -51,7 +51,8 @@ struct GemmArgs {
   int tiles_m;       // number of 128-row tiles of C
   int tiles_n;       // number of 128-column tiles of C (full mode)
   int lower;         // 1: only tiles (tm >= tn) of a tiles_m x tiles_m grid
-  int trap;          // full mode: 1 skips tiles with tm < tn (lower trapezoid)
+  int trap;          // full mode: 1 skips tiles with tm + trap_off < tn (lower trapezoid)
+  int trap_off;      // row-tile offset of C's base above its column-tile offset (0 usually)
   int wide;          // 1: 128-column CTAs (C aliases A across the 128-wide panel)
   double alpha;      // +1 or -1
   double beta;       // 0 (overwrite) or 1 (accumulate into C)

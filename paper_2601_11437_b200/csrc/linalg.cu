@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_ker
 
   int tm, tn, half;
   tile_coords<kBN>(g, &tm, &tn, &half);
-  if (g.trap && tm < tn) return;
+  if (g.trap && tm + g.trap_off < tn) return;
   const long long col0 = (long long)tn * 128 + (long long)half * kBN;
   // no __restrict__: panel products run in place (C aliases A or B; see engine.cu)
   const double* A = g.A[z] + (long long)tm * BM;
