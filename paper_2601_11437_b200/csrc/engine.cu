@@ -454,16 +454,61 @@ struct Launcher {
   int next = 0;
   double launches = 0.0;
 
+  // Timeline trace (MLE_TRACE=<file>, developer diagnostics): an event after every launch on
+  // its own stream; after the pass, each launch's completion time from the pass start is
+  // appended to the file as "pass label stream end_ms".
+  struct Mark {
+    cudaEvent_t ev;
+    const char* label;
+    int stream;
+  };
+  std::vector<Mark> marks;
+  cudaEvent_t trace_t0 = nullptr;
+  static const char* trace_path() {
+    static const char* p = std::getenv("MLE_TRACE");
+    return p;
+  }
+  int mark(const char* label, cudaStream_t st) {
+    if (!trace_path()) return MLE_OK;
+    Mark m{nullptr, label, st == s ? 0 : st == s2 ? 1 : st == s3 ? 2 : 3};
+    CUDA_TRY(cudaEventCreate(&m.ev));
+    CUDA_TRY(cudaEventRecord(m.ev, st));
+    marks.push_back(m);
+    return MLE_OK;
+  }
+  int trace_begin() {
+    if (!trace_path()) return MLE_OK;
+    CUDA_TRY(cudaEventCreate(&trace_t0));
+    CUDA_TRY(cudaEventRecord(trace_t0, s));
+    return MLE_OK;
+  }
+  int trace_end() {  // after the pass synchronized
+    if (!trace_path() || !trace_t0) return MLE_OK;
+    static long long pass = 0;
+    FILE* f = std::fopen(trace_path(), "a");
+    for (const Mark& m : marks) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, trace_t0, m.ev);
+      if (f) std::fprintf(f, "%lld %s %d %.4f\n", pass, m.label, m.stream, ms);
+      cudaEventDestroy(m.ev);
+    }
+    if (f) std::fclose(f);
+    cudaEventDestroy(trace_t0);
+    trace_t0 = nullptr;
+    marks.clear();
+    ++pass;
+    return MLE_OK;
+  }
   int gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t st) {
     launches += 1;
     CUDA_TRY(launch_gemm(g, bl, batch, st));
-    return MLE_OK;
+    return mark(g.wide ? "dgemm128" : "dgemm64", st);
   }
   int gemm(const GemmArgs& g, BLayout bl, int batch) { return gemm(g, bl, batch, s); }
   int gemm_small(const GemmArgs& g, int batch, cudaStream_t st, int rows_only) {
     launches += 1;
     CUDA_TRY(launch_gemm_small(g, batch, st, rows_only));
-    return MLE_OK;
+    return mark(rows_only ? "small_panel" : "small_update", st);
   }
   // kernel profiling: event pair per launch (kind 0 ozgemm, 1 slicing) + algorithmic work
   mle_ctx* prof = nullptr;
@@ -489,19 +534,23 @@ struct Launcher {
     pint8.push_back(int8_ops);
     return MLE_OK;
   }
-  int slice(const OzSliceArgs& a, long long rows, bool row_contig, int batch) {
+  int slice(const OzSliceArgs& a, long long rows, bool row_contig, int batch,
+            cudaStream_t st = nullptr) {
+    if (!st) st = s;
     launches += 1;
-    int rc = prof_begin(s);
+    int rc = prof_begin(st);
     if (rc) return rc;
-    CUDA_TRY(launch_oz_slice(a, (int)rows, row_contig, batch, s));
+    CUDA_TRY(launch_oz_slice(a, (int)rows, row_contig, batch, st));
+    if ((rc = mark("slice", st))) return rc;
     // algorithmic bytes: the FP64 operand read once, S int8 slices + exponents written
-    return prof_end(s, 1, (double)batch * rows * ((8.0 + oz_nslices(a.nslices)) * a.K + 4.0));
+    return prof_end(st, 1, (double)batch * rows * ((8.0 + oz_nslices(a.nslices)) * a.K + 4.0));
   }
   int ozgemm(const OzGemmArgs& g, int batch, cudaStream_t st) {
     launches += 1;
     int rc = prof_begin(st);
     if (rc) return rc;
     CUDA_TRY(launch_ozgemm(g, batch, st));
+    if ((rc = mark("ozgemm", st))) return rc;
     double tiles;
     if (g.lower) tiles = 0.5 * g.tiles_m * (g.tiles_m + 1.0);
     else if (g.trap) {
@@ -601,6 +650,7 @@ struct Launcher {
       }
       launches += 1;
       CUDA_TRY(launch_potrf_diag(d, m, s));
+      if ((rc = mark("diag", s))) return rc;
       const int rem = Nt - k - 1;
       if (rem == 0) break;
       const int wcols = b1 - k - 1;  // remaining tile columns of this outer block
@@ -1175,6 +1225,10 @@ int run_chunk(Item* items, int m) {
     }
   }
   CUDA_TRY(cudaEventRecord(pc->pre, s));
+  {
+    int rc = run.trace_begin();
+    if (rc) return rc;
+  }
   for (int b = 0; b < m; ++b) {
     Item& it = items[b];
     int rc = wait_spec(it.c, s);
@@ -1387,6 +1441,10 @@ int run_chunk(Item* items, int m) {
   }
   ++pc->passes;
   CUDA_TRY(cudaGetLastError());
+  {
+    int rc = run.trace_end();
+    if (rc) return rc;
+  }
   const auto host_t2 = std::chrono::steady_clock::now();
   {
     int rc = run.prof_collect();

@@ -287,14 +287,18 @@ __global__ void __launch_bounds__(256) dgemm_small_kernel(GemmArgs g) {
   const double* B = g.B[z] + c0;
   double* C = g.C[z] + r0 + (long long)c0 * g.ldc;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int idx = tid; idx < K * TM; idx += 256) {
-    const int k = idx / TM, m = idx % TM;
-    As[k * SAS + m] = A[m + (long long)k * g.lda];
+  // all 16-byte copies in flight at once (cp.async), then one wait: the fill is one L2
+  // round trip instead of K * (TM + TN) / 256 dependent ones
+  for (int idx = tid; idx < K * (TM / 2); idx += 256) {
+    const int k = idx / (TM / 2), m2 = (idx % (TM / 2)) * 2;
+    cp_async16(As + k * SAS + m2, A + m2 + (long long)k * g.lda);
   }
-  for (int idx = tid; idx < K * TN; idx += 256) {
-    const int k = idx / TN, n = idx % TN;
-    Bs[k * SBS + n] = B[n + (long long)k * g.ldb];
+  for (int idx = tid; idx < K * (TN / 2); idx += 256) {
+    const int k = idx / (TN / 2), n2 = (idx % (TN / 2)) * 2;
+    cp_async16(Bs + k * SBS + n2, B + n2 + (long long)k * g.ldb);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   const int gq = lane >> 2, tq = lane & 3;
   const unsigned neg = g.alpha < 0.0 ? 0x80000000u : 0u;
