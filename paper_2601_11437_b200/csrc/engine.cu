@@ -1288,7 +1288,25 @@ int run_chunk(Item* items, int m) {
   if (sig.second > 0) {
     run.launches += 2;
     launch_gen_table(sig.first, sig.second, false, s);
-    launch_gen_engine(sig.first, sig.second, s);
+    // Sigma: the first outer block's columns on the main stream (all the Cholesky's first
+    // inner steps read), the rest on the low-priority aux stream under those steps, so the
+    // chain's kernels win the SMs; the side stream (first trailing update) waits for it.
+    constexpr int kJcut = kOuter * kNB / 32;
+    if (run.s2 && aux != s && (lead->N + 31) / 32 > kJcut) {
+      GenArgs pa = sig.first, pb = sig.first;
+      pa.region = 1;
+      pa.jcut = kJcut;
+      pb.region = 2;
+      pb.jcut = kJcut;
+      int rc = run.join(s, aux);  // aux starts after the table, not after (a)
+      if (rc) return rc;
+      launch_gen_engine(pa, sig.second, s);
+      run.launches += 1;
+      launch_gen_engine(pb, sig.second, aux);
+      if ((rc = run.join(aux, run.s2))) return rc;
+    } else {
+      launch_gen_engine(sig.first, sig.second, s);
+    }
     CUDA_TRY(cudaGetLastError());
   }
   // derivative matrices: eval_all items first (the solves wait for these only), then the

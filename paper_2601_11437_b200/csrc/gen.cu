@@ -111,9 +111,19 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
   __shared__ __align__(16) ThetaParams P;
   __shared__ double s_da[kDerivs ? kGT : 1][kGT + 1];
   __shared__ double s_dn[kDerivs ? kGT : 1][kGT + 1];
-  stage_params(&P, it.P);
   int ti, tj;
-  lower_tile_index((long long)blockIdx.x, &ti, &tj);
+  if (a.region == 1) {  // tile columns < jcut: grid (tile rows) x jcut, upper ones skipped
+    ti = (int)(blockIdx.x / a.jcut);
+    tj = (int)(blockIdx.x % a.jcut);
+    if (tj > ti) return;
+  } else {
+    lower_tile_index((long long)blockIdx.x, &ti, &tj);
+    if (a.region == 2) {  // the lower triangle of the trailing block [jcut, T)^2
+      ti += a.jcut;
+      tj += a.jcut;
+    }
+  }
+  stage_params(&P, it.P);
   const int lane_row = threadIdx.x & (kGT - 1);
   const int col0 = threadIdx.x >> 5;
   const int i = ti * kGT + lane_row;
@@ -379,7 +389,12 @@ static long long lower_tiles(long long rows) {
 
 // Every item of one launch writes the same kind (Sigma, or the derivative pair).
 void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s) {
-  const dim3 grid((unsigned)lower_tiles(a.rows), (unsigned)items);
+  const long long T = (a.rows + kGT - 1) / kGT;
+  const long long blocks = a.region == 1 ? T * a.jcut
+                           : a.region == 2 ? (T - a.jcut) * (T - a.jcut + 1) / 2
+                                           : lower_tiles(a.rows);
+  if (blocks <= 0) return;
+  const dim3 grid((unsigned)blocks, (unsigned)items);
   if (a.item[0].write_derivs)
     gen_engine_kernel<1><<<grid, kGThreads, 0, s>>>(a);
   else

@@ -36,6 +36,8 @@ struct GenArgs {
   long long ld;       // leading dimension (column-major)
   long long rows;     // padded extent N (engine) / n (build)
   int n;              // number of locations
+  int region;         // engine: 0 every lower tile; 1 tile columns < jcut; 2 tile columns >= jcut
+  int jcut;           // in 32-wide generation tiles
 };
 
 // Operand layouts of op(B): B(n,k) at b[n + k*ldb] (kBNK) or b[k + n*ldb] (kBKN).
