@@ -608,6 +608,7 @@ struct Launcher {
   }
   cudaStream_t bulk() const { return s2 ? s2 : s; }
   cudaStream_t s3 = nullptr;   // inner look-ahead of the Cholesky (null: on s)
+  bool outer_on_inner = false;  // (i1) of the last outer update was issued on s3
   cudaStream_t inner() const { return s3 ? s3 : s; }
   // W request of the Cholesky: build W_b of these contexts on stream ws as each outer block
   // of the factor becomes final (Ozaki path only).
@@ -687,7 +688,13 @@ struct Launcher {
         t.alpha = -1.0; t.beta = 1.0;
         return small ? gemm_small(t, m, st, 0) : gemm(t, kBNK, m, st);
       };
-      if ((rc = join(s3, s))) return rc;  // the previous step's bulk work on the inner stream
+      // the previous step's bulk work on the inner stream (not at a block's first step when
+      // that stream only holds the last outer update's far columns, which it does not read)
+      if (k == b0 && outer_on_inner) {
+        outer_on_inner = false;
+      } else if ((rc = join(s3, s))) {
+        return rc;
+      }
       if (wcols == 0) {
         // last tile of the outer block: the whole panel (read by the trailing update)
         if ((rc = panel_gemm(rem, 0, s))) return rc;
@@ -741,7 +748,12 @@ struct Launcher {
         sa.K = kOzK;
         if ((rc = slice(sa, (long long)(Nt - b1) * kNB, true, m))) return rc;
         if ((rc = issue_w(ob))) return rc;
-        OzGemmArgs t = oz_base(ld, Nt - b1, b2 - b1);  // (i)
+        // (i) in two parts: the next block's first two tile columns on the main stream (its
+        // first inner step reads only those), the other two on the inner stream, where that
+        // step's own inner-stream work follows them in order
+        const int i0 = (s3 && b2 - b1 > 2) ? 2 : b2 - b1;
+        if (i0 < b2 - b1 && (rc = join(s, s3))) return rc;
+        OzGemmArgs t = oz_base(ld, Nt - b1, i0);  // (i0)
         t.trap = 1;
         for (int b = 0; b < m; ++b) {
           t.As[b] = t.Bs[b] = sa.slices[b];
@@ -750,6 +762,19 @@ struct Launcher {
           t.fail_flag[b] = cs[b]->fail_flag;
         }
         if ((rc = ozgemm(t, m, s))) return rc;
+        if (i0 < b2 - b1) {
+          OzGemmArgs t1 = oz_base(ld, Nt - b1 - i0, b2 - b1 - i0);  // (i1)
+          t1.trap = 1;
+          const long long o1 = t0 + (long long)i0 * kNB;
+          for (int b = 0; b < m; ++b) {
+            t1.As[b] = t1.Bs[b] = sa.slices[b] + (size_t)i0 * kOzTileBytes;
+            t1.ea[b] = t1.eb[b] = sa.e[b] + (size_t)i0 * kNB;
+            t1.C[b] = mats[b] + o1 + o1 * ld;
+            t1.fail_flag[b] = cs[b]->fail_flag;
+          }
+          if ((rc = ozgemm(t1, m, s3))) return rc;
+          outer_on_inner = true;  // the next block's first step must not wait for it
+        }
         if (b2 >= Nt) continue;
         if ((rc = join(s, s2))) return rc;
         OzGemmArgs u = oz_base(ld, Nt - b2, 0);        // (ii)
