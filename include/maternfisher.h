@@ -78,17 +78,19 @@ int mle_release_cached_memory(void);
 /*
  * Kernel profiling of the FP64 trailing-update GEMMs (roofline evidence for bench.py).
  * With profiling enabled, a pass (loglik / eval_all / eval_batch led by this context) runs
- * on one stream and brackets every Ozaki GEMM and slicing launch with CUDA events.
+ * on one stream and brackets every Ozaki GEMM, slicing and generation launch with CUDA events.
  * mle_kernel_stats then returns, for the last pass, MLE_KSTATS doubles:
  *   [0] GEMM launches  [1] GEMM ms (sum of launch durations)  [2] FP64-equivalent tile
- *   flops  [3] int8 tensor-core ops (36 slice products)  [4] slicing launches  [5] slicing
+ *   flops  [3] int8 tensor-core ops (28 slice products per FP64 MAC)  [4] slicing launches  [5] slicing
  *   ms  [6] slicing algorithmic bytes  [7] host time to enqueue the last pass (ms; also
  *   maintained when profiling is off)  [8] main-stream idle time between the previous pass on
  *   this device and the host's first enqueue of this one (ms)  [9] time this pass then waited
- *   for pending speculation and its parameter upload (ms).
+ *   for pending speculation and its parameter upload (ms)  [10] generation launches (Sigma
+ *   and derivative matrices)  [11] generation ms  [12] generation algorithmic bytes (8 B per
+ *   lower-triangle element per matrix written).
  * Diagnostic only: no reference counterpart.
  */
-#define MLE_KSTATS 10
+#define MLE_KSTATS 13
 /* (max L_jj / min L_jj)^2 of the context's last successful factorization (0 before any): a
  * cheap lower bound of cond(Sigma), reported for diagnostics. */
 int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out);

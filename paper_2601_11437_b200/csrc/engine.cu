@@ -53,6 +53,16 @@ struct PassClock {
   cudaEvent_t pre = nullptr;  // before the pass waits on pending speculation
   long long passes = 0;
 };
+// Streams and events of destroyed contexts, per device, for the next context (creating and
+// destroying 4 streams and ~30 events per context cost ~0.5 ms, i.e. ~1.5% of an end-to-end
+// config-2 step that builds five contexts).
+struct StreamSet {
+  cudaStream_t stream, side, inner, aux;
+  cudaEvent_t ev[5], ev_der, spec_done, pool[16], clk[4];
+};
+std::mutex g_sets_mutex;
+std::vector<std::vector<StreamSet>> g_sets;
+
 const double kLog2Pi = 1.8378770664093453;  // log(2 pi), likelihood.py:38
 constexpr int kOuter = 4;                   // outer block = 4 x 128 columns
 constexpr int kResults = 13;                // loglik, grad[3], fisher[9]
@@ -568,7 +578,7 @@ struct Launcher {
     for (size_t i = 0; i < pkind.size(); ++i) {
       float ms = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&ms, prof->kev[2 * i], prof->kev[2 * i + 1]));
-      const int base = pkind[i] == 0 ? 0 : 4;
+      const int base = pkind[i] == 0 ? 0 : pkind[i] == 1 ? 4 : 10;
       st[base] += 1.0;
       st[base + 1] += ms;
       st[base + 2] += pwork[i];
@@ -1309,9 +1319,15 @@ int run_chunk(Item* items, int m) {
     ga.n = (int)lead->n;
     return std::make_pair(ga, ng);
   };
+  // generation bytes of one launch set: 8 B per lower-triangle element per matrix written
+  const double tri_bytes = 8.0 * (double)lead->n * ((double)lead->n + 1.0) / 2.0;
   auto sig = gen_set(true);
   if (sig.second > 0) {
     run.launches += 2;
+    {
+      int rc = run.prof_begin(s);
+      if (rc) return rc;
+    }
     launch_gen_table(sig.first, sig.second, false, s);
     // Sigma: the first outer block's columns on the main stream (all the Cholesky's first
     // inner steps read), the rest on the low-priority aux stream under those steps, so the
@@ -1333,6 +1349,10 @@ int run_chunk(Item* items, int m) {
       launch_gen_engine(sig.first, sig.second, s);
     }
     CUDA_TRY(cudaGetLastError());
+    {  // (kernel profiling serialises: aux == s, one launch)
+      int rc = run.prof_end(s, 2, tri_bytes * sig.second);
+      if (rc) return rc;
+    }
   }
   // derivative matrices: eval_all items first (the solves wait for these only), then the
   // speculative loglik items
@@ -1364,17 +1384,21 @@ int run_chunk(Item* items, int m) {
     };
     if (nn > 0) {
       run.launches += 2;
+      if ((rc = run.prof_begin(aux))) return rc;
       launch_gen_table(now, nn, true, aux);
       launch_gen_engine(now, nn, aux);
       CUDA_TRY(cudaGetLastError());
+      if ((rc = run.prof_end(aux, 2, 2.0 * tri_bytes * nn))) return rc;
     }
     if ((rc = identities(false))) return rc;
     CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
     if (nl > 0) {
       run.launches += 2;
+      if ((rc = run.prof_begin(aux))) return rc;
       launch_gen_table(later, nl, true, aux);
       launch_gen_engine(later, nl, aux);
       CUDA_TRY(cudaGetLastError());
+      if ((rc = run.prof_end(aux, 2, 2.0 * tri_bytes * nl))) return rc;
     }
     if ((rc = identities(true))) return rc;
   } else {
@@ -1690,6 +1714,21 @@ int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out) {
 
 int mle_release_cached_memory(void) {
   cache_trim(-2);
+  std::lock_guard<std::mutex> lock(g_sets_mutex);
+  for (size_t d = 0; d < g_sets.size(); ++d) {
+    if (g_sets[d].empty()) continue;
+    cudaSetDevice((int)d);
+    for (StreamSet& st : g_sets[d]) {
+      for (cudaEvent_t e : st.ev) cudaEventDestroy(e);
+      for (cudaEvent_t e : st.pool) cudaEventDestroy(e);
+      for (cudaEvent_t e : st.clk)
+        if (e) cudaEventDestroy(e);
+      cudaEventDestroy(st.ev_der);
+      cudaEventDestroy(st.spec_done);
+      for (cudaStream_t q : {st.stream, st.side, st.inner, st.aux}) cudaStreamDestroy(q);
+    }
+    g_sets[d].clear();
+  }
   return MLE_OK;
 }
 
@@ -1738,16 +1777,39 @@ static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n,
   } while (0)
   // Priorities: the latency-bound factorization chain (main, look-ahead) wins SMs over the
   // throughput work on aux (derivative generation, speculation) as CTAs retire.
-  int prio_low = 0, prio_high = 0;
-  CTX_TRY(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
-  CTX_TRY(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_high));
-  CTX_TRY(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_high));
-  CTX_TRY(cudaStreamCreateWithPriority(&c->inner, cudaStreamNonBlocking, prio_high));
-  CTX_TRY(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_low));
-  for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
-  CTX_TRY(cudaEventCreateWithFlags(&c->ev_der, cudaEventDisableTiming));
-  CTX_TRY(cudaEventCreateWithFlags(&c->spec_done, cudaEventDisableTiming));
-  for (auto& e : c->pool) CTX_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  bool recycled = false;
+  {
+    std::lock_guard<std::mutex> lock(g_sets_mutex);
+    if ((int)g_sets.size() > device && !g_sets[device].empty()) {
+      const StreamSet st = g_sets[device].back();
+      g_sets[device].pop_back();
+      c->stream = st.stream;
+      c->side = st.side;
+      c->inner = st.inner;
+      c->aux = st.aux;
+      for (int i = 0; i < 5; ++i) c->ev[i] = st.ev[i];
+      c->ev_der = st.ev_der;
+      c->spec_done = st.spec_done;
+      for (int i = 0; i < kPoolEvents; ++i) c->pool[i] = st.pool[i];
+      c->pass_clock.start = st.clk[0];
+      c->pass_clock.pre = st.clk[1];
+      c->pass_clock.end[0] = st.clk[2];
+      c->pass_clock.end[1] = st.clk[3];
+      recycled = true;
+    }
+  }
+  if (!recycled) {
+    int prio_low = 0, prio_high = 0;
+    CTX_TRY(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+    CTX_TRY(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_high));
+    CTX_TRY(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_high));
+    CTX_TRY(cudaStreamCreateWithPriority(&c->inner, cudaStreamNonBlocking, prio_high));
+    CTX_TRY(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_low));
+    for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
+    CTX_TRY(cudaEventCreateWithFlags(&c->ev_der, cudaEventDisableTiming));
+    CTX_TRY(cudaEventCreateWithFlags(&c->spec_done, cudaEventDisableTiming));
+    for (auto& e : c->pool) CTX_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   CTX_TRY(dmalloc(&c->lx, sizeof(double) * n));
   CTX_TRY(dmalloc(&c->ly, sizeof(double) * n));
   CTX_TRY(dmalloc(&c->z, sizeof(double) * n));
@@ -1798,9 +1860,6 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->smat);
   dfree(c->linv);
   dfree(c->fail_flag);
-  for (cudaEvent_t e : {c->pass_clock.start, c->pass_clock.pre, c->pass_clock.end[0],
-                        c->pass_clock.end[1]})
-    if (e) cudaEventDestroy(e);
   dfree(c->fail_idx);
   dfree(c->partials);
   dfree(c->out);
@@ -1824,17 +1883,45 @@ void mle_ctx_destroy(mle_ctx* c) {
   dfree(c->wex);
   if (c->h_theta) dfree(c->h_theta);
   if (c->h_res) dfree(c->h_res);
-  for (auto& e : c->ev)
-    if (e) cudaEventDestroy(e);
-  for (auto& e : c->pool)
-    if (e) cudaEventDestroy(e);
   for (auto& e : c->kev) cudaEventDestroy(e);
-  if (c->ev_der) cudaEventDestroy(c->ev_der);
-  if (c->spec_done) cudaEventDestroy(c->spec_done);
-  if (c->side) cudaStreamDestroy(c->side);
-  if (c->inner) cudaStreamDestroy(c->inner);
-  if (c->aux) cudaStreamDestroy(c->aux);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  bool complete = c->stream && c->side && c->inner && c->aux && c->ev_der && c->spec_done;
+  for (auto& e : c->ev) complete = complete && e;
+  for (auto& e : c->pool) complete = complete && e;
+  const bool idle = complete && cudaStreamSynchronize(c->side) == cudaSuccess &&
+                    cudaStreamSynchronize(c->inner) == cudaSuccess &&
+                    cudaStreamSynchronize(c->aux) == cudaSuccess;
+  if (idle) {  // hand the stream set to the next context on this device
+    StreamSet st;
+    st.stream = c->stream;
+    st.side = c->side;
+    st.inner = c->inner;
+    st.aux = c->aux;
+    for (int i = 0; i < 5; ++i) st.ev[i] = c->ev[i];
+    st.ev_der = c->ev_der;
+    st.spec_done = c->spec_done;
+    for (int i = 0; i < kPoolEvents; ++i) st.pool[i] = c->pool[i];
+    st.clk[0] = c->pass_clock.start;
+    st.clk[1] = c->pass_clock.pre;
+    st.clk[2] = c->pass_clock.end[0];
+    st.clk[3] = c->pass_clock.end[1];
+    std::lock_guard<std::mutex> lock(g_sets_mutex);
+    if ((int)g_sets.size() <= c->device) g_sets.resize(c->device + 1);
+    g_sets[c->device].push_back(st);
+  } else {
+    for (cudaEvent_t e : {c->pass_clock.start, c->pass_clock.pre, c->pass_clock.end[0],
+                          c->pass_clock.end[1]})
+      if (e) cudaEventDestroy(e);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : c->pool)
+      if (e) cudaEventDestroy(e);
+    if (c->ev_der) cudaEventDestroy(c->ev_der);
+    if (c->spec_done) cudaEventDestroy(c->spec_done);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->inner) cudaStreamDestroy(c->inner);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->stream) cudaStreamDestroy(c->stream);
+  }
   delete c;
 }
 

@@ -123,13 +123,16 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
       tj += a.jcut;
     }
   }
-  stage_params(&P, it.P);
   const int lane_row = threadIdx.x & (kGT - 1);
   const int col0 = threadIdx.x >> 5;
   const int i = ti * kGT + lane_row;
   const long long ld = a.ld;
   const int n = a.n;
   if (ti != tj && (ti + 1) * kGT <= n && it.tab != nullptr) {
+    // Interior tile: the parameters are read straight from global memory (L1-resident: a few
+    // scalars and the interval arrays) instead of staging all ~7 KB per CTA, which cost as
+    // much L1 traffic as the tile's own output.
+    const ThetaParams& P = *it.P;
     const double xi = it.lx[i], yi = it.ly[i];
     const double lo = P.tab_lo, hi = P.tab_hi, alpha = P.alpha;
     const long long j0 = (long long)tj * kGT + col0;
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
       }
     }
   } else {
+    stage_params(&P, it.P);
 #pragma unroll 1
     for (int r = 0; r < kGT / 8; ++r) {
       const int jl = col0 + 8 * r;
@@ -229,11 +233,12 @@ __global__ void __launch_bounds__(kGThreads) gen_panel_kernel(GenArgs a, const i
 
 // Polynomial pieces of e^u * {c, dalpha, dnu}(u) on every table interval of every item (grid:
 // MLE_TAB_MAX x items; one CTA per interval).  Node values come from the exact evaluator
-// (matern_u), so the table inherits its accuracy: Chebyshev interpolation at 14 nodes (a
-// convergence factor ~22 per interval puts the degree-13 truncation far below one ulp), then
-// converted to the monomial basis in t in [-1, 1] for a one-FMA-per-term Horner evaluation.
-// The conversion is benign: |a_i| <~ sum_j |c_j| |T_j coefficients| with |c_j| ~ 22^-j against
-// coefficient growth (1 + sqrt 2)^j.  Layout [interval][power][c, dalpha, dnu, pad].
+// (matern_u), so the table inherits its accuracy: Chebyshev interpolation at 14 nodes on
+// intervals of log ratio 1.2 (a convergence factor ~22 puts the degree-13 truncation far
+// below one ulp), then converted to the monomial basis in t in [-1, 1] for a one-FMA-per-term
+// Horner evaluation.  The conversion is benign: |a_i| <~ sum_j |c_j| |T_j coefficients| with
+// |c_j| ~ 22^-j against coefficient growth (1 + sqrt 2)^j.  Layout [interval][c, da, dn]
+// [power] (16-byte aligned power pairs: the evaluator loads two coefficients per request).
 __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
   const GenItem& it = a.item[blockIdx.y];
   if (it.tab == nullptr || (it.fail_flag != nullptr && *it.fail_flag)) return;
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
       // higher j first would be marginally better; terms shrink ~22x per j either way
       for (int i = 0; i <= j; ++i) acc[i] = fma(cc[t][j], Tn[i], acc[i]);
     }
-    for (int i = 0; i < MLE_TAB_P; ++i) it.tab[((size_t)k * MLE_TAB_P + i) * 4 + t] = acc[i];
+    for (int i = 0; i < MLE_TAB_P; ++i) it.tab[((size_t)k * 3 + t) * MLE_TAB_P + i] = acc[i];
   }
 }
 

@@ -245,8 +245,22 @@ __device__ __forceinline__ int gen_tab_index(const ThetaParams& P, double u) {
   return P.seg_base[s] + k;
 }
 
-// tab: [MLE_TAB_MAX][MLE_TAB_P][4] monomial coefficients (powers of t in [-1, 1]) of
-// e^u * {c, dalpha, dnu}; Horner, one FMA per term.
+// tab: [MLE_TAB_MAX][3][MLE_TAB_P] monomial coefficients (powers of t in [-1, 1]) of
+// e^u * {c, dalpha, dnu}; Horner, one FMA per term, coefficients loaded in 16-byte pairs
+// (the L1 request count, not the arithmetic, bounds the generation kernels).
+__device__ __forceinline__ double horner_pairs(const double* __restrict__ c, double t) {
+  static_assert(MLE_TAB_P % 2 == 0, "pairs");
+  double2 q = __ldg(reinterpret_cast<const double2*>(c + MLE_TAB_P - 2));
+  double p = fma(q.y, t, q.x);
+#pragma unroll
+  for (int i = MLE_TAB_P - 4; i >= 0; i -= 2) {
+    q = __ldg(reinterpret_cast<const double2*>(c + i));
+    p = fma(p, t, q.y);
+    p = fma(p, t, q.x);
+  }
+  return p;
+}
+
 template <bool kDerivs>
 __device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
                                                    const double* __restrict__ tab, double u) {
@@ -254,26 +268,13 @@ __device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
   const double t = (u - P.tab_ctr[k]) * P.tab_ihw[k];
   // below 8.5 the series are of E itself (no e^u scaling error); above, of e^u E
   const double eu = u < MLE_SMALL_MID_SPLIT ? 1.0 : exp(-u);
-  const double* c = tab + (size_t)k * MLE_TAB_P * 4;
+  const double* c = tab + (size_t)k * 3 * MLE_TAB_P;
   MaternVals out;
+  out.c = eu * horner_pairs(c, t);
   if (kDerivs) {
-    double2 ca = __ldg(reinterpret_cast<const double2*>(c + 4 * (MLE_TAB_P - 1)));
-    double pc = ca.x, pa = ca.y, pn = __ldg(c + 4 * (MLE_TAB_P - 1) + 2);
-#pragma unroll
-    for (int i = MLE_TAB_P - 2; i >= 0; --i) {
-      const double2 q = __ldg(reinterpret_cast<const double2*>(c + 4 * i));
-      pc = fma(pc, t, q.x);
-      pa = fma(pa, t, q.y);
-      pn = fma(pn, t, __ldg(c + 4 * i + 2));
-    }
-    out.c = eu * pc;
-    out.dalpha = eu * pa;
-    out.dnu = eu * pn;
+    out.dalpha = eu * horner_pairs(c + MLE_TAB_P, t);
+    out.dnu = eu * horner_pairs(c + 2 * MLE_TAB_P, t);
   } else {
-    double pc = __ldg(c + 4 * (MLE_TAB_P - 1));
-#pragma unroll
-    for (int i = MLE_TAB_P - 2; i >= 0; --i) pc = fma(pc, t, __ldg(c + 4 * i));
-    out.c = eu * pc;
     out.dalpha = 0.0;
     out.dnu = 0.0;
   }

@@ -16,9 +16,9 @@
 #define MLE_CASE3_FAR 8          // bessel.py:54
 #define MLE_CASE4_TERMS 5        // bessel.py:55
 #define MLE_U_COEFF_STRIDE 40    // >= 3*12+1 coefficients per Debye polynomial
-#define MLE_TAB_P 14              // Chebyshev points per interval (degree 13)
-#define MLE_TAB_MAX 48            // intervals per table
-#define MLE_TAB_DOUBLES (MLE_TAB_MAX * MLE_TAB_P * 4)  // [interval][power][c, da, dn, pad]
+#define MLE_TAB_P 14              // interpolation points per interval (degree 13, even)
+#define MLE_TAB_MAX 48            // intervals per table (log ratio <= 1.2)
+#define MLE_TAB_DOUBLES (MLE_TAB_MAX * 3 * MLE_TAB_P)  // [interval][c, da, dn][power]
 #define MLE_TAB_LO 0.25           // below: exact evaluation (few pairs)
 #define MLE_TAB_HI 800.0          // above: exact evaluation (elements underflow anyway)
 #define MLE_SMALL_MID_SPLIT 8.5  // bessel.py:46

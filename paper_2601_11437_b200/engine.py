@@ -117,13 +117,15 @@ class Engine:
 
     def kernel_stats(self) -> dict:
         """Per-kernel sums of the last profiled pass (see mle_kernel_stats)."""
-        out = np.zeros(10)
+        out = np.zeros(13)  # MLE_KSTATS
         nat.check(nat.lib.mle_kernel_stats(self._ctx, nat.as_ptr(out)))
         return {"gemm_launches": int(out[0]), "gemm_ms": float(out[1]),
                 "gemm_fp64_flops": float(out[2]), "gemm_int8_ops": float(out[3]),
                 "slice_launches": int(out[4]), "slice_ms": float(out[5]),
                 "slice_bytes": float(out[6]), "host_enqueue_ms": float(out[7]),
-                "gpu_gap_ms": float(out[8]), "spec_wait_ms": float(out[9])}
+                "gpu_gap_ms": float(out[8]), "spec_wait_ms": float(out[9]),
+                "gen_launches": int(out[10]), "gen_ms": float(out[11]),
+                "gen_bytes": float(out[12])}
 
     def phase_times(self) -> dict:
         out = np.zeros(len(nat.PHASES) + 3)
