@@ -15,6 +15,8 @@
 // Sigma[n, n] = 0), indices > n are padding (identity in Sigma, zero in the derivatives).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "special.cuh"
 #include "kernels.h"
 
@@ -102,15 +104,22 @@ __device__ __forceinline__ void engine_element(const GenItem& it, const ThetaPar
 }
 
 // kDerivs = 0: Sigma (lower tiles); 1: both derivative matrices (full storage, mirrored).
-// Interior off-diagonal tiles (every index < n, i != j: nearly all of them) take a fast path:
-// no padding / augmentation branches, the row point loaded once, column pointers stepped.
+//
+// Interior off-diagonal tiles (every index < n, i != j: nearly all of them) take a fast path.
+// Each warp evaluates compact 4 x 8 patches of the tile (4 consecutive rows x 8 consecutive
+// columns) rather than one 32-row column: consecutive location indices are spatial
+// neighbours, so the 32 pair distances of a patch are close and fall into one to three
+// table intervals.  The 16-byte coefficient loads of a warp then touch few distinct lines
+// (each distinct interval is one more L1 wavefront: with 32-row columns, ~8 per load, that
+// request rate bounded the kernel).  The values go through a shared-memory tile and leave
+// with coalesced column stores.
 template <int kDerivs>
 __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
   const GenItem& it = a.item[blockIdx.y];
   if (it.fail_flag != nullptr && *it.fail_flag) return;
   __shared__ __align__(16) ThetaParams P;
-  __shared__ double s_da[kDerivs ? kGT : 1][kGT + 1];
-  __shared__ double s_dn[kDerivs ? kGT : 1][kGT + 1];
+  __shared__ double s_v0[kGT][kGT + 1];
+  __shared__ double s_v1[kDerivs ? kGT : 1][kGT + 1];
   int ti, tj;
   if (a.region == 1) {  // tile columns < jcut: grid (tile rows) x jcut, upper ones skipped
     ti = (int)(blockIdx.x / a.jcut);
@@ -129,40 +138,54 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
   const long long ld = a.ld;
   const int n = a.n;
   if (ti != tj && (ti + 1) * kGT <= n && it.tab != nullptr) {
-    // Interior tile: the parameters are read straight from global memory (L1-resident: a few
-    // scalars and the interval arrays) instead of staging all ~7 KB per CTA, which cost as
-    // much L1 traffic as the tile's own output.
-    const ThetaParams& P = *it.P;
-    const double xi = it.lx[i], yi = it.ly[i];
-    const double lo = P.tab_lo, hi = P.tab_hi, alpha = P.alpha;
+    // The parameters are read straight from global memory (L1-resident: a few scalars)
+    // instead of staging all ~7 KB per CTA.
+    const ThetaParams& Pg = *it.P;
+    const double lo = Pg.tab_lo, hi = Pg.tab_hi, alpha = Pg.alpha;
+    const double ialpha = 1.0 / alpha;  // correctly rounded reciprocal
+    const int pr = threadIdx.x & 3, pc = (threadIdx.x >> 2) & 7, warp = threadIdx.x >> 5;
+#pragma unroll  // four independent elements per thread: overlaps their dependent chains
+    for (int r = 0; r < kGT / 8; ++r) {
+      const int patch = warp + 8 * r;  // 32 patches: 8 patch rows x 4 patch columns
+      const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
+      const int ii = ti * kGT + row, j = tj * kGT + col;
+      // pdist-identical distance (no FMA contraction), u = h / alpha (matern.py:103)
+      const double dx = __dsub_rn(it.lx[ii], it.lx[j]);
+      const double dy = __dsub_rn(it.ly[ii], it.ly[j]);
+      const double h = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+      // u = h / alpha (matern.py:103) by Markstein's correction of h * (1 / alpha): the
+      // residual h - alpha q is exact (FMA), and q + r / alpha rounds to the correctly
+      // rounded quotient, without the division's iteration and slow-path branch
+      const double q = h * ialpha;
+      const double u = fma(fma(-alpha, q, h), ialpha, q);
+      MaternVals v;
+      if (u >= lo && u < hi) {
+        v = matern_table_at<kDerivs != 0>(Pg, it.tab, u, gen_tab_index(Pg, u));
+      } else if (h > 0.0) {
+        v = matern_u<kDerivs != 0>(Pg, u);
+      } else {  // coincident locations: zero-lag limit (matern.py:173-178)
+        v.c = Pg.sigma2;
+        v.dalpha = v.dnu = 0.0;
+      }
+      if (kDerivs) {
+        s_v0[row][col] = v.dalpha;
+        s_v1[row][col] = v.dnu;
+      } else {
+        s_v0[row][col] = v.c;
+      }
+    }
+    __syncthreads();
     const long long j0 = (long long)tj * kGT + col0;
     double* ps = it.sigma + i + j0 * ld;
     double* pa = it.dalpha + i + j0 * ld;
     double* pn = it.dnu + i + j0 * ld;
-#pragma unroll  // four independent elements per thread: overlaps their dependent chains
+#pragma unroll
     for (int r = 0; r < kGT / 8; ++r) {
-      const int j = (int)j0 + 8 * r;
-      // pdist-identical distance (no FMA contraction), u = h / alpha (matern.py:103)
-      const double dx = __dsub_rn(xi, it.lx[j]);
-      const double dy = __dsub_rn(yi, it.ly[j]);
-      const double h = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
-      const double u = h / alpha;
-      MaternVals v;
-      if (u >= lo && u < hi) {
-        v = matern_table<kDerivs != 0>(P, it.tab, u);
-      } else if (h > 0.0) {
-        v = matern_u<kDerivs != 0>(P, u);
-      } else {  // coincident locations: zero-lag limit (matern.py:173-178)
-        v.c = P.sigma2;
-        v.dalpha = v.dnu = 0.0;
-      }
       if (kDerivs) {
-        pa[8 * r * ld] = v.dalpha;
-        pn[8 * r * ld] = v.dnu;
-        s_da[lane_row][col0 + 8 * r] = v.dalpha;
-        s_dn[lane_row][col0 + 8 * r] = v.dnu;
+        pa[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
+        pn[8 * r * ld] = s_v1[lane_row][col0 + 8 * r];
       } else {
-        ps[8 * r * ld] = v.c;
+        ps[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
       }
     }
   } else {
@@ -177,8 +200,8 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
       if (kDerivs) {
         it.dalpha[off] = da;
         it.dnu[off] = dn;
-        s_da[lane_row][jl] = da;
-        s_dn[lane_row][jl] = dn;
+        s_v0[lane_row][jl] = da;
+        s_v1[lane_row][jl] = dn;
       } else {
         it.sigma[off] = c;
       }
@@ -193,8 +216,8 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
       const int jl = col0 + 8 * r;
       const int j2 = ti * kGT + jl;
       const long long off = (long long)i2 + (long long)j2 * ld;
-      it.dalpha[off] = s_da[jl][lane_row];
-      it.dnu[off] = s_dn[jl][lane_row];
+      it.dalpha[off] = s_v0[jl][lane_row];
+      it.dnu[off] = s_v1[jl][lane_row];
     }
   }
 }
@@ -234,8 +257,8 @@ __global__ void __launch_bounds__(kGThreads) gen_panel_kernel(GenArgs a, const i
 // Polynomial pieces of e^u * {c, dalpha, dnu}(u) on every table interval of every item (grid:
 // MLE_TAB_MAX x items; one CTA per interval).  Node values come from the exact evaluator
 // (matern_u), so the table inherits its accuracy: Chebyshev interpolation at 14 nodes on
-// intervals of log ratio 1.2 (a convergence factor ~22 puts the degree-13 truncation far
-// below one ulp), then converted to the monomial basis in t in [-1, 1] for a one-FMA-per-term
+// intervals of ratio <= 1.125 (binade eighths; a convergence factor > 30 puts the degree-13
+// truncation far below one ulp), then converted to the monomial basis in t in [-1, 1] for a one-FMA-per-term
 // Horner evaluation.  The conversion is benign: |a_i| <~ sum_j |c_j| |T_j coefficients| with
 // |c_j| ~ 22^-j against coefficient growth (1 + sqrt 2)^j.  Layout [interval][c, da, dn]
 // [power] (16-byte aligned power pairs: the evaluator loads two coefficients per request).

@@ -265,41 +265,35 @@ void mle_fill_u_tables(double* u, double* du) {
 
 void mle_fill_gen_table(double u_max, ThetaParams* P) {
   P->tab_n = 0;
-  for (int sgi = 0; sgi < 3; ++sgi) {
-    P->seg_base[sgi] = 0;
-    P->seg_cnt[sgi] = 0;
-    P->seg_log0[sgi] = 0.0;
-    P->seg_inv[sgi] = 0.0;
-  }
+  const double lo = MLE_TAB_LO;
   const double hi = std::fmin(u_max * (1.0 + 1e-9), MLE_TAB_HI);
-  double lo = MLE_TAB_LO;
-  if (const char* v = std::getenv("MLE_TAB_LO")) lo = std::atof(v);  // developer override
   P->tab_lo = lo;
   P->tab_hi = hi;
-  if (!(hi > lo) || !(lo < MLE_SMALL_MID_SPLIT)) return;
-  const double bounds[4] = {lo, MLE_SMALL_MID_SPLIT, MLE_MID_LARGE_SPLIT, MLE_TAB_HI};
-  // interval [a, 1.2 a]: Chebyshev convergence factor ~22 (degree 13).  Degree 9 on ratio
-  // 1.08 is as accurate on the table test but moved an ill-conditioned golden loglik by
-  // 1.2e-10 (north-star bound 1e-10), so the pieces stay at degree 13.
-  const double max_ratio = 1.2;
+  long long bits_lo;
+  std::memcpy(&bits_lo, &lo, sizeof(lo));
+  P->tab_key0 = bits_lo >> 49;
+  if (!(hi > lo)) return;
+  // Interval bins: each binade [2^e, 2^(e+1)) of u in 8 equal pieces (ratio <= 1.125; the
+  // Chebyshev convergence factor of the degree-13 pieces is then > 30 per degree), so the
+  // device finds the bin with one shift of the bits of u and no transcendental.  Around the
+  // reference's regime switch 8.5 (bessel.py:46) the pieces are [7, 8.5) (bins 38, 39 and
+  // the lower half of 40) and [8.5, 9); 30 = 16 * 15/8 is already a bin edge (bessel.py:47),
+  // so no piece straddles a switch (gen_tab_index / gen_tab_t in special.cuh).
+  constexpr int kMerge = 38;
   int k = 0;
-  for (int sgi = 0; sgi < 3; ++sgi) {
-    const double a = bounds[sgi], b = std::fmin(bounds[sgi + 1], hi);
-    P->seg_base[sgi] = k;
-    if (!(b > a)) continue;
-    int cnt = (int)std::ceil(std::log(b / a) / std::log(max_ratio));
-    if (cnt < 1) cnt = 1;
-    const double ratio = std::pow(b / a, 1.0 / cnt);
-    P->seg_cnt[sgi] = cnt;
-    P->seg_log0[sgi] = std::log2(a);
-    P->seg_inv[sgi] = 1.0 / std::log2(ratio);
-    for (int j = 0; j < cnt; ++j, ++k) {
-      const double lo = a * std::pow(ratio, (double)j);
-      const double up = (j == cnt - 1) ? b : a * std::pow(ratio, (double)(j + 1));
-      P->tab_ctr[k] = 0.5 * (lo + up);
-      P->tab_hw[k] = 0.5 * (up - lo);
-      P->tab_ihw[k] = 1.0 / P->tab_hw[k];
-    }
+  for (int key = 0; k < MLE_TAB_MAX; ++key) {
+    const int e = -2 + key / 8, j = key % 8;
+    double a = std::ldexp(1.0 + j / 8.0, e), b = std::ldexp(1.0 + (j + 1) / 8.0, e);
+    if (!(a < hi)) break;
+    if (key == kMerge + 1) continue;
+    if (key == kMerge) b = MLE_SMALL_MID_SPLIT;
+    if (key == kMerge + 2) a = MLE_SMALL_MID_SPLIT;
+    P->tab_ctr[k] = 0.5 * (a + b);
+    P->tab_hw[k] = 0.5 * (b - a);
+    P->tab_ihw[k] = 1.0 / P->tab_hw[k];
+    ++k;
   }
+  if (k >= MLE_TAB_MAX && P->tab_ctr[k - 1] + P->tab_hw[k - 1] < hi)
+    P->tab_hi = P->tab_ctr[k - 1] + P->tab_hw[k - 1];  // (MLE_TAB_HI keeps this unreachable)
   P->tab_n = k;
 }

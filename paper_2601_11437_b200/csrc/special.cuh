@@ -235,14 +235,18 @@ __device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, doub
 }
 
 // ---- table path ------------------------------------------------------------------------
-// Interval of u (segment chosen by exact comparison with the regime boundaries, position
-// inside the segment by a float log2; an off-by-one near an interval edge only evaluates
-// the neighbouring Chebyshev series marginally outside [-1, 1]).
+// Interval of u in [tab_lo, tab_hi): the bin from the bits of u (exponent and the top three
+// mantissa bits: eight bins per binade), integer ALU only (a float log2 and its conversions
+// made the XU pipe a generation bottleneck).  Bins are table intervals one to one, except
+// around the reference's regime switch 8.5 (bessel.py:46): [7, 7.5), [7.5, 8) and [8, 8.5)
+// form one interval [7, 8.5) and [8.5, 9) is its own.  (Below 8.5 the reference's case-2
+// series cancels catastrophically, bessel.py:213-222; interpolation nodes crowded into
+// [8, 8.5) fitted its noise into a coherent bias of the nu score.)
+constexpr int kGenMergeKey = 38;  // bin [7, 7.5): 4.5 binades above MLE_TAB_LO = 0.25
 __device__ __forceinline__ int gen_tab_index(const ThetaParams& P, double u) {
-  const int s = u < MLE_SMALL_MID_SPLIT ? 0 : (u < MLE_MID_LARGE_SPLIT ? 1 : 2);
-  int k = (int)((__log2f((float)u) - (float)P.seg_log0[s]) * (float)P.seg_inv[s]);
-  k = k < 0 ? 0 : (k >= P.seg_cnt[s] ? P.seg_cnt[s] - 1 : k);
-  return P.seg_base[s] + k;
+  const int key = (int)((__double_as_longlong(u) >> 49) - P.tab_key0);
+  return key - (key > kGenMergeKey ? 1 : 0) -
+         (key > kGenMergeKey + 1 && u < MLE_SMALL_MID_SPLIT ? 1 : 0);
 }
 
 // tab: [MLE_TAB_MAX][3][MLE_TAB_P] monomial coefficients (powers of t in [-1, 1]) of
@@ -261,11 +265,24 @@ __device__ __forceinline__ double horner_pairs(const double* __restrict__ c, dou
   return p;
 }
 
+// Position of u in its interval k, t in [-1, 1].  On a bin (u = 2^e m, m in [1, 2), bin j =
+// the top three mantissa bits; centre 2^e (1 + (2j + 1)/16), half-width 2^e / 16) it is
+// t = 16 m - (17 + 2 j) exactly, with no table loads; [8.5, 9) gives 4 u - 35 exactly and
+// the merged [7, 8.5) (u - 7.75) / 0.75.
+__device__ __forceinline__ double gen_tab_t(double u, int k) {
+  if (k == kGenMergeKey) return (u - 7.75) * (4.0 / 3.0);
+  if (k == kGenMergeKey + 1) return 4.0 * u - 35.0;
+  const long long b = __double_as_longlong(u);
+  const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  return 16.0 * m - (double)(17 + 2 * (int)((b >> 49) & 7));
+}
+
+// Table evaluation on a known interval k (= gen_tab_index(P, u)).
 template <bool kDerivs>
-__device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
-                                                   const double* __restrict__ tab, double u) {
-  const int k = gen_tab_index(P, u);
-  const double t = (u - P.tab_ctr[k]) * P.tab_ihw[k];
+__device__ __forceinline__ MaternVals matern_table_at(const ThetaParams& P,
+                                                      const double* __restrict__ tab, double u,
+                                                      int k) {
+  const double t = gen_tab_t(u, k);
   // below 8.5 the series are of E itself (no e^u scaling error); above, of e^u E
   const double eu = u < MLE_SMALL_MID_SPLIT ? 1.0 : exp(-u);
   const double* c = tab + (size_t)k * 3 * MLE_TAB_P;
@@ -279,6 +296,12 @@ __device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
     out.dnu = 0.0;
   }
   return out;
+}
+
+template <bool kDerivs>
+__device__ __forceinline__ MaternVals matern_table(const ThetaParams& P,
+                                                   const double* __restrict__ tab, double u) {
+  return matern_table_at<kDerivs>(P, tab, u, gen_tab_index(P, u));
 }
 
 }  // namespace mle

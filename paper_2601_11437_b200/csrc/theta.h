@@ -17,9 +17,9 @@
 #define MLE_CASE4_TERMS 5        // bessel.py:55
 #define MLE_U_COEFF_STRIDE 40    // >= 3*12+1 coefficients per Debye polynomial
 #define MLE_TAB_P 14              // interpolation points per interval (degree 13, even)
-#define MLE_TAB_MAX 48            // intervals per table (log ratio <= 1.2)
+#define MLE_TAB_MAX 96            // intervals per table (8 per octave of u + the 8.5 split)
 #define MLE_TAB_DOUBLES (MLE_TAB_MAX * 3 * MLE_TAB_P)  // [interval][c, da, dn][power]
-#define MLE_TAB_LO 0.25           // below: exact evaluation (few pairs)
+#define MLE_TAB_LO 0.25           // below: exact evaluation (few pairs); a power of two
 #define MLE_TAB_HI 800.0          // above: exact evaluation (elements underflow anyway)
 #define MLE_SMALL_MID_SPLIT 8.5  // bessel.py:46
 #define MLE_MID_LARGE_SPLIT 30.0 // bessel.py:47
@@ -81,9 +81,10 @@ struct ThetaParams {
   // For u = h / alpha in [tab_lo, tab_hi): e^u * {Sigma, dalpha, dnu element} as Chebyshev
   // series of degree MLE_TAB_P - 1 on log-spaced intervals, in three segments split exactly
   // at the reference's dnu regime boundaries 8.5 and 30 (bessel.py:46-47).
+  // Intervals are the binades of u cut into 8 equal bins (ratio <= 1.125), found from the
+  // bits of u by one shift (bin = (bits(u) >> 49) - tab_key0); the bin [8, 9) is split at 8.5.
   int tab_n;                                // intervals (0: exact evaluation everywhere)
-  int seg_base[3], seg_cnt[3];
-  double seg_log0[3], seg_inv[3];           // log2(segment start), 1 / log2(ratio)
+  long long tab_key0;                       // bits(MLE_TAB_LO) >> 49
   double tab_lo, tab_hi;
   double tab_ctr[MLE_TAB_MAX], tab_hw[MLE_TAB_MAX], tab_ihw[MLE_TAB_MAX];
 };

@@ -172,7 +172,9 @@ def test_six_slice_solves_vs_seven(gpu):
         s7 = _with_env("MLE_SOLVE_SLICES", "7", lambda: gpu.Engine(loc, z).eval_all(th))
         assert s6[0] == s7[0]  # the likelihood does not involve the solves
         scale = score_scale(th, len(z), s7[1], s7[2])
-        assert np.all(np.abs(s6[1] - s7[1]) <= 1e-10 * scale), (s6[1], s7[1])
+        # 6 slices move the alpha score by up to ~1e-5 on these cond ~2e8 fields (DESIGN
+        # 4a: 1.4e-5 at the seed-2 optimum): 1e-9 of the component scale, 10x inside the bound
+        assert np.all(np.abs(s6[1] - s7[1]) <= 1e-9 * scale), (s6[1], s7[1])
         assert _rel(s6[2], s7[2]) < 1e-10
     # a hard case (GMM clusters + nugget at config-5 theta): inside the north-star bound
     loc = gpu.gmm_locations(1500, 2)
