@@ -2,6 +2,11 @@
 breakdown (gen / Cholesky / solves / reductions).  Writes one JSON record to stdout.
 
     python tools/run_config.py config3 [--breakdown-only]
+    python tools/run_config.py config5 --loglik-only
+
+--loglik-only: the one-GPU share of a config that does not fit eval_all on one B200
+(config 5: Sigma, three derivative blocks and M are 4 x 80 GB): field simulation, then
+log-likelihoods at theta_true and two nearby thetas (Sigma 80 GB + factor slices 17.5 GB).
 """
 import json
 import sys
@@ -27,7 +32,20 @@ def main():
     data = m.SpatialDataset(loc, z, nugget=wl.nugget)
     eng = data.engine()
     rec = {"config": name, "n": wl.n, "theta_true": wl.theta_true, "theta0": wl.theta0,
-           "simulate_s": t_sim}
+           "nugget": wl.nugget, "simulate_s": t_sim}
+    if "--loglik-only" in sys.argv:
+        rec["loglik"] = []
+        for scale in ((1.0, 1.0, 1.0), (1.0, 1.05, 1.0), (1.1, 1.0, 0.95)):
+            th = np.array(wl.theta_true, float) * np.array(scale)
+            t0 = time.perf_counter()
+            ll = eng.loglik(th)
+            wall = time.perf_counter() - t0
+            p = eng.phase_times()
+            rec["loglik"].append({"theta": th.tolist(), "loglik": ll, "wall_s": wall,
+                                  "phases_ms": p,
+                                  "potrf_tflops": p["flops"] / (p["potrf_ms"] * 1e-3) / 1e12})
+        print(json.dumps(rec))
+        return
     # single-iteration breakdown at theta_true: a factoring eval_all and a loglik
     th = np.array(wl.theta_true, float)
     t0 = time.perf_counter()
