@@ -14,6 +14,7 @@ Usage:
     python tests/golden/make_golden.py config1
     python tests/golden/make_golden.py evals2        # config 2 seed 0 evaluations
     python tests/golden/make_golden.py fit config2 SEED
+    python tests/golden/make_golden.py fit config1 0 shift|cube
 """
 
 from __future__ import annotations
@@ -154,18 +155,32 @@ def make_evals2():
     (HERE / "config2_evals.json").write_text(json.dumps(evals, indent=1))
 
 
-def make_fit(name, seed):
+# Off-default driver variants on the config-1 data (the reference's own fisher_bt): the
+# Nelder-Mead shift forced by a gradient-call budget of 3 (optimizer.py:367-371,394-412), and
+# the paper's default start cube (cli.py:52-53) whose L9 grid hits extreme theta
+# (ill-conditioned or failing log-likelihoods -> -inf, optimizer.py:129-134).
+FIT_VARIANTS = {
+    "shift": dict(max_grad_calls=3),
+    "cube": dict(cube=((0.01, 0.01, 0.01), (5.0, 5.0, 2.0))),
+}
+
+
+def make_fit(name, seed, variant=None):
     wl = WORKLOADS[name]
     loc, z = _config_data(name, seed)
-    np.savez_compressed(HERE / f"{name}_seed{seed}_data.npz", loc=loc, z=z)
+    if variant is None:
+        np.savez_compressed(HERE / f"{name}_seed{seed}_data.npz", loc=loc, z=z)
     data = ref.SpatialDataset(loc, z)
-    th0 = ref.MaternParams(*wl.theta0)
-    cfg = ref.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    opts = dict(FIT_VARIANTS[variant]) if variant else {}
+    lo, hi = opts.pop("cube", (wl.theta0, wl.theta0))
+    cfg = ref.FisherBTConfig(theta_lower=ref.MaternParams(*lo),
+                             theta_upper=ref.MaternParams(*hi), **opts)
     t0 = time.perf_counter()
     res = ref.fisher_bt(data, cfg)
     wall = time.perf_counter() - t0
     rec = {
-        "config": name, "seed": seed, "theta0": list(wl.theta0),
+        "config": name, "seed": seed, "theta0": list(wl.theta0), "variant": variant,
+        "cube": [list(lo), list(hi)], "options": opts,
         "theta_hat": res.theta_hat.as_array().tolist(),
         "loglik_at_hat": res.loglik_at_hat,
         "fisher_at_hat": np.asarray(res.fisher_at_hat).tolist(),
@@ -176,7 +191,8 @@ def make_fit(name, seed):
         "iterate_trace": [[t.as_array().tolist(), ll] for t, ll in res.iterate_trace],
         "cpu_wall_s": wall, "cpu_threads": os.environ.get("OPENBLAS_NUM_THREADS", "default"),
     }
-    (HERE / f"{name}_seed{seed}_fit.json").write_text(json.dumps(rec, indent=1))
+    tag = f"_{variant}" if variant else ""
+    (HERE / f"{name}_seed{seed}{tag}_fit.json").write_text(json.dumps(rec, indent=1))
 
 
 if __name__ == "__main__":
@@ -190,6 +206,6 @@ if __name__ == "__main__":
     elif what == "evals2":
         make_evals2()
     elif what == "fit":
-        make_fit(sys.argv[2], int(sys.argv[3]))
+        make_fit(sys.argv[2], int(sys.argv[3]), sys.argv[4] if len(sys.argv) > 4 else None)
     else:
         raise SystemExit(f"unknown target {what}")
