@@ -143,36 +143,103 @@ __global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
     const ThetaParams& Pg = *it.P;
     const double lo = Pg.tab_lo, hi = Pg.tab_hi, alpha = Pg.alpha;
     const double ialpha = 1.0 / alpha;  // correctly rounded reciprocal
+    const long long key0 = Pg.tab_key0;
+    const double* __restrict__ tab = it.tab;
+    const double* __restrict__ lx = it.lx;
+    const double* __restrict__ ly = it.ly;
+    __shared__ unsigned short s_exact[kGT * kGT];
+    __shared__ int s_nexact;
+    if (threadIdx.x == 0) s_nexact = 0;
+    __syncthreads();
     const int pr = threadIdx.x & 3, pc = (threadIdx.x >> 2) & 7, warp = threadIdx.x >> 5;
-#pragma unroll  // four independent elements per thread: overlaps their dependent chains
-    for (int r = 0; r < kGT / 8; ++r) {
-      const int patch = warp + 8 * r;  // 32 patches: 8 patch rows x 4 patch columns
-      const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
-      const int ii = ti * kGT + row, j = tj * kGT + col;
-      // pdist-identical distance (no FMA contraction), u = h / alpha (matern.py:103)
-      const double dx = __dsub_rn(it.lx[ii], it.lx[j]);
-      const double dy = __dsub_rn(it.ly[ii], it.ly[j]);
-      const double h = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
-      // u = h / alpha (matern.py:103) by Markstein's correction of h * (1 / alpha): the
-      // residual h - alpha q is exact (FMA), and q + r / alpha rounds to the correctly
-      // rounded quotient, without the division's iteration and slow-path branch
-      const double q = h * ialpha;
-      const double u = fma(fma(-alpha, q, h), ialpha, q);
+    // kE elements at a time, their kF Horner chains interleaved (4 independent chains per
+    // thread: latency, not issue, bounded the element-serial version), branch-free for the
+    // table elements; the rare exact-path / coincident elements are patched afterwards.
+    constexpr int kF = kDerivs ? 2 : 1;
+    constexpr int kE = 4 / kF;
+#pragma unroll
+    for (int r0 = 0; r0 < kGT / 8; r0 += kE) {
+      double u[kE], t[kE];
+      int cofs[kE];
+      bool intab[kE];
+#pragma unroll
+      for (int e = 0; e < kE; ++e) {
+        const int patch = warp + 8 * (r0 + e);  // 32 patches: 8 patch rows x 4 patch columns
+        const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
+        const int ii = ti * kGT + row, j = tj * kGT + col;
+        // pdist-identical distance (no FMA contraction)
+        const double dx = __dsub_rn(lx[ii], lx[j]);
+        const double dy = __dsub_rn(ly[ii], ly[j]);
+        const double h = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+        // u = h / alpha (matern.py:103) by Markstein's correction of h * (1 / alpha): the
+        // residual h - alpha q is exact (FMA), and q + r / alpha rounds to the correctly
+        // rounded quotient, without the division's iteration and slow-path branch
+        const double q = h * ialpha;
+        u[e] = fma(fma(-alpha, q, h), ialpha, q);
+        intab[e] = u[e] >= lo && u[e] < hi;
+        const double ut = intab[e] ? u[e] : lo;  // any valid interval for the others
+        const long long b = __double_as_longlong(ut);
+        const int key = (int)((b >> 49) - key0);
+        const int k = key - (key > kGenMergeKey ? 1 : 0) -
+                      (key > kGenMergeKey + 1 && ut < MLE_SMALL_MID_SPLIT ? 1 : 0);
+        t[e] = gen_tab_t(ut, k);
+        cofs[e] = k * 3 * MLE_TAB_P + (kDerivs ? MLE_TAB_P : 0);
+      }
+      double p[kE][kF];
+#pragma unroll
+      for (int e = 0; e < kE; ++e)
+#pragma unroll
+        for (int f = 0; f < kF; ++f) {
+          const double2 c = __ldg(reinterpret_cast<const double2*>(
+              tab + cofs[e] + f * MLE_TAB_P + MLE_TAB_P - 2));
+          p[e][f] = fma(c.y, t[e], c.x);
+        }
+#pragma unroll
+      for (int i = MLE_TAB_P - 4; i >= 0; i -= 2)
+#pragma unroll
+        for (int e = 0; e < kE; ++e)
+#pragma unroll
+          for (int f = 0; f < kF; ++f) {
+            const double2 c =
+                __ldg(reinterpret_cast<const double2*>(tab + cofs[e] + f * MLE_TAB_P + i));
+            p[e][f] = fma(p[e][f], t[e], c.y);
+            p[e][f] = fma(p[e][f], t[e], c.x);
+          }
+#pragma unroll
+      for (int e = 0; e < kE; ++e) {
+        const int patch = warp + 8 * (r0 + e);
+        const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
+        // below 8.5 the series are of E itself; above, of e^u E (matern_table_at)
+        if (u[e] >= MLE_SMALL_MID_SPLIT) {
+          const double eu = exp(-u[e]);
+#pragma unroll
+          for (int f = 0; f < kF; ++f) p[e][f] *= eu;
+        }
+        if (intab[e]) {
+          s_v0[row][col] = p[e][0];
+          if (kDerivs) s_v1[row][col] = p[e][kF - 1];
+        } else {  // exact path: queued, evaluated below by the whole CTA
+          s_v0[row][col] = u[e];
+          s_exact[atomicAdd(&s_nexact, 1)] = (unsigned short)(row * kGT + col);
+        }
+      }
+    }
+    __syncthreads();
+    // The few pairs outside the table range (u < tab_lo: near neighbours, or coincident)
+    // run the exact evaluator compacted onto consecutive threads: one warp pass instead of a
+    // mostly idle warp per element (the near-diagonal tiles hold most of them).
+    for (int q = threadIdx.x; q < s_nexact; q += kGThreads) {
+      const int row = s_exact[q] / kGT, col = s_exact[q] % kGT;
+      const double ue = s_v0[row][col];
       MaternVals v;
-      if (u >= lo && u < hi) {
-        v = matern_table_at<kDerivs != 0>(Pg, it.tab, u, gen_tab_index(Pg, u));
-      } else if (h > 0.0) {
-        v = matern_u<kDerivs != 0>(Pg, u);
+      if (ue > 0.0) {
+        v = matern_u<kDerivs != 0>(Pg, ue);
       } else {  // coincident locations: zero-lag limit (matern.py:173-178)
         v.c = Pg.sigma2;
         v.dalpha = v.dnu = 0.0;
       }
-      if (kDerivs) {
-        s_v0[row][col] = v.dalpha;
-        s_v1[row][col] = v.dnu;
-      } else {
-        s_v0[row][col] = v.c;
-      }
+      s_v0[row][col] = kDerivs ? v.dalpha : v.c;
+      if (kDerivs) s_v1[row][col] = v.dnu;
     }
     __syncthreads();
     const long long j0 = (long long)tj * kGT + col0;

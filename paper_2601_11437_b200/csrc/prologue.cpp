@@ -276,13 +276,13 @@ void mle_fill_gen_table(double u_max, ThetaParams* P) {
   // Interval bins: each binade [2^e, 2^(e+1)) of u in 8 equal pieces (ratio <= 1.125; the
   // Chebyshev convergence factor of the degree-13 pieces is then > 30 per degree), so the
   // device finds the bin with one shift of the bits of u and no transcendental.  Around the
-  // reference's regime switch 8.5 (bessel.py:46) the pieces are [7, 8.5) (bins 38, 39 and
-  // the lower half of 40) and [8.5, 9); 30 = 16 * 15/8 is already a bin edge (bessel.py:47),
+  // reference's regime switch 8.5 (bessel.py:46) the pieces are [7, 8.5) (the bins [7, 7.5),
+  // [7.5, 8) and the lower half of [8, 9)) and [8.5, 9); 30 = 16 * 15/8 is a bin edge (bessel.py:47),
   // so no piece straddles a switch (gen_tab_index / gen_tab_t in special.cuh).
-  constexpr int kMerge = 38;
+  constexpr int kMerge = (2 - MLE_TAB_LO_EXP) * 8 + 6;  // = kGenMergeKey (special.cuh)
   int k = 0;
   for (int key = 0; k < MLE_TAB_MAX; ++key) {
-    const int e = -2 + key / 8, j = key % 8;
+    const int e = MLE_TAB_LO_EXP + key / 8, j = key % 8;
     double a = std::ldexp(1.0 + j / 8.0, e), b = std::ldexp(1.0 + (j + 1) / 8.0, e);
     if (!(a < hi)) break;
     if (key == kMerge + 1) continue;
@@ -290,7 +290,6 @@ void mle_fill_gen_table(double u_max, ThetaParams* P) {
     if (key == kMerge + 2) a = MLE_SMALL_MID_SPLIT;
     P->tab_ctr[k] = 0.5 * (a + b);
     P->tab_hw[k] = 0.5 * (b - a);
-    P->tab_ihw[k] = 1.0 / P->tab_hw[k];
     ++k;
   }
   if (k >= MLE_TAB_MAX && P->tab_ctr[k - 1] + P->tab_hw[k - 1] < hi)

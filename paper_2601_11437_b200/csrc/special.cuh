@@ -242,7 +242,7 @@ __device__ __forceinline__ MaternVals matern_positive(const ThetaParams& P, doub
 // form one interval [7, 8.5) and [8.5, 9) is its own.  (Below 8.5 the reference's case-2
 // series cancels catastrophically, bessel.py:213-222; interpolation nodes crowded into
 // [8, 8.5) fitted its noise into a coherent bias of the nu score.)
-constexpr int kGenMergeKey = 38;  // bin [7, 7.5): 4.5 binades above MLE_TAB_LO = 0.25
+constexpr int kGenMergeKey = (2 - MLE_TAB_LO_EXP) * 8 + 6;  // bin [7, 7.5) (binade [4, 8), j = 6)
 __device__ __forceinline__ int gen_tab_index(const ThetaParams& P, double u) {
   const int key = (int)((__double_as_longlong(u) >> 49) - P.tab_key0);
   return key - (key > kGenMergeKey ? 1 : 0) -
@@ -267,14 +267,16 @@ __device__ __forceinline__ double horner_pairs(const double* __restrict__ c, dou
 
 // Position of u in its interval k, t in [-1, 1].  On a bin (u = 2^e m, m in [1, 2), bin j =
 // the top three mantissa bits; centre 2^e (1 + (2j + 1)/16), half-width 2^e / 16) it is
-// t = 16 m - (17 + 2 j) exactly, with no table loads; [8.5, 9) gives 4 u - 35 exactly and
-// the merged [7, 8.5) (u - 7.75) / 0.75.
+// t = 16 m' - 17 exactly, m' = 1 + (the mantissa below those three bits): no table loads,
+// no conversion.  [8.5, 9) gives 4 u - 35 exactly and the merged [7, 8.5) (u - 7.75) / 0.75.
+// Branch-free (selects), so a warp's elements evaluate in lock step.
 __device__ __forceinline__ double gen_tab_t(double u, int k) {
-  if (k == kGenMergeKey) return (u - 7.75) * (4.0 / 3.0);
-  if (k == kGenMergeKey + 1) return 4.0 * u - 35.0;
   const long long b = __double_as_longlong(u);
-  const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
-  return 16.0 * m - (double)(17 + 2 * (int)((b >> 49) & 7));
+  const double m = __longlong_as_double((b & 0x0001FFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  double t = 16.0 * m - 17.0;
+  t = k == kGenMergeKey ? (u - 7.75) * (4.0 / 3.0) : t;
+  t = k == kGenMergeKey + 1 ? 4.0 * u - 35.0 : t;
+  return t;
 }
 
 // Table evaluation on a known interval k (= gen_tab_index(P, u)).

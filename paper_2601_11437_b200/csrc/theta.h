@@ -17,9 +17,12 @@
 #define MLE_CASE4_TERMS 5        // bessel.py:55
 #define MLE_U_COEFF_STRIDE 40    // >= 3*12+1 coefficients per Debye polynomial
 #define MLE_TAB_P 14              // interpolation points per interval (degree 13, even)
-#define MLE_TAB_MAX 96            // intervals per table (8 per octave of u + the 8.5 split)
+#define MLE_TAB_MAX 96            // intervals per table (8 per binade of u in [0.25, 800))
 #define MLE_TAB_DOUBLES (MLE_TAB_MAX * 3 * MLE_TAB_P)  // [interval][c, da, dn][power]
-#define MLE_TAB_LO 0.25           // below: exact evaluation (few pairs); a power of two
+#define MLE_TAB_LO_EXP (-2)       // tables from u = 2^-2 up; below, the exact evaluator: near
+                                  // u = 0, C ~ sigma^2 and the ill-conditioned goldens need its
+                                  // few-ulp accuracy (tables from 2^-16 moved one by 1.6e-10)
+#define MLE_TAB_LO 0.25           // 2^MLE_TAB_LO_EXP
 #define MLE_TAB_HI 800.0          // above: exact evaluation (elements underflow anyway)
 #define MLE_SMALL_MID_SPLIT 8.5  // bessel.py:46
 #define MLE_MID_LARGE_SPLIT 30.0 // bessel.py:47
@@ -86,7 +89,7 @@ struct ThetaParams {
   int tab_n;                                // intervals (0: exact evaluation everywhere)
   long long tab_key0;                       // bits(MLE_TAB_LO) >> 49
   double tab_lo, tab_hi;
-  double tab_ctr[MLE_TAB_MAX], tab_hw[MLE_TAB_MAX], tab_ihw[MLE_TAB_MAX];
+  double tab_ctr[MLE_TAB_MAX], tab_hw[MLE_TAB_MAX];  // interval centre, half-width
 };
 
 #ifdef __cplusplus
