@@ -72,7 +72,7 @@ def bessel_k(nu, x, device: int | None = None):
     if not math.isfinite(nu):
         raise ValueError("bessel_k requires finite nu and x")
     out = _device_call(nat.lib.mle_bessel_k, nu, x, device)
-    return float(out) if np.ndim(x) == 0 else out
+    return float(np.asarray(out).reshape(-1)[0]) if np.ndim(x) == 0 else out
 
 
 def dnu_xnu_knu(nu, x, device: int | None = None):
@@ -83,4 +83,4 @@ def dnu_xnu_knu(nu, x, device: int | None = None):
     if not math.isfinite(nu) or nu <= 0.0:
         raise ValueError("dnu_xnu_knu requires nu > 0")
     out = _device_call(nat.lib.mle_dnu_xnu_knu, nu, x, device)
-    return float(out) if np.ndim(x) == 0 else out
+    return float(np.asarray(out).reshape(-1)[0]) if np.ndim(x) == 0 else out
