@@ -393,6 +393,13 @@ size_t w_byte_offset(int Nt, int b) {
 }
 constexpr int kOzK = kOuter * kNB;               // K of every trailing update
 constexpr int kLookaheadCtas = 148 - 24;         // persistent grid of look-ahead updates
+int lookahead_ctas() {  // MLE_LOOKAHEAD_CTAS: developer override (A/B timing)
+  static const int v = [] {
+    const char* e = std::getenv("MLE_LOOKAHEAD_CTAS");
+    return e ? std::atoi(e) : kLookaheadCtas;
+  }();
+  return v;
+}
 constexpr size_t kOzRowBytes = (size_t)kOzK * kOzSlices;
 constexpr size_t kOzTileBytes = kOzRowBytes * kNB;
 
@@ -789,7 +796,7 @@ struct Launcher {
         if ((rc = join(s, s2))) return rc;
         OzGemmArgs u = oz_base(ld, Nt - b2, 0);        // (ii)
         u.lower = 1;
-        u.max_ctas = kLookaheadCtas;  // the next block's diagonal chain runs meanwhile
+        u.max_ctas = lookahead_ctas();  // the next block's diagonal chain runs meanwhile
         for (int b = 0; b < m; ++b) {
           u.As[b] = u.Bs[b] = sa.slices[b] + (size_t)(b2 - b1) * kOzTileBytes;
           u.ea[b] = u.eb[b] = sa.e[b] + (size_t)(b2 - b1) * kNB;

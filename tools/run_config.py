@@ -3,6 +3,7 @@ breakdown (gen / Cholesky / solves / reductions).  Writes one JSON record to std
 
     python tools/run_config.py config3 [--breakdown-only]
     python tools/run_config.py config5 --loglik-only
+    python tools/run_config.py config4 --breakdown-only --kernel-profile
 
 --loglik-only: the one-GPU share of a config that does not fit eval_all on one B200
 (config 5: Sigma, three derivative blocks and M are 4 x 80 GB): field simulation, then
@@ -61,6 +62,20 @@ def main():
     rec["loglik_potrf_tflops"] = rec["loglik_phases_ms"]["flops"] / (
         rec["loglik_phases_ms"]["potrf_ms"] * 1e-3) / 1e12
     rec["at_theta_true"] = {"loglik": ll, "grad": g.tolist(), "fisher": f.tolist()}
+    if "--kernel-profile" in sys.argv:
+        # one factoring eval_all serialised on one stream with CUDA events around every
+        # generation / slicing / Ozaki GEMM launch (mle_kernel_profile): per-kernel rates
+        eng.kernel_profile(True)
+        eng.eval_all(th * np.array([1.0, 1.0 - 1e-9, 1.0]))
+        ks = eng.kernel_stats()
+        eng.kernel_profile(False)
+        rec["kernel_profile"] = {
+            "stats": ks,
+            "gen_gbs": ks["gen_bytes"] / (ks["gen_ms"] * 1e-3) / 1e9,
+            "slice_gbs": ks["slice_bytes"] / (ks["slice_ms"] * 1e-3) / 1e9,
+            "ozgemm_int8_tops": ks["gemm_int8_ops"] / (ks["gemm_ms"] * 1e-3) / 1e12,
+            "ozgemm_fp64_equiv_tflops": ks["gemm_fp64_flops"] / (ks["gemm_ms"] * 1e-3) / 1e12,
+        }
     if not only_breakdown:
         th0 = m.MaternParams(*wl.theta0)
         cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
