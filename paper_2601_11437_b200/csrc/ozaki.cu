@@ -129,7 +129,14 @@ __device__ __forceinline__ void oz_combine16(uint32_t addr, uint32_t stride, dou
     for (int d = 1; d < 4; ++d) hi = hi * 256 + (int)v[d][j];
 #pragma unroll
     for (int d = 5; d < kS; ++d) lo = lo * 256 + (int)v[d][j];
-    out[j] = fma((double)hi, s_hi, (double)lo * s_lo);
+    // int64 -> double without I2F (an XU-pipe conversion, 64 per thread per tile, inside the
+    // serialised TMEM drain): for |x| < 2^51 the bits of x + (2^52 + 2^51) as a double are
+    // the integer 2^52 + 2^51 + x exactly; subtracting that constant leaves x exactly.
+    constexpr long long kMagic = 0x4338000000000000LL;  // bits of 2^52 + 2^51
+    constexpr double kMagicD = 6755399441055744.0;       // 2^52 + 2^51
+    const double hd = __longlong_as_double(hi + kMagic) - kMagicD;
+    const double ld = __longlong_as_double(lo + kMagic) - kMagicD;
+    out[j] = fma(hd, s_hi, ld * s_lo);
   }
 }
 
