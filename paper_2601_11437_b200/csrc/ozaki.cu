@@ -500,9 +500,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       const long long c_glob = (long long)o.tn * 128 + (long long)o.part * kN + ch * kCols;
       double* C = g.C[o.z] + r_glob + c_glob * g.ldc;
       const bool acc_c = g.beta != 0.0 && o.tm >= g.beta0_tm && o.tn >= g.beta0_tn;
-      // C prefetch before the accumulator wait (kN = 32; at kN = 64 it would spill: C is
-      // then read after TMEM is released, overlapping the next tile's MMAs)
-      constexpr int kPre = kN == 32 ? kCols : 0;
+      // C prefetch before the accumulator wait: all of the thread's columns at kN = 32, the
+      // first 16 at kN = 64 (all 32 would spill); the rest is read after TMEM is released,
+      // overlapping the next tile's MMAs
+      constexpr int kPre = kN == 32 ? kCols : 16;
       double cv[kPre > 0 ? kPre : 1];
 #pragma unroll
       for (int j = 0; j < kPre; ++j) cv[j] = acc_c ? __ldcg(C + (long long)j * g.ldc) : 0.0;
@@ -540,8 +541,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
         double cw[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          cw[j] = kPre > 0 ? cv[(c0 + j) % (kPre > 0 ? kPre : 1)]
-                           : (acc_c ? __ldcg(C + (long long)(c0 + j) * g.ldc) : 0.0);
+          cw[j] = c0 + j < kPre ? cv[(c0 + j) % kPre]
+                                : (acc_c ? __ldcg(C + (long long)(c0 + j) * g.ldc) : 0.0);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           __stcg(C + (long long)(c0 + j) * g.ldc,
