@@ -26,6 +26,9 @@ namespace {
 
 constexpr int kGT = 32;         // generation tile edge
 constexpr int kGThreads = 256;  // 8 columns per pass, 4 passes
+#ifndef MLE_GEN_MINB
+#define MLE_GEN_MINB 4
+#endif
 
 __device__ __forceinline__ void lower_tile_index(long long b, int* ti, int* tj) {
   // b = I (I + 1) / 2 + J, 0 <= J <= I
@@ -114,7 +117,7 @@ __device__ __forceinline__ void engine_element(const GenItem& it, const ThetaPar
 // request rate bounded the kernel).  The values go through a shared-memory tile and leave
 // with coalesced column stores.
 template <int kDerivs>
-__global__ void __launch_bounds__(kGThreads, 4) gen_engine_kernel(GenArgs a) {
+__global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(GenArgs a) {
   const GenItem& it = a.item[blockIdx.y];
   if (it.fail_flag != nullptr && *it.fail_flag) return;
   __shared__ __align__(16) ThetaParams P;

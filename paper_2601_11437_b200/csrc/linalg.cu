@@ -742,8 +742,10 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
     }
   }
   double* partials = ra.partials[item];
+  // (loglik-only items, Ba == null, have only log-det and y^T y: a block-uniform skip)
+  const int live = Ba == nullptr ? 2 : kSums;
   for (int q = 0; q < RN; ++q) {
-    const double t = q < kSums ? block_sum(s[q], sh) : 0.0;
+    const double t = q < live ? block_sum(s[q], sh) : 0.0;
     if (threadIdx.x == 0) partials[blockIdx.x * RP + q] = t;
   }
   if (threadIdx.x == 0) {
@@ -752,34 +754,42 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
   }
 }
 
-// out[0..RN) = fixed-order sums of the partials; out[RN..RN+3) = B_alpha, B_nu, M at [n,n].
-__global__ void reduce_final_kernel(ReduceArgs ra) {
+// out[0..RN) = fixed-order sums of the partials; out[RN..RN+3) = B_alpha, B_nu, M at [n,n];
+// out[RN+3], out[RN+4] = min / max of diag(L).  One warp per output (RN + 2 warps): lane l
+// folds partials l, l + 32, ... in order, then a fixed xor tree: deterministic, and ~50x
+// shorter than one thread walking all RBLOCKS partials (a dependent chain of L2 round trips
+// at the tail of every pass).
+constexpr int kFinalWarps = RN + 2;
+__global__ void __launch_bounds__(32 * kFinalWarps) reduce_final_kernel(ReduceArgs ra) {
   const int item = blockIdx.x;
   if (*ra.fail_flag[item]) return;
   const double* partials = ra.partials[item];
-  const double* Ba = ra.Ba[item];
-  const double* Bn = ra.Bn[item];
-  const double* Bm = ra.Bm[item];
   double* out = ra.out[item];
-  const long long diag_n = ra.n + (long long)ra.n * ra.ld;
-  const int q = threadIdx.x;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (q < RN) {
-    double s = 0.0;
-    for (int b = 0; b < RBLOCKS; ++b) s += partials[b * RP + q];
-    out[q] = s;
-  }
-  if (q == RN) out[RN] = Ba ? Ba[diag_n] : 0.0;
-  if (q == RN + 1) out[RN + 1] = Bn ? Bn[diag_n] : 0.0;
-  if (q == RN + 2) out[RN + 2] = Bm ? Bm[diag_n] : 0.0;
-  if (q == RN + 3) {
-    double v = INFINITY;
-    for (int b = 0; b < RBLOCKS; ++b) v = fmin(v, partials[b * RP + RN]);
-    out[RN + 3] = v;
-  }
-  if (q == RN + 4) {
     double v = 0.0;
-    for (int b = 0; b < RBLOCKS; ++b) v = fmax(v, partials[b * RP + RN + 1]);
-    out[RN + 4] = v;
+    for (int b = lane; b < RBLOCKS; b += 32) v += partials[b * RP + q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) out[q] = v;
+  } else if (q == RN) {
+    double v = INFINITY;
+    for (int b = lane; b < RBLOCKS; b += 32) v = fmin(v, partials[b * RP + RN]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) out[RN + 3] = v;
+  } else {
+    double v = 0.0;
+    for (int b = lane; b < RBLOCKS; b += 32) v = fmax(v, partials[b * RP + RN + 1]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) {
+      out[RN + 4] = v;
+      const long long diag_n = ra.n + (long long)ra.n * ra.ld;
+      out[RN] = ra.Ba[item] ? ra.Ba[item][diag_n] : 0.0;
+      out[RN + 1] = ra.Bn[item] ? ra.Bn[item][diag_n] : 0.0;
+      out[RN + 2] = ra.Bm[item] ? ra.Bm[item][diag_n] : 0.0;
+    }
   }
 }
 
@@ -790,7 +800,7 @@ cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {
     reduce_kernel<RN><<<dim3(RBLOCKS, items), RTHREADS, 0, s>>>(r);
   else
     reduce_kernel<7><<<dim3(RBLOCKS, items), RTHREADS, 0, s>>>(r);
-  reduce_final_kernel<<<items, 32, 0, s>>>(r);
+  reduce_final_kernel<<<items, 32 * kFinalWarps, 0, s>>>(r);
   return cudaGetLastError();
 }
 
