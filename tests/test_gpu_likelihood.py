@@ -200,3 +200,21 @@ def test_simulate_field_matches_reference_simulation(gpu):
     loc, z = config_data("config1")
     z_gpu = gpu.simulate_field(loc, (1.0, 0.1, 0.5), 0)
     np.testing.assert_allclose(z_gpu, z, rtol=0, atol=1e-12 * np.max(np.abs(z)))
+
+
+def test_sigma2_scaling_identity_config4_full_size(gpu):
+    """Size-independent property at BASELINE config 4's full size (n = 65,536; Sigma alone is
+    34 GB): Sigma(c s2) = c Sigma(s2), so l(c) = l(1) - n/2 log c - q (1/c - 1)/2 with one
+    unknown q = z^T Sigma^-1 z.  Two log-likelihoods (c = 1, 2) determine q; the third (c = 4)
+    must follow.  q must also be positive and O(n) for a field simulated at this theta."""
+    wl = gpu.WORKLOADS["config4"]
+    loc = wl.locations(wl.seeds[0])
+    th = np.array(wl.theta_true, float)
+    z = gpu.simulate_field(loc, tuple(th), wl.seeds[0])
+    data = gpu.SpatialDataset(loc, z)
+    n = loc.shape[0]
+    ll = {c: gpu.log_likelihood(data, (c * th[0], th[1], th[2])) for c in (1.0, 2.0, 4.0)}
+    q = (ll[1.0] - ll[2.0] - 0.5 * n * math.log(2.0)) / (0.5 * (1 / 2.0 - 1))
+    pred4 = ll[1.0] - 0.5 * n * math.log(4.0) - 0.5 * q * (1 / 4.0 - 1)
+    assert ll[4.0] == pytest.approx(pred4, rel=1e-11)
+    assert 0.9 * n < q < 1.1 * n  # z ~ N(0, Sigma): q ~ chi^2_n
