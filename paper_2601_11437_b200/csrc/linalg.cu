@@ -698,39 +698,60 @@ __global__ void __launch_bounds__(RTHREADS) reduce_kernel(ReduceArgs ra) {
 #pragma unroll
   for (int q = 0; q < RN; ++q) s[q] = 0.0;
   double dmin = INFINITY, dmax = 0.0;
-  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+  // One warp per column (column j on warp (j mod W) of block (j / W) mod grid, W = warps per
+  // block): the diagonal terms on lane 0, the strictly lower rows coalesced across the lanes,
+  // four rows' loads in flight per lane.  A fixed mapping, so the sums are deterministic and
+  // the loglik-only path (Ba == null) sums log-det / y^T y exactly as eval_all does.
+  const int warps = RTHREADS / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * warps + warp; j < n; j += gridDim.x * warps) {
     const long long cj = (long long)j * ld;
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       s[0] += log(L[j + cj]);
       dmin = fmin(dmin, L[j + cj]);
       dmax = fmax(dmax, L[j + cj]);
       const double y = L[n + cj];
       s[1] += y * y;
-      if (Ba == nullptr) continue;
-      const double a = Ba[j + cj], b = Bn[j + cj];
-      s[2] += a;
-      s[3] += b;
-      s[4] += a * a;
-      s[5] += a * b;
-      s[6] += b * b;
-      if (Bm != nullptr) {
-        const double c = Bm[j + cj];
-        s[7] += c;
-        s[8] += a * c;
-        s[9] += b * c;
-        s[10] += c * c;
+      if (Ba != nullptr) {
+        const double a = Ba[j + cj], b = Bn[j + cj];
+        s[2] += a;
+        s[3] += b;
+        s[4] += a * a;
+        s[5] += a * b;
+        s[6] += b * b;
+        if (Bm != nullptr) {
+          const double c = Bm[j + cj];
+          s[7] += c;
+          s[8] += a * c;
+          s[9] += b * c;
+          s[10] += c * c;
+        }
       }
     }
     if (Ba == nullptr) continue;
+    int i = j + 1 + lane;
     if (Bm == nullptr) {
-      for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
+      for (; i + 96 < n; i += 128) {
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = Ba[i + 32 * q + cj];
+          b[q] = Bn[i + 32 * q + cj];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s[4] += 2.0 * a[q] * a[q];
+          s[5] += 2.0 * a[q] * b[q];
+          s[6] += 2.0 * b[q] * b[q];
+        }
+      }
+      for (; i < n; i += 32) {
         const double a = Ba[i + cj], b = Bn[i + cj];
         s[4] += 2.0 * a * a;
         s[5] += 2.0 * a * b;
         s[6] += 2.0 * b * b;
       }
     } else {
-      for (int i = j + 1 + threadIdx.x; i < n; i += RTHREADS) {
+      for (; i < n; i += 32) {
         const double a = Ba[i + cj], b = Bn[i + cj], c = Bm[i + cj];
         s[4] += 2.0 * a * a;
         s[5] += 2.0 * a * b;
