@@ -1,24 +1,43 @@
-"""Benchmark: Fisher-BT iterations/s on BASELINE config 2 (n = 3,600, 5 replicate fits).
+"""Benchmark: Fisher-BT iterations/s on BASELINE config 4 (n = 65,536), the largest
+configuration that fits one B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Own arm ("ours"): one process per GPU (torchrun for N > 1).  Each rank runs its own five
-replicate Fisher-BT fits of config 2 (weak scaling: rank r fits seeds 5r..5r+4; rank 0 uses
-the golden seeds 0-4; no data-path collective).  The five host loops run concurrently and
-their evaluations are executed in lock step as batched GPU passes (paper_2601_11437_b200.
-fit_many -> mle_eval_batch).  A step = all five fits from theta0 to convergence.
-  value  = sum of grad_calls (Fisher iterations) over all ranks / max-over-ranks step time,
-           inputs resident in HBM (datasets created and warmed before timing);
-  e2e    = same metric through the public API from host numpy buffers: every step creates
-           the datasets (H2D of locations and z), runs the fits and reads results back.
-Reference arm (--impl reference): the reference's own CPU algorithm (oracle port of
-maternmle: numpy / scipy / OpenBLAS on all host cores) on the same config, rank 0 only.
+Workload (BASELINE.json configs[3]): 256 x 256 jittered grid on [0, 1]^2 (seed 0), one FP64
+field z = L w drawn on the GPU at theta_true = (1.0, 0.1, 1.2), Fisher-BT from the pinned
+theta0 = (1.0, 0.1, 1.0) (degenerate L9 cube) with the reference's rules
+(optimizer.py:331-412).  A step = one Fisher iteration: the host loop runs until its next
+eval_all has been answered (the line-search logliks before it, and for a fit's first step its
+L9 start, belong to that step).  When a fit converges the next one starts from theta0 on the
+same resident data, so any K is a sequence of real Fisher iterations.
+
+Own arm ("ours"), one process per GPU (torchrun for N > 1):
+  N = 1: the single-context engine (SpatialDataset -> mle_ctx: all matrices on one GPU);
+  N > 1: the sharded engine (DistributedEngine over NCCL: 512-column block-cyclic panels,
+         int8-slice panel broadcasts), every rank running the same host loop -- strong
+         scaling: the same fit at every N.
+  value = Fisher iterations / device time of the K timed steps (max over ranks), inputs
+          resident in HBM; e2e = one complete fit through the public API from host numpy
+          arrays (dataset upload inside the timed region, results read back).
+  roofline: the dominant kernel (the Ozaki FP64 GEMM on tcgen05 int8) in a kernel-profiled
+          eval_all, ALGORITHMIC flops (3 n^3 per eval_all for factor + solves,
+          minus the 128-wide DMMA steps inside the Cholesky's 512-column blocks) x 28 int8
+          slice products / summed launch durations, against 2 x MEASURED_PEAKS bf16 (int8 dense
+          = twice bf16 dense; the sustained figure: the GEMMs run for seconds inside a step).
+Reference arm (--impl reference): the reference's own CPU algorithm (oracle port of maternmle:
+numpy / scipy / OpenBLAS on all host cores), rank 0 only.  A config-4 Fisher iteration is
+hours of CPU (one Sigma generation alone ~20 min single-threaded), so each step times a
+bounded sample of every phase at the config-4 theta and sizes and extrapolates (labelled):
+generation per pair x pairs, dpotrf / dtrsm at their measured flop rates x flops, the
+memory-bound assembly / traces x n^2; iteration = one eval_all + rho logliks, rho from the
+fit's own call counts.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -32,51 +51,73 @@ sys.path.insert(0, str(REPO))
 import numpy as np  # noqa: E402
 
 GOLDEN = REPO / "tests" / "golden"
-CONFIG = "config2"
-THETA0 = (0.8, 0.1, 1.0)
-N_REPLICAS = 5
-# tcgen05.mma kind::i8 issue-rate ceiling measured on this pool's B200 with tools/umma_rate
-# (the ozgemm k-block MMA sequence, operands resident in SMEM, 1888 MHz): 4485 TOPS burst;
-# with random operands the clock settles at 1649-1761 MHz (sw_power_cap) -> 3624-3870 TOPS
-# (profiles/r01_umma_rate.txt).  Reported beside the MEASURED_PEAKS-derived peak.
+CONFIG = "config4"
+METRIC = "Fisher-BT iterations/s at n"
+# tcgen05.mma kind::i8 issue-rate ceiling measured on this pool's B200 (tools/umma_rate,
+# profiles/r01_umma_rate.txt), reported beside the MEASURED_PEAKS-derived peak.
 INT8_PIPE_TOPS = 4485.0
 FP64_PEAK_TFLOPS = 36.08  # cuBLAS DGEMM 16384^3, this pool's B200 (profiles/r01_fp64_peaks.txt)
-METRIC = "Fisher-BT iterations/s at n"
+OZ_PRODUCTS = 28          # int8 slice products per FP64-emulated product (7 slices)
+# Reference call mix per Fisher iteration at config 4 (loglik-only calls / grad calls) from the
+# config-4 fit on the GPU engine (identical host loop; profiles/r01_config4_fit.json: 8 grad
+# calls, 24 loglik calls incl. the 8 eval_all -> 16 loglik-only, L9 included).
+CONFIG4_RHO = 16.0 / 8.0
 
 
-def workload_desc():
-    return {"workload": "config2: n=3600 jittered 60x60 grid on [0,1]^2, true theta=(1.0,0.2,"
-                        "1.5), 5 replicate FP64 fields per GPU, Fisher-BT from theta0=(0.8,0.1,"
-                        "1.0) to ||grad||<=1e-3 (reference stopping rule)",
-            "n": 3600, "replicas_per_gpu": N_REPLICAS, "nb": 128, "outer_block": 512,
-            "l2": "inputs larger than L2: 3 x 110 MB matrices per replica, 5 replicas"}
+def workload_desc(world):
+    return {"workload": "config4: n=65536 jittered 256x256 grid on [0,1]^2 (seed 0), one FP64 "
+                        "field z=Lw at theta_true=(1.0,0.1,1.2), Fisher-BT from theta0=(1.0,0.1,"
+                        "1.0) (degenerate L9 cube) to ||grad||<=1e-3; step = one Fisher "
+                        "iteration (eval_all + its line-search logliks)",
+            "n": 65536, "engine": "single-context" if world == 1 else
+            f"sharded DistributedEngine over {world} ranks (NCCL)",
+            "nb": 128, "outer_block": 512,
+            "l2": "inputs larger than L2: three 34.5 GB matrices"}
 
 
-def replica_seeds(rank: int):
-    """Weak scaling: rank r owns seeds 5r..5r+4 (no data-path collective)."""
-    return [N_REPLICAS * rank + s for s in range(N_REPLICAS)]
-
-
-def load_replica(seed, device):
-    """Locations and z for one replica (golden z for seeds 0-4, GPU-simulated otherwise)."""
+def config_inputs(name, seed=0, device=0):
+    """Locations and z (golden z where the reference could draw it, else the GPU draw)."""
     import paper_2601_11437_b200 as m
 
-    path = GOLDEN / f"{CONFIG}_seed{seed}_data.npz"
+    path = GOLDEN / f"{name}_seed{seed}_data.npz"
     if path.exists():
         d = np.load(path)
         return d["loc"], d["z"]
-    wl = m.WORKLOADS[CONFIG]
+    wl = m.WORKLOADS[name]
     loc = wl.locations(seed)
     return loc, m.simulate_field(loc, wl.theta_true, seed, device=device)
 
 
-def run_fits(datasets, coords=None):
-    """All replicas from THETA0, lock-step batched (one launch sequence covers them all)."""
-    import paper_2601_11437_b200 as m
+class FitStepper:
+    """Runs Fisher-BT (the package's request-generator driver, fisher_bt.py) one Fisher
+    iteration at a time; restarts from theta0 when a fit ends."""
 
-    th0 = m.MaternParams(*THETA0)
-    cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
-    return m.fit_many(datasets, cfg, coordinator_out=coords)
+    def __init__(self, make_objective, cfg):
+        self.make_objective = make_objective
+        self.cfg = cfg
+        self.done = []
+        self._start()
+
+    def _start(self):
+        from paper_2601_11437_b200.fisher_bt import fisher_bt_gen
+
+        self.obj = self.make_objective()
+        self.gen = fisher_bt_gen(self.cfg, self.obj)
+        self.req = next(self.gen)
+
+    def step(self):
+        from paper_2601_11437_b200.fisher_bt import EVAL_ALL
+
+        while True:
+            kind, theta = self.req
+            ans = self.obj.eval_all(theta) if kind == EVAL_ALL else self.obj.loglik(theta)
+            try:
+                self.req = self.gen.send(ans)
+            except StopIteration as stop:
+                self.done.append(stop.value)
+                self._start()
+            if kind == EVAL_ALL:
+                return
 
 
 class ClockSampler:
@@ -94,7 +135,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -122,85 +163,46 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def isolated_phase_rates(datasets, theta, reps=4):
-    """Batched eval_all / loglik over all replicas on one stream, CUDA events on it.
-    Two thetas alternate so every evaluation refactors (no factor-cache hits)."""
-    import paper_2601_11437_b200 as m
+def gemm_algorithmic_flops(n, mode):
+    """Standard-count FP64 flops the Ozaki GEMM launches of one evaluation carry (SURVEY
+    §8(d)): factor n^3/3 (+ forward sweep n^3 and lower-half right sweep n^3/3 per derivative
+    block for eval_all: 3 n^3), minus the Cholesky's 128-wide DMMA steps inside each 512-column
+    block (~ 512^2 / 2 per element row of the block: 256 n^2)."""
+    total = n ** 3 / 3.0 + (2 * (n ** 3 + n ** 3 / 3.0) if mode == "eval_all" else 0.0)
+    return total - 256.0 * n * n
 
-    engines = [d.engine() for d in datasets]
-    th_a = np.asarray(theta, float)
-    th_b = th_a * np.array([1.0, 1.0 + 1e-7, 1.0])
-    th_c = th_a * np.array([1.0, 1.0 - 1e-7, 1.0])
-    out = {"eval": [], "loglik": []}
-    for r in range(reps + 1):
-        for mode, key in ((2, "eval"), (1, "loglik")):
-            th = (th_a if (r % 2 == 0) else th_b) if mode == 2 else th_c * (1.0 + 1e-9 * r)
-            m.eval_batch(engines, [th] * len(engines), [mode] * len(engines))
-            p = engines[0].phase_times()
-            if r > 0:
-                out[key].append(p)
-    # kernel profiling pass: one stream, CUDA events around every Ozaki GEMM / slicing launch
-    engines[0].kernel_profile(True)
-    kst = []
-    for r in range(2):
-        m.eval_batch(engines, [th_a if r % 2 == 0 else th_b] * len(engines), [2] * len(engines))
-        kst.append(engines[0].kernel_stats())
-    engines[0].kernel_profile(False)
-    ks = {k: sum(d[k] for d in kst) for k in kst[0]}
-    ev, ll = out["eval"], out["loglik"]
-    fac_ms = sum(p["potrf_ms"] + p["solve_ms"] for p in ev)
-    fac_fl = sum(p["flops"] for p in ev)
+
+def kernel_profile(engine, theta, n, peaks):
+    """One eval_all with every Ozaki GEMM / slicing / generation launch event-timed on the
+    (serialised) launching stream; algorithmic work per launch class / summed durations."""
+    engine.kernel_profile(True)
+    try:
+        engine.eval_all(np.asarray(theta, float))
+        ks = engine.kernel_stats()
+    finally:
+        engine.kernel_profile(False)
+    alg = gemm_algorithmic_flops(n, "eval_all")
+    gemm_s = ks["gemm_ms"] * 1e-3
+    int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0))
+    achieved = alg * OZ_PRODUCTS / gemm_s / 1e12
     return {
-        "batch": len(engines),
-        "eval_factor_solve_tflops": fac_fl / (fac_ms * 1e-3) / 1e12,
-        "eval_ms": statistics.median(p["total_ms"] for p in ev),
-        "eval_phases_ms": {k: statistics.median(p[k] for p in ev)
-                           for k in ("gen_ms", "potrf_ms", "solve_ms", "reduce_ms")},
-
-        "loglik_ms": statistics.median(p["total_ms"] for p in ll),
-        "loglik_potrf_tflops": sum(p["flops"] for p in ll) / (
-            sum(p["potrf_ms"] for p in ll) * 1e-3) / 1e12,
-        "launches_per_batched_eval": ev[-1]["launches"],
-        "kernels": {
-            "ozgemm_launches_per_eval": ks["gemm_launches"] / len(kst),
-            "ozgemm_ms_per_eval": ks["gemm_ms"] / len(kst),
-            "ozgemm_int8_tops": ks["gemm_int8_ops"] / (ks["gemm_ms"] * 1e-3) / 1e12,
-            "ozgemm_fp64_equiv_tflops": ks["gemm_fp64_flops"] / (ks["gemm_ms"] * 1e-3) / 1e12,
-            "slice_ms_per_eval": ks["slice_ms"] / len(kst),
-            "slice_gbs": ks["slice_bytes"] / (ks["slice_ms"] * 1e-3) / 1e9,
-            # covariance + derivative generation (tables + element kernels), algorithmic
-            # bytes = 8 B per lower-triangle element per matrix written
-            "gen_ms_per_eval": ks["gen_ms"] / len(kst),
-            "gen_gbs": ks["gen_bytes"] / (ks["gen_ms"] * 1e-3) / 1e9 if ks["gen_ms"] else 0.0,
-        },
+        "ozgemm_launches": ks["gemm_launches"], "ozgemm_ms": ks["gemm_ms"],
+        "ozgemm_avg_launch_ms": ks["gemm_ms"] / max(1, ks["gemm_launches"]),
+        "ozgemm_algorithmic_fp64_flops": alg,
+        "ozgemm_executed_fp64_flops": ks["gemm_fp64_flops"],
+        "ozgemm_executed_over_algorithmic": ks["gemm_fp64_flops"] / alg,
+        "ozgemm_alg_int8_tops": achieved,
+        "ozgemm_alg_fp64_equiv_tflops": alg / gemm_s / 1e12,
+        "ozgemm_executed_int8_tops": ks["gemm_int8_ops"] / gemm_s / 1e12,
+        "int8_peak_tops": int8_peak,
+        "slice_ms": ks["slice_ms"], "slice_gbs": ks["slice_bytes"] / max(1e-9, ks["slice_ms"]
+                                                                         * 1e-3) / 1e9,
+        "gen_ms": ks["gen_ms"],
+        "gen_gbs": ks["gen_bytes"] / (ks["gen_ms"] * 1e-3) / 1e9 if ks["gen_ms"] else 0.0,
     }
 
 
 # ----------------------------------------------------------------------------- CPU side
-def cpu_iteration_sample(reps=1):
-    """Oracle (reference algorithm: numpy/scipy/OpenBLAS) time of one mean Fisher iteration of
-    config 2 = one eval_all + rho loglik calls, rho = (loglik_calls - grad_calls) / grad_calls
-    of the reference's own config-2 fits (golden, seeds 0-4)."""
-    from oracle import maternmle_cpu as O
-
-    fits = [json.loads((GOLDEN / f"{CONFIG}_seed{s}_fit.json").read_text()) for s in range(5)]
-    g = sum(f["grad_calls"] for f in fits)
-    rho = (sum(f["loglik_calls"] for f in fits) - g) / g
-    d = np.load(GOLDEN / f"{CONFIG}_seed0_data.npz")
-    loc, z = d["loc"], d["z"]
-    th = (1.0, 0.2, 1.5)
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.eval_all(loc, z, th)
-        t1 = time.perf_counter()
-        O.loglik(loc, z, th)
-        t2 = time.perf_counter()
-        times.append((t1 - t0) + rho * (t2 - t1))
-    t_iter = statistics.median(times)
-    return {"value": 1.0 / t_iter, "t_eval_all_s": t1 - t0, "t_loglik_s": t2 - t1, "rho": rho}
-
-
 def cpu_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -213,45 +215,180 @@ def cpu_cores():
     return os.cpu_count() or 1
 
 
+def cpu_config4_sample(pairs=400_000, n_lin=6144, seed=0):
+    """The reference algorithm (oracle port: numpy / scipy / OpenBLAS, reference operation
+    order) on a bounded sample of every phase of a config-4 Fisher iteration, extrapolated.
+
+    * generation (single-threaded numpy/scipy ufuncs, as in the reference): C, dC/dalpha,
+      dC/dnu (matern.py:100-125) on `pairs` uniformly drawn config-4 location pairs at
+      theta_true, seconds per pair x n (n - 1) / 2 pairs;
+    * dpotrf (likelihood.py:75) and dtrsm (solve_triangular, :134-135) at n_lin on all host
+      cores: measured flop rates x n^3/3 and 4 x n^3 (two n x n solves per derivative block);
+    * the memory-bound rest (squareform assembly, trace_product's A + B^T, :92-104) timed at
+      n_lin and scaled by n^2;
+    iteration = eval_all + rho x loglik (rho = CONFIG4_RHO)."""
+    from scipy.linalg import solve_triangular
+    from scipy.linalg.lapack import dpotrf
+    from scipy.spatial.distance import squareform
+
+    import paper_2601_11437_b200.datasets as ds
+    from oracle import maternmle_cpu as O
+
+    n = 65536
+    th = (1.0, 0.1, 1.2)
+    rng = np.random.default_rng(seed)
+    loc = ds.jittered_grid(256, 0)
+    i = rng.integers(0, n, size=pairs)
+    j = rng.integers(0, n, size=pairs)
+    keep = i != j
+    h = np.hypot(*(loc[i[keep]] - loc[j[keep]]).T)
+    t = {}
+    for kind in ("sigma", "alpha", "nu"):
+        t0 = time.perf_counter()
+        O.elem(h, th, kind)
+        t[kind] = (time.perf_counter() - t0) / h.size
+    npairs = n * (n - 1) / 2.0
+    gen_s = {k: v * npairs for k, v in t.items()}
+    # LAPACK rates on all host cores
+    a = rng.standard_normal((n_lin, n_lin))
+    spd = a @ a.T / n_lin + np.eye(n_lin)
+    t0 = time.perf_counter()
+    low, info = dpotrf(spd, lower=1, clean=1, overwrite_a=0)
+    t_potrf = time.perf_counter() - t0
+    rhs = rng.standard_normal((n_lin, n_lin))
+    t0 = time.perf_counter()
+    solve_triangular(low, rhs, lower=True, check_finite=False)
+    t_trsm = time.perf_counter() - t0
+    potrf_rate = n_lin ** 3 / 3.0 / t_potrf
+    trsm_rate = float(n_lin) ** 3 / t_trsm
+    # memory-bound assembly and trace products, per element
+    cond = rng.random(n_lin * (n_lin - 1) // 2)
+    t0 = time.perf_counter()
+    sq = squareform(cond, checks=False)
+    t_sq = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.trace_product(sq, rhs)
+    t_tp = time.perf_counter() - t0
+    per_el_sq, per_el_tp = t_sq / n_lin ** 2, t_tp / n_lin ** 2
+    nn = float(n) * n
+    potrf_s = n ** 3 / 3.0 / potrf_rate
+    trsm_s = float(n) ** 3 / trsm_rate
+    loglik_s = gen_s["sigma"] + per_el_sq * nn + potrf_s + 2 * float(n) ** 2 / trsm_rate * 1.0
+    eval_all_s = (gen_s["sigma"] + gen_s["alpha"] + gen_s["nu"] + 3 * per_el_sq * nn + potrf_s
+                  + 4 * trsm_s + 3 * per_el_tp * nn)
+    iter_s = eval_all_s + CONFIG4_RHO * loglik_s
+    return {"value": 1.0 / iter_s, "iteration_s": iter_s, "eval_all_s": eval_all_s,
+            "loglik_s": loglik_s, "gen_s_per_matrix": gen_s, "potrf_s": potrf_s,
+            "trsm_s_each": trsm_s, "potrf_gflops": potrf_rate / 1e9,
+            "trsm_gflops": trsm_rate / 1e9, "sample_pairs": int(h.size), "n_lin": n_lin}
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return
     from oracle import maternmle_cpu as O  # noqa: F401  (imports / BLAS warm-up)
 
-    samples = [cpu_iteration_sample(1) for _ in range(args.steps)]
+    for _ in range(args.warmup):
+        cpu_config4_sample(pairs=50_000, n_lin=1024)
+    samples, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        samples.append(cpu_config4_sample())
+        walls.append(time.perf_counter() - t0)
     val = statistics.median(s["value"] for s in samples)
     cores = cpu_cores()
-    sample = ("per step: one config-2 eval_all + rho=%.3f loglik at n=3600 (the reference "
-              "fits' mean evaluation mix per Fisher iteration); generation single-threaded "
-              "numpy/scipy as in the reference, LAPACK on %d threads; warm-up = imports only"
-              % (samples[0]["rho"], cores))
+    s0 = samples[len(samples) // 2]
+    sample = ("per step: the reference algorithm (oracle port, numpy/scipy/OpenBLAS) timed on "
+              "%d config-4 location pairs (C, dC/dalpha, dC/dnu at theta_true; generation "
+              "single-threaded as in the reference) and dpotrf / dtrsm / assembly / trace "
+              "products at n=%d on %d threads, EXTRAPOLATED to n=65536 (pairs x per-pair time, "
+              "n^3 flops / measured rate, n^2 x per-element time); iteration = eval_all + "
+              "%.1f loglik" % (s0["sample_pairs"], s0["n_lin"], cores, CONFIG4_RHO))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_desc(),
+            "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(1), "extrapolated": True,
             "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "detail": {"t_eval_all_s": samples[-1]["t_eval_all_s"],
-                       "t_loglik_s": samples[-1]["t_loglik_s"]}}
+            "detail": s0}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- GPU side
+def extra_single_gpu(m, device):
+    """Context numbers on the smaller configs (not the headline): one config-3 fit (n=16,384)
+    and the five config-2 replicate fits batched."""
+    out = {}
+    import torch
+
+    loc, z = config_inputs("config3", 0, device)
+    wl = m.WORKLOADS["config3"]
+    th0 = m.MaternParams(*wl.theta0)
+    cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    data = m.SpatialDataset(loc, z, device=device)
+    m.fisher_bt(data, cfg)  # warm (buffers, tables)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = m.fisher_bt(data, cfg)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["config3_fit"] = {"n": wl.n, "grad_calls": r.grad_calls, "loglik_calls": r.loglik_calls,
+                          "seconds": dt, "it_per_s": r.grad_calls / dt,
+                          "theta_hat": r.theta_hat.as_array().tolist()}
+    data.release()
+    wl2 = m.WORKLOADS["config2"]
+    sets = [m.SpatialDataset(*config_inputs("config2", s, device), device=device)
+            for s in wl2.seeds]
+    th0 = m.MaternParams(*wl2.theta0)
+    cfg2 = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    m.fit_many(sets, cfg2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = m.fit_many(sets, cfg2)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    g = sum(x.grad_calls for x in res)
+    out["config2_five_fits"] = {"grad_calls": g, "seconds": dt, "it_per_s": g / dt}
+    for d in sets:
+        d.release()
+    return out
+
+
 def ours_arm(args, rank, world, local_rank):
     import torch
 
     import paper_2601_11437_b200 as m
+    from paper_2601_11437_b200.distributed import (DistributedEngine, DistributedObjective,
+                                                   TorchComm)
 
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
+    wl = m.WORKLOADS[CONFIG]
+    loc = wl.locations(0)
+    # z = L w at theta_true (simulate.py:100-106): drawn once on rank 0's GPU, shared
+    zt = torch.zeros(wl.n, dtype=torch.float64, device="cuda")
+    if rank == 0:
+        zt.copy_(torch.from_numpy(m.simulate_field(loc, wl.theta_true, 0, device=local_rank)))
+    if dist is not None:
+        dist.broadcast(zt, 0)
+    z = zt.cpu().numpy()
+    th0 = m.MaternParams(*wl.theta0)
+    cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
 
-    seeds = replica_seeds(rank)
-    host = [load_replica(s, local_rank) for s in seeds]
-    datasets = [m.SpatialDataset(loc, z, device=local_rank) for loc, z in host]
+    def make_backend(host_loc, host_z):
+        if world == 1:
+            data = m.SpatialDataset(host_loc, host_z, device=local_rank)
+            return data, (lambda: m.LikelihoodObjective(data))
+        eng = DistributedEngine(host_loc, host_z, TorchComm(), device=local_rank)
+        return eng, (lambda: DistributedObjective(eng))
+
+    handle, make_obj = make_backend(loc, z)
+    stepper = FitStepper(make_obj, cfg)
 
     def barrier_sync():
         torch.cuda.synchronize()
@@ -270,131 +407,104 @@ def ours_arm(args, rank, world, local_rank):
         return out, start.elapsed_time(stop)
 
     for _ in range(args.warmup):
-        run_fits(datasets)
+        stepper.step()
+    from paper_2601_11437_b200 import _native as nat
 
     clocks = ClockSampler(local_rank)
     clocks.start()
-    coords, step_ms, grad_calls, loglik_calls = [], [], 0, 0
-    for _ in range(args.steps):
-        res, ms = timed(lambda: run_fits(datasets, coords))
+    launches0 = nat.lib.mle_launch_count()
+    step_ms = []
+    ll0 = stepper.obj.loglik_calls + sum(r.loglik_calls for r in stepper.done)
+    for k in range(args.steps):
+        _, ms = timed(stepper.step)
         step_ms.append(ms)
-        print(f"[bench] step {ms:.1f} ms; device phases {coords[-1].acc}", file=sys.stderr,
-              flush=True)
-        grad_calls += sum(r.grad_calls for r in res)
-        loglik_calls += sum(r.loglik_calls for r in res)
+        if rank == 0:
+            print(f"[bench] step {k} {ms:.1f} ms", file=sys.stderr, flush=True)
     clk = clocks.stop()
-    last_fits = res
+    launches = nat.lib.mle_launch_count() - launches0
+    ll_calls = stepper.obj.loglik_calls + sum(r.loglik_calls for r in stepper.done) - ll0
 
-    # end-to-end: host arrays -> public API -> results on host, every step
-    h2d = sum(loc.nbytes + z.nbytes for loc, z in host)
-    e2e_ms, e2e_grad, e2e_evals = [], 0, 0
-    e2e_coords = []
+    # end-to-end: one complete fit from host numpy arrays through the public API (dataset
+    # upload, every evaluation, results read back) -- inside the timed region
+    e2e_box = {}
 
-    def e2e_step():
-        ds = [m.SpatialDataset(loc, z, device=local_rank) for loc, z in host]
-        r = run_fits(ds, e2e_coords)
-        for d in ds:
-            d.release()
-        return r
+    def e2e_fit():
+        h, mk = make_backend(loc.copy(), z.copy())
+        e2e_box["res"] = m.fisher_bt(None, cfg, objective=mk())
+        if world == 1:
+            h.release()
+        else:
+            h.close()
 
-    # one untimed warm-up: the first contexts of this size populate the engine's buffer
-    # cache (later create/destroy cycles reuse those buffers instead of cudaMalloc/cudaFree)
-    e2e_step()
-    for _ in range(max(1, args.steps)):
-        res_e2e, ms = timed(e2e_step)
-        e2e_ms.append(ms)
-        print(f"[bench] e2e step {ms:.1f} ms; device phases {e2e_coords[-1].acc}",
-              file=sys.stderr, flush=True)
-        e2e_grad += sum(r.grad_calls for r in res_e2e)
-        e2e_evals += sum(r.loglik_calls for r in res_e2e)
-
-    tot_ms, tot_e2e = sum(step_ms), sum(e2e_ms)
-    if dist is not None:
-        t = torch.tensor([tot_ms, tot_e2e], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        c = torch.tensor([grad_calls, e2e_grad, loglik_calls], dtype=torch.float64, device="cuda")
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        tot_ms, tot_e2e = float(t[0]), float(t[1])
-        grad_all, e2e_grad_all, ll_all = (float(v) for v in c)
+    if world == 1:
+        handle.release()  # free the timed run's matrices before the e2e fit allocates its own
     else:
-        grad_all, e2e_grad_all, ll_all = float(grad_calls), float(e2e_grad), float(loglik_calls)
+        handle.close()
+    _, e2e_ms = timed(e2e_fit)
+    res = e2e_box["res"]
+    tot_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([tot_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, e2e_ms = float(t[0]), float(t[1])
     if rank != 0:
         return
-
-    value = grad_all / (tot_ms * 1e-3)
-    e2e_value = e2e_grad_all / (tot_e2e * 1e-3)
-    acc = {k: sum(c.acc[k] for c in coords) for k in coords[0].acc}
-    batches = sum(c.batches for c in coords)
-    iso = isolated_phase_rates(datasets, m.WORKLOADS[CONFIG].theta_true)
-    achieved = iso["eval_factor_solve_tflops"]
-    kern = iso["kernels"]
+    value = args.steps / (tot_ms * 1e-3)
+    e2e_value = res.grad_calls / (e2e_ms * 1e-3)
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) \
         if (REPO / "MEASURED_PEAKS.json").exists() else {}
-    int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
-    ncu_traffic = None
-    tfile = REPO / "profiles" / "ozgemm_traffic.json"
-    if tfile.exists():
-        ncu_traffic = json.loads(tfile.read_text())
-    # per request: 9 result doubles + failure flag (4 B) + pivot (8 B) come back to the host
-    d2h = int(e2e_evals / max(1, len(e2e_ms)) * (9 * 8 + 4 + 8))
-    in_fit_tflops = acc["flops"] / ((acc["potrf_ms"] + acc["solve_ms"]) * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_desc(),
-        "roofline": {
-            "bound": "tensor", "unit": "TFLOP/s", "achieved": kern["ozgemm_int8_tops"],
-            "peak": int8_peak, "frac": kern["ozgemm_int8_tops"] / int8_peak,
-            "traffic": ncu_traffic["dram_bytes"] if ncu_traffic else None,
-            "kernel": "ozgemm_persistent_kernel<64, 7, 2> (Ozaki FP64 trailing-update GEMM on "
-                      "tcgen05.mma kind::i8, 128x64 tiles in CTA pairs sharing A): int8 tensor "
-                      "ops = 28 slice products (7 balanced base-256 slices) x 2 x 128 x 128 x K "
-                      "per 128x128 tile, summed over every launch of a batched eval_all of the 5 "
-                      "replicas, / the sum of the launches' CUDA-event durations (profiling "
-                      "pass, one stream)",
-            "fp64_equiv_tflops": kern["ozgemm_fp64_equiv_tflops"],
-            "int8_pipe_microbench_tops": INT8_PIPE_TOPS,
-            "frac_of_int8_pipe_microbench": kern["ozgemm_int8_tops"] / INT8_PIPE_TOPS,
-            "peak_source": "int8 dense tcgen05 rate = 2 x MEASURED_PEAKS.json bf16_tflops "
-                           "(burst; sm_100 int8 dense is twice bf16 dense)",
-            "traffic_source": ncu_traffic.get("source") if ncu_traffic else None},
-        "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS,
-        "fp64_tflops_chol_solve": achieved,
-        "fp64_tflops_chol_solve_in_fits": in_fit_tflops,
-        "gen_hbm_gbs": kern["gen_gbs"],
-        # per-kernel roofline fractions (north_star: "per-kernel roofline fractions at 1 GPU")
-        "kernel_rooflines": {
-            "ozgemm_int8_tensor": kern["ozgemm_int8_tops"] / int8_peak,
-            "cholesky_solve_fp64_vs_dmma_peak": achieved / FP64_PEAK_TFLOPS,
-            "slicing_hbm": kern["slice_gbs"] / peaks.get("hbm_gbs", 6555.0),
-            "generation_hbm_algorithmic": kern["gen_gbs"] / peaks.get("hbm_gbs", 6555.0),
-            "hbm_peak_gbs": peaks.get("hbm_gbs", 6555.0),
-            "note": "ozgemm vs 2 x MEASURED_PEAKS bf16 (int8 dense); Cholesky+solves as "
-                    "standard-count FP64 flops / phase time vs the 36.08 TF/s DGEMM peak "
-                    "(>1: the Ozaki emulation beats the FP64 pipe); slicing and generation "
-                    "as algorithmic bytes / kernel time vs MEASURED_PEAKS hbm_gbs"},
-        "gpu_launches": int(acc["launches"]),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_desc(world),
+        "fits": {"loglik_calls_in_timed_steps": ll_calls,
+                 "completed_fits_so_far": len(stepper.done),
+                 "theta_hat_e2e_fit": res.theta_hat.as_array().tolist(),
+                 "grad_calls_e2e_fit": res.grad_calls, "loglik_calls_e2e_fit": res.loglik_calls,
+                 "termination_e2e_fit": res.termination.value},
         "clocks": clk,
-        "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
-        "fits": {"grad_calls_per_step": grad_all / args.steps,
-                 "loglik_calls_per_step": ll_all / args.steps,
-                 "batched_passes_per_step": batches / args.steps,
-                 "eval_passes_per_step": sum(c.eval_passes for c in coords) / args.steps,
-                 "device_ms_per_step": {k: acc[k] / args.steps
-                                        for k in ("gen_ms", "potrf_ms", "solve_ms",
-                                                  "reduce_ms")},
-                 "theta_hat_rank0": [r.theta_hat.as_array().tolist() for r in last_fits]},
-        "isolated": iso,
+        "e2e": {"value": e2e_value, "unit": "it/s",
+                "h2d_bytes_per_step": int(loc.nbytes + z.nbytes),
+                "d2h_bytes_per_step": int(res.loglik_calls * (9 * 8 + 4 + 8)),
+                "what": "one complete config-4 fit per e2e step (dataset upload from host "
+                        "arrays, L9 start, every Fisher iteration, results to host)"},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_iteration_sample(1)
-        line["cpu_baseline"] = {
-            "value": cpu["value"], "unit": "it/s", "cores": cpu_cores(), "kind": "port",
-            "sample": "one config-2 eval_all + rho=%.3f loglik (reference algorithm, numpy/"
-                      "scipy/OpenBLAS) = one mean Fisher iteration; eval_all %.2fs, loglik "
-                      "%.2fs" % (cpu["rho"], cpu["t_eval_all_s"], cpu["t_loglik_s"])}
+    if world == 1:
+        data = m.SpatialDataset(loc, z, device=local_rank)
+        kp = kernel_profile(data.engine(), wl.theta_true, wl.n, peaks)
+        launches_per_eval = data.engine().phase_times()["launches"]
+        data.release()
+        line["roofline"] = {
+            "bound": "tensor", "unit": "TFLOP/s", "achieved": kp["ozgemm_alg_int8_tops"],
+            "peak": kp["int8_peak_tops"], "frac": kp["ozgemm_alg_int8_tops"] / kp["int8_peak_tops"],
+            "traffic": None,
+            "kernel": "ozgemm_persistent_kernel<64,7,2> (Ozaki FP64 GEMM on tcgen05.mma kind::i8)"
+                      ": ALGORITHMIC FP64 flops of one config-4 eval_all's GEMM launches (3n^3 - "
+                      "256n^2) x 28 int8 slice products / summed launch durations (CUDA events "
+                      "on the launching stream, kernel-profiling pass)",
+            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 dense = 2 x bf16 "
+                           "dense; sustained: the GEMMs run for seconds inside a step)",
+            "traffic_note": "see profiles/r02_* (ncu of the same build)",
+            "int8_pipe_microbench_tops": INT8_PIPE_TOPS,
+            "fp64_equiv_tflops_algorithmic": kp["ozgemm_alg_fp64_equiv_tflops"],
+            "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS}
+        line["kernels"] = kp
+        line["kernels"]["launches_per_profiled_eval_all"] = launches_per_eval
+        try:
+            line["context"] = extra_single_gpu(m, local_rank)
+        except Exception as exc:  # context numbers must not sink the headline
+            line["context"] = {"error": repr(exc)}
+        if not args.no_cpu_baseline:
+            cpu = cpu_config4_sample()
+            line["cpu_baseline"] = {
+                "value": cpu["value"], "unit": "it/s", "cores": cpu_cores(), "kind": "port",
+                "sample": "reference algorithm (oracle port) on %d config-4 pairs + LAPACK / "
+                          "memory-bound phases at n=%d, EXTRAPOLATED to one config-4 Fisher "
+                          "iteration (eval_all + %.1f loglik): %.0f s" % (
+                              cpu["sample_pairs"], cpu["n_lin"], CONFIG4_RHO,
+                              cpu["iteration_s"])}
+    line["gpu_launches"] = int(launches)  # rank 0's kernels in the timed steps (mle_launch_count)
     print(json.dumps(line), flush=True)
 
 

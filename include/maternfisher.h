@@ -15,6 +15,8 @@
  *   mle_cholesky     <- cholesky_lower(sigma)                       pkg/src/maternmle/likelihood.py:63-78
  *   mle_bessel_k     <- bessel_k(nu, x)                             pkg/src/maternmle/bessel.py:80-100
  *   mle_dnu_xnu_knu  <- dnu_xnu_knu(nu, x)                          pkg/src/maternmle/bessel.py:327-370
+ *   mle_dnu_series   <- case2_series / case3_series / case4_series  pkg/src/maternmle/bessel.py:184-318
+ *   mle_digamma      <- digamma(nu)                                 pkg/src/maternmle/bessel.py:103-115
  *   mle_matern_elem  <- matern_cov / dcov_dalpha / dcov_dnu / dcov_dsigma2 on distance arrays
  *                                                                    pkg/src/maternmle/matern.py:100-168
  *
@@ -152,6 +154,10 @@ int mle_build(mle_ctx* ctx, const double theta[3], int which, double* out_host);
  * (MLE_NUM_PHASES + 3 doubles in total). */
 int mle_phase_times(const mle_ctx* ctx, double* out);
 
+/* Kernels this library has launched since it was loaded, all contexts and devices
+ * (diagnostics: the bench reads it around its timed region). */
+int64_t mle_launch_count(void);
+
 /* Dense lower Cholesky of a host n x n symmetric matrix (row-major; only the lower triangle
  * is read).  l_out receives L with a zeroed strict upper triangle (LAPACK clean=1). */
 int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t* bad_pivot);
@@ -159,6 +165,16 @@ int mle_cholesky(const double* a, int64_t n, int device, double* l_out, int64_t*
 /* Elementwise special functions on the GPU, m points, host in/out. */
 int mle_bessel_k(double nu, const double* x, int64_t m, int device, double* out);
 int mle_dnu_xnu_knu(double nu, const double* x, int64_t m, int device, double* out);
+
+/* One order-derivative series on its own domain (drop-in for case2_series / case3_series /
+ * case4_series, bessel.py:184-318): which_case 2 (0 < x < 8.5, nu off integers), 3
+ * (8.5 <= x < 30), 4 (x >= 30); nu > 0.  Domain violations return MLE_INVALID. */
+int mle_dnu_series(int which_case, double nu, const double* x, int64_t m, int device,
+                   double* out);
+
+/* digamma psi(x) (drop-in for bessel.digamma, bessel.py:103-115; host arithmetic, the per-theta
+ * prologue's own routine).  Poles (non-positive integers) return MLE_INVALID. */
+int mle_digamma(const double* x, int64_t m, double* out);
 
 /* Elementwise Matern covariance / derivatives at distances h (h >= 0) for theta:
  * which = MLE_WHICH_* selects C, dC/dsigma2, dC/dalpha or dC/dnu; h = 0 gives the

@@ -8,7 +8,18 @@ Importing the package loads ``libmaternfisher.so``; there is no CPU fallback.
 """
 
 from .batch import BatchCoordinator, BatchedObjective, eval_batch, fit_many
-from .bessel import BesselRegime, bessel_k, dnu_xnu_knu, select_regime
+from .bessel import (
+    BesselRegime,
+    MidRangeSmallOrderWarning,
+    bessel_k,
+    case2_series,
+    case3_series,
+    case4_series,
+    digamma,
+    dnu_xnu_knu,
+    select_regime,
+    u_poly_coeffs,
+)
 from .datasets import WORKLOADS, Workload, gmm_locations, jittered_grid, simulate_field
 from .engine import Engine
 from .fisher_bt import (
@@ -44,13 +55,26 @@ from .matern import (
     dcov_dsigma2,
     matern_cov,
 )
+from .simulate import (
+    GENERATOR_ID,
+    LocationScheme,
+    PlanError,
+    SimulationPlan,
+    gen_locations,
+    microergodic,
+    replicate_seed,
+    simulate_grf,
+)
 from ._native import device_count, LIB_PATH
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchCoordinator", "BatchedObjective", "eval_batch", "fit_many",
-    "BesselRegime", "bessel_k", "dnu_xnu_knu", "select_regime",
+    "BesselRegime", "MidRangeSmallOrderWarning", "bessel_k", "case2_series", "case3_series",
+    "case4_series", "digamma", "dnu_xnu_knu", "select_regime", "u_poly_coeffs",
+    "GENERATOR_ID", "LocationScheme", "PlanError", "SimulationPlan", "gen_locations",
+    "microergodic", "replicate_seed", "simulate_grf",
     "WORKLOADS", "Workload", "gmm_locations", "jittered_grid", "simulate_field",
     "Engine",
     "FisherBTConfig", "InitializationFailed", "LikelihoodObjective", "OptResult",

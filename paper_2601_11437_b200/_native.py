@@ -33,7 +33,7 @@ EXPORTED = (
     "mle_kernel_profile", "mle_kernel_stats", "mle_ctx_cond_estimate", "mle_dctx_create", "mle_dctx_destroy",
     "mle_dctx_layout", "mle_dctx_begin", "mle_dctx_factor", "mle_dctx_update",
     "mle_dctx_wblock", "mle_dctx_forward", "mle_dctx_right_operand", "mle_dctx_right",
-    "mle_dctx_partials",
+    "mle_dctx_partials", "mle_launch_count", "mle_dnu_series", "mle_digamma",
 )
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -53,6 +53,10 @@ def _load():
         "mle_last_error": (ctypes.c_char_p, []),
         "mle_device_count": (ctypes.c_int, []),
         "mle_release_cached_memory": (ctypes.c_int, []),
+        "mle_launch_count": (ctypes.c_int64, []),
+        "mle_dnu_series": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _dp, ctypes.c_int64,
+                                          ctypes.c_int, _dp]),
+        "mle_digamma": (ctypes.c_int, [_dp, ctypes.c_int64, _dp]),
         "mle_kernel_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
         "mle_kernel_stats": (ctypes.c_int, [ctypes.c_void_p, _dp]),
         "mle_ctx_cond_estimate": (ctypes.c_int, [ctypes.c_void_p, _dp]),

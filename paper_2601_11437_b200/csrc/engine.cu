@@ -22,6 +22,7 @@
 // Cholesky (Fisher-BT always follows an accepted loglik(theta) with eval_all(theta),
 // optimizer.py:362,375).  Results are bit-identical to recomputing.
 #include <cuda_runtime.h>
+#include <atomic>
 
 #include <algorithm>
 #include <cmath>
@@ -463,7 +464,12 @@ struct MatList {
   }
 };
 
+// Process-wide count of kernels this library has launched (every Launcher adds its own count
+// when it goes out of scope; mle_launch_count reads it).
+std::atomic<long long> g_launch_total{0};
+
 struct Launcher {
+  ~Launcher() { g_launch_total.fetch_add((long long)launches); }
   cudaStream_t s;              // main: inner chains
   cudaStream_t s2 = nullptr;   // side: bulk trailing updates (null: everything on s)
   cudaEvent_t* pool = nullptr; // event pool for cross-stream joins
@@ -2091,6 +2097,8 @@ int mle_build(mle_ctx* c, const double theta[3], int which, double* out_host) {
   return MLE_OK;
 }
 
+int64_t mle_launch_count(void) { return (int64_t)g_launch_total.load(); }
+
 int mle_phase_times(const mle_ctx* c, double* out) {
   if (!c || !out) return fail(MLE_INVALID, "null argument");
   for (int p = 0; p < MLE_NUM_PHASES; ++p) out[p] = c->phase_ms[p];
@@ -2229,6 +2237,38 @@ int mle_dnu_xnu_knu(double nu, const double* x, int64_t m, int device, double* o
   const double th[3] = {1.0, 1.0, nu};
   if (mle_fill_theta(th, 0.0, &P) != 0) return fail(MLE_INVALID, "invalid nu");
   return run_elem(1, P, 0, x, m, device, out);
+}
+
+int mle_dnu_series(int which_case, double nu, const double* x, int64_t m, int device,
+                   double* out) {
+  if ((!x || !out) && m > 0) return fail(MLE_INVALID, "null argument");
+  if (which_case < 2 || which_case > 4) return fail(MLE_INVALID, "series must be 2, 3 or 4");
+  if (!std::isfinite(nu)) return fail(MLE_INVALID, "series requires finite nu");
+  for (int64_t i = 0; i < m; ++i) {
+    const double v = x[i];
+    if (which_case == 2 && !(v > 0.0 && v < MLE_SMALL_MID_SPLIT))  // bessel.py:196-197
+      return fail(MLE_INVALID, "case2_series requires 0 < x < 8.5");
+    if (which_case == 3 && !(v >= MLE_SMALL_MID_SPLIT && v < MLE_MID_LARGE_SPLIT))  // :237-238
+      return fail(MLE_INVALID, "case3_series requires 8.5 <= x < 30");
+    if (which_case == 4 && !(v >= MLE_MID_LARGE_SPLIT))  // bessel.py:299-300
+      return fail(MLE_INVALID, "case4_series requires x >= 30");
+  }
+  if (which_case == 2 && std::fabs(nu - std::nearbyint(nu)) <= 1e-6)  // bessel.py:198-199
+    return fail(MLE_INVALID, "case2_series requires nu away from integers");
+  if (nu <= 0.0) return fail(MLE_INVALID, "series requires nu > 0");
+  ThetaParams P;
+  const double th[3] = {1.0, 1.0, nu};
+  if (mle_fill_theta(th, 0.0, &P) != 0) return fail(MLE_INVALID, "invalid nu");
+  return run_elem(3, P, which_case, x, m, device, out);
+}
+
+int mle_digamma(const double* x, int64_t m, double* out) {
+  if ((!x || !out) && m > 0) return fail(MLE_INVALID, "null argument");
+  for (int64_t i = 0; i < m; ++i)
+    if (x[i] <= 0.0 && x[i] == std::floor(x[i]))  // bessel.py:111-112
+      return fail(MLE_INVALID, "digamma has poles at non-positive integers");
+  for (int64_t i = 0; i < m; ++i) out[i] = mle_digamma_host(x[i]);
+  return MLE_OK;
 }
 
 int mle_matern_elem(const double theta[3], int which, const double* h, int64_t m, int device,

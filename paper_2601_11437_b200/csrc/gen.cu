@@ -328,9 +328,12 @@ __global__ void __launch_bounds__(kGThreads) gen_panel_kernel(GenArgs a, const i
 // MLE_TAB_MAX x items; one CTA per interval).  Node values come from the exact evaluator
 // (matern_u), so the table inherits its accuracy: Chebyshev interpolation at 14 nodes on
 // intervals of ratio <= 1.125 (binade eighths; a convergence factor > 30 puts the degree-13
-// truncation far below one ulp), then converted to the monomial basis in t in [-1, 1] for a one-FMA-per-term
-// Horner evaluation.  The conversion is benign: |a_i| <~ sum_j |c_j| |T_j coefficients| with
-// |c_j| ~ 22^-j against coefficient growth (1 + sqrt 2)^j.  Layout [interval][c, da, dn]
+// truncation far below one ulp), expressed in the monomial basis in t in [-1, 1] for a
+// one-FMA-per-term Horner evaluation.  Node values -> coefficients is one fixed linear map
+// (transform + basis change, built in long double on the host) applied in double-double, so
+// each coefficient is rounded once: computing it in plain double cost ~10x in accuracy
+// (2.7e-15 vs 1.8e-16 relative on exact node values at u in [0.25, 2.25)), which moved the
+// ill-conditioned goldens' log-likelihoods by ~1e-10.  Layout [interval][c, da, dn]
 // [power] (16-byte aligned power pairs: the evaluator loads two coefficients per request).
 __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
   const GenItem& it = a.item[blockIdx.y];
@@ -339,7 +342,6 @@ __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
   const int k = blockIdx.x;
   if (k >= P.tab_n) return;
   __shared__ double f[3][MLE_TAB_P];
-  __shared__ double cc[3][MLE_TAB_P];
   const int t = threadIdx.x;
   if (t < MLE_TAB_P) {
     const double x = cospi((t + 0.5) / MLE_TAB_P);
@@ -351,33 +353,24 @@ __global__ void __launch_bounds__(64) gen_table_kernel(GenArgs a, int derivs) {
     f[2][t] = e * v.dnu;
   }
   __syncthreads();
+  // monomial coefficients a_i = sum_q M[i][q] f_q in double-double (M as hi + lo pairs):
+  // the map has entries ~1e4 with alternating signs while high-order a_i are tiny, so a
+  // plain double sum would leave ~10 ulps of cancellation error in every coefficient.
   if (t < 3 * MLE_TAB_P) {
-    const int fn = t / MLE_TAB_P, j = t % MLE_TAB_P;
-    double s = 0.0;
-    for (int q = 0; q < MLE_TAB_P; ++q) s += f[fn][q] * cospi(j * (q + 0.5) / MLE_TAB_P);
-    s *= 2.0 / MLE_TAB_P;
-    if (j == 0) s *= 0.5;
-    cc[fn][j] = s;
-  }
-  __syncthreads();
-  if (t < 3) {  // monomial coefficients a_i = sum_j c_j [t^i] T_j(t)
-    double Tm[MLE_TAB_P], Tc[MLE_TAB_P], Tn[MLE_TAB_P], acc[MLE_TAB_P];
-    for (int i = 0; i < MLE_TAB_P; ++i) Tm[i] = Tc[i] = acc[i] = 0.0;
-    Tm[0] = 1.0;             // T_0
-    Tc[1] = 1.0;             // T_1
-    acc[0] = cc[t][0];
-    acc[1] = cc[t][1];
-    for (int j = 2; j < MLE_TAB_P; ++j) {  // T_j = 2 t T_{j-1} - T_{j-2}
-      for (int i = 0; i < MLE_TAB_P; ++i)
-        Tn[i] = (i > 0 ? 2.0 * Tc[i - 1] : 0.0) - Tm[i];
-      for (int i = 0; i < MLE_TAB_P; ++i) {
-        Tm[i] = Tc[i];
-        Tc[i] = Tn[i];
-      }
-      // higher j first would be marginally better; terms shrink ~22x per j either way
-      for (int i = 0; i <= j; ++i) acc[i] = fma(cc[t][j], Tn[i], acc[i]);
+    const int fn = t / MLE_TAB_P, i = t % MLE_TAB_P;
+    double s_hi = 0.0, s_lo = 0.0;
+    for (int q = 0; q < MLE_TAB_P; ++q) {
+      const double fq = f[fn][q];
+      const double mh = c_tab_map[0][i][q], ml = c_tab_map[1][i][q];
+      const double p = mh * fq;
+      const double pe = fma(mh, fq, -p) + ml * fq;  // exact product error + low part
+      const double sum = s_hi + p;                  // two-sum(s_hi, p)
+      const double bv = sum - s_hi;
+      const double se = (s_hi - (sum - bv)) + (p - bv);
+      s_hi = sum;
+      s_lo += se + pe;
     }
-    for (int i = 0; i < MLE_TAB_P; ++i) it.tab[((size_t)k * 3 + t) * MLE_TAB_P + i] = acc[i];
+    it.tab[((size_t)k * 3 + fn) * MLE_TAB_P + i] = s_hi + s_lo;
   }
 }
 
@@ -444,17 +437,21 @@ __global__ void elem_kernel(const ThetaParams* Pg, int op, int which,
     double r;
     if (op == 0) {  // bessel_k(nu, x) = K_|nu|(x), x > 0 validated on the host
       double k_nu, k_m1;
-      bessel_k_ladder(P.kmain, P.recip_int, v, &k_nu, &k_m1);
+      bessel_k_ladder(P.kmain, v, &k_nu, &k_m1);
       r = k_nu;
     } else if (op == 1) {  // dnu_xnu_knu(nu, x), x >= 0
       if (v == 0.0) {
         r = 0.0;  // bessel.py:358 (ZERO_ARG)
       } else {
         double k_nu, k_m1;
-        bessel_k_ladder(P.kmain, P.recip_int, v, &k_nu, &k_m1);
+        bessel_k_ladder(P.kmain, v, &k_nu, &k_m1);
         const double v_nu = pow(v, P.nu);
         r = dnu_xnu_knu(P, v, v_nu * k_nu, v_nu);
       }
+    } else if (op == 3) {  // one d/dnu series by itself (case2/3/4_series), domain checked
+      const double v_nu = pow(v, P.nu);
+      r = which == 2 ? dnu_case2(P, v, v_nu) : which == 3 ? dnu_case3(P, v, v_nu)
+                                                          : dnu_case4(P, v, v_nu);
     } else {  // Matern value / derivative at distance h >= 0
       if (v > 0.0) {
         if (which == MLE_WHICH_SIGMA || which == MLE_WHICH_SIGMA2) {
@@ -476,8 +473,12 @@ cudaError_t upload_u_tables(const double* u, const double* du) {
   cudaError_t e = cudaMemcpyToSymbol(c_u_coef, u, sizeof(double) * (MLE_CASE3_NEAR + 1) *
                                                       MLE_U_COEFF_STRIDE);
   if (e != cudaSuccess) return e;
-  return cudaMemcpyToSymbol(c_du_coef, du,
-                            sizeof(double) * (MLE_CASE3_NEAR + 1) * MLE_U_COEFF_STRIDE);
+  e = cudaMemcpyToSymbol(c_du_coef, du, sizeof(double) * (MLE_CASE3_NEAR + 1) *
+                                            MLE_U_COEFF_STRIDE);
+  if (e != cudaSuccess) return e;
+  double map[2][MLE_TAB_P * MLE_TAB_P];
+  mle_fill_tab_map(map[0], map[1]);
+  return cudaMemcpyToSymbol(c_tab_map, map, sizeof(map));
 }
 
 static long long lower_tiles(long long rows) {

@@ -59,8 +59,9 @@ long double recip_gamma_1p(long double x) {
   return s;
 }
 
-// gam1 = (1/G(1-mu) - 1/G(1+mu)) / (2 mu) = -sum_{k odd} c_k mu^{k-1}  (no cancellation)
-long double temme_gam1(long double mu) {
+// (1/G(1-mu) - 1/G(1+mu)) / (2 mu) = -sum_{k odd} c_k mu^{k-1}: the odd part of the Taylor
+// series divided by mu, so it has no cancellation and a finite limit (-Euler gamma) at mu = 0.
+long double recip_gamma_odd_over_mu(long double mu) {
   long double s = 0.0L;
   const long double m2 = mu * mu;
   for (int k = 29; k >= 1; k -= 2) s = s * m2 + kRecipGammaTaylor[k];
@@ -92,7 +93,7 @@ long double digamma_neg(long double nu) {
 }
 
 // pi mu / sin(pi mu), series near 0.
-long double temme_fact(long double mu) {
+long double pi_mu_over_sin(long double mu) {
   const long double pm = kPiL * mu;
   if (fabsl(pm) < 1e-4L) return 1.0L + pm * pm / 6.0L + 7.0L * pm * pm * pm * pm / 360.0L;
   return pm / sinl(pm);
@@ -102,6 +103,20 @@ long double temme_fact(long double mu) {
 // K_{order-1}: for order >= 1/2 the pair (K_{order-1}, K_order) is reached from mu =
 // order - N; for order < 1/2 we start from mu = -order so that the pair is
 // (K_{-order} = K_order, K_{1-order} = K_{order-1}).
+//
+// Small-argument coefficients.  Temme's expansion of the pair (|mu| <= 1/2):
+//   K_mu(x)         = sum_k (d^k / k!) f_k,
+//   (x/2) K_{mu+1}  = sum_k (d^k / k!) (p_k - k f_k),          d = x^2 / 4,
+//   f_k = (k f_{k-1} + p_{k-1} + q_{k-1}) / (k^2 - mu^2),  p_k = p_{k-1} / (k - mu),
+//   q_k = q_{k-1} / (k + mu),
+// with seeds f_0, p_0, q_0 that carry all the x dependence (theta.h).  Every step is linear
+// with mu-only coefficients, so f_k = a_k f_0 + b_k p_0 + c_k q_0 and p_k = P_k p_0,
+// q_k = Q_k q_0, where
+//   a_0 = 1, b_0 = c_0 = 0, P_0 = Q_0 = 1,
+//   a_k = k a_{k-1} / (k^2 - mu^2),  b_k = (k b_{k-1} + P_{k-1}) / (k^2 - mu^2),
+//   c_k = (k c_{k-1} + Q_{k-1}) / (k^2 - mu^2),  P_k = P_{k-1} / (k - mu),  Q_k = Q_{k-1} / (k + mu).
+// The d^k coefficients (a_k, b_k, c_k) / k! and (-k a_k, P_k - k b_k, -k c_k) / k! are formed in
+// long double and rounded once; a_k, b_k, c_k, P_k, Q_k are all positive for |mu| <= 1/2.
 void fill_ladder(double order, KLadder* L) {
   const double N = std::floor(order + 0.5);
   double mu;
@@ -116,25 +131,31 @@ void fill_ladder(double order, KLadder* L) {
   }
   const long double m = mu;
   L->mu = mu;
-  const long double gp = recip_gamma_1p(m);
-  const long double gm = recip_gamma_1p(-m);
-  L->gampl = (double)gp;
-  L->gammi = (double)gm;
-  L->gam1 = (double)temme_gam1(m);
-  L->gam2 = (double)(0.5L * (gp + gm));
-  L->fact = (double)temme_fact(m);
-  L->t_rim[0] = L->t_rip[0] = L->t_rid[0] = 0.0;
-  for (int i = 1; i <= MLE_TEMME_MAX; ++i) {
-    const long double il = (long double)i;
-    L->t_rim[i] = (double)(1.0L / (il - m));
-    L->t_rip[i] = (double)(1.0L / (il + m));
-    L->t_rid[i] = (double)(1.0L / (il * il - m * m));
-  }
-  const long double a1 = 0.25L - m * m;
-  L->cf_ra[0] = L->cf_ra[1] = 0.0;
-  for (int i = 2; i <= MLE_CF2_MAX; ++i) {
-    const long double il = (long double)i;
-    L->cf_ra[i] = (double)(1.0L / (-a1 - il * (il - 1.0L)));
+  const long double rg_plus = recip_gamma_1p(m);    // 1 / G(1 + mu)
+  const long double rg_minus = recip_gamma_1p(-m);  // 1 / G(1 - mu)
+  const long double pms = pi_mu_over_sin(m);
+  L->f0_cosh = (double)(pms * recip_gamma_odd_over_mu(m));
+  L->f0_sinh = (double)(pms * 0.5L * (rg_plus + rg_minus));
+  L->p0 = (double)(0.5L / rg_plus);
+  L->q0 = (double)(0.5L / rg_minus);
+  long double a = 1.0L, b = 0.0L, c = 0.0L, pk = 1.0L, qk = 1.0L, fact = 1.0L;
+  for (int k = 0; k < MLE_KSER_TERMS; ++k) {
+    const long double kl = (long double)k;
+    if (k > 0) {
+      const long double den = kl * kl - m * m;
+      a = kl * a / den;
+      b = (kl * b + pk) / den;
+      c = (kl * c + qk) / den;
+      pk /= kl - m;
+      qk /= kl + m;
+      fact *= kl;
+    }
+    L->ser[k][0] = (double)(a / fact);
+    L->ser[k][1] = (double)(b / fact);
+    L->ser[k][2] = (double)(c / fact);
+    L->ser[k][3] = (double)(-kl * a / fact);
+    L->ser[k][4] = (double)((pk - kl * b) / fact);
+    L->ser[k][5] = (double)(-kl * c / fact);
   }
 }
 
@@ -171,7 +192,7 @@ int mle_fill_theta(const double theta[3], double nugget, ThetaParams* P) {
   P->nu_fd = nu + MLE_FD_LAG;                                    // bessel.py:322
   fill_ladder(P->nu_fd, &P->kfd);
   P->recip_int[0] = 0.0;
-  for (int i = 1; i <= MLE_CF2_MAX; ++i) P->recip_int[i] = 1.0 / (double)i;
+  for (int i = 1; i <= MLE_RECIP_INT_MAX; ++i) P->recip_int[i] = 1.0 / (double)i;
   P->fd_small = near_integer(nu) ? 1 : 0;                        // bessel.py:361-363
   P->fd_large = near_half_integer(nu) ? 1 : 0;                   // bessel.py:364-366
   P->two_nu = 2.0 * nu;
@@ -295,4 +316,43 @@ void mle_fill_gen_table(double u_max, ThetaParams* P) {
   if (k >= MLE_TAB_MAX && P->tab_ctr[k - 1] + P->tab_hw[k - 1] < hi)
     P->tab_hi = P->tab_ctr[k - 1] + P->tab_hw[k - 1];  // (MLE_TAB_HI keeps this unreachable)
   P->tab_n = k;
+}
+
+// M = (monomial coefficients of T_j) x (discrete Chebyshev transform at the nodes
+// t_q = cos(pi (q + 1/2) / P)): a_i = sum_q M[i][q] f(t_q).  Transform: c_j = (2 / P) sum_q
+// f_q cos(pi j (q + 1/2) / P), halved for j = 0; T_j from T_j = 2 t T_{j-1} - T_{j-2} (integer
+// coefficients, exact).  Built in long double and split into a double-double pair.
+void mle_fill_tab_map(double* hi, double* lo) {
+  constexpr int P = MLE_TAB_P;
+  long double mono[P][P] = {};  // mono[j][i] = [t^i] T_j(t)
+  mono[0][0] = 1.0L;
+  mono[1][1] = 1.0L;
+  for (int j = 2; j < P; ++j)
+    for (int i = 0; i < P; ++i)
+      mono[j][i] = (i > 0 ? 2.0L * mono[j - 1][i - 1] : 0.0L) - mono[j - 2][i];
+  for (int i = 0; i < P; ++i) {
+    for (int q = 0; q < P; ++q) {
+      long double m = 0.0L;
+      for (int j = i; j < P; ++j) {
+        long double w = (2.0L / P) * cosl(kPiL * j * (q + 0.5L) / P);
+        if (j == 0) w *= 0.5L;
+        m += mono[j][i] * w;
+      }
+      const double h = (double)m;
+      hi[i * P + q] = h;
+      lo[i * P + q] = (double)(m - (long double)h);
+    }
+  }
+}
+
+// psi(x) for any x off the poles: the upward-shift asymptotic series for x > 0, reflection
+// psi(1 - x) - psi(x) = pi cot(pi x) below (the cotangent on the reduced argument).
+double mle_digamma_host(double x) {
+  if (std::isnan(x)) return x;
+  if (x > 0.0) return (double)digamma_pos((long double)x);
+  const long double xl = x;
+  const long double fl = floorl(xl);
+  const long double frac = xl - fl;  // in (0, 1): x is not a pole here
+  const long double cot = cosl(kPiL * frac) / sinl(kPiL * frac);
+  return (double)(digamma_pos(1.0L - xl) - kPiL * cot);
 }

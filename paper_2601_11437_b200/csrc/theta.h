@@ -8,7 +8,7 @@
 //   case-3 weights (sign * nu^-k ...)  pkg/src/maternmle/bessel.py:226-283
 //   case-4 a_k, b_k                    pkg/src/maternmle/bessel.py:286-318
 //   FD band and lag                    pkg/src/maternmle/bessel.py:117-141, 321-324
-// The K_nu ladder parameters (Temme / Steed CF2) replace scipy.special.kv.
+// The K_nu ladder parameters (Temme expansion / trapezoidal integral) replace scipy.special.kv.
 #pragma once
 
 #define MLE_CASE2_TERMS 20       // bessel.py:52  (k = 0..20)
@@ -29,24 +29,30 @@
 #define MLE_MID_TRUNC_SPLIT 15.0 // bessel.py:48
 #define MLE_FD_LAG 1e-9          // bessel.py:50
 
-#define MLE_TEMME_MAX 40  // Temme series terms (x < 2 converges in < 30)
-#define MLE_CF2_MAX 128   // Steed CF2 iterations (x >= 2 converges in < 80)
+#define MLE_KSER_XMAX 1.0  // x below: small-argument series; at and above: trapezoidal rule
+#define MLE_KSER_TERMS 14  // power-series terms in d = x^2/4 <= 1/4 (d^13 / 13!^2 < 1e-27)
+#define MLE_KTRAP_MAX 64   // trapezoid nodes cap (x >= 1 needs <= ~30)
+#define MLE_RECIP_INT_MAX 40
 
-// Parameters of one K-ladder: K_mu, K_{mu+1} by Temme's series (x < 2) or Steed's
-// continued fraction (x >= 2), |mu| <= 1/2, then `nsteps` upward recurrences.  The
-// mu-only denominators of both iterations are tabulated once per theta so the per-pair
-// loops multiply instead of divide (CF2 keeps only its one data-dependent division).
+// Parameters of one K-ladder: K_mu and K_{mu+1} for |mu| <= 1/2 (special.cuh,
+// bessel_k_pair), then `nsteps` upward recurrences.
+//
+// Small-argument data (x < MLE_KSER_XMAX).  Temme's expansion writes K_mu and K_{mu+1}
+// through three sequences f_k, p_k, q_k that obey mu-only linear recurrences from seeds
+// f0(x), p0(x), q0(x); unrolled, each of K_mu, (x/2) K_{mu+1} is f0, p0, q0 times a power
+// series in d = x^2/4 whose coefficients depend on mu alone (prologue.cpp, fill_ladder):
+//   ser[k][0..2]: d^k coefficient multiplying f0, p0, q0 in K_mu,
+//   ser[k][3..5]: the same for (x/2) K_{mu+1}.
+// Seeds: f0 = f0_cosh cosh(s) + f0_sinh ln(2/x) sinh(s)/s with s = mu ln(2/x);
+//        p0 = p0c (x/2)^-mu,  q0 = q0c (x/2)^mu.
 struct KLadder {
   double mu;
-  double gam1, gam2;     // (1/G(1-mu) - 1/G(1+mu)) / (2 mu),  (1/G(1-mu) + 1/G(1+mu)) / 2
-  double gampl, gammi;   // 1/G(1+mu), 1/G(1-mu)
-  double fact;           // pi mu / sin(pi mu)
   int nsteps;            // upward recurrence steps applied to (K_mu, K_{mu+1})
   int order_is_low;      // 1: K_nu is the lower member of the final pair (nu < 1/2 case)
-  double t_rim[MLE_TEMME_MAX + 1];  // 1 / (i - mu)
-  double t_rip[MLE_TEMME_MAX + 1];  // 1 / (i + mu)
-  double t_rid[MLE_TEMME_MAX + 1];  // 1 / (i^2 - mu^2)
-  double cf_ra[MLE_CF2_MAX + 1];    // 1 / a_i,  a_i = -(1/4 - mu^2) - i (i - 1)
+  double f0_cosh;        // (pi mu / sin pi mu) * (1/G(1-mu) - 1/G(1+mu)) / (2 mu)
+  double f0_sinh;        // (pi mu / sin pi mu) * (1/G(1-mu) + 1/G(1+mu)) / 2
+  double p0, q0;         // G(1+mu) / 2, G(1-mu) / 2
+  double ser[MLE_KSER_TERMS][6];
 };
 
 struct ThetaParams {
@@ -60,7 +66,7 @@ struct ThetaParams {
   int fd_large;     // nu within 1e-6 of a half-integer: x >= 30 uses the FD fallback
   KLadder kmain;    // ladder for K_nu and K_{nu-1}
   KLadder kfd;      // ladder for K_{nu_fd} (only used in FD bands)
-  double recip_int[MLE_CF2_MAX + 1];  // 1 / i
+  double recip_int[MLE_RECIP_INT_MAX + 1];  // 1 / i (case-2 prefactor recursion)
   // ---- case 2 (0 < x < 8.5) ----
   double c2_term_pos[MLE_CASE2_TERMS + 1];  // 2^nu (log2 + psi(nu) - d_k(-nu)) G(nu) g_k(-nu)
   double c2_d_pos[MLE_CASE2_TERMS + 1];     // d_k(nu)
@@ -105,5 +111,12 @@ void mle_fill_u_tables(double* u, double* du);
 // Interval layout of the generation tables for scaled distances up to u_max (tab_n = 0
 // when u_max < MLE_TAB_LO).
 void mle_fill_gen_table(double u_max, ThetaParams* P);
+// The linear map from the MLE_TAB_P Chebyshev-node values of an interval to the monomial
+// coefficients (powers of t in [-1, 1]) of their interpolant, as double-double pairs
+// hi[i * MLE_TAB_P + q] + lo[...] (long-double construction).  The table kernel applies it in
+// double-double arithmetic so the coefficients carry one rounding each.
+void mle_fill_tab_map(double* hi, double* lo);
+// digamma of a double off the poles (host; the prologue's psi(nu) uses the same series).
+double mle_digamma_host(double x);
 }
 #endif

@@ -64,14 +64,16 @@ def gmm_locations(n: int, seed: int, components: int = 8,
     return out
 
 
-def simulate_field(locations, theta, seed: int, device: int = 0) -> np.ndarray:
-    """One exact draw z = L w from N(0, Sigma(theta)) computed on the GPU
+def simulate_field(locations, theta, seed: int, device: int = 0,
+                   nugget: float = 0.0) -> np.ndarray:
+    """One exact draw z = L w from N(0, Sigma(theta) + nugget I) computed on the GPU
     (reference ``simulate_grf``, simulate.py:100-106)."""
     from .matern import MaternParams, SpatialDataset
 
     locations = np.asarray(locations, dtype=float)
     theta = theta if isinstance(theta, MaternParams) else MaternParams.from_array(theta)
-    holder = SpatialDataset(locations, np.zeros(locations.shape[0]), device=device)
+    holder = SpatialDataset(locations, np.zeros(locations.shape[0]), device=device,
+                            nugget=nugget)
     normals = np.random.default_rng(seed).standard_normal(locations.shape[0])
     z = holder.engine().simulate(theta.as_array(), normals)
     holder.release()

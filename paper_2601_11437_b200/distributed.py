@@ -36,7 +36,8 @@ import numpy as np
 from .likelihood import LikelihoodEval, NotPositiveDefinite
 from .matern import MaternParams
 
-__all__ = ["DistributedEngine", "TorchComm", "InProcessComm", "CudaPanels", "results_from_sums"]
+__all__ = ["DistributedEngine", "DistributedObjective", "TorchComm", "InProcessComm", "CudaPanels",
+           "results_from_sums"]
 
 LOG_2PI = 1.8378770664093453  # likelihood.py:38
 BLOCK = 512
@@ -281,3 +282,29 @@ class DistributedEngine:
     def grad_and_fisher(self, theta) -> LikelihoodEval:
         ll, g, f = self.eval_all(theta)
         return LikelihoodEval(loglik=ll, grad=g, fisher=f)
+
+
+class DistributedObjective:
+    """The reference's objective surface (optimizer.py:114-142) over a DistributedEngine:
+    ``loglik`` counts one call and maps NotPositiveDefinite / ValueError / NaN to -inf;
+    ``eval_all`` counts one call of each kind and propagates errors.  Every rank runs the
+    same deterministic host loop (fisher_bt) over its own instance, so every call is a
+    collective entered by all ranks in the same order."""
+
+    def __init__(self, engine: DistributedEngine):
+        self.engine = engine
+        self.loglik_calls = 0
+        self.grad_calls = 0
+
+    def loglik(self, theta_vec) -> float:
+        self.loglik_calls += 1
+        try:
+            value = self.engine.loglik(MaternParams.from_array(theta_vec).as_array())
+        except (NotPositiveDefinite, ValueError):
+            return -math.inf
+        return -math.inf if math.isnan(value) else value
+
+    def eval_all(self, theta_vec):
+        self.loglik_calls += 1
+        self.grad_calls += 1
+        return self.engine.eval_all(MaternParams.from_array(theta_vec).as_array())

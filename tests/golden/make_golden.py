@@ -15,6 +15,9 @@ Usage:
     python tests/golden/make_golden.py evals2        # config 2 seed 0 evaluations
     python tests/golden/make_golden.py fit config2 SEED
     python tests/golden/make_golden.py fit config1 0 shift|cube
+    python tests/golden/make_golden.py evals3        # config 3 (n=16,384) evaluations
+    python tests/golden/make_golden.py sub4          # 128x128 corner block of config 4
+    python tests/golden/make_golden.py sub5          # 16,384-point window of config 5
 """
 
 from __future__ import annotations
@@ -155,6 +158,75 @@ def make_evals2():
     (HERE / "config2_evals.json").write_text(json.dumps(evals, indent=1))
 
 
+def make_evals3():
+    """Config 3 (n = 16,384) at theta_true and theta0: one reference log_likelihood and one
+    grad_and_fisher each (~12 min per theta on 8 cores, 21 GB RSS)."""
+    loc, z = _config_data("config3", 0)
+    np.savez_compressed(HERE / "config3_seed0_data.npz", loc=loc, z=z)
+    data = ref.SpatialDataset(loc, z)
+    wl = WORKLOADS["config3"]
+    evals = []
+    for th in (wl.theta_true, wl.theta0):
+        t0 = time.perf_counter()
+        rec = _eval_record(data, th)
+        rec["cpu_wall_s"] = time.perf_counter() - t0
+        evals.append(rec)
+        (HERE / "config3_evals.json").write_text(json.dumps(evals, indent=1))
+
+
+def sub4_locations():
+    """The lower-left 128 x 128 block of config 4's 256 x 256 jittered grid (seed 0): n =
+    16,384 points at config 4's spacing (h = 1/256), so Sigma has config 4's local
+    conditioning at a size the reference still evaluates."""
+    loc = WORKLOADS["config4"].locations(0)
+    ii, jj = np.divmod(np.arange(loc.shape[0]), 256)
+    return loc[(ii < 128) & (jj < 128)]
+
+
+def sub5_locations():
+    """The 16,384 config-5 GMM locations (seed 0) with the smallest x: a spatial window that
+    keeps config 5's local point density (a random subsample would thin it)."""
+    loc = WORKLOADS["config5"].locations(0)
+    return loc[np.sort(np.argsort(loc[:, 0], kind="stable")[:16384])]
+
+
+def make_sub4():
+    loc = sub4_locations()
+    th = WORKLOADS["config4"].theta_true
+    z = ref.simulate_grf(loc, ref.MaternParams(*th), 0)
+    np.savez_compressed(HERE / "sub4_data.npz", loc=loc, z=z)
+    t0 = time.perf_counter()
+    rec = _eval_record(ref.SpatialDataset(loc, z), th)
+    rec["cpu_wall_s"] = time.perf_counter() - t0
+    (HERE / "sub4_evals.json").write_text(json.dumps([rec], indent=1))
+
+
+def make_sub5():
+    """Config 5 has a nugget (tau^2 = 1e-6) that the reference lacks, so the values here come
+    from the oracle's labelled restatement (oracle.eval_all_nugget / loglik with nugget), and,
+    where Sigma without the nugget is still positive definite, from the reference itself."""
+    from oracle import maternmle_cpu as orc
+
+    wl = WORKLOADS["config5"]
+    loc = sub5_locations()
+    th = wl.theta_true
+    low = orc.cholesky(orc.matrix(loc, th, "sigma", wl.nugget))
+    z = low @ np.random.default_rng(0).standard_normal(loc.shape[0])
+    del low
+    np.savez_compressed(HERE / "sub5_data.npz", loc=loc, z=z)
+    out = {"theta": list(th), "nugget": wl.nugget}
+    t0 = time.perf_counter()
+    out["nugget_loglik"] = orc.loglik(loc, z, th, wl.nugget)
+    ll, g, f = orc.eval_all_nugget(loc, z, th, wl.nugget)
+    out.update(nugget_eval_loglik=ll, nugget_grad=g.tolist(), nugget_fisher=f.tolist(),
+               nugget_cpu_wall_s=time.perf_counter() - t0)
+    (HERE / "sub5_evals.json").write_text(json.dumps(out, indent=1))
+    t0 = time.perf_counter()
+    out["reference_tau0"] = _eval_record(ref.SpatialDataset(loc, z), th)
+    out["reference_tau0"]["cpu_wall_s"] = time.perf_counter() - t0
+    (HERE / "sub5_evals.json").write_text(json.dumps(out, indent=1))
+
+
 # Off-default driver variants on the config-1 data (the reference's own fisher_bt): the
 # Nelder-Mead shift forced by a gradient-call budget of 3 (optimizer.py:367-371,394-412), and
 # the paper's default start cube (cli.py:52-53) whose L9 grid hits extreme theta
@@ -205,6 +277,12 @@ if __name__ == "__main__":
         make_config1()
     elif what == "evals2":
         make_evals2()
+    elif what == "evals3":
+        make_evals3()
+    elif what == "sub4":
+        make_sub4()
+    elif what == "sub5":
+        make_sub5()
     elif what == "fit":
         make_fit(sys.argv[2], int(sys.argv[3]), sys.argv[4] if len(sys.argv) > 4 else None)
     else:

@@ -3,7 +3,14 @@ golden reference outputs and the CPU oracle.  Tolerances (north_star): log-likel
 relative; Fisher 1e-8 relative; score 1e-8 relative to its two component magnitudes
 (SURVEY.md §8(c)).  At finite-difference-regime theta (nu within 1e-6 of an integer) the
 reference's own d/dnu entries carry lag-1e-9 forward-difference noise (~1e-6 per element,
-amplified by cond(Sigma)), so the nu-dependent entries are compared at 1e-3 there."""
+amplified by cond(Sigma)), so the nu-dependent entries are compared at 1e-3 there.
+
+Log-likelihood noise floor of the reference itself: on a few very ill-conditioned small
+goldens (nu = 2.3 on random locations) the reference's own value is not determined to 1e-10 by
+its arithmetic -- replacing scipy's kv by 30-digit K_nu, or running its LAPACK on 1 instead of
+8 threads, moves it by up to 1.5e-10 (tests/golden/make_floor.py -> small_floor.json).  There
+the log-likelihood tolerance is max(1e-10, 3 x that measured floor); everywhere else the floor
+is < 3.3e-11 and the tolerance is the plain 1e-10 (3 x floor < 1e-10)."""
 
 import math
 
@@ -26,12 +33,13 @@ def score_scale(theta, n, grad, fisher):
     return half_tr + half_quad
 
 
-def check_eval(gpu, data, rec, n):
+def check_eval(gpu, data, rec, n, floor=0.0):
     th = rec["theta"]
+    ll_tol = max(LL_TOL, 3.0 * floor)
     ll = gpu.log_likelihood(data, th)
-    assert ll == pytest.approx(rec["loglik"], rel=LL_TOL)
+    assert ll == pytest.approx(rec["loglik"], rel=ll_tol)
     ev = gpu.grad_and_fisher(data, th)
-    assert ev.loglik == pytest.approx(rec["eval_loglik"], rel=LL_TOL)
+    assert ev.loglik == pytest.approx(rec["eval_loglik"], rel=ll_tol)
     np.testing.assert_array_equal(ev.fisher, ev.fisher.T)
     ref_g, ref_f = np.array(rec["grad"]), np.array(rec["fisher"])
     scale = score_scale(th, n, ev.grad, ev.fisher)
@@ -73,15 +81,18 @@ def test_matrices_vs_golden(gpu, golden_small):
 
 def test_small_evaluations_vs_golden(gpu, golden_small):
     arrays, ev = golden_small
+    floors = load_json("small_floor.json")
     for name, recs in ev["cases"].items():
         loc, z = arrays[f"{name}_loc"], arrays[f"{name}_z"]
         data = gpu.SpatialDataset(loc, z)
-        for rec in recs:
+        for k, rec in enumerate(recs):
             if "not_pd_pivot" in rec:
                 with pytest.raises(gpu.NotPositiveDefinite):
                     gpu.log_likelihood(data, rec["theta"])
                 continue
-            check_eval(gpu, data, rec, loc.shape[0])
+            fl = floors[name][k]
+            assert fl["theta"] == list(rec["theta"])
+            check_eval(gpu, data, rec, loc.shape[0], floor=fl["floor"])
 
 
 def test_config1_evaluations_vs_golden(gpu):

@@ -44,7 +44,10 @@ def test_ozaki_vs_dmma_engine(gpu):
     th = np.array([1.0, 0.2, 1.5])
     oz = _engine(gpu, loc, z, "ozaki").eval_all(th)
     dm = _engine(gpu, loc, z, "dmma").eval_all(th)
-    assert abs(oz[0] - dm[0]) <= 1e-12 * abs(dm[0])
+    # cond(Sigma) ~ 2e8 here: every engine variant (tables on/off x Ozaki/DMMA) lands within
+    # 0.6-3.6e-12 of the reference's own value (tools/ill_probe2.py), so the two GEMM paths
+    # agree to that noise, two orders inside the 1e-10 north-star tolerance
+    assert abs(oz[0] - dm[0]) <= 5e-12 * abs(dm[0])
     # the score is a difference of two O(n) terms: compare on their magnitude, as the
     # golden parity tests do, two orders inside the 1e-8 north-star tolerance
     scale = score_scale(th, len(z), dm[1], dm[2])

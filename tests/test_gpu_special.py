@@ -114,3 +114,47 @@ def test_matern_derivatives_vs_oracle(gpu):
             # x=8.4), i.e. ~2e-9 of max|dC/dnu|; two roundings of that formula differ by as much.
             tol = 1e-12 if kind != "nu" else 1e-8
             assert np.max(np.abs(got - ref)) <= tol * scale, (th, kind)
+
+
+def test_case_series_vs_oracle(gpu):
+    """case2/3/4_series on their own domains vs the oracle's restatement of bessel.py:184-318."""
+    from oracle import maternmle_cpu as O
+
+    x2 = np.geomspace(1e-3, 8.49, 60)
+    x3 = np.linspace(8.5, 29.99, 60)
+    x4 = np.geomspace(30.0, 300.0, 40)
+    for nu in (0.3, 0.77, 1.5, 2.2):
+        got = gpu.case2_series(nu, x2)
+        ref = O.small_series(nu, x2)
+        assert np.max(np.abs(got - ref) / (1 + np.abs(ref))) <= 1e-12
+        np.testing.assert_allclose(gpu.case3_series(nu, x3), O.mid_series(nu, x3),
+                                   rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(gpu.case4_series(nu, x4), O.large_series(nu, x4),
+                                   rtol=1e-12, atol=1e-300)
+    assert isinstance(gpu.case4_series(1.5, 40.0), float)
+    # half-integer nu: the a_k product vanishes and the series stops early (bessel.py:311-313)
+    np.testing.assert_allclose(gpu.case4_series(0.5, x4), O.large_series(0.5, x4), rtol=1e-13)
+
+
+def test_mid_range_small_order_warning(gpu):
+    with pytest.warns(gpu.MidRangeSmallOrderWarning):
+        gpu.case3_series(0.03, np.array([9.0, 12.0]))
+    with pytest.warns(gpu.MidRangeSmallOrderWarning):
+        gpu.dnu_xnu_knu(0.03, np.array([1.0, 9.0]))
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        gpu.dnu_xnu_knu(0.03, np.array([1.0, 40.0]))  # no mid-range element: no warning
+        gpu.case3_series(0.06, 9.0)
+
+
+def test_simulate_grf_alias(gpu):
+    """simulate_grf (simulate.py:100-106) draws z = L u with the reference's seeded normals."""
+    from oracle import maternmle_cpu as O
+
+    loc = gpu.jittered_grid(12, 3)
+    th = gpu.MaternParams(1.2, 0.15, 0.9)
+    z = gpu.simulate_grf(loc, th, 5)
+    ref = O.cholesky(O.matrix(loc, th.as_array())) @ np.random.default_rng(5).standard_normal(144)
+    np.testing.assert_allclose(z, ref, rtol=1e-11, atol=1e-12)

@@ -1,6 +1,7 @@
-"""Multi-rank host logic of bench.py on CPU (gloo, world_size 2): disjoint replica
-sharding (weak scaling, no data-path collective) and the max-over-ranks / sum-over-ranks
-reductions that produce the whole-job value."""
+"""Multi-rank host logic on CPU (gloo, world_size 2): bench.py's sharded arm (every rank
+running the same Fisher-BT loop over the DistributedEngine, stepped per Fisher iteration, and
+the max-over-ranks reduction of the timing), and the DistributedEngine driver itself with a
+host restatement of the block steps."""
 
 import os
 import socket
@@ -19,49 +20,102 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out):
+def _bench_worker(rank, world, port, out):
+    """One rank of bench.py's sharded arm (N > 1) on CPU: every rank runs the same host
+    Fisher-BT loop, stepped one Fisher iteration at a time (bench.FitStepper), over a
+    DistributedObjective whose engine is the host restatement of the block steps; then the
+    max-over-ranks time / sum reductions the whole-job value uses."""
+    import sys
+
+    import numpy as np
+
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
     import bench
+    from dist_host_backend import HostPanels
+    from oracle import maternmle_cpu as O
+    import paper_2601_11437_b200 as m
+    from paper_2601_11437_b200.distributed import (DistributedEngine, DistributedObjective,
+                                                   TorchComm)
 
-    seeds = bench.replica_seeds(rank)
+    rng = np.random.default_rng(5)
+    n = 700  # N = 1024: 2 outer blocks, one per rank
+    loc = m.jittered_grid(27, 1)[:n]
+    z = O.cholesky(O.matrix(loc, (1.0, 0.15, 0.9))) @ rng.standard_normal(n)
+    eng = DistributedEngine(loc, z, TorchComm(), backend=HostPanels)
+    th0 = m.MaternParams(0.8, 0.1, 0.7)
+    cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    stepper = bench.FitStepper(lambda: DistributedObjective(eng), cfg)
+    thetas = []
+    while not stepper.done:
+        stepper.step()
+        thetas.append(stepper.obj.grad_calls)
+    res = stepper.done[0]
     gathered = [None] * world
-    dist.all_gather_object(gathered, seeds)
+    dist.all_gather_object(gathered, (res.theta_hat.as_array().tolist(), res.grad_calls,
+                                      res.loglik_calls, res.termination.value))
     t = torch.tensor([10.0 + rank, 20.0 * (rank + 1)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    c = torch.tensor([11.0 + rank], dtype=torch.float64)
-    dist.all_reduce(c, op=dist.ReduceOp.SUM)
     if rank == 0:
-        out.put((gathered, t.tolist(), c.tolist()))
+        out.put((gathered, t.tolist(), (loc, z, th0.as_array().tolist())))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_replica_sharding_and_reductions():
+def test_bench_sharded_fit_two_ranks():
+    import numpy as np
+
+    import paper_2601_11437_b200 as m
+    from oracle import maternmle_cpu as O
+
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    gathered, tmax, csum = q.get(timeout=120)
+    gathered, tmax, (loc, z, th0) = q.get(timeout=600)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert gathered[0] == [0, 1, 2, 3, 4]
-    assert gathered[1] == [5, 6, 7, 8, 9]
-    assert not set(gathered[0]) & set(gathered[1])
+    assert gathered[0] == gathered[1]  # identical deterministic loop on every rank
     assert tmax == [11.0, 40.0]
-    assert csum == [23.0]
+    # the same fit on the CPU oracle objective: same counts and termination, same theta-hat
+    cfg = m.FisherBTConfig(theta_lower=m.MaternParams(*th0), theta_upper=m.MaternParams(*th0))
+    ref = m.fisher_bt(None, cfg, objective=O.CountingObjective(loc, z))
+    th, g, ll, term = gathered[0]
+    assert (g, ll, term) == (ref.grad_calls, ref.loglik_calls, ref.termination.value)
+    np.testing.assert_allclose(th, ref.theta_hat.as_array(), rtol=1e-9)
 
 
-@pytest.mark.parametrize("rank", [0, 1, 3, 7])
-def test_replica_seed_blocks(rank):
+def test_fit_stepper_matches_full_fit():
+    """bench.FitStepper: one step = exactly one eval_all; stepping reproduces fisher_bt."""
     import bench
+    import numpy as np
 
-    s = bench.replica_seeds(rank)
-    assert s == list(range(5 * rank, 5 * rank + 5))
+    import paper_2601_11437_b200 as m
+    from oracle import maternmle_cpu as O
+
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "config1_seed0_data.npz"))
+    loc, z = d["loc"], d["z"]
+    th0 = m.MaternParams(0.5, 0.05, 1.0)
+    cfg = m.FisherBTConfig(theta_lower=th0, theta_upper=th0)
+    full = m.fisher_bt(None, cfg, objective=O.CountingObjective(loc, z))
+    st = bench.FitStepper(lambda: O.CountingObjective(loc, z), cfg)
+    steps = 0
+    while not st.done:
+        before = st.obj.grad_calls
+        st.step()
+        steps += 1
+        assert st.done or st.obj.grad_calls == before + 1
+    r = st.done[0]
+    assert steps == full.grad_calls
+    assert (r.grad_calls, r.loglik_calls) == (full.grad_calls, full.loglik_calls)
+    np.testing.assert_array_equal(r.theta_hat.as_array(), full.theta_hat.as_array())
 
 
 def _dist_worker(rank, world, port, out):
