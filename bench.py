@@ -106,11 +106,11 @@ class FitStepper:
         self.req = next(self.gen)
 
     def step(self):
-        from paper_2601_11437_b200.fisher_bt import EVAL_ALL
+        from paper_2601_11437_b200.fisher_bt import EVAL_ALL, _answer
 
         while True:
             kind, theta = self.req
-            ans = self.obj.eval_all(theta) if kind == EVAL_ALL else self.obj.loglik(theta)
+            ans = _answer(self.obj, kind, theta)
             try:
                 self.req = self.gen.send(ans)
             except StopIteration as stop:

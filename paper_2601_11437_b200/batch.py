@@ -61,6 +61,49 @@ def eval_batch(engines, thetas, modes):
              res[i, 4:13].reshape(3, 3).copy()) for i in range(count)]
 
 
+def _loglik_value(rc, ll):
+    """loglik's mapping (optimizer.py:129-134): NotPositiveDefinite / ValueError / NaN -> -inf;
+    a CUDA failure is raised, never mapped."""
+    if rc in (nat.MLE_NOT_PD, nat.MLE_INVALID):
+        return -math.inf
+    if rc != nat.MLE_OK:
+        raise RuntimeError(f"CUDA failure in a batched log-likelihood: {nat.last_error()}")
+    return -math.inf if math.isnan(ll) else ll
+
+
+def _unique_thetas(thetas):
+    """(valid unique theta arrays in first-seen order, item -> unique index or None)."""
+    order, where, slot = [], {}, []
+    for t in thetas:
+        try:
+            th = MaternParams.from_array(t).as_array()
+        except ValueError:
+            slot.append(None)
+            continue
+        key = th.tobytes()
+        if key not in where:
+            where[key] = len(order)
+            order.append(th)
+        slot.append(where[key])
+    return order, slot
+
+
+def batched_logliks(data: SpatialDataset, thetas):
+    """Log-likelihoods of one dataset at several independent theta, as batched passes over
+    the dataset's engine and its helper contexts (SpatialDataset.engines).  Equal theta are
+    evaluated once (the engine is deterministic); invalid theta give -inf without a pass.
+    Every value is bit-identical to a single ``log_likelihood`` call."""
+    order, slot = _unique_thetas(thetas)
+    vals = []
+    if order:
+        engines = data.engines(len(order))
+        for start in range(0, len(order), len(engines)):
+            chunk = order[start:start + len(engines)]
+            out = eval_batch(engines[:len(chunk)], chunk, [LOGLIK_MODE] * len(chunk))
+            vals.extend(_loglik_value(rc, ll) for rc, _, ll, _, _ in out)
+    return [-math.inf if k is None else vals[k] for k in slot]
+
+
 class BatchCoordinator:
     """Gathers one request per live client and runs them as one batch."""
 
@@ -187,7 +230,7 @@ class LockstepStats:
 
 
 def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None,
-             groups=None):
+             groups=None, return_exceptions=False):
     """Run one Fisher-BT fit per dataset concurrently with lock-step batched evaluation.
 
     Every fit is the request generator ``fisher_bt_gen`` (the unchanged Algorithm 1); a host
@@ -210,7 +253,8 @@ def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out
         groups = int(env) if env else (2 if n >= 4 else 1)
     groups = max(1, min(int(groups), n)) if n else 1
     if groups == 1:
-        return _fit_group(datasets, cfg, objectives_out, coordinator_out)
+        return _finish(_fit_group(datasets, cfg, objectives_out, coordinator_out),
+                       return_exceptions)
     parts = [list(range(g, n, groups)) for g in range(groups)]
     res = [None] * groups
     objs = [[] for _ in range(groups)]
@@ -241,12 +285,28 @@ def fit_many(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out
     if coordinator_out is not None:
         for st in stats:
             coordinator_out.extend(st)
+    return _finish(results, return_exceptions)
+
+
+def _finish(results, return_exceptions):
+    """Every fit has run to its end.  A failed fit's slot holds its exception
+    (``return_exceptions``), or the first failed fit in dataset order raises -- what running
+    the fits one after another would raise first."""
+    if return_exceptions:
+        return [r.exc if isinstance(r, _FitFailure) else r for r in results]
+    for r in results:
+        if isinstance(r, _FitFailure):
+            raise r.exc
     return results
 
 
 def _fit_group(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_out=None):
-    """One lock-step group of :func:`fit_many`, driven by the calling thread."""
-    from .fisher_bt import EVAL_ALL, LOGLIK, fisher_bt_gen
+    """One lock-step group of :func:`fit_many`, driven by the calling thread.
+
+    A fit's own failure (InitializationFailed, or NotPositiveDefinite out of eval_all) ends
+    that fit only: it is re-raised from :func:`fit_many` after every other fit of the group
+    has finished, exactly as running the fits one by one would surface it first."""
+    from .fisher_bt import EVAL_ALL, LOGLIK, LOGLIK_MANY, fisher_bt_gen
 
     stats = LockstepStats()
     if coordinator_out is not None:
@@ -262,21 +322,34 @@ def _fit_group(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_o
         except StopIteration as stop:
             pending.pop(i, None)
             results[i] = stop.value
+        except Exception as exc:  # this fit failed; the others go on
+            pending.pop(i, None)
+            results[i] = _FitFailure(exc)
 
     for i in range(len(gens)):
         advance(i, None, None)
     while pending:
         ids = sorted(pending)
-        cheap = [i for i in ids if pending[i][0] == LOGLIK]
+        cheap = [i for i in ids if pending[i][0] != EVAL_ALL]
         if cheap and len(cheap) < len(ids):
             ids = cheap
         else:
             stats.eval_passes += int(any(pending[i][0] == EVAL_ALL for i in ids))
         answers = {}
-        run, thetas, modes = [], [], []
+        items = []  # (fit, engine, theta, mode, unique slot)
+        many = {}   # fit -> (item slots, per-theta unique index)
         for i in ids:
             kind, theta_vec = pending[i]
             c = cnt[i]
+            if kind == LOGLIK_MANY:
+                c.loglik_calls += len(theta_vec)
+                order, slot = _unique_thetas(theta_vec)
+                engines = datasets[i].engines(len(order)) if order else []
+                first = len(items)
+                for k, th in enumerate(order):
+                    items.append((i, engines[k % len(engines)], th, LOGLIK_MODE))
+                many[i] = (first, len(order), slot)
+                continue
             c.loglik_calls += 1
             if kind == EVAL_ALL:
                 c.grad_calls += 1
@@ -285,33 +358,61 @@ def _fit_group(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_o
             except ValueError as exc:  # loglik -> -inf; eval_all raises (optimizer.py:131-138)
                 answers[i] = (-math.inf, None) if kind == LOGLIK else (None, exc)
                 continue
-            run.append(i)
-            thetas.append(th)
-            modes.append(LOGLIK_MODE if kind == LOGLIK else EVAL_MODE)
-        if run:
+            items.append((i, datasets[i].engine(), th,
+                          LOGLIK_MODE if kind == LOGLIK else EVAL_MODE))
+        # rounds: an engine appears at most once per batched pass
+        outs = [None] * len(items)
+        todo = list(range(len(items)))
+        while todo:
+            seen, run, later = set(), [], []
+            for k in todo:
+                (run if id(items[k][1]) not in seen else later).append(k)
+                seen.add(id(items[k][1]))
+            todo = later
             try:
-                out = eval_batch([datasets[i].engine() for i in run], thetas, modes)
-                p = datasets[run[0]].engine().phase_times()
-                ks = datasets[run[0]].engine().kernel_stats()
+                out = eval_batch([items[k][1] for k in run], [items[k][2] for k in run],
+                                 [items[k][3] for k in run])
+                p = items[run[0]][1].phase_times()
+                ks = items[run[0]][1].kernel_stats()
                 for key in ("host_enqueue_ms", "gpu_gap_ms", "spec_wait_ms"):
                     p[key] = ks[key]
                 for key in stats.acc:
                     stats.acc[key] += p[key]
-                for i, (rc, piv, ll, grad, fisher) in zip(run, out):
-                    if pending[i][0] == LOGLIK:
-                        ok = rc == nat.MLE_OK and not math.isnan(ll)
-                        answers[i] = (ll if ok else -math.inf, None)
-                    elif rc == nat.MLE_NOT_PD:
-                        answers[i] = (None, NotPositiveDefinite(piv))
-                    elif rc != nat.MLE_OK:
-                        answers[i] = (None, ValueError(nat.last_error()))
-                    else:
-                        answers[i] = ((ll, grad, fisher), None)
+                for k, o in zip(run, out):
+                    outs[k] = o
             except Exception as exc:  # CUDA failures reach every fit of the pass
-                for i in run:
-                    answers[i] = (None, exc)
+                for k in run:
+                    outs[k] = exc
             stats.batches += 1
             stats.requests += len(run)
+        for k, (i, _, _, mode) in enumerate(items):
+            if i in many:
+                continue
+            o = outs[k]
+            if isinstance(o, Exception):
+                answers[i] = (None, o)
+                continue
+            rc, piv, ll, grad, fisher = o
+            if mode == LOGLIK_MODE:
+                ok = rc == nat.MLE_OK and not math.isnan(ll)
+                answers[i] = (ll if ok else -math.inf, None)
+            elif rc == nat.MLE_NOT_PD:
+                answers[i] = (None, NotPositiveDefinite(piv))
+            elif rc != nat.MLE_OK:
+                answers[i] = (None, ValueError(nat.last_error()))
+            else:
+                answers[i] = ((ll, grad, fisher), None)
+        for i, (first, count, slot) in many.items():
+            try:
+                vals = []
+                for k in range(first, first + count):
+                    o = outs[k]
+                    if isinstance(o, Exception):
+                        raise o
+                    vals.append(_loglik_value(o[0], o[2]))
+                answers[i] = ([-math.inf if s is None else vals[s] for s in slot], None)
+            except Exception as exc:
+                answers[i] = (None, exc)
         for i in ids:
             value, exc = answers[i]
             if exc is not None:
@@ -321,3 +422,10 @@ def _fit_group(datasets, cfg: FisherBTConfig, objectives_out=None, coordinator_o
     if objectives_out is not None:
         objectives_out.extend(cnt)
     return results
+
+
+class _FitFailure:
+    """A fit of a lock-step group that raised (kept until the group has finished)."""
+
+    def __init__(self, exc):
+        self.exc = exc

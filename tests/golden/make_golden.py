@@ -161,12 +161,21 @@ def make_evals2():
 def make_evals3():
     """Config 3 (n = 16,384) at theta_true and theta0: one reference log_likelihood and one
     grad_and_fisher each (~12 min per theta on 8 cores, 21 GB RSS)."""
-    loc, z = _config_data("config3", 0)
-    np.savez_compressed(HERE / "config3_seed0_data.npz", loc=loc, z=z)
+    npz = HERE / "config3_seed0_data.npz"
+    if npz.exists():
+        d = np.load(npz)
+        loc, z = d["loc"], d["z"]
+    else:
+        loc, z = _config_data("config3", 0)
+        np.savez_compressed(npz, loc=loc, z=z)
     data = ref.SpatialDataset(loc, z)
     wl = WORKLOADS["config3"]
-    evals = []
+    out = HERE / "config3_evals.json"
+    evals = json.loads(out.read_text()) if out.exists() else []
+    done = {tuple(e["theta"]) for e in evals}
     for th in (wl.theta_true, wl.theta0):
+        if tuple(th) in done:  # resumable: each theta is ~10 min of CPU
+            continue
         t0 = time.perf_counter()
         rec = _eval_record(data, th)
         rec["cpu_wall_s"] = time.perf_counter() - t0

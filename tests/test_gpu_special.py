@@ -126,7 +126,10 @@ def test_case_series_vs_oracle(gpu):
     for nu in (0.3, 0.77, 1.5, 2.2):
         got = gpu.case2_series(nu, x2)
         ref = O.small_series(nu, x2)
-        assert np.max(np.abs(got - ref) / (1 + np.abs(ref))) <= 1e-12
+        # the 21-term series cancels: its terms grow like I_0(x) (~700 at x = 8.49) while the
+        # sum stays O(1), so two correct summation orders differ by ~1e-16 x I_0(x)
+        # (bessel.py:213-222; measured 4.4e-12 of 1 + |ref| at x = 8.49)
+        assert np.all(np.abs(got - ref) <= 1e-13 * (1 + np.abs(ref) + np.i0(x2))), nu
         np.testing.assert_allclose(gpu.case3_series(nu, x3), O.mid_series(nu, x3),
                                    rtol=1e-12, atol=1e-300)
         np.testing.assert_allclose(gpu.case4_series(nu, x4), O.large_series(nu, x4),
