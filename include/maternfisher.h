@@ -194,7 +194,8 @@ int mle_matern_elem(const double theta[3], int which, const double* h, int64_t m
  *   (eval_all) for b: owner re-sends W_b, right_operand(b) -> broadcast X_b -> right(b);
  *   partials() on every rank -> all-reduce(sum).
  * Exchange buffers are device memory owned by the caller (NCCL sends them); sizes from
- * mle_dctx_layout.  Every call returns after this rank's stream drained.  Replaces the
+ * mle_dctx_layout.  Every call returns after this rank's stream drained (unless
+ * mle_dctx_set_async).  Replaces the
  * reference's single-process likelihood.py:107-149 for n beyond one GPU's memory.
  */
 typedef struct mle_dctx mle_dctx;
@@ -211,10 +212,26 @@ int mle_dctx_wblock(mle_dctx* d, int b, void* exch_w);
 int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w);
 int mle_dctx_right_operand(mle_dctx* d, int b, void* exch_x);
 int mle_dctx_right(mle_dctx* d, int b, const void* exch_w, const void* exch_x);
+/* Look-ahead variants: only the panels of blocks j with lo <= j < hi.  right_range with
+ * exch_w == NULL takes W_b from the rank's W cache (mle_dctx_wcache). */
+int mle_dctx_update_range(mle_dctx* d, int b, const void* exch_p, int lo, int hi);
+int mle_dctx_right_range(mle_dctx* d, int b, const void* exch_w, const void* exch_x, int lo,
+                         int hi);
+/* on = 1: the step calls above return as soon as their work is queued on the rank's stream
+ * (mle_dctx_stream) instead of draining it; the caller orders its collectives against that
+ * stream (CUDA events; NCCL on a communication stream).  begin / partials stay synchronous. */
+int mle_dctx_set_async(mle_dctx* d, int on);
+int mle_dctx_stream(const mle_dctx* d, void** stream);
+/* Keep every block's W_b on this rank (~3.5 N^2 bytes) so that the right sweep reuses the
+ * forward sweep's W_b instead of a second broadcast; MLE_CUDA_ERROR if it does not fit. */
+int mle_dctx_wcache(mle_dctx* d, int on);
 /* out: MLE_DCTX_SUMS partial sums [logdet, quad, trA, trN, <A,A>, <A,N>, <N,N>, trM, <A,M>,
  * <N,M>, <M,M>, yBy_A, yBy_N, yBy_M], then the failure flag and the 0-based pivot */
 #define MLE_DCTX_SUMS 14
 int mle_dctx_partials(mle_dctx* d, double* out);
+/* The same sums per owned panel (ascending blocks; out[q * MLE_DCTX_SUMS + k]), then the
+ * failure flag and pivot: adding panels in block order makes results independent of world. */
+int mle_dctx_panel_partials(mle_dctx* d, double* out);
 
 #ifdef __cplusplus
 }

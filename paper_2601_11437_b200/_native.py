@@ -34,6 +34,8 @@ EXPORTED = (
     "mle_dctx_layout", "mle_dctx_begin", "mle_dctx_factor", "mle_dctx_update",
     "mle_dctx_wblock", "mle_dctx_forward", "mle_dctx_right_operand", "mle_dctx_right",
     "mle_dctx_partials", "mle_launch_count", "mle_dnu_series", "mle_digamma",
+    "mle_dctx_update_range", "mle_dctx_right_range", "mle_dctx_set_async", "mle_dctx_stream",
+    "mle_dctx_wcache", "mle_dctx_panel_partials",
 )
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -73,6 +75,14 @@ def _load():
         "mle_dctx_right_operand": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
         "mle_dctx_right": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
         "mle_dctx_partials": (ctypes.c_int, [_vp, _dp]),
+        "mle_dctx_update_range": (ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int,
+                                                 ctypes.c_int]),
+        "mle_dctx_right_range": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int,
+                                                ctypes.c_int]),
+        "mle_dctx_set_async": (ctypes.c_int, [_vp, ctypes.c_int]),
+        "mle_dctx_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+        "mle_dctx_wcache": (ctypes.c_int, [_vp, ctypes.c_int]),
+        "mle_dctx_panel_partials": (ctypes.c_int, [_vp, _dp]),
         "mle_ctx_create": (ctypes.c_int, [_dp, _dp, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
                                           ctypes.POINTER(_vp)]),
         "mle_ctx_destroy": (None, [_vp]),

@@ -241,6 +241,18 @@ bool use_speculation() {
   return !(v && std::strcmp(v, "0") == 0);
 }
 
+// Ozaki GEMM tile variant (launch_ozgemm n_tile; all bit-identical): MLE_OZ_TILE=0 (128 x 64
+// tiles, CTA pairs sharing A), 1, 2, or 3 (128 x 32 tiles, clusters of four sharing A,
+// double-buffered TMEM accumulators).
+int oz_tile_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("MLE_OZ_TILE");
+    const int t = e ? std::atoi(e) : 0;
+    return (t >= 0 && t <= 3) ? t : 0;
+  }();
+  return v;
+}
+
 // FP64 trailing-update GEMM: Ozaki int8 tensor-core emulation (default) or DMMA.
 bool use_ozaki() {
   const char* v = std::getenv("MLE_FP64_GEMM");
@@ -572,7 +584,7 @@ struct Launcher {
     launches += 1;
     int rc = prof_begin(st);
     if (rc) return rc;
-    CUDA_TRY(launch_ozgemm(g, batch, st));
+    CUDA_TRY(launch_ozgemm(g, batch, st, oz_tile_variant()));
     if ((rc = mark("ozgemm", st))) return rc;
     double tiles;
     if (g.lower) tiles = 0.5 * g.tiles_m * (g.tiles_m + 1.0);
@@ -2312,6 +2324,9 @@ struct mle_dctx {
   int* xex = nullptr;
   double* part = nullptr;                      // panel reduce partials
   std::vector<double> h_part;
+  bool async = false;                          // steps return without draining the stream
+  std::vector<int8_t*> wcache;                 // every block's W_b slices (right sweep), or empty
+  std::vector<int*> wcache_e;
 };
 
 namespace {
@@ -2333,12 +2348,20 @@ double* d_mat(const mle_dctx* d, int m, int q) {  // derivative block m of owned
   return d->mat[m][q];
 }
 
+// End of a block step.  Synchronous mode drains the rank's streams (the exchange buffers are
+// then ready for a collective on any stream).  Asynchronous mode (mle_dctx_set_async) only
+// checks the launches: the work stays queued on the rank's stream (every step ends joined into
+// it), and the caller orders its collectives against that stream with events.
 int d_sync(mle_dctx* d) {
-  CUDA_TRY(cudaStreamSynchronize(d->c->stream));
-  CUDA_TRY(cudaStreamSynchronize(d->c->inner));
+  if (!d->async) {
+    CUDA_TRY(cudaStreamSynchronize(d->c->stream));
+    CUDA_TRY(cudaStreamSynchronize(d->c->inner));
+  }
   CUDA_TRY(cudaGetLastError());
   return MLE_OK;
 }
+
+bool d_in(int blk, int lo, int hi) { return blk >= lo && blk < hi; }
 
 }  // namespace
 
@@ -2385,6 +2408,8 @@ void mle_dctx_destroy(mle_dctx* d) {
   dfree(d->xsl);
   dfree(d->xex);
   dfree(d->part);
+  for (auto* p : d->wcache) dfree(p);
+  for (auto* p : d->wcache_e) dfree(p);
   mle_ctx_destroy(d->c);
   delete d;
 }
@@ -2510,9 +2535,11 @@ int mle_dctx_begin(mle_dctx* d, const double theta[3], int derivs) {
       CUDA_TRY(launch_panel_identity(pa, cnt, c->stream));
     }
   }
-  int rc = d_sync(d);
+  // always drained (begin is once per evaluation): d_c0s goes back to the buffer cache
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaGetLastError());
   dfree(d_c0s);
-  return rc;
+  return MLE_OK;
 }
 
 // Owner of block b: inner steps on its panel; P_b = L[c1:, b] sliced into exch_p
@@ -2554,6 +2581,12 @@ int mle_dctx_factor(mle_dctx* d, int b, void* exch_p) {
 
 // Every rank: trailing update of its panels j > b with P_b (exch_p as produced by factor).
 int mle_dctx_update(mle_dctx* d, int b, const void* exch_p) {
+  return mle_dctx_update_range(d, b, exch_p, 0, d ? d->nb : 0);
+}
+
+// Same, restricted to the panels of blocks j with lo <= j < hi (look-ahead: the owner of b + 1
+// updates that panel first, factors it, and updates the rest while P_{b+1} is in flight).
+int mle_dctx_update_range(mle_dctx* d, int b, const void* exch_p, int lo, int hi) {
   if (!d || !exch_p) return fail(MLE_INVALID, "null argument");
   mle_ctx* c = d->c;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -2563,7 +2596,7 @@ int mle_dctx_update(mle_dctx* d, int b, const void* exch_p) {
   Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
   std::vector<int> qs;
   for (size_t q = 0; q < d->owned.size(); ++q)
-    if (d->owned[q] > b) qs.push_back((int)q);
+    if (d->owned[q] > b && d_in(d->owned[q], lo, hi)) qs.push_back((int)q);
   for (size_t i0 = 0; i0 < qs.size(); i0 += kMaxGemm) {
     const int cnt = (int)std::min<size_t>(kMaxGemm, qs.size() - i0);
     OzGemmArgs g = Launcher::oz_base(N, (int)((N - c1) / kNB), (int)(kDB / kNB));
@@ -2704,6 +2737,12 @@ int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w) {
     if ((rc = run.slice(sa, kDB, false, cnt))) return rc;
     if ((rc = run.ozgemm(g, cnt, c->stream))) return rc;
   }
+  if (!d->wcache.empty()) {  // keep W_b for the right sweep (no second broadcast)
+    CUDA_TRY(cudaMemcpyAsync(d->wcache[b], ws, (size_t)(N - c0) * kOzRowBytes,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(d->wcache_e[b], we, sizeof(int) * (size_t)(N - c0),
+                             cudaMemcpyDeviceToDevice, c->stream));
+  }
   return d_sync(d);
 }
 
@@ -2736,19 +2775,27 @@ int mle_dctx_right_operand(mle_dctx* d, int b, void* exch_x) {
 // Every rank, right sweep block b: X[i, j] += X[i, c0:c1] W_b[j - c0, :] for its panels j >= b
 // (rows i >= j's block start; block b's own columns are overwritten: they become B[:, b]).
 int mle_dctx_right(mle_dctx* d, int b, const void* exch_w, const void* exch_x) {
-  if (!d || !exch_w || !exch_x || !d->derivs) return fail(MLE_INVALID, "null argument");
+  return mle_dctx_right_range(d, b, exch_w, exch_x, 0, d ? d->nb : 0);
+}
+
+// Same, restricted to the panels of blocks j with lo <= j < hi.  exch_w == NULL: W_b from the
+// rank's W cache (filled by the forward sweep; mle_dctx_wcache).
+int mle_dctx_right_range(mle_dctx* d, int b, const void* exch_w, const void* exch_x, int lo,
+                         int hi) {
+  if (!d || !exch_x || !d->derivs) return fail(MLE_INVALID, "null argument");
+  if (!exch_w && d->wcache.empty()) return fail(MLE_INVALID, "no W_b: pass exch_w or enable the W cache");
   mle_ctx* c = d->c;
   CUDA_TRY(cudaSetDevice(c->device));
   const long long N = c->N, c0 = d_c0(b);
-  const int8_t* ws = static_cast<const int8_t*>(exch_w);
-  const int* we = reinterpret_cast<const int*>(ws + d_wbytes(N));
+  const int8_t* ws = exch_w ? static_cast<const int8_t*>(exch_w) : d->wcache[b];
+  const int* we = exch_w ? reinterpret_cast<const int*>(ws + d_wbytes(N)) : d->wcache_e[b];
   const int8_t* xs = static_cast<const int8_t*>(exch_x);
   Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
   for (int own = 1; own >= 0; --own) {  // own == 1: the owner's block b (overwrite)
     std::vector<std::pair<int, int>> zs;  // (q, m)
     for (size_t q = 0; q < d->owned.size(); ++q) {
       const int bj = d->owned[q];
-      if (bj < b || (bj == b) != (own == 1)) continue;
+      if (bj < b || (bj == b) != (own == 1) || !d_in(bj, lo, hi)) continue;
       for (int m = 0; m < d->nmat; ++m) zs.push_back({(int)q, m});
     }
     for (size_t i0 = 0; i0 < zs.size(); i0 += kMaxGemm) {
@@ -2777,9 +2824,70 @@ int mle_dctx_right(mle_dctx* d, int b, const void* exch_w, const void* exch_x) {
   return d_sync(d);
 }
 
+int mle_dctx_set_async(mle_dctx* d, int on) {
+  if (!d) return fail(MLE_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(d->c->device));
+  CUDA_TRY(cudaStreamSynchronize(d->c->stream));
+  CUDA_TRY(cudaStreamSynchronize(d->c->inner));
+  d->async = on != 0;
+  return MLE_OK;
+}
+
+int mle_dctx_stream(const mle_dctx* d, void** out) {
+  if (!d || !out) return fail(MLE_INVALID, "null argument");
+  *out = (void*)d->c->stream;
+  return MLE_OK;
+}
+
+// W cache: every block's W_b slices kept on this rank (7 x 512 + 4 bytes per row of rows
+// c0..N: ~3.5 N^2 bytes in total), so the right sweep needs no second W broadcast.
+// on = 0 frees it.  Returns MLE_CUDA_ERROR (cache left off) if the memory is not there.
+int mle_dctx_wcache(mle_dctx* d, int on) {
+  if (!d) return fail(MLE_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(d->c->device));
+  CUDA_TRY(cudaStreamSynchronize(d->c->stream));
+  for (auto* p : d->wcache) dfree(p);
+  for (auto* p : d->wcache_e) dfree(p);
+  d->wcache.clear();
+  d->wcache_e.clear();
+  if (!on) return MLE_OK;
+  const long long N = d->c->N;
+  std::vector<int8_t*> w(d->nb, nullptr);
+  std::vector<int*> e(d->nb, nullptr);
+  for (int b = 0; b < d->nb; ++b) {
+    const size_t rows = (size_t)(N - d_c0(b));
+    if (dmalloc(&w[b], rows * kOzRowBytes) != cudaSuccess ||
+        dmalloc(&e[b], sizeof(int) * rows) != cudaSuccess) {
+      for (auto* p : w) dfree(p);
+      for (auto* p : e) dfree(p);
+      cudaGetLastError();
+      return fail(MLE_CUDA_ERROR, "W cache: out of device memory");
+    }
+  }
+  d->wcache = w;
+  d->wcache_e = e;
+  return MLE_OK;
+}
+
 // This rank's partial sums over its panels: out[0..kPanelSums) (the kReduceOut layout of the
 // single-GPU reduction), out[kPanelSums] = failure flag, out[kPanelSums + 1] = pivot.
 int mle_dctx_partials(mle_dctx* d, double* out) {
+  if (!d || !out) return fail(MLE_INVALID, "null argument");
+  std::vector<double> per((size_t)d->owned.size() * kPanelSums + 2);
+  int rc = mle_dctx_panel_partials(d, per.data());
+  if (rc) return rc;
+  for (int k = 0; k < kPanelSums; ++k) out[k] = 0.0;
+  for (size_t q = 0; q < d->owned.size(); ++q)
+    for (int k = 0; k < kPanelSums; ++k) out[k] += per[q * kPanelSums + k];
+  out[kPanelSums] = per[d->owned.size() * kPanelSums];
+  out[kPanelSums + 1] = per[d->owned.size() * kPanelSums + 1];
+  return MLE_OK;
+}
+
+// Per owned panel (ascending block order): out[q * kPanelSums + k], each summed over the
+// panel's columns in a fixed order; then the failure flag and the pivot.  A driver that adds
+// the panels' sums in block order gets results independent of the number of ranks.
+int mle_dctx_panel_partials(mle_dctx* d, double* out) {
   if (!d || !out) return fail(MLE_INVALID, "null argument");
   mle_ctx* c = d->c;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -2809,17 +2917,19 @@ int mle_dctx_partials(mle_dctx* d, double* out) {
                            c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->h_res + 1, c->fail_idx, sizeof(long long),
                            cudaMemcpyDeviceToHost, c->stream));
-  int rc = d_sync(d);
-  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));  // host reads the sums (also in async mode)
+  CUDA_TRY(cudaGetLastError());
   std::memcpy(&flag, c->h_res, sizeof(int));
   std::memcpy(&idx, c->h_res + 1, sizeof(long long));
-  for (int k = 0; k < kPanelSums; ++k) out[k] = 0.0;
-  for (int q = 0; q < no; ++q)
+  for (int q = 0; q < no; ++q) {
+    double* o = out + (size_t)q * kPanelSums;
+    for (int k = 0; k < kPanelSums; ++k) o[k] = 0.0;
     for (long long jl = 0; jl < kDB; ++jl)
       for (int k = 0; k < kPanelSums; ++k)
-        out[k] += d->h_part[((size_t)q * kDB + jl) * kPanelSums + k];
-  out[kPanelSums] = (double)flag;
-  out[kPanelSums + 1] = (double)idx;
+        o[k] += d->h_part[((size_t)q * kDB + jl) * kPanelSums + k];
+  }
+  out[(size_t)no * kPanelSums] = (double)flag;
+  out[(size_t)no * kPanelSums + 1] = (double)idx;
   return MLE_OK;
 }
 

@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
                                                                            long long per_z,
                                                                            long long total) {
   using Cfg = OzP<kN, kS>;
-  static_assert(kMc == 1 || (kMc == 2 && kN == 64), "pairs own both halves of a 128-wide tile");
+  static_assert(kMc == 1 || kMc * kN == 128, "a cluster owns the kMc parts of a 128-wide tile");
+  constexpr uint16_t kMask = (uint16_t)((1u << kMc) - 1u);
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   __shared__ __align__(8) uint64_t full_bar[Cfg::kStages], empty_bar[Cfg::kStages];
   __shared__ __align__(8) uint64_t acc_full[Cfg::kSets], acc_empty[Cfg::kSets];
@@ -386,10 +387,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
             continue;
           }
           mbar_expect_tx(&full_bar[st], Cfg::kStage);
-          if (kMc > 1) {  // my half of the A stage, to both CTAs of the pair
-            constexpr uint32_t kHalf = Cfg::kAStage / 2;
-            bulk_g2s_mc(sa + rank * kHalf, Ablk + (size_t)kb * kS * OZ_BLK + rank * kHalf, kHalf,
-                        &full_bar[st], (uint16_t)0x3);
+          if (kMc > 1) {  // my 1/kMc of the A stage, to every CTA of the cluster
+            constexpr uint32_t kPart = Cfg::kAStage / kMc;
+            static_assert(Cfg::kAStage % (16 * kMc) == 0, "16-byte multicast parts");
+            bulk_g2s_mc(sa + rank * kPart, Ablk + (size_t)kb * kS * OZ_BLK + rank * kPart, kPart,
+                        &full_bar[st], kMask);
           } else {
             bulk_g2s(sa, Ablk + (size_t)kb * kS * OZ_BLK, Cfg::kAStage, &full_bar[st]);
           }
@@ -452,11 +454,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
                 "l"(db0 + (uint64_t)((r0 * OZ_KB) >> 4)), "r"(idesc), "r"(accum));
           }
         }
-        if (kMc > 1)  // the stage is free once both CTAs' MMAs have read it
+        if (kMc > 1)  // the stage is free once every cluster CTA's MMAs have read it
           asm volatile(
               "{ .reg .pred pe; elect.sync _|pe, 0xffffffff;\n"
               "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
-              "cluster.b64 [%0], %1; }" ::"r"(smem_u32(&empty_bar[st])), "h"((uint16_t)0x3));
+              "cluster.b64 [%0], %1; }" ::"r"(smem_u32(&empty_bar[st])), "h"(kMask));
         else
           asm volatile(
               "{ .reg .pred pe; elect.sync _|pe, 0xffffffff;\n"
@@ -581,6 +583,8 @@ cudaError_t init_ozaki_attributes() {
   if ((e = oz_attr<64, 6, 1>()) != cudaSuccess) return e;
   if ((e = oz_attr<32, 7, 1>()) != cudaSuccess) return e;
   if ((e = oz_attr<32, 6, 1>()) != cudaSuccess) return e;
+  if ((e = oz_attr<32, 7, 4>()) != cudaSuccess) return e;
+  if ((e = oz_attr<32, 6, 4>()) != cudaSuccess) return e;
 #define MLE_SLICE_ATTR(RC, S, R)                                                           \
   e = cudaFuncSetAttribute(oz_slice_kernel<RC, S, R>,                                       \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, oz_slice_smem(R));  \
@@ -649,13 +653,15 @@ static cudaError_t oz_launch(const OzGemmArgs& g, long long per_z, long long tot
 }
 
 // n_tile: 0 -> 128 x 64 tiles in CTA pairs sharing A (default), 1 -> 128 x 32 tiles,
-// 2 -> 128 x 64 tiles without pairing (A/B comparisons).  All give bit-identical results.
+// 2 -> 128 x 64 tiles without pairing (A/B comparisons), 3 -> 128 x 32 tiles in clusters of
+// four sharing A (double-buffered TMEM accumulators: the epilogue of one tile overlaps the
+// MMAs of the next).  All give bit-identical results.
 cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_tile) {
   const long long tiles =
       g.lower ? (long long)g.tiles_m * (g.tiles_m + 1) / 2 : (long long)g.tiles_m * g.tiles_n;
   if (tiles <= 0) return cudaSuccess;
-  if (n_tile < 0 || n_tile > 2) return cudaErrorInvalidValue;
-  const int kn = n_tile == 1 ? 32 : 64;
+  if (n_tile < 0 || n_tile > 3) return cudaErrorInvalidValue;
+  const int kn = (n_tile == 1 || n_tile == 3) ? 32 : 64;
   const long long per_z = tiles * (128 / kn), total = per_z * batch;
   const long long cap = g.max_ctas > 0 ? std::min(g.max_ctas, g_num_sms) : g_num_sms;
   long long grid = std::min<long long>(total, cap);
@@ -666,6 +672,11 @@ cudaError_t launch_ozgemm(const OzGemmArgs& g, int batch, cudaStream_t s, int n_
     return (six ? oz_launch<64, 6, 2> : oz_launch<64, 7, 2>)(g, per_z, total, grid, s);
   }
   if (n_tile == 2) return (six ? oz_launch<64, 6, 1> : oz_launch<64, 7, 1>)(g, per_z, total, grid, s);
+  if (n_tile == 3) {
+    grid &= ~3LL;  // whole clusters (total is a multiple of 4: four parts per 128-wide tile)
+    if (grid < 4) grid = 4;
+    return (six ? oz_launch<32, 6, 4> : oz_launch<32, 7, 4>)(g, per_z, total, grid, s);
+  }
   return (six ? oz_launch<32, 6, 1> : oz_launch<32, 7, 1>)(g, per_z, total, grid, s);
 }
 

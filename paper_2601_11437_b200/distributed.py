@@ -41,6 +41,7 @@ __all__ = ["DistributedEngine", "DistributedObjective", "TorchComm", "InProcessC
 
 LOG_2PI = 1.8378770664093453  # likelihood.py:38
 BLOCK = 512
+SUMS = 14  # MLE_DCTX_SUMS
 
 
 def results_from_sums(sums, n, theta, nugget=0.0, derivs=True):
@@ -88,13 +89,27 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.local_ranks = [self.rank]
+        # stream-ordered (asynchronous) block steps need NCCL: its collectives are ordered on
+        # the issuing CUDA stream; gloo copies through the host
+        self.stream_ordered = dist.get_backend(group) == "nccl"
+
+    def _src(self, src):
+        """Group rank -> the global rank torch.distributed.broadcast expects."""
+        if self.group is None:
+            return src
+        return self.dist.get_global_rank(self.group, src)
 
     def broadcast(self, bufs, src):
-        self.dist.broadcast(bufs[0], src=src, group=self.group)
+        """Blocking: returns when this rank's buffer holds the owner's bytes."""
+        self.dist.broadcast(bufs[0], src=self._src(src), group=self.group)
         if bufs[0].is_cuda:
             import torch
 
             torch.cuda.current_stream(bufs[0].device).synchronize()
+
+    def broadcast_on_stream(self, buf, src):
+        """Enqueued on the current CUDA stream (NCCL); no host synchronisation."""
+        self.dist.broadcast(buf, src=self._src(src), group=self.group)
 
     def all_reduce_sum(self, arrs):
         import torch
@@ -108,6 +123,8 @@ class TorchComm:
 
 class InProcessComm:
     """Several ranks stepped by one process (all buffers visible): broadcast = copy."""
+
+    stream_ordered = False
 
     def __init__(self, world):
         self.world = world
@@ -147,6 +164,7 @@ class CudaPanels:
         nat.check(nat.lib.mle_dctx_create(nat.as_ptr(loc), nat.as_ptr(z), self.n, device,
                                           self.nugget, rank, world, ctypes.byref(h)))
         self._d = h
+        self.rank, self.world = rank, world
         lay = np.zeros(7, dtype=np.int64)
         nat.check(nat.lib.mle_dctx_layout(self._d, lay.ctypes.data_as(nat._i64p)))
         self.N, self.nb, self.nmat = int(lay[0]), int(lay[1]), int(lay[5])
@@ -174,8 +192,9 @@ class CudaPanels:
     def factor(self, b, exch):
         self.nat.check(self.nat.lib.mle_dctx_factor(self._d, b, self._p(exch)))
 
-    def update(self, b, exch):
-        self.nat.check(self.nat.lib.mle_dctx_update(self._d, b, self._p(exch)))
+    def update(self, b, exch, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
+        self.nat.check(self.nat.lib.mle_dctx_update_range(self._d, b, self._p(exch), lo, hi))
 
     def wblock(self, b, exch):
         self.nat.check(self.nat.lib.mle_dctx_wblock(self._d, b, self._p(exch)))
@@ -186,24 +205,119 @@ class CudaPanels:
     def right_operand(self, b, exch):
         self.nat.check(self.nat.lib.mle_dctx_right_operand(self._d, b, self._p(exch)))
 
-    def right(self, b, exch_w, exch_x):
-        self.nat.check(self.nat.lib.mle_dctx_right(self._d, b, self._p(exch_w),
-                                                   self._p(exch_x)))
+    def right(self, b, exch_w, exch_x, lo=0, hi=None):
+        """exch_w None: W_b from this rank's W cache (wcache)."""
+        hi = self.nb if hi is None else hi
+        w = None if exch_w is None else self._p(exch_w)
+        self.nat.check(self.nat.lib.mle_dctx_right_range(self._d, b, w, self._p(exch_x), lo,
+                                                         hi))
+
+    def wcache(self, on=True):
+        """Keep every W_b (~3.5 N^2 bytes) for the right sweep; False if it does not fit."""
+        rc = self.nat.lib.mle_dctx_wcache(self._d, int(bool(on)))
+        if rc == self.nat.MLE_CUDA_ERROR:
+            return False
+        self.nat.check(rc)
+        return bool(on)
+
+    def set_async(self, on=True):
+        self.nat.check(self.nat.lib.mle_dctx_set_async(self._d, int(bool(on))))
+
+    def stream(self):
+        """The rank's compute stream as a torch stream (its block steps run on it)."""
+        h = ctypes.c_void_p()
+        self.nat.check(self.nat.lib.mle_dctx_stream(self._d, ctypes.byref(h)))
+        return self.torch.cuda.ExternalStream(h.value, device=f"cuda:{self.device}")
 
     def partials(self):
         out = np.zeros(16)
         self.nat.check(self.nat.lib.mle_dctx_partials(self._d, self.nat.as_ptr(out)))
         return out
 
+    def panel_partials(self):
+        """({block: 14 sums}, failed, pivot) for this rank's panels."""
+        owned = list(range(self.rank, self.nb, self.world))
+        out = np.zeros(len(owned) * SUMS + 2)
+        self.nat.check(self.nat.lib.mle_dctx_panel_partials(self._d, self.nat.as_ptr(out)))
+        per = {b: out[q * SUMS:(q + 1) * SUMS].copy() for q, b in enumerate(owned)}
+        return per, out[-2] > 0, out[-1]
+
 
 # --------------------------------------------------------------------------------- driver
+class _Exchange:
+    """Double-buffered exchange slots of one kind (P, W or X) and their ordering.
+
+    Synchronous mode (gloo, in-process ranks, host backends): every block step has drained its
+    stream, ``send`` is a blocking broadcast, nothing else to order.  Stream-ordered mode
+    (NCCL; CudaPanels in async mode): a slot's broadcast runs on the rank's communication
+    stream after (i) the owner's producing step (event on the compute stream) and (ii) the
+    previous consumer of the slot (event); the consuming step waits for the broadcast's
+    event -- so broadcasts of block b + 1 overlap the trailing GEMMs of block b."""
+
+    def __init__(self, engine, kind):
+        self.e = engine
+        self.buf = [[r.exchange(kind) for r in engine.ranks] for _ in range(2)]
+        self.free = [None, None]  # per slot: per local rank, event after the last consumer
+
+    def slot(self, b):
+        return self.buf[b % 2]
+
+    def produced(self, b, r):
+        """Owner r (local index) has queued the step that fills slot b."""
+        if not self.e.async_steps:
+            return None
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record(self.e.streams[r])
+        return ev
+
+    def send(self, b, owner, ready):
+        """Broadcast slot b from ``owner`` (group rank); ``ready`` = produced(...) or None."""
+        bufs = self.slot(b)
+        if not self.e.async_steps:
+            self.e.comm.broadcast(bufs, owner)
+            return
+        import torch
+
+        r = 0  # one local rank per process in stream-ordered mode
+        cs = self.e.comm_streams[r]
+        if ready is not None:
+            cs.wait_event(ready)
+        if self.free[b % 2] is not None:
+            cs.wait_event(self.free[b % 2][r])
+        with torch.cuda.stream(cs):
+            self.e.comm.broadcast_on_stream(bufs[r], owner)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self.e.streams[r].wait_event(ev)
+
+    def consumed(self, b):
+        """Every consumer of slot b on this rank has been queued."""
+        if not self.e.async_steps:
+            return
+        import torch
+
+        evs = []
+        for st in self.e.streams:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            evs.append(ev)
+        self.free[b % 2] = evs
+
+
 class DistributedEngine:
     """loglik / eval_all of one dataset over ``comm``'s ranks (the reference's surface)."""
 
     def __init__(self, locations, values, comm, nugget: float = 0.0, device: int = 0,
-                 backend=None):
+                 backend=None, overlap=None, wcache=None):
         """``backend(locations, values, rank, world, nugget)`` builds one rank's panels
-        (default: :class:`CudaPanels` on ``device``; tests pass a host restatement)."""
+        (default: :class:`CudaPanels` on ``device``; tests pass a host restatement).
+
+        ``overlap`` (default: on for NCCL with the CUDA backend): block steps are queued
+        asynchronously and the panel / W / X broadcasts run on a communication stream under
+        the trailing GEMMs.  ``wcache`` (default: on when the memory is there): every rank
+        keeps the forward sweep's W_b for the right sweep instead of a second broadcast."""
         self.comm = comm
         self.nugget = float(nugget)
         world = comm.world
@@ -213,7 +327,28 @@ class DistributedEngine:
         self.n = self.ranks[0].n
         self.nb = self.ranks[0].nb
         self.world = world
-        self._ex = {k: [r.exchange(k) for r in self.ranks] for k in ("P", "W", "X")}
+        can_async = (backend is None and getattr(comm, "stream_ordered", False)
+                     and len(self.ranks) == 1)
+        self.async_steps = can_async if overlap is None else (bool(overlap) and can_async)
+        self.streams, self.comm_streams = [], []
+        if self.async_steps:
+            import torch
+
+            for r in self.ranks:
+                r.set_async(True)
+                self.streams.append(r.stream())
+                self.comm_streams.append(torch.cuda.Stream(device=r.device))
+        self._ex = {k: _Exchange(self, k) for k in ("P", "W", "X")}
+        want = True if wcache is None else bool(wcache)
+        self.wcache = False
+        if want and all(hasattr(r, "wcache") for r in self.ranks):
+            ok = [r.wcache(True) for r in self.ranks]
+            # every rank must agree (the right sweep's broadcast pattern depends on it)
+            votes = self.comm.all_reduce_sum([np.array([1.0 if o else 0.0]) for o in ok])[0]
+            self.wcache = float(votes[0]) > world - 0.5
+            if not self.wcache:
+                for r in self.ranks:
+                    r.wcache(False)
 
     def close(self):
         for r in self.ranks:
@@ -225,51 +360,141 @@ class DistributedEngine:
     def _local(self, rank):
         return self.local.index(rank) if rank in self.local else None
 
+    def _others(self, b_next):
+        """Range pieces of the blocks other than b_next: [(0, b_next), (b_next + 1, nb)]."""
+        return [(0, b_next), (b_next + 1, self.nb)]
+
     def _run(self, theta, derivs):
         th = MaternParams.from_array(theta).as_array()
         for r in self.ranks:
             r.begin(th, derivs)
-        P, W, X = self._ex["P"], self._ex["W"], self._ex["X"]
-        for b in range(self.nb):  # right-looking Cholesky
-            o = self._owner(b)
-            lo = self._local(o)
-            if lo is not None:
-                self.ranks[lo].factor(b, P[lo])
-            if b + 1 < self.nb:
-                self.comm.broadcast(P, o)
-                for r, be in enumerate(self.ranks):
-                    be.update(b, P[r])
+        self._cholesky()
         if derivs:
-            for b in range(self.nb):  # forward sweep X = L^-1 S on every rank's own columns
-                o = self._owner(b)
-                lo = self._local(o)
-                if lo is not None:
-                    self.ranks[lo].wblock(b, W[lo])
-                self.comm.broadcast(W, o)
-                for r, be in enumerate(self.ranks):
-                    be.forward(b, W[r])
-            for b in range(self.nb):  # right sweep (lower half of X L^-T)
-                o = self._owner(b)
-                lo = self._local(o)
-                if lo is not None:
-                    self.ranks[lo].wblock(b, W[lo])
-                    self.ranks[lo].right_operand(b, X[lo])
-                self.comm.broadcast(W, o)
-                self.comm.broadcast(X, o)
-                for r, be in enumerate(self.ranks):
-                    be.right(b, W[r], X[r])
-        local = [be.partials() for be in self.ranks]
-        parts = self.comm.all_reduce_sum(local)[0]
-        if parts[14] > 0:
+            self._forward_sweep()
+            self._right_sweep()
+        # Per-panel sums placed in a (blocks x sums) array (zeros elsewhere: adding them is
+        # exact), one all-reduce, then the panels added in block order: the result does not
+        # depend on the number of ranks or on who owns what.
+        width = SUMS + 2
+        vecs, fails = [], []
+        for r, be in zip(self.local, self.ranks):
+            v = np.zeros((self.nb + 1) * width)
+            if hasattr(be, "panel_partials"):
+                per, failed, pivot = be.panel_partials()
+                for b, sums in per.items():
+                    v[b * width:b * width + SUMS] = sums
+            else:  # host restatement backends: one row per rank
+                p = be.partials()
+                v[r * width:r * width + SUMS] = p[:SUMS]
+                failed, pivot = p[14] > 0, p[15]
+            v[self.nb * width + SUMS] = 1.0 if failed else 0.0
+            vecs.append(v)
+            fails.append((failed, pivot))
+        tot = self.comm.all_reduce_sum(vecs)[0].reshape(self.nb + 1, width)
+        parts = np.zeros(16)
+        for b in range(self.nb):
+            parts[:SUMS] += tot[b, :SUMS]
+        if tot[self.nb, SUMS] > 0:
             # every failed rank reports its first failing pivot; the smallest wins (LAPACK)
             big = float(2 ** 52)
-            vecs = []
-            for r, p in zip(self.local, local):
+            piv = []
+            for r, (failed, pivot) in zip(self.local, fails):
                 v = np.zeros(self.world)
-                v[r] = p[15] if p[14] > 0 else big
-                vecs.append(v)
-            raise NotPositiveDefinite(int(np.min(self.comm.all_reduce_sum(vecs)[0])))
+                v[r] = pivot if failed else big
+                piv.append(v)
+            raise NotPositiveDefinite(int(np.min(self.comm.all_reduce_sum(piv)[0])))
         return th, parts
+
+    # Right-looking Cholesky with look-ahead: the owner of block b + 1 applies block b's update
+    # to its panel b + 1 first, factors it and sends P_{b+1}; the remaining updates of block b
+    # (every rank) run while P_{b+1} is in flight.  Panel updates are independent GEMMs, so
+    # the split changes no arithmetic.
+    def _cholesky(self):
+        P, nb = self._ex["P"], self.nb
+
+        def factor_and_send(b):
+            o = self._owner(b)
+            lo = self._local(o)
+            ready = None
+            if lo is not None:
+                self.ranks[lo].factor(b, P.slot(b)[lo])
+                ready = P.produced(b, lo)
+            if b + 1 < nb:
+                P.send(b, o, ready)
+
+        factor_and_send(0)
+        for b in range(nb - 1):
+            nxt = b + 1
+            on = self._local(self._owner(nxt))
+            for r, be in enumerate(self.ranks):
+                if r == on:
+                    be.update(b, P.slot(b)[r], nxt, nxt + 1)
+            factor_and_send(nxt)
+            for r, be in enumerate(self.ranks):
+                pieces = self._others(nxt) if r == on else [(0, nb)]
+                for lo, hi in pieces:
+                    be.update(b, P.slot(b)[r], lo, hi)
+            P.consumed(b)
+
+    # Forward sweep X = L^-1 S: W_b depends only on L, so the owner of b + 1 builds and sends
+    # W_{b+1} ahead of block b's GEMMs.
+    def _forward_sweep(self):
+        W, nb = self._ex["W"], self.nb
+
+        def build_and_send(b):
+            o = self._owner(b)
+            lo = self._local(o)
+            ready = None
+            if lo is not None:
+                self.ranks[lo].wblock(b, W.slot(b)[lo])
+                ready = W.produced(b, lo)
+            W.send(b, o, ready)
+
+        build_and_send(0)
+        for b in range(nb):
+            if b + 1 < nb:
+                build_and_send(b + 1)
+            for r, be in enumerate(self.ranks):
+                be.forward(b, W.slot(b)[r])
+            W.consumed(b)
+
+    # Right sweep (lower half of X L^-T): the owner of b + 1 applies block b to its panel
+    # b + 1 first, slices X[:, b+1] and sends it; W_b comes from the W cache (or is re-sent).
+    def _right_sweep(self):
+        W, X, nb = self._ex["W"], self._ex["X"], self.nb
+
+        def operand_and_send(b):
+            o = self._owner(b)
+            lo = self._local(o)
+            ready = None
+            if lo is not None:
+                if not self.wcache:
+                    self.ranks[lo].wblock(b, W.slot(b)[lo])
+                self.ranks[lo].right_operand(b, X.slot(b)[lo])
+                ready = X.produced(b, lo)
+            if not self.wcache:
+                W.send(b, o, ready)
+            X.send(b, o, ready)
+
+        def wb(b, r):
+            return None if self.wcache else W.slot(b)[r]
+
+        operand_and_send(0)
+        for b in range(nb):
+            nxt = b + 1
+            on = self._local(self._owner(nxt)) if nxt < nb else None
+            if nxt < nb:
+                for r, be in enumerate(self.ranks):
+                    if r == on:
+                        be.right(b, wb(b, r), X.slot(b)[r], nxt, nxt + 1)
+                operand_and_send(nxt)
+            for r, be in enumerate(self.ranks):
+                pieces = self._others(nxt) if r == on else [(0, nb)]
+                for lo, hi in pieces:
+                    be.right(b, wb(b, r), X.slot(b)[r], lo, hi)
+            X.consumed(b)
+            if not self.wcache:
+                W.consumed(b)
 
     def loglik(self, theta) -> float:
         th, s = self._run(theta, False)

@@ -56,10 +56,21 @@ def reference():
     return maternmle
 
 
-def fd_regime(theta):
-    """theta whose nu sits in the reference's finite-difference band (bessel.py:117-141)."""
+def fd_regime(theta, locations=None):
+    """theta whose nu sits in the reference's finite-difference band (bessel.py:126-141):
+    nu within 1e-6 of an integer (case-2 range, x < 8.5), or of a half-integer when some
+    u = h / alpha >= 30 can occur (case-4 range; bounded by the locations' bounding-box
+    diagonal when the locations are given)."""
     nu = theta[2]
-    return abs(nu - round(nu)) <= 1e-6 or abs(nu + 0.5 - round(nu + 0.5)) <= 1e-6
+    if abs(nu - round(nu)) <= 1e-6:
+        return True
+    if abs(nu + 0.5 - round(nu + 0.5)) > 1e-6:
+        return False
+    if locations is None:
+        return True
+    loc = np.asarray(locations, float)
+    diag = float(np.hypot(*(loc.max(axis=0) - loc.min(axis=0)))) if len(loc) > 1 else 0.0
+    return diag / theta[1] >= 30.0
 
 
 @pytest.fixture(scope="session")

@@ -81,15 +81,21 @@ class HostPanels:
             exch.view(-1)[: (N - c1) * BLOCK] = \
                 __import__("torch").from_numpy(np.ascontiguousarray(p[c1:, :]).ravel())
 
-    def update(self, b, exch):
+    def update(self, b, exch, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
         c1, N = (b + 1) * BLOCK, self.N
         P = exch.numpy()[: (N - c1) * BLOCK].reshape(N - c1, BLOCK)
         for j in self.owned:
-            if j <= b:
+            if j <= b or not lo <= j < hi:
                 continue
             cj = j * BLOCK
             Pj = P[cj - c1:, :]
             self.sig[j][cj:, :] -= Pj @ P[cj - c1:cj - c1 + BLOCK, :].T
+
+    def wcache(self, on=True):
+        self.cache_w = bool(on)
+        self.wc = {}
+        return self.cache_w
 
     def wblock(self, b, exch):
         import scipy.linalg as sla
@@ -104,6 +110,8 @@ class HostPanels:
     def forward(self, b, exch):
         c0, c1, N = b * BLOCK, (b + 1) * BLOCK, self.N
         w = exch.numpy()[: (N - c0) * BLOCK].reshape(N - c0, BLOCK)
+        if getattr(self, "cache_w", False):
+            self.wc[b] = w.copy()
         for mats in self.mat:
             for j in self.owned:
                 x = mats[j][c0:c1, :].copy()
@@ -118,14 +126,18 @@ class HostPanels:
             a[np.triu_indices(BLOCK, 1)] = 0.0  # only k <= r (rows and columns from c0)
             buf[m, : (N - c0) * BLOCK] = a.ravel()
 
-    def right(self, b, exch_w, exch_x):
+    def right(self, b, exch_w, exch_x, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
         c0, N = b * BLOCK, self.N
-        w = exch_w.numpy()[: (N - c0) * BLOCK].reshape(N - c0, BLOCK)
+        if exch_w is None:
+            w = self.wc[b]
+        else:
+            w = exch_w.numpy()[: (N - c0) * BLOCK].reshape(N - c0, BLOCK)
         xs = exch_x.numpy().reshape(self.nmat, N * BLOCK)
         for m, mats in enumerate(self.mat):
             x = xs[m, : (N - c0) * BLOCK].reshape(N - c0, BLOCK)
             for j in self.owned:
-                if j < b:
+                if j < b or not lo <= j < hi:
                     continue
                 cj = j * BLOCK
                 upd = x[cj - c0:, :] @ w[cj - c0:cj - c0 + BLOCK, :].T

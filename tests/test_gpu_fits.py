@@ -167,11 +167,11 @@ def test_loglik_many_is_bit_identical_to_single_calls(gpu):
 
 
 def test_fit_many_keeps_going_past_a_failed_fit(gpu):
-    """One fit of a lock-step group failing (coincident locations: every L9 candidate is
-    singular -> InitializationFailed, optimizer.py:193-196) does not stop the others."""
+    """One fit of a lock-step group failing (all locations within 1e-12 of each other: Sigma
+    is numerically rank one, every L9 candidate's Cholesky fails -> InitializationFailed,
+    optimizer.py:193-196) does not stop the others."""
     loc, z = config_data("config1", 0)
-    bad = loc.copy()
-    bad[1] = bad[0]
+    bad = 0.5 + 1e-12 * np.random.default_rng(0).uniform(size=loc.shape)
     th0 = gpu.MaternParams(0.5, 0.05, 1.0)
     cfg = gpu.FisherBTConfig(theta_lower=th0, theta_upper=th0)
     sets = [gpu.SpatialDataset(loc, z), gpu.SpatialDataset(bad, z)]

@@ -24,8 +24,8 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, config_data
-from test_gpu_likelihood import FISHER_TOL, LL_TOL, SCORE_TOL, check_eval, score_scale
+from conftest import GOLDEN, config_data, fd_regime
+from test_gpu_likelihood import FD_TOL, FISHER_TOL, LL_TOL, SCORE_TOL, check_eval, score_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -78,12 +78,19 @@ def test_config5_window_vs_reference_and_restatement(gpu):
     eng.close()
     assert ll == pytest.approx(rec["nugget_eval_loglik"], rel=LL_TOL)
     ref_g, ref_f = np.array(rec["nugget_grad"]), np.array(rec["nugget_fisher"])
-    assert np.all(np.abs(f - ref_f) <= FISHER_TOL * np.abs(ref_f)), (f, ref_f)
-    # score scale from the restatement's own components (sigma^2 row: n / (2 s2) terms)
+    # config 5's nu = 1.0 is in the reference's forward-difference band (bessel.py:321-324):
+    # the restatement's d/dnu is scipy kv's lag-1e-9 difference (~1e-4 relative noise), so the
+    # nu-dependent entries get the FD carve-out of test_gpu_likelihood; the rest the
+    # north-star bounds
+    fd = fd_regime(th, loc)
+    tol_f = np.full((3, 3), FISHER_TOL)
+    if fd:
+        tol_f[2, :] = tol_f[:, 2] = FD_TOL
+    assert np.all(np.abs(f - ref_f) <= tol_f * np.abs(ref_f)), (f, ref_f)
     scale = score_scale(th, n, g, f)
     # case-2 cancellation near u = 8.5 (bessel.py:213-222) puts ~4e-8 of scale into the
     # reference's own nu score at config-5 theta (DESIGN.md §5 carve-out 2)
-    tol = np.array([SCORE_TOL, SCORE_TOL, 1e-7])
+    tol = np.array([SCORE_TOL, SCORE_TOL, FD_TOL if fd else 1e-7])
     assert np.all(np.abs(g - ref_g) <= tol * scale), (g, ref_g, scale)
 
 

@@ -2,8 +2,13 @@
 golden reference outputs and the CPU oracle.  Tolerances (north_star): log-likelihood 1e-10
 relative; Fisher 1e-8 relative; score 1e-8 relative to its two component magnitudes
 (SURVEY.md §8(c)).  At finite-difference-regime theta (nu within 1e-6 of an integer) the
-reference's own d/dnu entries carry lag-1e-9 forward-difference noise (~1e-6 per element,
-amplified by cond(Sigma)), so the nu-dependent entries are compared at 1e-3 there.
+reference's d/dnu is a lag-1e-9 forward difference of scipy's kv (bessel.py:321-324): kv's own
+error (up to 7e-14 relative near x = 2) divided by the 1e-9 lag puts up to ~1e-4 relative
+noise into every d/dnu element, which the engine (30-digit-accurate K_nu) cannot and should not
+reproduce.  Measured deviation of the nu-dependent Fisher entries there (tools/parity_report.py,
+profiles/r02_parity_report.json): 1.6e-6 (config 1, theta0), 1.3e-5 (config 2, theta0),
+4.7e-5 (config 3, theta0), 3.6e-4 (config 1, nu = 2); so those entries are compared at 1e-3,
+everything else at the north-star tolerances.
 
 Log-likelihood noise floor of the reference itself: on a few very ill-conditioned small
 goldens (nu = 2.3 on random locations) the reference's own value is not determined to 1e-10 by
@@ -43,7 +48,7 @@ def check_eval(gpu, data, rec, n, floor=0.0):
     np.testing.assert_array_equal(ev.fisher, ev.fisher.T)
     ref_g, ref_f = np.array(rec["grad"]), np.array(rec["fisher"])
     scale = score_scale(th, n, ev.grad, ev.fisher)
-    fd = fd_regime(th)
+    fd = fd_regime(th, data.locations)
     for i in range(3):
         tol = FD_TOL if (fd and i == 2) else SCORE_TOL
         assert abs(ev.grad[i] - ref_g[i]) <= tol * scale[i], (th, i, ev.grad, ref_g)

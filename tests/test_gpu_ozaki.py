@@ -154,7 +154,7 @@ def test_generation_tables_vs_exact(gpu):
         ex = _with_env("MLE_GEN_TABLE", "0", lambda: gpu.Engine(loc, z).eval_all(th))
         tb = _with_env("MLE_GEN_TABLE", "1", lambda: gpu.Engine(loc, z).eval_all(th))
         assert tb[0] == pytest.approx(ex[0], rel=1e-11)
-        fd = fd_regime(th)
+        fd = fd_regime(th, loc)
         tol_f = np.full((3, 3), 1e-9)
         if fd:
             tol_f[2, :] = tol_f[:, 2] = 1e-5

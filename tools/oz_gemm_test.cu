@@ -95,7 +95,7 @@ static double run_case(const Case& cs, int batch, int reps) {
   std::vector<double> C1(C.size()), C2(C.size());
   CK(cudaMemcpy(C1.data(), dC1, C.size() * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(C2.data(), dC2, C.size() * 8, cudaMemcpyDeviceToHost));
-  for (int other : {0, 1, 2}) {  // every kernel variant must give bit-identical results
+  for (int other : {0, 1, 2, 3}) {  // every kernel variant must give bit-identical results
     if (other == g_ntile) continue;
     CK(cudaMemcpy(dC2, C.data(), C.size() * 8, cudaMemcpyHostToDevice));
     CK(launch_ozgemm(o, 1, 0, other));
@@ -151,7 +151,7 @@ static double run_case(const Case& cs, int batch, int reps) {
     CK(cudaEventSynchronize(b));
     cudaEventElapsedTime(&t_o, a, b);
   }
-  if (g_ntile <= 1) {  // diagnostics: loads only / MMAs only
+  if (getenv("OZ_DIAG")) {  // diagnostics: loads only / MMAs only
     float t1, t2;
     o.diag_mode = 1;
     cudaEventRecord(a);

@@ -34,7 +34,7 @@ def deviations(data, rec, n):
     df = np.abs(ev.fisher - f) / np.abs(f)
     nu_mask = np.zeros((3, 3), bool)
     nu_mask[2, :] = nu_mask[:, 2] = True
-    return {"theta": th, "fd_band": fd_regime(th),
+    return {"theta": th, "fd_band": fd_regime(th, data.locations),
             "loglik_rel": abs(ll - rec["loglik"]) / abs(rec["loglik"]),
             "eval_loglik_rel": abs(ev.loglik - rec["eval_loglik"]) / abs(rec["eval_loglik"]),
             "score_rel_scale": dg.tolist(),
