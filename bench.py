@@ -20,10 +20,11 @@ Own arm ("ours"), one process per GPU (torchrun for N > 1):
           resident in HBM; e2e = one complete fit through the public API from host numpy
           arrays (dataset upload inside the timed region, results read back).
   roofline: the dominant kernel (the Ozaki FP64 GEMM on tcgen05 int8) in a kernel-profiled
-          eval_all, ALGORITHMIC flops (3 n^3 per eval_all for factor + solves,
-          minus the 128-wide DMMA steps inside the Cholesky's 512-column blocks) x 28 int8
-          slice products / summed launch durations, against 2 x MEASURED_PEAKS bf16 (int8 dense
-          = twice bf16 dense; the sustained figure: the GEMMs run for seconds inside a step).
+          eval_all, ALGORITHMIC flops of its launches (SURVEY §8(d) block sums: Cholesky
+          n^3 / 3 + per derivative block n^3 for the two-sided reduction used at this size;
+          gemm_algorithmic_flops) x 28 int8 slice products / summed launch durations, against
+          2 x MEASURED_PEAKS bf16 (int8 dense = twice bf16 dense; the sustained figure: the
+          GEMMs run for seconds inside a step).
 Reference arm (--impl reference): the reference's own CPU algorithm (oracle port of maternmle:
 numpy / scipy / OpenBLAS on all host cores), rank 0 only.  A config-4 Fisher iteration is
 hours of CPU (one Sigma generation alone ~20 min single-threaded), so each step times a
@@ -163,13 +164,41 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def gemm_algorithmic_flops(n, mode):
-    """Standard-count FP64 flops the Ozaki GEMM launches of one evaluation carry (SURVEY
-    §8(d)): factor n^3/3 (+ forward sweep n^3 and lower-half right sweep n^3/3 per derivative
-    block for eval_all: 3 n^3), minus the Cholesky's 128-wide DMMA steps inside each 512-column
-    block (~ 512^2 / 2 per element row of the block: 256 n^2)."""
-    total = n ** 3 / 3.0 + (2 * (n ** 3 + n ** 3 / 3.0) if mode == "eval_all" else 0.0)
-    return total - 256.0 * n * n
+TWO_SIDED_MIN_N = 16384  # engine.cu kTwoSidedMinN: eval_all's solve formulation by size
+
+
+def solve_path(n):
+    env = os.environ.get("MLE_SOLVE")
+    if env in ("w", "2s"):
+        return env
+    big_n = -(-(n + 1) // 128) * 128
+    return "2s" if big_n >= TWO_SIDED_MIN_N else "w"
+
+
+def gemm_algorithmic_flops(n, mode, path=None, nderiv=2, blk=512):
+    """Standard-count FP64 flops of one evaluation's Ozaki GEMM launches, as
+    block sums over the 512-column outer blocks (c0 = b blk, c1 = c0 + blk):
+      Cholesky trailing updates (lower):  sum (n - c1)^2 blk                        ~ n^3 / 3
+      eval_all, per derivative block, path "w" (solves_w):
+        forward sweep X = L^-1 S:         sum 2 (n - c0) blk n                      ~ n^3
+        right sweep (lower half):         sum (n - c0)^2 blk                        ~ n^3 / 3
+      path "2s" (solves_2s, the sygst recurrence):
+        syr2k trailing updates:           sum 2 (n - c1)^2 blk                      ~ 2 n^3 / 3
+        panel products (2), (3), (5):     sum 3 x 2 (n - c1) blk^2                  ~ 3 blk n^2
+        deferred forward sweep (lower):   sum 2 (n - c0) blk c0                     ~ n^3 / 3
+    The Cholesky's 128-wide DMMA steps inside each block (not Ozaki launches) are excluded."""
+    path = path or solve_path(n)
+    chol = derv = 0.0
+    for b in range(-(-n // blk)):
+        c0 = b * blk
+        c1 = min(n, c0 + blk)
+        chol += float(n - c1) ** 2 * blk
+        if path == "w":
+            derv += 2.0 * (n - c0) * blk * n + float(n - c0) ** 2 * blk
+        else:
+            derv += 2.0 * float(n - c1) ** 2 * blk + 6.0 * (n - c1) * blk * blk \
+                + 2.0 * (n - c0) * blk * c0
+    return chol + (nderiv * derv if mode == "eval_all" else 0.0)
 
 
 def kernel_profile(engine, theta, n, peaks):
@@ -183,6 +212,7 @@ def kernel_profile(engine, theta, n, peaks):
         engine.kernel_profile(False)
     alg = gemm_algorithmic_flops(n, "eval_all")
     gemm_s = ks["gemm_ms"] * 1e-3
+    pt = engine.phase_times()
     int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0))
     achieved = alg * OZ_PRODUCTS / gemm_s / 1e12
     return {
@@ -197,6 +227,13 @@ def kernel_profile(engine, theta, n, peaks):
         "int8_peak_tops": int8_peak,
         "slice_ms": ks["slice_ms"], "slice_gbs": ks["slice_bytes"] / max(1e-9, ks["slice_ms"]
                                                                          * 1e-3) / 1e9,
+        "solve_path": solve_path(n),
+        "eval_all_ms": pt["total_ms"],
+        # the reference's own work per eval_all (dpotrf + four n x n dtrsm: 13 n^3 / 3,
+        # likelihood.py:121-135) over this engine's eval_all time: algorithm changes show
+        # as speed-ups here, not as inflated TFLOP/s in the roofline
+        "reference_equivalent_tflops": 13.0 * float(n) ** 3 / 3.0 / (pt["total_ms"] * 1e-3)
+                                       / 1e12,
         "gen_ms": ks["gen_ms"],
         "gen_gbs": ks["gen_bytes"] / (ks["gen_ms"] * 1e-3) / 1e9 if ks["gen_ms"] else 0.0,
     }
@@ -480,9 +517,10 @@ def ours_arm(args, rank, world, local_rank):
             "peak": kp["int8_peak_tops"], "frac": kp["ozgemm_alg_int8_tops"] / kp["int8_peak_tops"],
             "traffic": None,
             "kernel": "ozgemm_persistent_kernel<64,7,2> (Ozaki FP64 GEMM on tcgen05.mma kind::i8)"
-                      ": ALGORITHMIC FP64 flops of one config-4 eval_all's GEMM launches (3n^3 - "
-                      "256n^2) x 28 int8 slice products / summed launch durations (CUDA events "
-                      "on the launching stream, kernel-profiling pass)",
+                      ": ALGORITHMIC FP64 flops of one config-4 eval_all's GEMM launches (block "
+                      "sums of the solve path used, bench.gemm_algorithmic_flops) x 28 int8 "
+                      "slice products / summed launch durations (CUDA events on the launching "
+                      "stream, kernel-profiling pass)",
             "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 dense = 2 x bf16 "
                            "dense; sustained: the GEMMs run for seconds inside a step)",
             "traffic_note": "see profiles/r02_* (ncu of the same build)",

@@ -253,7 +253,23 @@ int oz_tile_variant() {
   return v;
 }
 
+// Solve formulation of eval_all (both give B_i = L^-1 S_i L^-T, lower half):
+//   "w"  -- full forward sweep X = L^-1 S (n^3) + lower half of X L^-T (n^3 / 3);
+//   "2s" -- two-sided blocked reduction (the sygst recurrence, 2 n^3 / 3 of syr2k-shaped
+//           trailing updates) + the deferred forward sweep on the strictly lower block part
+//           (n^3 / 3): n^3 per derivative block instead of 4 n^3 / 3.
+// MLE_SOLVE=w|2s overrides; default "2s" from N >= kTwoSidedMinN (the recurrence's per-block
+// chain is latency-bound on small matrices).
+constexpr long long kTwoSidedMinN = 16384;
+bool use_two_sided(long long N) {
+  const char* e = std::getenv("MLE_SOLVE");
+  if (e && std::strcmp(e, "2s") == 0) return true;
+  if (e && std::strcmp(e, "w") == 0) return false;
+  return N >= kTwoSidedMinN;
+}
+
 // FP64 trailing-update GEMM: Ozaki int8 tensor-core emulation (default) or DMMA.
+bool use_ozaki();
 bool use_ozaki() {
   const char* v = std::getenv("MLE_FP64_GEMM");
   return !(v && std::strcmp(v, "dmma") == 0);
@@ -322,6 +338,12 @@ struct mle_ctx {
   int8_t* wsl = nullptr;
   int* wex = nullptr;
   int w_slices = 0;               // slice count of the resident W slices
+  // two-sided reduction (solves_2s): per derivative matrix a 512 x 512 FP64 scratch and the
+  // slices of its current diagonal block
+  double* ts2 = nullptr;
+  int8_t* a11sl = nullptr;
+  int* a11ex = nullptr;
+  bool deriv_lower = false;       // derivative matrices hold their lower tiles only (2s path)
   // Kernel profiling (mle_kernel_profile): single stream, CUDA events around every Ozaki
   // GEMM and slicing launch of the pass; mle_kernel_stats reports the sums.
   bool kprof = false;
@@ -356,6 +378,11 @@ struct Item {
   int64_t pivot = -1;
   double res[kResults] = {};
 };
+
+// Derivative matrices generated for the two-sided solves: lower tiles only.
+bool two_sided_gen(const mle_ctx* c) {
+  return c->ozaki && solve_slices() == kOzSlices && use_two_sided(c->N);
+}
 
 // Pending speculative work (issued on some batch leader's aux stream) must finish before
 // anything else touches this context's buffers.
@@ -433,6 +460,10 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
     CUDA_TRY(dmalloc(&c->wbuf, sizeof(double) * (size_t)c->N * 512));
     CUDA_TRY(dmalloc(&c->dtsl, (size_t)512 * kOzRowBytes));
     CUDA_TRY(dmalloc(&c->dtex, sizeof(int) * 512));
+    const int mats = regions / 2;
+    CUDA_TRY(dmalloc(&c->ts2, sizeof(double) * (size_t)mats * 512 * 512));
+    CUDA_TRY(dmalloc(&c->a11sl, (size_t)mats * 512 * kOzRowBytes));
+    CUDA_TRY(dmalloc(&c->a11ex, sizeof(int) * (size_t)mats * 512));
     CUDA_TRY(dmalloc(&c->wsl, std::max<size_t>(1, w_byte_offset(c->Nt, nb))));
     CUDA_TRY(dmalloc(&c->wex, sizeof(int) * std::max<long long>(1, w_row_offset(c->Nt, nb))));
     // the upper tiles of every D_b^-1 are never written and must read as exact zeros
@@ -869,6 +900,10 @@ struct Launcher {
         int rc = compute_w(rw, nw, ks);
         if (rc) return rc;
       }
+      // lower-only derivative matrices can only take the two-sided path
+      bool two = ks == kOzSlices && use_two_sided(cs[0]->N);
+      for (int i = 0; i < m; ++i) two = two || cs[i]->deriv_lower;
+      if (two) return solves_2s(cs, m);
       return solves_w(cs, m, ks);
     }
     return solves_dmma(cs, m);
@@ -1131,6 +1166,226 @@ struct Launcher {
     return join(s2, s);
   }
 
+  // ---- two-sided blocked reduction B = L^-1 S L^-T (lower half), the sygst recurrence ----
+  // For outer block b (columns [c0, c1), D = L11 = L[c0:c1, c0:c1], L21 = L[c1:, c0:c1], and
+  // S partitioned alike, S11 / S21 / S22 already updated by the blocks before b):
+  //   (1) S11 <- D^-1 S11 D^-T                      two 512^3 DMMA products (D^-1 resident)
+  //   (2) S21 <- S21 D^-T                           Ozaki GEMM, B = the rows of D^-1 (= the
+  //                                                 top slices of W_b)
+  //   (3) S21 <- S21 - 1/2 L21 S11                  Ozaki GEMM, A = the factor's panel slices
+  //   (4) S22 <- S22 - S21 L21^T - L21 S21^T        two lower-triangle Ozaki GEMMs (syr2k)
+  //   (5) S21 <- S21 - 1/2 L21 S11
+  // and S21 is final after the deferred (6) S21 <- L22^-1 S21, done for all blocks at once as
+  // the block-inverse forward sweep restricted to the columns left of each row block (the
+  // strictly lower block part): X[c0:, 0:c0] = W_b X[c0:c1, 0:c0].
+  // Flops per derivative block: (4) 2 n^3 / 3 + (6) n^3 / 3 = n^3, against n^3 + n^3 / 3 for
+  // the full forward sweep + right sweep of solves_w.  The diagonal blocks are exact after
+  // (1): the reductions read the lower half as before (B[n, n] = y^T B y on the augmented row).
+  int solves_2s(mle_ctx* const* cs, int m) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    const int nb = (Nt + kOuter - 1) / kOuter;
+    MatList ml(cs, m);
+    const int zb = ml.count;
+    auto S = [&](int z) { return ml.S(z); };
+    auto flag = [&](int z) { return (const int*)ml.c[z]->fail_flag; };
+    auto XS = [&](int z, int b) {
+      return ml.c[z]->xsl + ((size_t)ml.which[z] * 2 + (b & 1)) * ld * kOzRowBytes;
+    };
+    auto XE = [&](int z, int b) {
+      return ml.c[z]->xex + ((size_t)ml.which[z] * 2 + (b & 1)) * ld;
+    };
+    auto T2 = [&](int z) { return ml.c[z]->ts2 + (size_t)ml.which[z] * 512 * 512; };
+    auto AS = [&](int z) { return ml.c[z]->a11sl + (size_t)ml.which[z] * 512 * kOzRowBytes; };
+    auto AE = [&](int z) { return ml.c[z]->a11ex + (size_t)ml.which[z] * 512; };
+    int rc;
+    for (int b = 0; b < nb; ++b) {
+      const Blk k = blk(Nt, b);
+      const long long c1 = k.c0 + k.kb;
+      const int tb = k.t1 - k.t0;
+      const size_t woff = w_byte_offset(Nt, b);
+      const long long eoff = w_row_offset(Nt, b);
+      const long long eo = oz_panel_row_offset(Nt, b);
+      // (1) S11 <- D^-1 S11 D^-T.  Generation (lower_only) and the trailing updates (4) of the
+      // blocks before b write only lower tiles, so S11's upper tiles are restored from its
+      // lower ones first.
+      {
+        double* blks[kMaxGemm];
+        for (int z = 0; z < zb; ++z) blks[z] = S(z) + k.c0 + k.c0 * ld;
+        launches += 1;
+        CUDA_TRY(launch_mirror_lower(blks, zb, ld, (int)k.kb, s));
+      }
+      {
+        GemmArgs t = gemm_base(), u = gemm_base();
+        for (int z = 0; z < zb; ++z) {
+          const double* dinv_b = ml.c[z]->dinv + (size_t)b * 512 * 512;
+          t.A[z] = dinv_b;                          // A(i, kk) = Dinv(i, kk), lda 512
+          t.B[z] = S(z) + k.c0 + k.c0 * ld;         // B(n, kk) = S11(kk, n)   (kBKN)
+          t.C[z] = T2(z);
+          t.fail_flag[z] = flag(z);
+          u.A[z] = T2(z);                           // A(i, kk) = T(i, kk)
+          u.B[z] = dinv_b;                          // B(n, kk) = Dinv(n, kk)  (kBNK)
+          u.C[z] = S(z) + k.c0 + k.c0 * ld;
+          u.fail_flag[z] = flag(z);
+        }
+        t.lda = 512; t.ldb = ld; t.ldc = 512; t.K = (int)k.kb;
+        t.tiles_m = tb; t.tiles_n = tb; t.alpha = 1.0; t.beta = 0.0;
+        if ((rc = gemm(t, kBKN, zb))) return rc;
+        u.lda = 512; u.ldb = 512; u.ldc = ld; u.K = (int)k.kb;
+        u.tiles_m = tb; u.tiles_n = tb; u.alpha = 1.0; u.beta = 0.0;
+        if ((rc = gemm(u, kBNK, zb))) return rc;
+      }
+      if (c1 >= ld) break;
+      const int rt = (int)((ld - c1) / kNB);  // row tiles below the block
+      // slices of S21 (A operand: rows c1.., K over the block's columns)
+      auto slice_s21 = [&]() {
+        OzSliceArgs sa;
+        std::memset(&sa, 0, sizeof(sa));
+        for (int z = 0; z < zb; ++z) {
+          sa.X[z] = S(z) + c1 + k.c0 * ld;
+          sa.slices[z] = XS(z, b);
+          sa.e[z] = XE(z, b);
+          sa.fail_flag[z] = flag(z);
+        }
+        sa.ld = ld;
+        sa.K = (int)k.kb;
+        return slice(sa, ld - c1, true, zb);
+      };
+      // (2) S21 <- S21 D^-T
+      if ((rc = slice_s21())) return rc;
+      {
+        OzGemmArgs g = oz_base(ld, rt, tb);
+        g.kblocks = (int)(k.kb / 32);
+        g.alpha = 1.0;
+        g.beta = 0.0;
+        for (int z = 0; z < zb; ++z) {
+          g.As[z] = XS(z, b);
+          g.ea[z] = XE(z, b);
+          g.Bs[z] = ml.c[z]->wsl + woff;   // rows of D^-1 (W_b's top kb rows)
+          g.eb[z] = ml.c[z]->wex + eoff;
+          g.C[z] = S(z) + c1 + k.c0 * ld;
+          g.fail_flag[z] = flag(z);
+        }
+        if ((rc = ozgemm(g, zb, s))) return rc;
+      }
+      // slices of the new S11 (B operand of (3) / (5): B(n, kk) = S11(n, kk))
+      {
+        OzSliceArgs sa;
+        std::memset(&sa, 0, sizeof(sa));
+        for (int z = 0; z < zb; ++z) {
+          sa.X[z] = S(z) + k.c0 + k.c0 * ld;
+          sa.slices[z] = AS(z);
+          sa.e[z] = AE(z);
+          sa.fail_flag[z] = flag(z);
+        }
+        sa.ld = ld;
+        sa.K = (int)k.kb;
+        if ((rc = slice(sa, k.kb, true, zb))) return rc;
+      }
+      auto half_update = [&]() {  // S21 -= 1/2 L21 S11
+        OzGemmArgs g = oz_base(ld, rt, tb);
+        g.kblocks = (int)(k.kb / 32);
+        g.alpha = -0.5;
+        for (int z = 0; z < zb; ++z) {
+          g.As[z] = ml.c[z]->lsl + (size_t)eo * kOzRowBytes;
+          g.ea[z] = ml.c[z]->lex + eo;
+          g.Bs[z] = AS(z);
+          g.eb[z] = AE(z);
+          g.C[z] = S(z) + c1 + k.c0 * ld;
+          g.fail_flag[z] = flag(z);
+        }
+        return ozgemm(g, zb, s);
+      };
+      // (3)
+      if ((rc = half_update())) return rc;
+      // (4) S22 -= S21 L21^T + L21 S21^T, look-ahead split:
+      //   (i)  the next block's columns [c1, c2) (all rows >= c1, trapezoid) on the main
+      //        stream -- everything block b + 1's steps (1)-(3) read;
+      //   (ii) the lower tiles of [c2, N) on the side stream, under block b + 1's chain.
+      // (ii) of block b - 1 wrote tiles (i) touches: the main stream waits for it first.
+      if ((rc = slice_s21())) return rc;
+      if ((rc = join(s2, s))) return rc;
+      const int tn1 = std::min(kOuter, rt);  // tile columns of the next block
+      for (int pass = 0; pass < 2; ++pass) {
+        OzGemmArgs g = oz_base(ld, rt, tn1);
+        g.kblocks = (int)(k.kb / 32);
+        g.trap = 1;
+        for (int z = 0; z < zb; ++z) {
+          const int8_t* ls = ml.c[z]->lsl + (size_t)eo * kOzRowBytes;
+          const int* le = ml.c[z]->lex + eo;
+          g.As[z] = pass == 0 ? XS(z, b) : ls;
+          g.ea[z] = pass == 0 ? XE(z, b) : le;
+          g.Bs[z] = pass == 0 ? ls : XS(z, b);
+          g.eb[z] = pass == 0 ? le : XE(z, b);
+          g.C[z] = S(z) + c1 + c1 * ld;
+          g.fail_flag[z] = flag(z);
+        }
+        if ((rc = ozgemm(g, zb, s))) return rc;
+      }
+      if (rt > tn1) {
+        if ((rc = join(s, s2))) return rc;  // (ii) reads this block's S21 slices
+        const int t2r = rt - tn1;           // tiles of [c2, N)
+        const long long c2 = c1 + (long long)tn1 * kNB;
+        const size_t skip = (size_t)tn1 * kOzTileBytes;
+        for (int pass = 0; pass < 2; ++pass) {
+          OzGemmArgs g = oz_base(ld, t2r, 0);
+          g.kblocks = (int)(k.kb / 32);
+          g.lower = 1;
+          for (int z = 0; z < zb; ++z) {
+            const int8_t* ls = ml.c[z]->lsl + (size_t)eo * kOzRowBytes + skip;
+            const int* le = ml.c[z]->lex + eo + (long long)tn1 * kNB;
+            const int8_t* xs = XS(z, b) + skip;
+            const int* xe = XE(z, b) + (long long)tn1 * kNB;
+            g.As[z] = pass == 0 ? xs : ls;
+            g.ea[z] = pass == 0 ? xe : le;
+            g.Bs[z] = pass == 0 ? ls : xs;
+            g.eb[z] = pass == 0 ? le : xe;
+            g.C[z] = S(z) + c2 + c2 * ld;
+            g.fail_flag[z] = flag(z);
+          }
+          g.max_ctas = solve_ctas();
+          if ((rc = ozgemm(g, zb, bulk()))) return rc;
+        }
+      }
+      // (5): S21 itself (the GEMMs of (4) read its slices)
+      if ((rc = half_update())) return rc;
+    }
+    if ((rc = join(s2, s))) return rc;
+    // (6) deferred: S21 <- L22^-1 S21 for every block column, as the block-inverse forward
+    // sweep over row blocks b restricted to the columns [0, c0)
+    for (int b = 1; b < nb; ++b) {
+      const Blk k = blk(Nt, b);
+      const size_t woff = w_byte_offset(Nt, b);
+      const long long eoff = w_row_offset(Nt, b);
+      OzSliceArgs sa;  // B(n, kk) = X[c0 + kk, n], n < c0
+      std::memset(&sa, 0, sizeof(sa));
+      for (int z = 0; z < zb; ++z) {
+        sa.X[z] = S(z) + k.c0;
+        sa.slices[z] = XS(z, b);
+        sa.e[z] = XE(z, b);
+        sa.fail_flag[z] = flag(z);
+      }
+      sa.ld = ld;
+      sa.K = (int)k.kb;
+      if ((rc = slice(sa, k.c0, false, zb))) return rc;
+      OzGemmArgs t = oz_base(ld, Nt - k.t0, k.t0);  // rows [c0, N) x columns [0, c0)
+      t.kblocks = (int)(k.kb / 32);
+      t.alpha = 1.0;
+      t.beta0_tm = k.t1 - k.t0;  // the block's own rows are overwritten (D^-1 X)
+      for (int z = 0; z < zb; ++z) {
+        t.As[z] = ml.c[z]->wsl + woff;
+        t.ea[z] = ml.c[z]->wex + eoff;
+        t.Bs[z] = XS(z, b);
+        t.eb[z] = XE(z, b);
+        t.C[z] = S(z) + k.c0;
+        t.fail_flag[z] = flag(z);
+      }
+      t.max_ctas = solve_ctas();
+      if ((rc = ozgemm(t, zb, s))) return rc;
+    }
+    return MLE_OK;
+  }
+
   // DMMA path (MLE_FP64_GEMM=dmma): 128-wide inner steps + K = 512 outer updates.
   int solves_dmma(mle_ctx* const* cs, int m) {
     const long long ld = cs[0]->N;
@@ -1338,7 +1593,13 @@ int run_chunk(Item* items, int m) {
       gi.tab = it.P.tab_n > 0 ? (sigma_pass ? it.c->gtab_s : it.c->gtab_d) : nullptr;
       gi.write_sigma = sigma_pass ? 1 : 0;
       gi.write_derivs = sigma_pass ? 0 : 1;
+      if (!sigma_pass) it.c->deriv_lower = two_sided_gen(it.c);
     }
+    // the two-sided solves read only the lower tiles of the derivative matrices
+    ga.lower_only = (!sigma_pass && ng > 0) ? (items[0].c->deriv_lower ? 1 : 0) : 0;
+    if (!sigma_pass)
+      for (int b = 0; b < m; ++b)
+        if ((items[b].gen_derivs || items[b].spec) && !items[b].c->deriv_lower) ga.lower_only = 0;
     ga.ld = lead->N;
     ga.rows = lead->N;
     ga.n = (int)lead->n;

@@ -106,7 +106,8 @@ __device__ __forceinline__ void engine_element(const GenItem& it, const ThetaPar
   }
 }
 
-// kDerivs = 0: Sigma (lower tiles); 1: both derivative matrices (full storage, mirrored).
+// kDerivs = 0: Sigma (lower tiles); 1: both derivative matrices (full storage, mirrored;
+// lower tiles only with GenArgs.lower_only -- the two-sided solves read only those).
 //
 // Interior off-diagonal tiles (every index < n, i != j: nearly all of them) take a fast path.
 // Each warp evaluates compact 4 x 8 patches of the tile (4 consecutive rows x 8 consecutive
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       }
     }
   }
-  if (kDerivs && ti != tj) {
+  if (kDerivs && ti != tj && !a.lower_only) {
     __syncthreads();
     // mirrored tile (J, I): rows from tile J, columns from tile I
     const int i2 = tj * kGT + lane_row;

@@ -38,6 +38,7 @@ struct GenArgs {
   int n;              // number of locations
   int region;         // engine: 0 every lower tile; 1 tile columns < jcut; 2 tile columns >= jcut
   int jcut;           // in 32-wide generation tiles
+  int lower_only;     // derivative matrices: lower tiles only (no mirrored upper tiles)
 };
 
 // Operand layouts of op(B): B(n,k) at b[n + k*ldb] (kBNK) or b[k + n*ldb] (kBKN).
@@ -206,6 +207,9 @@ struct PanelReduceArgs {
 cudaError_t launch_linv_to_dinv_block(double* const* dinv, const double* const* linv,
                                       int k_begin, int tiles, int items, cudaStream_t s);
 cudaError_t launch_panel_identity(const PanelArgs& a, int items, cudaStream_t s);
+// upper triangle of a size x size block (column-major, ld) from its lower triangle, batched
+cudaError_t launch_mirror_lower(double* const* a, int items, long long ld, int size,
+                                cudaStream_t s);
 cudaError_t launch_panel_reduce(const PanelReduceArgs& r, int width, int items, cudaStream_t s);
 
 constexpr int kReduceBlocks = 148 * 4;

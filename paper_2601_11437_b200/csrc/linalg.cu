@@ -952,6 +952,39 @@ cudaError_t launch_linv_to_dinv_block(double* const* dinv, const double* const* 
   return cudaGetLastError();
 }
 
+// Upper triangle of one size x size block from its lower triangle (a[i + j ld] = a[j + i ld]
+// for i < j), batched: 32 x 32 sub-tiles through shared memory (coalesced on both sides).
+struct MirrorArgs {
+  double* a[kMaxGemm];
+};
+
+__global__ void __launch_bounds__(256) mirror_lower_kernel(MirrorArgs m, long long ld, int size) {
+  __shared__ double t[32][33];
+  const int tiles = size / 32;
+  const int bi = blockIdx.x % tiles, bj = blockIdx.x / tiles;  // source tile (bi >= bj)
+  if (bi < bj) return;
+  double* a = m.a[blockIdx.y];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8)  // element (32 bi + tx, 32 bj + r)
+    t[r][tx] = a[(32LL * bi + tx) + (32LL * bj + r) * ld];
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {  // destination (32 bj + tx, 32 bi + r) = source (bi.., bj..)
+    const int i = 32 * bj + tx, j = 32 * bi + r;
+    if (i < j) a[i + (long long)j * ld] = t[tx][r];
+  }
+}
+
+cudaError_t launch_mirror_lower(double* const* a, int items, long long ld, int size,
+                                cudaStream_t s) {
+  if (size % 32 || items > kMaxGemm) return cudaErrorInvalidValue;
+  MirrorArgs m;
+  for (int z = 0; z < items; ++z) m.a[z] = a[z];
+  const int tiles = size / 32;
+  mirror_lower_kernel<<<dim3((unsigned)(tiles * tiles), (unsigned)items), 256, 0, s>>>(m, ld,
+                                                                                    size);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) panel_identity_kernel(PanelArgs a) {
   double* S = a.p[blockIdx.y];
   const long long c0 = a.c0[blockIdx.y];

@@ -12,8 +12,9 @@
 //     int32 tensor-core GEMM, the S diagonals d accumulate in S TMEM accumulators)
 //   * the FP64 epilogue folds the diagonals exactly, scales (exact powers of two) and
 //     accumulates into C with one rounding.
-// S = 7 (55-bit operands, 28 products) for the Cholesky and the W_b construction, S = 6
-// (47-bit operands, 21 products) for the solve sweeps (accuracy study: DESIGN.md 4a).
+// S = 7 (55-bit operands, 28 products) everywhere by default; S = 6 (47-bit operands, 21
+// products) for the solve sweeps only with MLE_SOLVE_SLICES=6 (it flips a Fisher-BT stopping
+// decision on config 2: DESIGN.md 4a).
 //
 // Layouts.  Slices are written by oz_slice_kernel in the UMMA canonical K-major
 // SWIZZLE_NONE layout: for each 128-row tile and each 32-wide k block, S slices of a
@@ -301,6 +302,57 @@ struct OzTile {
   int z, tm, tn, part;
 };
 
+// Tile order: groups of kOzGroup consecutive row tiles.  Inside a group the tiles run down
+// the rows first, then across the columns, so the CTAs working at any moment share a few B
+// (column) panels and the group's A (row) panels -- kOzGroup x 128 rows x K x S bytes, 29 MB
+// at K = 512, S = 7 -- stay resident in L2 while the group sweeps all columns.  Each A panel
+// is then read from DRAM once per launch and each B panel once per group, instead of every
+// A panel once per column of tiles (253 GB of DRAM reads in one config-4 sweep GEMM whose
+// operands are 2 x 235 MB: ncu, profiles/r02_ozgemm_config4_summary.txt).
+constexpr int kOzGroup = 64;
+
+// Full / trapezoid grid (tiles_m x tiles_n): index b -> (tm, tn), grouped.
+__device__ __forceinline__ void oz_full_tile(int b, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int per_group = kOzGroup * tiles_n;
+  const int g = b / per_group;
+  const int m0 = g * kOzGroup;
+  const int gs = min(kOzGroup, tiles_m - m0);
+  const int l = b - g * per_group;
+  tm = m0 + l % gs;
+  tn = l / gs;
+}
+
+// Lower triangle (tm >= tn) of a tiles_m x tiles_m grid: index b -> (tm, tn), grouped.  Group
+// g holds rows [m0, m0 + gs): the full columns tn < m0 (gs tiles each), then the group's own
+// triangle column by column (column j: rows j .. gs - 1).
+__device__ __forceinline__ void oz_lower_tile(int b, int tiles_m, int& tm, int& tn) {
+  constexpr int G = kOzGroup;
+  int g = 0, base = 0;
+  for (;;) {
+    const int m0 = g * G, gs = min(G, tiles_m - m0);
+    const int size = gs * m0 + gs * (gs + 1) / 2;
+    if (b < base + size || m0 + gs >= tiles_m) {
+      int l = b - base;
+      if (l < gs * m0) {
+        tn = l / gs;
+        tm = m0 + l % gs;
+        return;
+      }
+      l -= gs * m0;
+      int j = 0;
+      while (l >= gs - j) {
+        l -= gs - j;
+        ++j;
+      }
+      tn = m0 + j;
+      tm = m0 + j + l;
+      return;
+    }
+    base += size;
+    ++g;
+  }
+}
+
 // Tile t of the launch -> coordinates; false if the tile is skipped (trapezoid / failed item).
 template <int kN>
 __device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, long long per_z, long long t,
@@ -311,14 +363,9 @@ __device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, long long per_z, lo
   const int b = (int)(r / kParts);
   o.part = (int)(r % kParts);
   if (g.lower) {
-    int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
-    while (I * (I + 1) / 2 > b) --I;
-    while ((I + 1) * (I + 2) / 2 <= b) ++I;
-    o.tm = I;
-    o.tn = b - I * (I + 1) / 2;
+    oz_lower_tile(b, g.tiles_m, o.tm, o.tn);
   } else {
-    o.tm = b % g.tiles_m;
-    o.tn = b / g.tiles_m;
+    oz_full_tile(b, g.tiles_m, g.tiles_n, o.tm, o.tn);
     if (g.tiles_m_z[o.z] > 0 && o.tm >= g.tiles_m_z[o.z]) return false;
   }
   if (g.trap && o.tm < o.tn) return false;

@@ -248,9 +248,13 @@ FIT_VARIANTS = {
 
 def make_fit(name, seed, variant=None):
     wl = WORKLOADS[name]
-    loc, z = _config_data(name, seed)
-    if variant is None:
-        np.savez_compressed(HERE / f"{name}_seed{seed}_data.npz", loc=loc, z=z)
+    npz = HERE / f"{name}_seed{seed}_data.npz"
+    if npz.exists():  # the committed field (other goldens were made on exactly these bytes)
+        d = np.load(npz)
+        loc, z = d["loc"], d["z"]
+    else:
+        loc, z = _config_data(name, seed)
+        np.savez_compressed(npz, loc=loc, z=z)
     data = ref.SpatialDataset(loc, z)
     opts = dict(FIT_VARIANTS[variant]) if variant else {}
     lo, hi = opts.pop("cube", (wl.theta0, wl.theta0))
