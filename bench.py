@@ -510,12 +510,14 @@ def ours_arm(args, rank, world, local_rank):
     if world == 1:
         data = m.SpatialDataset(loc, z, device=local_rank)
         kp = kernel_profile(data.engine(), wl.theta_true, wl.n, peaks)
+        tpath = REPO / "profiles" / "r02_ozgemm_traffic.json"
+        traffic = json.loads(tpath.read_text()) if tpath.exists() else {}
         launches_per_eval = data.engine().phase_times()["launches"]
         data.release()
         line["roofline"] = {
             "bound": "tensor", "unit": "TFLOP/s", "achieved": kp["ozgemm_alg_int8_tops"],
             "peak": kp["int8_peak_tops"], "frac": kp["ozgemm_alg_int8_tops"] / kp["int8_peak_tops"],
-            "traffic": None,
+            "traffic": traffic.get("traffic_bytes_per_launch"),
             "kernel": "ozgemm_persistent_kernel<64,7,2> (Ozaki FP64 GEMM on tcgen05.mma kind::i8)"
                       ": ALGORITHMIC FP64 flops of one config-4 eval_all's GEMM launches (block "
                       "sums of the solve path used, bench.gemm_algorithmic_flops) x 28 int8 "
@@ -523,7 +525,8 @@ def ours_arm(args, rank, world, local_rank):
                       "stream, kernel-profiling pass)",
             "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 dense = 2 x bf16 "
                            "dense; sustained: the GEMMs run for seconds inside a step)",
-            "traffic_note": "see profiles/r02_* (ncu of the same build)",
+            "traffic_source": traffic.get("source", "no ncu capture committed"),
+            "traffic_launch_ms": traffic.get("launch_ms"),
             "int8_pipe_microbench_tops": INT8_PIPE_TOPS,
             "fp64_equiv_tflops_algorithmic": kp["ozgemm_alg_fp64_equiv_tflops"],
             "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS}
