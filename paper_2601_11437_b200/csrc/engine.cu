@@ -433,10 +433,20 @@ size_t w_byte_offset(int Nt, int b) {
 }
 constexpr int kOzK = kOuter * kNB;               // K of every trailing update
 constexpr int kLookaheadCtas = 148 - 24;         // persistent grid of look-ahead updates
+int far_ctas();
 int lookahead_ctas() {  // MLE_LOOKAHEAD_CTAS: developer override (A/B timing)
   static const int v = [] {
     const char* e = std::getenv("MLE_LOOKAHEAD_CTAS");
     return e ? std::atoi(e) : kLookaheadCtas;
+  }();
+  return v;
+}
+// Grid cap of the Cholesky's far trailing update (ii-b), which runs under the next block's
+// inner chain; MLE_FAR_CTAS overrides (developer A/B timing).
+int far_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("MLE_FAR_CTAS");
+    return e ? std::atoi(e) : lookahead_ctas();
   }();
   return v;
 }
@@ -667,7 +677,7 @@ struct Launcher {
   // `to` waits for all work enqueued so far on `from`.
   int join(cudaStream_t from, cudaStream_t to) {
     if (from == to || from == nullptr || to == nullptr) return MLE_OK;
-    cudaEvent_t e = pool[next++ % npool];
+    cudaEvent_t e = pool[next++ % (npool - 1)];  // pool[npool - 1]: ev_near (potrf)
     CUDA_TRY(cudaEventRecord(e, from));
     CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
     return MLE_OK;
@@ -675,6 +685,7 @@ struct Launcher {
   cudaStream_t bulk() const { return s2 ? s2 : s; }
   cudaStream_t s3 = nullptr;   // inner look-ahead of the Cholesky (null: on s)
   bool outer_on_inner = false;  // (i1) of the last outer update was issued on s3
+  bool near_pending = false;    // (ii-a) of the last outer update recorded ev_near on s2
   cudaStream_t inner() const { return s3 ? s3 : s; }
   // W request of the Cholesky: build W_b of these contexts on stream ws as each outer block
   // of the factor becomes final (Ozaki path only).
@@ -797,7 +808,7 @@ struct Launcher {
       // trailing update with P = L[T, b0:b1], K = (b1 - b0) * 128
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
-      if ((rc = join(s2, s))) return rc;  // (ii) of the previous block touched these tiles
+      if (!cs[0]->lsl && (rc = join(s2, s))) return rc;  // (ii) of the previous block
       if (cs[0]->lsl) {
         // Ozaki path: slice P = L[b1:, b0:b1] once (kept for the solves), then C -= P P^T
         const int ob = b0 / kOuter;
@@ -814,6 +825,14 @@ struct Launcher {
         sa.K = kOzK;
         if ((rc = slice(sa, (long long)(Nt - b1) * kNB, true, m))) return rc;
         if ((rc = issue_w(ob))) return rc;
+        // (i) updates the next block's columns, which the previous block's (ii-a) updated
+        // too: wait for that part only (ev_near), not for the whole far update (ii-b)
+        if (near_pending && s2) {
+          CUDA_TRY(cudaStreamWaitEvent(s, pool[npool - 1], 0));
+          near_pending = false;
+        } else if ((rc = join(s2, s))) {
+          return rc;
+        }
         // (i) in two parts: the next block's first two tile columns on the main stream (its
         // first inner step reads only those), the other two on the inner stream, where that
         // step's own inner-stream work follows them in order
@@ -843,13 +862,33 @@ struct Launcher {
         }
         if (b2 >= Nt) continue;
         if ((rc = join(s, s2))) return rc;
-        OzGemmArgs u = oz_base(ld, Nt - b2, 0);        // (ii)
-        u.lower = 1;
-        u.max_ctas = lookahead_ctas();  // the next block's diagonal chain runs meanwhile
+        // (ii) in two parts on the side stream: (ii-a) the block after next's columns
+        // [b2, b3) -- all that block's (i) will wait for (ev_near) -- then (ii-b) the lower
+        // tiles of [b3, Nt).  Every tile sees the same sequence of updates as one launch.
+        const int b3 = std::min(Nt, b2 + kOuter);
+        OzGemmArgs ua = oz_base(ld, Nt - b2, b3 - b2);  // (ii-a)
+        ua.trap = 1;
+        ua.max_ctas = lookahead_ctas();  // the next block's diagonal chain runs meanwhile
         for (int b = 0; b < m; ++b) {
-          u.As[b] = u.Bs[b] = sa.slices[b] + (size_t)(b2 - b1) * kOzTileBytes;
-          u.ea[b] = u.eb[b] = sa.e[b] + (size_t)(b2 - b1) * kNB;
-          u.C[b] = mats[b] + u0 + u0 * ld;
+          ua.As[b] = ua.Bs[b] = sa.slices[b] + (size_t)(b2 - b1) * kOzTileBytes;
+          ua.ea[b] = ua.eb[b] = sa.e[b] + (size_t)(b2 - b1) * kNB;
+          ua.C[b] = mats[b] + u0 + u0 * ld;
+          ua.fail_flag[b] = cs[b]->fail_flag;
+        }
+        if ((rc = ozgemm(ua, m, bulk()))) return rc;
+        if (s2) {
+          CUDA_TRY(cudaEventRecord(pool[npool - 1], s2));
+          near_pending = true;
+        }
+        if (b3 >= Nt) continue;
+        OzGemmArgs u = oz_base(ld, Nt - b3, 0);        // (ii-b)
+        u.lower = 1;
+        u.max_ctas = far_ctas();
+        const long long u3 = (long long)b3 * kNB;
+        for (int b = 0; b < m; ++b) {
+          u.As[b] = u.Bs[b] = sa.slices[b] + (size_t)(b3 - b1) * kOzTileBytes;
+          u.ea[b] = u.eb[b] = sa.e[b] + (size_t)(b3 - b1) * kNB;
+          u.C[b] = mats[b] + u3 + u3 * ld;
           u.fail_flag[b] = cs[b]->fail_flag;
         }
         if ((rc = ozgemm(u, m, bulk()))) return rc;
@@ -1995,6 +2034,29 @@ int mle_kernel_stats(const mle_ctx* ctx, double* out) {
 int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out) {
   if (!ctx || !out) return fail(MLE_INVALID, "null argument");
   *out = ctx->cond_est;
+  return MLE_OK;
+}
+
+// Developer diagnostics (not in the public header): trace every potrf_diag_kernel CTA into a
+// device buffer of `cap` records of 6 int64 (enable = 1), or stop and copy the records to
+// `host` (enable = 0; *count = records written).
+int mle_diag_trace(int enable, long long cap, long long* host, long long* count) {
+  static long long* dbuf = nullptr;
+  static long long dcap = 0;
+  if (enable) {
+    if (dbuf) cudaFree(dbuf);
+    CUDA_TRY(cudaMalloc(&dbuf, sizeof(long long) * 6 * (size_t)cap));
+    dcap = cap;
+    CUDA_TRY(diag_trace_control(dbuf, (unsigned long long)cap, nullptr));
+    return MLE_OK;
+  }
+  unsigned long long n = 0;
+  CUDA_TRY(diag_trace_control(nullptr, 0, &n));
+  if (count) *count = (long long)n;
+  if (host && dbuf) {
+    const size_t m = (size_t)std::min<long long>((long long)n, dcap);
+    CUDA_TRY(cudaMemcpy(host, dbuf, sizeof(long long) * 6 * m, cudaMemcpyDeviceToHost));
+  }
   return MLE_OK;
 }
 

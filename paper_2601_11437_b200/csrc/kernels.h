@@ -207,6 +207,8 @@ struct PanelReduceArgs {
 cudaError_t launch_linv_to_dinv_block(double* const* dinv, const double* const* linv,
                                       int k_begin, int tiles, int items, cudaStream_t s);
 cudaError_t launch_panel_identity(const PanelArgs& a, int items, cudaStream_t s);
+// developer diagnostics: per-CTA globaltimer trace of potrf_diag_kernel (linalg.cu)
+cudaError_t diag_trace_control(long long* buf, unsigned long long cap, unsigned long long* count);
 // upper triangle of a size x size block (column-major, ld) from its lower triangle, batched
 cudaError_t launch_mirror_lower(double* const* a, int items, long long ld, int size,
                                 cudaStream_t s);

@@ -462,6 +462,18 @@ __device__ __forceinline__ void chol16_step(double (&v)[16], double (&rv)[16], d
 }
 }  // namespace
 
+// Developer diagnostics (mle_diag_trace): when g_diag_trace is set, thread 0 of every
+// potrf_diag_kernel CTA appends {globaltimer at entry, after the tile load, after the pivot
+// blocks, after the inverse, at exit, SM id} (6 x int64) to it; g_diag_trace_n counts records.
+__device__ long long* g_diag_trace = nullptr;
+__device__ unsigned long long g_diag_trace_n = 0;
+__device__ unsigned long long g_diag_trace_cap = 0;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 #ifdef MLE_DIAG_TIMING
 __device__ long long g_diag_clock[32];
 #define DIAG_T(slot) \
@@ -488,12 +500,16 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   double* A = a + (long long)k0 + (long long)k0 * ld;
+  long long* trace = g_diag_trace;
+  long long tr[5] = {0, 0, 0, 0, 0};
+  if (trace && tid == 0) tr[0] = gtimer();
   for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
     const int i = idx & (DT - 1), j = idx >> 7;
     Ls[j * DS + i] = A[i + (long long)j * ld];
   }
   if (tid == 0) s_fail = 0;
   __syncthreads();
+  if (trace && tid == 0) tr[1] = gtimer();
   DIAG_T(0)
 #define LS(i, j) Ls[(j) * DS + (i)]
 #pragma unroll 1
@@ -574,6 +590,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
     DIAG_T(3 + 3 * J)
   }
 
+  if (trace && tid == 0) tr[2] = gtimer();
   // ---- inverse X = L^-1 (dinv holds the reciprocal pivots) ----
   // (i) diagonal 16x16 blocks: thread per (block, column), forward substitution in registers
   if (tid < DT) {
@@ -640,14 +657,41 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
     __syncthreads();
   }
   DIAG_T(26)
+  if (trace && tid == 0) tr[3] = gtimer();
   // write back L (lower incl. diagonal) and Linv (dense 128x128, zero upper)
   for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
     const int i = idx & (DT - 1), j = idx >> 7;
     if (i >= j) A[i + (long long)j * ld] = LS(i, j);
     linv[idx] = XS(i, j);
   }
+  if (trace && tid == 0) {
+    tr[4] = gtimer();
+    const unsigned long long slot = atomicAdd(&g_diag_trace_n, 1ull);
+    if (slot < g_diag_trace_cap) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      long long* o = trace + 6 * slot;
+      for (int q = 0; q < 5; ++q) o[q] = tr[q];
+      o[5] = (long long)sm * 1000 + k0 / 128;  // SM id, tile index
+    }
+  }
 #undef XS
 #undef LS
+}
+
+// Diagnostics: start (buf != null, cap records) or stop (buf == null) the per-CTA trace of
+// potrf_diag_kernel; returns the number of records written since the last start in *count.
+cudaError_t diag_trace_control(long long* buf, unsigned long long cap, unsigned long long* count) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return e;
+  if (count) {
+    e = cudaMemcpyFromSymbol(count, g_diag_trace_n, sizeof(*count));
+    if (e != cudaSuccess) return e;
+  }
+  const unsigned long long zero = 0;
+  if ((e = cudaMemcpyToSymbol(g_diag_trace_n, &zero, sizeof(zero))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(g_diag_trace_cap, &cap, sizeof(cap))) != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(g_diag_trace, &buf, sizeof(buf));
 }
 
 cudaError_t init_diag_attributes() {

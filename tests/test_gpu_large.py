@@ -153,3 +153,16 @@ def test_config4_full_size_tables_vs_exact(gpu, config4):
     tb = _eval(gpu, loc, z, th, MLE_GEN_TABLE="1")
     ex = _eval(gpu, loc, z, th, MLE_GEN_TABLE="0")
     _agree(tb, ex, th, loc.shape[0], "tables_vs_exact")
+
+
+def test_config3_fit_vs_reference(gpu):
+    """The full config-3 Fisher-BT fit (n = 16,384; two-sided solves at this size) against the
+    unmodified reference's own fit (tests/golden/make_golden.py fit config3 0: hours of CPU):
+    identical call counts and termination, theta_hat within 1e-6, loglik at theta_hat 1e-10,
+    fisher_at_hat 1e-6."""
+    from test_gpu_fits import run_fit, check
+
+    if not (GOLDEN / "config3_seed0_fit.json").exists():
+        pytest.skip("reference config-3 fit golden not generated in this tree")
+    gold, res = run_fit(gpu, "config3", 0)
+    check(gold, res)
