@@ -531,6 +531,18 @@ def ours_arm(args, rank, world, local_rank):
             "fp64_equiv_tflops_algorithmic": kp["ozgemm_alg_fp64_equiv_tflops"],
             "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS}
         line["kernels"] = kp
+        gpath = REPO / "profiles" / "r02_gen_ncu.json"
+        if gpath.exists():  # ncu of the generation kernels (same build): FP64 pipe, L1, DRAM
+            g = json.loads(gpath.read_text())
+            line["kernels"]["generation_ncu"] = {
+                "fp64_pipe_pct_derivs": g["derivs_fp64_pipe_pct"],
+                "fp64_pipe_pct_sigma": g["sigma_fp64_pipe_pct"],
+                "l1tex_pct_derivs": g["derivs_l1tex_pct"],
+                "dram_write_over_algorithmic": g["derivs_dram_write_bytes"]
+                / g["derivs_algorithmic_bytes"],
+                "hbm_frac": kp["gen_gbs"] / peaks.get("hbm_gbs", 6548.5) if kp["gen_gbs"]
+                else None,
+                "bound": g["bound"], "source": g["source"]}
         line["kernels"]["launches_per_profiled_eval_all"] = launches_per_eval
         try:
             line["context"] = extra_single_gpu(m, local_rank)

@@ -20,6 +20,32 @@
 
 namespace mle {
 
+// Programmatic dependent launch for the Cholesky's latency-bound chain (diagonal tile ->
+// panel rows -> next tile's update -> next diagonal tile): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may be scheduled once its predecessor
+// signals (pdl_trigger, issued near the predecessor's end); it waits in pdl_wait until the
+// predecessor has completed and its writes are visible.  Without the attribute both are
+// no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+static cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 namespace {
 
 constexpr int BM = 128;
@@ -275,6 +301,7 @@ __global__ void __launch_bounds__(256) dgemm_small_kernel(GemmArgs g) {
   double* As = sm_small;              // [K][SAS]
   double* Bs = sm_small + SM_K * SAS;  // [K][SBS]
   const int z = blockIdx.z;
+  pdl_wait();
   if (__ldcv(g.fail_flag[z])) return;
   constexpr int CM = 128 / TM, CN = 128 / TN;  // CTAs per 128 x 128 tile
   const int sub = blockIdx.x % (CM * CN), tile = blockIdx.x / (CM * CN);
@@ -329,6 +356,7 @@ __global__ void __launch_bounds__(256) dgemm_small_kernel(GemmArgs g) {
           : "d"(a), "d"(b));
     }
   }
+  pdl_trigger();  // the chain's next kernel may be scheduled during the stores
 #pragma unroll
   for (int q = 0; q < PER_WARP; ++q) {
     double* p0 = C + om[q] + gq + (long long)(on[q] + 2 * tq) * g.ldc;
@@ -355,14 +383,16 @@ cudaError_t launch_gemm_small(const GemmArgs& g, int batch, cudaStream_t s, int 
   const long long tiles = (long long)g.tiles_m * g.tiles_n;
   if (tiles <= 0) return cudaSuccess;
   if (g.K > SM_K || g.K % 4) return cudaErrorInvalidValue;
+  GemmArgs ga = g;
+  void* args[] = {&ga};
   if (rows_only) {
     const dim3 grid((unsigned)(tiles * 8), 1, (unsigned)batch);
-    dgemm_small_kernel<16, 128><<<grid, 256, small_smem<16, 128>(), s>>>(g);
-  } else {
-    const dim3 grid((unsigned)(tiles * 16), 1, (unsigned)batch);
-    dgemm_small_kernel<32, 32><<<grid, 256, small_smem<32, 32>(), s>>>(g);
+    return launch_pdl((const void*)dgemm_small_kernel<16, 128>, grid, dim3(256),
+                      small_smem<16, 128>(), s, args);
   }
-  return cudaGetLastError();
+  const dim3 grid((unsigned)(tiles * 16), 1, (unsigned)batch);
+  return launch_pdl((const void*)dgemm_small_kernel<32, 32>, grid, dim3(256),
+                    small_smem<32, 32>(), s, args);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -485,6 +515,7 @@ __device__ long long g_diag_clock[32];
 __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
   const int item = blockIdx.x;
   int* fail_flag = da.fail_flag[item];
+  pdl_wait();
   if (*fail_flag) return;
   long long* fail_idx = da.fail_idx[item];
   double* a = da.a[item];
@@ -658,6 +689,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
   }
   DIAG_T(26)
   if (trace && tid == 0) tr[3] = gtimer();
+  pdl_trigger();  // the chain's next kernel may be scheduled during the write-back
   // write back L (lower incl. diagonal) and Linv (dense 128x128, zero upper)
   for (int idx = tid; idx < DT * DT; idx += DTHREADS) {
     const int i = idx & (DT - 1), j = idx >> 7;
@@ -700,8 +732,10 @@ cudaError_t init_diag_attributes() {
 }
 
 cudaError_t launch_potrf_diag(const DiagArgs& d, int items, cudaStream_t s) {
-  potrf_diag_kernel<<<items, DTHREADS, kDiagSmem, s>>>(d);
-  return cudaGetLastError();
+  DiagArgs da = d;
+  void* args[] = {&da};
+  return launch_pdl((const void*)potrf_diag_kernel, dim3(items), dim3(DTHREADS), kDiagSmem, s,
+                    args);
 }
 
 // ---------------------------------------------------------------------------------------
