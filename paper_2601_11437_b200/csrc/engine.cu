@@ -442,11 +442,13 @@ int lookahead_ctas() {  // MLE_LOOKAHEAD_CTAS: developer override (A/B timing)
   return v;
 }
 // Grid cap of the Cholesky's far trailing update (ii-b), which runs under the next block's
-// inner chain; MLE_FAR_CTAS overrides (developer A/B timing).
+// inner chain.  Uncapped (0: one CTA per SM): the far update is most of the factorization's
+// work, and capping it to leave SMs to the chain measured slower (config 4: 1.22 s at 148
+// CTAs, 1.28 s at 124, 1.47 s at 96; config 2 within noise).  MLE_FAR_CTAS overrides.
 int far_ctas() {
   static const int v = [] {
     const char* e = std::getenv("MLE_FAR_CTAS");
-    return e ? std::atoi(e) : lookahead_ctas();
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }

@@ -75,3 +75,20 @@ def test_two_sided_nugget(gpu, two_sided):
     scale = score_scale(th, len(z), ref[1], ref[2])
     assert np.all(np.abs(got[1] - ref[1]) <= 1e-9 * scale), (got[1], ref[1])
     np.testing.assert_allclose(got[2], ref[2], rtol=1e-9)
+
+
+def test_two_sided_batched_is_bit_identical_to_single(gpu, two_sided):
+    """Several datasets in one batched pass (mle_eval_batch: every launch covers all items)
+    on the two-sided path give each item's single-evaluation result bit for bit."""
+    sets = [config_data("config2", s) for s in range(3)]
+    engines = [gpu.Engine(loc, z) for loc, z in sets]
+    thetas = [np.array([1.0, 0.2, 1.5]), np.array([0.9, 0.15, 1.3]), np.array([1.1, 0.22, 1.7])]
+    batched = gpu.eval_batch(engines, thetas, [2, 2, 2])
+    for eng, th, (rc, piv, ll, g, f) in zip(engines, thetas, batched):
+        assert rc == 0
+        single = gpu.Engine(*sets[engines.index(eng)]).eval_all(th)
+        assert ll == single[0]
+        np.testing.assert_array_equal(g, single[1])
+        np.testing.assert_array_equal(f, single[2])
+    for e in engines:
+        e.close()
