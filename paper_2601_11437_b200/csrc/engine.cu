@@ -58,7 +58,7 @@ struct PassClock {
 // destroying 4 streams and ~30 events per context cost ~0.5 ms, i.e. ~1.5% of an end-to-end
 // config-2 step that builds five contexts).
 struct StreamSet {
-  cudaStream_t stream, side, inner, aux;
+  cudaStream_t stream, side, inner, aux, edge;
   cudaEvent_t ev[5], ev_der, spec_done, pool[16], clk[4];
 };
 std::mutex g_sets_mutex;
@@ -236,6 +236,15 @@ int solve_slices() {
   return (v && std::strcmp(v, "6") == 0) ? 6 : 7;
 }
 
+// MLE_BOUNDARY_SPLIT=1: the Cholesky's outer boundaries with the chain-first split
+// (boundary_split).  Off by default: bit-identical, but the batched config-2 loglik pass
+// measured 3.25 ms with it against 3.19 ms without (the off-chain rest of the boundary then
+// delays the block's last step and the next boundary's far update).
+bool use_boundary_split() {
+  const char* v = std::getenv("MLE_BOUNDARY_SPLIT");
+  return v && std::strcmp(v, "1") == 0;
+}
+
 bool use_speculation() {
   const char* v = std::getenv("MLE_SPECULATE");
   return !(v && std::strcmp(v, "0") == 0);
@@ -287,6 +296,7 @@ struct mle_ctx {
   cudaStream_t side = nullptr;    // look-ahead bulk trailing updates
   cudaStream_t inner = nullptr;   // inner (128-wide) look-ahead of the Cholesky
   cudaStream_t aux = nullptr;     // derivative generation concurrent with the Cholesky
+  cudaStream_t edge = nullptr;    // the Cholesky's outer-boundary work off the chain
   cudaEvent_t pool[kPoolEvents] = {};
   double* lx = nullptr;
   double* ly = nullptr;
@@ -679,7 +689,9 @@ struct Launcher {
   // `to` waits for all work enqueued so far on `from`.
   int join(cudaStream_t from, cudaStream_t to) {
     if (from == to || from == nullptr || to == nullptr) return MLE_OK;
-    cudaEvent_t e = pool[next++ % (npool - 1)];  // pool[npool - 1]: ev_near (potrf)
+    // reserved: pool[npool - 1] ev_near (potrf), pool[npool - 2] ev_t1 (inner_block),
+    // pool[npool - 3] ev_rest (boundary_split)
+    cudaEvent_t e = pool[next++ % (npool - 3)];
     CUDA_TRY(cudaEventRecord(e, from));
     CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
     return MLE_OK;
@@ -688,6 +700,12 @@ struct Launcher {
   cudaStream_t s3 = nullptr;   // inner look-ahead of the Cholesky (null: on s)
   bool outer_on_inner = false;  // (i1) of the last outer update was issued on s3
   bool near_pending = false;    // (ii-a) of the last outer update recorded ev_near on s2
+  bool t1_pending = false;      // the last inner step's (T1) recorded ev_t1 on s3
+  // potrf (Ozaki path): the block's last inner step computes only the panel's head rows (the
+  // next block's first two row tiles) on the chain; potrf issues the rest on the inner stream
+  bool split_last = false;
+  cudaStream_t s4 = nullptr;    // outer-boundary work off the chain (boundary_split)
+  bool rest_pending = false;    // boundary_split recorded ev_rest on s4: T2 waits for it
   cudaStream_t inner() const { return s3 ? s3 : s; }
   // W request of the Cholesky: build W_b of these contexts on stream ws as each outer block
   // of the factor becomes final (Ozaki path only).
@@ -695,9 +713,9 @@ struct Launcher {
   int nwreq = 0;
   int wks = 0;
   cudaStream_t ws = nullptr;
-  int issue_w(int b) {
+  int issue_w(int b, cudaStream_t after = nullptr) {
     if (nwreq == 0) return MLE_OK;
-    int rc = join(s, ws);
+    int rc = join(after ? after : s, ws);
     if (rc) return rc;
     const cudaStream_t keep = s;
     s = ws;
@@ -767,16 +785,28 @@ struct Launcher {
         t.alpha = -1.0; t.beta = 1.0;
         return small ? gemm_small(t, m, st, 0) : gemm(t, kBNK, m, st);
       };
-      // the previous step's bulk work on the inner stream (not at a block's first step when
-      // that stream only holds the last outer update's far columns, which it does not read)
+      // What this step reads from the previous step's inner-stream work: only (T1), the
+      // panel row and the two tiles the chain needs next (ev_t1); at a block's first step the
+      // inner stream holds only the last outer update's far columns, which it does not read.
+      // The whole panel of the block's last step is read by the trailing update: all of it.
       if (k == b0 && outer_on_inner) {
         outer_on_inner = false;
-      } else if ((rc = join(s3, s))) {
-        return rc;
+        t1_pending = false;
+      } else if (t1_pending && wcols > 0) {
+        CUDA_TRY(cudaStreamWaitEvent(s, pool[npool - 2], 0));
+        t1_pending = false;
+      } else {
+        t1_pending = false;
+        if ((rc = join(s3, s))) return rc;
       }
       if (wcols == 0) {
-        // last tile of the outer block: the whole panel (read by the trailing update)
-        if ((rc = panel_gemm(rem, 0, s))) return rc;
+        // last tile of the outer block: the whole panel (read by the trailing update); with
+        // split_last only its head rows here (potrf issues the rest off the chain)
+        if (split_last && s3 && s4 && rem > 3) {
+          if ((rc = panel_gemm(3, 0, s, true))) return rc;
+        } else if ((rc = panel_gemm(rem, 0, s))) {
+          return rc;
+        }
         continue;
       }
       // Inner look-ahead: the critical chain to the next diagonal tile is only
@@ -788,12 +818,149 @@ struct Launcher {
       if ((rc = update(0, 1, 0, 1, true, s, true))) return rc;
       if (rem > 1) {
         cudaStream_t in = inner();
-        if ((rc = panel_gemm(rem - 1, 1, in))) return rc;
-        // rows >= k+2 of the block's remaining columns k+1.. (one launch, lower trapezoid)
-        if ((rc = update(1, rem - 1, 0, wcols, true, in, false, 1))) return rc;
+        // (T1) what the next step's chain reads: panel row k+2 and its update of tiles
+        // (k+2, k+1) and (k+2, k+2) (within the block), on small-tile CTAs, then ev_t1
+        if ((rc = panel_gemm(1, 1, in, true))) return rc;
+        if ((rc = update(1, 1, 0, std::min(2, wcols), false, in, true))) return rc;
+        if (in != s) {
+          CUDA_TRY(cudaEventRecord(pool[npool - 2], in));
+          t1_pending = true;
+        }
+        if (rest_pending) {  // T2 reads rows the boundary's rest (on s4) updates
+          CUDA_TRY(cudaStreamWaitEvent(in, pool[npool - 3], 0));
+          rest_pending = false;
+        }
+        // (T2) the rest: panel rows >= k+3 and their update of the block's remaining columns
+        // (one launch, lower trapezoid).  Same per-tile arithmetic as one launch: the small
+        // and large DMMA kernels use the same k order (bit-identical results).
+        if (rem > 2) {
+          if ((rc = panel_gemm(rem - 2, 2, in))) return rc;
+          if ((rc = update(2, rem - 2, 0, wcols, true, in, false, 2))) return rc;
+        }
       }
     }
+    t1_pending = false;
     return join(s3, s);
+  }
+
+  // Outer-block boundary with the next block's chain first (Ozaki path, inner and edge
+  // streams present, more than three row tiles below).  The next block's first inner step
+  // (its chain and its T1) reads only the trailing update's head: tiles rows [b1, b1+3) x
+  // columns [b1, b1+3) (lower), which need only the panel's three head row tiles:
+  //   main:  [head panel rows (inner_block)] -> slice them -> wait ev_near -> (i0h) the six
+  //          head tiles, K = 512 -> the next block's inner chain starts;
+  //   edge:  the rest of the panel (rows >= b1+3) -> slice it -> W_b -> (i0r) / (i1r):
+  //          rows >= b1+3 of the next block's columns -> ev_rest (the first inner step's T2
+  //          waits for it) -> (ii-a) / (ii-b) go to the side stream after it.
+  // Every tile sees the same updates in the same order as the unsplit boundary (bit-identical,
+  // tools/boundary_ab.py).
+  int boundary_split(mle_ctx* const* cs, double* const* mats, int m, int b0, int b1, int b2) {
+    const long long ld = cs[0]->N;
+    const int Nt = cs[0]->Nt;
+    const int ob = b0 / kOuter;
+    const long long eo = oz_panel_row_offset(Nt, ob);
+    const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
+    constexpr int hr = 3;                      // head row tiles
+    const int hc = std::min(hr, b2 - b1);      // head columns (within the next block)
+    const int i0 = std::min(2, b2 - b1);
+    int rc;
+    OzSliceArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    for (int b = 0; b < m; ++b) {
+      sa.X[b] = mats[b] + t0 + c0 * ld;
+      sa.slices[b] = cs[b]->lsl + (size_t)eo * kOzRowBytes;
+      sa.e[b] = cs[b]->lex + eo;
+      sa.fail_flag[b] = cs[b]->fail_flag;
+    }
+    sa.ld = ld;
+    sa.K = kOzK;
+    if ((rc = slice(sa, (long long)hr * kNB, true, m, s))) return rc;
+    if (near_pending && s2) {
+      CUDA_TRY(cudaStreamWaitEvent(s, pool[npool - 1], 0));
+      near_pending = false;
+    } else if ((rc = join(s2, s))) {
+      return rc;
+    }
+    {  // (i0h): rows [b1, b1 + hr) x columns [b1, b1 + hc), lower
+      OzGemmArgs t = oz_base(ld, hr, hc);
+      t.trap = 1;
+      for (int b = 0; b < m; ++b) {
+        t.As[b] = t.Bs[b] = sa.slices[b];
+        t.ea[b] = t.eb[b] = sa.e[b];
+        t.C[b] = mats[b] + t0 + t0 * ld;
+        t.fail_flag[b] = cs[b]->fail_flag;
+      }
+      if ((rc = ozgemm(t, m, s))) return rc;
+    }
+    if ((rc = join(s, s4))) return rc;
+    {  // the rest of the last column's panel (rows >= b1 + hr), in place
+      const int k = b1 - 1;
+      const long long k0 = (long long)k * kNB;
+      GemmArgs g = gemm_base();
+      for (int b = 0; b < m; ++b) {
+        double* panel = mats[b] + (t0 + (long long)hr * kNB) + k0 * ld;
+        g.A[b] = panel;
+        g.B[b] = cs[b]->linv + (size_t)k * kNB * kNB;
+        g.C[b] = panel;
+        g.fail_flag[b] = cs[b]->fail_flag;
+      }
+      g.lda = ld; g.ldb = kNB; g.ldc = ld;
+      g.tiles_m = Nt - b1 - hr; g.tiles_n = 1; g.alpha = 1.0; g.beta = 0.0; g.wide = 1;
+      if ((rc = gemm(g, kBNK, m, s4))) return rc;
+    }
+    OzSliceArgs sr = sa;
+    for (int b = 0; b < m; ++b) {
+      sr.X[b] = sa.X[b] + (long long)hr * kNB;
+      sr.slices[b] = sa.slices[b] + (size_t)hr * kOzTileBytes;
+      sr.e[b] = sa.e[b] + (long long)hr * kNB;
+    }
+    if ((rc = slice(sr, (long long)(Nt - b1 - hr) * kNB, true, m, s4))) return rc;
+    if ((rc = issue_w(ob, s4))) return rc;
+    {  // (i0r) + (i1r): rows >= b1 + hr of all the next block's columns (none above the
+       // diagonal: the columns end at b1 + 4 <= b1 + hr + 1)
+      OzGemmArgs t = oz_base(ld, Nt - b1 - hr, b2 - b1);
+      for (int b = 0; b < m; ++b) {
+        t.As[b] = sr.slices[b];
+        t.ea[b] = sr.e[b];
+        t.Bs[b] = sa.slices[b];
+        t.eb[b] = sa.e[b];
+        t.C[b] = mats[b] + (t0 + (long long)hr * kNB) + t0 * ld;
+        t.fail_flag[b] = cs[b]->fail_flag;
+      }
+      if ((rc = ozgemm(t, m, s4))) return rc;
+    }
+    (void)i0;
+    CUDA_TRY(cudaEventRecord(pool[npool - 3], s4));
+    rest_pending = true;
+    outer_on_inner = true;  // the next block's first step must not wait for the inner stream
+    if (b2 >= Nt) return MLE_OK;
+    if ((rc = join(s4, s2))) return rc;  // (ii) reads the whole panel's slices
+    const long long u0 = (long long)b2 * kNB;
+    const int b3 = std::min(Nt, b2 + kOuter);
+    OzGemmArgs ua = oz_base(ld, Nt - b2, b3 - b2);  // (ii-a)
+    ua.trap = 1;
+    ua.max_ctas = lookahead_ctas();
+    for (int b = 0; b < m; ++b) {
+      ua.As[b] = ua.Bs[b] = sa.slices[b] + (size_t)(b2 - b1) * kOzTileBytes;
+      ua.ea[b] = ua.eb[b] = sa.e[b] + (size_t)(b2 - b1) * kNB;
+      ua.C[b] = mats[b] + u0 + u0 * ld;
+      ua.fail_flag[b] = cs[b]->fail_flag;
+    }
+    if ((rc = ozgemm(ua, m, bulk()))) return rc;
+    CUDA_TRY(cudaEventRecord(pool[npool - 1], s2));
+    near_pending = true;
+    if (b3 >= Nt) return MLE_OK;
+    OzGemmArgs u = oz_base(ld, Nt - b3, 0);  // (ii-b)
+    u.lower = 1;
+    u.max_ctas = far_ctas();
+    const long long u3 = (long long)b3 * kNB;
+    for (int b = 0; b < m; ++b) {
+      u.As[b] = u.Bs[b] = sa.slices[b] + (size_t)(b3 - b1) * kOzTileBytes;
+      u.ea[b] = u.eb[b] = sa.e[b] + (size_t)(b3 - b1) * kNB;
+      u.C[b] = mats[b] + u3 + u3 * ld;
+      u.fail_flag[b] = cs[b]->fail_flag;
+    }
+    return ozgemm(u, m, bulk());
   }
 
   int potrf(mle_ctx* const* cs, double* const* mats, const long long* n_aug, int m) {
@@ -802,7 +969,10 @@ struct Launcher {
     int rc;
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
       const int b1 = std::min(Nt, b0 + kOuter);
+      split_last = cs[0]->lsl && s3 && s2 && s4 && Nt - b1 > 3 && use_boundary_split();
       if ((rc = inner_block(cs, mats, n_aug, m, b0, b1))) return rc;
+      const bool split = split_last;
+      split_last = false;
       if (b1 >= Nt) {
         if ((rc = issue_w(b0 / kOuter))) return rc;
         continue;
@@ -811,6 +981,10 @@ struct Launcher {
       const int b2 = std::min(Nt, b1 + kOuter);
       const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB, u0 = (long long)b2 * kNB;
       if (!cs[0]->lsl && (rc = join(s2, s))) return rc;  // (ii) of the previous block
+      if (split) {
+        if ((rc = boundary_split(cs, mats, m, b0, b1, b2))) return rc;
+        continue;
+      }
       if (cs[0]->lsl) {
         // Ozaki path: slice P = L[b1:, b0:b1] once (kept for the solves), then C -= P P^T
         const int ob = b0 / kOuter;
@@ -1568,7 +1742,10 @@ int run_chunk(Item* items, int m) {
   cudaStream_t s = lead->stream;
   const bool lookahead = !lead->kprof && use_lookahead();
   Launcher run{s, lookahead ? lead->side : nullptr, lead->pool, kPoolEvents};
-  if (lookahead) run.s3 = lead->inner;
+  if (lookahead) {
+    run.s3 = lead->inner;
+    run.s4 = lead->edge;
+  }
   if (lead->kprof) run.prof = lead;
   cudaStream_t aux = lead->kprof ? s : lead->aux;  // profiling: everything serialised
   PassClock* pc = &lead->pass_clock;
@@ -2137,6 +2314,7 @@ static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n,
       c->side = st.side;
       c->inner = st.inner;
       c->aux = st.aux;
+      c->edge = st.edge;
       for (int i = 0; i < 5; ++i) c->ev[i] = st.ev[i];
       c->ev_der = st.ev_der;
       c->spec_done = st.spec_done;
@@ -2155,6 +2333,7 @@ static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n,
     CTX_TRY(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_high));
     CTX_TRY(cudaStreamCreateWithPriority(&c->inner, cudaStreamNonBlocking, prio_high));
     CTX_TRY(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_low));
+    CTX_TRY(cudaStreamCreateWithPriority(&c->edge, cudaStreamNonBlocking, prio_high));
     for (auto& e : c->ev) CTX_TRY(cudaEventCreate(&e));
     CTX_TRY(cudaEventCreateWithFlags(&c->ev_der, cudaEventDisableTiming));
     CTX_TRY(cudaEventCreateWithFlags(&c->spec_done, cudaEventDisableTiming));
@@ -2234,18 +2413,21 @@ void mle_ctx_destroy(mle_ctx* c) {
   if (c->h_theta) dfree(c->h_theta);
   if (c->h_res) dfree(c->h_res);
   for (auto& e : c->kev) cudaEventDestroy(e);
-  bool complete = c->stream && c->side && c->inner && c->aux && c->ev_der && c->spec_done;
+  bool complete = c->stream && c->side && c->inner && c->aux && c->edge && c->ev_der &&
+                  c->spec_done;
   for (auto& e : c->ev) complete = complete && e;
   for (auto& e : c->pool) complete = complete && e;
   const bool idle = complete && cudaStreamSynchronize(c->side) == cudaSuccess &&
                     cudaStreamSynchronize(c->inner) == cudaSuccess &&
-                    cudaStreamSynchronize(c->aux) == cudaSuccess;
+                    cudaStreamSynchronize(c->aux) == cudaSuccess &&
+                    cudaStreamSynchronize(c->edge) == cudaSuccess;
   if (idle) {  // hand the stream set to the next context on this device
     StreamSet st;
     st.stream = c->stream;
     st.side = c->side;
     st.inner = c->inner;
     st.aux = c->aux;
+    st.edge = c->edge;
     for (int i = 0; i < 5; ++i) st.ev[i] = c->ev[i];
     st.ev_der = c->ev_der;
     st.spec_done = c->spec_done;
@@ -2270,6 +2452,7 @@ void mle_ctx_destroy(mle_ctx* c) {
     if (c->side) cudaStreamDestroy(c->side);
     if (c->inner) cudaStreamDestroy(c->inner);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->edge) cudaStreamDestroy(c->edge);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;

@@ -66,3 +66,17 @@ def test_no_gpu_fails_loudly():
     obj = m.LikelihoodObjective(data)
     with pytest.raises(nat.NativeError):  # CUDA failures are never mapped to -inf
         obj.loglik([1.0, 0.1, 0.5])
+
+
+def test_sharded_entry_points_reject_null_handles():
+    """The rank-sharded C-ABI (mle_dctx_*) validates its handle before any device work."""
+    out = np.zeros(32)
+    h = ctypes.c_void_p()
+    assert nat.lib.mle_dctx_set_async(None, 1) == nat.MLE_INVALID
+    assert nat.lib.mle_dctx_stream(None, ctypes.byref(h)) == nat.MLE_INVALID
+    assert nat.lib.mle_dctx_wcache(None, 1) == nat.MLE_INVALID
+    assert nat.lib.mle_dctx_update_range(None, 0, None, 0, 1) == nat.MLE_INVALID
+    assert nat.lib.mle_dctx_right_range(None, 0, None, None, 0, 1) == nat.MLE_INVALID
+    assert nat.lib.mle_dctx_panel_partials(None, nat.as_ptr(out)) == nat.MLE_INVALID
+    assert nat.lib.mle_dctx_create(nat.as_ptr(np.zeros((2, 2))), nat.as_ptr(np.zeros(2)), 2, 0,
+                                   0.0, 2, 2, ctypes.byref(h)) == nat.MLE_INVALID  # rank >= world
