@@ -350,8 +350,38 @@ def reference_arm(args, rank, world):
                              "sample": sample},
             "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "detail": s0}
+            "detail": s0,
+            "measured_reference": measured_reference()}
     print(json.dumps(line), flush=True)
+
+
+def measured_reference():
+    """What the unmodified reference itself measured where it could run (committed goldens,
+    made by tests/golden/make_golden.py in the build container, 8 cores): the calibration
+    points next to the extrapolation above."""
+    out = {}
+    path = GOLDEN / "config3_evals.json"
+    if path.exists():
+        recs = json.loads(path.read_text())
+        out["config3_log_likelihood_plus_grad_and_fisher_s"] = [r.get("cpu_wall_s")
+                                                                for r in recs]
+    fits = []
+    for seed in range(5):
+        fp = GOLDEN / f"config2_seed{seed}_fit.json"
+        if fp.exists():
+            f = json.loads(fp.read_text())
+            fits.append({"seed": seed, "seconds": f["cpu_wall_s"], "grad_calls": f["grad_calls"],
+                         "it_per_s": f["grad_calls"] / f["cpu_wall_s"]})
+    if fits:
+        out["config2_full_fits"] = fits
+    fp = GOLDEN / "config3_seed0_fit.json"
+    if fp.exists():
+        f = json.loads(fp.read_text())
+        out["config3_full_fit"] = {"seconds": f["cpu_wall_s"], "grad_calls": f["grad_calls"],
+                                   "it_per_s": f["grad_calls"] / f["cpu_wall_s"]}
+    out["note"] = ("reference package (maternmle, numpy/scipy/OpenBLAS) on 8 build-container "
+                   "cores; generation single-threaded")
+    return out
 
 
 # ----------------------------------------------------------------------------- GPU side

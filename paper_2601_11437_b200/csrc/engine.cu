@@ -862,7 +862,6 @@ struct Launcher {
     const long long c0 = (long long)b0 * kNB, t0 = (long long)b1 * kNB;
     constexpr int hr = 3;                      // head row tiles
     const int hc = std::min(hr, b2 - b1);      // head columns (within the next block)
-    const int i0 = std::min(2, b2 - b1);
     int rc;
     OzSliceArgs sa;
     std::memset(&sa, 0, sizeof(sa));
@@ -929,7 +928,6 @@ struct Launcher {
       }
       if ((rc = ozgemm(t, m, s4))) return rc;
     }
-    (void)i0;
     CUDA_TRY(cudaEventRecord(pool[npool - 3], s4));
     rest_pending = true;
     outer_on_inner = true;  // the next block's first step must not wait for the inner stream
