@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(16 * kR) oz_slice_kernel(OzSliceArgs sa) {
   }
 }
 
+#ifndef OZ_STORE  // C store of the epilogue (developer A/B: __stcs streaming, __stwt ...)
+#define OZ_STORE __stcg
+#endif
+
 // Persistent GEMM: one CTA per SM walks the tile list (tile t, t + gridDim.x, ...).
 // The kernel is bound by the ingress of the slices (L2 -> SMEM), not by the tensor pipe: a
 // 128 x kN tile needs S x 32 (128 + kN) bytes per k block for S(S+1)/2 x 128 x kN x 32 MACs,
@@ -289,7 +293,11 @@ template <int kN, int kS>
 struct OzP {
   static constexpr int kAStage = kS * OZ_BLK;
   static constexpr int kStage = kAStage + kS * kN * OZ_KB;
-  static constexpr int kStages = (220 * 1024) / kStage > 8 ? 8 : (220 * 1024) / kStage;
+#ifndef OZ_MAX_STAGES  // developer A/B (Makefile EXTRA=-DOZ_MAX_STAGES=...)
+#define OZ_MAX_STAGES 8
+#endif
+  static constexpr int kStages0 = (220 * 1024) / kStage > 8 ? 8 : (220 * 1024) / kStage;
+  static constexpr int kStages = kStages0 < OZ_MAX_STAGES ? kStages0 : OZ_MAX_STAGES;
   static constexpr int kSmem = kStages * kStage;
   static constexpr int kAcc = kS * kN;              // TMEM columns per accumulator set
   static constexpr int kSets = kN == 32 ? 2 : 1;
@@ -552,7 +560,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       // C prefetch before the accumulator wait: all of the thread's columns at kN = 32, the
       // first 16 at kN = 64 (all 32 would spill); the rest is read after TMEM is released,
       // overlapping the next tile's MMAs
-      constexpr int kPre = kN == 32 ? kCols : 16;
+#ifndef OZ_PRE64  // C columns prefetched before the accumulator wait at kN = 64 (A/B)
+#define OZ_PRE64 16
+#endif
+      constexpr int kPre = kN == 32 ? kCols : OZ_PRE64;
       double cv[kPre > 0 ? kPre : 1];
 #pragma unroll
       for (int j = 0; j < kPre; ++j) cv[j] = acc_c ? __ldcg(C + (long long)j * g.ldc) : 0.0;
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
                                 : (acc_c ? __ldcg(C + (long long)(c0 + j) * g.ldc) : 0.0);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          __stcg(C + (long long)(c0 + j) * g.ldc,
+          OZ_STORE(C + (long long)(c0 + j) * g.ldc,
                  cw[j] + (acc[c0 + j] * s_row) * pow2i(__ldg(eb + c0 + j)));
       }
       ++local;

@@ -180,3 +180,34 @@ def test_fit_many_keeps_going_past_a_failed_fit(gpu):
     check(fit_golden("config1", 0), out[0])
     with pytest.raises(gpu.InitializationFailed):
         gpu.fit_many(sets, cfg, groups=1)
+
+
+def test_loglik_many_rounds_when_helpers_are_capped(gpu, monkeypatch):
+    """With the helper-context memory cap below one context, the independent logliks run in
+    rounds on the dataset's own engine: same values, same counts."""
+    loc, z = config_data("config1", 0)
+    cands = [c.as_array() for c in gpu.l9_candidates(gpu.MaternParams(0.3, 0.03, 0.4),
+                                                      gpu.MaternParams(1.5, 0.2, 2.2))]
+    monkeypatch.setenv("MLE_HELPER_BYTES", "1")
+    capped = gpu.LikelihoodObjective(gpu.SpatialDataset(loc, z))
+    got = capped.loglik_many(cands)
+    assert capped.data.engines(9) == [capped.data.engine()]  # no helpers under the cap
+    monkeypatch.delenv("MLE_HELPER_BYTES")
+    free = gpu.LikelihoodObjective(gpu.SpatialDataset(loc, z))
+    assert got == free.loglik_many(cands)
+    assert capped.loglik_calls == free.loglik_calls == 9
+
+
+def test_fit_many_default_cube_batches_l9(gpu):
+    """fit_many with the paper's default start cube: the nine distinct L9 candidates of every
+    fit run as batched passes (LOGLIK_MANY over helper contexts); each fit is bit-identical to
+    running it alone."""
+    lo, hi = gpu.MaternParams(0.01, 0.01, 0.01), gpu.MaternParams(5.0, 5.0, 2.0)
+    cfg = gpu.FisherBTConfig(theta_lower=lo, theta_upper=hi)
+    sets = [gpu.SpatialDataset(*config_data("config1", 0)) for _ in range(2)]
+    alone = gpu.fisher_bt(gpu.SpatialDataset(*config_data("config1", 0)), cfg)
+    stats = []
+    both = gpu.fit_many(sets, cfg, groups=1, coordinator_out=stats)
+    for r in both:
+        np.testing.assert_array_equal(r.theta_hat.as_array(), alone.theta_hat.as_array())
+        assert (r.grad_calls, r.loglik_calls) == (alone.grad_calls, alone.loglik_calls)
