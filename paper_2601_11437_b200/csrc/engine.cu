@@ -245,6 +245,15 @@ bool use_boundary_split() {
   return v && std::strcmp(v, "1") == 0;
 }
 
+// MLE_INNER_DEEP=1: the inner steps' T2 split once more (T2a row k+3 on the inner stream,
+// T2b on the edge stream).  Off by default: bit-identical, but the batched config-2 loglik
+// pass measured 3.28 ms with it against 3.19 ms without (the bulk work it moves off the chain
+// is then waited for at the outer boundary instead).
+bool use_inner_deep() {
+  const char* v = std::getenv("MLE_INNER_DEEP");
+  return v && std::strcmp(v, "1") == 0;
+}
+
 bool use_speculation() {
   const char* v = std::getenv("MLE_SPECULATE");
   return !(v && std::strcmp(v, "0") == 0);
@@ -690,8 +699,8 @@ struct Launcher {
   int join(cudaStream_t from, cudaStream_t to) {
     if (from == to || from == nullptr || to == nullptr) return MLE_OK;
     // reserved: pool[npool - 1] ev_near (potrf), pool[npool - 2] ev_t1 (inner_block),
-    // pool[npool - 3] ev_rest (boundary_split)
-    cudaEvent_t e = pool[next++ % (npool - 3)];
+    // pool[npool - 3] ev_rest (boundary_split), pool[npool - 4] ev_t2b (inner_block)
+    cudaEvent_t e = pool[next++ % (npool - 4)];
     CUDA_TRY(cudaEventRecord(e, from));
     CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
     return MLE_OK;
@@ -704,7 +713,9 @@ struct Launcher {
   // potrf (Ozaki path): the block's last inner step computes only the panel's head rows (the
   // next block's first two row tiles) on the chain; potrf issues the rest on the inner stream
   bool split_last = false;
-  cudaStream_t s4 = nullptr;    // outer-boundary work off the chain (boundary_split)
+  cudaStream_t s4 = nullptr;    // edge stream: boundary_split's rest or the inner T2b
+  bool t2b_pending = false;     // the last inner step's T2b recorded ev_t2b on s4
+  bool split_last_any = false;  // boundary_split in use this pass (it owns s4)
   bool rest_pending = false;    // boundary_split recorded ev_rest on s4: T2 waits for it
   cudaStream_t inner() const { return s3 ? s3 : s; }
   // W request of the Cholesky: build W_b of these contexts on stream ws as each outer block
@@ -797,6 +808,10 @@ struct Launcher {
         t1_pending = false;
       } else {
         t1_pending = false;
+        if (t2b_pending) {  // the inner stream catches up with the edge stream first
+          CUDA_TRY(cudaStreamWaitEvent(s3 ? s3 : s, pool[npool - 4], 0));
+          t2b_pending = false;
+        }
         if ((rc = join(s3, s))) return rc;
       }
       if (wcols == 0) {
@@ -830,16 +845,43 @@ struct Launcher {
           CUDA_TRY(cudaStreamWaitEvent(in, pool[npool - 3], 0));
           rest_pending = false;
         }
-        // (T2) the rest: panel rows >= k+3 and their update of the block's remaining columns
-        // (one launch, lower trapezoid).  Same per-tile arithmetic as one launch: the small
-        // and large DMMA kernels use the same k order (bit-identical results).
-        if (rem > 2) {
+        // (T2) the rest: panel rows >= k+3 and their update of the block's remaining columns.
+        // Same per-tile arithmetic as one launch: the small and large DMMA kernels use the
+        // same k order (bit-identical results).  With the edge stream and the boundary split
+        // off, T2 is split once more so that the next step's T1 (behind it on the inner
+        // stream) waits only for row k+3:
+        //   (T2a) panel row k+3 and its tiles, inner stream, after the previous step's T2b;
+        //   (T2b) rows >= k+4, edge stream (ev_t2b): the chain is two steps ahead of it.
+        const bool deep = s4 && !split_last_any && in != s && use_inner_deep();
+        if (rem > 2 && deep) {
+          if (t2b_pending) {
+            CUDA_TRY(cudaStreamWaitEvent(in, pool[npool - 4], 0));
+            t2b_pending = false;
+          }
+          if ((rc = panel_gemm(1, 2, in, true))) return rc;
+          if ((rc = update(2, 1, 0, std::min(3, wcols), false, in, true))) return rc;
+          if (rem > 3) {
+            if ((rc = join(in, s4))) return rc;
+            if ((rc = panel_gemm(rem - 3, 3, s4))) return rc;
+            if ((rc = update(3, rem - 3, 0, wcols, true, s4, false, 3))) return rc;
+            CUDA_TRY(cudaEventRecord(pool[npool - 4], s4));
+            t2b_pending = true;
+          }
+        } else if (rem > 2) {
+          if (t2b_pending) {
+            CUDA_TRY(cudaStreamWaitEvent(in, pool[npool - 4], 0));
+            t2b_pending = false;
+          }
           if ((rc = panel_gemm(rem - 2, 2, in))) return rc;
           if ((rc = update(2, rem - 2, 0, wcols, true, in, false, 2))) return rc;
         }
       }
     }
     t1_pending = false;
+    if (t2b_pending) {  // everything of the block is in L[:, b0:b1] for the caller
+      CUDA_TRY(cudaStreamWaitEvent(s3 ? s3 : s, pool[npool - 4], 0));
+      t2b_pending = false;
+    }
     return join(s3, s);
   }
 
@@ -968,6 +1010,7 @@ struct Launcher {
     for (int b0 = 0; b0 < Nt; b0 += kOuter) {
       const int b1 = std::min(Nt, b0 + kOuter);
       split_last = cs[0]->lsl && s3 && s2 && s4 && Nt - b1 > 3 && use_boundary_split();
+      split_last_any = use_boundary_split();
       if ((rc = inner_block(cs, mats, n_aug, m, b0, b1))) return rc;
       const bool split = split_last;
       split_last = false;

@@ -24,7 +24,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.exit(0)
 res = {}
 for flag in ("1", "0"):
-    env = dict(os.environ, MLE_BOUNDARY_SPLIT=flag)
+    env = dict(os.environ, **{os.environ.get("AB_VAR", "MLE_BOUNDARY_SPLIT"): flag})
     path = f"/tmp/ab_{flag}.npy"
     subprocess.run([sys.executable, __file__, "child", path], env=env, check=True)
     res[flag] = np.load(path)
