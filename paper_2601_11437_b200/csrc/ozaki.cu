@@ -66,6 +66,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
   if (!done) asm volatile("trap;");
 }
+// Spin on the non-suspending test_wait (developer A/B against try_wait's suspend/wake cost
+// on the MMA issuer's critical path).
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  for (uint32_t it = 0; it < (1u << 30) && !done; ++it) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+  if (!done) asm volatile("trap;");
+}
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -274,6 +288,12 @@ __global__ void __launch_bounds__(16 * kR) oz_slice_kernel(OzSliceArgs sa) {
   }
 }
 
+#ifndef OZ_EARLY_WAIT  // MMA issuer waits for the next stage before this one's last MMAs
+#define OZ_EARLY_WAIT 0
+#endif
+#ifndef OZ_TEST_WAIT  // MMA issuer waits on full stages with test_wait spins (A/B)
+#define OZ_TEST_WAIT 0
+#endif
 #ifndef OZ_STORE  // C store of the epilogue (developer A/B: __stcs streaming, __stwt ...)
 #define OZ_STORE __stcg
 #endif
@@ -424,7 +444,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
   if (warp == 0) {
     if (lane == 0) {  // producer
       long long gk = 0;
-      for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+      for (long long t = blockIdx.x; t < total && g.diag_mode < 8; t += gridDim.x) {
         OzTile o;
         if (!oz_tile<kN>(g, per_z, t, o)) continue;
         const int8_t* Ablk = g.As[o.z] + (size_t)o.tm * kblocks * kS * OZ_BLK;
@@ -473,7 +493,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       const long long use = local / Cfg::kSets;
       {
         const long long c0 = clock64();
-        if (use >= 1 && g.diag_mode != 7) mbar_wait(&acc_empty[ab], (uint32_t)((use - 1) & 1));
+        if (use >= 1 && g.diag_mode < 7) mbar_wait(&acc_empty[ab], (uint32_t)((use - 1) & 1));
         c_acc += clock64() - c0;
       }
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -481,18 +501,40 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
       // The whole warp walks the k blocks (uniform values, uniform registers); one elected
       // lane issues each MMA / commit.  Descriptors: stage base + constant offsets (the
       // address field is addr >> 4 in the low 14 bits).
+      bool ready = false;  // the current stage's full barrier already waited (early wait)
       for (int kb = 0; kb < kblocks; ++kb, ++gk) {
-        {
+        if (g.diag_mode < 8 && !ready) {  // diagnostics 8 / 9: no producer, stage 0 re-read
           const long long c0 = clock64();
+#if OZ_TEST_WAIT
+          mbar_wait_spin(&full_bar[st], ph);
+#else
           mbar_wait(&full_bar[st], ph);
+#endif
           c_full += clock64() - c0;
         }
+        ready = false;
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint64_t da0 = sdesc(smem_base + (uint32_t)st * Cfg::kStage);
         const uint64_t db0 = da0 + (uint64_t)(Cfg::kAStage >> 4);
 #pragma unroll
         for (int p = 1; p <= kS; ++p) {
+#if OZ_EARLY_WAIT
+          // wait for the next stage while this k block's last MMAs are still queued, so the
+          // barrier's wake-up latency overlaps tensor work instead of following it
+          if (p == kS - 1 && g.diag_mode < 8 && kb + 1 < kblocks) {
+            const int nst = st + 1 == Cfg::kStages ? 0 : st + 1;
+            const uint32_t nph = st + 1 == Cfg::kStages ? (ph ^ 1u) : ph;
+            const long long c0 = clock64();
+#if OZ_TEST_WAIT
+            mbar_wait_spin(&full_bar[nst], nph);
+#else
+            mbar_wait(&full_bar[nst], nph);
+#endif
+            c_full += clock64() - c0;
+            ready = true;
+          }
+#endif
           if (g.diag_mode == 1 && !(kb == 0 && p == 1)) continue;
           const int rows = kN * (kS + 1 - p);  // B rows [B_1 .. B_{kS+1-p}]
           const uint32_t accum = (kb > 0 || p > 1) ? 1u : 0u;
@@ -509,7 +551,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
                 "l"(db0 + (uint64_t)((r0 * OZ_KB) >> 4)), "r"(idesc), "r"(accum));
           }
         }
-        if (kMc > 1)  // the stage is free once every cluster CTA's MMAs have read it
+        if (g.diag_mode == 8) {  // diagnostics: no per-k-block commit (pure MMA issue)
+        } else if (kMc > 1)  // the stage is free once every cluster CTA's MMAs have read it
           asm volatile(
               "{ .reg .pred pe; elect.sync _|pe, 0xffffffff;\n"
               "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
@@ -568,7 +611,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(OzGem
 #pragma unroll
       for (int j = 0; j < kPre; ++j) cv[j] = acc_c ? __ldcg(C + (long long)j * g.ldc) : 0.0;
       const double s_row = g.alpha * pow2i(g.ea[o.z][r_glob]);
-      if (g.diag_mode == 7) {  // diagnostics: no accumulator handoff at all
+      if (g.diag_mode >= 7) {  // diagnostics: no accumulator handoff at all
         ++local;
         continue;
       }

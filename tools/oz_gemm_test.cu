@@ -182,7 +182,7 @@ static double run_case(const Case& cs, int batch, int reps) {
     long long* dd;
     CK(cudaMalloc(&dd, 8 * sizeof(long long)));
     o.diag_out = dd;
-    for (int mode : {0, 5, 6, 7}) {
+    for (int mode : {0, 5, 6, 7, 8, 9}) {
       o.diag_mode = mode;
       launch_ozgemm(o, batch, 0, g_ntile);
       long long h[8];
