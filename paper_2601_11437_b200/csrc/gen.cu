@@ -62,6 +62,23 @@ __device__ __forceinline__ void stage_params(ThetaParams* dst, const ThetaParams
 
 }  // namespace
 
+// The exact evaluator, inlined (default) or out of line (MLE_GEN_EXACT_NOINLINE=1, A/B):
+// out of line, the fast path's allocation no longer carries the Bessel ladder, but the
+// measured throughput is lower at every occupancy (config-2 batch: 886 / 918 / 892 GB/s at
+// 4 / 5 / 6 CTAs per SM against 920 inlined at 4).
+#ifndef MLE_GEN_EXACT_NOINLINE
+#define MLE_GEN_EXACT_NOINLINE 0
+#endif
+template <bool kD>
+#if MLE_GEN_EXACT_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+MaternVals matern_u_call(const ThetaParams& P, double u) {
+  return matern_u<kD>(P, u);
+}
+
 // Element (i, j) of the engine's padded matrices (Sigma with the augmented row / column n
 // and identity padding; the derivative blocks zero outside [0, n)^2).
 __device__ __forceinline__ void engine_element(const GenItem& it, const ThetaParams& P, int i,
@@ -93,9 +110,9 @@ __device__ __forceinline__ void engine_element(const GenItem& it, const ThetaPar
         else
           v = matern_table<false>(P, it.tab, u);
       } else if (derivs) {
-        v = matern_u<true>(P, u);
+        v = matern_u_call<true>(P, u);
       } else {
-        v = matern_u<false>(P, u);
+        v = matern_u_call<false>(P, u);
       }
       c = v.c;
       da = v.dalpha;
@@ -237,7 +254,7 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       const double ue = s_v0[row][col];
       MaternVals v;
       if (ue > 0.0) {
-        v = matern_u<kDerivs != 0>(Pg, ue);
+        v = matern_u_call<kDerivs != 0>(Pg, ue);
       } else {  // coincident locations: zero-lag limit (matern.py:173-178)
         v.c = Pg.sigma2;
         v.dalpha = v.dnu = 0.0;
