@@ -197,3 +197,18 @@ def test_driver_matches_live_reference_driver(reference, seed):
         assert ours.termination.value == theirs.termination.value
         assert ours.used_fallback == theirs.used_fallback
         assert len(ours.iterate_trace) == len(theirs.iterate_trace)
+
+
+def test_bench_algorithmic_flop_counts():
+    """bench.py's roofline numerator (block sums) against the closed forms of SURVEY §8(d):
+    Cholesky n^3/3; per derivative block n^3 + n^3/3 (full sweeps) or 2n^3/3 + n^3/3 (two-sided)."""
+    import bench
+
+    n = 65536
+    chol = bench.gemm_algorithmic_flops(n, "loglik")
+    w = bench.gemm_algorithmic_flops(n, "eval_all", path="w")
+    two = bench.gemm_algorithmic_flops(n, "eval_all", path="2s")
+    assert abs(chol / (n ** 3 / 3) - 1) < 0.03
+    assert abs(w / (3 * n ** 3) - 1) < 0.02
+    assert abs(two / (7 * n ** 3 / 3) - 1) < 0.03
+    assert bench.solve_path(65536) == "2s" and bench.solve_path(3600) == "w"
