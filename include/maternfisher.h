@@ -221,6 +221,17 @@ int mle_dctx_right_range(mle_dctx* d, int b, const void* exch_w, const void* exc
  * (mle_dctx_stream) instead of draining it; the caller orders its collectives against that
  * stream (CUDA events; NCCL on a communication stream).  begin / partials stay synchronous. */
 int mle_dctx_set_async(mle_dctx* d, int on);
+/* Two-sided reduction on the panels (the single-context engine's path from N >= 16,384):
+ * per block b: wblock(b) and 2s_owner(b) on the owner (steps 1-3, S21 slices into exch_x),
+ * panel_slices(b) (P_b into exch_p), broadcast both, 2s_update_range(b) on every rank
+ * (step 4, the syr2k of its panels j > b), 2s_finish(b) on the owner (step 5); then the
+ * deferred sweep: for b >= 1, W_b broadcast and forward_range(b, W, 0, b) on every rank. */
+int mle_dctx_2s_owner(mle_dctx* d, int b, void* exch_x);
+int mle_dctx_2s_finish(mle_dctx* d, int b);
+int mle_dctx_2s_update_range(mle_dctx* d, int b, const void* exch_x, const void* exch_p, int lo,
+                             int hi);
+int mle_dctx_panel_slices(mle_dctx* d, int b, void* exch_p);
+int mle_dctx_forward_range(mle_dctx* d, int b, const void* exch_w, int lo, int hi);
 int mle_dctx_stream(const mle_dctx* d, void** stream);
 /* Keep every block's W_b on this rank (~3.5 N^2 bytes) so that the right sweep reuses the
  * forward sweep's W_b instead of a second broadcast; MLE_CUDA_ERROR if it does not fit. */

@@ -35,7 +35,8 @@ EXPORTED = (
     "mle_dctx_wblock", "mle_dctx_forward", "mle_dctx_right_operand", "mle_dctx_right",
     "mle_dctx_partials", "mle_launch_count", "mle_dnu_series", "mle_digamma",
     "mle_dctx_update_range", "mle_dctx_right_range", "mle_dctx_set_async", "mle_dctx_stream",
-    "mle_dctx_wcache", "mle_dctx_panel_partials",
+    "mle_dctx_wcache", "mle_dctx_panel_partials", "mle_dctx_2s_owner", "mle_dctx_2s_finish",
+    "mle_dctx_2s_update_range", "mle_dctx_panel_slices", "mle_dctx_forward_range",
 )
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -83,6 +84,13 @@ def _load():
         "mle_dctx_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
         "mle_dctx_wcache": (ctypes.c_int, [_vp, ctypes.c_int]),
         "mle_dctx_panel_partials": (ctypes.c_int, [_vp, _dp]),
+        "mle_dctx_2s_owner": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+        "mle_dctx_2s_finish": (ctypes.c_int, [_vp, ctypes.c_int]),
+        "mle_dctx_2s_update_range": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int,
+                                                    ctypes.c_int]),
+        "mle_dctx_panel_slices": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+        "mle_dctx_forward_range": (ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int,
+                                                  ctypes.c_int]),
         "mle_ctx_create": (ctypes.c_int, [_dp, _dp, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
                                           ctypes.POINTER(_vp)]),
         "mle_ctx_destroy": (None, [_vp]),

@@ -2874,6 +2874,13 @@ struct mle_dctx {
   double* part = nullptr;                      // panel reduce partials
   std::vector<double> h_part;
   bool async = false;                          // steps return without draining the stream
+  // two-sided reduction (mle_dctx_2s_*): per derivative matrix a 512 x 512 scratch, the slices
+  // of the current diagonal block and of the current S21 panel
+  double* ts2 = nullptr;
+  int8_t* a11sl = nullptr;
+  int* a11ex = nullptr;
+  int8_t* s21sl = nullptr;
+  int* s21ex = nullptr;
   std::vector<int8_t*> wcache;                 // every block's W_b slices (right sweep), or empty
   std::vector<int*> wcache_e;
 };
@@ -2959,6 +2966,11 @@ void mle_dctx_destroy(mle_dctx* d) {
   dfree(d->part);
   for (auto* p : d->wcache) dfree(p);
   for (auto* p : d->wcache_e) dfree(p);
+  dfree(d->ts2);
+  dfree(d->a11sl);
+  dfree(d->a11ex);
+  dfree(d->s21sl);
+  dfree(d->s21ex);
   mle_ctx_destroy(d->c);
   delete d;
 }
@@ -3251,6 +3263,12 @@ int mle_dctx_wblock(mle_dctx* d, int b, void* exch_w) {
 
 // Every rank, forward sweep X = L^-1 S, block b: X[c0:, owned columns] = W_b X[c0:c1, owned].
 int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w) {
+  return mle_dctx_forward_range(d, b, exch_w, 0, d ? d->nb : 0);
+}
+
+// Same, restricted to the panels of blocks j with lo <= j < hi (the two-sided path's deferred
+// sweep: block b acts on the panels left of it only).
+int mle_dctx_forward_range(mle_dctx* d, int b, const void* exch_w, int lo, int hi) {
   if (!d || !exch_w || !d->derivs) return fail(MLE_INVALID, "null argument / no derivatives");
   mle_ctx* c = d->c;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -3258,7 +3276,11 @@ int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w) {
   const int8_t* ws = static_cast<const int8_t*>(exch_w);
   const int* we = reinterpret_cast<const int*>(ws + d_wbytes(N));
   Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
-  const int no = (int)d->owned.size(), total = no * d->nmat;
+  std::vector<int> items;  // q * nmat + m of the panels in range
+  for (size_t q = 0; q < d->owned.size(); ++q)
+    if (d_in(d->owned[q], lo, hi))
+      for (int m = 0; m < d->nmat; ++m) items.push_back((int)q * d->nmat + m);
+  const int total = (int)items.size();
   int rc;
   for (int i0 = 0; i0 < total; i0 += kMaxGemm) {
     const int cnt = std::min(kMaxGemm, total - i0);
@@ -3268,7 +3290,7 @@ int mle_dctx_forward(mle_dctx* d, int b, const void* exch_w) {
     g.alpha = 1.0;
     g.beta0_tm = (int)(kDB / kNB);
     for (int z = 0; z < cnt; ++z) {
-      const int idx = i0 + z, q = idx / d->nmat, m = idx % d->nmat;
+      const int idx = items[i0 + z], q = idx / d->nmat, m = idx % d->nmat;
       double* panel = d_mat(d, m, q);
       sa.X[z] = panel + c0;  // B(n, k) = X[c0 + k, n]: k-contig rows = the panel's columns
       sa.slices[z] = d->xsl + (size_t)idx * kDB * kOzRowBytes;
@@ -3369,6 +3391,206 @@ int mle_dctx_right_range(mle_dctx* d, int b, const void* exch_w, const void* exc
       int rc = run.ozgemm(g, cnt, c->stream);
       if (rc) return rc;
     }
+  }
+  return d_sync(d);
+}
+
+// ---- two-sided reduction on the panels (the single-context solves_2s) -----
+namespace {
+int d_ensure_2s(mle_dctx* d) {
+  if (d->ts2) return MLE_OK;
+  const long long N = d->c->N;
+  CUDA_TRY(dmalloc(&d->ts2, sizeof(double) * (size_t)d->nmat * kDB * kDB));
+  CUDA_TRY(dmalloc(&d->a11sl, (size_t)d->nmat * kDB * kOzRowBytes));
+  CUDA_TRY(dmalloc(&d->a11ex, sizeof(int) * (size_t)d->nmat * kDB));
+  CUDA_TRY(dmalloc(&d->s21sl, (size_t)d->nmat * N * kOzRowBytes));
+  CUDA_TRY(dmalloc(&d->s21ex, sizeof(int) * (size_t)d->nmat * N));
+  return MLE_OK;
+}
+}  // namespace
+
+// Owner of block b (after mle_dctx_wblock(b): D_b^-1 and W_b's slices), every derivative
+// matrix: (1) S11 <- D^-1 S11 D^-T, (2) S21 <- S21 D^-T, (3) S21 <- S21 - 1/2 L21 S11, then the
+// slices of S21 (rows c1..N) into exch_x (matrix m at m * the X-exchange stride, exponents
+// after the slices) for the other ranks' trailing updates.
+int mle_dctx_2s_owner(mle_dctx* d, int b, void* exch_x) {
+  const int q = d ? d_index(d, b) : -1;
+  if (q < 0 || !exch_x || !d->derivs) return fail(MLE_INVALID, "block not owned / no derivs");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = d_ensure_2s(d);
+  if (rc) return rc;
+  const long long N = c->N, c0 = d_c0(b), c1 = c0 + kDB;
+  const int nm = d->nmat;
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  double* blks[kMaxGemm];
+  for (int m = 0; m < nm; ++m) blks[m] = d_mat(d, m, q) + c0;  // S11 (ld N)
+  run.launches += 1;
+  CUDA_TRY(launch_mirror_lower(blks, nm, N, (int)kDB, c->stream));
+  {
+    GemmArgs t = gemm_base(), u = gemm_base();
+    for (int m = 0; m < nm; ++m) {
+      t.A[m] = d->dinv[q];
+      t.B[m] = blks[m];
+      t.C[m] = d->ts2 + (size_t)m * kDB * kDB;
+      t.fail_flag[m] = c->fail_flag;
+      u.A[m] = t.C[m];
+      u.B[m] = d->dinv[q];
+      u.C[m] = blks[m];
+      u.fail_flag[m] = c->fail_flag;
+    }
+    t.lda = kDB; t.ldb = N; t.ldc = kDB; t.K = (int)kDB;
+    t.tiles_m = (int)(kDB / kNB); t.tiles_n = (int)(kDB / kNB); t.alpha = 1.0; t.beta = 0.0;
+    if ((rc = run.gemm(t, kBKN, nm))) return rc;
+    u.lda = kDB; u.ldb = kDB; u.ldc = N; u.K = (int)kDB;
+    u.tiles_m = (int)(kDB / kNB); u.tiles_n = (int)(kDB / kNB); u.alpha = 1.0; u.beta = 0.0;
+    if ((rc = run.gemm(u, kBNK, nm))) return rc;
+  }
+  if (c1 >= N) return d_sync(d);
+  const int rt = (int)((N - c1) / kNB), tb = (int)(kDB / kNB);
+  auto slice_s21 = [&](int8_t* const* dst, int* const* dex) {
+    OzSliceArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    for (int m = 0; m < nm; ++m) {
+      sa.X[m] = d_mat(d, m, q) + c1;  // rows c1.., the block's columns
+      sa.slices[m] = dst[m];
+      sa.e[m] = dex[m];
+      sa.fail_flag[m] = c->fail_flag;
+    }
+    sa.ld = N;
+    sa.K = (int)kDB;
+    return run.slice(sa, N - c1, true, nm);
+  };
+  int8_t* sl[kMaxGemm];
+  int* se[kMaxGemm];
+  for (int m = 0; m < nm; ++m) {
+    sl[m] = d->s21sl + (size_t)m * N * kOzRowBytes;
+    se[m] = d->s21ex + (size_t)m * N;
+  }
+  if ((rc = slice_s21(sl, se))) return rc;
+  {  // (2) S21 <- S21 D^-T: B = the rows of D^-1 = W_b's top slices
+    OzGemmArgs g = Launcher::oz_base(N, rt, tb);
+    g.alpha = 1.0;
+    g.beta = 0.0;
+    for (int m = 0; m < nm; ++m) {
+      g.As[m] = sl[m];
+      g.ea[m] = se[m];
+      g.Bs[m] = d->wsl[q];
+      g.eb[m] = d->wex[q];
+      g.C[m] = d_mat(d, m, q) + c1;
+      g.fail_flag[m] = c->fail_flag;
+    }
+    if ((rc = run.ozgemm(g, nm, c->stream))) return rc;
+  }
+  {  // slices of the new S11 (B operand of (3) / (5))
+    OzSliceArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    for (int m = 0; m < nm; ++m) {
+      sa.X[m] = blks[m];
+      sa.slices[m] = d->a11sl + (size_t)m * kDB * kOzRowBytes;
+      sa.e[m] = d->a11ex + (size_t)m * kDB;
+      sa.fail_flag[m] = c->fail_flag;
+    }
+    sa.ld = N;
+    sa.K = (int)kDB;
+    if ((rc = run.slice(sa, kDB, true, nm))) return rc;
+  }
+  if ((rc = mle_dctx_2s_finish(d, b))) return rc;  // (3) = the same product as (5)
+  int8_t* xs[kMaxGemm];
+  int* xe[kMaxGemm];
+  for (int m = 0; m < nm; ++m) {
+    int8_t* base = static_cast<int8_t*>(exch_x) + (size_t)m * d_xstride(N);
+    xs[m] = base;
+    xe[m] = reinterpret_cast<int*>(base + d_wbytes(N));
+  }
+  if ((rc = slice_s21(xs, xe))) return rc;
+  return d_sync(d);
+}
+
+// Owner of block b: S21 <- S21 - 1/2 L21 S11 (step (5); also step (3) inside 2s_owner).
+int mle_dctx_2s_finish(mle_dctx* d, int b) {
+  const int q = d ? d_index(d, b) : -1;
+  if (q < 0 || !d->derivs || !d->a11sl) return fail(MLE_INVALID, "block not owned / no 2s state");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c1 = d_c0(b) + kDB;
+  if (c1 >= N) return d_sync(d);
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  OzGemmArgs g = Launcher::oz_base(N, (int)((N - c1) / kNB), (int)(kDB / kNB));
+  g.alpha = -0.5;
+  for (int m = 0; m < d->nmat; ++m) {
+    g.As[m] = d->lsl[q];
+    g.ea[m] = d->lex[q];
+    g.Bs[m] = d->a11sl + (size_t)m * kDB * kOzRowBytes;
+    g.eb[m] = d->a11ex + (size_t)m * kDB;
+    g.C[m] = d_mat(d, m, q) + c1;
+    g.fail_flag[m] = c->fail_flag;
+  }
+  int rc = run.ozgemm(g, d->nmat, c->stream);
+  if (rc) return rc;
+  return d_sync(d);
+}
+
+// Every rank, step (4) of block b on its panels j > b with lo <= j < hi:
+// S22 -= S21 L21^T + L21 S21^T (lower part of each panel), from the broadcast slices of S21
+// (exch_x, as written by 2s_owner) and of L21 = P_b (exch_p, as written by factor or
+// panel_slices).
+int mle_dctx_2s_update_range(mle_dctx* d, int b, const void* exch_x, const void* exch_p, int lo,
+                             int hi) {
+  if (!d || !exch_x || !exch_p || !d->derivs) return fail(MLE_INVALID, "null argument");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c1 = d_c0(b) + kDB;
+  const int8_t* ps = static_cast<const int8_t*>(exch_p);
+  const int* pe = reinterpret_cast<const int*>(ps + d_pbytes(N));
+  Launcher run{c->stream, nullptr, c->pool, kPoolEvents};
+  std::vector<std::pair<int, int>> zs;  // (q, m)
+  for (size_t q = 0; q < d->owned.size(); ++q)
+    if (d->owned[q] > b && d_in(d->owned[q], lo, hi))
+      for (int m = 0; m < d->nmat; ++m) zs.push_back({(int)q, m});
+  for (int pass = 0; pass < 2; ++pass) {
+    for (size_t i0 = 0; i0 < zs.size(); i0 += kMaxGemm) {
+      const int cnt = (int)std::min<size_t>(kMaxGemm, zs.size() - i0);
+      OzGemmArgs g = Launcher::oz_base(N, (int)((N - c1) / kNB), (int)(kDB / kNB));
+      g.trap = 1;
+      for (int z = 0; z < cnt; ++z) {
+        const int q = zs[i0 + z].first, m = zs[i0 + z].second;
+        const long long cj = d_c0(d->owned[q]);
+        const size_t toff = (size_t)((cj - c1) / kNB) * kOzTileBytes;
+        const int8_t* xm = static_cast<const int8_t*>(exch_x) + (size_t)m * d_xstride(N);
+        const int* xem = reinterpret_cast<const int*>(xm + d_wbytes(N));
+        const int8_t* a = pass == 0 ? xm : ps;
+        const int* ea = pass == 0 ? xem : pe;
+        const int8_t* bb = pass == 0 ? ps : xm;
+        const int* eb = pass == 0 ? pe : xem;
+        g.As[z] = a + toff;
+        g.ea[z] = ea + (cj - c1);
+        g.Bs[z] = bb + toff;
+        g.eb[z] = eb + (cj - c1);
+        g.C[z] = d_mat(d, m, q) + cj;  // rows cj.., first column of panel j
+        g.tiles_m_z[z] = (int)((N - cj) / kNB);
+        g.fail_flag[z] = c->fail_flag;
+      }
+      int rc = run.ozgemm(g, cnt, c->stream);
+      if (rc) return rc;
+    }
+  }
+  return d_sync(d);
+}
+
+// Owner of block b: P_b = L[c1:, b]'s slices (kept since the factorization) into exch_p.
+int mle_dctx_panel_slices(mle_dctx* d, int b, void* exch_p) {
+  const int q = d ? d_index(d, b) : -1;
+  if (q < 0 || !exch_p) return fail(MLE_INVALID, "block not owned");
+  mle_ctx* c = d->c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long N = c->N, c1 = d_c0(b) + kDB;
+  if (c1 < N) {
+    int8_t* ex = static_cast<int8_t*>(exch_p);
+    CUDA_TRY(cudaMemcpyAsync(ex, d->lsl[q], (size_t)(N - c1) * kOzRowBytes,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(ex + d_pbytes(N), d->lex[q], sizeof(int) * (size_t)(N - c1),
+                             cudaMemcpyDeviceToDevice, c->stream));
   }
   return d_sync(d);
 }

@@ -197,10 +197,27 @@ class CudaPanels:
         self.nat.check(self.nat.lib.mle_dctx_update_range(self._d, b, self._p(exch), lo, hi))
 
     def wblock(self, b, exch):
-        self.nat.check(self.nat.lib.mle_dctx_wblock(self._d, b, self._p(exch)))
+        """W_b on the owner (kept); exch None: no copy into an exchange buffer."""
+        ptr = ctypes.c_void_p(None) if exch is None else self._p(exch)
+        self.nat.check(self.nat.lib.mle_dctx_wblock(self._d, b, ptr))
 
-    def forward(self, b, exch):
-        self.nat.check(self.nat.lib.mle_dctx_forward(self._d, b, self._p(exch)))
+    def forward(self, b, exch, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
+        self.nat.check(self.nat.lib.mle_dctx_forward_range(self._d, b, self._p(exch), lo, hi))
+
+    def ts_owner(self, b, exch_x):
+        self.nat.check(self.nat.lib.mle_dctx_2s_owner(self._d, b, self._p(exch_x)))
+
+    def ts_finish(self, b):
+        self.nat.check(self.nat.lib.mle_dctx_2s_finish(self._d, b))
+
+    def ts_update(self, b, exch_x, exch_p, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
+        self.nat.check(self.nat.lib.mle_dctx_2s_update_range(self._d, b, self._p(exch_x),
+                                                             self._p(exch_p), lo, hi))
+
+    def panel_slices(self, b, exch_p):
+        self.nat.check(self.nat.lib.mle_dctx_panel_slices(self._d, b, self._p(exch_p)))
 
     def right_operand(self, b, exch):
         self.nat.check(self.nat.lib.mle_dctx_right_operand(self._d, b, self._p(exch)))
@@ -310,7 +327,7 @@ class DistributedEngine:
     """loglik / eval_all of one dataset over ``comm``'s ranks (the reference's surface)."""
 
     def __init__(self, locations, values, comm, nugget: float = 0.0, device: int = 0,
-                 backend=None, overlap=None, wcache=None):
+                 backend=None, overlap=None, wcache=None, solve=None):
         """``backend(locations, values, rank, world, nugget)`` builds one rank's panels
         (default: :class:`CudaPanels` on ``device``; tests pass a host restatement).
 
@@ -339,6 +356,15 @@ class DistributedEngine:
                 self.streams.append(r.stream())
                 self.comm_streams.append(torch.cuda.Stream(device=r.device))
         self._ex = {k: _Exchange(self, k) for k in ("P", "W", "X")}
+        # solve formulation, as in the single-context engine: the two-sided reduction from
+        # N >= 16,384 (MLE_SOLVE=w|2s overrides), the full forward + right sweeps below
+        import os
+
+        env = os.environ.get("MLE_SOLVE")
+        big_n = self.ranks[0].N
+        self.solve = solve or (env if env in ("w", "2s") else ("2s" if big_n >= 16384 else "w"))
+        if self.solve == "2s" and not all(hasattr(r, "ts_owner") for r in self.ranks):
+            self.solve = "w"
         want = True if wcache is None else bool(wcache)
         self.wcache = False
         if want and all(hasattr(r, "wcache") for r in self.ranks):
@@ -369,7 +395,10 @@ class DistributedEngine:
         for r in self.ranks:
             r.begin(th, derivs)
         self._cholesky()
-        if derivs:
+        if derivs and self.solve == "2s":
+            self._two_sided()
+            self._deferred_sweep()
+        elif derivs:
             self._forward_sweep()
             self._right_sweep()
         # Per-panel sums placed in a (blocks x sums) array (zeros elsewhere: adding them is
@@ -495,6 +524,63 @@ class DistributedEngine:
             X.consumed(b)
             if not self.wcache:
                 W.consumed(b)
+
+    # Two-sided reduction (the single-context solves_2s recurrence) on the
+    # panels: the owner of block b runs steps (1)-(3) on its panel and sends the slices of S21
+    # and of P_b = L21; every rank applies the syr2k (4) to its panels j > b; the owner
+    # finishes with (5).  Look-ahead: the owner of b + 1 updates that panel first.
+    def _two_sided(self):
+        X, P, nb = self._ex["X"], self._ex["P"], self.nb
+
+        def owner_step(b):
+            o = self._owner(b)
+            lo = self._local(o)
+            ready = None
+            if lo is not None:
+                self.ranks[lo].wblock(b, None)  # D_b^-1 and W_b (kept for the deferred sweep)
+                self.ranks[lo].ts_owner(b, X.slot(b)[lo])
+                if b + 1 < nb:
+                    self.ranks[lo].panel_slices(b, P.slot(b)[lo])
+                ready = X.produced(b, lo)
+            if b + 1 < nb:
+                X.send(b, o, ready)
+                P.send(b, o, ready)
+
+        owner_step(0)
+        for b in range(nb):
+            o = self._local(self._owner(b))
+            if b + 1 >= nb:
+                break
+            if o is not None:
+                self.ranks[o].ts_finish(b)
+            nxt = b + 1
+            on = self._local(self._owner(nxt))
+            for r, be in enumerate(self.ranks):
+                if r == on:
+                    be.ts_update(b, X.slot(b)[r], P.slot(b)[r], nxt, nxt + 1)
+            owner_step(nxt)
+            for r, be in enumerate(self.ranks):
+                pieces = self._others(nxt) if r == on else [(0, nb)]
+                for lo, hi in pieces:
+                    be.ts_update(b, X.slot(b)[r], P.slot(b)[r], lo, hi)
+            X.consumed(b)
+            P.consumed(b)
+
+    # Deferred sweep: S21 <- L22^-1 S21 for every block column, as the block-inverse forward
+    # sweep restricted to the panels left of each row block; W_b goes out once.
+    def _deferred_sweep(self):
+        W, nb = self._ex["W"], self.nb
+        for b in range(1, nb):
+            o = self._owner(b)
+            lo = self._local(o)
+            ready = None
+            if lo is not None:
+                self.ranks[lo].wblock(b, W.slot(b)[lo])  # recomputed: ~0.3% of the work
+                ready = W.produced(b, lo)
+            W.send(b, o, ready)
+            for r, be in enumerate(self.ranks):
+                be.forward(b, W.slot(b)[r], 0, b)
+            W.consumed(b)
 
     def loglik(self, theta) -> float:
         th, s = self._run(theta, False)

@@ -105,15 +105,61 @@ class HostPanels:
         dinv = sla.solve_triangular(p[c0:c1, :], np.eye(BLOCK), lower=True)
         w = np.vstack([dinv, -p[c1:, :] @ dinv])
         self.W[b] = w
-        exch.view(-1)[: (N - c0) * BLOCK] = __import__("torch").from_numpy(w.ravel())
+        self.Dinv = getattr(self, "Dinv", {})
+        self.Dinv[b] = dinv
+        if exch is not None:
+            exch.view(-1)[: (N - c0) * BLOCK] = __import__("torch").from_numpy(w.ravel())
 
-    def forward(self, b, exch):
+    # two-sided reduction (the sygst recurrence) on the panels, FP64
+    def ts_owner(self, b, exch_x):
+        c0, c1, N = b * BLOCK, (b + 1) * BLOCK, self.N
+        dinv, L21 = self.Dinv[b], self.sig[b][c1:, :]
+        self.S11 = getattr(self, "S11", {})
+        buf = exch_x.numpy().reshape(self.nmat, N * BLOCK)
+        for m, mats in enumerate(self.mat):
+            s11 = dinv @ mats[b][c0:c1, :] @ dinv.T
+            mats[b][c0:c1, :] = s11
+            self.S11[(b, m)] = s11
+            if c1 < N:
+                s21 = mats[b][c1:, :] @ dinv.T - 0.5 * L21 @ s11
+                mats[b][c1:, :] = s21
+                buf[m, : (N - c1) * BLOCK] = s21.ravel()
+
+    def ts_finish(self, b):
+        c1 = (b + 1) * BLOCK
+        for m, mats in enumerate(self.mat):
+            if c1 < self.N:
+                mats[b][c1:, :] -= 0.5 * self.sig[b][c1:, :] @ self.S11[(b, m)]
+
+    def ts_update(self, b, exch_x, exch_p, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
+        c1, N = (b + 1) * BLOCK, self.N
+        L = exch_p.numpy()[: (N - c1) * BLOCK].reshape(N - c1, BLOCK)
+        xs = exch_x.numpy().reshape(self.nmat, N * BLOCK)
+        for m, mats in enumerate(self.mat):
+            S = xs[m, : (N - c1) * BLOCK].reshape(N - c1, BLOCK)
+            for j in self.owned:
+                if j <= b or not lo <= j < hi:
+                    continue
+                r = j * BLOCK - c1
+                mats[j][j * BLOCK:, :] -= S[r:] @ L[r:r + BLOCK].T + L[r:] @ S[r:r + BLOCK].T
+
+    def panel_slices(self, b, exch_p):
+        c1, N = (b + 1) * BLOCK, self.N
+        if c1 < N:
+            exch_p.view(-1)[: (N - c1) * BLOCK] = \
+                __import__("torch").from_numpy(np.ascontiguousarray(self.sig[b][c1:, :]).ravel())
+
+    def forward(self, b, exch, lo=0, hi=None):
+        hi = self.nb if hi is None else hi
         c0, c1, N = b * BLOCK, (b + 1) * BLOCK, self.N
         w = exch.numpy()[: (N - c0) * BLOCK].reshape(N - c0, BLOCK)
         if getattr(self, "cache_w", False):
             self.wc[b] = w.copy()
         for mats in self.mat:
             for j in self.owned:
+                if not lo <= j < hi:
+                    continue
                 x = mats[j][c0:c1, :].copy()
                 mats[j][c0:c1, :] = w[:BLOCK] @ x
                 mats[j][c1:, :] += w[BLOCK:] @ x

@@ -21,13 +21,15 @@ def _ref(gpu, loc, z, th, nugget=0.0):
 
 
 @pytest.mark.parametrize("world", [1, 3])
-def test_cuda_panels_match_engine(gpu, world):
+@pytest.mark.parametrize("solve", ["w", "2s"])
+def test_cuda_panels_match_engine(gpu, world, solve):
     from paper_2601_11437_b200.distributed import DistributedEngine, InProcessComm
 
     loc, z = config_data("config2", 1)  # n = 3,600 -> N = 4,096: 8 blocks
     th = (1.0, 0.2, 1.5)
     (ll, g, f), ll_only = _ref(gpu, loc, z, th)
-    eng = DistributedEngine(loc, z, InProcessComm(world))
+    eng = DistributedEngine(loc, z, InProcessComm(world), solve=solve)
+    assert eng.solve == solve
     dll, dg, df = eng.eval_all(th)
     assert dll == pytest.approx(ll, rel=1e-12)
     # same kernels and slice counts, but N is padded to 512 (vs 128) and the final sums run in
@@ -48,6 +50,14 @@ def test_cuda_panels_nugget_and_failure(gpu):
     z = rng.standard_normal(1500)
     th = (0.9, 0.08, 1.013)
     (ll, g, f), _ = _ref(gpu, loc, z, th, nugget=1e-4)
+    for solve in ("w", "2s"):
+        eng = DistributedEngine(loc, z, InProcessComm(2), nugget=1e-4, solve=solve)
+        dll, dg, df = eng.eval_all(th)
+        assert dll == pytest.approx(ll, rel=1e-12)
+        np.testing.assert_allclose(df, f, rtol=1e-9)
+        scale = score_scale(th, len(z), g, f)
+        assert np.all(np.abs(dg - g) <= 1e-8 * scale), (solve, dg, g, scale)
+        eng.close()
     eng = DistributedEngine(loc, z, InProcessComm(2), nugget=1e-4)
     dll, dg, df = eng.eval_all(th)
     assert dll == pytest.approx(ll, rel=1e-12)
@@ -79,7 +89,7 @@ def test_results_do_not_depend_on_world_size(gpu):
     th = (0.9, 0.15, 1.3)
     outs = []
     for world, wc in ((1, True), (2, True), (3, True), (3, False)):
-        eng = DistributedEngine(loc, z, InProcessComm(world), wcache=wc)
+        eng = DistributedEngine(loc, z, InProcessComm(world), wcache=wc, solve="w")
         assert eng.wcache == wc
         outs.append((eng.eval_all(th), eng.loglik(th)))
         eng.close()
@@ -112,14 +122,17 @@ def _nccl_world1(q, port):
 
     loc, z = cd("config2", 2)
     th = (1.0, 0.2, 1.5)
-    a = DistributedEngine(loc, z, TorchComm(), overlap=True)
-    b = DistributedEngine(loc, z, TorchComm(), overlap=False)
-    ra, rb = a.eval_all(th), b.eval_all(th)
-    la, lb = a.loglik(th), b.loglik(th)
-    q.put((a.async_steps, b.async_steps, ra[0] == rb[0], bool(np.all(ra[1] == rb[1])),
-           bool(np.all(ra[2] == rb[2])), la == lb))
-    a.close()
-    b.close()
+    res = []
+    for solve in ("w", "2s"):
+        a = DistributedEngine(loc, z, TorchComm(), overlap=True, solve=solve)
+        b = DistributedEngine(loc, z, TorchComm(), overlap=False, solve=solve)
+        ra, rb = a.eval_all(th), b.eval_all(th)
+        la, lb = a.loglik(th), b.loglik(th)
+        res.append((a.async_steps, b.async_steps, ra[0] == rb[0], bool(np.all(ra[1] == rb[1])),
+                    bool(np.all(ra[2] == rb[2])), la == lb))
+        a.close()
+        b.close()
+    q.put(res)
     dist.destroy_process_group()
 
 
@@ -132,10 +145,11 @@ def test_stream_ordered_schedule_nccl_world1(gpu):
     q = ctx.Queue()
     p = ctx.Process(target=_nccl_world1, args=(q, _free_port()))
     p.start()
-    res = q.get(timeout=600)
+    out = q.get(timeout=600)
     p.join(60)
-    assert res[0] is True and res[1] is False
-    assert all(res[2:]), res
+    for res in out:  # full sweeps, two-sided
+        assert res[0] is True and res[1] is False
+        assert all(res[2:]), res
 
 
 def _gloo_cuda_rank(rank, world, port, q):
@@ -194,3 +208,20 @@ def test_cuda_panels_two_processes_gloo(gpu):
     np.testing.assert_array_equal(g, rg)
     np.testing.assert_array_equal(f, rf)
     ref.close()
+
+
+def test_two_sided_panels_do_not_depend_on_world_size(gpu):
+    """The sharded two-sided path: 1, 2 and 3 ranks bit-identical."""
+    from paper_2601_11437_b200.distributed import DistributedEngine, InProcessComm
+
+    loc, z = config_data("config2", 3)
+    th = (0.9, 0.15, 1.3)
+    outs = []
+    for world in (1, 2, 3):
+        eng = DistributedEngine(loc, z, InProcessComm(world), solve="2s")
+        outs.append(eng.eval_all(th))
+        eng.close()
+    for ll, g, f in outs[1:]:
+        assert ll == outs[0][0]
+        np.testing.assert_array_equal(g, outs[0][1])
+        np.testing.assert_array_equal(f, outs[0][2])

@@ -146,6 +146,10 @@ def _dist_worker(rank, world, port, out):
     tau2 = 1e-3
     engn = DistributedEngine(loc, z, comm, nugget=tau2, backend=HostPanels)
     resn = engn.eval_all(th)
+    # the two-sided reduction on the panels (the single-context path from N >= 16,384)
+    res2 = DistributedEngine(loc, z, comm, backend=HostPanels, solve="2s").eval_all(th)
+    res2n = DistributedEngine(loc, z, comm, nugget=tau2, backend=HostPanels,
+                              solve="2s").eval_all(th)
     # a failing factorization: coincident locations -> NotPositiveDefinite on every rank
     bad = loc.copy()
     bad[900] = bad[899]
@@ -156,7 +160,8 @@ def _dist_worker(rank, world, port, out):
         pivot = getattr(exc, "pivot", repr(exc))
     if rank == 0:
         out.put((res[0], res[1].tolist(), res[2].tolist(), ll, resn[0], resn[1].tolist(),
-                 resn[2].tolist(), pivot))
+                 resn[2].tolist(), pivot, [res2[0], res2[1].tolist(), res2[2].tolist()],
+                 [res2n[0], res2n[1].tolist(), res2n[2].tolist()]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -174,7 +179,7 @@ def test_distributed_engine_driver_gloo():
     procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    ll, g, f, ll2, lln, gn, fn, pivot = q.get(timeout=300)
+    ll, g, f, ll2, lln, gn, fn, pivot, two, twon = q.get(timeout=300)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -193,3 +198,10 @@ def test_distributed_engine_driver_gloo():
     np.testing.assert_allclose(gn, refn[1], rtol=1e-8)
     np.testing.assert_allclose(fn, refn[2], rtol=1e-10)
     assert pivot == 900
+    # two-sided path (solve="2s"), with and without the nugget
+    assert two[0] == pytest.approx(ref[0], rel=1e-11)
+    np.testing.assert_allclose(two[1], ref[1], rtol=1e-8)
+    np.testing.assert_allclose(two[2], ref[2], rtol=1e-10)
+    assert twon[0] == pytest.approx(refn[0], rel=1e-11)
+    np.testing.assert_allclose(twon[1], refn[1], rtol=1e-8)
+    np.testing.assert_allclose(twon[2], refn[2], rtol=1e-10)

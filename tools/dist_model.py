@@ -26,7 +26,7 @@ BLK = 512
 SLICE_ROW = 7 * 512 + 4      # bytes per row of a 512-wide int8-sliced operand (+ exponent)
 
 
-def model(n, P, rate_tf=77.7, t_factor=0.40e-3, bw=350e9, t_launch=10e-6, nmat=2):
+def model(n, P, rate_tf=77.7, t_factor=0.40e-3, bw=350e9, t_launch=10e-6, nmat=2, solve="w"):
     N = -(-(n + 1) // BLK) * BLK
     nb = N // BLK
     rate = rate_tf * 1e12
@@ -42,6 +42,26 @@ def model(n, P, rate_tf=77.7, t_factor=0.40e-3, bw=350e9, t_launch=10e-6, nmat=2
         bc = rows * SLICE_ROW / bw if P > 1 else 0.0
         chain = early + t_factor + bc
         chol += max(share, chain)
+    if solve == "2s":
+        ts = dfr = 0.0
+        for b in range(nb):
+            c0, c1 = b * BLK, (b + 1) * BLK
+            rows = N - c1
+            # syr2k of the panels j > b: 2 products x 2 (N - c_j) 512^2 per panel and matrix
+            upd = sum(4.0 * (N - j * BLK) * BLK * BLK * nmat for j in range(b + 1, nb))
+            share = gemm(upd / P) + t_launch
+            # owner chain: W_b, steps (1)-(3), slicing, broadcast of S21 (+ P_b)
+            own = (gemm(2.0 * rows * BLK * BLK) + 0.15e-3            # W_b
+                   + 4.0 * BLK ** 3 * nmat / 20e12                  # (1) DMMA
+                   + gemm(2.0 * 2.0 * rows * BLK * BLK * nmat)      # (2), (3)
+                   + 2 * nmat * rows * BLK * 15.0 / 3.5e12)         # slicings
+            bc = (nmat + 1) * rows * SLICE_ROW / bw if P > 1 else 0.0
+            ts += max(share, own + bc)
+            # deferred sweep block b: the panels j < b, rows c0..N
+            dshare = gemm(2.0 * (N - c0) * BLK * c0 * nmat / P) + t_launch
+            dfr += max(dshare, (N - c0) * SLICE_ROW / bw if P > 1 else 0.0)
+        return {"chol_s": chol, "forward_s": dfr, "right_s": ts,
+                "eval_all_s": chol + ts + dfr, "loglik_s": chol}
     for b in range(nb):
         c0 = b * BLK
         rows = N - c0
@@ -69,17 +89,21 @@ def main():
         line = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
         rate = line["roofline"]["fp64_equiv_tflops_algorithmic"]
     print(f"Ozaki GEMM rate {rate:.1f} TF/s FP64-equivalent (single B200, measured)")
-    for name, n, nmat in (("config4", 65536, 2), ("config5", 100000, 3)):
-        base = model(n, 1, rate, nmat=nmat)
-        print(f"\n{name} (n = {n}, {nmat} derivative blocks)")
-        print(" P   eval_all s   loglik s   eval_all eff   loglik eff   FP64 TF/s/GPU (3n^3 std)")
-        for P in (1, 2, 4, 8):
-            m = model(n, P, rate, nmat=nmat)
-            eff = base["eval_all_s"] / (P * m["eval_all_s"])
-            effl = base["loglik_s"] / (P * m["loglik_s"])
-            tf = (3.0 if nmat == 2 else 13.0 / 3.0) * n ** 3 / m["eval_all_s"] / P / 1e12
-            print(f"{P:2d}   {m['eval_all_s']:9.3f}   {m['loglik_s']:8.3f}   {eff:11.3f}   "
-                  f"{effl:10.3f}   {tf:8.1f}")
+    for solve in ("2s", "w"):
+        for name, n, nmat in (("config4", 65536, 2), ("config5", 100000, 3)):
+            base = model(n, 1, rate, nmat=nmat, solve=solve)
+            # standard-count flops of the path: n^3/3 + nmat x (n^3 [2s] or 4n^3/3 [w])
+            std = n ** 3 / 3.0 + nmat * (n ** 3 if solve == "2s" else 4.0 * n ** 3 / 3.0)
+            print(f"\n{name} (n = {n}, {nmat} derivative blocks), solve path {solve}")
+            print(" P   eval_all s   loglik s   eval_all eff   loglik eff   "
+                  "FP64 TF/s/GPU (path's standard count)")
+            for P in (1, 2, 4, 8):
+                m = model(n, P, rate, nmat=nmat, solve=solve)
+                eff = base["eval_all_s"] / (P * m["eval_all_s"])
+                effl = base["loglik_s"] / (P * m["loglik_s"])
+                tf = std / m["eval_all_s"] / P / 1e12
+                print(f"{P:2d}   {m['eval_all_s']:9.3f}   {m['loglik_s']:8.3f}   {eff:11.3f}   "
+                      f"{effl:10.3f}   {tf:8.1f}")
 
 
 if __name__ == "__main__":
