@@ -22,6 +22,7 @@
 // Cholesky (Fisher-BT always follows an accepted loglik(theta) with eval_all(theta),
 // optimizer.py:362,375).  Results are bit-identical to recomputing.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <atomic>
 
 #include <algorithm>
@@ -37,6 +38,43 @@
 #include <vector>
 
 #include "kernels.h"
+
+// NVTX ranges (MLE_NVTX=1) around every pass and its four phases, on the host timeline of the
+// enqueueing thread: Nsight Systems / ncu --nvtx then attribute each launch to its phase.
+// nvtx3 is header-only and a no-op without an attached tool; the switch keeps even that
+// cost off the default path.
+namespace {
+struct NvtxPhases {
+  bool on;
+  int depth = 0;
+  NvtxPhases() {
+    static const bool enabled = [] {
+      const char* e = getenv("MLE_NVTX");
+      return e && e[0] == '1';
+    }();
+    on = enabled;
+  }
+  void push(const char* name) {
+    if (on) {
+      nvtxRangePushA(name);
+      ++depth;
+    }
+  }
+  void pop() {
+    if (on && depth > 0) {
+      nvtxRangePop();
+      --depth;
+    }
+  }
+  void next(const char* name) {  // close the current phase, open the next
+    pop();
+    push(name);
+  }
+  ~NvtxPhases() {
+    while (depth > 0) pop();  // error returns leave no range open
+  }
+};
+}  // namespace
 
 using namespace mle;
 
@@ -1829,6 +1867,9 @@ int run_chunk(Item* items, int m) {
     run.launches += 1;
     CUDA_TRY(launch_scatter_theta(io, lead->d_stage, m, s));
   }
+  NvtxPhases nvtx;
+  nvtx.push(m > 1 ? "mle pass (batched)" : "mle pass");
+  nvtx.push("gen");
   CUDA_TRY(cudaEventRecord(lead->ev[0], s));
   CUDA_TRY(cudaEventRecord(pc->start, s));
   // Generation.  Sigma (items that factor) on the main stream; the derivative matrices on
@@ -1949,6 +1990,7 @@ int run_chunk(Item* items, int m) {
   } else {
     CUDA_TRY(cudaEventRecord(lead->ev_der, aux));
   }
+  nvtx.next("potrf");
   CUDA_TRY(cudaEventRecord(lead->ev[1], s));
   // W_b of the items that factor in this pass and need it (eval_all, or speculation for a
   // loglik item) is built on the aux stream block by block during their Cholesky.
@@ -1983,6 +2025,7 @@ int run_chunk(Item* items, int m) {
       if (rc) return rc;
     }
   }
+  nvtx.next("solve");
   CUDA_TRY(cudaEventRecord(lead->ev[2], s));
   if (any_spec) {
     for (int b = 0; b < m; ++b)
@@ -2009,6 +2052,7 @@ int run_chunk(Item* items, int m) {
       if (rc) return rc;
     }
   }
+  nvtx.next("reduce");
   CUDA_TRY(cudaEventRecord(lead->ev[3], s));
   ReduceArgs ra;
   std::memset(&ra, 0, sizeof(ra));
@@ -2026,6 +2070,7 @@ int run_chunk(Item* items, int m) {
   ra.n = (int)lead->n;
   run.launches += 2;
   CUDA_TRY(launch_reduce(ra, m, s));
+  nvtx.next("results");
   CUDA_TRY(cudaEventRecord(lead->ev[4], s));
   {  // gather every item's results + flag + pivot, one D2H copy
     PassIo io;

@@ -5,7 +5,8 @@
 // trace_product (likelihood.py:92-104).
 //
 //  * dgemm_kernel: 128x128x16 CTA tiles, 8 warps of 64x32, FP64 tensor-core MMA
-//    (mma.sync.m16n8k8.f64 -> DMMA), 3-stage cp.async shared-memory pipeline.  Used for every
+//    (mma.sync.m8n8k4.f64 -> DMMA); operand stages by bulk copies (cp.async.bulk on an mbarrier
+//    ring, a producer warp ahead of eight DMMA warps) or cp.async.  Used for every
 //    panel product and trailing update: Cholesky (panel x Linv^T, lower SYRK), forward
 //    solve X = L^-1 S (row panel, full update), lower-only right solve B = X L^-T.
 //  * potrf_diag_kernel: one CTA factors a 128x128 diagonal tile in shared memory (16-wide
@@ -14,6 +15,8 @@
 //  * reduce kernels: deterministic two-pass FP64 sums of log L_jj, y^T y, tr B_i,
 //    <B_i, B_j>_F and y^T B_i y (the augmented entry B_i[n, n]).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "kernels.h"
 #include "pivot_math.cuh"
@@ -50,13 +53,22 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int GEMM_THREADS = 256;
+#ifndef MLE_DGEMM_STAGES_WIDE
+#define MLE_DGEMM_STAGES_WIDE 3
+#endif
+#ifndef MLE_DGEMM_STAGES_NARROW
+#define MLE_DGEMM_STAGES_NARROW 2
+#endif
+#ifndef MLE_DGEMM_BK_NARROW
+#define MLE_DGEMM_BK_NARROW 32
+#endif
 constexpr int SA = BM + 4;   // A smem: [BK][SA], m contiguous (SA = 4 mod 16 -> conflict free)
 
 // Per CTA-width constants.  kBN = 128: 2 x 4 warps of 64 x 32 (1 CTA / SM, used for the
 // in-place panel products that need the whole 128-column panel in one CTA).  kBN = 64:
 // 4 x 2 warps of 32 x 32 with <= 128 registers, so two CTAs share an SM and one CTA's
 // C preload / store phases overlap the other's DMMA main loop.
-template <int kBN>
+template <int kBN, bool kBulk = false>
 struct Tile {
   static constexpr int WM_CNT = (kBN == 128) ? 2 : 4;
   static constexpr int WN_CNT = 8 / WM_CNT;
@@ -66,13 +78,18 @@ struct Tile {
   static constexpr int NI = WTN / 8;       // n8 blocks per warp
   static constexpr int SBN = kBN + 4;      // B (kBNK) smem stride
   static constexpr int MIN_BLOCKS = (kBN == 128) ? 1 : 2;
-  static constexpr int BK = (kBN == 128) ? 16 : 32;     // k-tile
-  static constexpr int STAGES = (kBN == 128) ? 3 : 2;   // cp.async pipeline depth
+  // k-tile and pipeline depth.  Finer k-tiles with a deeper bulk-copy ring in the same
+  // shared-memory budget (16 x 4 narrow, 5 wide stages) measured the same on the loglik pass
+  // and slower on the kBKN sweeps, so both stagings share one shape.
+  static constexpr int BK = (kBN == 128) ? 16 : (kBulk ? MLE_DGEMM_BK_NARROW : 32);
+  static constexpr int STAGES = kBulk ? ((kBN == 128) ? MLE_DGEMM_STAGES_WIDE : MLE_DGEMM_STAGES_NARROW)
+                                      : ((kBN == 128) ? 3 : 2);
   static constexpr int SBK = BK + 4;                    // B (kBKN) smem: [BN][SBK]
   static constexpr int A_STAGE = BK * SA;
   template <int kBL>
   static constexpr size_t smem_bytes() {
-    return sizeof(double) * STAGES * (A_STAGE + (kBL == kBNK ? BK * SBN : kBN * SBK));
+    return sizeof(double) * STAGES * (A_STAGE + (kBL == kBNK ? BK * SBN : kBN * SBK)) +
+           16 * STAGES;  // + a full and an empty mbarrier per stage (bulk-copy staging)
   }
 };
 
@@ -84,6 +101,40 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Bulk-copy (TMA engine) staging: one warp issues whole-column cp.async.bulk copies that
+// complete on a shared-memory mbarrier; no thread of the CTA computes addresses or holds the
+// data in flight.  The waits are bounded (a lost completion traps instead of hanging).
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done = 0;
+  for (unsigned it = 0; it < (1u << 28) && !done; ++it) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  }
+  if (!done) asm volatile("trap;");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_addr(smem)), "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4],
@@ -116,9 +167,13 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& g, int* tm, int* tn,
 }  // namespace
 
 // C[tm, tn] = alpha * sum_k A(m, k) B(n, k) + beta * C, A(m,k) = A[m + k*lda].
-template <int kBL, int kBN>
-__global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_kernel(GemmArgs g) {
-  using T = Tile<kBN>;
+// kBulk: operand stages arrive by cp.async.bulk column copies (the TMA engine) on a full /
+// empty mbarrier ring driven by a ninth, producer warp; otherwise by per-thread 16-byte
+// cp.async with a CTA barrier per k-tile.  Same k order: the two produce identical bits.
+template <int kBL, int kBN, bool kBulk>
+__global__ void __launch_bounds__(kBulk ? GEMM_THREADS + 32 : GEMM_THREADS, Tile<kBN, kBulk>::MIN_BLOCKS)
+    dgemm_kernel(GemmArgs g) {
+  using T = Tile<kBN, kBulk>;
   constexpr int BK = T::BK, STAGES = T::STAGES, SBK = T::SBK, A_STAGE = T::A_STAGE;
   const int z = blockIdx.z;
   if (*g.fail_flag[z]) return;
@@ -126,6 +181,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_ker
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
   constexpr int B_STAGE = (kBL == kBNK) ? BK * T::SBN : kBN * SBK;
+  unsigned long long* full_bar =
+      reinterpret_cast<unsigned long long*>(smem + STAGES * (A_STAGE + B_STAGE));
+  unsigned long long* empty_bar = full_bar + STAGES;
 
   int tm, tn, half;
   tile_coords<kBN>(g, &tm, &tn, &half);
@@ -166,11 +224,55 @@ __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_ker
     }
   };
 
-  const int KT = g.K / BK;
+  // producer warp only: one expect_tx for the stage's bytes, then one bulk copy per operand
+  // column (A and kBNK B: BK columns of 128 / kBN doubles; kBKN B: kBN rows of BK doubles)
+  auto load_stage_bulk = [&](int stage, int kt) {
+    double* as = As + stage * A_STAGE;
+    double* bs = Bs + stage * B_STAGE;
+    unsigned long long* bar = full_bar + stage;
+    const int k0 = kt * BK;
+    if (lane == 0) mbar_expect_tx(bar, (unsigned)(sizeof(double) * (BM + kBN) * BK));
+    __syncwarp();
+    if (lane < BK) {
+      bulk_g2s(as + lane * SA, A + (long long)(k0 + lane) * lda, BM * 8, bar);
+      if (kBL == kBNK)
+        bulk_g2s(bs + lane * T::SBN, B + (long long)(k0 + lane) * ldb, kBN * 8, bar);
+    }
+    if (kBL != kBNK) {
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
-    cp_async_commit();
+      for (int nn = lane; nn < kBN; nn += 32)
+        bulk_g2s(bs + nn * SBK, B + k0 + (long long)nn * ldb, BK * 8, bar);
+    }
+  };
+
+  const int KT = g.K / BK;
+  if (kBulk) {
+    // Warp 8 is the producer: it runs ahead of the eight DMMA warps through a full / empty
+    // mbarrier ring, so the main loop has no CTA-wide barrier and no thread of the compute
+    // warps touches an address of the operand stream.
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(full_bar + s, 1);
+        mbar_init(empty_bar + s, GEMM_THREADS / 32);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == GEMM_THREADS / 32) {
+      for (int kt = 0; kt < KT; ++kt) {
+        const int st = kt % STAGES, use = kt / STAGES;
+        if (use >= 1) mbar_wait(empty_bar + st, (unsigned)((use - 1) & 1));
+        load_stage_bulk(st, kt);
+      }
+      return;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < KT) load_stage(s, s);
+      cp_async_commit();
+    }
   }
 
   // Accumulators start from C (beta = 1) so the C read overlaps the pipeline prologue and
@@ -198,9 +300,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_ker
   const unsigned neg = g.alpha < 0.0 ? 0x80000000u : 0u;
 
   for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
+    if (kBulk) {
+      mbar_wait(full_bar + kt % STAGES, (unsigned)((kt / STAGES) & 1));
+    } else {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
       const int nk = kt + STAGES - 1;
       if (nk < KT) load_stage(nk % STAGES, nk);
       cp_async_commit();
@@ -230,8 +334,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_ker
               : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
               : "d"(af[mi]), "d"(bf[ni]));
     }
+    if (kBulk) {  // this warp is done with the stage: one arrival per warp frees it
+      // The stage is refilled through the async proxy: the warp's generic-proxy reads of it
+      // must be ordered before that write (without this fence the refill overtook the last
+      // fragment loads: wrong factors at n >= 16,384, measured).
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                         smem_addr(empty_bar + kt % STAGES))
+                     : "memory");
+    }
   }
-  cp_async_wait<0>();
+  if (!kBulk) cp_async_wait<0>();
 
   // epilogue: store-only
 #pragma unroll
@@ -247,19 +362,57 @@ __global__ void __launch_bounds__(GEMM_THREADS, Tile<kBN>::MIN_BLOCKS) dgemm_ker
   }
 }
 
+// Operand staging of dgemm_kernel.  Default: the bulk-copy ring for kBNK products (both
+// operands arrive as whole 512 B - 1 KB columns: the Cholesky's panel products and updates)
+// and per-thread cp.async for kBKN products, whose B operand is 64-128 rows of only
+// 128-256 B (measured: the small bulk copies cost the config-2 solve sweeps 3%).
+// MLE_DGEMM_STAGE=cpasync | bulk forces one staging everywhere (A/B timing; the results are
+// bit-identical either way).
+static bool dgemm_bulk_staging(BLayout bl) {
+  static const int mode = [] {
+    const char* e = getenv("MLE_DGEMM_STAGE");
+    return !e ? 0 : (e[0] == 'c' ? 1 : 2);
+  }();
+  return mode == 0 ? bl == kBNK : mode == 2;
+}
+
 // Opt-in shared-memory limits; must run once per device before the first launch.
 cudaError_t init_kernel_attributes() {
   cudaError_t e;
-#define MLE_SET_SMEM(BL, BNW)                                                           \
-  e = cudaFuncSetAttribute(dgemm_kernel<BL, BNW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)Tile<BNW>::template smem_bytes<BL>());                   \
+#define MLE_SET_SMEM(BL, BNW, BULK)                                                        \
+  e = cudaFuncSetAttribute(dgemm_kernel<BL, BNW, BULK>,                                    \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                           (int)Tile<BNW, BULK>::template smem_bytes<BL>());                     \
   if (e != cudaSuccess) return e;
-  MLE_SET_SMEM(kBNK, 128)
-  MLE_SET_SMEM(kBKN, 128)
-  MLE_SET_SMEM(kBNK, 64)
-  MLE_SET_SMEM(kBKN, 64)
+  MLE_SET_SMEM(kBNK, 128, true)
+  MLE_SET_SMEM(kBKN, 128, true)
+  MLE_SET_SMEM(kBNK, 64, true)
+  MLE_SET_SMEM(kBKN, 64, true)
+  MLE_SET_SMEM(kBNK, 128, false)
+  MLE_SET_SMEM(kBKN, 128, false)
+  MLE_SET_SMEM(kBNK, 64, false)
+  MLE_SET_SMEM(kBKN, 64, false)
 #undef MLE_SET_SMEM
   return cudaSuccess;
+}
+
+template <bool kBulk>
+static void launch_gemm_staged(const GemmArgs& g, BLayout bl, long long tiles, int batch,
+                               cudaStream_t s) {
+  const int threads = kBulk ? GEMM_THREADS + 32 : GEMM_THREADS;  // + the producer warp
+  if (g.wide) {
+    const dim3 grid((unsigned)tiles, 1, (unsigned)batch);
+    if (bl == kBNK)
+      dgemm_kernel<kBNK, 128, kBulk><<<grid, threads, Tile<128, kBulk>::template smem_bytes<kBNK>(), s>>>(g);
+    else
+      dgemm_kernel<kBKN, 128, kBulk><<<grid, threads, Tile<128, kBulk>::template smem_bytes<kBKN>(), s>>>(g);
+  } else {
+    const dim3 grid((unsigned)(2 * tiles), 1, (unsigned)batch);
+    if (bl == kBNK)
+      dgemm_kernel<kBNK, 64, kBulk><<<grid, threads, Tile<64, kBulk>::template smem_bytes<kBNK>(), s>>>(g);
+    else
+      dgemm_kernel<kBKN, 64, kBulk><<<grid, threads, Tile<64, kBulk>::template smem_bytes<kBKN>(), s>>>(g);
+  }
 }
 
 // wide = 1 selects 128-column CTAs (required when C aliases A across the whole panel).
@@ -267,19 +420,10 @@ cudaError_t launch_gemm(const GemmArgs& g, BLayout bl, int batch, cudaStream_t s
   const long long tiles =
       g.lower ? (long long)g.tiles_m * (g.tiles_m + 1) / 2 : (long long)g.tiles_m * g.tiles_n;
   if (tiles <= 0) return cudaSuccess;
-  if (g.wide) {
-    const dim3 grid((unsigned)tiles, 1, (unsigned)batch);
-    if (bl == kBNK)
-      dgemm_kernel<kBNK, 128><<<grid, GEMM_THREADS, Tile<128>::smem_bytes<kBNK>(), s>>>(g);
-    else
-      dgemm_kernel<kBKN, 128><<<grid, GEMM_THREADS, Tile<128>::smem_bytes<kBKN>(), s>>>(g);
-  } else {
-    const dim3 grid((unsigned)(2 * tiles), 1, (unsigned)batch);
-    if (bl == kBNK)
-      dgemm_kernel<kBNK, 64><<<grid, GEMM_THREADS, Tile<64>::smem_bytes<kBNK>(), s>>>(g);
-    else
-      dgemm_kernel<kBKN, 64><<<grid, GEMM_THREADS, Tile<64>::smem_bytes<kBKN>(), s>>>(g);
-  }
+  if (dgemm_bulk_staging(bl))
+    launch_gemm_staged<true>(g, bl, tiles, batch, s);
+  else
+    launch_gemm_staged<false>(g, bl, tiles, batch, s);
   return cudaGetLastError();
 }
 
