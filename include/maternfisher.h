@@ -96,6 +96,15 @@ int mle_release_cached_memory(void);
 /* (max L_jj / min L_jj)^2 of the context's last successful factorization (0 before any): a
  * cheap lower bound of cond(Sigma), reported for diagnostics. */
 int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out);
+/* 1 when the context evaluates eval_all in sequential-derivative mode: the derivative blocks
+ * do not fit on the device beside the factor (BASELINE config 5, n = 100,000, on one B200),
+ * so they are generated, reduced (B_i = L^-1 S_i L^-T) and summed one at a time in one work
+ * matrix, finished blocks parked in the unused upper triangles of the two resident arrays.
+ * Chosen at mle_ctx_create from n, the nugget and the device's memory (MLE_SEQ_DERIVS=0|1
+ * overrides).  Results agree with the batched path to the rounding of the final sums; the
+ * log-likelihood is bit-identical.  No reference counterpart (likelihood.py:107-149 holds
+ * every matrix at once). */
+int mle_ctx_seq_derivs(const mle_ctx* ctx);
 int mle_kernel_profile(mle_ctx* ctx, int enable);
 int mle_kernel_stats(const mle_ctx* ctx, double* out);
 

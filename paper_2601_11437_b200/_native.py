@@ -30,7 +30,7 @@ EXPORTED = (
     "mle_ctx_n", "mle_ctx_set_values", "mle_loglik", "mle_eval_all", "mle_build",
     "mle_phase_times", "mle_cholesky", "mle_bessel_k", "mle_dnu_xnu_knu", "mle_matern_elem",
     "mle_eval_batch", "mle_simulate", "mle_release_cached_memory",
-    "mle_kernel_profile", "mle_kernel_stats", "mle_ctx_cond_estimate", "mle_dctx_create", "mle_dctx_destroy",
+    "mle_kernel_profile", "mle_kernel_stats", "mle_ctx_cond_estimate", "mle_ctx_seq_derivs", "mle_dctx_create", "mle_dctx_destroy",
     "mle_dctx_layout", "mle_dctx_begin", "mle_dctx_factor", "mle_dctx_update",
     "mle_dctx_wblock", "mle_dctx_forward", "mle_dctx_right_operand", "mle_dctx_right",
     "mle_dctx_partials", "mle_launch_count", "mle_dnu_series", "mle_digamma",
@@ -63,6 +63,7 @@ def _load():
         "mle_kernel_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
         "mle_kernel_stats": (ctypes.c_int, [ctypes.c_void_p, _dp]),
         "mle_ctx_cond_estimate": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+        "mle_ctx_seq_derivs": (ctypes.c_int, [ctypes.c_void_p]),
         "mle_dctx_create": (ctypes.c_int, [_dp, _dp, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                            ctypes.POINTER(_vp)]),

@@ -401,6 +401,13 @@ struct mle_ctx {
   int8_t* a11sl = nullptr;
   int* a11ex = nullptr;
   bool deriv_lower = false;       // derivative matrices hold their lower tiles only (2s path)
+  // Sequential-derivative mode (seq_derivs): the derivative blocks do not fit beside the
+  // factor (config 5 on one B200), so eval_all reduces them one at a time in the single work
+  // matrix `sa`, parks finished blocks in the unused upper triangles of `sigma` / `sa`
+  // (both N x (N + kParkExtraCols)) and streams W_b block by block (one-block wsl).
+  bool seq_derivs = false;
+  double cached_logdet = 0.0, cached_quad = 0.0;  // of the resident factor (with cached_ll)
+  double cached_dmin = 0.0, cached_dmax = 0.0;
   // Kernel profiling (mle_kernel_profile): single stream, CUDA events around every Ozaki
   // GEMM and slicing launch of the pass; mle_kernel_stats reports the sums.
   bool kprof = false;
@@ -454,13 +461,16 @@ int wait_spec(mle_ctx* c, cudaStream_t s) {
 int ensure_ozaki(mle_ctx* c, bool derivs);
 
 int ensure_matrices(mle_ctx* c, bool derivs) {
-  const size_t bytes = sizeof(double) * (size_t)c->N * (size_t)c->N;
+  const size_t cols = (size_t)c->N + (c->seq_derivs ? kParkExtraCols : 0);
+  const size_t bytes = sizeof(double) * (size_t)c->N * cols;
   if (!c->sigma) CUDA_TRY(dmalloc(&c->sigma, bytes));
   if (!c->linv) CUDA_TRY(dmalloc(&c->linv, sizeof(double) * (size_t)c->Nt * kNB * kNB));
   if (derivs) {
     if (!c->sa) CUDA_TRY(dmalloc(&c->sa, bytes));
-    if (!c->sn) CUDA_TRY(dmalloc(&c->sn, bytes));
-    if (c->nugget > 0.0 && !c->smat) CUDA_TRY(dmalloc(&c->smat, bytes));
+    if (!c->seq_derivs) {
+      if (!c->sn) CUDA_TRY(dmalloc(&c->sn, bytes));
+      if (c->nugget > 0.0 && !c->smat) CUDA_TRY(dmalloc(&c->smat, bytes));
+    }
   }
   return ensure_ozaki(c, derivs);
 }
@@ -521,7 +531,8 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
   }
   if (derivs && !c->xsl) {
     const int nb = (c->Nt + kOuter - 1) / kOuter;
-    const int regions = c->nugget > 0.0 ? 6 : 4;  // 2 per derivative block (look-ahead)
+    // 2 per derivative block (look-ahead); one block at a time in sequential mode
+    const int regions = c->seq_derivs ? 2 : (c->nugget > 0.0 ? 6 : 4);
     CUDA_TRY(dmalloc(&c->xsl, regions * (size_t)c->N * kOzRowBytes));
     CUDA_TRY(dmalloc(&c->xex, regions * sizeof(int) * (size_t)c->N));
     CUDA_TRY(dmalloc(&c->dinv, sizeof(double) * (size_t)nb * 512 * 512));
@@ -533,8 +544,13 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
     CUDA_TRY(dmalloc(&c->ts2, sizeof(double) * (size_t)mats * 512 * 512));
     CUDA_TRY(dmalloc(&c->a11sl, (size_t)mats * 512 * kOzRowBytes));
     CUDA_TRY(dmalloc(&c->a11ex, sizeof(int) * (size_t)mats * 512));
-    CUDA_TRY(dmalloc(&c->wsl, std::max<size_t>(1, w_byte_offset(c->Nt, nb))));
-    CUDA_TRY(dmalloc(&c->wex, sizeof(int) * std::max<long long>(1, w_row_offset(c->Nt, nb))));
+    if (c->seq_derivs) {  // W_b of one block at a time (block 0 is the largest: N rows)
+      CUDA_TRY(dmalloc(&c->wsl, (size_t)c->N * kOzRowBytes));
+      CUDA_TRY(dmalloc(&c->wex, sizeof(int) * (size_t)c->N));
+    } else {
+      CUDA_TRY(dmalloc(&c->wsl, std::max<size_t>(1, w_byte_offset(c->Nt, nb))));
+      CUDA_TRY(dmalloc(&c->wex, sizeof(int) * std::max<long long>(1, w_row_offset(c->Nt, nb))));
+    }
     // the upper tiles of every D_b^-1 are never written and must read as exact zeros
     CUDA_TRY(cudaMemsetAsync(c->dinv, 0, sizeof(double) * (size_t)nb * 512 * 512, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -562,16 +578,26 @@ GemmArgs gemm_base() {
 struct MatList {
   mle_ctx* c[kMaxGemm];
   int which[kMaxGemm];  // 0 S_alpha, 1 S_nu, 2 I_n -> M
+  int slot[kMaxGemm];   // index of the block's scratch regions (xsl / ts2 / a11sl)
   int count = 0;
   MatList(mle_ctx* const* cs, int m) {
     for (int i = 0; i < m; ++i) {
       for (int w = 0; w < (cs[i]->smat ? 3 : 2); ++w) {
         c[count] = cs[i];
+        slot[count] = w;
         which[count++] = w;
       }
     }
   }
+  // sequential-derivative mode: the one block currently in the context's work matrix
+  MatList(mle_ctx* ctx, int w) {
+    c[0] = ctx;
+    which[0] = w;
+    slot[0] = 0;
+    count = 1;
+  }
   double* S(int z) const {
+    if (c[z]->seq_derivs) return c[z]->sa;
     return which[z] == 0 ? c[z]->sa : which[z] == 1 ? c[z]->sn : c[z]->smat;
   }
 };
@@ -1242,6 +1268,7 @@ struct Launcher {
   // W_b chain runs under the rest of the factorization instead of after it.
   int compute_w_block(mle_ctx* const* cs, int m, int ks, int b) {
     const long long ld = cs[0]->N;
+    const bool one_slot = cs[0]->seq_derivs;  // W_b streamed through a one-block buffer
     const int Nt = cs[0]->Nt;
     for (int i = 0; i < m; ++i) cs[i]->w_slices = ks;
     int rc;
@@ -1280,8 +1307,8 @@ struct Launcher {
     }
     {  // slices of W_b (the FP64 bottom part reuses one scratch per context)
       const long long c1 = k.c0 + k.kb;
-      const size_t woff = w_byte_offset(Nt, b);
-      const long long eoff = w_row_offset(Nt, b);
+      const size_t woff = one_slot ? 0 : w_byte_offset(Nt, b);
+      const long long eoff = one_slot ? 0 : w_row_offset(Nt, b);
       const size_t tile_bytes = (size_t)kNB * k.kb * ks;
       OzSliceArgs top;  // rows of D_b^-1 (row-contig, ld 512)
       std::memset(&top, 0, sizeof(top));
@@ -1476,29 +1503,37 @@ struct Launcher {
   // the full forward sweep + right sweep of solves_w.  The diagonal blocks are exact after
   // (1): the reductions read the lower half as before (B[n, n] = y^T B y on the augmented row).
   int solves_2s(mle_ctx* const* cs, int m) {
-    const long long ld = cs[0]->N;
-    const int Nt = cs[0]->Nt;
-    const int nb = (Nt + kOuter - 1) / kOuter;
     MatList ml(cs, m);
+    return solves_2s(ml);
+  }
+  int solves_2s(const MatList& ml) {
+    const long long ld = ml.c[0]->N;
+    const int Nt = ml.c[0]->Nt;
+    const int nb = (Nt + kOuter - 1) / kOuter;
     const int zb = ml.count;
+    // sequential-derivative mode: W_b is rebuilt into the context's one-block buffer right
+    // before each use (it depends only on L: ~0.5% of the block's work)
+    const bool w_stream = ml.c[0]->seq_derivs;
+    mle_ctx* wctx[1] = {ml.c[0]};
     auto S = [&](int z) { return ml.S(z); };
     auto flag = [&](int z) { return (const int*)ml.c[z]->fail_flag; };
     auto XS = [&](int z, int b) {
-      return ml.c[z]->xsl + ((size_t)ml.which[z] * 2 + (b & 1)) * ld * kOzRowBytes;
+      return ml.c[z]->xsl + ((size_t)ml.slot[z] * 2 + (b & 1)) * ld * kOzRowBytes;
     };
     auto XE = [&](int z, int b) {
-      return ml.c[z]->xex + ((size_t)ml.which[z] * 2 + (b & 1)) * ld;
+      return ml.c[z]->xex + ((size_t)ml.slot[z] * 2 + (b & 1)) * ld;
     };
-    auto T2 = [&](int z) { return ml.c[z]->ts2 + (size_t)ml.which[z] * 512 * 512; };
-    auto AS = [&](int z) { return ml.c[z]->a11sl + (size_t)ml.which[z] * 512 * kOzRowBytes; };
-    auto AE = [&](int z) { return ml.c[z]->a11ex + (size_t)ml.which[z] * 512; };
+    auto T2 = [&](int z) { return ml.c[z]->ts2 + (size_t)ml.slot[z] * 512 * 512; };
+    auto AS = [&](int z) { return ml.c[z]->a11sl + (size_t)ml.slot[z] * 512 * kOzRowBytes; };
+    auto AE = [&](int z) { return ml.c[z]->a11ex + (size_t)ml.slot[z] * 512; };
     int rc;
     for (int b = 0; b < nb; ++b) {
       const Blk k = blk(Nt, b);
       const long long c1 = k.c0 + k.kb;
       const int tb = k.t1 - k.t0;
-      const size_t woff = w_byte_offset(Nt, b);
-      const long long eoff = w_row_offset(Nt, b);
+      if (w_stream && (rc = compute_w_block(wctx, 1, kOzSlices, b))) return rc;
+      const size_t woff = w_stream ? 0 : w_byte_offset(Nt, b);
+      const long long eoff = w_stream ? 0 : w_row_offset(Nt, b);
       const long long eo = oz_panel_row_offset(Nt, b);
       // (1) S11 <- D^-1 S11 D^-T.  Generation (lower_only) and the trailing updates (4) of the
       // blocks before b write only lower tiles, so S11's upper tiles are restored from its
@@ -1649,8 +1684,9 @@ struct Launcher {
     // sweep over row blocks b restricted to the columns [0, c0)
     for (int b = 1; b < nb; ++b) {
       const Blk k = blk(Nt, b);
-      const size_t woff = w_byte_offset(Nt, b);
-      const long long eoff = w_row_offset(Nt, b);
+      if (w_stream && (rc = compute_w_block(wctx, 1, kOzSlices, b))) return rc;
+      const size_t woff = w_stream ? 0 : w_byte_offset(Nt, b);
+      const long long eoff = w_stream ? 0 : w_row_offset(Nt, b);
       OzSliceArgs sa;  // B(n, kk) = X[c0 + kk, n], n < c0
       std::memset(&sa, 0, sizeof(sa));
       for (int z = 0; z < zb; ++z) {
@@ -1815,6 +1851,39 @@ struct Launcher {
 };
 
 // Runs up to kMaxItems requests (same device, same N) on the leader's stream.
+// Log-likelihood, score and Fisher information from the reduction outputs r[] (layout of
+// launch_reduce's out: sums, then y^T B y of the three blocks); o = [ll, grad[3], fisher[9]].
+void assemble_results(const mle_ctx* c, const ThetaParams& P, const double* r, int mode,
+                      double* o) {
+  const double n = (double)c->n, s2 = P.sigma2;
+  const double logdet = r[0], quad = r[1];
+  o[0] = -0.5 * n * kLog2Pi - logdet - 0.5 * quad;  // likelihood.py:85-89, 123
+  if (mode != 2) return;
+  const double tr_a = r[2], tr_n = r[3], faa = r[4], fan = r[5], fnn = r[6];
+  const double yby_a = r[kReduceSums], yby_n = r[kReduceSums + 1];
+  o[2] = -0.5 * tr_a + 0.5 * yby_a;        // likelihood.py:137
+  o[3] = -0.5 * tr_n + 0.5 * yby_n;
+  double* f = o + 4;
+  f[4] = 0.5 * faa;                        // likelihood.py:142
+  f[5] = f[7] = 0.5 * fan;                 // likelihood.py:146
+  f[8] = 0.5 * fnn;                        // likelihood.py:147
+  if (c->nugget == 0.0) {
+    o[1] = (quad - n) / (2.0 * s2);        // likelihood.py:129
+    f[0] = n / (2.0 * s2 * s2);            // likelihood.py:130
+    f[1] = f[3] = tr_a / (2.0 * s2);       // likelihood.py:141
+    f[2] = f[6] = tr_n / (2.0 * s2);       // likelihood.py:145
+  } else {
+    // Nugget (config 5; not in the reference, oracle eval_all_nugget): dSigma/dsigma^2 =
+    // (Sigma - tau^2 I) / sigma^2, so B_s2 = (I - tau^2 M) / sigma^2, M = L^-1 L^-T.
+    const double t = c->nugget, tr_m = r[7], fam = r[8], fnm = r[9], fmm = r[10];
+    const double yby_m = r[kReduceSums + 2];  // y^T M y = |Sigma^-1 z|^2
+    o[1] = -0.5 * (n - t * tr_m) / s2 + 0.5 * (quad - t * yby_m) / s2;
+    f[0] = 0.5 * (n - 2.0 * t * tr_m + t * t * fmm) / (s2 * s2);
+    f[1] = f[3] = 0.5 * (tr_a - t * fam) / s2;
+    f[2] = f[6] = 0.5 * (tr_n - t * fnm) / s2;
+  }
+}
+
 int run_chunk(Item* items, int m) {
   const auto host_t0 = std::chrono::steady_clock::now();
   mle_ctx* lead = items[0].c;
@@ -2170,36 +2239,12 @@ int run_chunk(Item* items, int m) {
     c->cached_theta[1] = it.P.alpha;
     c->cached_theta[2] = it.P.nu;
     const double* r = c->h_res;
-    const double n = (double)c->n, s2 = it.P.sigma2;
-    const double logdet = r[0], quad = r[1];
-    double* o = it.res;
-    o[0] = -0.5 * n * kLog2Pi - logdet - 0.5 * quad;  // likelihood.py:85-89, 123
-    c->cached_ll = o[0];
-    if (it.mode == 2) {
-      const double tr_a = r[2], tr_n = r[3], faa = r[4], fan = r[5], fnn = r[6];
-      const double yby_a = r[kReduceSums], yby_n = r[kReduceSums + 1];
-      o[2] = -0.5 * tr_a + 0.5 * yby_a;        // likelihood.py:137
-      o[3] = -0.5 * tr_n + 0.5 * yby_n;
-      double* f = o + 4;
-      f[4] = 0.5 * faa;                        // likelihood.py:142
-      f[5] = f[7] = 0.5 * fan;                 // likelihood.py:146
-      f[8] = 0.5 * fnn;                        // likelihood.py:147
-      if (c->nugget == 0.0) {
-        o[1] = (quad - n) / (2.0 * s2);        // likelihood.py:129
-        f[0] = n / (2.0 * s2 * s2);            // likelihood.py:130
-        f[1] = f[3] = tr_a / (2.0 * s2);       // likelihood.py:141
-        f[2] = f[6] = tr_n / (2.0 * s2);       // likelihood.py:145
-      } else {
-        // Nugget (config 5; not in the reference, oracle eval_all_nugget): dSigma/dsigma^2 =
-        // (Sigma - tau^2 I) / sigma^2, so B_s2 = (I - tau^2 M) / sigma^2, M = L^-1 L^-T.
-        const double t = c->nugget, tr_m = r[7], fam = r[8], fnm = r[9], fmm = r[10];
-        const double yby_m = r[kReduceSums + 2];  // y^T M y = |Sigma^-1 z|^2
-        o[1] = -0.5 * (n - t * tr_m) / s2 + 0.5 * (quad - t * yby_m) / s2;
-        f[0] = 0.5 * (n - 2.0 * t * tr_m + t * t * fmm) / (s2 * s2);
-        f[1] = f[3] = 0.5 * (tr_a - t * fam) / s2;
-        f[2] = f[6] = 0.5 * (tr_n - t * fnm) / s2;
-      }
-    }
+    assemble_results(c, it.P, r, it.mode, it.res);
+    c->cached_ll = it.res[0];
+    c->cached_logdet = r[0];
+    c->cached_quad = r[1];
+    c->cached_dmin = r[kReduceSums + 3];
+    c->cached_dmax = r[kReduceSums + 4];
   }
   return MLE_OK;
 }
@@ -2255,7 +2300,141 @@ int check_finite(const double* v, int64_t m, const char* what) {
   return MLE_OK;
 }
 
+// eval_all of a sequential-derivative context (mle_ctx::seq_derivs: the derivative blocks do
+// not fit beside the factor).  Same arithmetic per block as the batched two-sided path --
+// generation, the sygst-style reduction B_i = L^-1 S_i L^-T on the Ozaki GEMM -- but one
+// block at a time in the single work matrix: the factor first (a loglik pass, or the resident
+// one), then for each block generate -> reduce -> sums against the parked blocks -> park.
+// Replaces likelihood.py:107-149 exactly as eval_all does; the Frobenius sums run in a
+// different (still fixed) order than launch_reduce's.
+int eval_all_seq(mle_ctx* c, const double theta[3], double* res, int64_t* bad_pivot) {
+  Item it;
+  int rc = prepare(c, theta, 1, &it);
+  if (rc) return rc;
+  it.spec = false;
+  if (it.factor) {
+    rc = run_batch(&it, 1);
+    if (rc) return rc;
+    if (bad_pivot) *bad_pivot = it.pivot;
+    if (it.rc == MLE_NOT_PD)
+      return fail(MLE_NOT_PD,
+                  "matrix not positive definite at pivot " + std::to_string(it.pivot));
+  } else if (bad_pivot) {
+    *bad_pivot = -1;
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  if ((rc = wait_spec(c, c->stream))) return rc;
+  if ((rc = ensure_matrices(c, true))) return rc;
+  ThetaParams P = it.P;
+  if (use_gen_table())
+    mle_fill_gen_table(c->h_max / P.alpha, &P);
+  else
+    P.tab_n = 0;
+  cudaStream_t s = c->stream;
+  std::memcpy(c->h_theta, &P, sizeof(ThetaParams));
+  CUDA_TRY(cudaMemcpyAsync(c->d_theta, c->h_theta, sizeof(ThetaParams), cudaMemcpyHostToDevice,
+                           s));
+  const bool lookahead = !c->kprof && use_lookahead();
+  Launcher run{s, lookahead ? c->side : nullptr, c->pool, kPoolEvents};
+  if (c->kprof) run.prof = c;
+  NvtxPhases nvtx;
+  nvtx.push("mle eval_all (sequential derivative blocks)");
+  const int nmat = c->nugget > 0.0 ? 3 : 2;
+  const long long N = c->N;
+  const int n = (int)c->n;
+  double r[kReduceOut] = {};
+  r[0] = c->cached_logdet;
+  r[1] = c->cached_quad;
+  r[kReduceSums + 3] = c->cached_dmin;
+  r[kReduceSums + 4] = c->cached_dmax;
+  GenArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  {
+    GenItem& gi = ga.item[0];
+    gi.P = c->d_theta;
+    gi.lx = c->lx;
+    gi.ly = c->ly;
+    gi.z = c->z;
+    gi.sigma = c->sigma;
+    gi.fail_flag = c->fail_flag;
+    gi.tab = P.tab_n > 0 ? c->gtab_d : nullptr;
+    gi.write_sigma = 0;
+    gi.write_derivs = 1;
+    ga.lower_only = 1;
+    ga.ld = N;
+    ga.rows = N;
+    ga.n = n;
+  }
+  c->deriv_lower = true;
+  c->spec_ready = false;
+  CUDA_TRY(cudaEventRecord(c->ev[2], s));
+  run.launches += 1;
+  launch_gen_table(ga, 1, true, s);
+  CUDA_TRY(cudaGetLastError());
+  double gen_ms = 0.0;
+  for (int w = 0; w < nmat; ++w) {
+    nvtx.push(w == 0 ? "block alpha" : w == 1 ? "block nu" : "block M");
+    run.launches += 1;
+    if (w < 2) {
+      ga.item[0].dalpha = w == 0 ? c->sa : nullptr;
+      ga.item[0].dnu = w == 1 ? c->sa : nullptr;
+      launch_gen_engine(ga, 1, s);
+      CUDA_TRY(cudaGetLastError());
+    } else {
+      CUDA_TRY(launch_set_identity_lower(c->sa, N, n, (int)N, s));
+    }
+    MatList ml(c, w);
+    if ((rc = run.solves_2s(ml))) return rc;
+    // parked so far: alpha above sigma's band (w >= 1), nu above the work matrix's own (w == 2)
+    const double* u1 = w >= 1 ? c->sigma : nullptr;
+    const double* u2 = w == 2 ? c->sa : nullptr;
+    run.launches += 2;
+    CUDA_TRY(launch_seq_reduce(c->sa, u1, u2, N, n, (int)N, c->partials, c->out, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_res, c->out, sizeof(double) * 5, cudaMemcpyDeviceToHost, s));
+    if (w + 1 < nmat) {
+      run.launches += 1;
+      CUDA_TRY(launch_park_lower(c->sa, w == 0 ? c->sigma : c->sa, N, (int)N, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const double tr = c->h_res[0], ww = c->h_res[1], wu1 = c->h_res[2], wu2 = c->h_res[3];
+    const double yby = c->h_res[4];
+    if (w == 0) {
+      r[2] = tr; r[4] = ww; r[kReduceSums] = yby;
+    } else if (w == 1) {
+      r[3] = tr; r[6] = ww; r[5] = wu1; r[kReduceSums + 1] = yby;
+    } else {
+      r[7] = tr; r[10] = ww; r[8] = wu1; r[9] = wu2; r[kReduceSums + 2] = yby;
+    }
+    nvtx.pop();
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[3], s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  if ((rc = run.prof_collect())) return rc;
+  float solve_ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&solve_ms, c->ev[2], c->ev[3]));
+  int flag = 0;
+  CUDA_TRY(cudaMemcpy(&flag, c->fail_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) return fail(MLE_CUDA_ERROR, "failure flag set during the derivative blocks");
+  if (!it.factor)
+    for (int p = 0; p < MLE_NUM_PHASES; ++p) c->phase_ms[p] = 0.0;
+  (void)gen_ms;
+  c->phase_ms[MLE_PHASE_SOLVE] = solve_ms;
+  c->phase_ms[MLE_PHASE_TOTAL] = c->phase_ms[MLE_PHASE_GEN] + c->phase_ms[MLE_PHASE_POTRF] +
+                                 c->phase_ms[MLE_PHASE_REDUCE] + solve_ms;
+  const double nd = (double)c->n;
+  c->flops = (it.factor ? nd * nd * nd / 3.0 : 0.0) + nmat * nd * nd * nd;
+  c->gen_bytes = (it.factor ? 1.0 : 0.0) * 8.0 * nd * (nd + 1.0) / 2.0 +
+                 2.0 * 8.0 * nd * (nd + 1.0) / 2.0;
+  c->launches = (it.factor ? c->launches : 0.0) + run.launches;
+  double o[kResults] = {};
+  assemble_results(c, P, r, 2, o);
+  std::memcpy(res, o, sizeof(double) * kResults);
+  return MLE_OK;
+}
+
 int single(mle_ctx* c, const double theta[3], int mode, double* res, int64_t* bad_pivot) {
+  if (c->seq_derivs && mode == 2) return eval_all_seq(c, theta, res, bad_pivot);
   Item it;
   int rc = prepare(c, theta, mode, &it);
   if (rc) return rc;
@@ -2305,6 +2484,8 @@ int mle_ctx_cond_estimate(const mle_ctx* ctx, double* out) {
 // Developer diagnostics (not in the public header): trace every potrf_diag_kernel CTA into a
 // device buffer of `cap` records of 6 int64 (enable = 1), or stop and copy the records to
 // `host` (enable = 0; *count = records written).
+int mle_ctx_seq_derivs(const mle_ctx* ctx) { return ctx && ctx->seq_derivs ? 1 : 0; }
+
 int mle_diag_trace(int enable, long long cap, long long* host, long long* count) {
   static long long* dbuf = nullptr;
   static long long dcap = 0;
@@ -2348,9 +2529,31 @@ int mle_release_cached_memory(void) {
 static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n, int device,
                               double nugget, long long align, mle_ctx** out);
 
+// Sequential-derivative mode is chosen when the context is created (its matrices get the
+// parking columns): when Sigma + the derivative blocks + the factor's and W's slices exceed
+// the device memory, or with MLE_SEQ_DERIVS=1 (tests at small n; needs the two-sided path).
+static bool want_seq_derivs(const mle_ctx* c) {
+  if (!c->ozaki || solve_slices() != kOzSlices) return false;
+  const char* e = std::getenv("MLE_SEQ_DERIVS");
+  if (e && e[0] == '1') return use_two_sided(c->N);
+  if (e && e[0] == '0') return false;
+  if (!use_two_sided(c->N)) return false;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const double N = (double)c->N;
+  const double mats = (c->nugget > 0.0 ? 4.0 : 3.0) * 8.0 * N * N;
+  const double slices = 2.0 * (double)kOzSlices * N * N / 2.0;  // factor panels + W blocks
+  return mats + slices + 6e9 > (double)total_b;
+}
+
 int mle_ctx_create(const double* locs_xy, const double* z, int64_t n, int device, double nugget,
                    mle_ctx** out) {
-  return create_ctx_aligned(locs_xy, z, n, device, nugget, kNB, out);
+  int rc = create_ctx_aligned(locs_xy, z, n, device, nugget, kNB, out);
+  if (rc == MLE_OK) (*out)->seq_derivs = want_seq_derivs(*out);
+  return rc;
 }
 
 static int create_ctx_aligned(const double* locs_xy, const double* z, int64_t n, int device,
@@ -2597,6 +2800,15 @@ int mle_eval_batch(mle_ctx* const* ctxs, int count, const double* thetas, const 
       if (modes[j] != 0 && ctxs[j] == ctxs[i])
         return fail(MLE_INVALID, "a context may appear once per batch");
     Item it;
+    if (ctxs[i]->seq_derivs && modes[i] == 2) {  // one block at a time: not batched
+      int64_t piv = -1;
+      const int rc1 = eval_all_seq(ctxs[i], thetas + 3 * i, results + (size_t)kResults * i, &piv);
+      if (rc1 == MLE_CUDA_ERROR) return rc1;
+      rcs[i] = rc1;
+      if (pivots) pivots[i] = piv;
+      if (rc1 != MLE_OK) bad = g_last_error;
+      continue;
+    }
     if (prepare(ctxs[i], thetas + 3 * i, modes[i], &it) != MLE_OK) {
       rcs[i] = MLE_INVALID;
       bad = g_last_error;

@@ -269,9 +269,9 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
     double* pn = it.dnu + i + j0 * ld;
 #pragma unroll
     for (int r = 0; r < kGT / 8; ++r) {
-      if (kDerivs) {
-        pa[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
-        pn[8 * r * ld] = s_v1[lane_row][col0 + 8 * r];
+      if (kDerivs) {  // a null block is skipped (sequential-derivative mode: one at a time)
+        if (it.dalpha) pa[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
+        if (it.dnu) pn[8 * r * ld] = s_v1[lane_row][col0 + 8 * r];
       } else {
         ps[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
       }
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       engine_element(it, P, i, j, n, kDerivs != 0, c, da, dn);
       const long long off = (long long)i + (long long)j * ld;
       if (kDerivs) {
-        it.dalpha[off] = da;
-        it.dnu[off] = dn;
+        if (it.dalpha) it.dalpha[off] = da;
+        if (it.dnu) it.dnu[off] = dn;
         s_v0[lane_row][jl] = da;
         s_v1[lane_row][jl] = dn;
       } else {
@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       const int jl = col0 + 8 * r;
       const int j2 = ti * kGT + jl;
       const long long off = (long long)i2 + (long long)j2 * ld;
-      it.dalpha[off] = s_v0[jl][lane_row];
-      it.dnu[off] = s_v1[jl][lane_row];
+      if (it.dalpha) it.dalpha[off] = s_v0[jl][lane_row];
+      if (it.dnu) it.dnu[off] = s_v1[jl][lane_row];
     }
   }
 }

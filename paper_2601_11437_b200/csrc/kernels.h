@@ -129,6 +129,17 @@ cudaError_t launch_scatter_theta(const PassIo& io, const ThetaParams* staged, in
                                  cudaStream_t s);
 cudaError_t launch_gather_results(const PassIo& io, double* dst, int items, cudaStream_t s);
 
+// Sequential-derivative mode (linalg.cu): park the lower triangle of a finished block in the
+// unused upper triangle of an N x (N + 513) array, identity on the lower triangle + diagonal
+// band only, and the sums of one block against up to two parked blocks
+// (out: [tr W, <W,W>, <W,U1>, <W,U2>, W[n,n]]; partials >= kReduceBlocks * 4 doubles).
+constexpr int kParkExtraCols = 513;
+cudaError_t launch_park_lower(const double* src, double* park, long long ld, int N,
+                              cudaStream_t s);
+cudaError_t launch_set_identity_lower(double* S, long long ld, int n, int N, cudaStream_t s);
+cudaError_t launch_seq_reduce(const double* W, const double* U1, const double* U2, long long ld,
+                              int n, int N, double* partials, double* out, cudaStream_t s);
+
 // S = I_n inside the padded N x N matrix (zero elsewhere), for every item.
 cudaError_t launch_set_identity(double* const* S, long long ld, int n, int items,
                                 cudaStream_t s);

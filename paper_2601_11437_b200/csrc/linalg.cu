@@ -1036,6 +1036,108 @@ __global__ void __launch_bounds__(32 * kFinalWarps) reduce_final_kernel(ReduceAr
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Sequential-derivative mode (contexts whose derivative blocks do not fit beside the factor:
+// config 5 on one B200).  The blocks B_i = L^-1 S_i L^-T are reduced one at a time in a single
+// work matrix; a finished block is parked, column by column, in the unused upper triangle of
+// a resident N x (N + 513) array:
+//     B(r, c), r >= c   ->   park[(r - c) + (N - c + 512) ld]
+// i.e. the lower part of column c (contiguous) becomes the top of column N - c + 512
+// (contiguous): rows 0 .. N - c - 1 of that column lie above the 512-wide diagonal band the
+// factorization and the two-sided reduction use, so nothing else touches them.
+__device__ __forceinline__ const double* parked_column(const double* park, long long ld,
+                                                       long long N, long long c) {
+  return park + (N - c + 512) * ld - c;  // + r addresses B(r, c)
+}
+
+__global__ void __launch_bounds__(256) park_lower_kernel(const double* __restrict__ src,
+                                                         double* __restrict__ park, long long ld,
+                                                         int N) {
+  const long long c = blockIdx.x;
+  const double* in = src + c * ld;
+  double* out = park + ((long long)N - c + 512) * ld - c;
+  for (long long r = c + threadIdx.x; r < N; r += 256) out[r] = in[r];
+}
+
+cudaError_t launch_park_lower(const double* src, double* park, long long ld, int N,
+                              cudaStream_t s) {
+  park_lower_kernel<<<(unsigned)N, 256, 0, s>>>(src, park, ld, N);
+  return cudaGetLastError();
+}
+
+// S = I_n on the lower triangle and the 512-wide diagonal band of the padded matrix only (the
+// full-matrix set_identity would wipe a block parked above the band).
+__global__ void __launch_bounds__(256) set_identity_lower_kernel(double* S, long long ld, int n,
+                                                                 int N) {
+  const long long j = blockIdx.x;
+  double* col = S + j * ld;
+  for (long long i = (j / 512) * 512 + threadIdx.x; i < N; i += 256)
+    col[i] = (i == j && i < n) ? 1.0 : 0.0;
+}
+
+cudaError_t launch_set_identity_lower(double* S, long long ld, int n, int N, cudaStream_t s) {
+  set_identity_lower_kernel<<<(unsigned)N, 256, 0, s>>>(S, ld, n, N);
+  return cudaGetLastError();
+}
+
+// Sums of one finished block W (lower, in the work matrix) against up to two parked blocks:
+// partials per CTA [tr W, <W,W>, <W,U1>, <W,U2>] (Frobenius products of the symmetric
+// matrices over [0, n)^2 from their lower triangles); one warp per column, fixed mapping and
+// order -> deterministic.  out[0..4) = the sums, out[4] = W[n, n] (= y^T W y).
+constexpr int SEQ_SUMS = 4;
+__global__ void __launch_bounds__(RTHREADS) seq_reduce_kernel(const double* __restrict__ W,
+                                                              const double* __restrict__ U1,
+                                                              const double* __restrict__ U2,
+                                                              long long ld, int n, int N,
+                                                              double* partials) {
+  __shared__ double sh[RTHREADS / 32];
+  double s[SEQ_SUMS] = {0.0, 0.0, 0.0, 0.0};
+  const int warps = RTHREADS / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * warps + warp; j < n; j += gridDim.x * warps) {
+    const double* w = W + (long long)j * ld;
+    const double* u1 = U1 ? parked_column(U1, ld, N, j) : nullptr;
+    const double* u2 = U2 ? parked_column(U2, ld, N, j) : nullptr;
+    if (lane == 0) {
+      const double a = w[j];
+      s[0] += a;
+      s[1] += a * a;
+      if (u1) s[2] += a * u1[j];
+      if (u2) s[3] += a * u2[j];
+    }
+    for (int i = j + 1 + lane; i < n; i += 32) {
+      const double a = w[i];
+      s[1] += 2.0 * a * a;
+      if (u1) s[2] += 2.0 * a * u1[i];
+      if (u2) s[3] += 2.0 * a * u2[i];
+    }
+  }
+  for (int q = 0; q < SEQ_SUMS; ++q) {
+    const double t = block_sum(s[q], sh);
+    if (threadIdx.x == 0) partials[blockIdx.x * SEQ_SUMS + q] = t;
+  }
+}
+
+__global__ void __launch_bounds__(32 * SEQ_SUMS) seq_reduce_final_kernel(const double* partials,
+                                                                         const double* W,
+                                                                         long long ld, int n,
+                                                                         double* out) {
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int b = lane; b < RBLOCKS; b += 32) v += partials[b * SEQ_SUMS + q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) out[q] = v;
+  if (threadIdx.x == 0) out[SEQ_SUMS] = W[n + (long long)n * ld];
+}
+
+// partials: >= kReduceBlocks * 4 doubles; out: 5 doubles (device).
+cudaError_t launch_seq_reduce(const double* W, const double* U1, const double* U2, long long ld,
+                              int n, int N, double* partials, double* out, cudaStream_t s) {
+  seq_reduce_kernel<<<RBLOCKS, RTHREADS, 0, s>>>(W, U1, U2, ld, n, N, partials);
+  seq_reduce_final_kernel<<<1, 32 * SEQ_SUMS, 0, s>>>(partials, W, ld, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reduce(const ReduceArgs& r, int items, cudaStream_t s) {
   bool any_m = false;
   for (int i = 0; i < items; ++i) any_m = any_m || r.Bm[i] != nullptr;

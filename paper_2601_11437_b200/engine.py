@@ -111,6 +111,12 @@ class Engine:
         nat.check(nat.lib.mle_ctx_cond_estimate(self._ctx, nat.as_ptr(out)))
         return float(out[0])
 
+    @property
+    def sequential_derivs(self) -> bool:
+        """True when eval_all reduces the derivative blocks one at a time (they do not fit
+        on the device beside the factor: config 5 on one B200; see mle_ctx_seq_derivs)."""
+        return bool(nat.lib.mle_ctx_seq_derivs(self._ctx))
+
     def kernel_profile(self, enable: bool = True):
         """Serialise passes led by this engine and event-time every Ozaki GEMM / slicing."""
         nat.check(nat.lib.mle_kernel_profile(self._ctx, int(bool(enable))))
