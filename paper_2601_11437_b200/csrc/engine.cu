@@ -406,6 +406,12 @@ struct mle_ctx {
   // matrix `sa`, parks finished blocks in the unused upper triangles of `sigma` / `sa`
   // (both N x (N + kParkExtraCols)) and streams W_b block by block (one-block wsl).
   bool seq_derivs = false;
+  // seq_derivs: the factor's panel slices (7 N^2 / 2 bytes: 35 GB at config 5) do not fit
+  // beside the two arrays either.  During a factorizing pass `lsl` aliases the (then idle)
+  // work matrix `sa`; the derivative phase overwrites it and re-slices each panel of L into
+  // one of two slots right before the block that uses it.
+  int8_t* psl = nullptr;          // 2 slots of (N x 512) panel slices
+  int* pex = nullptr;             // their row exponents (2 x N)
   double cached_logdet = 0.0, cached_quad = 0.0;  // of the resident factor (with cached_ll)
   double cached_dmin = 0.0, cached_dmax = 0.0;
   // Kernel profiling (mle_kernel_profile): single stream, CUDA events around every Ozaki
@@ -465,6 +471,7 @@ int ensure_matrices(mle_ctx* c, bool derivs) {
   const size_t bytes = sizeof(double) * (size_t)c->N * cols;
   if (!c->sigma) CUDA_TRY(dmalloc(&c->sigma, bytes));
   if (!c->linv) CUDA_TRY(dmalloc(&c->linv, sizeof(double) * (size_t)c->Nt * kNB * kNB));
+  if (c->seq_derivs && !c->sa) CUDA_TRY(dmalloc(&c->sa, bytes));  // also backs lsl
   if (derivs) {
     if (!c->sa) CUDA_TRY(dmalloc(&c->sa, bytes));
     if (!c->seq_derivs) {
@@ -526,7 +533,12 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
   if (!c->ozaki) return MLE_OK;
   if (!c->lsl) {
     const long long rows = oz_panel_row_offset(c->Nt, (c->Nt + kOuter - 1) / kOuter);
-    CUDA_TRY(dmalloc(&c->lsl, std::max<size_t>(1, (size_t)rows * kOzRowBytes)));
+    if (c->seq_derivs) {
+      // 7 N^2 / 2 bytes of slices inside the 8 N (N + 513)-byte work matrix
+      c->lsl = reinterpret_cast<int8_t*>(c->sa);
+    } else {
+      CUDA_TRY(dmalloc(&c->lsl, std::max<size_t>(1, (size_t)rows * kOzRowBytes)));
+    }
     CUDA_TRY(dmalloc(&c->lex, sizeof(int) * std::max<long long>(1, rows)));
   }
   if (derivs && !c->xsl) {
@@ -547,6 +559,8 @@ int ensure_ozaki(mle_ctx* c, bool derivs) {
     if (c->seq_derivs) {  // W_b of one block at a time (block 0 is the largest: N rows)
       CUDA_TRY(dmalloc(&c->wsl, (size_t)c->N * kOzRowBytes));
       CUDA_TRY(dmalloc(&c->wex, sizeof(int) * (size_t)c->N));
+      CUDA_TRY(dmalloc(&c->psl, 2 * (size_t)c->N * kOzRowBytes));
+      CUDA_TRY(dmalloc(&c->pex, 2 * sizeof(int) * (size_t)c->N));
     } else {
       CUDA_TRY(dmalloc(&c->wsl, std::max<size_t>(1, w_byte_offset(c->Nt, nb))));
       CUDA_TRY(dmalloc(&c->wex, sizeof(int) * std::max<long long>(1, w_row_offset(c->Nt, nb))));
@@ -1266,9 +1280,39 @@ struct Launcher {
   // W_b of one outer block: needs only L[c0:, c0:c1] (final once block b is factored) and
   // its Linv tiles, so the Cholesky issues it block by block (potrf's W request) and the
   // W_b chain runs under the rest of the factorization instead of after it.
+  // seq_derivs: the slices of panel P_b = L[c1:, c0:c1] are not resident (mle_ctx::psl): they
+  // are cut again from L into slot b & 1 on the main stream.  Two slots: the side stream's
+  // far update of block b still reads slot b & 1 while block b + 1 fills the other; block
+  // b + 2 refills it after the main stream joined the side stream in block b + 1's step (4).
+  static const int8_t* panel_slices(const mle_ctx* c, int b, long long eo) {
+    return c->seq_derivs ? c->psl + (size_t)(b & 1) * c->N * kOzRowBytes
+                         : c->lsl + (size_t)eo * kOzRowBytes;
+  }
+  static const int* panel_exps(const mle_ctx* c, int b, long long eo) {
+    return c->seq_derivs ? c->pex + (size_t)(b & 1) * c->N : c->lex + eo;
+  }
+  int slice_panel_slot(mle_ctx* c, int b) {
+    const Blk k = blk(c->Nt, b);
+    const long long ld = c->N, c1 = k.c0 + k.kb;
+    if (c1 >= ld) return MLE_OK;
+    OzSliceArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    sa.X[0] = c->sigma + c1 + k.c0 * ld;
+    sa.slices[0] = c->psl + (size_t)(b & 1) * ld * kOzRowBytes;
+    sa.e[0] = c->pex + (size_t)(b & 1) * ld;
+    sa.fail_flag[0] = c->fail_flag;
+    sa.ld = ld;
+    sa.K = kOzK;
+    return slice(sa, ld - c1, true, 1);
+  }
+
   int compute_w_block(mle_ctx* const* cs, int m, int ks, int b) {
     const long long ld = cs[0]->N;
     const bool one_slot = cs[0]->seq_derivs;  // W_b streamed through a one-block buffer
+    if (one_slot) {
+      int rc0 = slice_panel_slot(cs[0], b);
+      if (rc0) return rc0;
+    }
     const int Nt = cs[0]->Nt;
     for (int i = 0; i < m; ++i) cs[i]->w_slices = ks;
     int rc;
@@ -1339,8 +1383,8 @@ struct Launcher {
       g.kblocks = (int)(k.kb / 32);
       g.beta = 0.0;  // C = -P_b D_b^-1
       for (int it = 0; it < m; ++it) {
-        g.As[it] = cs[it]->lsl + (size_t)eo * kOzRowBytes;
-        g.ea[it] = cs[it]->lex + eo;
+        g.As[it] = panel_slices(cs[it], b, eo);
+        g.ea[it] = panel_exps(cs[it], b, eo);
         g.Bs[it] = cs[it]->dtsl;
         g.eb[it] = cs[it]->dtex;
         g.C[it] = cs[it]->wbuf;
@@ -1616,8 +1660,8 @@ struct Launcher {
         g.kblocks = (int)(k.kb / 32);
         g.alpha = -0.5;
         for (int z = 0; z < zb; ++z) {
-          g.As[z] = ml.c[z]->lsl + (size_t)eo * kOzRowBytes;
-          g.ea[z] = ml.c[z]->lex + eo;
+          g.As[z] = panel_slices(ml.c[z], b, eo);
+          g.ea[z] = panel_exps(ml.c[z], b, eo);
           g.Bs[z] = AS(z);
           g.eb[z] = AE(z);
           g.C[z] = S(z) + c1 + k.c0 * ld;
@@ -1640,8 +1684,8 @@ struct Launcher {
         g.kblocks = (int)(k.kb / 32);
         g.trap = 1;
         for (int z = 0; z < zb; ++z) {
-          const int8_t* ls = ml.c[z]->lsl + (size_t)eo * kOzRowBytes;
-          const int* le = ml.c[z]->lex + eo;
+          const int8_t* ls = panel_slices(ml.c[z], b, eo);
+          const int* le = panel_exps(ml.c[z], b, eo);
           g.As[z] = pass == 0 ? XS(z, b) : ls;
           g.ea[z] = pass == 0 ? XE(z, b) : le;
           g.Bs[z] = pass == 0 ? ls : XS(z, b);
@@ -1661,8 +1705,8 @@ struct Launcher {
           g.kblocks = (int)(k.kb / 32);
           g.lower = 1;
           for (int z = 0; z < zb; ++z) {
-            const int8_t* ls = ml.c[z]->lsl + (size_t)eo * kOzRowBytes + skip;
-            const int* le = ml.c[z]->lex + eo + (long long)tn1 * kNB;
+            const int8_t* ls = panel_slices(ml.c[z], b, eo) + skip;
+            const int* le = panel_exps(ml.c[z], b, eo) + (long long)tn1 * kNB;
             const int8_t* xs = XS(z, b) + skip;
             const int* xe = XE(z, b) + (long long)tn1 * kNB;
             g.As[z] = pass == 0 ? xs : ls;
@@ -2688,8 +2732,10 @@ void mle_ctx_destroy(mle_ctx* c) {
   if (c->h_resb) dfree(c->h_resb);
   dfree(c->gtab_s);
   dfree(c->gtab_d);
-  dfree(c->lsl);
+  if (!c->seq_derivs) dfree(c->lsl);
   dfree(c->lex);
+  dfree(c->psl);
+  dfree(c->pex);
   dfree(c->xsl);
   dfree(c->xex);
   dfree(c->dinv);

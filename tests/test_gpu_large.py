@@ -166,3 +166,38 @@ def test_config3_fit_vs_reference(gpu):
         pytest.skip("reference config-3 fit golden not generated in this tree")
     gold, res = run_fit(gpu, "config3", 0)
     check(gold, res)
+
+
+def test_config5_full_size_on_one_gpu(gpu):
+    """BASELINE config 5 at full size (n = 100,000 GMM locations, nugget 1e-6) on ONE B200:
+    the context must come up in sequential-derivative mode (four 80 GB matrices do not fit),
+    and its eval_all -- three derivative blocks reduced one at a time -- is checked by a path
+    that shares nothing with the solves: central differences of the log-likelihood
+    (generation + Cholesky only) against the score.  Evaluated off the integer nu of
+    theta_true, where the reference's own d/dnu is a lag-1e-9 forward difference
+    (bessel.py:321-324).  Measured agreement 6e-8 .. 1.2e-6 of the score (the differences'
+    own truncation error); the Fisher matrix must be symmetric positive definite and
+    eval_all's log-likelihood is the loglik pass's bit for bit."""
+    import gc
+
+    gc.collect()  # contexts of earlier tests still referenced by dead objects: 165 GB needed
+    wl = gpu.WORKLOADS["config5"]
+    loc = wl.locations(0)
+    z = gpu.simulate_field(loc, wl.theta_true, 0, nugget=wl.nugget)
+    data = gpu.SpatialDataset(loc, z, nugget=wl.nugget)
+    eng = data.engine()
+    assert eng.sequential_derivs
+    th = np.array(wl.theta_true) * np.array([1.0, 1.0, 1.03])
+    ll = eng.loglik(th)
+    ll2, g, f = eng.eval_all(th)[:3]
+    assert ll2 == ll
+    f = np.asarray(f)
+    assert np.array_equal(f, f.T) and np.all(np.linalg.eigvalsh(f) > 0)
+    for i in range(3):
+        h = 1e-4 * th[i]
+        tp, tm = th.copy(), th.copy()
+        tp[i] += h
+        tm[i] -= h
+        fd = (eng.loglik(tp) - eng.loglik(tm)) / (2 * h)
+        assert abs(fd - g[i]) <= 1e-5 * abs(g[i]), (i, fd, g[i])
+    data.release()
