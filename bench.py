@@ -429,7 +429,45 @@ def extra_single_gpu(m, device):
     out["config2_five_fits"] = {"grad_calls": g, "seconds": dt, "it_per_s": g / dt}
     for d in sets:
         d.release()
+    if os.environ.get("MLE_BENCH_CONFIG5", "1") != "0":
+        try:
+            out["config5_one_gpu"] = config5_one_gpu(m, device)
+        except Exception as exc:  # 165 GB: never at the expense of the other context numbers
+            out["config5_one_gpu"] = {"error": repr(exc)}
     return out
+
+
+def config5_one_gpu(m, device):
+    """BASELINE config 5 (n = 100,000, nugget 1e-6) on this one GPU in the engine's
+    sequential-derivative mode: one log-likelihood and one eval_all
+    (factor resident: the three derivative blocks, 3 n^3 flops), timed once each."""
+    import gc
+
+    import torch
+
+    gc.collect()
+    m.release_cached_memory()
+    wl = m.WORKLOADS["config5"]
+    loc = wl.locations(0)
+    z = m.simulate_field(loc, wl.theta_true, 0, device=device, nugget=wl.nugget)
+    data = m.SpatialDataset(loc, z, device=device, nugget=wl.nugget)
+    eng = data.engine()
+    th = wl.theta_true
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ll = eng.loglik(th)
+    t1 = time.perf_counter()
+    ev = eng.eval_all(th)
+    t2 = time.perf_counter()
+    nd = float(wl.n)
+    rec = {"n": wl.n, "nugget": wl.nugget, "sequential_derivs": bool(eng.sequential_derivs),
+           "loglik_s": t1 - t0, "loglik_fp64_equiv_tflops": nd ** 3 / 3.0 / (t1 - t0) / 1e12,
+           "eval_all_blocks_s": t2 - t1,
+           "blocks_fp64_equiv_tflops": 3.0 * nd ** 3 / (t2 - t1) / 1e12,
+           "loglik": float(ll), "eval_all_loglik_identical": float(ev[0]) == float(ll)}
+    data.release()
+    m.release_cached_memory()
+    return rec
 
 
 def ours_arm(args, rank, world, local_rank):

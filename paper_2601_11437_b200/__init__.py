@@ -65,7 +65,7 @@ from .simulate import (
     replicate_seed,
     simulate_grf,
 )
-from ._native import device_count, LIB_PATH
+from ._native import device_count, release_cached_memory, LIB_PATH
 
 __version__ = "0.1.0"
 
@@ -84,5 +84,5 @@ __all__ = [
     "log_likelihood", "trace_product",
     "MaternParams", "SpatialDataset", "build_cov_matrix", "build_dcov_matrix",
     "dcov_dalpha", "dcov_dnu", "dcov_dsigma2", "matern_cov",
-    "device_count", "LIB_PATH", "__version__",
+    "device_count", "release_cached_memory", "LIB_PATH", "__version__",
 ]

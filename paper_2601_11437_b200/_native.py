@@ -152,5 +152,11 @@ def device_count() -> int:
     return int(lib.mle_device_count())
 
 
+def release_cached_memory() -> None:
+    """Hand the idle buffers of destroyed contexts back to the driver
+    (mle_release_cached_memory)."""
+    check(lib.mle_release_cached_memory())
+
+
 def default_device() -> int:
     return int(os.environ.get("MLE_DEVICE", "0"))
