@@ -552,7 +552,10 @@ constexpr int DS = DT + 4;  // smem stride (= 4 mod 16: conflict-free mma fragme
 constexpr int DB = 16;      // register block
 constexpr int DTHREADS = 512;
 constexpr int DWARPS = DTHREADS / 32;
-constexpr int DSCR = 64 * 64;  // scratch for the inverse doubling products
+// scratch of the inverse's doubling products T = L21 X11: one buffer per pair and level (four
+// 16 x 16, two 32 x 32, one 64 x 64), so that a level's T can be formed as soon as its inputs
+// are final, under a later pivot block; + the pivot chain's broadcast buffer (64 doubles)
+constexpr int DSCR = 4 * 16 * 16 + 2 * 32 * 32 + 64 * 64 + 64;
 constexpr size_t kDiagSmem = sizeof(double) * (DT * DS + DT + DSCR);
 
 __device__ __forceinline__ double flip_sign(double x, unsigned neg) {
@@ -687,6 +690,74 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
   if (trace && tid == 0) tr[1] = gtimer();
   DIAG_T(0)
 #define LS(i, j) Ls[(j) * DS + (i)]
+#define XS(i, j) ((i) > (j) ? Ls[(i) * DS + (j)] : ((i) == (j) ? dinv[i] : 0.0))
+  // ---- the inverse X = L^-1, in pieces (dinv holds the reciprocal pivots) ----
+  // X lives in the other triangle of Ls.  Recursive doubling: [[X11, 0], [X21, X22]] with
+  // X21 = -X22 (L21 X11), levels 16 -> 32 -> 64.  Every piece depends only on finished pivot
+  // blocks, so warps 1..15 compute it under the NEXT blocks' pivot chains (warp 0), and only
+  // the last block's pieces remain after the factorization (three dependent products instead
+  // of the whole inverse: ~3.5 us of tail instead of ~11).  Same operands, same k order as
+  // the one-shot inverse it replaces: bit-identical.
+  double* colbuf = scr;                    // pivot chain broadcast (chol16_step)
+  double* T16 = scr + 64;                  // [pair][16 x 16]
+  double* T32 = T16 + 4 * 16 * 16;         // [pair][32 x 32]
+  double* T64 = T32 + 2 * 32 * 32;         // 64 x 64
+  // diagonal 16 x 16 block blk: thread c (< 16) does column c by forward substitution
+  auto inv_diag = [&](int blk, int c) {
+    const int o = blk * DB;
+    double x[DB];
+#pragma unroll
+    for (int r = 0; r < DB; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int m = 0; m < r; ++m) v -= LS(o + r, o + m) * x[m];
+      x[r] = (r >= c) ? v * dinv[o + r] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < DB; ++r)
+      if (r > c) Ls[(o + r) * DS + (o + c)] = x[r];
+  };
+  // T = L21 X11 of the pair at offset o, level s (s x s, column-major), 16 x 16 task q
+  auto inv_T = [&](double* T, int o, int sz, int q) {
+    const int bps = sz / DB, bi = q % bps, bj = q / bps;
+    double acc[2][4] = {};
+    mma16x16(
+        acc, [&](int rr, int k) { return LS(o + sz + bi * DB + rr, o + k); },
+        [&](int cc, int k) { return XS(o + k, o + bj * DB + cc); }, sz, 0u);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int cc = bj * DB + nt * 8 + 2 * t, rr = bi * DB + g;
+      T[cc * sz + rr] = acc[nt][0];
+      T[(cc + 1) * sz + rr] = acc[nt][1];
+      T[cc * sz + rr + 8] = acc[nt][2];
+      T[(cc + 1) * sz + rr + 8] = acc[nt][3];
+    }
+  };
+  // X21 = -X22 T of the same pair, task q
+  auto inv_X21 = [&](const double* T, int o, int sz, int q) {
+    const int bps = sz / DB, bi = q % bps, bj = q / bps;
+    double acc[2][4] = {};
+    mma16x16(
+        acc, [&](int rr, int k) { return XS(o + sz + bi * DB + rr, o + sz + k); },
+        [&](int cc, int k) { return T[(bj * DB + cc) * sz + k]; }, sz, 0x80000000u);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int i0 = o + sz + bi * DB + g, j1 = o + bj * DB + nt * 8 + 2 * t;
+      Ls[i0 * DS + j1] = acc[nt][0];
+      Ls[i0 * DS + j1 + 1] = acc[nt][1];
+      Ls[(i0 + 8) * DS + j1] = acc[nt][2];
+      Ls[(i0 + 8) * DS + j1 + 1] = acc[nt][3];
+    }
+  };
+  // helper warps: the 12 warps that do not share warp 0's scheduler (warps 4, 8, 12 would
+  // take issue slots from the latency-bound pivot chain)
+  constexpr int HW = DWARPS - DWARPS / 4;
+  const bool helper = (warp & 3) != 0;
+  const int hw = warp - 1 - (warp >> 2);  // 0 .. 11 over warps 1,2,3,5,6,7,...
+  auto helpers_sync = [&]() {
+    __syncwarp();
+    asm volatile("bar.sync 1, %0;" ::"n"(HW * 32) : "memory");
+  };
 #pragma unroll 1
   for (int J = 0; J < DT / DB; ++J) {
     const int j0 = J * DB;
@@ -697,7 +768,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
 #pragma unroll
       for (int s = 0; s < DB; ++s) v[s] = (s <= r) ? LS(j0 + r, j0 + s) : 0.0;
       int fc = -1;
-      chol16_step<0>(v, rv, LS(j0, j0), r, (long long)k0 + j0, n_aug, fc, scr);
+      chol16_step<0>(v, rv, LS(j0, j0), r, (long long)k0 + j0, n_aug, fc, colbuf);
       if (lane < DB) {
 #pragma unroll
         for (int s = 0; s < DB; ++s)
@@ -713,6 +784,30 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
         *fail_idx = (long long)k0 + j0 + fc;
         *fail_flag = 1;
       }
+    } else if (helper && J >= 1) {
+      // inverse pieces whose inputs were final before this step (prev = J - 1 is factored):
+      //   stage 1: X_prev; T16 of pair (prev - 1, prev) [prev odd]; T32 of blocks 0-3 [J = 3]
+      //            and 4-7 [J = 7]; T64 [J = 5]
+      //   stage 2: X21 of that 16-pair [prev odd]; T16 of pair (6, 7) [J = 7, needs X_6]
+      //   stage 3: X21 of the 32-pair 0-3 [J = 4]
+      const int prev = J - 1;
+      if (hw == HW - 1 && lane < DB) inv_diag(prev, lane);
+      if (prev & 1) {
+        if (hw == 0) inv_T(T16 + (prev >> 1) * 256, (prev - 1) * DB, DB, 0);
+      }
+      if (J == 3 || J == 7) {
+        const int p = J == 3 ? 0 : 1;
+        if (hw >= 1 && hw <= 4) inv_T(T32 + p * 1024, p * 64, 32, hw - 1);
+      }
+      if (J == 5)
+        for (int q = hw; q < 16; q += HW) inv_T(T64, 0, 64, q);
+      helpers_sync();
+      if (prev & 1) {
+        if (hw == 0) inv_X21(T16 + (prev >> 1) * 256, (prev - 1) * DB, DB, 0);
+      }
+      if (J == 7 && hw == 1) inv_T(T16 + 3 * 256, 6 * DB, DB, 0);
+      helpers_sync();
+      if (J == 4 && hw < 4) inv_X21(T32, 0, 32, hw);
     }
     __syncthreads();
     DIAG_T(1 + 3 * J)
@@ -766,71 +861,16 @@ __global__ void __launch_bounds__(DTHREADS, 1) potrf_diag_kernel(DiagArgs da) {
   }
 
   if (trace && tid == 0) tr[2] = gtimer();
-  // ---- inverse X = L^-1 (dinv holds the reciprocal pivots) ----
-  // (i) diagonal 16x16 blocks: thread per (block, column), forward substitution in registers
-  if (tid < DT) {
-    const int blk = tid >> 4, c = tid & (DB - 1);
-    const int o = blk * DB;
-    double x[DB];
-#pragma unroll
-    for (int r = 0; r < DB; ++r) {
-      double v = (r == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int m = 0; m < r; ++m) v -= LS(o + r, o + m) * x[m];
-      x[r] = (r >= c) ? v * dinv[o + r] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < DB; ++r)
-      if (r > c) Ls[(o + r) * DS + (o + c)] = x[r];
-  }
+  // ---- what is left of the inverse: the last block's pieces, three dependent products ----
+  if (tid < DB) inv_diag(DT / DB - 1, tid);
   __syncthreads();
   DIAG_T(25)
-  // (ii) recursive doubling: [[X11, 0], [X21, X22]] with X21 = -X22 (L21 X11)
-#define XS(i, j) ((i) > (j) ? Ls[(i) * DS + (j)] : ((i) == (j) ? dinv[i] : 0.0))
-#pragma unroll 1
-  for (int s = DB; s < DT; s *= 2) {
-    const int pairs = DT / (2 * s), bps = s / DB, per_pair = bps * bps;
-    // T_p = L21 X11   (s x s, column-major in scr at p * s * s)
-    for (int task = warp; task < pairs * per_pair; task += DWARPS) {
-      const int p = task / per_pair, q = task % per_pair;
-      const int bi = q % bps, bj = q / bps;
-      const int o = 2 * s * p;
-      double acc[2][4] = {};
-      mma16x16(
-          acc, [&](int rr, int k) { return LS(o + s + bi * DB + rr, o + k); },
-          [&](int cc, int k) { return XS(o + k, o + bj * DB + cc); }, s, 0u);
-      double* T = scr + p * s * s;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int cc = bj * DB + nt * 8 + 2 * t, rr = bi * DB + g;
-        T[cc * s + rr] = acc[nt][0];
-        T[(cc + 1) * s + rr] = acc[nt][1];
-        T[cc * s + rr + 8] = acc[nt][2];
-        T[(cc + 1) * s + rr + 8] = acc[nt][3];
-      }
-    }
-    __syncthreads();
-    // X21 = -X22 T_p
-    for (int task = warp; task < pairs * per_pair; task += DWARPS) {
-      const int p = task / per_pair, q = task % per_pair;
-      const int bi = q % bps, bj = q / bps;
-      const int o = 2 * s * p;
-      const double* T = scr + p * s * s;
-      double acc[2][4] = {};
-      mma16x16(
-          acc, [&](int rr, int k) { return XS(o + s + bi * DB + rr, o + s + k); },
-          [&](int cc, int k) { return T[(bj * DB + cc) * s + k]; }, s, 0x80000000u);
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int i0 = o + s + bi * DB + g, j1 = o + bj * DB + nt * 8 + 2 * t;
-        Ls[i0 * DS + j1] = acc[nt][0];
-        Ls[i0 * DS + j1 + 1] = acc[nt][1];
-        Ls[(i0 + 8) * DS + j1] = acc[nt][2];
-        Ls[(i0 + 8) * DS + j1 + 1] = acc[nt][3];
-      }
-    }
-    __syncthreads();
-  }
+  if (warp == 0) inv_X21(T16 + 3 * 256, 6 * DB, DB, 0);
+  __syncthreads();
+  if (warp < 4) inv_X21(T32 + 1024, 64, 32, warp);
+  __syncthreads();
+  inv_X21(T64, 0, 64, warp);  // 16 tasks, one per warp
+  __syncthreads();
   DIAG_T(26)
   if (trace && tid == 0) tr[3] = gtimer();
   pdl_trigger();  // the chain's next kernel may be scheduled during the write-back

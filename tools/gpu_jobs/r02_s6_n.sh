@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 3000 python -m pytest tests -m gpu -q 2>&1 | tail -3
