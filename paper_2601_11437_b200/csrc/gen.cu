@@ -16,7 +16,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
+#include "pivot_math.cuh"
 #include "special.cuh"
 #include "kernels.h"
 
@@ -26,17 +28,33 @@ namespace {
 
 constexpr int kGT = 32;         // generation tile edge
 constexpr int kGThreads = 256;  // 8 columns per pass, 4 passes
+constexpr int kGenSlots = 24;   // table intervals a tile stages in shared memory (3 binades)
 #ifndef MLE_GEN_MINB
 #define MLE_GEN_MINB 4
 #endif
 
-__device__ __forceinline__ void lower_tile_index(long long b, int* ti, int* tj) {
-  // b = I (I + 1) / 2 + J, 0 <= J <= I
-  long long I = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+// b = I (I + 1) / 2 + J, 0 <= J <= I, for a block index b < 2^31 (a grid's x extent): a
+// float estimate of I (approximate sqrt, error << 1 for b < 2^24 and a few units at most
+// beyond) corrected exactly in 32-bit integers ((I + 1)(I + 2) < 2^32 for every such b).
+// The double-precision sqrt with 64-bit corrections this replaces was ~60 instructions of
+// every CTA's prologue.
+__device__ __forceinline__ void lower_tile_index(unsigned b, int* ti, int* tj) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaf(8.0f, (float)b, 1.0f)));
+  unsigned I = (unsigned)fmaxf((r - 1.0f) * 0.5f, 0.0f);
   while (I * (I + 1) / 2 > b) --I;
   while ((I + 1) * (I + 2) / 2 <= b) ++I;
   *ti = (int)I;
   *tj = (int)(b - I * (I + 1) / 2);
+}
+
+// Slot of element (row, col) in a 32 x 32 shared-memory value tile.  The column is XOR-swizzled
+// by the row so that all three access patterns of the generation kernel are free of bank
+// conflicts on 8-byte words: the 4 x 8 patch writes of a warp (rows R..R+3, R % 4 == 0;
+// the 33-double padded rows made these 4-way conflicts), the column reads (32 consecutive
+// rows, one column) and the transposed reads of the mirrored tile (one row, 32 columns).
+__device__ __forceinline__ int tile_slot(int row, int col) {
+  return row * kGT + (col ^ (((row & 3) << 2) | ((row >> 2) & 3)));
 }
 
 // pdist-identical Euclidean distance (no FMA contraction).
@@ -139,15 +157,15 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
   const GenItem& it = a.item[blockIdx.y];
   if (it.fail_flag != nullptr && *it.fail_flag) return;
   __shared__ __align__(16) ThetaParams P;
-  __shared__ double s_v0[kGT][kGT + 1];
-  __shared__ double s_v1[kDerivs ? kGT : 1][kGT + 1];
+  __shared__ double s_v0[kGT * kGT];
+  __shared__ double s_v1[kDerivs ? kGT * kGT : 1];
   int ti, tj;
   if (a.region == 1) {  // tile columns < jcut: grid (tile rows) x jcut, upper ones skipped
     ti = (int)(blockIdx.x / a.jcut);
     tj = (int)(blockIdx.x % a.jcut);
     if (tj > ti) return;
   } else {
-    lower_tile_index((long long)blockIdx.x, &ti, &tj);
+    lower_tile_index(blockIdx.x, &ti, &tj);
     if (a.region == 2) {  // the lower triangle of the trailing block [jcut, T)^2
       ti += a.jcut;
       tj += a.jcut;
@@ -170,88 +188,158 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
     const double* __restrict__ ly = it.ly;
     __shared__ unsigned short s_exact[kGT * kGT];
     __shared__ int s_nexact;
-    if (threadIdx.x == 0) s_nexact = 0;
+    // The tile's table intervals staged in shared memory (a.stage_tab): a warp's coefficient
+    // load costs the L1 pipe 3.3 cycles from global memory (LDG.128, any address pattern)
+    // and 1.7 from shared memory (LDS.128, up to eight distinct intervals conflict-free at
+    // the 84-word interval stride) -- tools/microbench/ld_bcast.cu.  Same coefficients, same
+    // Horner order: bit-identical to the global-memory path.
+    __shared__ __align__(16) double s_tab[kGenSlots * 3 * MLE_TAB_P];
+    __shared__ int s_kmin, s_kmax;
+    if (threadIdx.x == 0) {
+      s_nexact = 0;
+      s_kmin = MLE_TAB_MAX;
+      s_kmax = -1;
+    }
     __syncthreads();
     const int pr = threadIdx.x & 3, pc = (threadIdx.x >> 2) & 7, warp = threadIdx.x >> 5;
+    // This thread's four elements: lane position (pr, pc) of patches warp + 8 e (32 patches:
+    // 8 patch rows x 4 patch columns).
+    double u[4];
+    unsigned kk = 0;     // the four interval indices, one byte each (MLE_TAB_MAX < 256)
+    unsigned intab = 0;  // bit e: element e is inside the table range
+    int kmin_t = MLE_TAB_MAX, kmax_t = -1;
+    // pdist-identical distances (no FMA contraction).  The square root is the branch-free
+    // correctly rounded one of the pivot chain (pivot_math.cuh: bit-equal to __dsqrt_rn on
+    // normal-range inputs), so the four elements' chains interleave instead of each sitting
+    // in its own slow-path basic block; squared distances outside its range (coincident or
+    // denormally close points) take the IEEE intrinsic below.
+    double s2[4];
+    bool odd = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int patch = warp + 8 * e;
+      const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
+      const int ii = ti * kGT + row, j = tj * kGT + col;
+      const double dx = __dsub_rn(lx[ii], lx[j]);
+      const double dy = __dsub_rn(ly[ii], ly[j]);
+      s2[e] = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      odd |= !(s2[e] >= 1e-280 && s2[e] <= 1e280);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double h = pivot_sqrt_rn(s2[e]);
+      if (odd) h = __dsqrt_rn(s2[e]);
+      // u = h / alpha (matern.py:103) by Markstein's correction of h * (1 / alpha): the
+      // residual h - alpha q is exact (FMA), and q + r / alpha rounds to the correctly
+      // rounded quotient, without the division's iteration and slow-path branch
+      const double q = h * ialpha;
+      u[e] = fma(fma(-alpha, q, h), ialpha, q);
+      const bool in = u[e] >= lo && u[e] < hi;
+      const double ut = in ? u[e] : lo;  // any valid interval for the others
+      const long long b = __double_as_longlong(ut);
+      const int key = (int)((b >> 49) - key0);
+      const int k = key - (key > kGenMergeKey ? 1 : 0) -
+                    (key > kGenMergeKey + 1 && ut < MLE_SMALL_MID_SPLIT ? 1 : 0);
+      kk |= (unsigned)k << (8 * e);
+      intab |= (in ? 1u : 0u) << e;
+      kmin_t = min(kmin_t, k);
+      kmax_t = max(kmax_t, k);
+    }
+    bool staged = false;
+    int kbase = 0;
+    if (a.stage_tab) {
+      kmin_t = __reduce_min_sync(0xffffffffu, kmin_t);
+      kmax_t = __reduce_max_sync(0xffffffffu, kmax_t);
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_kmin, kmin_t);
+        atomicMax(&s_kmax, kmax_t);
+      }
+      __syncthreads();
+      kbase = s_kmin;
+      const int nslots = s_kmax - kbase + 1;
+      staged = nslots <= kGenSlots;  // CTA-uniform; wider tiles (near neighbours) read global
+      if (staged) {
+        constexpr int kPer = 3 * MLE_TAB_P / 2;  // 16-byte words per interval
+        const double2* src = reinterpret_cast<const double2*>(tab) + (size_t)kbase * kPer;
+        double2* dst = reinterpret_cast<double2*>(s_tab);
+        for (int w = threadIdx.x; w < nslots * kPer; w += kGThreads) dst[w] = __ldg(src + w);
+        __syncthreads();
+      }
+    }
     // kE elements at a time, their kF Horner chains interleaved (4 independent chains per
     // thread: latency, not issue, bounded the element-serial version), branch-free for the
     // table elements; the rare exact-path / coincident elements are patched afterwards.
     constexpr int kF = kDerivs ? 2 : 1;
     constexpr int kE = 4 / kF;
+    auto rounds = [&](auto staged_tag) {
+      constexpr bool kStaged = decltype(staged_tag)::value;
+      const int kofs = kStaged ? kbase : 0;
 #pragma unroll
-    for (int r0 = 0; r0 < kGT / 8; r0 += kE) {
-      double u[kE], t[kE];
-      int cofs[kE];
-      bool intab[kE];
+      for (int r0 = 0; r0 < kGT / 8; r0 += kE) {
+        double t[kE];
+        int cofs[kE];
 #pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        const int patch = warp + 8 * (r0 + e);  // 32 patches: 8 patch rows x 4 patch columns
-        const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
-        const int ii = ti * kGT + row, j = tj * kGT + col;
-        // pdist-identical distance (no FMA contraction)
-        const double dx = __dsub_rn(lx[ii], lx[j]);
-        const double dy = __dsub_rn(ly[ii], ly[j]);
-        const double h = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
-        // u = h / alpha (matern.py:103) by Markstein's correction of h * (1 / alpha): the
-        // residual h - alpha q is exact (FMA), and q + r / alpha rounds to the correctly
-        // rounded quotient, without the division's iteration and slow-path branch
-        const double q = h * ialpha;
-        u[e] = fma(fma(-alpha, q, h), ialpha, q);
-        intab[e] = u[e] >= lo && u[e] < hi;
-        const double ut = intab[e] ? u[e] : lo;  // any valid interval for the others
-        const long long b = __double_as_longlong(ut);
-        const int key = (int)((b >> 49) - key0);
-        const int k = key - (key > kGenMergeKey ? 1 : 0) -
-                      (key > kGenMergeKey + 1 && ut < MLE_SMALL_MID_SPLIT ? 1 : 0);
-        t[e] = gen_tab_t(ut, k);
-        cofs[e] = k * 3 * MLE_TAB_P + (kDerivs ? MLE_TAB_P : 0);
-      }
-      double p[kE][kF];
-#pragma unroll
-      for (int e = 0; e < kE; ++e)
-#pragma unroll
-        for (int f = 0; f < kF; ++f) {
-          const double2 c = __ldg(reinterpret_cast<const double2*>(
-              tab + cofs[e] + f * MLE_TAB_P + MLE_TAB_P - 2));
-          p[e][f] = fma(c.y, t[e], c.x);
+        for (int e = 0; e < kE; ++e) {
+          // (an element outside the table range gets some finite t of the first interval's
+          // map: its polynomial value is discarded below)
+          const int k = (int)((kk >> (8 * (r0 + e))) & 255u);
+          t[e] = gen_tab_t(u[r0 + e], k);
+          cofs[e] = (k - kofs) * 3 * MLE_TAB_P + (kDerivs ? MLE_TAB_P : 0);
         }
-#pragma unroll
-      for (int i = MLE_TAB_P - 4; i >= 0; i -= 2)
+        double p[kE][kF];
 #pragma unroll
         for (int e = 0; e < kE; ++e)
 #pragma unroll
           for (int f = 0; f < kF; ++f) {
-            const double2 c =
-                __ldg(reinterpret_cast<const double2*>(tab + cofs[e] + f * MLE_TAB_P + i));
-            p[e][f] = fma(p[e][f], t[e], c.y);
-            p[e][f] = fma(p[e][f], t[e], c.x);
+            const int o = cofs[e] + f * MLE_TAB_P + MLE_TAB_P - 2;
+            const double2 c = kStaged ? *reinterpret_cast<const double2*>(s_tab + o)
+                                      : __ldg(reinterpret_cast<const double2*>(tab + o));
+            p[e][f] = fma(c.y, t[e], c.x);
           }
 #pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        const int patch = warp + 8 * (r0 + e);
-        const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
-        // below 8.5 the series are of E itself; above, of e^u E (matern_table_at)
-        if (u[e] >= MLE_SMALL_MID_SPLIT) {
-          const double eu = exp(-u[e]);
+        for (int i = MLE_TAB_P - 4; i >= 0; i -= 2)
 #pragma unroll
-          for (int f = 0; f < kF; ++f) p[e][f] *= eu;
-        }
-        if (intab[e]) {
-          s_v0[row][col] = p[e][0];
-          if (kDerivs) s_v1[row][col] = p[e][kF - 1];
-        } else {  // exact path: queued, evaluated below by the whole CTA
-          s_v0[row][col] = u[e];
-          s_exact[atomicAdd(&s_nexact, 1)] = (unsigned short)(row * kGT + col);
+          for (int e = 0; e < kE; ++e)
+#pragma unroll
+            for (int f = 0; f < kF; ++f) {
+              const int o = cofs[e] + f * MLE_TAB_P + i;
+              const double2 c = kStaged ? *reinterpret_cast<const double2*>(s_tab + o)
+                                        : __ldg(reinterpret_cast<const double2*>(tab + o));
+              p[e][f] = fma(p[e][f], t[e], c.y);
+              p[e][f] = fma(p[e][f], t[e], c.x);
+            }
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int patch = warp + 8 * (r0 + e);
+          const int row = 4 * (patch & 7) + pr, col = 8 * (patch >> 3) + pc;
+          const double ue = u[r0 + e];
+          // below 8.5 the series are of E itself; above, of e^u E (matern_table_at)
+          if (ue >= MLE_SMALL_MID_SPLIT) {
+            const double eu = exp(-ue);
+#pragma unroll
+            for (int f = 0; f < kF; ++f) p[e][f] *= eu;
+          }
+          if ((intab >> (r0 + e)) & 1u) {
+            s_v0[tile_slot(row, col)] = p[e][0];
+            if (kDerivs) s_v1[tile_slot(row, col)] = p[e][kF - 1];
+          } else {  // exact path: queued, evaluated below by the whole CTA
+            s_v0[tile_slot(row, col)] = ue;
+            s_exact[atomicAdd(&s_nexact, 1)] = (unsigned short)(row * kGT + col);
+          }
         }
       }
-    }
+    };
+    if (staged)
+      rounds(std::true_type{});
+    else
+      rounds(std::false_type{});
     __syncthreads();
     // The few pairs outside the table range (u < tab_lo: near neighbours, or coincident)
     // run the exact evaluator compacted onto consecutive threads: one warp pass instead of a
     // mostly idle warp per element (the near-diagonal tiles hold most of them).
     for (int q = threadIdx.x; q < s_nexact; q += kGThreads) {
       const int row = s_exact[q] / kGT, col = s_exact[q] % kGT;
-      const double ue = s_v0[row][col];
+      const double ue = s_v0[tile_slot(row, col)];
       MaternVals v;
       if (ue > 0.0) {
         v = matern_u_call<kDerivs != 0>(Pg, ue);
@@ -259,8 +347,8 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
         v.c = Pg.sigma2;
         v.dalpha = v.dnu = 0.0;
       }
-      s_v0[row][col] = kDerivs ? v.dalpha : v.c;
-      if (kDerivs) s_v1[row][col] = v.dnu;
+      s_v0[tile_slot(row, col)] = kDerivs ? v.dalpha : v.c;
+      if (kDerivs) s_v1[tile_slot(row, col)] = v.dnu;
     }
     __syncthreads();
     const long long j0 = (long long)tj * kGT + col0;
@@ -270,10 +358,10 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
 #pragma unroll
     for (int r = 0; r < kGT / 8; ++r) {
       if (kDerivs) {  // a null block is skipped (sequential-derivative mode: one at a time)
-        if (it.dalpha) pa[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
-        if (it.dnu) pn[8 * r * ld] = s_v1[lane_row][col0 + 8 * r];
+        if (it.dalpha) pa[8 * r * ld] = s_v0[tile_slot(lane_row, col0 + 8 * r)];
+        if (it.dnu) pn[8 * r * ld] = s_v1[tile_slot(lane_row, col0 + 8 * r)];
       } else {
-        ps[8 * r * ld] = s_v0[lane_row][col0 + 8 * r];
+        ps[8 * r * ld] = s_v0[tile_slot(lane_row, col0 + 8 * r)];
       }
     }
   } else {
@@ -288,8 +376,8 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       if (kDerivs) {
         if (it.dalpha) it.dalpha[off] = da;
         if (it.dnu) it.dnu[off] = dn;
-        s_v0[lane_row][jl] = da;
-        s_v1[lane_row][jl] = dn;
+        s_v0[tile_slot(lane_row, jl)] = da;
+        s_v1[tile_slot(lane_row, jl)] = dn;
       } else {
         it.sigma[off] = c;
       }
@@ -304,8 +392,8 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       const int jl = col0 + 8 * r;
       const int j2 = ti * kGT + jl;
       const long long off = (long long)i2 + (long long)j2 * ld;
-      if (it.dalpha) it.dalpha[off] = s_v0[jl][lane_row];
-      if (it.dnu) it.dnu[off] = s_v1[jl][lane_row];
+      if (it.dalpha) it.dalpha[off] = s_v0[tile_slot(jl, lane_row)];
+      if (it.dnu) it.dnu[off] = s_v1[tile_slot(jl, lane_row)];
     }
   }
 }
@@ -399,7 +487,7 @@ __global__ void __launch_bounds__(kGThreads) gen_build_kernel(GenArgs a, int whi
   __shared__ double s_v[kGT][kGT + 1];
   stage_params(&P, it.P);
   int ti, tj;
-  lower_tile_index((long long)blockIdx.x, &ti, &tj);
+  lower_tile_index(blockIdx.x, &ti, &tj);
   const int lane_row = threadIdx.x & (kGT - 1);
   const int col0 = threadIdx.x >> 5;
   const int i = ti * kGT + lane_row;
@@ -512,10 +600,20 @@ void launch_gen_engine(const GenArgs& a, int items, cudaStream_t s) {
                                            : lower_tiles(a.rows);
   if (blocks <= 0) return;
   const dim3 grid((unsigned)blocks, (unsigned)items);
-  if (a.item[0].write_derivs)
-    gen_engine_kernel<1><<<grid, kGThreads, 0, s>>>(a);
+  // The derivative kernel (two functions per element: L1-bound on its coefficient loads)
+  // stages the tile's table intervals in shared memory: config 4 1485 -> 1581 GB/s.  The
+  // Sigma kernel (one function, issue-bound) loses 4% to the extra barrier, so it reads
+  // global memory.  MLE_GEN_STAGE=0 / 2: neither / both (A/B; all bit-identical).
+  static const int stage = [] {
+    const char* e = std::getenv("MLE_GEN_STAGE");
+    return (e != nullptr && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+  }();
+  GenArgs b = a;
+  b.stage_tab = stage == 2 || (stage == 1 && a.item[0].write_derivs);
+  if (b.item[0].write_derivs)
+    gen_engine_kernel<1><<<grid, kGThreads, 0, s>>>(b);
   else
-    gen_engine_kernel<0><<<grid, kGThreads, 0, s>>>(a);
+    gen_engine_kernel<0><<<grid, kGThreads, 0, s>>>(b);
 }
 
 void launch_gen_panels(const GenArgs& a, const int* c0s_dev, int width, int items,

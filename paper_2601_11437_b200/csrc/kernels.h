@@ -39,6 +39,7 @@ struct GenArgs {
   int region;         // engine: 0 every lower tile; 1 tile columns < jcut; 2 tile columns >= jcut
   int jcut;           // in 32-wide generation tiles
   int lower_only;     // derivative matrices: lower tiles only (no mirrored upper tiles)
+  int stage_tab;      // engine fast path: stage the tile's table intervals in shared memory
 };
 
 // Operand layouts of op(B): B(n,k) at b[n + k*ldb] (kBNK) or b[k + n*ldb] (kBKN).
