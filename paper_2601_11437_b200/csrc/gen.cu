@@ -30,7 +30,7 @@ constexpr int kGT = 32;         // generation tile edge
 constexpr int kGThreads = 256;  // 8 columns per pass, 4 passes
 constexpr int kGenSlots = 24;   // table intervals a tile stages in shared memory (3 binades)
 #ifndef MLE_GEN_MINB
-#define MLE_GEN_MINB 4
+#define MLE_GEN_MINB 5
 #endif
 
 // b = I (I + 1) / 2 + J, 0 <= J <= I, for a block index b < 2^31 (a grid's x extent): a
@@ -55,6 +55,20 @@ __device__ __forceinline__ void lower_tile_index(unsigned b, int* ti, int* tj) {
 // rows, one column) and the transposed reads of the mirrored tile (one row, 32 columns).
 __device__ __forceinline__ int tile_slot(int row, int col) {
   return row * kGT + (col ^ (((row & 3) << 2) | ((row >> 2) & 3)));
+}
+
+// A 16-byte coefficient pair from shared memory; MLE_GEN_LDS64 (A/B) splits it into two
+// 8-byte loads.
+__device__ __forceinline__ double2 lds_pair(const double* p) {
+#ifdef MLE_GEN_LDS64
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  double2 c;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(c.x) : "r"(a));
+  asm volatile("ld.shared.f64 %0, [%1+8];" : "=d"(c.y) : "r"(a));
+  return c;
+#else
+  return *reinterpret_cast<const double2*>(p);
+#endif
 }
 
 // pdist-identical Euclidean distance (no FMA contraction).
@@ -270,7 +284,13 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
     // thread: latency, not issue, bounded the element-serial version), branch-free for the
     // table elements; the rare exact-path / coincident elements are patched afterwards.
     constexpr int kF = kDerivs ? 2 : 1;
-    constexpr int kE = 4 / kF;
+#ifndef MLE_GEN_KE_D
+#define MLE_GEN_KE_D 2
+#endif
+#ifndef MLE_GEN_KE_S
+#define MLE_GEN_KE_S 4
+#endif
+    constexpr int kE = kDerivs ? MLE_GEN_KE_D : MLE_GEN_KE_S;  // elements per round
     auto rounds = [&](auto staged_tag) {
       constexpr bool kStaged = decltype(staged_tag)::value;
       const int kofs = kStaged ? kbase : 0;
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
 #pragma unroll
           for (int f = 0; f < kF; ++f) {
             const int o = cofs[e] + f * MLE_TAB_P + MLE_TAB_P - 2;
-            const double2 c = kStaged ? *reinterpret_cast<const double2*>(s_tab + o)
+            const double2 c = kStaged ? lds_pair(s_tab + o)
                                       : __ldg(reinterpret_cast<const double2*>(tab + o));
             p[e][f] = fma(c.y, t[e], c.x);
           }
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
 #pragma unroll
             for (int f = 0; f < kF; ++f) {
               const int o = cofs[e] + f * MLE_TAB_P + i;
-              const double2 c = kStaged ? *reinterpret_cast<const double2*>(s_tab + o)
+              const double2 c = kStaged ? lds_pair(s_tab + o)
                                         : __ldg(reinterpret_cast<const double2*>(tab + o));
               p[e][f] = fma(p[e][f], t[e], c.y);
               p[e][f] = fma(p[e][f], t[e], c.x);
