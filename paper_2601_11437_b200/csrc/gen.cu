@@ -35,17 +35,18 @@ constexpr int kGenSlots = 24;   // table intervals a tile stages in shared memor
 
 // b = I (I + 1) / 2 + J, 0 <= J <= I, for a block index b < 2^31 (a grid's x extent): a
 // float estimate of I (approximate sqrt, error << 1 for b < 2^24 and a few units at most
-// beyond) corrected exactly in 32-bit integers ((I + 1)(I + 2) < 2^32 for every such b).
+// beyond) corrected exactly in integers (the products in 64 bits: (I + 1)(I + 2) passes 2^32
+// at the very top of that range).
 // The double-precision sqrt with 64-bit corrections this replaces was ~60 instructions of
 // every CTA's prologue.
 __device__ __forceinline__ void lower_tile_index(unsigned b, int* ti, int* tj) {
   float r;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaf(8.0f, (float)b, 1.0f)));
   unsigned I = (unsigned)fmaxf((r - 1.0f) * 0.5f, 0.0f);
-  while (I * (I + 1) / 2 > b) --I;
-  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  while ((unsigned long long)I * (I + 1) / 2 > b) --I;
+  while ((unsigned long long)(I + 1) * (I + 2) / 2 <= b) ++I;
   *ti = (int)I;
-  *tj = (int)(b - I * (I + 1) / 2);
+  *tj = (int)(b - (unsigned)((unsigned long long)I * (I + 1) / 2));
 }
 
 // Slot of element (row, col) in a 32 x 32 shared-memory value tile.  The column is XOR-swizzled
@@ -239,10 +240,16 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       s2[e] = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
       odd |= !(s2[e] >= 1e-280 && s2[e] <= 1e280);
     }
+    double hh[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) hh[e] = pivot_sqrt_rn(s2[e]);
+    if (odd) {  // rare: one branch per thread instead of one per element
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hh[e] = __dsqrt_rn(s2[e]);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      double h = pivot_sqrt_rn(s2[e]);
-      if (odd) h = __dsqrt_rn(s2[e]);
+      const double h = hh[e];
       // u = h / alpha (matern.py:103) by Markstein's correction of h * (1 / alpha): the
       // residual h - alpha q is exact (FMA), and q + r / alpha rounds to the correctly
       // rounded quotient, without the division's iteration and slow-path branch
