@@ -248,6 +248,18 @@ def kernel_profile(engine, theta, n, peaks):
 
 
 # ----------------------------------------------------------------------------- CPU side
+def use_all_host_threads():
+    """torchrun exports OMP_NUM_THREADS=1 to its workers: give the CPU arms' BLAS / LAPACK
+    every core this process may run on again (the reference arm is timed 'with all the host
+    threads it can use')."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=len(os.sched_getaffinity(0)), user_api="blas")
+    except Exception:
+        pass
+
+
 def cpu_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -333,6 +345,7 @@ def reference_arm(args, rank, world):
         return
     from oracle import maternmle_cpu as O  # noqa: F401  (imports / BLAS warm-up)
 
+    use_all_host_threads()
     for _ in range(args.warmup):
         cpu_config4_sample(pairs=50_000, n_lin=1024)
     samples, walls = [], []
@@ -625,6 +638,7 @@ def ours_arm(args, rank, world, local_rank):
         except Exception as exc:  # context numbers must not sink the headline
             line["context"] = {"error": repr(exc)}
         if not args.no_cpu_baseline:
+            use_all_host_threads()
             cpu = cpu_config4_sample()
             line["cpu_baseline"] = {
                 "value": cpu["value"], "unit": "it/s", "cores": cpu_cores(), "kind": "port",
