@@ -129,6 +129,24 @@ def test_oracle_parity_random(gpu):
                                "grad": g.tolist(), "fisher": f.tolist()}, n)
 
 
+def test_oracle_parity_unordered_locations(gpu):
+    """Unordered random locations at short and long ranges: a 32 x 32 generation tile's pairs
+    then span from one to dozens of table intervals (gen.cu: the shared-memory staging of a
+    tile's intervals and its per-tile fallback to global loads both run inside one launch),
+    with the nearest pairs on the exact path (u < 0.25)."""
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(23)
+    n = 900
+    loc = rng.uniform(size=(n, 2))
+    z = rng.standard_normal(n)
+    data = gpu.SpatialDataset(loc, z)
+    for th in ((0.8, 0.02, 1.2), (1.3, 0.004, 0.6), (1.0, 0.25, 0.4)):
+        ll, g, f = O.eval_all(loc, z, th)
+        check_eval(gpu, data, {"theta": th, "loglik": O.loglik(loc, z, th), "eval_loglik": ll,
+                               "grad": g.tolist(), "fisher": f.tolist()}, n)
+
+
 def test_univariate_and_closed_forms(gpu):
     d0 = gpu.SpatialDataset(np.array([[0.0, 0.0]]), np.array([0.0]))
     assert gpu.log_likelihood(d0, (1.0, 0.1, 0.5)) == pytest.approx(-0.5 * math.log(2 * math.pi),
