@@ -38,7 +38,7 @@ def score_scale(theta, n, grad, fisher):
     return half_tr + half_quad
 
 
-def check_eval(gpu, data, rec, n, floor=0.0):
+def check_eval(gpu, data, rec, n, floor=0.0, nu_score_tol=None):
     th = rec["theta"]
     ll_tol = max(LL_TOL, 3.0 * floor)
     ll = gpu.log_likelihood(data, th)
@@ -51,6 +51,8 @@ def check_eval(gpu, data, rec, n, floor=0.0):
     fd = fd_regime(th, data.locations)
     for i in range(3):
         tol = FD_TOL if (fd and i == 2) else SCORE_TOL
+        if i == 2 and nu_score_tol is not None and not fd:
+            tol = max(tol, nu_score_tol)
         assert abs(ev.grad[i] - ref_g[i]) <= tol * scale[i], (th, i, ev.grad, ref_g)
         for j in range(3):
             tol = FD_TOL if (fd and 2 in (i, j)) else FISHER_TOL
@@ -145,6 +147,40 @@ def test_oracle_parity_unordered_locations(gpu):
         ll, g, f = O.eval_all(loc, z, th)
         check_eval(gpu, data, {"theta": th, "loglik": O.loglik(loc, z, th), "eval_loglik": ll,
                                "grad": g.tolist(), "fisher": f.tolist()}, n)
+
+
+def test_oracle_parity_theta_sweep(gpu):
+    """Seeded sweep of theta over the four d/dnu regimes' territory (small and large u, nu
+    from 0.15 to 2.2 incl. values next to half-integers and integers outside the FD band) on
+    one jittered grid: every evaluation against the CPU oracle at the north-star tolerances.
+
+    One carve-out, measured (tools/theta_sweep_probe.py, tools/nu_score_truth.py,
+    profiles/r02_nu_score_noise.txt): the reference's case-2 series (bessel.py:184-223)
+    cancels against the pole of Gamma(-nu) and loses ~1/|nu - k| digits next to an integer k,
+    on top of its x-cancellation below 8.5.  At nu = 1.929 its d/dnu elements are off by up
+    to 7e-7 relative against 30-digit mpmath values and its nu-score by 2.2e-8 of scale; the
+    engine (tables through the same series' node values: a different realisation of that
+    noise) is 4.0e-8 from the truth and 1.8e-8 from the reference; at nu = 1.001 the
+    deviation is 9.9e-8 (exact per-element path: 2.2e-8).  Away from integers the sweep sits
+    at 1e-10 .. 1e-14.  So the nu component of the score is compared at
+    max(1e-8, 2e-9 / |nu - k|): the north-star 1e-8 wherever the reference's own value is
+    determined that well, i.e. for |nu - k| >= 0.2; everything else at the plain tolerances."""
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(41)
+    loc = gpu.jittered_grid(14, 5)
+    n = loc.shape[0]
+    z = rng.standard_normal(n)
+    data = gpu.SpatialDataset(loc, z)
+    thetas = [(float(s2), float(a), float(nu)) for s2, a, nu in zip(
+        rng.uniform(0.2, 5.0, 12), rng.uniform(0.02, 0.15, 12), rng.uniform(0.15, 2.2, 12))]
+    thetas += [(1.0, 0.1, 0.5), (2.0, 0.05, 1.5), (0.7, 0.12, 1.001), (1.5, 0.03, 0.4999)]
+    for th in thetas:
+        ll, g, f = O.eval_all(loc, z, th)
+        pole = max(abs(th[2] - round(th[2])), 1e-6)
+        check_eval(gpu, data, {"theta": th, "loglik": O.loglik(loc, z, th), "eval_loglik": ll,
+                               "grad": g.tolist(), "fisher": f.tolist()}, n,
+                   nu_score_tol=2e-9 / pole)
 
 
 def test_univariate_and_closed_forms(gpu):
