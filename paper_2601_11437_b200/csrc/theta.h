@@ -17,13 +17,18 @@
 #define MLE_CASE4_TERMS 5        // bessel.py:55
 #define MLE_U_COEFF_STRIDE 40    // >= 3*12+1 coefficients per Debye polynomial
 #define MLE_TAB_P 14              // interpolation points per interval (degree 13, even)
-#define MLE_TAB_MAX 96            // intervals per table (8 per binade of u in [0.25, 800))
+#define MLE_TAB_MAX 96            // intervals per table (8 per binade of u in [0.25, 1024))
 #define MLE_TAB_DOUBLES (MLE_TAB_MAX * 3 * MLE_TAB_P)  // [interval][c, da, dn][power]
 #define MLE_TAB_LO_EXP (-2)       // tables from u = 2^-2 up; below, the exact evaluator: near
                                   // u = 0, C ~ sigma^2 and the ill-conditioned goldens need its
                                   // few-ulp accuracy (tables from 2^-16 moved one by 1.6e-10)
 #define MLE_TAB_LO 0.25           // 2^MLE_TAB_LO_EXP
-#define MLE_TAB_HI 800.0          // above: exact evaluation (elements underflow anyway)
+#define MLE_TAB_HI 640.0          // above: exact evaluation (elements ~1e-280 sigma^2 or zero).  A
+                                  // bin edge well below 709.78: the tables hold e^u E(u), and
+                                  // exp(u) overflows there (at 800 the bins from 704 up were
+                                  // inf x 0 = NaN: a very short range, u > 709 for some pair,
+                                  // made Sigma NaN -- found by a theta probe, pinned by
+                                  // tests/test_gpu_likelihood.py::test_very_short_range)
 #define MLE_SMALL_MID_SPLIT 8.5  // bessel.py:46
 #define MLE_MID_LARGE_SPLIT 30.0 // bessel.py:47
 #define MLE_MID_TRUNC_SPLIT 15.0 // bessel.py:48

@@ -183,6 +183,32 @@ def test_oracle_parity_theta_sweep(gpu):
                    nu_score_tol=2e-9 / pole)
 
 
+def test_very_short_range(gpu):
+    """Ranges so short that u = h / alpha runs from ~30 into the thousands: table bins up to
+    u = 640, the exact path beyond (elements underflow towards zero; e^u itself overflows at
+    709.78, which once poisoned the last table bins with inf x 0), Sigma ~ sigma^2 I.  The
+    log-likelihood and the sigma^2 entries against the oracle at the north-star tolerances;
+    the alpha / nu entries are sums of e^-2u-sized terms, compared on the scale of the
+    matrix's largest entry."""
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(77)
+    loc = gpu.jittered_grid(14, 5)
+    n = loc.shape[0]
+    z = rng.standard_normal(n)
+    data = gpu.SpatialDataset(loc, z)
+    for th in ((1.0, 0.0008, 0.7), (2.0, 0.001, 2.2), (3.0, 0.0012, 0.012), (1.0, 0.0003, 0.5)):
+        ll, g, f = O.eval_all(loc, z, th)
+        assert gpu.log_likelihood(data, th) == pytest.approx(O.loglik(loc, z, th), rel=LL_TOL)
+        ev = gpu.grad_and_fisher(data, th)
+        assert ev.loglik == pytest.approx(ll, rel=LL_TOL)
+        assert np.all(np.isfinite(ev.grad)) and np.all(np.isfinite(ev.fisher))
+        assert ev.grad[0] == pytest.approx(g[0], rel=SCORE_TOL, abs=SCORE_TOL * n / th[0])
+        assert ev.fisher[0, 0] == pytest.approx(f[0, 0], rel=FISHER_TOL)
+        np.testing.assert_allclose(ev.fisher, f, rtol=1e-6, atol=FISHER_TOL * np.abs(f).max())
+        np.testing.assert_allclose(ev.grad, g, rtol=1e-6, atol=SCORE_TOL * n / th[0])
+
+
 def test_univariate_and_closed_forms(gpu):
     d0 = gpu.SpatialDataset(np.array([[0.0, 0.0]]), np.array([0.0]))
     assert gpu.log_likelihood(d0, (1.0, 0.1, 0.5)) == pytest.approx(-0.5 * math.log(2 * math.pi),
