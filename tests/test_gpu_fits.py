@@ -211,3 +211,37 @@ def test_fit_many_default_cube_batches_l9(gpu):
     for r in both:
         np.testing.assert_array_equal(r.theta_hat.as_array(), alone.theta_hat.as_array())
         assert (r.grad_calls, r.loglik_calls) == (alone.grad_calls, alone.loglik_calls)
+
+
+SWEEP_CASES = [
+    # name, locations, theta_true, cube lower corner, cube upper corner (None: degenerate cube)
+    ("gmm300", lambda m: m.gmm_locations(300, 11), (1.2, 0.05, 0.6), (1.0, 0.1, 1.0), None),
+    ("grid324", lambda m: m.jittered_grid(18, 3), (0.8, 0.12, 1.8), (0.5, 0.05, 1.0), None),
+    ("gmm300-L9", lambda m: m.gmm_locations(300, 12), (1.5, 0.07, 0.9), (0.5, 0.03, 0.4),
+     (2.0, 0.2, 1.6)),
+    ("unif350", lambda m: np.random.default_rng(4).uniform(size=(350, 2)), (2.0, 0.03, 0.35),
+     (1.0, 0.1, 1.0), None),
+]
+
+
+@pytest.mark.parametrize("case", SWEEP_CASES, ids=[c[0] for c in SWEEP_CASES])
+def test_fit_sweep_vs_oracle_fits(gpu, case):
+    """Seeded small fields beyond the BASELINE configs (clustered, gridded and unordered
+    uniform locations; a finite-difference-band start nu0 = 1; a non-degenerate L9 start
+    cube): the same host loop on the GPU objective and on the CPU oracle's objective must
+    take the same calls to the same theta_hat (tools/fit_sweep_probe.py prints the pairs)."""
+    from oracle import maternmle_cpu as O
+
+    _, mk, th_true, lo, hi = case
+    loc = mk(gpu)
+    z = O.cholesky(O.matrix(loc, th_true, "sigma")) @ np.random.default_rng(99).standard_normal(
+        len(loc))
+    cfg = gpu.FisherBTConfig(theta_lower=gpu.MaternParams(*lo),
+                             theta_upper=gpu.MaternParams(*(hi or lo)))
+    ref = gpu.fisher_bt(gpu.SpatialDataset(loc, z), cfg, objective=O.CountingObjective(loc, z))
+    res = gpu.fisher_bt(gpu.SpatialDataset(loc, z), cfg)
+    assert (res.grad_calls, res.loglik_calls) == (ref.grad_calls, ref.loglik_calls)
+    assert res.termination == ref.termination and res.used_fallback == ref.used_fallback
+    np.testing.assert_allclose(res.theta_hat.as_array(), ref.theta_hat.as_array(), rtol=1e-6)
+    assert res.loglik_at_hat == pytest.approx(ref.loglik_at_hat, rel=1e-10)
+    np.testing.assert_allclose(res.fisher_at_hat, ref.fisher_at_hat, rtol=1e-6)
