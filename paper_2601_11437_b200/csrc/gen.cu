@@ -95,15 +95,17 @@ __device__ __forceinline__ void stage_params(ThetaParams* dst, const ThetaParams
 
 }  // namespace
 
-// The exact evaluator, inlined (default) or out of line (MLE_GEN_EXACT_NOINLINE=1, A/B):
-// out of line, the fast path's allocation no longer carries the Bessel ladder, but the
-// measured throughput is lower at every occupancy (config-2 batch: 886 / 918 / 892 GB/s at
-// 4 / 5 / 6 CTAs per SM against 920 inlined at 4).
+// The exact evaluator: inlined everywhere (0), out of line everywhere (1), or out of line in
+// the derivative kernel's fast path only (2, default).  Out of line, the fast path's register
+// allocation no longer carries the Bessel ladder.  At 48 registers (five CTAs per SM) that
+// pays for the derivative kernel (config 4: 1,793 -> 1,845 GB/s; config-2 batch 1,032 ->
+// 1,042) and costs the Sigma kernel 5%, hence the split; at 64 registers it measured slower
+// everywhere (config-2 batch: 886 / 918 / 892 GB/s at 4 / 5 / 6 CTAs per SM against 920).
 #ifndef MLE_GEN_EXACT_NOINLINE
-#define MLE_GEN_EXACT_NOINLINE 0
+#define MLE_GEN_EXACT_NOINLINE 2
 #endif
 template <bool kD>
-#if MLE_GEN_EXACT_NOINLINE
+#if MLE_GEN_EXACT_NOINLINE == 1
 __device__ __noinline__
 #else
 __device__ __forceinline__
@@ -111,6 +113,11 @@ __device__ __forceinline__
 MaternVals matern_u_call(const ThetaParams& P, double u) {
   return matern_u<kD>(P, u);
 }
+#if MLE_GEN_EXACT_NOINLINE == 2  // A/B: out of line in the derivative kernel's fast path only
+__device__ __noinline__ MaternVals matern_u_derivs_outofline(const ThetaParams& P, double u) {
+  return matern_u<true>(P, u);
+}
+#endif
 
 // Element (i, j) of the engine's padded matrices (Sigma with the augmented row / column n
 // and identity padding; the derivative blocks zero outside [0, n)^2).
@@ -373,7 +380,14 @@ __global__ void __launch_bounds__(kGThreads, MLE_GEN_MINB) gen_engine_kernel(Gen
       const double ue = s_v0[tile_slot(row, col)];
       MaternVals v;
       if (ue > 0.0) {
+#if MLE_GEN_EXACT_NOINLINE == 2
+        if (kDerivs)
+          v = matern_u_derivs_outofline(Pg, ue);
+        else
+          v = matern_u_call<false>(Pg, ue);
+#else
         v = matern_u_call<kDerivs != 0>(Pg, ue);
+#endif
       } else {  // coincident locations: zero-lag limit (matern.py:173-178)
         v.c = Pg.sigma2;
         v.dalpha = v.dnu = 0.0;

@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
 cp paper_2601_11437_b200/libmaternfisher.so /tmp/lib_default.so
-for v in default s6 s4 default s6; do
+for v in default noinl2 default noinl2; do
   if [ $v = default ]; then cp /tmp/lib_default.so paper_2601_11437_b200/libmaternfisher.so; else cp gpurun_variants/lib_$v.so paper_2601_11437_b200/libmaternfisher.so; fi
   echo "== $v"
   timeout 600 python tools/gen_config4_probe.py config4 2>&1 | grep GENPROBE | python -c "
