@@ -131,6 +131,25 @@ def test_oracle_parity_random(gpu):
                                "grad": g.tolist(), "fisher": f.tolist()}, n)
 
 
+def test_oracle_parity_tile_edges(gpu):
+    """Sizes around the 32-wide generation tiles and the 128-wide factorization tiles (the
+    generation fast path takes a tile only when it lies wholly inside [0, n)): jittered grids
+    cut to n points, so that interior tiles do use the table fast path."""
+    from oracle import maternmle_cpu as O
+
+    rng = np.random.default_rng(29)
+    for n in (31, 32, 33, 63, 64, 65, 96, 97, 160, 161, 255, 256, 383, 385):
+        side = int(np.ceil(np.sqrt(n)))
+        loc = gpu.jittered_grid(side, n)[:n]
+        th = (float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.03, 0.12)),
+              float(rng.uniform(0.3, 1.4)) + 0.0137)
+        z = rng.standard_normal(n)
+        data = gpu.SpatialDataset(loc, z)
+        ll, g, f = O.eval_all(loc, z, th)
+        check_eval(gpu, data, {"theta": th, "loglik": O.loglik(loc, z, th), "eval_loglik": ll,
+                               "grad": g.tolist(), "fisher": f.tolist()}, n)
+
+
 def test_oracle_parity_unordered_locations(gpu):
     """Unordered random locations at short and long ranges: a 32 x 32 generation tile's pairs
     then span from one to dozens of table intervals (gen.cu: the shared-memory staging of a
