@@ -245,3 +245,25 @@ def test_fit_sweep_vs_oracle_fits(gpu, case):
     np.testing.assert_allclose(res.theta_hat.as_array(), ref.theta_hat.as_array(), rtol=1e-6)
     assert res.loglik_at_hat == pytest.approx(ref.loglik_at_hat, rel=1e-10)
     np.testing.assert_allclose(res.fisher_at_hat, ref.fisher_at_hat, rtol=1e-6)
+
+
+@pytest.mark.parametrize("groups", [1, 3])
+def test_fit_many_more_fits_than_batch_slots(gpu, groups):
+    """Twenty lock-step fits (the five config-2 replicas four times over): more live fits per
+    group than one batched launch holds (eight items), so every pass is several launches.
+    Every fit must reproduce its golden and its replicas bit for bit."""
+    data, gold = [], []
+    for _ in range(4):
+        for seed in range(5):
+            g = fit_golden("config2", seed)
+            if g is None:
+                pytest.skip("no config-2 golden fits")
+            loc, z = config_data("config2", seed)
+            data.append(gpu.SpatialDataset(loc, z))
+            gold.append(g)
+    th0 = gpu.MaternParams(*gold[0]["theta0"])
+    res = gpu.fit_many(data, gpu.FisherBTConfig(theta_lower=th0, theta_upper=th0), groups=groups)
+    for i, (r, g) in enumerate(zip(res, gold)):
+        check(g, r)
+        np.testing.assert_array_equal(r.theta_hat.as_array(), res[i % 5].theta_hat.as_array())
+        np.testing.assert_array_equal(r.fisher_at_hat, res[i % 5].fisher_at_hat)
